@@ -1,0 +1,280 @@
+/*
+ * mpeig_b200.h -- C ABI of the B200-native (sm_100a) LOBPCG / PINVIT hot path.
+ *
+ * Drop-in boundary for the reference library `mpeig` (arXiv 2302.12528
+ * artifact).  Every entry point cites the reference interface it replaces
+ * (paths relative to the reference's proj/ directory).  Plain pointers and
+ * sizes only: no C++ or torch types cross this boundary.
+ *
+ * Memory model: block vectors are column-major (dense_matrix.hpp:38-41)
+ * device arrays with a caller-chosen leading dimension.  Host arrays are
+ * named *_host.  All work is ordered on the context's CUDA stream.
+ *
+ * Errors: every function returns an mpeig_status.  Codes 1..8 are 1:1 with
+ * the reference exception types thrown on the solver path (errors.hpp:10-62);
+ * mpeig_last_error() returns the message and the index payload
+ * (NotPositiveDefinite::index, SingularTriangular::index,
+ * RankDeficient::column).  Non-convergence within maxit is NOT an error
+ * (converged = 0), as in eigensolvers.hpp:248-262.
+ */
+#ifndef MPEIG_B200_H
+#define MPEIG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ status codes */
+typedef enum {
+  MPEIG_OK = 0,
+  MPEIG_E_DIMENSION = 1,       /* DimensionMismatch      errors.hpp:11   */
+  MPEIG_E_CONFIG = 2,          /* ConfigError            errors.hpp:15   */
+  MPEIG_E_NOT_PD = 3,          /* NotPositiveDefinite    errors.hpp:24   */
+  MPEIG_E_SINGULAR_TRI = 4,    /* SingularTriangular     errors.hpp:30   */
+  MPEIG_E_RANK_DEFICIENT = 5,  /* RankDeficient          errors.hpp:36   */
+  MPEIG_E_RANK_COLLAPSE = 6,   /* RankCollapse           errors.hpp:46   */
+  MPEIG_E_NO_CONVERGENCE = 7,  /* NoConvergence          errors.hpp:50   */
+  MPEIG_E_OVERFLOW = 8,        /* OverflowError          errors.hpp:55   */
+  MPEIG_E_CALLBACK = 20,       /* a user callback returned nonzero      */
+  MPEIG_E_CUDA = 30,
+  MPEIG_E_CUSOLVER = 31,
+  MPEIG_E_COMM = 32,
+  MPEIG_E_OTHER = 99
+} mpeig_status;
+
+/* Variant (solver_types.hpp:11) */
+typedef enum {
+  MPEIG_DLOBPCG_DCHOL = 0,
+  MPEIG_DLOBPCG_SCHOL = 1,
+  MPEIG_MPLOBPCG_SCHOL = 2,
+  MPEIG_PINVIT = 3
+} mpeig_variant;
+
+/* Precision (precision.hpp:14) */
+typedef enum { MPEIG_WORKING = 0, MPEIG_LOWER = 1 } mpeig_precision;
+
+typedef struct mpeig_ctx mpeig_ctx;
+typedef struct mpeig_op mpeig_op;
+
+/* SolverConfig (solver_types.hpp:31-57).  block == 0 picks (3k+1)/2. */
+typedef struct {
+  int64_t k;
+  int64_t block;
+  int64_t maxit;
+  double tol;
+  double lower_tol;
+  uint64_t seed;
+  int32_t variant;       /* mpeig_variant */
+  int64_t sketch_rows;
+} mpeig_cfg;
+
+/* StageOptions (eigensolvers.hpp:176-181) */
+typedef struct {
+  double tol;
+  int32_t use_mixed_qr;
+  int32_t stagnation_exit;
+  int32_t tag;           /* mpeig_precision of the history records */
+} mpeig_stage_opts;
+
+/* IterationRecord (solver_types.hpp:59-66); passed to the history sink once
+ * per iteration.  Arrays are valid only during the callback. */
+typedef struct {
+  int32_t stage;         /* mpeig_precision */
+  int64_t m;
+  const double* ritz_values;
+  const double* residual_norms;
+  int64_t n_converged;
+  int64_t w_columns_dropped;
+  int32_t basis_rotation_fallback;
+} mpeig_iter_record;
+typedef void (*mpeig_history_sink)(void* user, const mpeig_iter_record* rec);
+
+/* StageTimings (solver_types.hpp:68-74), seconds, accumulated */
+typedef struct {
+  double factorize;
+  double precond_apply;
+  double orthogonalize;
+  double projected_eig;
+  double total;
+} mpeig_timings;
+
+/* StageOutcome (eigensolvers.hpp:183-190).  X is a caller-owned device
+ * buffer (n x m, ld ldx) of the stage's precision; theta / residual_norms
+ * are caller-owned host arrays of length m. */
+typedef struct {
+  void* X;
+  int64_t ldx;
+  double* theta;
+  double* residual_norms;
+  int64_t iterations;
+  int32_t converged;
+} mpeig_stage_out;
+
+/* EigResult (solver_types.hpp:76-88).  Caller-owned host arrays of length k;
+ * X optional (device, n x k fp64, ld ldx; NULL to skip). */
+typedef struct {
+  double* theta;
+  double* residual_norms;
+  double* X;
+  int64_t ldx;
+  int64_t iterations_lower;
+  int64_t iterations_working;
+  int32_t converged;
+  double a_norm_estimate;
+  mpeig_timings timings;
+} mpeig_result;
+
+/* ------------------------------------------------------------- context */
+/* One context per (GPU, stream); not thread-safe per context, independent
+ * contexts may run concurrently (SPEC.md:526 / SURVEY §8b threading). */
+int mpeig_ctx_create(int device, void* cuda_stream, mpeig_ctx** out);
+void mpeig_ctx_destroy(mpeig_ctx* ctx);
+/* message of the last failure on this context; *index gets the payload */
+const char* mpeig_last_error(mpeig_ctx* ctx, int64_t* index);
+/* number of kernels this library launched on ctx since creation / reset */
+int64_t mpeig_launch_count(mpeig_ctx* ctx, int reset);
+/* device stream the context orders its work on */
+void* mpeig_ctx_stream(mpeig_ctx* ctx);
+
+/* ------------------------------------------------------------ operators */
+/* BlockOperator<T> (dense_kernels.hpp:15-16).  Device callback: Y = op(X),
+ * X/Y device column-major n_local x ncols, stream-ordered on `stream`,
+ * must not synchronise the device.  Return 0 on success. */
+typedef int (*mpeig_apply_fn)(void* user, int64_t n_local, int64_t ncols,
+                              const void* X, int64_t ldx, void* Y, int64_t ldy,
+                              void* stream);
+/* Host BlockOperator adapter: contiguous column-major host arrays (n x ncols).
+ * Lets a reference-style CPU callback run unchanged (D2H, call, H2D). */
+typedef int (*mpeig_host_apply_fn)(void* user, int64_t n, int64_t ncols,
+                                   const void* X_host, void* Y_host);
+
+/* Built-in operators.  Each provides a working (fp64) and a lower (fp32)
+ * apply; the lower one uses to_lower() of the coefficients
+ * (csr_matrix.hpp:136-146), overflow -> MPEIG_E_OVERFLOW. */
+/* 3-D 7-point Dirichlet Laplacian, diag 6 / off -1, row = x + nx(y + ny z),
+ * entries summed in ascending column order like spmv_block
+ * (sparse_kernels.hpp:16-33) -> bitwise equal to the reference's CSR apply */
+int mpeig_op_lap3d(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, mpeig_op** out);
+/* gen_laplace2d (generators.cpp:13-30) applied matrix-free */
+int mpeig_op_lap2d(mpeig_ctx* ctx, int64_t nx, int64_t ny, mpeig_op** out);
+/* CsrMatrix<double> (csr_matrix.hpp:13-146): int64 row_ptr/col_idx, sorted
+ * columns, host arrays (copied to the device) */
+int mpeig_op_csr(mpeig_ctx* ctx, int64_t n, const int64_t* row_ptr_host,
+                 const int64_t* col_idx_host, const double* vals_host, mpeig_op** out);
+/* dense symmetric n x n, herm_product (dense_kernels.hpp:66-72); host array */
+int mpeig_op_dense(mpeig_ctx* ctx, int64_t n, const double* A_host, int64_t lda,
+                   mpeig_op** out);
+/* user device callbacks (either may be NULL if that precision is unused) */
+int mpeig_op_device_callback(mpeig_ctx* ctx, int64_t n, mpeig_apply_fn apply_working,
+                             mpeig_apply_fn apply_lower, void* user, mpeig_op** out);
+/* user host callbacks (the CPU BlockOperator adapter) */
+int mpeig_op_host_callback(mpeig_ctx* ctx, int64_t n, mpeig_host_apply_fn apply_working,
+                           mpeig_host_apply_fn apply_lower, void* user, mpeig_op** out);
+/* Jacobi preconditioner f_T = diag(A)^-1 built at `precision`
+ * (Preconditioner<T>::build, precond.hpp:33-77, with a diagonal factor):
+ *   WORKING: apply(R) = R .* dinv                       (fp64)
+ *   LOWER:   apply(R) = to_working(to_lower(R) .* dinvf) (precond.hpp:92-100)
+ *            apply_lower(R) = R .* dinvf                (precond.hpp:103-109)
+ * The solver fuses it with the residual and the conversions (one HBM pass). */
+int mpeig_precond_jacobi(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision,
+                         mpeig_op** out);
+void mpeig_op_destroy(mpeig_op* op);
+int64_t mpeig_op_n(const mpeig_op* op);
+/* Y = op(X) in working (fp64) or lower (fp32) precision, device arrays */
+int mpeig_op_apply(mpeig_ctx* ctx, const mpeig_op* op, int32_t precision, int64_t ncols,
+                   const void* X, int64_t ldx, void* Y, int64_t ldy);
+
+/* ------------------------------------------------------ solver entry points */
+/* spectral_norm_estimate (norm_estimate.hpp:15-24): Omega drawn on the host
+ * with the reference PCG64/Box-Muller stream (bit-exact), one device apply */
+int mpeig_spectral_norm_estimate(mpeig_ctx* ctx, const mpeig_op* A, int64_t sketch_rows,
+                                 uint64_t seed, double* out);
+
+/* lobpcg_stage<double> / <float> (eigensolvers.hpp:195-321).  X0 is an
+ * orthonormal device block (n x m, ld ldx0) of the stage precision.  The
+ * preconditioner T is applied as T.apply (f64) or T.apply_lower (f32). */
+int mpeig_lobpcg_stage_f64(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const double* X0,
+                           int64_t ldx0, int64_t m, const mpeig_cfg* cfg, const mpeig_op* T,
+                           double a_norm_est, const mpeig_stage_opts* opt,
+                           mpeig_history_sink sink, void* sink_user,
+                           mpeig_stage_out* out, mpeig_timings* tim);
+int mpeig_lobpcg_stage_f32(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const float* X0,
+                           int64_t ldx0, int64_t m, const mpeig_cfg* cfg, const mpeig_op* T,
+                           double a_norm_est, const mpeig_stage_opts* opt,
+                           mpeig_history_sink sink, void* sink_user,
+                           mpeig_stage_out* out, mpeig_timings* tim);
+
+/* pinvit<double> (eigensolvers.hpp:326-390), with the preconditioner as an
+ * operator (generalises the reference's concrete Preconditioner<T>&).
+ * a_norm_est <= 0 computes the sketch as the reference does. */
+int mpeig_pinvit_f64(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const double* X0,
+                     int64_t ldx0, int64_t m, const mpeig_cfg* cfg, const mpeig_op* T,
+                     double a_norm_est, mpeig_history_sink sink, void* sink_user,
+                     mpeig_result* out);
+
+/* solve() (drivers.hpp:158-181) + run_variant (drivers.hpp:57-111):
+ * sketch, X0 = orthonormal_q(gaussian_matrix(n, m, seed), true), then the
+ * variant's stage(s).  T must be built at the variant's precision
+ * (DLOBPCG_DCHOL: WORKING, others: LOWER; drivers.hpp:113-116). */
+int mpeig_solve(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T, const mpeig_cfg* cfg,
+                mpeig_history_sink sink, void* sink_user, mpeig_result* out);
+
+/* run_variant on an explicit start block X0 (device fp64, n x m) with a
+ * precomputed norm estimate (drivers.hpp:57-111; mixed_lobpcg :122-152) */
+int mpeig_run_variant(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T,
+                      const mpeig_cfg* cfg, const double* X0, int64_t ldx0,
+                      double a_norm_est, mpeig_history_sink sink, void* sink_user,
+                      mpeig_result* out);
+
+/* ----------------------------------------------- kernel-level entry points
+ * (used by the parity tests; each mirrors one reference routine) */
+/* gaussian_matrix<double> (dense_matrix.hpp:144-161) drawn on the host with
+ * the reference stream, written to a host array (rows x cols) */
+int mpeig_gaussian_matrix_host(int64_t rows, int64_t cols, uint64_t seed, double* out_host);
+/* detail::orthonormal_q (eigensolvers.hpp:55-70): mixed_qr with Householder
+ * fallback (use_mixed, fp64) or Householder-equivalent QR.  In place on W. */
+int mpeig_orthonormal_q_f64(mpeig_ctx* ctx, int64_t n, int64_t m, double* W, int64_t ldw,
+                            int32_t use_mixed);
+int mpeig_orthonormal_q_f32(mpeig_ctx* ctx, int64_t n, int64_t m, float* W, int64_t ldw);
+/* mixed_qr (ortho.hpp:173-186, Alg. 2): Q in place on W, R (m x m) to R_out */
+int mpeig_mixed_qr_f64(mpeig_ctx* ctx, int64_t n, int64_t m, double* W, int64_t ldw,
+                       double* R_out);
+/* householder_qr (ortho.hpp:127-140) equivalent: unique Q with diag(R) > 0 */
+int mpeig_householder_qr_f64(mpeig_ctx* ctx, int64_t n, int64_t m, double* W, int64_t ldw,
+                             double* R_out);
+/* orthonormal_q_dropping (eigensolvers.hpp:74-85): returns kept column count */
+int mpeig_orthonormal_q_dropping_f64(mpeig_ctx* ctx, int64_t n, int64_t m, double* W,
+                                     int64_t ldw, int32_t use_mixed, int64_t* kept);
+/* G = A^T B (adjoint_matmul, dense_kernels.hpp:36-52); G ka x kb, ld ka */
+int mpeig_gram_f64(mpeig_ctx* ctx, int64_t n, int64_t ka, const double* A, int64_t lda,
+                   int64_t kb, const double* B, int64_t ldb, double* G);
+/* Y = beta Z + alpha A C (matmul, dense_kernels.hpp:20-34) */
+int mpeig_gemm_f64(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, double alpha,
+                   const double* A, int64_t lda, const double* Cm, int64_t ldc, double beta,
+                   const double* Z, int64_t ldz, double* Y, int64_t ldy);
+/* block_project_out (ortho.hpp:190-200): W -= B (B^T W), `passes` times */
+int mpeig_project_out_f64(mpeig_ctx* ctx, int64_t n, int64_t b, const double* B,
+                          int64_t ldb, int64_t w, double* W, int64_t ldw, int32_t passes);
+/* small_herm_eig (small_eig.hpp:92-218) on device (cuSOLVER syevd):
+ * M device s x s, values (device, ascending), vectors (device s x s) */
+int mpeig_small_eig_f64(mpeig_ctx* ctx, int64_t s, const double* M, double* values,
+                        double* vectors);
+/* hl_update (eigensolvers.hpp:148-174): coefficient block [c_x c_pv]
+ * (device s x (m+p), ld s) from eigenvectors C (device s x s); returns p
+ * and the rotation-fallback flag */
+int mpeig_hl_coeffs_f64(mpeig_ctx* ctx, int64_t s, int64_t m, const double* C,
+                        double* coef, int64_t* p, int32_t* fallback);
+/* residual_block + column norms + f_T (eigensolvers.hpp:104-129,
+ * precond.hpp:92-100) fused: W = T(AX - X diag(theta)); norms to host */
+int mpeig_residual_precond_f64(mpeig_ctx* ctx, const mpeig_op* T, int64_t n, int64_t m,
+                               const double* X, int64_t ldx, const double* AX,
+                               int64_t ldax, const double* theta_host, double* W,
+                               int64_t ldw, double* rnorm_host, double* xnorm_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPEIG_B200_H */

@@ -1,0 +1,508 @@
+"""Python mirror of the reference solver interface, backed by the sm_100a C ABI.
+
+Names, argument meaning and error behaviour follow the reference library
+(``/root/reference/proj/include/mpeig``):
+
+=============================  ===============================================
+this module                    reference
+=============================  ===============================================
+``SolverConfig``               ``SolverConfig``      solver_types.hpp:31-57
+``StageOptions``               ``StageOptions``      eigensolvers.hpp:176-181
+``IterationRecord``            ``IterationRecord``   solver_types.hpp:59-66
+``StageTimings``               ``StageTimings``      solver_types.hpp:68-74
+``EigResult``                  ``EigResult<T>``      solver_types.hpp:76-88
+``lobpcg_stage``               ``lobpcg_stage<T>``   eigensolvers.hpp:195-321
+``pinvit``                     ``pinvit<T>``         eigensolvers.hpp:326-390
+``mixed_lobpcg``               ``mixed_lobpcg``      drivers.hpp:122-152
+``solve``                      ``solve``             drivers.hpp:158-210
+``spectral_norm_estimate``     norm_estimate.hpp:15-24
+``converged_count``            eigensolvers.hpp:25-43
+exceptions                     errors.hpp:10-62
+=============================  ===============================================
+
+Device block vectors are torch CUDA tensors used as plain device memory: an
+n x m column-major block is a contiguous tensor of shape (m, ld) (row j =
+column j).  All numerical work happens in libmpeig_b200.so; there is no CPU
+fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from . import _lib as L
+
+# ----------------------------------------------------------------- errors
+
+
+class MpeigError(Exception):
+    code = L.E_OTHER
+
+    def __init__(self, msg="", index=-1):
+        super().__init__(msg)
+        self.index = index
+
+
+class DimensionMismatch(MpeigError, ValueError):
+    code = L.E_DIMENSION
+
+
+class ConfigError(MpeigError, ValueError):
+    code = L.E_CONFIG
+
+
+class NotPositiveDefinite(MpeigError, RuntimeError):
+    code = L.E_NOT_PD
+
+
+class SingularTriangular(MpeigError, RuntimeError):
+    code = L.E_SINGULAR_TRI
+
+
+class RankDeficient(MpeigError, RuntimeError):
+    code = L.E_RANK_DEFICIENT
+
+    @property
+    def column(self):
+        return self.index
+
+
+class RankCollapse(MpeigError, RuntimeError):
+    code = L.E_RANK_COLLAPSE
+
+
+class NoConvergence(MpeigError, RuntimeError):
+    code = L.E_NO_CONVERGENCE
+
+
+class OverflowError_(MpeigError, ArithmeticError):
+    """OverflowError (errors.hpp:55): a finite value left the binary32 range."""
+    code = L.E_OVERFLOW
+
+
+class CallbackError(MpeigError, RuntimeError):
+    code = L.E_CALLBACK
+
+
+class CudaError(MpeigError, RuntimeError):
+    code = L.E_CUDA
+
+
+_ERRORS = {c.code: c for c in (DimensionMismatch, ConfigError, NotPositiveDefinite,
+                               SingularTriangular, RankDeficient, RankCollapse, NoConvergence,
+                               OverflowError_, CallbackError, CudaError)}
+
+# ----------------------------------------------------------------- types
+
+WORKING, LOWER = L.WORKING, L.LOWER
+
+
+@dataclass
+class SolverConfig:
+    k: int = 1
+    block: int = 0
+    maxit: int = 2000
+    tol: float = 1e-12
+    lower_tol: float = 5e-6
+    seed: int = 0
+    variant: str = "mplobpcg-schol"
+    sketch_rows: int = 8
+
+    def block_size(self) -> int:
+        return self.block if self.block != 0 else (3 * self.k + 1) // 2
+
+    def to_c(self) -> L.Cfg:
+        return L.Cfg(self.k, self.block, self.maxit, self.tol, self.lower_tol,
+                     self.seed & 0xFFFFFFFFFFFFFFFF, L.VARIANTS[self.variant], self.sketch_rows)
+
+
+@dataclass
+class StageOptions:
+    tol: float = 1e-12
+    use_mixed_qr: bool = False
+    stagnation_exit: bool = False
+    tag: int = WORKING
+
+
+@dataclass
+class IterationRecord:
+    stage: int
+    ritz_values: List[float]
+    residual_norms: List[float]
+    n_converged: int
+    w_columns_dropped: int
+    basis_rotation_fallback: bool
+
+
+@dataclass
+class StageTimings:
+    factorize: float = 0.0
+    precond_apply: float = 0.0
+    orthogonalize: float = 0.0
+    projected_eig: float = 0.0
+    total: float = 0.0
+
+
+@dataclass
+class EigResult:
+    theta: np.ndarray
+    X: Optional[object]
+    residual_norms: np.ndarray
+    iterations_lower: int
+    iterations_working: int
+    history: List[IterationRecord] = field(default_factory=list)
+    converged: bool = False
+    timings: StageTimings = field(default_factory=StageTimings)
+    a_norm_estimate: float = 0.0
+
+
+@dataclass
+class StageOutcome:
+    X: object
+    theta: np.ndarray
+    residual_norms: np.ndarray
+    iterations: int
+    converged: bool
+
+
+# ----------------------------------------------------------------- context
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2302_12528_b200 needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+class Context:
+    """One library context per (GPU, stream); ordered on torch's current stream."""
+
+    def __init__(self, device: int = 0, stream=None):
+        torch = _torch()
+        self.lib = L.load()
+        self.device = device
+        with torch.cuda.device(device):
+            s = stream if stream is not None else torch.cuda.current_stream(device)
+        self.torch_stream = s
+        h = C.c_void_p()
+        rc = self.lib.mpeig_ctx_create(device, C.c_void_p(s.cuda_stream), C.byref(h))
+        if rc != 0:
+            raise CudaError(f"mpeig_ctx_create failed ({rc})")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.mpeig_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc: int):
+        if rc == 0:
+            return
+        idx = C.c_int64(-1)
+        msg = self.lib.mpeig_last_error(self.h, C.byref(idx))
+        msg = msg.decode(errors="replace") if msg else ""
+        raise _ERRORS.get(rc, MpeigError)(msg, idx.value)
+
+    def launches(self, reset=False) -> int:
+        return int(self.lib.mpeig_launch_count(self.h, 1 if reset else 0))
+
+
+_default_ctx: dict = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default_ctx:
+        _default_ctx[device] = Context(device)
+    return _default_ctx[device]
+
+
+# ----------------------------------------------------------------- operators
+
+
+class Operator:
+    """Handle to a device block operator (BlockOperator<T>, dense_kernels.hpp:15-16)."""
+
+    def __init__(self, ctx: Context, handle: C.c_void_p, n: int, kind: str, keep=()):
+        self.ctx, self.h, self.n, self.kind = ctx, handle, n, kind
+        self._keep = keep  # keeps ctypes callbacks alive
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.ctx.lib.mpeig_op_destroy(self.h)
+        except Exception:
+            pass
+
+    def apply(self, X, Y=None, precision=WORKING):
+        """Y = A X for a device block X (torch tensor of shape (ncols, ld))."""
+        torch = _torch()
+        ncols, ldx = X.shape
+        if Y is None:
+            Y = torch.empty_like(X)
+        self.ctx.check(self.ctx.lib.mpeig_op_apply(self.ctx.h, self.h, precision, ncols,
+                                                   C.c_void_p(X.data_ptr()), ldx,
+                                                   C.c_void_p(Y.data_ptr()), Y.shape[1]))
+        return Y
+
+
+def _mk(ctx, fn, *args):
+    h = C.c_void_p()
+    ctx.check(fn(ctx.h, *args, C.byref(h)))
+    return h
+
+
+def laplace3d(nx: int, ny: int = None, nz: int = None, ctx: Context = None) -> Operator:
+    """3-D 7-point Dirichlet Laplacian (diag 6, off -1), row = x + nx (y + ny z)."""
+    ctx = ctx or default_context()
+    ny = nx if ny is None else ny
+    nz = nx if nz is None else nz
+    return Operator(ctx, _mk(ctx, ctx.lib.mpeig_op_lap3d, nx, ny, nz), nx * ny * nz, "lap3d")
+
+
+def laplace2d(nx: int, ny: int = None, ctx: Context = None) -> Operator:
+    """gen_laplace2d (generators.cpp:13-30) applied matrix-free."""
+    ctx = ctx or default_context()
+    ny = nx if ny is None else ny
+    return Operator(ctx, _mk(ctx, ctx.lib.mpeig_op_lap2d, nx, ny), nx * ny, "lap2d")
+
+
+def csr_matrix(row_ptr, col_idx, vals, ctx: Context = None) -> Operator:
+    """CsrMatrix<double> (csr_matrix.hpp:13-146); columns sorted per row."""
+    ctx = ctx or default_context()
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col_idx, np.int64)
+    v = np.ascontiguousarray(vals, np.float64)
+    n = len(rp) - 1
+    h = _mk(ctx, ctx.lib.mpeig_op_csr, n, rp.ctypes.data, ci.ctypes.data, v.ctypes.data)
+    return Operator(ctx, h, n, "csr")
+
+
+def dense_matrix(A, ctx: Context = None) -> Operator:
+    """Dense symmetric operator (herm_product, dense_kernels.hpp:66-72)."""
+    ctx = ctx or default_context()
+    A = np.asfortranarray(A, dtype=np.float64)
+    n = A.shape[0]
+    h = _mk(ctx, ctx.lib.mpeig_op_dense, n, A.ctypes.data, n)
+    return Operator(ctx, h, n, "dense")
+
+
+def host_operator(n: int, apply_working: Callable, apply_lower: Callable = None,
+                  ctx: Context = None) -> Operator:
+    """Wrap a CPU BlockOperator (numpy n x c column-major in -> out)."""
+    ctx = ctx or default_context()
+
+    def wrap(fn, dtype):
+        if fn is None:
+            return L.HOST_APPLY()
+
+        def cb(user, nn, nc, xp, yp):
+            try:
+                X = np.ctypeslib.as_array(C.cast(xp, C.POINTER(np.ctypeslib.as_ctypes_type(dtype))),
+                                          shape=(nc * nn,)).reshape((nn, nc), order="F")
+                Y = np.asarray(fn(X), dtype=dtype)
+                out = np.ctypeslib.as_array(C.cast(yp, C.POINTER(np.ctypeslib.as_ctypes_type(dtype))),
+                                            shape=(nc * nn,)).reshape((nn, nc), order="F")
+                out[...] = Y
+                return 0
+            except Exception:  # surfaced as CallbackError
+                return 1
+        return L.HOST_APPLY(cb)
+
+    fw, fl = wrap(apply_working, np.float64), wrap(apply_lower, np.float32)
+    h = _mk(ctx, ctx.lib.mpeig_op_host_callback, n, fw, fl, None)
+    return Operator(ctx, h, n, "host", keep=(fw, fl))
+
+
+def jacobi(A: Operator, precision: int = LOWER) -> Operator:
+    """Jacobi f_T = diag(A)^-1 built at `precision` (Preconditioner::build)."""
+    h = _mk(A.ctx, A.ctx.lib.mpeig_precond_jacobi, A.h, precision)
+    return Operator(A.ctx, h, A.n, "jacobi")
+
+
+def build_precision_for(variant: str) -> int:
+    """drivers.hpp:113-116."""
+    return WORKING if variant == "dlobpcg-dchol" else LOWER
+
+
+# ----------------------------------------------------------------- solvers
+
+
+class _History:
+    def __init__(self):
+        self.records: List[IterationRecord] = []
+
+        def sink(user, rec_p):
+            r = rec_p.contents
+            m = r.m
+            self.records.append(IterationRecord(
+                int(r.stage), [r.ritz_values[j] for j in range(m)],
+                [r.residual_norms[j] for j in range(m)], int(r.n_converged),
+                int(r.w_columns_dropped), bool(r.basis_rotation_fallback)))
+        self.cb = L.SINK(sink)
+
+
+def _timings(t: L.Timings) -> StageTimings:
+    return StageTimings(t.factorize, t.precond_apply, t.orthogonalize, t.projected_eig, t.total)
+
+
+def spectral_norm_estimate(A: Operator, sketch_rows: int = 8, seed: int = 0) -> float:
+    out = C.c_double()
+    A.ctx.check(A.ctx.lib.mpeig_spectral_norm_estimate(A.ctx.h, A.h, sketch_rows,
+                                                       seed & 0xFFFFFFFFFFFFFFFF, C.byref(out)))
+    return out.value
+
+
+def solve(A: Operator, cfg: SolverConfig, T: Operator = None, want_X: bool = True,
+          history: bool = True) -> EigResult:
+    """solve() (drivers.hpp:158-181) with a Jacobi f_T at the variant's precision."""
+    torch = _torch()
+    ctx = A.ctx
+    if T is None:
+        T = jacobi(A, build_precision_for(cfg.variant))
+    k = cfg.k
+    theta = np.zeros(k)
+    resid = np.zeros(k)
+    X = None
+    res = L.Result()
+    res.theta = theta.ctypes.data_as(C.POINTER(C.c_double))
+    res.residual_norms = resid.ctypes.data_as(C.POINTER(C.c_double))
+    if want_X:
+        X = torch.empty((k, A.n), dtype=torch.float64, device=f"cuda:{ctx.device}")
+        res.X, res.ldx = C.c_void_p(X.data_ptr()), A.n
+    hist = _History()
+    c = cfg.to_c()
+    ctx.check(ctx.lib.mpeig_solve(ctx.h, A.h, T.h, C.byref(c),
+                                  hist.cb if history else L.SINK(), None, C.byref(res)))
+    return EigResult(theta, X, resid, res.iterations_lower, res.iterations_working,
+                     hist.records, bool(res.converged), _timings(res.timings),
+                     res.a_norm_estimate)
+
+
+def run_variant(A: Operator, X0, cfg: SolverConfig, a_norm_est: float, T: Operator = None,
+                want_X: bool = True) -> EigResult:
+    """detail::run_variant (drivers.hpp:57-111) on an explicit fp64 device start block."""
+    torch = _torch()
+    ctx = A.ctx
+    if T is None:
+        T = jacobi(A, build_precision_for(cfg.variant))
+    k = cfg.k
+    theta, resid = np.zeros(k), np.zeros(k)
+    X = None
+    res = L.Result()
+    res.theta = theta.ctypes.data_as(C.POINTER(C.c_double))
+    res.residual_norms = resid.ctypes.data_as(C.POINTER(C.c_double))
+    if want_X:
+        X = torch.empty((k, A.n), dtype=torch.float64, device=f"cuda:{ctx.device}")
+        res.X, res.ldx = C.c_void_p(X.data_ptr()), A.n
+    hist = _History()
+    c = cfg.to_c()
+    ctx.check(ctx.lib.mpeig_run_variant(ctx.h, A.h, T.h, C.byref(c), C.c_void_p(X0.data_ptr()),
+                                        X0.shape[1], a_norm_est, hist.cb, None, C.byref(res)))
+    return EigResult(theta, X, resid, res.iterations_lower, res.iterations_working, hist.records,
+                     bool(res.converged), _timings(res.timings), res.a_norm_estimate)
+
+
+def mixed_lobpcg(A: Operator, X0, cfg: SolverConfig) -> EigResult:
+    """mixed_lobpcg (drivers.hpp:122-152): forces MPLOBPCG_schol, fp32 Jacobi."""
+    cfg = SolverConfig(**{**cfg.__dict__, "variant": "mplobpcg-schol"})
+    est = spectral_norm_estimate(A, cfg.sketch_rows, cfg.seed ^ 0x9E3779B97F4A7C15)
+    return run_variant(A, X0, cfg, est, jacobi(A, LOWER))
+
+
+def lobpcg_stage(A: Operator, n: int, X0, cfg: SolverConfig, T: Operator, a_norm_est: float,
+                 opt: StageOptions, history: list = None, tim: StageTimings = None) -> StageOutcome:
+    """lobpcg_stage<T> (eigensolvers.hpp:195-321); dtype of X0 picks T (f64/f32)."""
+    torch = _torch()
+    ctx = A.ctx
+    m, ldx = X0.shape
+    Xo = torch.empty((m, n), dtype=X0.dtype, device=X0.device)
+    theta, resid = np.zeros(m), np.zeros(m)
+    out = L.StageOut(C.c_void_p(Xo.data_ptr()), n, theta.ctypes.data_as(C.POINTER(C.c_double)),
+                     resid.ctypes.data_as(C.POINTER(C.c_double)), 0, 0)
+    hist = _History()
+    t = L.Timings()
+    c = cfg.to_c()
+    o = L.StageOpts(opt.tol, int(opt.use_mixed_qr), int(opt.stagnation_exit), opt.tag)
+    fn = ctx.lib.mpeig_lobpcg_stage_f64 if X0.dtype == torch.float64 else ctx.lib.mpeig_lobpcg_stage_f32
+    rc = fn(ctx.h, A.h, n, C.c_void_p(X0.data_ptr()), ldx, m, C.byref(c), T.h, a_norm_est,
+            C.byref(o), hist.cb, None, C.byref(out), C.byref(t))
+    if history is not None:
+        history.extend(hist.records)
+    if tim is not None:
+        tim.precond_apply += t.precond_apply
+        tim.orthogonalize += t.orthogonalize
+        tim.projected_eig += t.projected_eig
+    ctx.check(rc)
+    return StageOutcome(Xo, theta, resid, int(out.iterations), bool(out.converged))
+
+
+def pinvit(A: Operator, n: int, X0, cfg: SolverConfig, T: Operator, a_norm_est: float = 0.0):
+    """pinvit<double> (eigensolvers.hpp:326-390), preconditioner as an operator."""
+    torch = _torch()
+    ctx = A.ctx
+    m, ldx = X0.shape
+    k = cfg.k
+    theta, resid = np.zeros(k), np.zeros(k)
+    X = torch.empty((k, n), dtype=torch.float64, device=X0.device)
+    res = L.Result()
+    res.theta = theta.ctypes.data_as(C.POINTER(C.c_double))
+    res.residual_norms = resid.ctypes.data_as(C.POINTER(C.c_double))
+    res.X, res.ldx = C.c_void_p(X.data_ptr()), n
+    hist = _History()
+    c = cfg.to_c()
+    ctx.check(ctx.lib.mpeig_pinvit_f64(ctx.h, A.h, n, C.c_void_p(X0.data_ptr()), ldx, m,
+                                       C.byref(c), T.h, a_norm_est, hist.cb, None, C.byref(res)))
+    return EigResult(theta, X, resid, 0, res.iterations_working, hist.records,
+                     bool(res.converged), _timings(res.timings), res.a_norm_estimate)
+
+
+def converged_count(a_norm_est: float, xnorm, theta, rnorm, tol: float) -> int:
+    """converged_count (eigensolvers.hpp:25-43) on precomputed column norms."""
+    n_c = 0
+    for j in range(len(theta)):
+        if rnorm[j] <= tol * (a_norm_est + abs(theta[j])) * xnorm[j]:
+            n_c += 1
+        else:
+            break
+    return n_c
+
+
+def gaussian_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
+    """gaussian_matrix<double> (dense_matrix.hpp:144-161), bit-exact stream."""
+    out = np.zeros((rows, cols), order="F")
+    rc = L.load().mpeig_gaussian_matrix_host(rows, cols, seed & 0xFFFFFFFFFFFFFFFF, out.ctypes.data)
+    if rc != 0:
+        raise MpeigError("gaussian_matrix failed")
+    return out
+
+
+# ------------------------------------------------- device <-> host helpers
+
+def to_device(A: np.ndarray, dtype=None, device: int = 0):
+    """n x c host block -> (c, n) contiguous CUDA tensor (column-major block)."""
+    torch = _torch()
+    A = np.asarray(A)
+    if A.ndim == 1:
+        A = A[:, None]
+    t = torch.from_numpy(np.ascontiguousarray(A.T))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(f"cuda:{device}")
+
+
+def to_host(X, n: int = None) -> np.ndarray:
+    """(c, ld) CUDA tensor -> n x c numpy (Fortran order)."""
+    a = X.detach().cpu().numpy()
+    if n is not None:
+        a = a[:, :n]
+    return np.asfortranarray(a.T)

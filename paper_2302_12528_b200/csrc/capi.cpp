@@ -1,0 +1,562 @@
+// capi.cpp -- the extern "C" boundary (include/mpeig_b200.h).
+//
+// Every entry point catches mpb::Error and CUDA failures and maps them to an
+// mpeig_status (1:1 with the reference exception types, errors.hpp:10-62),
+// keeping the message and index payload on the context.
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "context.hpp"
+#include "solver.hpp"
+
+using namespace mpb;
+
+namespace {
+
+template <typename F>
+int guard(mpeig_ctx* ctx, F&& f) {
+  try {
+    f();
+    if (ctx) {
+      ctx->last_msg.clear();
+      ctx->last_index = -1;
+    }
+    return MPEIG_OK;
+  } catch (const Error& e) {
+    if (ctx) {
+      ctx->last_msg = e.what();
+      ctx->last_index = e.index;
+    }
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->last_msg = "host allocation failed";
+    return MPEIG_E_OTHER;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->last_msg = e.what();
+    return MPEIG_E_OTHER;
+  }
+}
+
+void set_device(mpeig_ctx* ctx) { MPB_CUDA(cudaSetDevice(ctx->device)); }
+
+mpeig_op* new_op(mpeig_ctx* ctx, OpKind k, int64_t n) {
+  auto* op = new mpeig_op();
+  op->kind = k;
+  op->ctx = ctx;
+  op->n = n;
+  return op;
+}
+
+template <typename T>
+T* upload(const T* host, size_t count, cudaStream_t s) {
+  T* d = nullptr;
+  MPB_CUDA(cudaMalloc(reinterpret_cast<void**>(&d), count * sizeof(T)));
+  MPB_CUDA(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  return d;
+}
+
+// to_lower of a coefficient array (precision.hpp:102-107); false on overflow
+bool narrow(const double* src, size_t count, std::vector<float>& dst) {
+  dst.resize(count);
+  bool ok = true;
+  for (size_t i = 0; i < count; ++i) {
+    const float y = static_cast<float>(src[i]);
+    if (std::isfinite(src[i]) && !std::isfinite(y)) ok = false;
+    dst[i] = y;
+  }
+  return ok;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mpeig_ctx_create(int device, void* cuda_stream, mpeig_ctx** out) {
+  auto* ctx = new mpeig_ctx();
+  ctx->device = device;
+  const int rc = guard(ctx, [&] {
+    MPB_CUDA(cudaSetDevice(device));
+    if (cuda_stream) {
+      ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+    } else {
+      MPB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      ctx->own_stream = true;
+    }
+    if (cusolverDnCreate(&ctx->cusolver) != CUSOLVER_STATUS_SUCCESS)
+      throw Error(MPEIG_E_CUSOLVER, "cusolverDnCreate failed");
+    cusolverDnSetStream(ctx->cusolver, ctx->stream);
+    if (cublasCreate(&ctx->cublas) != CUBLAS_STATUS_SUCCESS)
+      throw Error(MPEIG_E_CUDA, "cublasCreate failed");
+    cublasSetStream(ctx->cublas, ctx->stream);
+    cublasSetMathMode(ctx->cublas, CUBLAS_PEDANTIC_MATH);  // no TF32 in the fp32 stage
+    MPB_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->d_status), 16 * sizeof(int)));
+    MPB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_status), 16 * sizeof(int)));
+    ctx->h_pinned_elems = 4096;
+    MPB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_pinned),
+                            static_cast<size_t>(ctx->h_pinned_elems) * sizeof(double)));
+    // keep freed stage buffers cached in the stream-ordered pool
+    cudaMemPool_t pool;
+    MPB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  });
+  if (rc != MPEIG_OK) {
+    mpeig_ctx_destroy(ctx);
+    *out = nullptr;
+    return rc;
+  }
+  *out = ctx;
+  return MPEIG_OK;
+}
+
+void mpeig_ctx_destroy(mpeig_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->cusolver) cusolverDnDestroy(ctx->cusolver);
+  if (ctx->cublas) cublasDestroy(ctx->cublas);
+  if (ctx->d_status) cudaFree(ctx->d_status);
+  if (ctx->h_status) cudaFreeHost(ctx->h_status);
+  if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* mpeig_last_error(mpeig_ctx* ctx, int64_t* index) {
+  if (!ctx) return "null context";
+  if (index) *index = ctx->last_index;
+  return ctx->last_msg.c_str();
+}
+
+int64_t mpeig_launch_count(mpeig_ctx* ctx, int reset) {
+  (void)ctx;
+  return reset ? g_launches.exchange(0) : g_launches.load();
+}
+
+void* mpeig_ctx_stream(mpeig_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+// ---------------------------------------------------------------- operators
+int mpeig_op_lap3d(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, mpeig_op** out) {
+  return guard(ctx, [&] {
+    if (nx < 1 || ny < 1 || nz < 1) throw Error(MPEIG_E_CONFIG, "lap3d: grid sides must be >= 1");
+    mpeig_op* op = new_op(ctx, kOpLap3d, nx * ny * nz);
+    op->nx = nx;
+    op->ny = ny;
+    op->nz = nz;
+    *out = op;
+  });
+}
+
+int mpeig_op_lap2d(mpeig_ctx* ctx, int64_t nx, int64_t ny, mpeig_op** out) {
+  return guard(ctx, [&] {
+    if (nx < 1 || ny < 1) throw Error(MPEIG_E_CONFIG, "gen_laplace2d: grid sides must be >= 1");
+    mpeig_op* op = new_op(ctx, kOpLap2d, nx * ny);
+    op->nx = nx;
+    op->ny = ny;
+    op->nz = 1;
+    *out = op;
+  });
+}
+
+int mpeig_op_csr(mpeig_ctx* ctx, int64_t n, const int64_t* row_ptr_host,
+                 const int64_t* col_idx_host, const double* vals_host, mpeig_op** out) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    if (n < 1) throw Error(MPEIG_E_DIMENSION, "csr: n must be >= 1");
+    const int64_t nnz = row_ptr_host[n];
+    for (int64_t i = 0; i < n; ++i) {
+      if (row_ptr_host[i + 1] < row_ptr_host[i]) throw Error(MPEIG_E_DIMENSION, "csr: row_ptr not monotone");
+      for (int64_t q = row_ptr_host[i]; q < row_ptr_host[i + 1]; ++q) {
+        if (col_idx_host[q] < 0 || col_idx_host[q] >= n)
+          throw Error(MPEIG_E_DIMENSION, "from_triplets: index out of range");
+        if (q > row_ptr_host[i] && col_idx_host[q] <= col_idx_host[q - 1])
+          throw Error(MPEIG_E_DIMENSION, "csr: columns must be sorted and unique per row");
+      }
+    }
+    mpeig_op* op = new_op(ctx, kOpCsr, n);
+    cudaStream_t s = ctx->stream;
+    op->rp = upload(row_ptr_host, static_cast<size_t>(n + 1), s);
+    op->ci = upload(col_idx_host, static_cast<size_t>(nnz), s);
+    op->vals = upload(vals_host, static_cast<size_t>(nnz), s);
+    std::vector<float> vl;
+    op->lower_overflow = !narrow(vals_host, static_cast<size_t>(nnz), vl);
+    op->vals_l = upload(vl.data(), vl.size(), s);
+    MPB_CUDA(cudaStreamSynchronize(s));
+    *out = op;
+  });
+}
+
+int mpeig_op_dense(mpeig_ctx* ctx, int64_t n, const double* A_host, int64_t lda, mpeig_op** out) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    if (n < 1 || lda < n) throw Error(MPEIG_E_DIMENSION, "dense: bad shape");
+    mpeig_op* op = new_op(ctx, kOpDense, n);
+    std::vector<double> a(static_cast<size_t>(n * n));
+    for (int64_t j = 0; j < n; ++j) std::memcpy(&a[j * n], A_host + j * lda, sizeof(double) * n);
+    cudaStream_t s = ctx->stream;
+    op->A = upload(a.data(), a.size(), s);
+    op->lda = n;
+    std::vector<float> al;
+    op->lower_overflow = !narrow(a.data(), a.size(), al);
+    op->Al = upload(al.data(), al.size(), s);
+    MPB_CUDA(cudaStreamSynchronize(s));
+    *out = op;
+  });
+}
+
+int mpeig_op_device_callback(mpeig_ctx* ctx, int64_t n, mpeig_apply_fn apply_working,
+                             mpeig_apply_fn apply_lower, void* user, mpeig_op** out) {
+  return guard(ctx, [&] {
+    mpeig_op* op = new_op(ctx, kOpDeviceCb, n);
+    op->dev_w = apply_working;
+    op->dev_l = apply_lower;
+    op->user = user;
+    *out = op;
+  });
+}
+
+int mpeig_op_host_callback(mpeig_ctx* ctx, int64_t n, mpeig_host_apply_fn apply_working,
+                           mpeig_host_apply_fn apply_lower, void* user, mpeig_op** out) {
+  return guard(ctx, [&] {
+    mpeig_op* op = new_op(ctx, kOpHostCb, n);
+    op->host_w = apply_working;
+    op->host_l = apply_lower;
+    op->user = user;
+    *out = op;
+  });
+}
+
+int mpeig_precond_jacobi(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision, mpeig_op** out) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    const int64_t n = A->n;
+    std::vector<double> d(static_cast<size_t>(n));
+    cudaStream_t s = ctx->stream;
+    switch (A->kind) {
+      case kOpLap3d:
+        std::fill(d.begin(), d.end(), 6.0);
+        break;
+      case kOpLap2d:
+        std::fill(d.begin(), d.end(), 4.0);
+        break;
+      case kOpCsr: {
+        std::vector<int64_t> rp(static_cast<size_t>(n + 1));
+        MPB_CUDA(cudaMemcpyAsync(rp.data(), A->rp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+        MPB_CUDA(cudaStreamSynchronize(s));
+        std::vector<int64_t> ci(static_cast<size_t>(rp[n]));
+        std::vector<double> v(static_cast<size_t>(rp[n]));
+        MPB_CUDA(cudaMemcpyAsync(ci.data(), A->ci, sizeof(int64_t) * rp[n], cudaMemcpyDeviceToHost, s));
+        MPB_CUDA(cudaMemcpyAsync(v.data(), A->vals, sizeof(double) * rp[n], cudaMemcpyDeviceToHost, s));
+        MPB_CUDA(cudaStreamSynchronize(s));
+        for (int64_t i = 0; i < n; ++i) {
+          d[i] = 0.0;
+          for (int64_t q = rp[i]; q < rp[i + 1]; ++q)
+            if (ci[q] == i) d[i] = v[q];
+        }
+        break;
+      }
+      case kOpDense: {
+        for (int64_t i = 0; i < n; ++i)
+          MPB_CUDA(cudaMemcpyAsync(&d[i], A->A + i + i * A->lda, sizeof(double), cudaMemcpyDeviceToHost, s));
+        MPB_CUDA(cudaStreamSynchronize(s));
+        break;
+      }
+      default:
+        throw Error(MPEIG_E_CONFIG, "jacobi: operator has no explicit diagonal");
+    }
+    std::vector<double> dinv(static_cast<size_t>(n));
+    std::vector<float> dinvf(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      if (!(d[i] != 0.0)) throw Error(MPEIG_E_NOT_PD, "jacobi: zero diagonal", i);
+      dinv[i] = 1.0 / d[i];
+      dinvf[i] = static_cast<float>(dinv[i]);
+    }
+    mpeig_op* op = new_op(ctx, kOpJacobi, n);
+    op->precision = precision;
+    op->dinv = upload(dinv.data(), dinv.size(), s);
+    op->dinvf = upload(dinvf.data(), dinvf.size(), s);
+    MPB_CUDA(cudaStreamSynchronize(s));
+    *out = op;
+  });
+}
+
+void mpeig_op_destroy(mpeig_op* op) {
+  if (!op) return;
+  if (op->ctx && op->ctx->stream) cudaStreamSynchronize(op->ctx->stream);
+  cudaFree(op->rp);
+  cudaFree(op->ci);
+  cudaFree(op->vals);
+  cudaFree(op->vals_l);
+  cudaFree(op->A);
+  cudaFree(op->Al);
+  cudaFree(op->dinv);
+  cudaFree(op->dinvf);
+  delete op;
+}
+
+int64_t mpeig_op_n(const mpeig_op* op) { return op ? op->n : 0; }
+
+int mpeig_op_apply(mpeig_ctx* ctx, const mpeig_op* op, int32_t precision, int64_t ncols,
+                   const void* X, int64_t ldx, void* Y, int64_t ldy) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    if (precision == MPEIG_WORKING)
+      op_apply<double>(ctx, op, ncols, static_cast<const double*>(X), ldx, static_cast<double*>(Y), ldy);
+    else
+      op_apply<float>(ctx, op, ncols, static_cast<const float*>(X), ldx, static_cast<float*>(Y), ldy);
+    MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// ------------------------------------------------------------------ solvers
+int mpeig_spectral_norm_estimate(mpeig_ctx* ctx, const mpeig_op* A, int64_t sketch_rows,
+                                 uint64_t seed, double* out) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    *out = spectral_norm_estimate(ctx, A, sketch_rows, seed);
+  });
+}
+
+static void fill_stage_out(const StageResult& r, int64_t m, mpeig_stage_out* out) {
+  out->iterations = r.iterations;
+  out->converged = r.converged ? 1 : 0;
+  for (int64_t j = 0; j < m; ++j) {
+    if (out->theta) out->theta[j] = r.theta[j];
+    if (out->residual_norms) out->residual_norms[j] = r.resid[j];
+  }
+}
+
+int mpeig_lobpcg_stage_f64(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const double* X0,
+                           int64_t ldx0, int64_t m, const mpeig_cfg* cfg, const mpeig_op* T,
+                           double a_norm_est, const mpeig_stage_opts* opt,
+                           mpeig_history_sink sink, void* sink_user, mpeig_stage_out* out,
+                           mpeig_timings* tim) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    if (A->n != n) throw Error(MPEIG_E_DIMENSION, "lobpcg_stage: X0 has wrong rows");
+    const StageResult r = lobpcg_stage<double>(ctx, A, n, X0, ldx0, m, *cfg, T, a_norm_est, *opt, sink,
+                                               sink_user, static_cast<double*>(out->X), out->ldx, tim);
+    fill_stage_out(r, m, out);
+  });
+}
+
+int mpeig_lobpcg_stage_f32(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const float* X0,
+                           int64_t ldx0, int64_t m, const mpeig_cfg* cfg, const mpeig_op* T,
+                           double a_norm_est, const mpeig_stage_opts* opt,
+                           mpeig_history_sink sink, void* sink_user, mpeig_stage_out* out,
+                           mpeig_timings* tim) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    if (A->n != n) throw Error(MPEIG_E_DIMENSION, "lobpcg_stage: X0 has wrong rows");
+    const StageResult r = lobpcg_stage<float>(ctx, A, n, X0, ldx0, m, *cfg, T, a_norm_est, *opt, sink,
+                                              sink_user, static_cast<float*>(out->X), out->ldx, tim);
+    fill_stage_out(r, m, out);
+  });
+}
+
+int mpeig_pinvit_f64(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const double* X0, int64_t ldx0,
+                     int64_t m, const mpeig_cfg* cfg, const mpeig_op* T, double a_norm_est,
+                     mpeig_history_sink sink, void* sink_user, mpeig_result* out) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    validate_cfg(*cfg, n);
+    if (m < cfg->k) throw Error(MPEIG_E_CONFIG, "pinvit: X0 has fewer columns than k");
+    if (a_norm_est <= 0)
+      a_norm_est = spectral_norm_estimate(ctx, A, cfg->sketch_rows, cfg->seed ^ 0x9e3779b97f4a7c15ULL);
+    const int64_t ld = padded_ld(n);
+    DevBuf<double> Xf(static_cast<size_t>(ld * m), ctx->stream);
+    const StageResult r = pinvit(ctx, A, n, X0, ldx0, m, *cfg, T, a_norm_est, sink, sink_user, Xf.p,
+                                 ld, &out->timings);
+    out->a_norm_estimate = a_norm_est;
+    out->iterations_lower = 0;
+    out->iterations_working = r.iterations;
+    out->converged = r.converged ? 1 : 0;
+    for (int64_t j = 0; j < cfg->k; ++j) {
+      if (out->theta) out->theta[j] = r.theta[j];
+      if (out->residual_norms) out->residual_norms[j] = r.resid[j];
+    }
+    if (out->X) copy_block<double>(n, cfg->k, Xf.p, ld, out->X, out->ldx, ctx->stream);
+    MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int mpeig_solve(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T, const mpeig_cfg* cfg,
+                mpeig_history_sink sink, void* sink_user, mpeig_result* out) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    out->timings = mpeig_timings{};
+    solve(ctx, A, T, *cfg, sink, sink_user, out);
+  });
+}
+
+int mpeig_run_variant(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T, const mpeig_cfg* cfg,
+                      const double* X0, int64_t ldx0, double a_norm_est, mpeig_history_sink sink,
+                      void* sink_user, mpeig_result* out) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    validate_cfg(*cfg, A->n);
+    out->timings = mpeig_timings{};
+    run_variant(ctx, A, T, *cfg, X0, ldx0, a_norm_est, sink, sink_user, out);
+  });
+}
+
+// ----------------------------------------------------- kernel-level entries
+int mpeig_gaussian_matrix_host(int64_t rows, int64_t cols, uint64_t seed, double* out_host) {
+  return guard(nullptr, [&] { gaussian_fill(rows, cols, seed, out_host); });
+}
+
+int mpeig_orthonormal_q_f64(mpeig_ctx* ctx, int64_t n, int64_t m, double* W, int64_t ldw,
+                            int32_t use_mixed) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    Work<double> w(ctx, n, m, m);
+    orthonormal_q<double>(w, m, W, ldw, use_mixed != 0);
+    MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int mpeig_orthonormal_q_f32(mpeig_ctx* ctx, int64_t n, int64_t m, float* W, int64_t ldw) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    Work<float> w(ctx, n, m, m);
+    orthonormal_q<float>(w, m, W, ldw, false);
+    MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+static int qr_entry(mpeig_ctx* ctx, int64_t n, int64_t m, double* W, int64_t ldw, double* R_out,
+                    bool lower) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    if (n < m) throw Error(MPEIG_E_DIMENSION, "qr: more columns than rows");
+    Work<double> w(ctx, n, m, m);
+    int64_t idx = 0;
+    DevBuf<double> R(static_cast<size_t>(m * m), ctx->stream);
+    const int st = qr_with_r(w, m, W, ldw, lower, R.p, &idx);
+    if (st != 0) throw Error(st, lower ? "mixed_qr failed" : "householder_qr failed", idx);
+    if (R_out) MPB_CUDA(cudaMemcpyAsync(R_out, R.p, sizeof(double) * m * m, cudaMemcpyDeviceToDevice,
+                                        ctx->stream));
+    MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int mpeig_mixed_qr_f64(mpeig_ctx* ctx, int64_t n, int64_t m, double* W, int64_t ldw, double* R_out) {
+  return qr_entry(ctx, n, m, W, ldw, R_out, true);
+}
+
+int mpeig_householder_qr_f64(mpeig_ctx* ctx, int64_t n, int64_t m, double* W, int64_t ldw,
+                             double* R_out) {
+  return qr_entry(ctx, n, m, W, ldw, R_out, false);
+}
+
+int mpeig_orthonormal_q_dropping_f64(mpeig_ctx* ctx, int64_t n, int64_t m, double* W, int64_t ldw,
+                                     int32_t use_mixed, int64_t* kept) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    Work<double> w(ctx, n, m, m);
+    int64_t dropped = 0;
+    *kept = orthonormal_q_dropping<double>(w, m, W, ldw, use_mixed != 0, &dropped);
+    MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int mpeig_gram_f64(mpeig_ctx* ctx, int64_t n, int64_t ka, const double* A, int64_t lda, int64_t kb,
+                   const double* B, int64_t ldb, double* G) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    DevBuf<double> wk(static_cast<size_t>(gram_workspace_elems<double>(n, ka, kb)), ctx->stream);
+    gram<double>(n, ka, A, lda, kb, B, ldb, G, ka, 0, wk.p, ctx->stream);
+    MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int mpeig_gemm_f64(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, double alpha, const double* A,
+                   int64_t lda, const double* Cm, int64_t ldc, double beta, const double* Z,
+                   int64_t ldz, double* Y, int64_t ldy) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    gemm_tn<double>(n, k, c, alpha, A, lda, Cm, ldc, beta, Z, ldz, Y, ldy, ctx->stream);
+    MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int mpeig_project_out_f64(mpeig_ctx* ctx, int64_t n, int64_t b, const double* B, int64_t ldb,
+                          int64_t wc, double* W, int64_t ldw, int32_t passes) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    Work<double> w(ctx, n, std::max(b, wc), std::max(b, wc));
+    project_out<double>(w, B, b, ldb, W, wc, ldw, passes);
+    MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int mpeig_small_eig_f64(mpeig_ctx* ctx, int64_t s, const double* M, double* values,
+                        double* vectors) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    Work<double> w(ctx, 3 * s, s, s);
+    MPB_CUDA(cudaMemcpyAsync(vectors, M, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, ctx->stream));
+    status_clear(ctx);
+    small_eig<double>(w, s, vectors, s, values);
+    status_fetch(ctx);
+    if (ctx->h_status[3] > 0) throw Error(MPEIG_E_NO_CONVERGENCE, "small_herm_eig: syevd did not converge");
+  });
+}
+
+int mpeig_hl_coeffs_f64(mpeig_ctx* ctx, int64_t s, int64_t m, const double* C, double* coef,
+                        int64_t* p, int32_t* fallback) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    if (s < m) throw Error(MPEIG_E_DIMENSION, "hl_update: fewer columns than m");
+    const int64_t pn = std::min(m, s - m);
+    DevBuf<double> scratch(static_cast<size_t>(pn * m + 2 * pn * pn + pn + 1), ctx->stream);
+    status_clear(ctx);
+    hl_coeffs(s, m, pn, C, s, coef, scratch.p, ctx->d_status + 4, ctx->stream);
+    status_fetch(ctx);
+    *p = pn;
+    *fallback = ctx->h_status[4];
+  });
+}
+
+int mpeig_residual_precond_f64(mpeig_ctx* ctx, const mpeig_op* T, int64_t n, int64_t m,
+                               const double* X, int64_t ldx, const double* AX, int64_t ldax,
+                               const double* theta_host, double* W, int64_t ldw, double* rnorm_host,
+                               double* xnorm_host) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    cudaStream_t s = ctx->stream;
+    DevBuf<double> th(static_cast<size_t>(m), s);
+    DevBuf<double> wk(static_cast<size_t>(resid_workspace_elems(n, m) + 2 * m), s);
+    MPB_CUDA(cudaMemcpyAsync(th.p, theta_host, sizeof(double) * m, cudaMemcpyHostToDevice, s));
+    const void* dinv = nullptr;
+    int mode = kResidPlain;
+    if (T) {
+      if (T->kind != kOpJacobi) throw Error(MPEIG_E_CONFIG, "residual_precond: T must be Jacobi");
+      if (T->precision == MPEIG_WORKING) {
+        mode = kResidJacobiT;
+        dinv = T->dinv;
+      } else {
+        mode = kResidSandwich;
+        dinv = T->dinvf;
+      }
+    }
+    status_clear(ctx);
+    double* norms = wk.p + resid_workspace_elems(n, m);
+    residual_precond<double>(mode, n, m, X, ldx, AX, ldax, th.p, dinv, W, ldw, norms, norms + m,
+                             ctx->d_status + 2, wk.p, s);
+    std::vector<double> h(static_cast<size_t>(2 * m));
+    MPB_CUDA(cudaMemcpyAsync(h.data(), norms, sizeof(double) * 2 * m, cudaMemcpyDeviceToHost, s));
+    status_fetch(ctx);
+    for (int64_t j = 0; j < m; ++j) {
+      rnorm_host[j] = h[j];
+      xnorm_host[j] = h[m + j];
+    }
+    if (ctx->h_status[2]) throw Error(MPEIG_E_OVERFLOW, "to_lower: value exceeds binary32 range");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,50 @@
+// common.cuh -- shared definitions for the sm_100a LOBPCG hot path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "mpeig_b200.h"
+
+namespace mpb {
+
+// Exception carrying an mpeig_status code (1:1 with the reference's
+// errors.hpp types, see include/mpeig_b200.h) and an optional index payload.
+struct Error : std::runtime_error {
+  int code;
+  int64_t index;
+  Error(int c, const std::string& m, int64_t idx = -1)
+      : std::runtime_error(m), code(c), index(idx) {}
+};
+
+#define MPB_CUDA(call)                                                          \
+  do {                                                                          \
+    cudaError_t e_ = (call);                                                    \
+    if (e_ != cudaSuccess)                                                      \
+      throw ::mpb::Error(MPEIG_E_CUDA, std::string(#call) + ": " +              \
+                                           cudaGetErrorString(e_));             \
+  } while (0)
+
+// Kernels launched by this library (reported as gpu_launches by bench.py).
+extern std::atomic<int64_t> g_launches;
+
+#define MPB_LAUNCH_CHECK()                      \
+  do {                                          \
+    ::mpb::g_launches.fetch_add(1, std::memory_order_relaxed); \
+    MPB_CUDA(cudaGetLastError());               \
+  } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+constexpr int kNumSMs = 148;  // B200
+
+// Leading dimension of every device block vector: rows padded to 32
+// elements (256 B for fp64) so every column starts 256-B aligned.
+inline int64_t padded_ld(int64_t n) { return round_up(n, 32); }
+
+}  // namespace mpb

@@ -1,0 +1,105 @@
+// context.hpp -- context, operators and device buffers (host side).
+#pragma once
+
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+struct mpeig_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cusolverDnHandle_t cusolver = nullptr;
+  cublasHandle_t cublas = nullptr;
+  std::string last_msg;
+  int64_t last_index = -1;
+  int* d_status = nullptr;      // 16 ints of device status slots
+  int* h_status = nullptr;      // pinned mirror
+  double* h_pinned = nullptr;   // pinned staging for per-iteration records
+  int64_t h_pinned_elems = 0;
+};
+
+enum OpKind { kOpLap3d, kOpLap2d, kOpCsr, kOpDense, kOpDeviceCb, kOpHostCb, kOpJacobi };
+
+struct mpeig_op {
+  OpKind kind;
+  mpeig_ctx* ctx = nullptr;
+  int64_t n = 0, nx = 0, ny = 0, nz = 0;
+  // CSR (device)
+  int64_t* rp = nullptr;
+  int64_t* ci = nullptr;
+  double* vals = nullptr;
+  float* vals_l = nullptr;
+  // dense (device)
+  double* A = nullptr;
+  float* Al = nullptr;
+  int64_t lda = 0;
+  // callbacks
+  mpeig_apply_fn dev_w = nullptr, dev_l = nullptr;
+  mpeig_host_apply_fn host_w = nullptr, host_l = nullptr;
+  void* user = nullptr;
+  // Jacobi
+  int32_t precision = MPEIG_WORKING;
+  double* dinv = nullptr;   // 1 / diag, fp64
+  float* dinvf = nullptr;   // to_lower(1 / diag)
+  bool lower_overflow = false;  // to_lower of the coefficients overflowed
+};
+
+namespace mpb {
+
+// RAII stream-ordered device buffer
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t count = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t n, cudaStream_t st) { alloc(n, st); }
+  void alloc(size_t n, cudaStream_t st) {
+    release();
+    s = st;
+    count = n;
+    if (n) MPB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), st));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    count = 0;
+  }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), count(o.count), s(o.s) { o.p = nullptr; o.count = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    release();
+    p = o.p;
+    count = o.count;
+    s = o.s;
+    o.p = nullptr;
+    o.count = 0;
+    return *this;
+  }
+  T* get() const { return p; }
+};
+
+// host-side gaussian block generation (rng.cpp)
+void gaussian_fill(int64_t rows, int64_t cols, uint64_t seed, double* out);
+uint64_t pcg64_draw(uint64_t seed, uint64_t index);
+
+// operator application (ops dispatch in solver.cpp)
+template <typename T>
+void op_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* X, int64_t ldx, T* Y,
+              int64_t ldy);
+
+// status helpers
+void status_clear(mpeig_ctx* ctx);
+void status_fetch(mpeig_ctx* ctx);  // synchronises the stream
+
+}  // namespace mpb

@@ -1,0 +1,131 @@
+// kernels.cuh -- launcher declarations for the sm_100a kernels.
+//
+// All block vectors are column-major device arrays with explicit leading
+// dimensions.  Every launcher is stream-ordered and never synchronises.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace mpb {
+
+// ----------------------------------------------------------------- dense
+// Workspace (device) needed by gram(): floats of type T.
+template <typename T>
+int64_t gram_workspace_elems(int64_t n, int64_t ka, int64_t kb);
+
+// G (ka x kb, ld ldg) = A^T B over n rows (adjoint_matmul,
+// dense_kernels.hpp:36-52).  Split-n partial products reduced in a fixed
+// order -> bitwise deterministic for a given n.  `sym` != 0 additionally
+// symmetrises G in place like hermitize (dense_kernels.hpp:77-88); needs
+// ka == kb.  work: gram_workspace_elems<T>() elements.
+template <typename T>
+void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B,
+          int64_t ldb, T* G, int64_t ldg, int sym, T* work, cudaStream_t s);
+
+// Y (n x c) = beta Z + alpha A (n x k) C (k x c)   (matmul, dense_kernels.hpp:20-34)
+// Y may alias Z (elementwise read-before-write); Y must not alias A.
+template <typename T>
+void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, const T* C,
+             int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y, int64_t ldy, cudaStream_t s);
+
+// dst = (To) src, elementwise over an n x c block; to_lower() narrowing sets
+// *overflow_flag = 1 on finite -> inf (precision.hpp:102-107).
+void convert_f64_to_f32(int64_t n, int64_t c, const double* src, int64_t lds, float* dst,
+                        int64_t ldd, int* overflow_flag, cudaStream_t s);
+void convert_f32_to_f64(int64_t n, int64_t c, const float* src, int64_t lds, double* dst,
+                        int64_t ldd, cudaStream_t s);
+template <typename T>
+void copy_block(int64_t n, int64_t c, const T* src, int64_t lds, T* dst, int64_t ldd,
+                cudaStream_t s);
+
+// Y = alpha X (elementwise; Y may alias X)
+template <typename T>
+void scale_block(int64_t n, int64_t c, T alpha, const T* X, int64_t ldx, T* Y, int64_t ldy,
+                 cudaStream_t s);
+
+// sum of squares of every entry of an n x c block -> *out (device, double)
+template <typename T>
+void frob_sq(int64_t n, int64_t c, const T* X, int64_t ldx, double* out, double* work,
+             cudaStream_t s);
+
+// ------------------------------------------------------------- residual
+// Jacobi/f_T modes of the fused residual kernel
+enum ResidMode {
+  kResidPlain = 0,     // W = R
+  kResidJacobiT = 1,   // W = R .* dinv (dinv in T)
+  kResidSandwich = 2,  // W = to_working(to_lower(R) .* dinvf)   (T = double)
+};
+int64_t resid_workspace_elems(int64_t n, int64_t m);
+// R = AX - X diag(theta) (residual_block, eigensolvers.hpp:104-115); column
+// norms of R and X (col_norm, dense_matrix.hpp:74-82) -> rnorm/xnorm (device
+// double, length m); W = f(R) by mode.  dinv is T or float per mode.
+template <typename T>
+void residual_precond(int mode, int64_t n, int64_t m, const T* X, int64_t ldx, const T* AX,
+                      int64_t ldax, const T* theta, const void* dinv, T* W, int64_t ldw,
+                      double* rnorm, double* xnorm, int* overflow_flag, double* work,
+                      cudaStream_t s);
+// W = f_T(R) without residual (generic Jacobi apply on a block)
+template <typename T>
+void jacobi_apply(int mode, int64_t n, int64_t c, const T* R, int64_t ldr, const void* dinv,
+                  T* W, int64_t ldw, int* overflow_flag, cudaStream_t s);
+// Y = X - W (subtract, dense_kernels.hpp:54-62)
+template <typename T>
+void subtract(int64_t n, int64_t c, const T* X, int64_t ldx, const T* W, int64_t ldw, T* Y,
+              int64_t ldy, cudaStream_t s);
+
+// ------------------------------------------------------------- operators
+// 3-D 7-point / 2-D 5-point Laplacian, matrix-free, reference summation order
+template <typename T>
+void stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t c, const T* X, int64_t ldx, T* Y,
+              int64_t ldy, cudaStream_t s);
+template <typename T>
+void stencil5(int64_t nx, int64_t ny, int64_t c, const T* X, int64_t ldx, T* Y, int64_t ldy,
+              cudaStream_t s);
+// CSR SpMM (spmv_block, sparse_kernels.hpp:16-33), ascending-column order
+template <typename T>
+void csr_spmm(int64_t n, const int64_t* row_ptr, const int64_t* col_idx, const T* vals,
+              int64_t c, const T* X, int64_t ldx, T* Y, int64_t ldy, cudaStream_t s);
+
+// ---------------------------------------------------------- small dense
+// Small (<= ~600) matrices, single-CTA kernels working in global memory.
+// status layout (device int[2]): [0] code, [1] index; the first error wins.
+template <typename T>
+void small_symmetrize(int64_t s, T* G, int64_t ldg, cudaStream_t st);
+// lower Cholesky G = L L^T (dense_cholesky, dense_kernels.hpp:128-152) and
+// Uinv = L^{-T} (upper).  On failure status = {NOT_PD|OVERFLOW, index}.
+template <typename T>
+void small_cholesky_inv(int64_t m, const T* G, int64_t ldg, T* L, T* Uinv, int* status,
+                        cudaStream_t st);
+// Rinv = R^{-1} for upper-triangular R (check_tri_diag, dense_kernels.hpp:163-170)
+template <typename T>
+void small_upper_inverse(int64_t m, const T* R, int64_t ldr, T* Rinv, int* status,
+                         cudaStream_t st);
+// C = A B for small square/rect blocks (all device, col-major)
+template <typename T>
+void small_matmul(int64_t r, int64_t k, int64_t c, const T* A, int64_t lda, const T* B,
+                  int64_t ldb, T* C, int64_t ldc, cudaStream_t st);
+// B = A^T
+template <typename T>
+void small_transpose(int64_t r, int64_t c, const T* A, int64_t lda, T* B, int64_t ldb,
+                     cudaStream_t st);
+// Hetmaniuk-Lehoucq coefficient block (eigensolvers.hpp:148-174):
+// coef = [C(:,0:m) | C(:,m:m+p) V], V from householder_qr_square of
+// C(0:m, m:m+p)^T (ortho.hpp:114-121); rank-deficient -> V = I, flag.
+void hl_coeffs(int64_t s, int64_t m, int64_t p, const double* C, int64_t ldc, double* coef,
+               double* scratch, int* fallback, cudaStream_t st);
+void hl_coeffs_f32(int64_t s, int64_t m, int64_t p, const float* C, int64_t ldc, float* coef,
+                   float* scratch, int* fallback, cudaStream_t st);
+
+// ------------------------------------------------------------------ TSQR
+// R factor (m x m, upper, positive diagonal) of a tall n x m block by a
+// Householder TSQR tree in precision Tq; the input is read in Tin and
+// narrowed on load when Tin != Tq (to_lower with overflow check).
+// status: [0] = RANK_DEFICIENT / OVERFLOW, [1] = column index.
+template <typename Tin, typename Tq>
+int64_t tsqr_workspace_elems(int64_t n, int64_t m);
+template <typename Tin, typename Tq>
+void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr, Tq* work,
+            int* status, cudaStream_t s);
+
+}  // namespace mpb

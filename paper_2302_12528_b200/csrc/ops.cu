@@ -1,0 +1,127 @@
+// ops.cu -- block operator apply A.X (K1): matrix-free stencils and CSR SpMM.
+//
+// Every output entry accumulates its row's entries in ascending column order
+// starting from zero, each product and sum rounded separately, exactly like
+// spmv_block (sparse_kernels.hpp:16-33) on the CSR form of the same matrix
+// (csr_matrix.hpp:31-58 sorts columns).  The result is therefore bitwise
+// identical to the reference operator, so A.X never contributes to
+// trajectory drift.  Coefficients are exactly representable in fp32 as well
+// (to_lower of -1, 4, 6), so the lower-precision apply follows the same code.
+#include "common.cuh"
+#include "kernels.cuh"
+#include "rn.cuh"
+
+namespace mpb {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T acc_neg(T s, T x) {  // s += (-1) * x
+  return add_rn(s, mul_rn(T(-1), x));
+}
+
+// One thread per (row, column); rows of a column are consecutive threads so
+// every neighbour load of a warp is a contiguous 256-B segment (L1/L2 absorb
+// the 7-fold reuse; HBM traffic stays ~ read X + write Y).
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_stencil7(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t ldx,
+           T* __restrict__ Y, int64_t ldy) {
+  const int64_t n = nx * ny * nz;
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p >= n) return;
+  const int64_t j = blockIdx.y;
+  const T* x = X + j * ldx;
+  const int64_t xi = p % nx;
+  const int64_t yz = p / nx;
+  const int64_t yi = yz % ny;
+  const int64_t zi = yz / ny;
+  const int64_t sy = nx, sz = nx * ny;
+  T s = T(0);
+  if (zi > 0) s = acc_neg(s, x[p - sz]);
+  if (yi > 0) s = acc_neg(s, x[p - sy]);
+  if (xi > 0) s = acc_neg(s, x[p - 1]);
+  s = add_rn(s, mul_rn(T(6), x[p]));
+  if (xi + 1 < nx) s = acc_neg(s, x[p + 1]);
+  if (yi + 1 < ny) s = acc_neg(s, x[p + sy]);
+  if (zi + 1 < nz) s = acc_neg(s, x[p + sz]);
+  Y[p + j * ldy] = s;
+}
+
+// gen_laplace2d (generators.cpp:13-30): row p = i + nx*j, diag 4
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_stencil5(int64_t nx, int64_t ny, const T* __restrict__ X, int64_t ldx, T* __restrict__ Y,
+           int64_t ldy) {
+  const int64_t n = nx * ny;
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p >= n) return;
+  const int64_t c = blockIdx.y;
+  const T* x = X + c * ldx;
+  const int64_t i = p % nx, j = p / nx;
+  T s = T(0);
+  if (j > 0) s = acc_neg(s, x[p - nx]);
+  if (i > 0) s = acc_neg(s, x[p - 1]);
+  s = add_rn(s, mul_rn(T(4), x[p]));
+  if (i + 1 < nx) s = acc_neg(s, x[p + 1]);
+  if (j + 1 < ny) s = acc_neg(s, x[p + nx]);
+  Y[p + c * ldy] = s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_csr_spmm(int64_t n, const int64_t* __restrict__ rp, const int64_t* __restrict__ ci,
+           const T* __restrict__ v, const T* __restrict__ X, int64_t ldx, T* __restrict__ Y,
+           int64_t ldy) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const int64_t c = blockIdx.y;
+  const T* x = X + c * ldx;
+  T s = T(0);
+  const int64_t e = rp[i + 1];
+  for (int64_t q = rp[i]; q < e; ++q) s = add_rn(s, mul_rn(v[q], x[ci[q]]));
+  Y[i + c * ldy] = s;
+}
+
+}  // namespace
+
+template <typename T>
+void stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t c, const T* X, int64_t ldx, T* Y,
+              int64_t ldy, cudaStream_t s) {
+  const int64_t n = nx * ny * nz;
+  if (n <= 0 || c <= 0) return;
+  dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(c));
+  k_stencil7<T><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy);
+  MPB_LAUNCH_CHECK();
+}
+
+template <typename T>
+void stencil5(int64_t nx, int64_t ny, int64_t c, const T* X, int64_t ldx, T* Y, int64_t ldy,
+              cudaStream_t s) {
+  const int64_t n = nx * ny;
+  if (n <= 0 || c <= 0) return;
+  dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(c));
+  k_stencil5<T><<<grid, 256, 0, s>>>(nx, ny, X, ldx, Y, ldy);
+  MPB_LAUNCH_CHECK();
+}
+
+template <typename T>
+void csr_spmm(int64_t n, const int64_t* row_ptr, const int64_t* col_idx, const T* vals,
+              int64_t c, const T* X, int64_t ldx, T* Y, int64_t ldy, cudaStream_t s) {
+  if (n <= 0 || c <= 0) return;
+  dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(c));
+  k_csr_spmm<T><<<grid, 256, 0, s>>>(n, row_ptr, col_idx, vals, X, ldx, Y, ldy);
+  MPB_LAUNCH_CHECK();
+}
+
+#define MPB_INST(T)                                                                          \
+  template void stencil7<T>(int64_t, int64_t, int64_t, int64_t, const T*, int64_t, T*,       \
+                            int64_t, cudaStream_t);                                          \
+  template void stencil5<T>(int64_t, int64_t, int64_t, const T*, int64_t, T*, int64_t,       \
+                            cudaStream_t);                                                   \
+  template void csr_spmm<T>(int64_t, const int64_t*, const int64_t*, const T*, int64_t,      \
+                            const T*, int64_t, T*, int64_t, cudaStream_t);
+MPB_INST(double)
+MPB_INST(float)
+#undef MPB_INST
+
+}  // namespace mpb

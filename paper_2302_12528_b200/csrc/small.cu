@@ -1,0 +1,350 @@
+// small.cu -- single-CTA kernels for the small (<= 3m x 3m) dense steps.
+//
+// These run once or twice per iteration on matrices of order <= 576 that
+// live in L2; they are latency-, not bandwidth-bound.  Inner products keep
+// the reference's sequential order with separately rounded operations, so
+// for identical inputs they reproduce the reference's small factorizations
+// (dense_cholesky, dense_kernels.hpp:128-152; householder_qr_square,
+// ortho.hpp:30-121) bit for bit.
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "rn.cuh"
+
+namespace mpb {
+namespace {
+
+constexpr int kSmallThreads = 256;
+
+template <typename T>
+__global__ void k_symmetrize(int64_t s, T* G, int64_t ldg) {
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < s * s;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx % s, j = idx / s;
+    if (i < j) {
+      const T v = (G[i + j * ldg] + G[j + i * ldg]) / T(2);
+      G[i + j * ldg] = v;
+      G[j + i * ldg] = v;
+    }
+  }
+}
+
+// Left-looking Cholesky, column j computed after columns < j; rows of a
+// column in parallel.  status = {code, index}.
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads)
+k_cholesky_inv(int m, const T* __restrict__ G, int64_t ldg, T* __restrict__ L,
+               T* __restrict__ Uinv, int* status) {
+  __shared__ int fail;
+  if (threadIdx.x == 0) fail = 0;
+  for (int64_t idx = threadIdx.x; idx < static_cast<int64_t>(m) * m; idx += blockDim.x) L[idx] = T(0);
+  __syncthreads();
+  for (int j = 0; j < m; ++j) {
+    // diagonal first (one thread), then the column below it
+    if (threadIdx.x == 0) {
+      T s = G[j + static_cast<int64_t>(j) * ldg];
+      for (int k = 0; k < j; ++k) {
+        const T ljk = L[j + static_cast<int64_t>(k) * m];
+        s = sub_rn(s, mul_rn(ljk, ljk));
+      }
+      if (!isfinite(static_cast<double>(s))) {
+        fail = 1;
+        if (status[0] == 0) {
+          status[0] = MPEIG_E_OVERFLOW;
+          status[1] = j;
+        }
+      } else if (!(s > T(0))) {
+        fail = 1;
+        if (status[0] == 0) {
+          status[0] = MPEIG_E_NOT_PD;
+          status[1] = j;
+        }
+      } else {
+        L[j + static_cast<int64_t>(j) * m] = sqrt(s);
+      }
+    }
+    __syncthreads();
+    if (fail) return;
+    const T djj = L[j + static_cast<int64_t>(j) * m];
+    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) {
+      T s = G[i + static_cast<int64_t>(j) * ldg];
+      for (int k = 0; k < j; ++k)
+        s = sub_rn(s, mul_rn(L[i + static_cast<int64_t>(k) * m], L[j + static_cast<int64_t>(k) * m]));
+      L[i + static_cast<int64_t>(j) * m] = s / djj;
+    }
+    __syncthreads();
+  }
+  if (!Uinv) return;
+  // Uinv = L^{-T}: column c of L^{-1} by forward substitution (thread per c);
+  // stored transposed so Uinv is upper triangular.
+  for (int c = threadIdx.x; c < m; c += blockDim.x) {
+    for (int k = 0; k < m; ++k) Uinv[c + static_cast<int64_t>(k) * m] = T(0);
+    for (int k = c; k < m; ++k) {
+      T s = (k == c) ? T(1) : T(0);
+      for (int l = c; l < k; ++l)
+        s = sub_rn(s, mul_rn(L[k + static_cast<int64_t>(l) * m], Uinv[c + static_cast<int64_t>(l) * m]));
+      Uinv[c + static_cast<int64_t>(k) * m] = s / L[k + static_cast<int64_t>(k) * m];
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads)
+k_upper_inverse(int m, const T* __restrict__ R, int64_t ldr, T* __restrict__ Rinv, int* status) {
+  __shared__ int fail;
+  if (threadIdx.x == 0) {
+    fail = 0;
+    const T tiny = sizeof(T) == 8 ? T(DBL_MIN) : T(FLT_MIN);
+    for (int j = 0; j < m; ++j) {
+      const T a = fabs(R[j + static_cast<int64_t>(j) * ldr]);
+      if (a == T(0) || a < tiny) {
+        fail = 1;
+        if (status[0] == 0) {
+          status[0] = MPEIG_E_SINGULAR_TRI;
+          status[1] = j;
+        }
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  if (fail) return;
+  for (int c = threadIdx.x; c < m; c += blockDim.x) {
+    for (int k = c + 1; k < m; ++k) Rinv[k + static_cast<int64_t>(c) * m] = T(0);
+    Rinv[c + static_cast<int64_t>(c) * m] = T(1) / R[c + static_cast<int64_t>(c) * ldr];
+    for (int k = c - 1; k >= 0; --k) {
+      T s = T(0);
+      for (int l = k + 1; l <= c; ++l)
+        s = add_rn(s, mul_rn(R[k + static_cast<int64_t>(l) * ldr], Rinv[l + static_cast<int64_t>(c) * m]));
+      Rinv[k + static_cast<int64_t>(c) * m] = -s / R[k + static_cast<int64_t>(k) * ldr];
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_small_transpose(int r, int c, const T* __restrict__ A, int64_t lda,
+                                  T* __restrict__ B, int64_t ldb) {
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+       idx < static_cast<int64_t>(r) * c; idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(idx % r), j = static_cast<int>(idx / r);
+    B[j + i * ldb] = A[i + j * lda];
+  }
+}
+
+template <typename T>
+__global__ void k_small_matmul(int r, int k, int c, const T* __restrict__ A, int64_t lda,
+                               const T* __restrict__ B, int64_t ldb, T* __restrict__ C, int64_t ldc) {
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+       idx < static_cast<int64_t>(r) * c; idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(idx % r), j = static_cast<int>(idx / r);
+    T s = T(0);
+    for (int l = 0; l < k; ++l) s = fma(A[i + l * lda], B[l + j * ldb], s);
+    C[i + j * ldc] = s;
+  }
+}
+
+// Hetmaniuk-Lehoucq coefficients, single CTA.  scratch layout (T):
+//   M  p x m   (C(0:m, m:m+p)^T, reduced in place to R)
+//   V  p x p   (reflector j in column j, rows j..p-1)
+//   Q  p x p
+//   beta p
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads)
+k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __restrict__ coef,
+            T* __restrict__ scratch, int* fallback) {
+  T* M = scratch;
+  T* V = M + static_cast<int64_t>(p) * m;
+  T* Q = V + static_cast<int64_t>(p) * p;
+  T* beta = Q + static_cast<int64_t>(p) * p;
+  __shared__ int fb;
+  __shared__ T sh_beta, sh_diag;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // c_x = C(:, 0:m)
+  for (int64_t idx = tid; idx < static_cast<int64_t>(s) * m; idx += nt) {
+    const int i = static_cast<int>(idx % s), j = static_cast<int>(idx / s);
+    coef[i + static_cast<int64_t>(j) * s] = C[i + static_cast<int64_t>(j) * ldc];
+  }
+  if (p == 0) return;
+  if (tid == 0) fb = 0;
+  // M(a, b) = C(b, m + a)   (a < p rows, b < m cols): top^*
+  for (int64_t idx = tid; idx < static_cast<int64_t>(p) * m; idx += nt) {
+    const int a = static_cast<int>(idx % p), b = static_cast<int>(idx / p);
+    M[a + static_cast<int64_t>(b) * p] = C[b + static_cast<int64_t>(m + a) * ldc];
+  }
+  __syncthreads();
+  // householder_reduce (ortho.hpp:30-76) on the p x m block, steps = p
+  for (int j = 0; j < p; ++j) {
+    const int len = p - j;
+    if (tid == 0) {
+      T nrm2 = T(0);
+      for (int i = j; i < p; ++i) {
+        const T a = fabs(M[i + static_cast<int64_t>(j) * p]);
+        nrm2 = add_rn(nrm2, mul_rn(a, a));
+      }
+      const T nrm = sqrt(nrm2);
+      if (nrm == T(0)) {
+        fb = 1;
+      } else {
+        const T x0 = M[j + static_cast<int64_t>(j) * p];
+        const T ax0 = fabs(x0);
+        const T phase = ax0 > T(0) ? x0 / ax0 : T(1);
+        T* v = V + static_cast<int64_t>(j) * p + j;
+        v[0] = add_rn(x0, mul_rn(phase, nrm));
+        for (int i = 1; i < len; ++i) v[i] = M[j + i + static_cast<int64_t>(j) * p];
+        T vn2 = T(0);
+        for (int i = 0; i < len; ++i) {
+          const T a = fabs(v[i]);
+          vn2 = add_rn(vn2, mul_rn(a, a));
+        }
+        sh_beta = T(2) / vn2;
+        beta[j] = sh_beta;
+        sh_diag = -phase * nrm;  // R(j,j) after the reflection (ortho.hpp:72)
+      }
+    }
+    __syncthreads();
+    if (fb) break;
+    const T b = sh_beta;
+    const T* v = V + static_cast<int64_t>(j) * p + j;
+    for (int c = j + tid; c < m; c += nt) {
+      T* col = M + static_cast<int64_t>(c) * p + j;
+      T sdot = T(0);
+      for (int i = 0; i < len; ++i) sdot = add_rn(sdot, mul_rn(v[i], col[i]));
+      sdot = mul_rn(sdot, b);
+      for (int i = 0; i < len; ++i) col[i] = sub_rn(col[i], mul_rn(sdot, v[i]));
+    }
+    __syncthreads();
+    if (tid == 0) {
+      M[j + static_cast<int64_t>(j) * p] = sh_diag;
+      for (int i = j + 1; i < p; ++i) M[i + static_cast<int64_t>(j) * p] = T(0);
+    }
+    __syncthreads();
+  }
+  if (!fb) {
+    // Q = I, reflectors applied last to first (apply_reflectors_to, ortho.hpp:78-92)
+    for (int64_t idx = tid; idx < static_cast<int64_t>(p) * p; idx += nt) {
+      const int i = static_cast<int>(idx % p), j = static_cast<int>(idx / p);
+      Q[idx] = i == j ? T(1) : T(0);
+    }
+    __syncthreads();
+    for (int jj = p - 1; jj >= 0; --jj) {
+      const int len = p - jj;
+      const T* v = V + static_cast<int64_t>(jj) * p + jj;
+      const T b = beta[jj];
+      for (int c = tid; c < p; c += nt) {
+        T* qc = Q + static_cast<int64_t>(c) * p + (p - len);
+        T sdot = T(0);
+        for (int i = 0; i < len; ++i) sdot = add_rn(sdot, mul_rn(v[i], qc[i]));
+        sdot = mul_rn(sdot, b);
+        for (int i = 0; i < len; ++i) qc[i] = sub_rn(qc[i], mul_rn(sdot, v[i]));
+      }
+      __syncthreads();
+    }
+    // fix_diagonal_phases (ortho.hpp:95-110): steps = min(p, m) = p
+    if (tid == 0) {
+      for (int j = 0; j < p; ++j)
+        if (M[j + static_cast<int64_t>(j) * p] == T(0)) fb = 1;
+    }
+    __syncthreads();
+    if (!fb) {
+      for (int j = 0; j < p; ++j) {
+        const T d = M[j + static_cast<int64_t>(j) * p];
+        if (d < T(0))
+          for (int i = tid; i < p; i += nt) Q[i + static_cast<int64_t>(j) * p] = -Q[i + static_cast<int64_t>(j) * p];
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *fallback = fb;
+  // c_pv = C(:, m:m+p) V  (V = I on fallback)
+  for (int64_t idx = tid; idx < static_cast<int64_t>(s) * p; idx += nt) {
+    const int i = static_cast<int>(idx % s), j = static_cast<int>(idx / s);
+    T acc;
+    if (fb) {
+      acc = C[i + static_cast<int64_t>(m + j) * ldc];
+    } else {
+      // matmul(cp, Q): ascending l, separately rounded (dense_kernels.hpp:20-34)
+      acc = T(0);
+      for (int l = 0; l < p; ++l)
+        acc = add_rn(acc, mul_rn(C[i + static_cast<int64_t>(m + l) * ldc], Q[l + static_cast<int64_t>(j) * p]));
+    }
+    coef[i + static_cast<int64_t>(m + j) * s] = acc;
+  }
+}
+
+}  // namespace
+
+template <typename T>
+void small_symmetrize(int64_t s, T* G, int64_t ldg, cudaStream_t st) {
+  if (s <= 1) return;
+  k_symmetrize<T><<<static_cast<unsigned>(ceil_div(s * s, 256) > 64 ? 64 : ceil_div(s * s, 256)), 256,
+                    0, st>>>(s, G, ldg);
+  MPB_LAUNCH_CHECK();
+}
+
+template <typename T>
+void small_cholesky_inv(int64_t m, const T* G, int64_t ldg, T* L, T* Uinv, int* status,
+                        cudaStream_t st) {
+  if (m <= 0) return;
+  k_cholesky_inv<T><<<1, kSmallThreads, 0, st>>>(static_cast<int>(m), G, ldg, L, Uinv, status);
+  MPB_LAUNCH_CHECK();
+}
+
+template <typename T>
+void small_upper_inverse(int64_t m, const T* R, int64_t ldr, T* Rinv, int* status,
+                         cudaStream_t st) {
+  if (m <= 0) return;
+  k_upper_inverse<T><<<1, kSmallThreads, 0, st>>>(static_cast<int>(m), R, ldr, Rinv, status);
+  MPB_LAUNCH_CHECK();
+}
+
+template <typename T>
+void small_matmul(int64_t r, int64_t k, int64_t c, const T* A, int64_t lda, const T* B,
+                  int64_t ldb, T* C, int64_t ldc, cudaStream_t st) {
+  if (r * c <= 0) return;
+  int64_t g = ceil_div(r * c, 256);
+  if (g > 256) g = 256;
+  k_small_matmul<T><<<static_cast<unsigned>(g), 256, 0, st>>>(
+      static_cast<int>(r), static_cast<int>(k), static_cast<int>(c), A, lda, B, ldb, C, ldc);
+  MPB_LAUNCH_CHECK();
+}
+
+template <typename T>
+void small_transpose(int64_t r, int64_t c, const T* A, int64_t lda, T* B, int64_t ldb,
+                     cudaStream_t st) {
+  if (r * c <= 0) return;
+  int64_t g = ceil_div(r * c, 256);
+  if (g > 256) g = 256;
+  k_small_transpose<T><<<static_cast<unsigned>(g), 256, 0, st>>>(static_cast<int>(r),
+                                                                 static_cast<int>(c), A, lda, B, ldb);
+  MPB_LAUNCH_CHECK();
+}
+
+void hl_coeffs(int64_t s, int64_t m, int64_t p, const double* C, int64_t ldc, double* coef,
+               double* scratch, int* fallback, cudaStream_t st) {
+  k_hl_coeffs<double><<<1, kSmallThreads, 0, st>>>(static_cast<int>(s), static_cast<int>(m),
+                                                   static_cast<int>(p), C, ldc, coef, scratch,
+                                                   fallback);
+  MPB_LAUNCH_CHECK();
+}
+
+void hl_coeffs_f32(int64_t s, int64_t m, int64_t p, const float* C, int64_t ldc, float* coef,
+                   float* scratch, int* fallback, cudaStream_t st) {
+  k_hl_coeffs<float><<<1, kSmallThreads, 0, st>>>(static_cast<int>(s), static_cast<int>(m),
+                                                  static_cast<int>(p), C, ldc, coef, scratch,
+                                                  fallback);
+  MPB_LAUNCH_CHECK();
+}
+
+#define MPB_INST(T)                                                                            \
+  template void small_symmetrize<T>(int64_t, T*, int64_t, cudaStream_t);                       \
+  template void small_cholesky_inv<T>(int64_t, const T*, int64_t, T*, T*, int*, cudaStream_t); \
+  template void small_upper_inverse<T>(int64_t, const T*, int64_t, T*, int*, cudaStream_t);    \
+  template void small_matmul<T>(int64_t, int64_t, int64_t, const T*, int64_t, const T*,        \
+                                int64_t, T*, int64_t, cudaStream_t);                            \
+  template void small_transpose<T>(int64_t, int64_t, const T*, int64_t, T*, int64_t, cudaStream_t);
+MPB_INST(double)
+MPB_INST(float)
+#undef MPB_INST
+
+}  // namespace mpb

@@ -1,0 +1,782 @@
+// solver.cpp -- the LOBPCG / PINVIT iteration on the device (host orchestration).
+//
+// Mirrors the reference solver step for step:
+//   lobpcg_stage<T>  eigensolvers.hpp:195-321
+//   pinvit<T>        eigensolvers.hpp:326-390
+//   run_variant      drivers.hpp:57-111,   solve() drivers.hpp:158-181
+// Every block vector stays on the device; per iteration the host receives
+// only theta, the residual / column norms and a few status words (needed for
+// the prefix convergence rule and the history record), exactly the data the
+// reference's IterationRecord carries.
+//
+// Device layout: S = [X | P | W] and AS = [AX | AP | AW] are
+// single column-major allocations (ld = n rounded up to 32), so the
+// reference's hconcat copies (dense_matrix.hpp:90-107) vanish; the next X, P,
+// AX, AP are written to a second pair of buffers and the pairs swap.
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <utility>
+#include <vector>
+
+#include "context.hpp"
+#include "solver.hpp"
+
+namespace mpb {
+
+std::atomic<int64_t> g_launches{0};
+
+// ------------------------------------------------------------------ status
+void status_clear(mpeig_ctx* ctx) {
+  MPB_CUDA(cudaMemsetAsync(ctx->d_status, 0, 16 * sizeof(int), ctx->stream));
+}
+
+void status_fetch(mpeig_ctx* ctx) {
+  MPB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->d_status, 16 * sizeof(int), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+static void cusolver_check(cusolverStatus_t st, const char* what) {
+  if (st != CUSOLVER_STATUS_SUCCESS)
+    throw Error(MPEIG_E_CUSOLVER, std::string(what) + " failed (cusolver status " +
+                                      std::to_string(static_cast<int>(st)) + ")");
+}
+
+static void cublas_check(cublasStatus_t st, const char* what) {
+  if (st != CUBLAS_STATUS_SUCCESS)
+    throw Error(MPEIG_E_CUDA, std::string(what) + " failed (cublas status " +
+                                  std::to_string(static_cast<int>(st)) + ")");
+}
+
+// --------------------------------------------------------------- operators
+template <typename T>
+void op_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* X, int64_t ldx, T* Y,
+              int64_t ldy) {
+  constexpr bool kW = sizeof(T) == 8;
+  cudaStream_t s = ctx->stream;
+  if (ncols <= 0) return;
+  switch (op->kind) {
+    case kOpLap3d:
+      stencil7<T>(op->nx, op->ny, op->nz, ncols, X, ldx, Y, ldy, s);
+      return;
+    case kOpLap2d:
+      stencil5<T>(op->nx, op->ny, ncols, X, ldx, Y, ldy, s);
+      return;
+    case kOpCsr:
+      if constexpr (kW) {
+        csr_spmm<double>(op->n, op->rp, op->ci, op->vals, ncols, X, ldx, Y, ldy, s);
+      } else {
+        if (op->lower_overflow) throw Error(MPEIG_E_OVERFLOW, "to_lower: matrix exceeds binary32 range");
+        csr_spmm<float>(op->n, op->rp, op->ci, op->vals_l, ncols, X, ldx, Y, ldy, s);
+      }
+      return;
+    case kOpDense: {
+      // herm_product (dense_kernels.hpp:66-72): a plain library GEMM
+      const int n = static_cast<int>(op->n), c = static_cast<int>(ncols);
+      if constexpr (kW) {
+        const double one = 1.0, zero = 0.0;
+        cublas_check(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, n, c, n, &one, op->A,
+                                 static_cast<int>(op->lda), X, static_cast<int>(ldx), &zero, Y,
+                                 static_cast<int>(ldy)),
+                     "cublasDgemm");
+      } else {
+        if (op->lower_overflow) throw Error(MPEIG_E_OVERFLOW, "to_lower: matrix exceeds binary32 range");
+        const float one = 1.f, zero = 0.f;
+        cublas_check(cublasSgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, n, c, n, &one, op->Al,
+                                 static_cast<int>(op->lda), X, static_cast<int>(ldx), &zero, Y,
+                                 static_cast<int>(ldy)),
+                     "cublasSgemm");
+      }
+      return;
+    }
+    case kOpDeviceCb: {
+      mpeig_apply_fn f = kW ? op->dev_w : op->dev_l;
+      if (!f) throw Error(MPEIG_E_CONFIG, "operator callback missing for this precision");
+      const int rc = f(op->user, op->n, ncols, X, ldx, Y, ldy, s);
+      if (rc != 0) throw Error(MPEIG_E_CALLBACK, "operator callback failed", rc);
+      return;
+    }
+    case kOpHostCb: {
+      mpeig_host_apply_fn f = kW ? op->host_w : op->host_l;
+      if (!f) throw Error(MPEIG_E_CONFIG, "host operator callback missing for this precision");
+      std::vector<T> hx(static_cast<size_t>(op->n * ncols)), hy(hx.size());
+      MPB_CUDA(cudaMemcpy2DAsync(hx.data(), sizeof(T) * op->n, X, sizeof(T) * ldx, sizeof(T) * op->n,
+                                 ncols, cudaMemcpyDeviceToHost, s));
+      MPB_CUDA(cudaStreamSynchronize(s));
+      const int rc = f(op->user, op->n, ncols, hx.data(), hy.data());
+      if (rc != 0) throw Error(MPEIG_E_CALLBACK, "host operator callback failed", rc);
+      MPB_CUDA(cudaMemcpy2DAsync(Y, sizeof(T) * ldy, hy.data(), sizeof(T) * op->n, sizeof(T) * op->n,
+                                 ncols, cudaMemcpyHostToDevice, s));
+      MPB_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+    case kOpJacobi:
+      precond_apply<T>(ctx, op, ncols, X, ldx, Y, ldy);
+      return;
+  }
+}
+
+// Jacobi mode for a block of precision T (Preconditioner::apply / apply_lower)
+template <typename T>
+static int jacobi_mode(const mpeig_op* op, const void** dinv) {
+  if constexpr (sizeof(T) == 8) {
+    if (op->precision == MPEIG_WORKING) {
+      *dinv = op->dinv;
+      return kResidJacobiT;
+    }
+    *dinv = op->dinvf;
+    return kResidSandwich;
+  } else {
+    if (op->precision != MPEIG_LOWER)
+      throw Error(MPEIG_E_CONFIG, "precond apply_lower: factor was built at working precision");
+    *dinv = op->dinvf;
+    return kResidJacobiT;
+  }
+}
+
+template <typename T>
+void precond_apply(mpeig_ctx* ctx, const mpeig_op* T_op, int64_t ncols, const T* R, int64_t ldr,
+                   T* W, int64_t ldw) {
+  if (T_op->kind != kOpJacobi) {
+    op_apply<T>(ctx, T_op, ncols, R, ldr, W, ldw);
+    return;
+  }
+  const void* dinv = nullptr;
+  const int mode = jacobi_mode<T>(T_op, &dinv);
+  status_clear(ctx);
+  jacobi_apply<T>(mode, T_op->n, ncols, R, ldr, dinv, W, ldw, ctx->d_status + 2, ctx->stream);
+  status_fetch(ctx);
+  if (ctx->h_status[2]) throw Error(MPEIG_E_OVERFLOW, "to_lower: value exceeds binary32 range");
+}
+
+// ---------------------------------------------------------------- workspace
+template <typename T>
+Work<T>::Work(mpeig_ctx* c, int64_t n_, int64_t m_, int64_t smax_) : ctx(c), n(n_), m(m_), smax(smax_) {
+  s = ctx->stream;
+  ld = padded_ld(n);
+  S.alloc(static_cast<size_t>(ld * smax), s);
+  AS.alloc(static_cast<size_t>(ld * smax), s);
+  S2.alloc(static_cast<size_t>(ld * smax), s);
+  AS2.alloc(static_cast<size_t>(ld * smax), s);
+  V.alloc(static_cast<size_t>(ld * m), s);
+  G.alloc(static_cast<size_t>(smax * smax), s);
+  evals.alloc(static_cast<size_t>(smax), s);
+  coef.alloc(static_cast<size_t>(smax * smax), s);
+  small.alloc(static_cast<size_t>(8 * m * m + 4 * smax * smax), s);
+  smallf.alloc(static_cast<size_t>(2 * m * m), s);
+  int64_t gw = 0;
+  gw = std::max(gw, gram_workspace_elems<T>(n, smax, smax));
+  gw = std::max(gw, gram_workspace_elems<T>(n, 2 * m, m));
+  gw = std::max(gw, gram_workspace_elems<T>(n, m, m));
+  gw = std::max(gw, gram_workspace_elems<T>(n, m, 1));
+  gramw.alloc(static_cast<size_t>(gw), s);
+  tsqr_w.alloc(static_cast<size_t>(tsqr_workspace_elems<T, T>(n, m)), s);
+  if constexpr (sizeof(T) == 8)
+    tsqr_f.alloc(static_cast<size_t>(tsqr_workspace_elems<double, float>(n, m)), s);
+  rw.alloc(static_cast<size_t>(std::max<int64_t>(resid_workspace_elems(n, m), kNumSMs * 2) + 4 * m + 8), s);
+  theta.alloc(static_cast<size_t>(smax), s);
+  // cuSOLVER syevd workspace for the largest projected problem
+  int lw = 0;
+  if constexpr (sizeof(T) == 8)
+    cusolver_check(cusolverDnDsyevd_bufferSize(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR,
+                                               CUBLAS_FILL_MODE_LOWER, static_cast<int>(smax), G.p,
+                                               static_cast<int>(smax), evals.p, &lw),
+                   "syevd_bufferSize");
+  else
+    cusolver_check(cusolverDnSsyevd_bufferSize(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR,
+                                               CUBLAS_FILL_MODE_LOWER, static_cast<int>(smax), G.p,
+                                               static_cast<int>(smax), evals.p, &lw),
+                   "syevd_bufferSize");
+  lwork = lw;
+  eigw.alloc(static_cast<size_t>(lw > 0 ? lw : 1), s);
+}
+
+template <typename T>
+T* Work<T>::L() { return small.p; }
+template <typename T>
+T* Work<T>::Uinv() { return small.p + m * m; }
+template <typename T>
+T* Work<T>::Rw() { return small.p + 2 * m * m; }
+template <typename T>
+T* Work<T>::Rinv() { return small.p + 3 * m * m; }
+template <typename T>
+T* Work<T>::Lt() { return small.p + 4 * m * m; }
+template <typename T>
+T* Work<T>::scratch() { return small.p + 8 * m * m; }
+template <typename T>
+double* Work<T>::rnorm() { return rw.p + (rw.count - 4 * m - 8); }
+template <typename T>
+double* Work<T>::xnorm() { return rnorm() + m; }
+template <typename T>
+double* Work<T>::dscal() { return rnorm() + 2 * m; }
+
+// ----------------------------------------------------------- small eig
+// small_herm_eig (small_eig.hpp:92-218) -> cuSOLVER syevd on the device:
+// ascending values, vectors overwrite G.  info > 0 -> NoConvergence.
+template <typename T>
+void small_eig(Work<T>& w, int64_t sdim, T* G, int64_t ldg, T* vals) {
+  mpeig_ctx* ctx = w.ctx;
+  if constexpr (sizeof(T) == 8)
+    cusolver_check(cusolverDnDsyevd(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                    static_cast<int>(sdim), G, static_cast<int>(ldg), vals, w.eigw.p,
+                                    w.lwork, ctx->d_status + 3),
+                   "cusolverDnDsyevd");
+  else
+    cusolver_check(cusolverDnSsyevd(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                    static_cast<int>(sdim), G, static_cast<int>(ldg), vals, w.eigw.p,
+                                    w.lwork, ctx->d_status + 3),
+                   "cusolverDnSsyevd");
+}
+
+// ------------------------------------------------------------- QR family
+// Q (in place) by "R from a Householder TSQR, then Cholesky-QR of W R^-1":
+//   lower = true  (T = double): Alg. 2 / mixed_qr (ortho.hpp:173-186) --
+//                 fp32 Householder R_l, V = W R_l^-1 in fp64, CholQR(V).
+//   lower = false: Householder QR (ortho.hpp:127-140) equivalent -- the same
+//                 structure with an R of the block's own precision; Q is the
+//                 unique positive-diagonal Q to rounding.
+// Returns the status {code, index}; W is overwritten only on success.
+template <typename T>
+static int qr_core(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, T* Rout, int64_t* idx) {
+  mpeig_ctx* ctx = w.ctx;
+  cudaStream_t s = w.s;
+  const int64_t n = w.n;
+  status_clear(ctx);
+  if constexpr (sizeof(T) == 8) {
+    if (lower) {
+      tsqr_r<double, float>(n, m, W, ldw, w.smallf.p, m, w.tsqr_f.p, ctx->d_status, s);
+      convert_f32_to_f64(m, m, w.smallf.p, m, w.Rw(), m, s);
+    } else {
+      tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, ctx->d_status, s);
+    }
+  } else {
+    (void)lower;
+    tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, ctx->d_status, s);
+  }
+  small_upper_inverse<T>(m, w.Rw(), m, w.Rinv(), ctx->d_status, s);
+  gemm_tn<T>(n, m, m, T(1), W, ldw, w.Rinv(), m, T(0), nullptr, 0, w.V.p, w.ld, s);
+  gram<T>(n, m, w.V.p, w.ld, m, w.V.p, w.ld, w.G.p, m, 1, w.gramw.p, s);
+  small_cholesky_inv<T>(m, w.G.p, m, w.L(), w.Uinv(), ctx->d_status, s);
+  status_fetch(ctx);
+  const int code = ctx->h_status[0];
+  *idx = ctx->h_status[1];
+  if (code != 0) return code;
+  gemm_tn<T>(n, m, m, T(1), w.V.p, w.ld, w.Uinv(), m, T(0), nullptr, 0, W, ldw, s);
+  if (Rout) {
+    // R = R_chol R_w with R_chol = L^T   (ortho.hpp:184)
+    small_transpose<T>(m, m, w.L(), m, w.Lt(), m, s);
+    small_matmul<T>(m, m, m, w.Lt(), m, w.Rw(), m, Rout, m, s);
+  }
+  return 0;
+}
+
+// detail::orthonormal_q (eigensolvers.hpp:55-70)
+template <typename T>
+void orthonormal_q(Work<T>& w, int64_t m, T* W, int64_t ldw, bool use_mixed) {
+  int64_t idx = 0;
+  if constexpr (sizeof(T) == 8) {
+    if (use_mixed) {
+      const int st = qr_core<T>(w, m, W, ldw, true, nullptr, &idx);
+      if (st == 0) return;
+      if (st == MPEIG_E_RANK_DEFICIENT) throw Error(st, "householder_qr: column vanished", idx);
+      if (st == MPEIG_E_SINGULAR_TRI) throw Error(st, "tri_solve: zero or subnormal diagonal", idx);
+      // NotPositiveDefinite / OverflowError -> Householder at working precision
+    }
+  }
+  const int st = qr_core<T>(w, m, W, ldw, false, nullptr, &idx);
+  if (st == 0) return;
+  // a vanished column (or a numerically singular block) is rank deficiency
+  throw Error(MPEIG_E_RANK_DEFICIENT, "householder_qr: column vanished",
+              st == MPEIG_E_RANK_DEFICIENT || st == MPEIG_E_SINGULAR_TRI ? idx : m - 1);
+}
+
+// orthonormalize_dropping (ortho.hpp:205-250): two-pass Gram-Schmidt that
+// drops columns whose projected norm falls below drop_tol * original norm.
+template <typename T>
+int64_t ortho_dropping(Work<T>& w, int64_t m, T* W, int64_t ldw, T drop_tol) {
+  mpeig_ctx* ctx = w.ctx;
+  cudaStream_t s = w.s;
+  const int64_t n = w.n;
+  T* v = w.V.p;  // column 0 of the QR scratch
+  T* g = w.G.p;
+  double* d2 = w.dscal();
+  double h2 = 0;
+  int64_t kept = 0;
+  for (int64_t j = 0; j < m; ++j) {
+    copy_block<T>(n, 1, W + j * ldw, ldw, v, w.ld, s);
+    frob_sq<T>(n, 1, v, w.ld, d2, w.rw.p, s);
+    MPB_CUDA(cudaMemcpyAsync(&h2, d2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    MPB_CUDA(cudaStreamSynchronize(s));
+    const T n0 = static_cast<T>(std::sqrt(h2));
+    if (n0 == T(0)) continue;
+    for (int pass = 0; pass < 2 && kept > 0; ++pass) {
+      gram<T>(n, kept, W, ldw, 1, v, w.ld, g, kept, 0, w.gramw.p, s);
+      gemm_tn<T>(n, kept, 1, T(-1), W, ldw, g, kept, T(1), v, w.ld, v, w.ld, s);
+    }
+    frob_sq<T>(n, 1, v, w.ld, d2, w.rw.p, s);
+    MPB_CUDA(cudaMemcpyAsync(&h2, d2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    MPB_CUDA(cudaStreamSynchronize(s));
+    const T nv = static_cast<T>(std::sqrt(h2));
+    if (nv <= drop_tol * n0) continue;
+    scale_block<T>(n, 1, T(1) / nv, v, w.ld, W + kept * ldw, ldw, s);
+    ++kept;
+  }
+  return kept;
+}
+
+// detail::orthonormal_q_dropping (eigensolvers.hpp:74-85)
+template <typename T>
+int64_t orthonormal_q_dropping(Work<T>& w, int64_t m, T* W, int64_t ldw, bool use_mixed,
+                               int64_t* dropped) {
+  *dropped = 0;
+  try {
+    orthonormal_q<T>(w, m, W, ldw, use_mixed);
+    return m;
+  } catch (const Error& e) {
+    if (e.code != MPEIG_E_RANK_DEFICIENT) throw;
+  }
+  const T tol = std::sqrt(std::numeric_limits<T>::epsilon());
+  const int64_t kept = ortho_dropping<T>(w, m, W, ldw, tol);
+  *dropped = m - kept;
+  return kept;
+}
+
+// block_project_out (ortho.hpp:190-200): W -= B (B^T W), `passes` times
+template <typename T>
+void project_out(Work<T>& w, const T* B, int64_t b, int64_t ldb, T* W, int64_t wc, int64_t ldw,
+                 int passes) {
+  if (b == 0 || wc == 0) return;
+  for (int p = 0; p < passes; ++p) {
+    gram<T>(w.n, b, B, ldb, wc, W, ldw, w.G.p, b, 0, w.gramw.p, w.s);
+    gemm_tn<T>(w.n, b, wc, T(-1), B, ldb, w.G.p, b, T(1), W, ldw, W, ldw, w.s);
+  }
+}
+
+// detail::ritz_rotate (eigensolvers.hpp:89-102): X <- X V, AX <- AX V,
+// theta = eig(X^T AX).  Reads S/AS column block 0, writes S2/AS2, swaps.
+template <typename T>
+void ritz_rotate(Work<T>& w) {
+  const int64_t m = w.m;
+  gram<T>(w.n, m, w.S.p, w.ld, m, w.AS.p, w.ld, w.G.p, m, 1, w.gramw.p, w.s);
+  small_eig<T>(w, m, w.G.p, m, w.evals.p);
+  gemm_tn<T>(w.n, m, m, T(1), w.S.p, w.ld, w.G.p, m, T(0), nullptr, 0, w.S2.p, w.ld, w.s);
+  gemm_tn<T>(w.n, m, m, T(1), w.AS.p, w.ld, w.G.p, m, T(0), nullptr, 0, w.AS2.p, w.ld, w.s);
+  MPB_CUDA(cudaMemcpyAsync(w.theta.p, w.evals.p, sizeof(T) * m, cudaMemcpyDeviceToDevice, w.s));
+  std::swap(w.S, w.S2);
+  std::swap(w.AS, w.AS2);
+}
+
+// ------------------------------------------------------------ iteration
+// Residual + norms (+ fused Jacobi f_T into Wdst when possible), then one
+// D2H of {theta, ||r||, ||x||, status}.  Returns true if f_T was fused.
+template <typename T>
+static bool residual_step(Work<T>& w, const mpeig_op* T_op, const T* X, const T* AX, T* Wdst,
+                          std::vector<double>& theta, std::vector<double>& rn,
+                          std::vector<double>& xn, bool* overflow) {
+  mpeig_ctx* ctx = w.ctx;
+  const int64_t m = w.m;
+  const bool fused = T_op && T_op->kind == kOpJacobi;
+  const void* dinv = nullptr;
+  int mode = kResidPlain;
+  if (fused) mode = jacobi_mode<T>(T_op, &dinv);
+  status_clear(ctx);
+  residual_precond<T>(mode, w.n, m, X, w.ld, AX, w.ld, w.theta.p, dinv,
+                      fused ? Wdst : w.V.p, w.ld, w.rnorm(), w.xnorm(), ctx->d_status + 2,
+                      w.rw.p, w.s);
+  std::vector<T> th(static_cast<size_t>(m));
+  MPB_CUDA(cudaMemcpyAsync(th.data(), w.theta.p, sizeof(T) * m, cudaMemcpyDeviceToHost, w.s));
+  MPB_CUDA(cudaMemcpyAsync(ctx->h_pinned, w.rnorm(), sizeof(double) * 2 * m, cudaMemcpyDeviceToHost,
+                           w.s));
+  status_fetch(ctx);
+  theta.resize(m);
+  rn.resize(m);
+  xn.resize(m);
+  for (int64_t j = 0; j < m; ++j) {
+    theta[j] = static_cast<double>(th[j]);
+    // col_norm is computed in real_t<T> (dense_matrix.hpp:74-82)
+    rn[j] = static_cast<double>(static_cast<T>(ctx->h_pinned[j]));
+    xn[j] = static_cast<double>(static_cast<T>(ctx->h_pinned[m + j]));
+  }
+  *overflow = ctx->h_status[2] != 0;
+  return fused;
+}
+
+// converged_count (eigensolvers.hpp:25-43): prefix rule
+static int64_t converged_prefix(double a_norm_est, const std::vector<double>& theta,
+                                const std::vector<double>& rn, const std::vector<double>& xn,
+                                double tol) {
+  int64_t n_c = 0;
+  for (size_t j = 0; j < theta.size(); ++j) {
+    const double thr = tol * (a_norm_est + std::abs(theta[j])) * xn[j];
+    if (rn[j] <= thr)
+      ++n_c;
+    else
+      break;
+  }
+  return n_c;
+}
+
+struct EvTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  explicit EvTimer(cudaStream_t st) : s(st) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+  }
+  ~EvTimer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  void start() { cudaEventRecord(a, s); }
+  double stop() {  // seconds; synchronises on the end event
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms * 1e-3;
+  }
+};
+
+template <typename T>
+StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* X0, int64_t ldx0,
+                         int64_t m, const mpeig_cfg& cfg, const mpeig_op* T_op, double a_norm_est,
+                         const mpeig_stage_opts& opt, mpeig_history_sink sink, void* sink_user,
+                         T* Xout, int64_t ldxout, mpeig_timings* tim) {
+  if (n <= 0 || m <= 0) throw Error(MPEIG_E_DIMENSION, "lobpcg_stage: empty block");
+  const int64_t smax = 3 * m;
+  Work<T> w(ctx, n, m, smax);
+  cudaStream_t s = w.s;
+  EvTimer timer(s);
+  mpeig_timings local{};
+  mpeig_timings& tm = tim ? *tim : local;
+
+  // X = X0, AX = A X, Ritz rotation (eigensolvers.hpp:207-216)
+  copy_block<T>(n, m, X0, ldx0, w.S.p, w.ld, s);
+  op_apply<T>(ctx, A, m, w.S.p, w.ld, w.AS.p, w.ld);
+  timer.start();
+  ritz_rotate<T>(w);
+  tm.projected_eig += timer.stop();
+  int64_t p = 0;
+
+  double best_metric = std::numeric_limits<double>::infinity();
+  int64_t since_improvement = 0;
+  constexpr int64_t kStagnationWindow = 40;
+
+  std::vector<double> theta, rn, xn;
+  StageResult res;
+  for (int64_t iter = 0;; ++iter) {
+    T* X = w.S.p;
+    T* AX = w.AS.p;
+    T* Wslot = w.S.p + (m + p) * w.ld;
+    bool overflow = false;
+    const bool fused = residual_step<T>(w, T_op, X, AX, Wslot, theta, rn, xn, &overflow);
+    const int64_t n_c = converged_prefix(a_norm_est, theta, rn, xn, opt.tol);
+
+    if (opt.stagnation_exit) {
+      double metric = 0;
+      for (int64_t j = 0; j < cfg.k && j < m; ++j) {
+        const double denom = (a_norm_est + std::abs(theta[j])) * xn[j];
+        const double ratio = denom > 0 ? rn[j] / denom : std::numeric_limits<double>::infinity();
+        if (ratio > metric) metric = ratio;
+      }
+      if (metric < 0.99 * best_metric) {
+        best_metric = metric;
+        since_improvement = 0;
+      } else {
+        ++since_improvement;
+      }
+    }
+    mpeig_iter_record rec{};
+    rec.stage = opt.tag;
+    rec.m = m;
+    rec.ritz_values = theta.data();
+    rec.residual_norms = rn.data();
+    rec.n_converged = n_c;
+
+    const bool done = n_c >= cfg.k;
+    const bool out_of_iters = iter >= cfg.maxit;
+    const bool stalled = opt.stagnation_exit && since_improvement >= kStagnationWindow;
+    if (done || out_of_iters || stalled) {
+      if (sink) sink(sink_user, &rec);
+      if (Xout) copy_block<T>(n, m, X, w.ld, Xout, ldxout, s);
+      MPB_CUDA(cudaStreamSynchronize(s));
+      res.theta = theta;
+      res.resid = rn;
+      res.iterations = iter;
+      res.converged = done;
+      return res;
+    }
+
+    // W = T(R)  (eigensolvers.hpp:266-271)
+    timer.start();
+    if (overflow) throw Error(MPEIG_E_OVERFLOW, "to_lower: value exceeds binary32 range");
+    if (!fused) precond_apply<T>(ctx, T_op, m, w.V.p, w.ld, Wslot, w.ld);
+    tm.precond_apply += timer.stop();
+
+    // project + QR, twice (eigensolvers.hpp:272-291)
+    timer.start();
+    const int64_t b = m + p;
+    int64_t dropped = 0, wc = m;
+    project_out<T>(w, w.S.p, b, w.ld, Wslot, wc, w.ld, 2);
+    wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, opt.use_mixed_qr != 0, &dropped);
+    if (wc > 0) {
+      int64_t more = 0;
+      project_out<T>(w, w.S.p, b, w.ld, Wslot, wc, w.ld, 1);
+      wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, opt.use_mixed_qr != 0, &more);
+      dropped += more;
+    }
+    rec.w_columns_dropped = dropped;
+    tm.orthogonalize += timer.stop();
+    if (wc == 0 && p == 0) {
+      if (sink) sink(sink_user, &rec);
+      throw Error(MPEIG_E_RANK_COLLAPSE, "lobpcg_stage: no usable search directions left");
+    }
+
+    // AW = A W; Rayleigh-Ritz on S = [X P W] (eigensolvers.hpp:297-311)
+    op_apply<T>(ctx, A, wc, Wslot, w.ld, w.AS.p + (m + p) * w.ld, w.ld);
+    timer.start();
+    const int64_t sdim = m + p + wc;
+    status_clear(ctx);
+    gram<T>(n, sdim, w.S.p, w.ld, sdim, w.AS.p, w.ld, w.G.p, sdim, 1, w.gramw.p, s);
+    small_eig<T>(w, sdim, w.G.p, sdim, w.evals.p);
+    const int64_t pn = std::min(m, sdim - m);
+    if constexpr (sizeof(T) == 8)
+      hl_coeffs(sdim, m, pn, w.G.p, sdim, w.coef.p, w.scratch(), ctx->d_status + 4, s);
+    else
+      hl_coeffs_f32(sdim, m, pn, w.G.p, sdim, w.coef.p, w.scratch(), ctx->d_status + 4, s);
+    // X, P = S [c_x c_pv]; AX, AP = AS [c_x c_pv] (eigensolvers.hpp:315-319)
+    gemm_tn<T>(n, sdim, m + pn, T(1), w.S.p, w.ld, w.coef.p, sdim, T(0), nullptr, 0, w.S2.p, w.ld, s);
+    gemm_tn<T>(n, sdim, m + pn, T(1), w.AS.p, w.ld, w.coef.p, sdim, T(0), nullptr, 0, w.AS2.p, w.ld,
+               s);
+    MPB_CUDA(cudaMemcpyAsync(w.theta.p, w.evals.p, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
+    status_fetch(ctx);
+    tm.projected_eig += timer.stop();
+    if (ctx->h_status[3] > 0) throw Error(MPEIG_E_NO_CONVERGENCE, "small_herm_eig: syevd did not converge");
+    if (ctx->h_status[3] < 0) throw Error(MPEIG_E_CUSOLVER, "syevd: invalid argument", -ctx->h_status[3]);
+    rec.basis_rotation_fallback = ctx->h_status[4];
+    if (sink) sink(sink_user, &rec);
+    std::swap(w.S, w.S2);
+    std::swap(w.AS, w.AS2);
+    p = pn;
+  }
+}
+
+// pinvit<double> (eigensolvers.hpp:326-390) with an operator preconditioner
+StageResult pinvit(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const double* X0, int64_t ldx0,
+                   int64_t m, const mpeig_cfg& cfg, const mpeig_op* T_op, double a_norm_est,
+                   mpeig_history_sink sink, void* sink_user, double* Xout, int64_t ldxout,
+                   mpeig_timings* tim) {
+  using T = double;
+  Work<T> w(ctx, n, m, m);
+  cudaStream_t s = w.s;
+  EvTimer timer(s);
+  mpeig_timings local{};
+  mpeig_timings& tm = tim ? *tim : local;
+  // Xt lives in S2 column block 0 between iterations (ritz_rotate swaps S/S2)
+  T* Xt = w.S2.p;
+  copy_block<T>(n, m, X0, ldx0, Xt, w.ld, s);
+  std::vector<double> theta, rn, xn;
+  StageResult res;
+  for (int64_t iter = 0;; ++iter) {
+    timer.start();
+    copy_block<T>(n, m, Xt, w.ld, w.S.p, w.ld, s);
+    try {
+      orthonormal_q<T>(w, m, w.S.p, w.ld, true);
+    } catch (const Error& e) {
+      if (e.code == MPEIG_E_RANK_DEFICIENT)
+        throw Error(MPEIG_E_RANK_COLLAPSE, "pinvit: iterate block lost rank");
+      throw;
+    }
+    tm.orthogonalize += timer.stop();
+    op_apply<T>(ctx, A, m, w.S.p, w.ld, w.AS.p, w.ld);
+    timer.start();
+    ritz_rotate<T>(w);  // X, AX now in S, AS
+    tm.projected_eig += timer.stop();
+    bool overflow = false;
+    T* W = w.AS2.p;  // free after ritz_rotate's swap
+    const bool fused = residual_step<T>(w, T_op, w.S.p, w.AS.p, W, theta, rn, xn, &overflow);
+    const int64_t n_c = converged_prefix(a_norm_est, theta, rn, xn, cfg.tol);
+    mpeig_iter_record rec{};
+    rec.stage = MPEIG_WORKING;
+    rec.m = m;
+    rec.ritz_values = theta.data();
+    rec.residual_norms = rn.data();
+    rec.n_converged = n_c;
+    if (sink) sink(sink_user, &rec);
+    const bool done = n_c >= cfg.k;
+    if (done || iter >= cfg.maxit) {
+      if (Xout) copy_block<T>(n, m, w.S.p, w.ld, Xout, ldxout, s);
+      MPB_CUDA(cudaStreamSynchronize(s));
+      res.theta = theta;
+      res.resid = rn;
+      res.iterations = iter;
+      res.converged = done;
+      return res;
+    }
+    timer.start();
+    if (overflow) throw Error(MPEIG_E_OVERFLOW, "to_lower: value exceeds binary32 range");
+    if (!fused) precond_apply<T>(ctx, T_op, m, w.V.p, w.ld, W, w.ld);
+    tm.precond_apply += timer.stop();
+    Xt = w.S2.p;
+    subtract<T>(n, m, w.S.p, w.ld, W, w.ld, Xt, w.ld, s);  // Xt = X - W (:388)
+  }
+}
+
+// spectral_norm_estimate (norm_estimate.hpp:15-24)
+double spectral_norm_estimate(mpeig_ctx* ctx, const mpeig_op* A, int64_t sketch_rows,
+                              uint64_t seed) {
+  if (sketch_rows < 1) throw Error(MPEIG_E_CONFIG, "spectral_norm_estimate: sketch_rows < 1");
+  const int64_t n = A->n;
+  const int64_t ld = padded_ld(n);
+  std::vector<double> om(static_cast<size_t>(n * sketch_rows));
+  gaussian_fill(n, sketch_rows, seed, om.data());
+  double den2 = 0;  // frobenius_norm, sequential like the reference
+  for (double v : om) den2 += std::abs(v) * std::abs(v);
+  const double denom = std::sqrt(den2);
+  cudaStream_t s = ctx->stream;
+  DevBuf<double> O(static_cast<size_t>(ld * sketch_rows), s), Y(static_cast<size_t>(ld * sketch_rows), s),
+      wk(kNumSMs * 2 + 2, s);
+  MPB_CUDA(cudaMemcpy2DAsync(O.p, sizeof(double) * ld, om.data(), sizeof(double) * n,
+                             sizeof(double) * n, sketch_rows, cudaMemcpyHostToDevice, s));
+  op_apply<double>(ctx, A, sketch_rows, O.p, ld, Y.p, ld);
+  frob_sq<double>(n, sketch_rows, Y.p, ld, wk.p + kNumSMs * 2, wk.p, s);
+  double y2 = 0;
+  MPB_CUDA(cudaMemcpyAsync(&y2, wk.p + kNumSMs * 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+  MPB_CUDA(cudaStreamSynchronize(s));
+  if (denom == 0) return 0;
+  return std::sqrt(y2) / denom;
+}
+
+// run_variant (drivers.hpp:57-111) on a device start block
+void run_variant(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T_op, const mpeig_cfg& cfg,
+                 const double* X0, int64_t ldx0, double a_norm_est, mpeig_history_sink sink,
+                 void* sink_user, mpeig_result* out) {
+  const int64_t n = A->n;
+  const int64_t m = cfg.block != 0 ? cfg.block : (3 * cfg.k + 1) / 2;
+  cudaStream_t s = ctx->stream;
+  out->a_norm_estimate = a_norm_est;
+  out->iterations_lower = 0;
+  out->iterations_working = 0;
+  const int64_t ld = padded_ld(n);
+  DevBuf<double> Xf(static_cast<size_t>(ld * m), s);
+  StageResult st;
+  if (cfg.variant == MPEIG_PINVIT) {
+    st = pinvit(ctx, A, n, X0, ldx0, m, cfg, T_op, a_norm_est, sink, sink_user, Xf.p, ld,
+                &out->timings);
+    out->iterations_working = st.iterations;
+  } else {
+    DevBuf<double> X(static_cast<size_t>(ld * m), s);
+    copy_block<double>(n, m, X0, ldx0, X.p, ld, s);
+    const bool mixed = cfg.variant == MPEIG_MPLOBPCG_SCHOL;
+    if (mixed) {
+      // stage 1: everything in binary32 to lower_tol, stagnation exit
+      mpeig_stage_opts lo{cfg.lower_tol, 0, 1, MPEIG_LOWER};
+      StageResult st1;
+      {
+        DevBuf<float> Xl(static_cast<size_t>(ld * m), s), X1(static_cast<size_t>(ld * m), s);
+        status_clear(ctx);
+        convert_f64_to_f32(n, m, X.p, ld, Xl.p, ld, ctx->d_status + 5, s);
+        status_fetch(ctx);
+        if (ctx->h_status[5]) throw Error(MPEIG_E_OVERFLOW, "to_lower: value exceeds binary32 range");
+        st1 = lobpcg_stage<float>(ctx, A, n, Xl.p, ld, m, cfg, T_op, a_norm_est, lo, sink, sink_user,
+                                  X1.p, ld, &out->timings);
+        out->iterations_lower = st1.iterations;
+        // a stalled or capped first stage still hands over its block
+        convert_f32_to_f64(n, m, X1.p, ld, X.p, ld, s);
+      }
+      Work<double> w(ctx, n, m, m);
+      orthonormal_q<double>(w, m, X.p, ld, true);
+    }
+    mpeig_stage_opts hi{cfg.tol, mixed ? 1 : 0, 0, MPEIG_WORKING};
+    st = lobpcg_stage<double>(ctx, A, n, X.p, ld, m, cfg, T_op, a_norm_est, hi, sink, sink_user,
+                              Xf.p, ld, &out->timings);
+    out->iterations_working = st.iterations;
+  }
+  out->converged = st.converged ? 1 : 0;
+  for (int64_t j = 0; j < cfg.k; ++j) {
+    if (out->theta) out->theta[j] = st.theta[j];
+    if (out->residual_norms) out->residual_norms[j] = st.resid[j];
+  }
+  if (out->X) copy_block<double>(n, cfg.k, Xf.p, ld, out->X, out->ldx, s);
+  MPB_CUDA(cudaStreamSynchronize(s));
+}
+
+// solve (drivers.hpp:158-181): sketch, seeded start block, run_variant
+void solve(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T_op, const mpeig_cfg& cfg,
+           mpeig_history_sink sink, void* sink_user, mpeig_result* out) {
+  const int64_t n = A->n;
+  validate_cfg(cfg, n);
+  const int64_t m = cfg.block != 0 ? cfg.block : (3 * cfg.k + 1) / 2;
+  const auto t0 = std::chrono::steady_clock::now();
+  const double est =
+      spectral_norm_estimate(ctx, A, cfg.sketch_rows, cfg.seed ^ 0x9e3779b97f4a7c15ULL);
+  std::vector<double> g(static_cast<size_t>(n * m));
+  gaussian_fill(n, m, cfg.seed, g.data());
+  const int64_t ld = padded_ld(n);
+  cudaStream_t s = ctx->stream;
+  DevBuf<double> X0(static_cast<size_t>(ld * m), s);
+  MPB_CUDA(cudaMemcpy2DAsync(X0.p, sizeof(double) * ld, g.data(), sizeof(double) * n,
+                             sizeof(double) * n, m, cudaMemcpyHostToDevice, s));
+  {
+    Work<double> w(ctx, n, m, m);
+    orthonormal_q<double>(w, m, X0.p, ld, true);
+  }
+  run_variant(ctx, A, T_op, cfg, X0.p, ld, est, sink, sink_user, out);
+  out->timings.total =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// SolverConfig::validate (solver_types.hpp:43-56)
+void validate_cfg(const mpeig_cfg& cfg, int64_t n) {
+  const int64_t m = cfg.block != 0 ? cfg.block : (3 * cfg.k + 1) / 2;
+  if (cfg.k < 1) throw Error(MPEIG_E_CONFIG, "config: k must be at least 1");
+  if (m < cfg.k) throw Error(MPEIG_E_CONFIG, "config: block size below k");
+  if (3 * m > n)
+    throw Error(MPEIG_E_CONFIG, "config: block size " + std::to_string(m) + " too large for n=" +
+                                    std::to_string(n) + " (need 3*block <= n)");
+  if (!(cfg.tol > 0) || !(cfg.tol < 1)) throw Error(MPEIG_E_CONFIG, "config: tol outside (0,1)");
+  if (!(cfg.lower_tol > 0) || !(cfg.lower_tol < 1))
+    throw Error(MPEIG_E_CONFIG, "config: lower_tol outside (0,1)");
+  if (cfg.maxit < 1) throw Error(MPEIG_E_CONFIG, "config: maxit must be at least 1");
+  if (cfg.sketch_rows < 1) throw Error(MPEIG_E_CONFIG, "config: sketch_rows must be at least 1");
+}
+
+// explicit instantiations
+template void op_apply<double>(mpeig_ctx*, const mpeig_op*, int64_t, const double*, int64_t, double*,
+                               int64_t);
+template void op_apply<float>(mpeig_ctx*, const mpeig_op*, int64_t, const float*, int64_t, float*,
+                              int64_t);
+template void precond_apply<double>(mpeig_ctx*, const mpeig_op*, int64_t, const double*, int64_t,
+                                    double*, int64_t);
+template void precond_apply<float>(mpeig_ctx*, const mpeig_op*, int64_t, const float*, int64_t,
+                                   float*, int64_t);
+template struct Work<double>;
+template struct Work<float>;
+template void orthonormal_q<double>(Work<double>&, int64_t, double*, int64_t, bool);
+template void orthonormal_q<float>(Work<float>&, int64_t, float*, int64_t, bool);
+template int64_t orthonormal_q_dropping<double>(Work<double>&, int64_t, double*, int64_t, bool,
+                                                int64_t*);
+template void project_out<double>(Work<double>&, const double*, int64_t, int64_t, double*, int64_t,
+                                  int64_t, int);
+template void small_eig<double>(Work<double>&, int64_t, double*, int64_t, double*);
+template StageResult lobpcg_stage<double>(mpeig_ctx*, const mpeig_op*, int64_t, const double*,
+                                          int64_t, int64_t, const mpeig_cfg&, const mpeig_op*,
+                                          double, const mpeig_stage_opts&, mpeig_history_sink,
+                                          void*, double*, int64_t, mpeig_timings*);
+template StageResult lobpcg_stage<float>(mpeig_ctx*, const mpeig_op*, int64_t, const float*,
+                                         int64_t, int64_t, const mpeig_cfg&, const mpeig_op*,
+                                         double, const mpeig_stage_opts&, mpeig_history_sink,
+                                         void*, float*, int64_t, mpeig_timings*);
+
+int qr_with_r(Work<double>& w, int64_t m, double* W, int64_t ldw, bool lower, double* Rout,
+              int64_t* idx) {
+  return qr_core<double>(w, m, W, ldw, lower, Rout, idx);
+}
+
+}  // namespace mpb

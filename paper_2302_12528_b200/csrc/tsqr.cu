@@ -1,0 +1,240 @@
+// tsqr.cu -- R factor of a tall-skinny block by a Householder TSQR tree.
+//
+// The reference factors the whole n x m block with a sequential Householder
+// QR (householder_reduce, ortho.hpp:30-76) -- in fp32 for step 1 of mixed_qr
+// (Alg. 2, ortho.hpp:173-186) and for the lower stage, in fp64 for the
+// working-precision modes.  On the GPU the same reflections run on
+// shared-memory row blocks (leaves) and then on stacked leaf R factors (tree
+// levels); only R is formed.  R is unique up to row signs; the final step
+// makes diag(R) positive like fix_diagonal_phases (ortho.hpp:95-110).
+//
+// The fp64 -> fp32 narrowing of mixed_qr's to_lower (precision.hpp:102-107)
+// happens as the leaf loads W, with the overflow check.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mpb {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int64_t kSmemBudget = 100 * 1024;  // 2 CTAs / SM
+
+template <typename Tq>
+int64_t max_rows(int64_t m) {
+  int64_t b = kSmemBudget / (m * static_cast<int64_t>(sizeof(Tq)));
+  b = (b / 32) * 32;
+  if (b > 1024) b = 1024;
+  return b;
+}
+
+template <typename Tq>
+struct TsqrPlan {
+  int64_t leaf_rows;  // rows per leaf
+  int64_t group;      // R factors stacked per tree node
+  int64_t nleaf;
+  bool ok;
+};
+
+template <typename Tq>
+TsqrPlan<Tq> tsqr_plan(int64_t n, int64_t m) {
+  TsqrPlan<Tq> p;
+  const int64_t mr = round_up(m, 32);
+  int64_t b = max_rows<Tq>(m);
+  p.ok = b >= mr;
+  if (!p.ok) {
+    // large m: one 227 KB CTA per leaf as long as m rows fit
+    b = mr;
+    p.ok = b * m * static_cast<int64_t>(sizeof(Tq)) <= 220 * 1024;
+  }
+  p.leaf_rows = b;
+  p.group = std::max<int64_t>(2, b / m);
+  if (p.group * m * static_cast<int64_t>(sizeof(Tq)) * m > 220 * 1024) p.group = 2;
+  p.nleaf = ceil_div(n, b);
+  return p;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// Householder reduction of the b x m tile (column-major, ld b) in shared
+// memory.  On exit the upper triangle holds R.  A column whose remaining
+// norm is zero gets no reflector (R(j,j) = 0; rank is judged on the final R).
+template <typename Tq>
+__device__ void householder_tile(Tq* t, int b, int m) {
+  __shared__ Tq red[kThreads / 32];
+  __shared__ Tq sh_beta, sh_diag;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int steps = min(b, m);
+  for (int j = 0; j < steps; ++j) {
+    Tq* cj = t + static_cast<int64_t>(j) * b;
+    Tq part = Tq(0);
+    for (int i = j + 1 + tid; i < b; i += kThreads) part = fma(cj[i], cj[i], part);
+    part = warp_sum(part);
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    if (tid == 0) {
+      Tq tail2 = Tq(0);
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) tail2 += red[w];
+      const Tq x0 = cj[j];
+      const Tq nrm = sqrt(fma(x0, x0, tail2));
+      if (nrm == Tq(0)) {
+        sh_beta = Tq(0);
+        sh_diag = Tq(0);
+      } else {
+        const Tq phase = x0 >= Tq(0) ? Tq(1) : Tq(-1);
+        const Tq v0 = x0 + phase * nrm;
+        sh_beta = Tq(2) / fma(v0, v0, tail2);
+        sh_diag = -phase * nrm;
+        cj[j] = v0;
+      }
+    }
+    __syncthreads();
+    const Tq beta = sh_beta;
+    if (beta != Tq(0)) {
+      for (int c = j + 1 + warp; c < m; c += kThreads / 32) {
+        Tq* cc = t + static_cast<int64_t>(c) * b;
+        Tq s = Tq(0);
+        for (int i = j + lane; i < b; i += 32) s = fma(cj[i], cc[i], s);
+        s = warp_sum(s);
+        s = __shfl_sync(0xffffffffu, s, 0) * beta;
+        for (int i = j + lane; i < b; i += 32) cc[i] = fma(-s, cj[i], cc[i]);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) cj[j] = sh_diag;
+    __syncthreads();
+  }
+}
+
+template <typename Tin, typename Tq>
+__device__ __forceinline__ Tq narrow(Tin x, int* ovf) {
+  if constexpr (sizeof(Tin) > sizeof(Tq)) {
+    const Tq y = static_cast<Tq>(x);
+    if (isfinite(static_cast<double>(x)) && !isfinite(static_cast<double>(y))) *ovf = 1;
+    return y;
+  } else {
+    return static_cast<Tq>(x);
+  }
+}
+
+template <typename Tin, typename Tq>
+__global__ void __launch_bounds__(kThreads)
+k_tsqr_leaf(int64_t n, int m, const Tin* __restrict__ W, int64_t ldw, int b, Tq* __restrict__ Rout,
+            int* status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Tq* t = reinterpret_cast<Tq*>(smem_raw);
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * b;
+  int ovf = 0;
+  for (int j = 0; j < m; ++j)
+    for (int i = threadIdx.x; i < b; i += kThreads) {
+      const int64_t row = r0 + i;
+      t[i + static_cast<int64_t>(j) * b] = row < n ? narrow<Tin, Tq>(W[row + j * ldw], &ovf) : Tq(0);
+    }
+  if (ovf) atomicCAS(status, 0, MPEIG_E_OVERFLOW);
+  __syncthreads();
+  householder_tile<Tq>(t, b, m);
+  Tq* R = Rout + static_cast<int64_t>(blockIdx.x) * m * m;
+  for (int64_t idx = threadIdx.x; idx < static_cast<int64_t>(m) * m; idx += kThreads) {
+    const int i = static_cast<int>(idx % m), j = static_cast<int>(idx / m);
+    R[idx] = (i <= j && i < b) ? t[i + static_cast<int64_t>(j) * b] : Tq(0);
+  }
+}
+
+template <typename Tq>
+__global__ void __launch_bounds__(kThreads)
+k_tsqr_node(int64_t nR, int m, int group, const Tq* __restrict__ Rin, Tq* __restrict__ Rout) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Tq* t = reinterpret_cast<Tq*>(smem_raw);
+  const int b = group * m;
+  for (int g = 0; g < group; ++g) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * group + g;
+    for (int64_t idx = threadIdx.x; idx < static_cast<int64_t>(m) * m; idx += kThreads) {
+      const int i = static_cast<int>(idx % m), j = static_cast<int>(idx / m);
+      t[g * m + i + static_cast<int64_t>(j) * b] = q < nR ? Rin[q * m * m + idx] : Tq(0);
+    }
+  }
+  __syncthreads();
+  householder_tile<Tq>(t, b, m);
+  Tq* R = Rout + static_cast<int64_t>(blockIdx.x) * m * m;
+  for (int64_t idx = threadIdx.x; idx < static_cast<int64_t>(m) * m; idx += kThreads) {
+    const int i = static_cast<int>(idx % m), j = static_cast<int>(idx / m);
+    R[idx] = i <= j ? t[i + static_cast<int64_t>(j) * b] : Tq(0);
+  }
+}
+
+// positive diagonal (fix_diagonal_phases), rank check, copy to R (ld ldr)
+template <typename Tq>
+__global__ void k_tsqr_finish(int m, const Tq* __restrict__ Rin, Tq* __restrict__ R, int64_t ldr,
+                              int* status) {
+  for (int64_t idx = threadIdx.x; idx < static_cast<int64_t>(m) * m; idx += blockDim.x) {
+    const int i = static_cast<int>(idx % m), j = static_cast<int>(idx / m);
+    const Tq d = Rin[i + static_cast<int64_t>(i) * m];
+    const Tq v = Rin[idx];
+    R[i + static_cast<int64_t>(j) * ldr] = d < Tq(0) ? -v : v;
+  }
+  if (threadIdx.x == 0 && status[0] == 0) {
+    for (int j = 0; j < m; ++j)
+      if (Rin[j + static_cast<int64_t>(j) * m] == Tq(0)) {
+        status[0] = MPEIG_E_RANK_DEFICIENT;
+        status[1] = j;
+        break;
+      }
+  }
+}
+
+}  // namespace
+
+template <typename Tin, typename Tq>
+int64_t tsqr_workspace_elems(int64_t n, int64_t m) {
+  const TsqrPlan<Tq> p = tsqr_plan<Tq>(n, m);
+  return (p.nleaf + ceil_div(p.nleaf, p.group) + 1) * m * m;
+}
+
+template <typename Tin, typename Tq>
+void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr, Tq* work,
+            int* status, cudaStream_t s) {
+  const TsqrPlan<Tq> p = tsqr_plan<Tq>(n, m);
+  if (!p.ok) throw Error(MPEIG_E_CONFIG, "tsqr: block too wide for the shared-memory leaf");
+  const int mi = static_cast<int>(m);
+  const size_t leaf_smem = static_cast<size_t>(p.leaf_rows * m * sizeof(Tq));
+  MPB_CUDA(cudaFuncSetAttribute(k_tsqr_leaf<Tin, Tq>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(std::max<size_t>(leaf_smem, 48 * 1024))));
+  Tq* bufA = work;
+  Tq* bufB = work + p.nleaf * m * m;
+  k_tsqr_leaf<Tin, Tq><<<static_cast<unsigned>(p.nleaf), kThreads, leaf_smem, s>>>(
+      n, mi, W, ldw, static_cast<int>(p.leaf_rows), bufA, status);
+  MPB_LAUNCH_CHECK();
+  int64_t nR = p.nleaf;
+  const size_t node_smem = static_cast<size_t>(p.group * m * m * sizeof(Tq));
+  MPB_CUDA(cudaFuncSetAttribute(k_tsqr_node<Tq>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(std::max<size_t>(node_smem, 48 * 1024))));
+  while (nR > 1) {
+    const int64_t nout = ceil_div(nR, p.group);
+    k_tsqr_node<Tq><<<static_cast<unsigned>(nout), kThreads, node_smem, s>>>(
+        nR, mi, static_cast<int>(p.group), bufA, bufB);
+    MPB_LAUNCH_CHECK();
+    std::swap(bufA, bufB);
+    nR = nout;
+  }
+  k_tsqr_finish<Tq><<<1, 256, 0, s>>>(mi, bufA, R, ldr, status);
+  MPB_LAUNCH_CHECK();
+}
+
+template int64_t tsqr_workspace_elems<double, double>(int64_t, int64_t);
+template int64_t tsqr_workspace_elems<double, float>(int64_t, int64_t);
+template int64_t tsqr_workspace_elems<float, float>(int64_t, int64_t);
+template void tsqr_r<double, double>(int64_t, int64_t, const double*, int64_t, double*, int64_t,
+                                     double*, int*, cudaStream_t);
+template void tsqr_r<double, float>(int64_t, int64_t, const double*, int64_t, float*, int64_t,
+                                    float*, int*, cudaStream_t);
+template void tsqr_r<float, float>(int64_t, int64_t, const float*, int64_t, float*, int64_t,
+                                   float*, int*, cudaStream_t);
+
+}  // namespace mpb

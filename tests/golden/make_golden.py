@@ -1,0 +1,88 @@
+"""Generate the golden fixtures under tests/golden/ from the REFERENCE itself.
+
+Runs the unmodified reference library (oracle/_ref/libmpeig_ref.so, built from
+/root/reference/proj by oracle/Makefile) through its own lobpcg_stage /
+BlockOperator API (oracle/ref_harness.cpp) and stores the results as small
+.npz files.  The GPU box has no /root/reference; the fixtures travel instead.
+
+    python tests/golden/make_golden.py            # fast set (< 1 min)
+    python tests/golden/make_golden.py --case cfg1-dlobpcg-dchol   # one long case
+
+Each fixture holds: theta, resid, iteration counts, converged, a_norm_est,
+the full per-iteration history (stage, n_c, dropped, rotation fallback, Ritz
+values, residual norms) and the reference's own wall time.
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+from oracle import Oracle, Problem  # noqa: E402
+
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from problems import spd_dense  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+CASES = {
+    # name: (problem factory, variant, solve kwargs)
+    "lap3d8-dlobpcg-dchol": (lambda: Problem.lap3d(8), "dlobpcg-dchol", dict(k=4, tol=1e-10, maxit=500)),
+    "lap3d8-dlobpcg-schol": (lambda: Problem.lap3d(8), "dlobpcg-schol", dict(k=4, tol=1e-10, maxit=500)),
+    "lap3d8-mplobpcg-schol": (lambda: Problem.lap3d(8), "mplobpcg-schol", dict(k=4, tol=1e-10, maxit=500)),
+    "lap3d8-pinvit": (lambda: Problem.lap3d(8), "pinvit", dict(k=4, tol=1e-10, maxit=5000)),
+    "lap3d16-dlobpcg-dchol": (lambda: Problem.lap3d(16), "dlobpcg-dchol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
+    "lap3d16-dlobpcg-schol": (lambda: Problem.lap3d(16), "dlobpcg-schol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
+    "lap3d16-mplobpcg-schol": (lambda: Problem.lap3d(16), "mplobpcg-schol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
+    "lap2d50-mplobpcg-schol": (lambda: Problem.lap2d(50), "mplobpcg-schol", dict(k=10, block=15, tol=1e-12, maxit=600, seed=7)),
+    "lap2d50-dlobpcg-dchol": (lambda: Problem.lap2d(50), "dlobpcg-dchol", dict(k=10, block=15, tol=1e-12, maxit=600, seed=7)),
+    "lap2d5x500-mplobpcg-schol": (lambda: Problem.lap2d(5, 500), "mplobpcg-schol", dict(k=5, block=8, tol=1e-10, maxit=8000, seed=1)),
+    "dense256-dlobpcg-dchol": (lambda: Problem.dense_matrix(spd_dense(256, 1e3, 5)[0]), "dlobpcg-dchol", dict(k=8, tol=1e-10, maxit=2000, seed=3)),
+    "dense256-mplobpcg-schol": (lambda: Problem.dense_matrix(spd_dense(256, 1e3, 5)[0]), "mplobpcg-schol", dict(k=8, tol=1e-10, maxit=2000, seed=3)),
+    "lap2d32-pinvit": (lambda: Problem.lap2d(32), "pinvit", dict(k=4, block=6, tol=1e-8, maxit=400)),
+    # cfg 1 (BASELINE.json configs[0]) -- minutes each on one core
+    "cfg1-dlobpcg-dchol": (lambda: Problem.lap3d(32), "dlobpcg-dchol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
+    "cfg1-dlobpcg-schol": (lambda: Problem.lap3d(32), "dlobpcg-schol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
+    "cfg1-mplobpcg-schol": (lambda: Problem.lap3d(32), "mplobpcg-schol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
+}
+FAST = [c for c in CASES if not c.startswith("cfg1")]
+
+
+def run(name: str) -> None:
+    make, variant, kw = CASES[name]
+    prob = make()
+    r = Oracle("ref").solve(prob, variant, **kw)
+    np.savez_compressed(
+        os.path.join(OUT, name + ".npz"),
+        variant=variant, kw=repr(kw), status=r.status, msg=r.msg, converged=r.converged,
+        iters_lower=r.iters_lower, iters_working=r.iters_working, a_norm_est=r.a_norm_est,
+        theta=r.theta, resid=r.resid, hist_stage=r.hist_stage, hist_nc=r.hist_nc,
+        hist_dropped=r.hist_dropped, hist_fallback=r.hist_fallback,
+        hist_ritz=r.hist_ritz, hist_resid=r.hist_resid, t_total=r.t_total)
+    print(f"{name}: status={r.status} conv={r.converged} iters={r.iters_lower}+{r.iters_working} "
+          f"theta0={r.theta[0]!r} t={r.t_total:.2f}s", flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", action="append")
+    a = ap.parse_args()
+    for name in a.case or FAST:
+        run(name)
+    # PCG64 golden outputs (tests/test_precision.cpp:56-71 values are asserted
+    # in tests/test_oracle.py; these are the longer streams)
+    o = Oracle("ref")
+    np.savez_compressed(os.path.join(OUT, "pcg64.npz"),
+                        s0=o.pcg64(0, 64), s42=o.pcg64(42, 64), s2026=o.pcg64(2026, 64),
+                        gauss_0_33x5=o.gaussian(33, 5, 0),
+                        gauss_sketch=o.gaussian(40, 8, 0 ^ 0x9E3779B97F4A7C15))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,284 @@
+"""Kernel-level parity of the sm_100a path against the reference (via the oracle).
+
+Bitwise for the elementwise / operator kernels (the reference's exact
+operation order is reproduced), tolerance-level for reductions.
+All calls go through the C ABI (libmpeig_b200.so).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import Oracle, Problem, available
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -53
+
+
+def ref_or_port():
+    return Oracle("ref") if available("ref") else Oracle("port")
+
+
+def rand(n, m, seed, dtype=np.float64):
+    return np.asfortranarray(np.random.default_rng(seed).standard_normal((n, m)).astype(dtype))
+
+
+@pytest.mark.parametrize("prob,mk", [
+    (Problem.lap3d(8, 7, 6), lambda mp: mp.laplace3d(8, 7, 6)),
+    (Problem.lap3d(5), lambda mp: mp.laplace3d(5)),
+    (Problem.lap2d(9, 8), lambda mp: mp.laplace2d(9, 8)),
+])
+def test_stencil_apply_bitwise(gpu, prob, mk):
+    mp = gpu
+    A = mk(mp)
+    X = rand(prob.n, 5, 1)
+    Y = mp.to_host(A.apply(mp.to_device(X)))
+    Yr = ref_or_port().apply_op(prob, X)
+    assert np.array_equal(Y, Yr), np.abs(Y - Yr).max()
+
+
+def csr_of_lap2d(nx, ny):
+    rp, ci, vv = [0], [], []
+    for j in range(ny):
+        for i in range(nx):
+            p = i + nx * j
+            ent = []
+            if j > 0:
+                ent.append((p - nx, -1.0))
+            if i > 0:
+                ent.append((p - 1, -1.0))
+            ent.append((p, 4.0))
+            if i + 1 < nx:
+                ent.append((p + 1, -1.0))
+            if j + 1 < ny:
+                ent.append((p + nx, -1.0))
+            for c, v in ent:
+                ci.append(c)
+                vv.append(v)
+            rp.append(len(ci))
+    return np.array(rp), np.array(ci), np.array(vv)
+
+
+def test_csr_apply_bitwise(gpu):
+    mp = gpu
+    rp, ci, vv = csr_of_lap2d(11, 7)
+    rng = np.random.default_rng(3)
+    vv = vv * (1 + 0.1 * rng.random(len(vv)))  # non-trivial coefficients
+    A = mp.csr_matrix(rp, ci, vv)
+    X = rand(77, 4, 2)
+    Y = mp.to_host(A.apply(mp.to_device(X)))
+    Yr = ref_or_port().apply_op(Problem.csr(rp, ci, vv), X)
+    assert np.array_equal(Y, Yr)
+
+
+def test_dense_apply(gpu):
+    mp = gpu
+    M = rand(64, 64, 4)
+    M = np.asfortranarray(M + M.T)
+    A = mp.dense_matrix(M)
+    X = rand(64, 3, 5)
+    Y = mp.to_host(A.apply(mp.to_device(X)))
+    assert np.allclose(Y, M @ X, rtol=0, atol=1e-12 * np.abs(M).sum())
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_residual_precond_bitwise(gpu, precision):
+    """W = f_T(AX - X diag(theta)) bitwise; norms to 1e-15."""
+    mp = gpu
+    n, m = 4099, 11
+    A = mp.laplace3d(17, 241, 1)
+    T = mp.jacobi(A, precision)
+    X, AX = rand(n, m, 6), rand(n, m, 7)
+    theta = np.random.default_rng(8).random(m)
+    W = np.zeros((n, m), order="F")
+    rn, xn = np.zeros(m), np.zeros(m)
+    ctx = A.ctx
+    Xd, AXd = mp.to_device(X), mp.to_device(AX)
+    Wd = mp.to_device(W)
+    ctx.check(ctx.lib.mpeig_residual_precond_f64(
+        ctx.h, T.h, n, m, C.c_void_p(Xd.data_ptr()), n, C.c_void_p(AXd.data_ptr()), n,
+        theta.ctypes.data, C.c_void_p(Wd.data_ptr()), n, rn.ctypes.data, xn.ctypes.data))
+    W = mp.to_host(Wd)
+    R = AX - X * theta[None, :]          # numpy: separate mul / sub, like the reference
+    dinv = np.full(n, 1.0 / 6.0)
+    if precision == 0:
+        Wr = R * dinv[:, None]
+    else:
+        Wr = (R.astype(np.float32) * dinv.astype(np.float32)[:, None]).astype(np.float64)
+    assert np.array_equal(W, Wr)
+    assert np.allclose(rn, np.linalg.norm(R, axis=0), rtol=1e-14, atol=0)
+    assert np.allclose(xn, np.linalg.norm(X, axis=0), rtol=1e-14, atol=0)
+
+
+def test_residual_overflow_is_loud(gpu):
+    mp = gpu
+    n, m = 64, 2
+    A = mp.laplace3d(4)
+    T = mp.jacobi(A, 1)
+    X = np.zeros((n, m), order="F")
+    AX = np.zeros((n, m), order="F")
+    AX[3, 1] = 1e300
+    W = np.zeros((n, m), order="F")
+    rn, xn = np.zeros(m), np.zeros(m)
+    ctx = A.ctx
+    Xd, AXd, Wd = mp.to_device(X), mp.to_device(AX), mp.to_device(W)
+    rc = ctx.lib.mpeig_residual_precond_f64(
+        ctx.h, T.h, n, m, C.c_void_p(Xd.data_ptr()), n, C.c_void_p(AXd.data_ptr()), n,
+        np.zeros(m).ctypes.data, C.c_void_p(Wd.data_ptr()), n, rn.ctypes.data, xn.ctypes.data)
+    assert rc == 8  # OverflowError
+
+
+@pytest.mark.parametrize("n,ka,kb", [(100003, 48, 37), (1000, 144, 144), (31, 5, 7)])
+def test_gram(gpu, n, ka, kb):
+    mp = gpu
+    A, B = rand(n, ka, 9), rand(n, kb, 10)
+    ctx = mp.default_context()
+    Ad, Bd = mp.to_device(A), mp.to_device(B)
+    G = np.zeros((ka, kb), order="F")
+    import torch
+    Gd = torch.zeros((kb, ka), dtype=torch.float64, device="cuda")
+    ctx.check(ctx.lib.mpeig_gram_f64(ctx.h, n, ka, C.c_void_p(Ad.data_ptr()), n, kb,
+                                     C.c_void_p(Bd.data_ptr()), n, C.c_void_p(Gd.data_ptr())))
+    G = mp.to_host(Gd)
+    Gr = A.T @ B
+    scale = np.sqrt(np.outer((A * A).sum(0), (B * B).sum(0)))
+    assert np.all(np.abs(G - Gr) <= 1e-14 * np.sqrt(n) * scale + 1e-300)
+
+
+def test_gemm(gpu):
+    mp = gpu
+    import torch
+    n, k, c = 50001, 96, 70
+    A, Cm, Z = rand(n, k, 11), rand(k, c, 12), rand(n, c, 13)
+    ctx = mp.default_context()
+    Ad, Cd, Zd = mp.to_device(A), mp.to_device(Cm), mp.to_device(Z)
+    ctx.check(ctx.lib.mpeig_gemm_f64(ctx.h, n, k, c, -1.0, C.c_void_p(Ad.data_ptr()), n,
+                                     C.c_void_p(Cd.data_ptr()), k, 1.0, C.c_void_p(Zd.data_ptr()),
+                                     n, C.c_void_p(Zd.data_ptr()), n))
+    Y = mp.to_host(Zd)
+    Yr = Z - A @ Cm
+    assert np.abs(Y - Yr).max() <= 1e-13 * np.abs(A).max() * np.abs(Cm).max() * k
+
+
+def graded(n, m, kappa, seed):
+    rng = np.random.default_rng(seed)
+    Q1, _ = np.linalg.qr(rng.standard_normal((n, m)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    s = kappa ** (-np.arange(m) / (m - 1))
+    return np.asfortranarray((Q1 * s) @ Q2)
+
+
+@pytest.mark.parametrize("kappa", [1e1, 1e3, 1e5, 1e7])
+def test_mixed_qr_orthogonality(gpu, kappa):
+    """acceptance criterion 6 (tests/acceptance.cpp:367-387): <= 100*200*u_h."""
+    mp = gpu
+    import torch
+    n, m = 20000, 24
+    A = graded(n, m, kappa, 17)
+    Wd = mp.to_device(A)
+    Rd = torch.zeros((m, m), dtype=torch.float64, device="cuda")
+    ctx = mp.default_context()
+    ctx.check(ctx.lib.mpeig_mixed_qr_f64(ctx.h, n, m, C.c_void_p(Wd.data_ptr()), n,
+                                         C.c_void_p(Rd.data_ptr())))
+    Q, R = mp.to_host(Wd), mp.to_host(Rd)
+    orth = np.linalg.norm(Q.T @ Q - np.eye(m))
+    assert orth <= 100 * 200 * U
+    assert np.all(np.diag(R) > 0)
+    assert np.linalg.norm(Q @ R - A) <= 1e-12 * np.linalg.norm(A) * (1 + kappa * 1e-4)
+    # same unique Q as the reference's Householder (to rounding x kappa)
+    st, Qr, Rr = ref_or_port().mixed_qr(A)
+    assert st == 0
+    assert np.abs(Q - Qr).max() <= 1e-14 * kappa * 100
+
+
+def test_householder_qr_matches_reference(gpu):
+    mp = gpu
+    import torch
+    n, m = 3001, 16
+    A = rand(n, m, 21)
+    Wd = mp.to_device(A)
+    Rd = torch.zeros((m, m), dtype=torch.float64, device="cuda")
+    ctx = mp.default_context()
+    ctx.check(ctx.lib.mpeig_householder_qr_f64(ctx.h, n, m, C.c_void_p(Wd.data_ptr()), n,
+                                               C.c_void_p(Rd.data_ptr())))
+    Q, R = mp.to_host(Wd), mp.to_host(Rd)
+    st, Qr, Rr = ref_or_port().householder_qr(A)
+    assert np.abs(Q - Qr).max() < 1e-13
+    assert np.abs(R - Rr).max() < 1e-12 * np.abs(Rr).max()
+
+
+def test_rank_deficient_drops(gpu):
+    """orthonormal_q_dropping falls back to MGS with column dropping."""
+    mp = gpu
+    n = 500
+    A = rand(n, 6, 22)
+    A[:, 4] = A[:, 1] * 2.0  # exactly dependent
+    A[:, 5] = 0.0            # vanished column
+    Wd = mp.to_device(A)
+    ctx = mp.default_context()
+    kept = C.c_int64()
+    ctx.check(ctx.lib.mpeig_orthonormal_q_dropping_f64(ctx.h, n, 6, C.c_void_p(Wd.data_ptr()), n,
+                                                       1, C.byref(kept)))
+    Qr = ref_or_port().ortho_dropping(A, np.sqrt(np.finfo(float).eps))
+    assert kept.value == Qr.shape[1] == 4
+    Q = mp.to_host(Wd)[:, :kept.value]
+    assert np.linalg.norm(Q.T @ Q - np.eye(4)) < 1e-13
+    assert np.abs(np.abs(Q) - np.abs(Qr)).max() < 1e-10
+
+
+def test_project_out(gpu):
+    mp = gpu
+    n, b, w = 7000, 20, 8
+    B, _ = np.linalg.qr(rand(n, b, 23))
+    B = np.asfortranarray(B)
+    W = rand(n, w, 24)
+    Bd, Wd = mp.to_device(B), mp.to_device(W)
+    ctx = mp.default_context()
+    ctx.check(ctx.lib.mpeig_project_out_f64(ctx.h, n, b, C.c_void_p(Bd.data_ptr()), n, w,
+                                            C.c_void_p(Wd.data_ptr()), n, 2))
+    Y = mp.to_host(Wd)
+    Yr = ref_or_port().project_out(B, W, 2)
+    assert np.abs(Y - Yr).max() <= 1e-13
+    assert np.abs(B.T @ Y).max() <= 1e-13
+
+
+def test_small_eig(gpu):
+    mp = gpu
+    import torch
+    s = 48
+    M = rand(s, s, 25)
+    M = np.asfortranarray(M + M.T)
+    Md = mp.to_device(M)
+    vals = torch.zeros(s, dtype=torch.float64, device="cuda")
+    vecs = torch.zeros((s, s), dtype=torch.float64, device="cuda")
+    ctx = mp.default_context()
+    ctx.check(ctx.lib.mpeig_small_eig_f64(ctx.h, s, C.c_void_p(Md.data_ptr()),
+                                          C.c_void_p(vals.data_ptr()), C.c_void_p(vecs.data_ptr())))
+    st, vr, Vr = ref_or_port().small_herm_eig(M)
+    v = vals.cpu().numpy()
+    assert np.abs(v - vr).max() <= 1e-13 * np.abs(vr).max()
+    V = mp.to_host(vecs)
+    assert np.linalg.norm(M @ V - V * v) <= 1e-12 * np.abs(vr).max()
+
+
+def test_hl_coeffs_match_reference(gpu):
+    """hl_update (eigensolvers.hpp:148-174) rotation from identical C."""
+    mp = gpu
+    import torch
+    n, s, m = 30, 12, 4
+    S, _ = np.linalg.qr(rand(n, s, 44))
+    H = rand(s, s, 45)
+    G = H.T @ H
+    st, vals, Cm = ref_or_port().small_herm_eig(G)
+    st, Xr, Pr, cpv_r, fb_r = ref_or_port().hl_update(S, Cm, m)
+    Cd = mp.to_device(Cm)
+    coef = torch.zeros((2 * m, s), dtype=torch.float64, device="cuda")
+    p, fb = C.c_int64(), C.c_int32()
+    ctx = mp.default_context()
+    ctx.check(ctx.lib.mpeig_hl_coeffs_f64(ctx.h, s, m, C.c_void_p(Cd.data_ptr()),
+                                          C.c_void_p(coef.data_ptr()), C.byref(p), C.byref(fb)))
+    cf = mp.to_host(coef)
+    assert p.value == m and fb.value == fb_r == 0
+    assert np.array_equal(cf[:, :m], Cm[:, :m])
+    assert np.abs(cf[:, m:] - cpv_r).max() <= 1e-15
