@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""bench.py -- LOBPCG time-to-solution of the B200 (sm_100a) path vs the reference.
+
+Workload (N=1): BASELINE.json configs[0] / BASELINE.md §2 ("cfg1"): 3-D 7-point
+Laplacian 32^3 (n = 32,768), k = 10, m = 16, tol 1e-10, Jacobi f_T, seed 0,
+mixed precision (MPLOBPCG-schol: fp32 stage to 5e-6, then fp64 with mixed_qr).
+This is the only configuration whose time-to-solution the reference can be
+measured on (configs[1] at tol 1e-10 needs >1e4 unpreconditioned iterations;
+see DESIGN.md §Measurement).  A "step" is one complete solve.
+
+    python bench.py                        # N=1, 5 timed solves after 3 warm-ups
+    python bench.py --impl reference       # the reference CPU solver (oracle/_ref)
+    torchrun --nproc-per-node N bench.py --gpus N   # N independent replicas
+
+Prints ONE JSON line (rank 0).  `value` = mean device time of one solve with
+all inputs resident in HBM (seconds, lower is better); `e2e` = the same solve
+through the C ABI with the start block / sketch copied from pinned host memory
+and the eigenvectors copied back inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "cfg1": dict(dims=(32, 32, 32), k=10, block=16, tol=1e-10, maxit=2000, seed=0,
+                 desc="3-D 7-pt Laplacian 32^3 (n=32768), k=10, m=16, tol 1e-10, Jacobi f_T"),
+}
+METRIC = "LOBPCG time-to-solution (k eigpairs, tol 1e-10)"
+REF_SAMPLE_ITERS = 10  # per stage, per reference sample
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+def golden_iters(workload, variant):
+    p = os.path.join(ROOT, "tests", "golden", f"{workload}-{variant}.npz")
+    if not os.path.exists(p):
+        return None
+    g = np.load(p)
+    return {"lower": int(g["iters_lower"]), "working": int(g["iters_working"]),
+            "theta": g["theta"], "t_total": float(g["t_total"])}
+
+
+# --------------------------------------------------------------- reference arm
+def reference_sample(workload, variant):
+    """One bounded sample of the reference solve (oracle/_ref, unmodified reference
+    library through its own lobpcg_stage API), extrapolated to time-to-solution with
+    the reference's own full-run iteration counts (tests/golden)."""
+    from oracle import Oracle, Problem, available
+    w = WORKLOADS[workload]
+    which = "ref" if available("ref") else "port"
+    orc = Oracle(which)
+    r = orc.solve(Problem.lap3d(*w["dims"]), variant, k=w["k"], block=w["block"], tol=w["tol"],
+                  maxit=REF_SAMPLE_ITERS, seed=w["seed"])
+    gi = golden_iters(workload, variant)
+    t1 = r.extra.get("t_stage1", 0.0)
+    t_hi = r.t_total - r.t_setup - t1
+    n_lo, n_hi = r.iters_lower, r.iters_working
+    full_lo, full_hi = (gi["lower"], gi["working"]) if gi else (n_lo, n_hi)
+    est = r.t_setup + (t1 / max(n_lo, 1)) * full_lo + (t_hi / max(n_hi, 1)) * full_hi
+    sample = (f"{'reference' if which == 'ref' else 'C port'} solver capped at {n_lo}+{n_hi} "
+              f"iterations ({r.t_total:.2f} s), extrapolated per stage to its own full-run "
+              f"iteration count {full_lo}+{full_hi} (tests/golden/{workload}-{variant}.npz)")
+    return est, sample, ("reference" if which == "ref" else "port")
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    vals = []
+    sample = kind = None
+    for i in range(args.warmup + args.steps):
+        v, sample, kind = reference_sample(args.workload, args.variant)
+        if i >= args.warmup:
+            vals.append(v)
+    value = float(np.mean(vals))
+    w = WORKLOADS[args.workload]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(args.variant),
+        "data": "synthetic (deterministic Laplacian, seeded PCG64 start block)",
+        "config": {"workload": f"{args.workload}: {w['desc']}", "variant": args.variant},
+        "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def dtype_of(variant):
+    return {"mplobpcg-schol": "f64+f32", "dlobpcg-schol": "f64 (f32 f_T)",
+            "dlobpcg-dchol": "f64", "pinvit": "f64 (f32 f_T)"}[variant]
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import paper_2302_12528_b200 as mp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    w = WORKLOADS[args.workload]
+    ctx = mp.Context(local)
+    A = mp.laplace3d(*w["dims"], ctx=ctx)
+    cfg = mp.SolverConfig(k=w["k"], block=w["block"], tol=w["tol"], maxit=w["maxit"], seed=w["seed"],
+                          variant=args.variant)
+    T = mp.jacobi(A, mp.build_precision_for(args.variant))
+    n, m, k, sr = A.n, cfg.block_size(), cfg.k, cfg.sketch_rows
+    dev = f"cuda:{local}"
+
+    # inputs: gaussian_matrix(n, m, seed) and the sketch Omega, drawn once on the host
+    X0h = mp.gaussian_matrix(n, m, cfg.seed)
+    Omh = mp.gaussian_matrix(n, sr, cfg.seed ^ 0x9E3779B97F4A7C15)
+    om_fro = float(np.sqrt(np.sum(np.abs(Omh.ravel(order="F")) ** 2)))
+    X0pin = torch.from_numpy(np.ascontiguousarray(X0h.T)).pin_memory()
+    Ompin = torch.from_numpy(np.ascontiguousarray(Omh.T)).pin_memory()
+    X0d, Omd = X0pin.to(dev), Ompin.to(dev)
+    Xout = torch.empty((k, n), dtype=torch.float64, device=dev)
+    Xhost = torch.empty((k, n), dtype=torch.float64).pin_memory()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 2x L2
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def solve_resident():
+        return mp.solve_prepared(A, cfg, X0d, Omd, om_fro, T=T, X_out=Xout)
+
+    def solve_e2e():
+        xd = X0pin.to(dev, non_blocking=True)
+        od = Ompin.to(dev, non_blocking=True)
+        r = mp.solve_prepared(A, cfg, xd, od, om_fro, T=T, X_out=Xout)
+        Xhost.copy_(Xout, non_blocking=True)
+        stream.synchronize()
+        return r
+
+    for _ in range(args.warmup):
+        r = solve_resident()
+    # ---- timed region (inputs resident)
+    times, iters = [], []
+    launches0 = ctx.launches()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = solve_resident()
+            e1.record(stream)
+            barrier()
+            times.append(e0.elapsed_time(e1) / 1e3)
+            iters.append((r.iterations_lower, r.iterations_working))
+    launches = ctx.launches() - launches0
+    t_step = float(np.mean(times))
+    # ---- e2e through the C ABI with host buffers
+    e2e_times = []
+    for _ in range(max(2, args.steps // 2)):
+        flush.fill_(1.0)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        r_e2e = solve_e2e()
+        e1.record(stream)
+        barrier()
+        e2e_times.append(max(e0.elapsed_time(e1) / 1e3, time.perf_counter() - t0))
+    t_e2e = float(np.mean(e2e_times))
+    if dist:
+        t = torch.tensor([t_step, t_e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step, t_e2e = t.tolist()
+    # ---- roofline: one instrumented solve (CUDA events around every launch)
+    with mp.profile():
+        solve_resident()
+        torch.cuda.synchronize()
+        prof = mp.profile.report()
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    peak, peak_kind = load_peaks()
+    tot_ms = sum(v["ms"] for v in prof.values()) or 1.0
+    kernels = {}
+    for name, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"]):
+        c = max(v["count"], 1)
+        kernels[name] = {"launches": v["count"], "share": round(v["ms"] / tot_ms, 4),
+                         "us_per_launch": round(1e3 * v["ms"] / c, 3),
+                         "GBps": round(v["bytes"] / (v["ms"] * 1e6), 1) if v["ms"] > 0 and v["bytes"] > 0 else None}
+    top = next((nme for nme in kernels if prof[nme]["bytes"] > 0), None)
+    roof = None
+    if top:
+        v = prof[top]
+        c = max(v["count"], 1)
+        achieved = (v["bytes"] / c) / ((v["ms"] / c) * 1e6)
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get(args.workload, {}).get(top)
+        roof = {"kernel": top, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": traffic, "algorithmic_bytes_per_launch": v["bytes"] / c,
+                "launches": v["count"], "share_of_solve": kernels[top]["share"]}
+    gi = golden_iters(args.workload, args.variant)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, sample, kind = reference_sample(args.workload, args.variant)
+        cpu = {"value": v, "unit": "s", "cores": 1, "kind": kind, "sample": sample}
+    theta_err = None
+    if gi is not None:
+        theta_err = float(np.max(np.abs(r.theta - gi["theta"]) / np.abs(gi["theta"])))
+    line = {
+        "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(args.variant),
+        "data": "synthetic (deterministic Laplacian, seeded PCG64 start block)",
+        "config": {"workload": f"{args.workload}: {w['desc']}", "variant": args.variant,
+                   "l2": "flushed (256 MB write) before every solve",
+                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "iterations": {"lower": iters[-1][0], "working": iters[-1][1]},
+                   "reference_iterations": {"lower": gi["lower"], "working": gi["working"]} if gi else None,
+                   "theta_max_rel_err_vs_reference": theta_err,
+                   "iters_per_s": (iters[-1][0] + iters[-1][1]) / t_step},
+        "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": 8 * n * (m + sr),
+                "d2h_bytes_per_step": 8 * n * k + 16 * k},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "kernels": kernels,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg1", choices=sorted(WORKLOADS))
+    ap.add_argument("--variant", default="mplobpcg-schol",
+                    choices=["mplobpcg-schol", "dlobpcg-schol", "dlobpcg-dchol", "pinvit"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

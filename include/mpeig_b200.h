@@ -222,6 +222,16 @@ int mpeig_pinvit_f64(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const double*
 int mpeig_solve(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T, const mpeig_cfg* cfg,
                 mpeig_history_sink sink, void* sink_user, mpeig_result* out);
 
+/* solve() from device-resident raw inputs: X0raw = gaussian_matrix(n, m, seed)
+ * (NOT yet orthonormal, device n x m) and Omega = gaussian_matrix(n,
+ * sketch_rows, seed ^ 0x9e3779b97f4a7c15) (device); omega_fro = ||Omega||_F
+ * (<= 0: computed on the device).  Equivalent to mpeig_solve minus the host
+ * RNG and uploads; this is the timed region of the benchmark. */
+int mpeig_solve_prepared(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T,
+                         const mpeig_cfg* cfg, const double* X0raw, int64_t ldx0,
+                         const double* omega, int64_t ldo, double omega_fro,
+                         mpeig_history_sink sink, void* sink_user, mpeig_result* out);
+
 /* run_variant on an explicit start block X0 (device fp64, n x m) with a
  * precomputed norm estimate (drivers.hpp:57-111; mixed_lobpcg :122-152) */
 int mpeig_run_variant(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T,
@@ -273,6 +283,16 @@ int mpeig_residual_precond_f64(mpeig_ctx* ctx, const mpeig_op* T, int64_t n, int
                                const double* X, int64_t ldx, const double* AX,
                                int64_t ldax, const double* theta_host, double* W,
                                int64_t ldw, double* rnorm_host, double* xnorm_host);
+
+/* ------------------------------------------------------ instrumentation
+ * Per-kernel-class CUDA-event timing (off by default): every launch of a
+ * class is bracketed by events on its stream and its algorithmic bytes and
+ * flops are recorded.  Used by bench.py for the roofline figures. */
+void mpeig_profile_enable(int on);
+void mpeig_profile_reset(void);
+int mpeig_profile_names(char* buf, int64_t cap);
+int mpeig_profile_query(const char* name, int64_t* count, double* ms, double* bytes,
+                        double* flops);
 
 #ifdef __cplusplus
 }

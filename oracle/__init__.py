@@ -59,7 +59,8 @@ class MpResult(C.Structure):
                 ("hist_dropped", C.POINTER(C.c_int64)),
                 ("hist_fallback", C.POINTER(C.c_int32)),
                 ("hist_ritz", C.POINTER(C.c_double)), ("hist_resid", C.POINTER(C.c_double)),
-                ("t_total", C.c_double), ("t_setup", C.c_double), ("msg", C.c_char * 256)]
+                ("t_total", C.c_double), ("t_setup", C.c_double), ("t_stage1", C.c_double),
+                ("msg", C.c_char * 256)]
 
 
 def _ptr(a, ctype):
@@ -181,7 +182,7 @@ class Oracle:
         return SolveResult(r.status, r.msg.decode(errors="replace"), bool(r.converged),
                            r.iters_lower, r.iters_working, r.a_norm_est, theta, resid, X,
                            hs[:L], hn[:L], hd[:L], hf[:L], hr[:L], hq[:L], r.t_total,
-                           r.t_setup)
+                           r.t_setup, {"t_stage1": r.t_stage1})
 
     # ---------------------------------------------------------- unit kernels
     def pcg64(self, seed, count):

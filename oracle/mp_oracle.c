@@ -366,6 +366,7 @@ int mporc_solve(const mp_problem* prob, int variant, const mp_cfg* c, mp_result*
     gaussian_fill(n, m, c->seed, X);
     orthonormal_q_d(n, m, X, 1);
     out->t_setup = now_s() - t0;
+    out->t_stage1 = 0;
     out->a_norm_est = est;
     out->iters_lower = 0;
     out->iters_working = 0;
@@ -423,6 +424,7 @@ int mporc_solve(const mp_problem* prob, int variant, const mp_cfg* c, mp_result*
       const int mixed = variant == MP_MPLOBPCG_SCHOL;
       if (mixed) {
         /* stage 1 in binary32 (drivers.hpp:79-96) */
+        const double t1 = now_s();
         float* Xl = (float*)xmalloc((size_t)(n * m) * sizeof(float));
         for (int64_t i = 0; i < n * m; ++i) Xl[i] = to_lower_checked(X[i]);
         prec_t_f PL;
@@ -438,6 +440,7 @@ int mporc_solve(const mp_problem* prob, int variant, const mp_cfg* c, mp_result*
         free(s1.theta);
         free(s1.resid);
         orthonormal_q_d(n, m, X, 1);
+        out->t_stage1 = now_s() - t1;
       }
       stage_out_d s2 = lobpcg_stage_d(&sys.A, n, X, m, c->k, c->maxit, &PW, est, c->tol, mixed, 0,
                                       0, &hs);

@@ -66,6 +66,7 @@ typedef struct {
   double* hist_resid;          /* hist_cap*m                               */
   double t_total;              /* seconds inside the solve                 */
   double t_setup;              /* norm sketch + initial QR                 */
+  double t_stage1;             /* fp32 stage + hand-off QR (mixed only)    */
   char msg[256];
 } mp_result;
 

@@ -276,6 +276,7 @@ int mpref_solve(const mp_problem* prob, int variant, const mp_cfg* c, mp_result*
     const DenseMatrix<double> X0 =
         detail::orthonormal_q(gaussian_matrix<double>(n, m, cfg.seed), true);
     out->t_setup = secs(t0);
+    out->t_stage1 = 0;
     EigResult<double> r;
     r.a_norm_estimate = est;
     if (variant == MP_PINVIT) {
@@ -289,11 +290,13 @@ int mpref_solve(const mp_problem* prob, int variant, const mp_cfg* c, mp_result*
         lo.use_mixed_qr = false;
         lo.stagnation_exit = true;
         lo.tag = Precision::Lower;
+        const auto t1 = clk::now();
         StageOutcome<float> st1 = lobpcg_stage<float>(sys->op_lower(), n, to_lower(X), cfg,
                                                       jacobi_lower(*sys), est, lo,
                                                       r.history, r.timings);
         r.iterations_lower = st1.iterations;
         X = detail::orthonormal_q(to_working(st1.X), true);
+        out->t_stage1 = secs(t1);
       }
       StageOptions hi;
       hi.tol = cfg.tol;

@@ -11,7 +11,8 @@ from .api import (  # noqa: F401
     OverflowError_, RankCollapse, RankDeficient, SingularTriangular, SolverConfig,
     StageOptions, StageOutcome, StageTimings, build_precision_for, converged_count, csr_matrix,
     default_context, dense_matrix, gaussian_matrix, host_operator, jacobi, laplace2d, laplace3d,
-    lobpcg_stage, mixed_lobpcg, pinvit, run_variant, solve, spectral_norm_estimate, to_device,
+    lobpcg_stage, mixed_lobpcg, pinvit, profile, run_variant, solve, solve_prepared,
+    spectral_norm_estimate, to_device,
     to_host,
 )
 from ._lib import LIB_PATH, SYMBOLS, load  # noqa: F401

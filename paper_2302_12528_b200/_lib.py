@@ -75,7 +75,8 @@ SYMBOLS = [
     "mpeig_orthonormal_q_f32", "mpeig_mixed_qr_f64", "mpeig_householder_qr_f64",
     "mpeig_orthonormal_q_dropping_f64", "mpeig_gram_f64", "mpeig_gemm_f64",
     "mpeig_project_out_f64", "mpeig_small_eig_f64", "mpeig_hl_coeffs_f64",
-    "mpeig_residual_precond_f64",
+    "mpeig_residual_precond_f64", "mpeig_solve_prepared", "mpeig_profile_enable",
+    "mpeig_profile_reset", "mpeig_profile_names", "mpeig_profile_query",
 ]
 
 _lib = None
@@ -134,6 +135,13 @@ def load() -> C.CDLL:
         "mpeig_hl_coeffs_f64": (C.c_int, [vp, i64, i64, vp, vp, C.POINTER(i64), C.POINTER(i32)]),
         "mpeig_residual_precond_f64": (C.c_int, [vp, vp, i64, i64, vp, i64, vp, i64, vp, vp, i64,
                                                  vp, vp]),
+        "mpeig_solve_prepared": (C.c_int, [vp, vp, vp, C.POINTER(Cfg), vp, i64, vp, i64, dbl, SINK,
+                                           vp, C.POINTER(Result)]),
+        "mpeig_profile_enable": (None, [C.c_int]),
+        "mpeig_profile_reset": (None, []),
+        "mpeig_profile_names": (C.c_int, [C.c_char_p, i64]),
+        "mpeig_profile_query": (C.c_int, [C.c_char_p, C.POINTER(i64), C.POINTER(dbl),
+                                          C.POINTER(dbl), C.POINTER(dbl)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

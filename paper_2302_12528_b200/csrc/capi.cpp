@@ -393,6 +393,17 @@ int mpeig_solve(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T, const mpei
   });
 }
 
+int mpeig_solve_prepared(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T,
+                         const mpeig_cfg* cfg, const double* X0raw, int64_t ldx0,
+                         const double* omega, int64_t ldo, double omega_fro,
+                         mpeig_history_sink sink, void* sink_user, mpeig_result* out) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    out->timings = mpeig_timings{};
+    solve_prepared(ctx, A, T, *cfg, X0raw, ldx0, omega, ldo, omega_fro, sink, sink_user, out);
+  });
+}
+
 int mpeig_run_variant(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T, const mpeig_cfg* cfg,
                       const double* X0, int64_t ldx0, double a_norm_est, mpeig_history_sink sink,
                       void* sink_user, mpeig_result* out) {

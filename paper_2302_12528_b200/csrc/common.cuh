@@ -38,6 +38,23 @@ extern std::atomic<int64_t> g_launches;
     MPB_CUDA(cudaGetLastError());               \
   } while (0)
 
+// Per-kernel-class device timing (bench.py roofline): when enabled, every
+// launcher brackets its kernel(s) with CUDA events on the launching stream and
+// records the algorithmic bytes / flops of that launch.
+void prof_begin(const char* name, cudaStream_t s, double bytes, double flops);
+void prof_end(const char* name, cudaStream_t s);
+extern bool g_prof_on;
+struct ProfScope {
+  const char* name;
+  cudaStream_t s;
+  ProfScope(const char* n, cudaStream_t st, double bytes, double flops) : name(n), s(st) {
+    if (g_prof_on) prof_begin(n, st, bytes, flops);
+  }
+  ~ProfScope() {
+    if (g_prof_on) prof_end(name, s);
+  }
+};
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 

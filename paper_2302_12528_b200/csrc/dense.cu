@@ -266,6 +266,8 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
       MPB_CUDA(cudaMemsetAsync(G + j * ldg, 0, sizeof(T) * ka, s));
     return;
   }
+  ProfScope prof("gram", s, double(sizeof(T)) * n * (A == B ? ka : ka + kb),
+                 2.0 * n * ka * kb);
   const GramPlan p = gram_plan(n, ka, kb);
   dim3 grid(static_cast<unsigned>(p.tiles_m * p.tiles_n), static_cast<unsigned>(p.nchunk));
   k_gram_partial<T><<<grid, 256, 0, s>>>(n, static_cast<int>(ka), static_cast<int>(kb), A, lda, B,
@@ -289,6 +291,8 @@ void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, 
     }
     return;
   }
+  ProfScope prof("gemm", s, double(sizeof(T)) * n * (k + (beta != T(0) ? 2 : 1) * c),
+                 2.0 * n * k * c);
   dim3 grid(static_cast<unsigned>(ceil_div(n, kTile)), static_cast<unsigned>(ceil_div(c, kTile)));
   k_gemm_tn<T><<<grid, 256, 0, s>>>(n, static_cast<int>(k), static_cast<int>(c), alpha, A, lda, C,
                                     ldc, beta, Z, ldz, Y, ldy);

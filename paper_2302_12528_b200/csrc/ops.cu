@@ -89,6 +89,7 @@ void stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t c, const T* X, int64_t
               int64_t ldy, cudaStream_t s) {
   const int64_t n = nx * ny * nz;
   if (n <= 0 || c <= 0) return;
+  ProfScope prof("stencil", s, 2.0 * sizeof(T) * n * c, 13.0 * n * c);
   dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(c));
   k_stencil7<T><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy);
   MPB_LAUNCH_CHECK();
@@ -99,6 +100,7 @@ void stencil5(int64_t nx, int64_t ny, int64_t c, const T* X, int64_t ldx, T* Y, 
               cudaStream_t s) {
   const int64_t n = nx * ny;
   if (n <= 0 || c <= 0) return;
+  ProfScope prof("stencil", s, 2.0 * sizeof(T) * n * c, 9.0 * n * c);
   dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(c));
   k_stencil5<T><<<grid, 256, 0, s>>>(nx, ny, X, ldx, Y, ldy);
   MPB_LAUNCH_CHECK();
@@ -108,6 +110,7 @@ template <typename T>
 void csr_spmm(int64_t n, const int64_t* row_ptr, const int64_t* col_idx, const T* vals,
               int64_t c, const T* X, int64_t ldx, T* Y, int64_t ldy, cudaStream_t s) {
   if (n <= 0 || c <= 0) return;
+  ProfScope prof("spmm", s, 0.0, 0.0);
   dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(c));
   k_csr_spmm<T><<<grid, 256, 0, s>>>(n, row_ptr, col_idx, vals, X, ldx, Y, ldy);
   MPB_LAUNCH_CHECK();

@@ -164,6 +164,7 @@ void residual_precond(int mode, int64_t n, int64_t m, const T* X, int64_t ldx, c
                       double* rnorm, double* xnorm, int* overflow_flag, double* work,
                       cudaStream_t s) {
   if (m <= 0) return;
+  ProfScope prof("residual_ft", s, double(sizeof(T)) * n * m * (W ? 3 : 2), 6.0 * n * m);
   const ResidPlan p = resid_plan(n, m);
   dim3 grid(static_cast<unsigned>(p.nchunk), static_cast<unsigned>(ceil_div(m, kColGroup)));
   const int mi = static_cast<int>(m);

@@ -286,6 +286,7 @@ template <typename T>
 void small_cholesky_inv(int64_t m, const T* G, int64_t ldg, T* L, T* Uinv, int* status,
                         cudaStream_t st) {
   if (m <= 0) return;
+  ProfScope prof("small_chol", st, 0, 0);
   k_cholesky_inv<T><<<1, kSmallThreads, 0, st>>>(static_cast<int>(m), G, ldg, L, Uinv, status);
   MPB_LAUNCH_CHECK();
 }
@@ -294,6 +295,7 @@ template <typename T>
 void small_upper_inverse(int64_t m, const T* R, int64_t ldr, T* Rinv, int* status,
                          cudaStream_t st) {
   if (m <= 0) return;
+  ProfScope prof("small_trinv", st, 0, 0);
   k_upper_inverse<T><<<1, kSmallThreads, 0, st>>>(static_cast<int>(m), R, ldr, Rinv, status);
   MPB_LAUNCH_CHECK();
 }
@@ -322,6 +324,7 @@ void small_transpose(int64_t r, int64_t c, const T* A, int64_t lda, T* B, int64_
 
 void hl_coeffs(int64_t s, int64_t m, int64_t p, const double* C, int64_t ldc, double* coef,
                double* scratch, int* fallback, cudaStream_t st) {
+  ProfScope prof("hl_coeffs", st, 0, 0);
   k_hl_coeffs<double><<<1, kSmallThreads, 0, st>>>(static_cast<int>(s), static_cast<int>(m),
                                                    static_cast<int>(p), C, ldc, coef, scratch,
                                                    fallback);
@@ -330,6 +333,7 @@ void hl_coeffs(int64_t s, int64_t m, int64_t p, const double* C, int64_t ldc, do
 
 void hl_coeffs_f32(int64_t s, int64_t m, int64_t p, const float* C, int64_t ldc, float* coef,
                    float* scratch, int* fallback, cudaStream_t st) {
+  ProfScope prof("hl_coeffs", st, 0, 0);
   k_hl_coeffs<float><<<1, kSmallThreads, 0, st>>>(static_cast<int>(s), static_cast<int>(m),
                                                   static_cast<int>(p), C, ldc, coef, scratch,
                                                   fallback);

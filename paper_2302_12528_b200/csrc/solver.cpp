@@ -222,6 +222,7 @@ double* Work<T>::dscal() { return rnorm() + 2 * m; }
 template <typename T>
 void small_eig(Work<T>& w, int64_t sdim, T* G, int64_t ldg, T* vals) {
   mpeig_ctx* ctx = w.ctx;
+  ProfScope prof("small_eig", w.s, 0, 0);
   if constexpr (sizeof(T) == 8)
     cusolver_check(cusolverDnDsyevd(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
                                     static_cast<int>(sdim), G, static_cast<int>(ldg), vals, w.eigw.p,
@@ -723,6 +724,44 @@ void solve(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T_op, const mpeig_
   DevBuf<double> X0(static_cast<size_t>(ld * m), s);
   MPB_CUDA(cudaMemcpy2DAsync(X0.p, sizeof(double) * ld, g.data(), sizeof(double) * n,
                              sizeof(double) * n, m, cudaMemcpyHostToDevice, s));
+  {
+    Work<double> w(ctx, n, m, m);
+    orthonormal_q<double>(w, m, X0.p, ld, true);
+  }
+  run_variant(ctx, A, T_op, cfg, X0.p, ld, est, sink, sink_user, out);
+  out->timings.total =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// solve() from device-resident raw inputs: the Gaussian start block X0raw
+// (n x m, not yet orthonormal) and the sketch Omega (n x sketch_rows), as
+// drawn by gaussian_matrix on the host.  omega_fro = ||Omega||_F (computed on
+// the device when <= 0).  This is the timed region of bench.py:
+// sketch apply, initial orthonormalisation and both stages.
+void solve_prepared(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T_op, const mpeig_cfg& cfg,
+                    const double* X0raw, int64_t ldx0, const double* omega, int64_t ldo,
+                    double omega_fro, mpeig_history_sink sink, void* sink_user, mpeig_result* out) {
+  const int64_t n = A->n;
+  validate_cfg(cfg, n);
+  const int64_t m = cfg.block != 0 ? cfg.block : (3 * cfg.k + 1) / 2;
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaStream_t s = ctx->stream;
+  const int64_t ld = padded_ld(n);
+  const int64_t sr = cfg.sketch_rows;
+  double est = 0;
+  {
+    DevBuf<double> Y(static_cast<size_t>(ld * sr), s), wk(kNumSMs * 2 + 4, s);
+    op_apply<double>(ctx, A, sr, omega, ldo, Y.p, ld);
+    frob_sq<double>(n, sr, Y.p, ld, wk.p + kNumSMs * 2, wk.p, s);
+    if (omega_fro <= 0) frob_sq<double>(n, sr, omega, ldo, wk.p + kNumSMs * 2 + 1, wk.p, s);
+    double h[2] = {0, 0};
+    MPB_CUDA(cudaMemcpyAsync(h, wk.p + kNumSMs * 2, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
+    MPB_CUDA(cudaStreamSynchronize(s));
+    const double den = omega_fro > 0 ? omega_fro : std::sqrt(h[1]);
+    est = den == 0 ? 0 : std::sqrt(h[0]) / den;
+  }
+  DevBuf<double> X0(static_cast<size_t>(ld * m), s);
+  copy_block<double>(n, m, X0raw, ldx0, X0.p, ld, s);
   {
     Work<double> w(ctx, n, m, m);
     orthonormal_q<double>(w, m, X0.p, ld, true);

@@ -79,6 +79,9 @@ void run_variant(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T_op, const 
                  void* sink_user, mpeig_result* out);
 void solve(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T_op, const mpeig_cfg& cfg,
            mpeig_history_sink sink, void* sink_user, mpeig_result* out);
+void solve_prepared(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T_op, const mpeig_cfg& cfg,
+                    const double* X0raw, int64_t ldx0, const double* omega, int64_t ldo,
+                    double omega_fro, mpeig_history_sink sink, void* sink_user, mpeig_result* out);
 void validate_cfg(const mpeig_cfg& cfg, int64_t n);
 
 }  // namespace mpb

@@ -202,6 +202,7 @@ void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr,
             int* status, cudaStream_t s) {
   const TsqrPlan<Tq> p = tsqr_plan<Tq>(n, m);
   if (!p.ok) throw Error(MPEIG_E_CONFIG, "tsqr: block too wide for the shared-memory leaf");
+  ProfScope prof("tsqr", s, double(sizeof(Tin)) * n * m, 2.0 * n * m * m);
   const int mi = static_cast<int>(m);
   const size_t leaf_smem = static_cast<size_t>(p.leaf_rows * m * sizeof(Tq));
   MPB_CUDA(cudaFuncSetAttribute(k_tsqr_leaf<Tin, Tq>, cudaFuncAttributeMaxDynamicSharedMemorySize,
