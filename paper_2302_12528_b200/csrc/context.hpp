@@ -24,6 +24,7 @@ struct mpeig_ctx {
   int* h_status = nullptr;      // pinned mirror
   double* h_pinned = nullptr;   // pinned staging for per-iteration records
   int64_t h_pinned_elems = 0;
+  int eig_backend = 0;          // 0 auto (one-CTA syev for s <= kSyevMax), 1 cuSOLVER
 };
 
 enum OpKind { kOpLap3d, kOpLap2d, kOpCsr, kOpDense, kOpDeviceCb, kOpHostCb, kOpJacobi };

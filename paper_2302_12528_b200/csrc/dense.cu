@@ -28,7 +28,8 @@ GramPlan gram_plan(int64_t n, int64_t ka, int64_t kb) {
   p.tiles_n = ceil_div(kb, kTile);
   const int64_t ntiles = p.tiles_m * p.tiles_n;
   int64_t nchunk = ceil_div(kTargetCTAs, ntiles);
-  const int64_t max_chunks = ceil_div(n, 256);
+  // >= 512 rows per chunk: the chunk partials are summed sequentially per entry
+  const int64_t max_chunks = ceil_div(n, 512);
   if (nchunk > max_chunks) nchunk = max_chunks;
   if (nchunk < 1) nchunk = 1;
   p.rows_per_chunk = round_up(ceil_div(n, nchunk), kGramBK);

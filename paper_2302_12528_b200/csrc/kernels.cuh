@@ -117,6 +117,14 @@ void hl_coeffs(int64_t s, int64_t m, int64_t p, const double* C, int64_t ldc, do
 void hl_coeffs_f32(int64_t s, int64_t m, int64_t p, const float* C, int64_t ldc, float* coef,
                    float* scratch, int* fallback, cudaStream_t st);
 
+// Symmetric eigendecomposition of a small s x s matrix in one CTA (syev.cu):
+// ascending values, vectors overwrite G.  info = 1 on QL non-convergence.
+constexpr int64_t kSyevMax = 96;
+template <typename T>
+bool small_syev_supported(int64_t s);
+template <typename T>
+void small_syev(int64_t s, T* G, int64_t ldg, T* vals, int* info, cudaStream_t st);
+
 // ------------------------------------------------------------------ TSQR
 // R factor (m x m, upper, positive diagonal) of a tall n x m block by a
 // Householder TSQR tree in precision Tq; the input is read in Tin and

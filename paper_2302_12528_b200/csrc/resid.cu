@@ -26,7 +26,7 @@ struct ResidPlan {
 ResidPlan resid_plan(int64_t n, int64_t m) {
   const int64_t groups = ceil_div(m, kColGroup);
   int64_t nchunk = ceil_div(static_cast<int64_t>(kNumSMs) * 8, groups);
-  const int64_t maxc = ceil_div(n, kThreads);
+  const int64_t maxc = ceil_div(n, 4 * kThreads);  // >= 1024 rows per chunk
   if (nchunk > maxc) nchunk = maxc;
   if (nchunk < 1) nchunk = 1;
   ResidPlan p;

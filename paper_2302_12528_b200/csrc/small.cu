@@ -1,11 +1,12 @@
 // small.cu -- single-CTA kernels for the small (<= 3m x 3m) dense steps.
 //
-// These run once or twice per iteration on matrices of order <= 576 that
-// live in L2; they are latency-, not bandwidth-bound.  Inner products keep
-// the reference's sequential order with separately rounded operations, so
-// for identical inputs they reproduce the reference's small factorizations
+// These run once or twice per iteration on matrices of order <= 576.  They
+// are latency-bound, so each stages its matrices in shared memory (global
+// scratch only when they do not fit) and keeps the reference's sequential
+// inner-product order with separately rounded operations: for identical
+// inputs they reproduce the reference's small factorizations
 // (dense_cholesky, dense_kernels.hpp:128-152; householder_qr_square,
-// ortho.hpp:30-121) bit for bit.
+// ortho.hpp:30-121; matmul :20-34) bit for bit.
 #include <cfloat>
 
 #include "common.cuh"
@@ -16,6 +17,7 @@ namespace mpb {
 namespace {
 
 constexpr int kSmallThreads = 256;
+constexpr size_t kSmemCap = 200 * 1024;
 
 template <typename T>
 __global__ void k_symmetrize(int64_t s, T* G, int64_t ldg) {
@@ -30,22 +32,25 @@ __global__ void k_symmetrize(int64_t s, T* G, int64_t ldg) {
   }
 }
 
-// Left-looking Cholesky, column j computed after columns < j; rows of a
-// column in parallel.  status = {code, index}.
+// Left-looking Cholesky G = L L^T: column j after columns < j, rows of a
+// column in parallel; then Uinv = L^{-T} by forward substitution (thread per
+// column of L^{-1}).  status = {code, index}, first error wins.
 template <typename T>
 __global__ void __launch_bounds__(kSmallThreads)
 k_cholesky_inv(int m, const T* __restrict__ G, int64_t ldg, T* __restrict__ L,
-               T* __restrict__ Uinv, int* status) {
+               T* __restrict__ Uinv, int* status, int use_smem) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  T* Ls = use_smem ? reinterpret_cast<T*>(raw) : L;
+  T* Us = use_smem ? Ls + m * m : Uinv;
   __shared__ int fail;
   if (threadIdx.x == 0) fail = 0;
-  for (int64_t idx = threadIdx.x; idx < static_cast<int64_t>(m) * m; idx += blockDim.x) L[idx] = T(0);
+  for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) Ls[idx] = T(0);
   __syncthreads();
   for (int j = 0; j < m; ++j) {
-    // diagonal first (one thread), then the column below it
     if (threadIdx.x == 0) {
       T s = G[j + static_cast<int64_t>(j) * ldg];
       for (int k = 0; k < j; ++k) {
-        const T ljk = L[j + static_cast<int64_t>(k) * m];
+        const T ljk = Ls[j + k * m];
         s = sub_rn(s, mul_rn(ljk, ljk));
       }
       if (!isfinite(static_cast<double>(s))) {
@@ -61,38 +66,49 @@ k_cholesky_inv(int m, const T* __restrict__ G, int64_t ldg, T* __restrict__ L,
           status[1] = j;
         }
       } else {
-        L[j + static_cast<int64_t>(j) * m] = sqrt(s);
+        Ls[j + j * m] = sqrt(s);
       }
     }
     __syncthreads();
     if (fail) return;
-    const T djj = L[j + static_cast<int64_t>(j) * m];
+    const T djj = Ls[j + j * m];
     for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) {
       T s = G[i + static_cast<int64_t>(j) * ldg];
-      for (int k = 0; k < j; ++k)
-        s = sub_rn(s, mul_rn(L[i + static_cast<int64_t>(k) * m], L[j + static_cast<int64_t>(k) * m]));
-      L[i + static_cast<int64_t>(j) * m] = s / djj;
+      for (int k = 0; k < j; ++k) s = sub_rn(s, mul_rn(Ls[i + k * m], Ls[j + k * m]));
+      Ls[i + j * m] = s / djj;
     }
     __syncthreads();
   }
-  if (!Uinv) return;
-  // Uinv = L^{-T}: column c of L^{-1} by forward substitution (thread per c);
-  // stored transposed so Uinv is upper triangular.
-  for (int c = threadIdx.x; c < m; c += blockDim.x) {
-    for (int k = 0; k < m; ++k) Uinv[c + static_cast<int64_t>(k) * m] = T(0);
-    for (int k = c; k < m; ++k) {
-      T s = (k == c) ? T(1) : T(0);
-      for (int l = c; l < k; ++l)
-        s = sub_rn(s, mul_rn(L[k + static_cast<int64_t>(l) * m], Uinv[c + static_cast<int64_t>(l) * m]));
-      Uinv[c + static_cast<int64_t>(k) * m] = s / L[k + static_cast<int64_t>(k) * m];
+  if (Uinv) {
+    for (int c = threadIdx.x; c < m; c += blockDim.x) {
+      for (int k = 0; k < m; ++k) Us[c + k * m] = T(0);
+      for (int k = c; k < m; ++k) {
+        T s = (k == c) ? T(1) : T(0);
+        for (int l = c; l < k; ++l) s = sub_rn(s, mul_rn(Ls[k + l * m], Us[c + l * m]));
+        Us[c + k * m] = s / Ls[k + k * m];
+      }
+    }
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
+      L[idx] = Ls[idx];
+      if (Uinv) Uinv[idx] = Us[idx];
     }
   }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kSmallThreads)
-k_upper_inverse(int m, const T* __restrict__ R, int64_t ldr, T* __restrict__ Rinv, int* status) {
+k_upper_inverse(int m, const T* __restrict__ R, int64_t ldr, T* __restrict__ Rinv, int* status,
+                int use_smem) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  T* Rs = reinterpret_cast<T*>(raw);
+  T* Is = use_smem ? Rs + m * m : Rinv;
   __shared__ int fail;
+  if (use_smem)
+    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x)
+      Rs[idx] = R[(idx % m) + static_cast<int64_t>(idx / m) * ldr];
   if (threadIdx.x == 0) {
     fail = 0;
     const T tiny = sizeof(T) == 8 ? T(DBL_MIN) : T(FLT_MIN);
@@ -110,15 +126,20 @@ k_upper_inverse(int m, const T* __restrict__ R, int64_t ldr, T* __restrict__ Rin
   }
   __syncthreads();
   if (fail) return;
+  const T* Rr = use_smem ? Rs : R;
+  const int64_t ld = use_smem ? m : ldr;
   for (int c = threadIdx.x; c < m; c += blockDim.x) {
-    for (int k = c + 1; k < m; ++k) Rinv[k + static_cast<int64_t>(c) * m] = T(0);
-    Rinv[c + static_cast<int64_t>(c) * m] = T(1) / R[c + static_cast<int64_t>(c) * ldr];
+    for (int k = c + 1; k < m; ++k) Is[k + c * m] = T(0);
+    Is[c + c * m] = T(1) / Rr[c + c * ld];
     for (int k = c - 1; k >= 0; --k) {
       T s = T(0);
-      for (int l = k + 1; l <= c; ++l)
-        s = add_rn(s, mul_rn(R[k + static_cast<int64_t>(l) * ldr], Rinv[l + static_cast<int64_t>(c) * m]));
-      Rinv[k + static_cast<int64_t>(c) * m] = -s / R[k + static_cast<int64_t>(k) * ldr];
+      for (int l = k + 1; l <= c; ++l) s = add_rn(s, mul_rn(Rr[k + l * ld], Is[l + c * m]));
+      Is[k + c * m] = -s / Rr[k + k * ld];
     }
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) Rinv[idx] = Is[idx];
   }
 }
 
@@ -144,7 +165,8 @@ __global__ void k_small_matmul(int r, int k, int c, const T* __restrict__ A, int
   }
 }
 
-// Hetmaniuk-Lehoucq coefficients, single CTA.  scratch layout (T):
+// Hetmaniuk-Lehoucq coefficients, single CTA.  Work layout (T), in shared
+// memory when it fits, else in `scratch`:
 //   M  p x m   (C(0:m, m:m+p)^T, reduced in place to R)
 //   V  p x p   (reflector j in column j, rows j..p-1)
 //   Q  p x p
@@ -152,11 +174,12 @@ __global__ void k_small_matmul(int r, int k, int c, const T* __restrict__ A, int
 template <typename T>
 __global__ void __launch_bounds__(kSmallThreads)
 k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __restrict__ coef,
-            T* __restrict__ scratch, int* fallback) {
-  T* M = scratch;
-  T* V = M + static_cast<int64_t>(p) * m;
-  T* Q = V + static_cast<int64_t>(p) * p;
-  T* beta = Q + static_cast<int64_t>(p) * p;
+            T* __restrict__ scratch, int* fallback, int use_smem) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  T* M = use_smem ? reinterpret_cast<T*>(raw) : scratch;
+  T* V = M + p * m;
+  T* Q = V + p * p;
+  T* beta = Q + p * p;
   __shared__ int fb;
   __shared__ T sh_beta, sh_diag;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -168,9 +191,9 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
   if (p == 0) return;
   if (tid == 0) fb = 0;
   // M(a, b) = C(b, m + a)   (a < p rows, b < m cols): top^*
-  for (int64_t idx = tid; idx < static_cast<int64_t>(p) * m; idx += nt) {
-    const int a = static_cast<int>(idx % p), b = static_cast<int>(idx / p);
-    M[a + static_cast<int64_t>(b) * p] = C[b + static_cast<int64_t>(m + a) * ldc];
+  for (int idx = tid; idx < p * m; idx += nt) {
+    const int a = idx % p, b = idx / p;
+    M[a + b * p] = C[b + static_cast<int64_t>(m + a) * ldc];
   }
   __syncthreads();
   // householder_reduce (ortho.hpp:30-76) on the p x m block, steps = p
@@ -179,19 +202,19 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
     if (tid == 0) {
       T nrm2 = T(0);
       for (int i = j; i < p; ++i) {
-        const T a = fabs(M[i + static_cast<int64_t>(j) * p]);
+        const T a = fabs(M[i + j * p]);
         nrm2 = add_rn(nrm2, mul_rn(a, a));
       }
       const T nrm = sqrt(nrm2);
       if (nrm == T(0)) {
         fb = 1;
       } else {
-        const T x0 = M[j + static_cast<int64_t>(j) * p];
+        const T x0 = M[j + j * p];
         const T ax0 = fabs(x0);
         const T phase = ax0 > T(0) ? x0 / ax0 : T(1);
-        T* v = V + static_cast<int64_t>(j) * p + j;
+        T* v = V + j * p + j;
         v[0] = add_rn(x0, mul_rn(phase, nrm));
-        for (int i = 1; i < len; ++i) v[i] = M[j + i + static_cast<int64_t>(j) * p];
+        for (int i = 1; i < len; ++i) v[i] = M[j + i + j * p];
         T vn2 = T(0);
         for (int i = 0; i < len; ++i) {
           const T a = fabs(v[i]);
@@ -205,9 +228,9 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
     __syncthreads();
     if (fb) break;
     const T b = sh_beta;
-    const T* v = V + static_cast<int64_t>(j) * p + j;
+    const T* v = V + j * p + j;
     for (int c = j + tid; c < m; c += nt) {
-      T* col = M + static_cast<int64_t>(c) * p + j;
+      T* col = M + c * p + j;
       T sdot = T(0);
       for (int i = 0; i < len; ++i) sdot = add_rn(sdot, mul_rn(v[i], col[i]));
       sdot = mul_rn(sdot, b);
@@ -215,24 +238,21 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
     }
     __syncthreads();
     if (tid == 0) {
-      M[j + static_cast<int64_t>(j) * p] = sh_diag;
-      for (int i = j + 1; i < p; ++i) M[i + static_cast<int64_t>(j) * p] = T(0);
+      M[j + j * p] = sh_diag;
+      for (int i = j + 1; i < p; ++i) M[i + j * p] = T(0);
     }
     __syncthreads();
   }
   if (!fb) {
     // Q = I, reflectors applied last to first (apply_reflectors_to, ortho.hpp:78-92)
-    for (int64_t idx = tid; idx < static_cast<int64_t>(p) * p; idx += nt) {
-      const int i = static_cast<int>(idx % p), j = static_cast<int>(idx / p);
-      Q[idx] = i == j ? T(1) : T(0);
-    }
+    for (int idx = tid; idx < p * p; idx += nt) Q[idx] = (idx % p) == (idx / p) ? T(1) : T(0);
     __syncthreads();
     for (int jj = p - 1; jj >= 0; --jj) {
       const int len = p - jj;
-      const T* v = V + static_cast<int64_t>(jj) * p + jj;
+      const T* v = V + jj * p + jj;
       const T b = beta[jj];
       for (int c = tid; c < p; c += nt) {
-        T* qc = Q + static_cast<int64_t>(c) * p + (p - len);
+        T* qc = Q + c * p + (p - len);
         T sdot = T(0);
         for (int i = 0; i < len; ++i) sdot = add_rn(sdot, mul_rn(v[i], qc[i]));
         sdot = mul_rn(sdot, b);
@@ -243,14 +263,13 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
     // fix_diagonal_phases (ortho.hpp:95-110): steps = min(p, m) = p
     if (tid == 0) {
       for (int j = 0; j < p; ++j)
-        if (M[j + static_cast<int64_t>(j) * p] == T(0)) fb = 1;
+        if (M[j + j * p] == T(0)) fb = 1;
     }
     __syncthreads();
     if (!fb) {
-      for (int j = 0; j < p; ++j) {
-        const T d = M[j + static_cast<int64_t>(j) * p];
-        if (d < T(0))
-          for (int i = tid; i < p; i += nt) Q[i + static_cast<int64_t>(j) * p] = -Q[i + static_cast<int64_t>(j) * p];
+      for (int idx = tid; idx < p * p; idx += nt) {
+        const int j = idx / p;
+        if (M[j + j * p] < T(0)) Q[idx] = -Q[idx];
       }
     }
     __syncthreads();
@@ -266,10 +285,30 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
       // matmul(cp, Q): ascending l, separately rounded (dense_kernels.hpp:20-34)
       acc = T(0);
       for (int l = 0; l < p; ++l)
-        acc = add_rn(acc, mul_rn(C[i + static_cast<int64_t>(m + l) * ldc], Q[l + static_cast<int64_t>(j) * p]));
+        acc = add_rn(acc, mul_rn(C[i + static_cast<int64_t>(m + l) * ldc], Q[l + j * p]));
     }
     coef[i + static_cast<int64_t>(m + j) * s] = acc;
   }
+}
+
+template <typename K>
+void allow_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024)
+    MPB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(bytes)));
+}
+
+template <typename T>
+void hl_coeffs_t(int64_t s, int64_t m, int64_t p, const T* C, int64_t ldc, T* coef, T* scratch,
+                 int* fallback, cudaStream_t st) {
+  ProfScope prof("hl_coeffs", st, 0, 0);
+  const size_t bytes = static_cast<size_t>(p * m + 2 * p * p + p) * sizeof(T);
+  const int use = bytes <= kSmemCap;
+  if (use) allow_smem(k_hl_coeffs<T>, bytes);
+  k_hl_coeffs<T><<<1, kSmallThreads, use ? bytes : 0, st>>>(
+      static_cast<int>(s), static_cast<int>(m), static_cast<int>(p), C, ldc, coef, scratch,
+      fallback, use);
+  MPB_LAUNCH_CHECK();
 }
 
 }  // namespace
@@ -287,7 +326,11 @@ void small_cholesky_inv(int64_t m, const T* G, int64_t ldg, T* L, T* Uinv, int* 
                         cudaStream_t st) {
   if (m <= 0) return;
   ProfScope prof("small_chol", st, 0, 0);
-  k_cholesky_inv<T><<<1, kSmallThreads, 0, st>>>(static_cast<int>(m), G, ldg, L, Uinv, status);
+  const size_t bytes = static_cast<size_t>(2 * m * m) * sizeof(T);
+  const int use = bytes <= kSmemCap;
+  if (use) allow_smem(k_cholesky_inv<T>, bytes);
+  k_cholesky_inv<T><<<1, kSmallThreads, use ? bytes : 0, st>>>(static_cast<int>(m), G, ldg, L, Uinv,
+                                                               status, use);
   MPB_LAUNCH_CHECK();
 }
 
@@ -296,7 +339,11 @@ void small_upper_inverse(int64_t m, const T* R, int64_t ldr, T* Rinv, int* statu
                          cudaStream_t st) {
   if (m <= 0) return;
   ProfScope prof("small_trinv", st, 0, 0);
-  k_upper_inverse<T><<<1, kSmallThreads, 0, st>>>(static_cast<int>(m), R, ldr, Rinv, status);
+  const size_t bytes = static_cast<size_t>(2 * m * m) * sizeof(T);
+  const int use = bytes <= kSmemCap;
+  if (use) allow_smem(k_upper_inverse<T>, bytes);
+  k_upper_inverse<T><<<1, kSmallThreads, use ? bytes : 0, st>>>(static_cast<int>(m), R, ldr, Rinv,
+                                                                status, use);
   MPB_LAUNCH_CHECK();
 }
 
@@ -324,20 +371,12 @@ void small_transpose(int64_t r, int64_t c, const T* A, int64_t lda, T* B, int64_
 
 void hl_coeffs(int64_t s, int64_t m, int64_t p, const double* C, int64_t ldc, double* coef,
                double* scratch, int* fallback, cudaStream_t st) {
-  ProfScope prof("hl_coeffs", st, 0, 0);
-  k_hl_coeffs<double><<<1, kSmallThreads, 0, st>>>(static_cast<int>(s), static_cast<int>(m),
-                                                   static_cast<int>(p), C, ldc, coef, scratch,
-                                                   fallback);
-  MPB_LAUNCH_CHECK();
+  hl_coeffs_t<double>(s, m, p, C, ldc, coef, scratch, fallback, st);
 }
 
 void hl_coeffs_f32(int64_t s, int64_t m, int64_t p, const float* C, int64_t ldc, float* coef,
                    float* scratch, int* fallback, cudaStream_t st) {
-  ProfScope prof("hl_coeffs", st, 0, 0);
-  k_hl_coeffs<float><<<1, kSmallThreads, 0, st>>>(static_cast<int>(s), static_cast<int>(m),
-                                                  static_cast<int>(p), C, ldc, coef, scratch,
-                                                  fallback);
-  MPB_LAUNCH_CHECK();
+  hl_coeffs_t<float>(s, m, p, C, ldc, coef, scratch, fallback, st);
 }
 
 #define MPB_INST(T)                                                                            \

@@ -222,7 +222,11 @@ double* Work<T>::dscal() { return rnorm() + 2 * m; }
 template <typename T>
 void small_eig(Work<T>& w, int64_t sdim, T* G, int64_t ldg, T* vals) {
   mpeig_ctx* ctx = w.ctx;
-  ProfScope prof("small_eig", w.s, 0, 0);
+  if (ctx->eig_backend != 1 && small_syev_supported<T>(sdim)) {
+    small_syev<T>(sdim, G, ldg, vals, ctx->d_status + 3, w.s);
+    return;
+  }
+  ProfScope prof("small_eig_cusolver", w.s, 0, 0);
   if constexpr (sizeof(T) == 8)
     cusolver_check(cusolverDnDsyevd(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
                                     static_cast<int>(sdim), G, static_cast<int>(ldg), vals, w.eigw.p,

@@ -41,15 +41,21 @@ template <typename Tq>
 TsqrPlan<Tq> tsqr_plan(int64_t n, int64_t m) {
   TsqrPlan<Tq> p;
   const int64_t mr = round_up(m, 32);
-  int64_t b = max_rows<Tq>(m);
-  p.ok = b >= mr;
+  const int64_t bmax = max_rows<Tq>(m);
+  p.ok = bmax >= mr;
+  int64_t b = bmax;
   if (!p.ok) {
     // large m: one 227 KB CTA per leaf as long as m rows fit
     b = mr;
     p.ok = b * m * static_cast<int64_t>(sizeof(Tq)) <= 220 * 1024;
+  } else {
+    // short leaves: the per-column Householder step is latency-bound, so many
+    // small leaves in parallel beat few tall ones; the tree nodes stack as
+    // many R factors as shared memory allows.
+    b = std::min(bmax, std::max<int64_t>(round_up(2 * m, 32), 128));
   }
   p.leaf_rows = b;
-  p.group = std::max<int64_t>(2, b / m);
+  p.group = std::max<int64_t>(2, (p.ok && bmax >= mr ? bmax : b) / m);
   if (p.group * m * static_cast<int64_t>(sizeof(Tq)) * m > 220 * 1024) p.group = 2;
   p.nleaf = ceil_div(n, b);
   return p;
