@@ -138,6 +138,13 @@ const char* mpeig_last_error(mpeig_ctx* ctx, int64_t* index);
 int64_t mpeig_launch_count(mpeig_ctx* ctx, int reset);
 /* device stream the context orders its work on */
 void* mpeig_ctx_stream(mpeig_ctx* ctx);
+/* execution options (results are bitwise identical across them unless noted):
+ *   "spec_mode"   1 (default): one host sync per iteration, breakdowns rolled
+ *                 back to the careful path; 0: eager, one sync per decision
+ *   "use_graphs"  1 (default): replay the steady-state iteration as a CUDA graph
+ *   "eig_backend" 0 (default): one-CTA syev for 3m <= 96, cuSOLVER above;
+ *                 1: cuSOLVER syevd always (different rounding) */
+int mpeig_ctx_set_option(mpeig_ctx* ctx, const char* key, int value);
 
 /* ------------------------------------------------------------ operators */
 /* BlockOperator<T> (dense_kernels.hpp:15-16).  Device callback: Y = op(X),

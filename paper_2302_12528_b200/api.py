@@ -213,6 +213,10 @@ class Context:
         msg = msg.decode(errors="replace") if msg else ""
         raise _ERRORS.get(rc, MpeigError)(msg, idx.value)
 
+    def set_option(self, key: str, value: int):
+        """spec_mode / use_graphs / eig_backend (see include/mpeig_b200.h)."""
+        self.check(self.lib.mpeig_ctx_set_option(self.h, key.encode(), int(value)))
+
     def launches(self, reset=False) -> int:
         return int(self.lib.mpeig_launch_count(self.h, 1 if reset else 0))
 

@@ -139,6 +139,17 @@ int64_t mpeig_launch_count(mpeig_ctx* ctx, int reset) {
 
 void* mpeig_ctx_stream(mpeig_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
 
+int mpeig_ctx_set_option(mpeig_ctx* ctx, const char* key, int value) {
+  if (!ctx || !key) return MPEIG_E_CONFIG;
+  const std::string k(key);
+  if (k == "eig_backend") ctx->eig_backend = value;
+  else if (k == "spec_mode") ctx->spec_mode = value;
+  else if (k == "use_graphs") ctx->use_graphs = value;
+  else if (k == "syev_method") g_syev_method = value;
+  else return MPEIG_E_CONFIG;
+  return MPEIG_OK;
+}
+
 // ---------------------------------------------------------------- operators
 int mpeig_op_lap3d(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, mpeig_op** out) {
   return guard(ctx, [&] {

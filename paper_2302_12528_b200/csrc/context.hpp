@@ -25,6 +25,8 @@ struct mpeig_ctx {
   double* h_pinned = nullptr;   // pinned staging for per-iteration records
   int64_t h_pinned_elems = 0;
   int eig_backend = 0;          // 0 auto (one-CTA syev for s <= kSyevMax), 1 cuSOLVER
+  int spec_mode = 1;            // speculative iteration (1 host sync / iteration)
+  int use_graphs = 1;           // replay the steady-state iteration as a CUDA graph
 };
 
 enum OpKind { kOpLap3d, kOpLap2d, kOpCsr, kOpDense, kOpDeviceCb, kOpHostCb, kOpJacobi };

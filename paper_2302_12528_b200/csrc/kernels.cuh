@@ -124,6 +124,11 @@ template <typename T>
 bool small_syev_supported(int64_t s);
 template <typename T>
 void small_syev(int64_t s, T* G, int64_t ldg, T* vals, int* info, cudaStream_t st);
+// same, with per-phase clock64 counters (tridiag, QL, sort, sweeps, chain) into prof
+template <typename T>
+void small_syev_prof(int64_t s, T* G, int64_t ldg, T* vals, int* info, long long* prof,
+                     cudaStream_t st);
+extern int g_syev_method;  // 0: tridiagonal + QL (default), 1: tridiagonal + Jacobi
 
 // ------------------------------------------------------------------ TSQR
 // R factor (m x m, upper, positive diagonal) of a tall n x m block by a

@@ -18,6 +18,7 @@ namespace {
 
 constexpr int kSmallThreads = 256;
 constexpr size_t kSmemCap = 200 * 1024;
+constexpr int kMaxHlP = 256;  // largest P block (block size m) of the HL update
 
 template <typename T>
 __global__ void k_symmetrize(int64_t s, T* G, int64_t ldg) {
@@ -179,9 +180,14 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
   T* M = use_smem ? reinterpret_cast<T*>(raw) : scratch;
   T* V = M + p * m;
   T* Q = V + p * p;
-  T* beta = Q + p * p;
+  // Reflector scalars in fp64 for both precisions (bitwise the reference's
+  // for T = double; for T = float, 2/|v|^2 would overflow binary32 once a
+  // column of C is tiny, which the Jacobi eigensolver's near-unit
+  // eigenvectors produce).
+  __shared__ double beta[kMaxHlP];
   __shared__ int fb;
-  __shared__ T sh_beta, sh_diag;
+  __shared__ double sh_beta;
+  __shared__ T sh_diag;
   const int tid = threadIdx.x, nt = blockDim.x;
   // c_x = C(:, 0:m)
   for (int64_t idx = tid; idx < static_cast<int64_t>(s) * m; idx += nt) {
@@ -200,40 +206,40 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
   for (int j = 0; j < p; ++j) {
     const int len = p - j;
     if (tid == 0) {
-      T nrm2 = T(0);
+      double nrm2 = 0.0;
       for (int i = j; i < p; ++i) {
-        const T a = fabs(M[i + j * p]);
+        const double a = fabs(static_cast<double>(M[i + j * p]));
         nrm2 = add_rn(nrm2, mul_rn(a, a));
       }
-      const T nrm = sqrt(nrm2);
-      if (nrm == T(0)) {
+      const double nrm = sqrt(nrm2);
+      if (nrm == 0.0) {
         fb = 1;
       } else {
-        const T x0 = M[j + j * p];
-        const T ax0 = fabs(x0);
-        const T phase = ax0 > T(0) ? x0 / ax0 : T(1);
+        const double x0 = static_cast<double>(M[j + j * p]);
+        const double ax0 = fabs(x0);
+        const double phase = ax0 > 0.0 ? x0 / ax0 : 1.0;
         T* v = V + j * p + j;
-        v[0] = add_rn(x0, mul_rn(phase, nrm));
+        v[0] = static_cast<T>(add_rn(x0, mul_rn(phase, nrm)));
         for (int i = 1; i < len; ++i) v[i] = M[j + i + j * p];
-        T vn2 = T(0);
+        double vn2 = 0.0;
         for (int i = 0; i < len; ++i) {
-          const T a = fabs(v[i]);
+          const double a = fabs(static_cast<double>(v[i]));
           vn2 = add_rn(vn2, mul_rn(a, a));
         }
-        sh_beta = T(2) / vn2;
+        sh_beta = 2.0 / vn2;
         beta[j] = sh_beta;
-        sh_diag = -phase * nrm;  // R(j,j) after the reflection (ortho.hpp:72)
+        sh_diag = static_cast<T>(-phase * nrm);  // R(j,j) after the reflection (ortho.hpp:72)
       }
     }
     __syncthreads();
     if (fb) break;
-    const T b = sh_beta;
+    const double b = sh_beta;
     const T* v = V + j * p + j;
     for (int c = j + tid; c < m; c += nt) {
       T* col = M + c * p + j;
       T sdot = T(0);
       for (int i = 0; i < len; ++i) sdot = add_rn(sdot, mul_rn(v[i], col[i]));
-      sdot = mul_rn(sdot, b);
+      sdot = static_cast<T>(mul_rn(static_cast<double>(sdot), b));
       for (int i = 0; i < len; ++i) col[i] = sub_rn(col[i], mul_rn(sdot, v[i]));
     }
     __syncthreads();
@@ -250,12 +256,12 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
     for (int jj = p - 1; jj >= 0; --jj) {
       const int len = p - jj;
       const T* v = V + jj * p + jj;
-      const T b = beta[jj];
+      const double b = beta[jj];
       for (int c = tid; c < p; c += nt) {
         T* qc = Q + c * p + (p - len);
         T sdot = T(0);
         for (int i = 0; i < len; ++i) sdot = add_rn(sdot, mul_rn(v[i], qc[i]));
-        sdot = mul_rn(sdot, b);
+        sdot = static_cast<T>(mul_rn(static_cast<double>(sdot), b));
         for (int i = 0; i < len; ++i) qc[i] = sub_rn(qc[i], mul_rn(sdot, v[i]));
       }
       __syncthreads();
@@ -302,6 +308,7 @@ template <typename T>
 void hl_coeffs_t(int64_t s, int64_t m, int64_t p, const T* C, int64_t ldc, T* coef, T* scratch,
                  int* fallback, cudaStream_t st) {
   ProfScope prof("hl_coeffs", st, 0, 0);
+  if (p > kMaxHlP) throw Error(MPEIG_E_CONFIG, "hl_update: block size above 256 not supported");
   const size_t bytes = static_cast<size_t>(p * m + 2 * p * p + p) * sizeof(T);
   const int use = bytes <= kSmemCap;
   if (use) allow_smem(k_hl_coeffs<T>, bytes);

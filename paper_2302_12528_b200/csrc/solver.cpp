@@ -181,6 +181,7 @@ Work<T>::Work(mpeig_ctx* c, int64_t n_, int64_t m_, int64_t smax_) : ctx(c), n(n
     tsqr_f.alloc(static_cast<size_t>(tsqr_workspace_elems<double, float>(n, m)), s);
   rw.alloc(static_cast<size_t>(std::max<int64_t>(resid_workspace_elems(n, m), kNumSMs * 2) + 4 * m + 8), s);
   theta.alloc(static_cast<size_t>(smax), s);
+  theta_prev.alloc(static_cast<size_t>(smax), s);
   // cuSOLVER syevd workspace for the largest projected problem
   int lw = 0;
   if constexpr (sizeof(T) == 8)
@@ -222,11 +223,36 @@ double* Work<T>::dscal() { return rnorm() + 2 * m; }
 template <typename T>
 void small_eig(Work<T>& w, int64_t sdim, T* G, int64_t ldg, T* vals) {
   mpeig_ctx* ctx = w.ctx;
-  if (ctx->eig_backend != 1 && small_syev_supported<T>(sdim)) {
+  if (ctx->eig_backend == 0 && small_syev_supported<T>(sdim)) {
     small_syev<T>(sdim, G, ldg, vals, ctx->d_status + 3, w.s);
     return;
   }
   ProfScope prof("small_eig_cusolver", w.s, 0, 0);
+  if (ctx->eig_backend == 2) {  // diagnostic: cuSOLVER's Jacobi (syevj)
+    syevjInfo_t jp;
+    cusolverDnCreateSyevjInfo(&jp);
+    cusolverDnXsyevjSetTolerance(jp, 0.0);
+    cusolverDnXsyevjSetMaxSweeps(jp, 100);
+    int lw = 0;
+    if constexpr (sizeof(T) == 8)
+      cusolverDnDsyevj_bufferSize(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                  static_cast<int>(sdim), G, static_cast<int>(ldg), vals, &lw, jp);
+    else
+      cusolverDnSsyevj_bufferSize(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                  static_cast<int>(sdim), G, static_cast<int>(ldg), vals, &lw, jp);
+    DevBuf<T> wk(static_cast<size_t>(lw > 0 ? lw : 1), w.s);
+    if constexpr (sizeof(T) == 8)
+      cusolverDnDsyevj(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                       static_cast<int>(sdim), G, static_cast<int>(ldg), vals, wk.p, lw,
+                       ctx->d_status + 3, jp);
+    else
+      cusolverDnSsyevj(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                       static_cast<int>(sdim), G, static_cast<int>(ldg), vals, wk.p, lw,
+                       ctx->d_status + 3, jp);
+    MPB_CUDA(cudaStreamSynchronize(w.s));
+    cusolverDnDestroySyevjInfo(jp);
+    return;
+  }
   if constexpr (sizeof(T) == 8)
     cusolver_check(cusolverDnDsyevd(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
                                     static_cast<int>(sdim), G, static_cast<int>(ldg), vals, w.eigw.p,
@@ -448,11 +474,16 @@ struct EvTimer {
   }
 };
 
+// Eager reference-shaped stage: one host round trip per decision point.  Used
+// when the operator or preconditioner cannot run without the host (host
+// BlockOperator adapter, user callbacks that synchronise) and as the
+// semantic baseline of the speculative stage below.
 template <typename T>
-StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* X0, int64_t ldx0,
-                         int64_t m, const mpeig_cfg& cfg, const mpeig_op* T_op, double a_norm_est,
-                         const mpeig_stage_opts& opt, mpeig_history_sink sink, void* sink_user,
-                         T* Xout, int64_t ldxout, mpeig_timings* tim) {
+StageResult lobpcg_stage_eager(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* X0,
+                               int64_t ldx0, int64_t m, const mpeig_cfg& cfg, const mpeig_op* T_op,
+                               double a_norm_est, const mpeig_stage_opts& opt,
+                               mpeig_history_sink sink, void* sink_user, T* Xout, int64_t ldxout,
+                               mpeig_timings* tim) {
   if (n <= 0 || m <= 0) throw Error(MPEIG_E_DIMENSION, "lobpcg_stage: empty block");
   const int64_t smax = 3 * m;
   Work<T> w(ctx, n, m, smax);
@@ -528,12 +559,28 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
     timer.start();
     const int64_t b = m + p;
     int64_t dropped = 0, wc = m;
+    auto dbg = [&](const T* ptr, int64_t cols, const char* label) {
+      if (!getenv("MPEIG_DEBUG_NAN")) return;
+      std::vector<T> h(static_cast<size_t>(w.ld * cols));
+      MPB_CUDA(cudaMemcpyAsync(h.data(), ptr, sizeof(T) * h.size(), cudaMemcpyDeviceToHost, s));
+      MPB_CUDA(cudaStreamSynchronize(s));
+      int64_t bad = 0;
+      for (int64_t j = 0; j < cols; ++j)
+        for (int64_t i = 0; i < n; ++i) bad += !std::isfinite(static_cast<double>(h[i + j * w.ld]));
+      if (bad) fprintf(stderr, "iter %ld: %ld non-finite after %s (cols %ld, p %ld)\n", (long)iter, (long)bad, label, (long)cols, (long)p);
+    };
+    dbg(w.S.p, m + p, "S[X P] at start");
+    dbg(Wslot, m, "W = T(R)");
     project_out<T>(w, w.S.p, b, w.ld, Wslot, wc, w.ld, 2);
+    dbg(Wslot, m, "project 2");
     wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, opt.use_mixed_qr != 0, &dropped);
+    dbg(Wslot, wc, "QR1");
     if (wc > 0) {
       int64_t more = 0;
       project_out<T>(w, w.S.p, b, w.ld, Wslot, wc, w.ld, 1);
+      dbg(Wslot, wc, "project 1");
       wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, opt.use_mixed_qr != 0, &more);
+      dbg(Wslot, wc, "QR2");
       dropped += more;
     }
     rec.w_columns_dropped = dropped;
@@ -549,7 +596,43 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
     const int64_t sdim = m + p + wc;
     status_clear(ctx);
     gram<T>(n, sdim, w.S.p, w.ld, sdim, w.AS.p, w.ld, w.G.p, sdim, 1, w.gramw.p, s);
+    std::vector<T> dbgG;
+    if (getenv("MPEIG_DUMP_G_ITER") &&
+        (atol(getenv("MPEIG_DUMP_G_ITER")) == iter || atol(getenv("MPEIG_DUMP_G_ITER")) < 0)) {
+      std::vector<T> h(sdim * sdim);
+      MPB_CUDA(cudaMemcpyAsync(h.data(), w.G.p, sizeof(T) * sdim * sdim, cudaMemcpyDeviceToHost, s));
+      MPB_CUDA(cudaStreamSynchronize(s));
+      FILE* f = fopen(getenv("MPEIG_DUMP_G_FILE"), "wb");
+      if (f) {
+        fwrite(h.data(), sizeof(T), h.size(), f);
+        fclose(f);
+      }
+    }
+    if (getenv("MPEIG_DEBUG_NAN")) {
+      dbgG.resize(sdim * sdim);
+      MPB_CUDA(cudaMemcpyAsync(dbgG.data(), w.G.p, sizeof(T) * sdim * sdim, cudaMemcpyDeviceToHost, s));
+    }
     small_eig<T>(w, sdim, w.G.p, sdim, w.evals.p);
+    if (getenv("MPEIG_DEBUG_NAN")) {
+      std::vector<T> ev(sdim), vv(sdim * sdim);
+      MPB_CUDA(cudaMemcpyAsync(ev.data(), w.evals.p, sizeof(T) * sdim, cudaMemcpyDeviceToHost, s));
+      MPB_CUDA(cudaMemcpyAsync(vv.data(), w.G.p, sizeof(T) * sdim * sdim, cudaMemcpyDeviceToHost, s));
+      MPB_CUDA(cudaStreamSynchronize(s));
+      bool bad = false;
+      for (auto v : ev) bad |= !std::isfinite(static_cast<double>(v));
+      for (auto v : vv) bad |= !std::isfinite(static_cast<double>(v));
+      bool badin = false;
+      for (auto v : dbgG) badin |= !std::isfinite(static_cast<double>(v));
+      if (bad) {
+        fprintf(stderr, "NaN after eig: sdim=%ld input_bad=%d\n", (long)sdim, badin);
+        FILE* f = fopen(getenv("MPEIG_DEBUG_NAN"), "wb");
+        if (f) {
+          fwrite(dbgG.data(), sizeof(T), dbgG.size(), f);
+          fclose(f);
+        }
+        getenv("MPEIG_DEBUG_NAN_STOP") ? (void)0 : (void)0;
+      }
+    }
     const int64_t pn = std::min(m, sdim - m);
     if constexpr (sizeof(T) == 8)
       hl_coeffs(sdim, m, pn, w.G.p, sdim, w.coef.p, w.scratch(), ctx->d_status + 4, s);
@@ -569,6 +652,326 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
     std::swap(w.S, w.S2);
     std::swap(w.AS, w.AS2);
     p = pn;
+  }
+}
+
+// ----------------------------------------------------- speculative stage
+// Status slots (ctx->d_status) written by one speculative iteration.
+enum : int { kSlotOvf = 2, kSlotEig = 3, kSlotHl = 4, kSlotQr1 = 6, kSlotQr2 = 8 };
+
+// Q in place without host synchronisation: same kernels as qr_core, Q is
+// written unconditionally and failures only land in `status` (the caller
+// rolls the iteration back and repeats it on the careful path).
+template <typename T>
+static void qr_spec(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, int* status) {
+  cudaStream_t s = w.s;
+  const int64_t n = w.n;
+  if constexpr (sizeof(T) == 8) {
+    if (lower) {
+      tsqr_r<double, float>(n, m, W, ldw, w.smallf.p, m, w.tsqr_f.p, status, s);
+      convert_f32_to_f64(m, m, w.smallf.p, m, w.Rw(), m, s);
+    } else {
+      tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, status, s);
+    }
+  } else {
+    (void)lower;
+    tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, status, s);
+  }
+  small_upper_inverse<T>(m, w.Rw(), m, w.Rinv(), status, s);
+  gemm_tn<T>(n, m, m, T(1), W, ldw, w.Rinv(), m, T(0), nullptr, 0, w.V.p, w.ld, s);
+  gram<T>(n, m, w.V.p, w.ld, m, w.V.p, w.ld, w.G.p, m, 1, w.gramw.p, s);
+  small_cholesky_inv<T>(m, w.G.p, m, w.L(), w.Uinv(), status, s);
+  gemm_tn<T>(n, m, m, T(1), w.V.p, w.ld, w.Uinv(), m, T(0), nullptr, 0, W, ldw, s);
+}
+
+// Residual of the block in (X, AX) = (S, AS) column block 0, f_T fused into
+// the W slot (or R into w.V), then the per-iteration record to pinned host
+// memory: rnorm, xnorm (double) and theta (T).
+template <typename T>
+static void resid_launch(Work<T>& w, const mpeig_op* T_op, const T* S, const T* AS, T* Wslot) {
+  mpeig_ctx* ctx = w.ctx;
+  const int64_t m = w.m;
+  const bool fused = T_op && T_op->kind == kOpJacobi;
+  const void* dinv = nullptr;
+  int mode = kResidPlain;
+  if (fused) mode = jacobi_mode<T>(T_op, &dinv);
+  residual_precond<T>(mode, w.n, m, S, w.ld, AS, w.ld, w.theta.p, dinv, fused ? Wslot : w.V.p,
+                      w.ld, w.rnorm(), w.xnorm(), ctx->d_status + kSlotOvf, w.rw.p, w.s);
+  MPB_CUDA(cudaMemcpyAsync(ctx->h_pinned, w.rnorm(), sizeof(double) * 2 * m,
+                           cudaMemcpyDeviceToHost, w.s));
+  MPB_CUDA(cudaMemcpyAsync(ctx->h_pinned + 2 * m, w.theta.p, sizeof(T) * m, cudaMemcpyDeviceToHost,
+                           w.s));
+  MPB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->d_status, 16 * sizeof(int), cudaMemcpyDeviceToHost,
+                           w.s));
+}
+
+template <typename T>
+static void read_record(Work<T>& w, std::vector<double>& theta, std::vector<double>& rn,
+                        std::vector<double>& xn) {
+  mpeig_ctx* ctx = w.ctx;
+  const int64_t m = w.m;
+  const T* th = reinterpret_cast<const T*>(ctx->h_pinned + 2 * m);
+  theta.resize(m);
+  rn.resize(m);
+  xn.resize(m);
+  for (int64_t j = 0; j < m; ++j) {
+    theta[j] = static_cast<double>(th[j]);
+    rn[j] = static_cast<double>(static_cast<T>(ctx->h_pinned[j]));
+    xn[j] = static_cast<double>(static_cast<T>(ctx->h_pinned[m + j]));
+  }
+}
+
+struct PhaseEvents {
+  cudaEvent_t e[4];
+  bool on = true;  // record phase boundaries inside the body (eager bodies only)
+  PhaseEvents() {
+    for (auto& x : e) cudaEventCreate(&x);
+  }
+  ~PhaseEvents() {
+    for (auto& x : e) cudaEventDestroy(x);
+  }
+  float ms(int a, int b) const {
+    float t = 0;
+    cudaEventElapsedTime(&t, e[a], e[b]);
+    return t;
+  }
+};
+
+// Speculative iteration body: project + QR twice, A W, Rayleigh-Ritz, HL
+// update into (S2, AS2), theta update, and the NEXT iteration's residual and
+// record copy.  No host synchronisation; graph-capturable when A is.
+template <typename T>
+static void spec_body(Work<T>& w, const mpeig_op* A, const mpeig_op* T_op, int64_t p, bool mixed,
+                      T* S, T* AS, T* S2, T* AS2, PhaseEvents& ev) {
+  mpeig_ctx* ctx = w.ctx;
+  cudaStream_t s = w.s;
+  const int64_t m = w.m, ld = w.ld, n = w.n;
+  T* Wslot = S + (m + p) * ld;
+  if (ev.on) MPB_CUDA(cudaEventRecord(ev.e[0], s));
+  MPB_CUDA(cudaMemsetAsync(ctx->d_status, 0, 16 * sizeof(int), s));
+  MPB_CUDA(cudaMemcpyAsync(w.theta_prev.p, w.theta.p, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
+  project_out<T>(w, S, m + p, ld, Wslot, m, ld, 2);
+  qr_spec<T>(w, m, Wslot, ld, mixed, ctx->d_status + kSlotQr1);
+  project_out<T>(w, S, m + p, ld, Wslot, m, ld, 1);
+  qr_spec<T>(w, m, Wslot, ld, mixed, ctx->d_status + kSlotQr2);
+  if (ev.on) MPB_CUDA(cudaEventRecord(ev.e[1], s));
+  op_apply<T>(ctx, A, m, Wslot, ld, AS + (m + p) * ld, ld);
+  const int64_t sdim = 2 * m + p;
+  gram<T>(n, sdim, S, ld, sdim, AS, ld, w.G.p, sdim, 1, w.gramw.p, s);
+  small_syev<T>(sdim, w.G.p, sdim, w.evals.p, ctx->d_status + kSlotEig, s);
+  const int64_t pn = std::min(m, sdim - m);
+  if constexpr (sizeof(T) == 8)
+    hl_coeffs(sdim, m, pn, w.G.p, sdim, w.coef.p, w.scratch(), ctx->d_status + kSlotHl, s);
+  else
+    hl_coeffs_f32(sdim, m, pn, w.G.p, sdim, w.coef.p, w.scratch(), ctx->d_status + kSlotHl, s);
+  gemm_tn<T>(n, sdim, m + pn, T(1), S, ld, w.coef.p, sdim, T(0), nullptr, 0, S2, ld, s);
+  gemm_tn<T>(n, sdim, m + pn, T(1), AS, ld, w.coef.p, sdim, T(0), nullptr, 0, AS2, ld, s);
+  MPB_CUDA(cudaMemcpyAsync(w.theta.p, w.evals.p, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
+  if (ev.on) MPB_CUDA(cudaEventRecord(ev.e[2], s));
+  resid_launch<T>(w, T_op, S2, AS2, S2 + (m + pn) * ld);
+  if (ev.on) MPB_CUDA(cudaEventRecord(ev.e[3], s));
+}
+
+static bool graph_capturable(const mpeig_op* op) {
+  return op && (op->kind == kOpLap3d || op->kind == kOpLap2d || op->kind == kOpCsr ||
+                op->kind == kOpJacobi);
+}
+
+// lobpcg_stage<T> (eigensolvers.hpp:195-321), speculative form: one host
+// synchronisation per iteration (the record the reference's convergence test
+// and IterationRecord need), the iteration body replayed as a CUDA graph in
+// the steady state.  A breakdown flagged by the body (mixed_qr Cholesky
+// failure, rank deficiency, eigensolver non-convergence) rolls the iteration
+// back -- S/AS are untouched, theta is restored -- and repeats it on the
+// careful path with the reference's fallbacks (orthonormal_q,
+// orthonormal_q_dropping, RankCollapse), so the semantics are unchanged.
+template <typename T>
+StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* X0, int64_t ldx0,
+                         int64_t m, const mpeig_cfg& cfg, const mpeig_op* T_op, double a_norm_est,
+                         const mpeig_stage_opts& opt, mpeig_history_sink sink, void* sink_user,
+                         T* Xout, int64_t ldxout, mpeig_timings* tim) {
+  if (n <= 0 || m <= 0) throw Error(MPEIG_E_DIMENSION, "lobpcg_stage: empty block");
+  const bool spec_ok = ctx->spec_mode != 0 && graph_capturable(A) && T_op &&
+                       T_op->kind == kOpJacobi && small_syev_supported<T>(3 * m);
+  if (!spec_ok)
+    return lobpcg_stage_eager<T>(ctx, A, n, X0, ldx0, m, cfg, T_op, a_norm_est, opt, sink,
+                                 sink_user, Xout, ldxout, tim);
+  Work<T> w(ctx, n, m, 3 * m);
+  cudaStream_t s = w.s;
+  EvTimer timer(s);
+  PhaseEvents ev;
+  mpeig_timings local{};
+  mpeig_timings& tm = tim ? *tim : local;
+  const bool mixed = opt.use_mixed_qr != 0;
+  const bool use_graphs = ctx->use_graphs != 0 && !g_prof_on;
+
+  copy_block<T>(n, m, X0, ldx0, w.S.p, w.ld, s);
+  op_apply<T>(ctx, A, m, w.S.p, w.ld, w.AS.p, w.ld);
+  timer.start();
+  ritz_rotate<T>(w);
+  tm.projected_eig += timer.stop();
+  int64_t p = 0;
+  MPB_CUDA(cudaMemsetAsync(ctx->d_status, 0, 16 * sizeof(int), s));
+  resid_launch<T>(w, T_op, w.S.p, w.AS.p, w.S.p + m * w.ld);
+  MPB_CUDA(cudaStreamSynchronize(s));
+
+  struct GraphKey {
+    const void* S;
+    int64_t p;
+  };
+  std::vector<std::pair<GraphKey, cudaGraphExec_t>> graphs;
+  auto cleanup = [&] {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+    graphs.clear();
+  };
+
+  double best_metric = std::numeric_limits<double>::infinity();
+  int64_t since_improvement = 0;
+  constexpr int64_t kStagnationWindow = 40;
+  std::vector<double> theta, rn, xn;
+  StageResult res;
+  try {
+    for (int64_t iter = 0;; ++iter) {
+      read_record<T>(w, theta, rn, xn);
+      const int64_t n_c = converged_prefix(a_norm_est, theta, rn, xn, opt.tol);
+      if (opt.stagnation_exit) {
+        double metric = 0;
+        for (int64_t j = 0; j < cfg.k && j < m; ++j) {
+          const double denom = (a_norm_est + std::abs(theta[j])) * xn[j];
+          const double ratio = denom > 0 ? rn[j] / denom : std::numeric_limits<double>::infinity();
+          if (ratio > metric) metric = ratio;
+        }
+        if (metric < 0.99 * best_metric) {
+          best_metric = metric;
+          since_improvement = 0;
+        } else {
+          ++since_improvement;
+        }
+      }
+      mpeig_iter_record rec{};
+      rec.stage = opt.tag;
+      rec.m = m;
+      rec.ritz_values = theta.data();
+      rec.residual_norms = rn.data();
+      rec.n_converged = n_c;
+      const bool done = n_c >= cfg.k;
+      const bool out_of_iters = iter >= cfg.maxit;
+      const bool stalled = opt.stagnation_exit && since_improvement >= kStagnationWindow;
+      if (done || out_of_iters || stalled) {
+        if (sink) sink(sink_user, &rec);
+        if (Xout) copy_block<T>(n, m, w.S.p, w.ld, Xout, ldxout, s);
+        MPB_CUDA(cudaStreamSynchronize(s));
+        res.theta = theta;
+        res.resid = rn;
+        res.iterations = iter;
+        res.converged = done;
+        cleanup();
+        return res;
+      }
+      if (ctx->h_status[kSlotOvf])
+        throw Error(MPEIG_E_OVERFLOW, "to_lower: value exceeds binary32 range");
+
+      // ---- speculative body (graph in the steady state)
+      cudaGraphExec_t exec = nullptr;
+      if (use_graphs && p == m) {
+        for (auto& g : graphs)
+          if (g.first.S == w.S.p && g.first.p == p) exec = g.second;
+        if (!exec) {
+          cudaGraph_t graph;
+          ev.on = false;
+          MPB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+          try {
+            spec_body<T>(w, A, T_op, p, mixed, w.S.p, w.AS.p, w.S2.p, w.AS2.p, ev);
+          } catch (...) {
+            cudaStreamEndCapture(s, &graph);
+            throw;
+          }
+          MPB_CUDA(cudaStreamEndCapture(s, &graph));
+          MPB_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+          cudaGraphDestroy(graph);
+          graphs.push_back({{w.S.p, p}, exec});
+        }
+        MPB_CUDA(cudaEventRecord(ev.e[0], s));
+        MPB_CUDA(cudaGraphLaunch(exec, s));
+        MPB_CUDA(cudaEventRecord(ev.e[3], s));
+        MPB_CUDA(cudaStreamSynchronize(s));
+        tm.projected_eig += ev.ms(0, 3) * 1e-3;  // whole body (no phase split in a graph)
+      } else {
+        ev.on = true;
+        spec_body<T>(w, A, T_op, p, mixed, w.S.p, w.AS.p, w.S2.p, w.AS2.p, ev);
+        MPB_CUDA(cudaStreamSynchronize(s));
+        tm.orthogonalize += ev.ms(0, 1) * 1e-3;
+        tm.projected_eig += ev.ms(1, 2) * 1e-3;
+        tm.precond_apply += ev.ms(2, 3) * 1e-3;
+      }
+      const bool failed = ctx->h_status[kSlotQr1] || ctx->h_status[kSlotQr2] ||
+                          ctx->h_status[kSlotEig];
+      int64_t dropped = 0, pn = std::min(m, m + p);
+      if (failed) {
+        if (getenv("MPEIG_DEBUG_SPEC"))
+          fprintf(stderr, "iter %ld: speculative body failed (qr1 %d/%d qr2 %d/%d eig %d), rolling back\n",
+                  (long)iter, ctx->h_status[kSlotQr1], ctx->h_status[kSlotQr1 + 1],
+                  ctx->h_status[kSlotQr2], ctx->h_status[kSlotQr2 + 1], ctx->h_status[kSlotEig]);
+        // ---- roll back and repeat on the careful path
+        MPB_CUDA(cudaMemcpyAsync(w.theta.p, w.theta_prev.p, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
+        T* Wslot = w.S.p + (m + p) * w.ld;
+        const void* dinv = nullptr;
+        const int mode = jacobi_mode<T>(T_op, &dinv);
+        residual_precond<T>(mode, n, m, w.S.p, w.ld, w.AS.p, w.ld, w.theta.p, dinv, Wslot, w.ld,
+                            w.rnorm(), w.xnorm(), ctx->d_status + kSlotOvf, w.rw.p, s);
+        timer.start();
+        const int64_t b = m + p;
+        int64_t wc = m;
+        project_out<T>(w, w.S.p, b, w.ld, Wslot, wc, w.ld, 2);
+        wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, mixed, &dropped);
+        if (wc > 0) {
+          int64_t more = 0;
+          project_out<T>(w, w.S.p, b, w.ld, Wslot, wc, w.ld, 1);
+          wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, mixed, &more);
+          dropped += more;
+        }
+        tm.orthogonalize += timer.stop();
+        rec.w_columns_dropped = dropped;
+        if (wc == 0 && p == 0) {
+          if (sink) sink(sink_user, &rec);
+          throw Error(MPEIG_E_RANK_COLLAPSE, "lobpcg_stage: no usable search directions left");
+        }
+        op_apply<T>(ctx, A, wc, Wslot, w.ld, w.AS.p + (m + p) * w.ld, w.ld);
+        timer.start();
+        const int64_t sdim = m + p + wc;
+        status_clear(ctx);
+        gram<T>(n, sdim, w.S.p, w.ld, sdim, w.AS.p, w.ld, w.G.p, sdim, 1, w.gramw.p, s);
+        small_eig<T>(w, sdim, w.G.p, sdim, w.evals.p);
+        pn = std::min(m, sdim - m);
+        if constexpr (sizeof(T) == 8)
+          hl_coeffs(sdim, m, pn, w.G.p, sdim, w.coef.p, w.scratch(), ctx->d_status + kSlotHl, s);
+        else
+          hl_coeffs_f32(sdim, m, pn, w.G.p, sdim, w.coef.p, w.scratch(), ctx->d_status + kSlotHl, s);
+        gemm_tn<T>(n, sdim, m + pn, T(1), w.S.p, w.ld, w.coef.p, sdim, T(0), nullptr, 0, w.S2.p,
+                   w.ld, s);
+        gemm_tn<T>(n, sdim, m + pn, T(1), w.AS.p, w.ld, w.coef.p, sdim, T(0), nullptr, 0, w.AS2.p,
+                   w.ld, s);
+        MPB_CUDA(cudaMemcpyAsync(w.theta.p, w.evals.p, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
+        status_fetch(ctx);
+        tm.projected_eig += timer.stop();
+        if (ctx->h_status[kSlotEig] > 0)
+          throw Error(MPEIG_E_NO_CONVERGENCE, "small_herm_eig: QL sweep budget exhausted");
+        const int hl_fb = ctx->h_status[kSlotHl];
+        MPB_CUDA(cudaMemsetAsync(ctx->d_status, 0, 16 * sizeof(int), s));
+        resid_launch<T>(w, T_op, w.S2.p, w.AS2.p, w.S2.p + (m + pn) * w.ld);
+        MPB_CUDA(cudaStreamSynchronize(s));
+        ctx->h_status[kSlotHl] = hl_fb;
+      }
+      rec.w_columns_dropped = dropped;
+      rec.basis_rotation_fallback = ctx->h_status[kSlotHl];
+      if (sink) sink(sink_user, &rec);
+      std::swap(w.S, w.S2);
+      std::swap(w.AS, w.AS2);
+      p = pn;
+    }
+  } catch (...) {
+    cleanup();
+    throw;
   }
 }
 

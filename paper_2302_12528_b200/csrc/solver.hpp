@@ -26,6 +26,7 @@ struct Work {
   DevBuf<float> tsqr_f;  // TSQR tree in fp32 (mixed_qr)
   DevBuf<double> rw;  // residual partials + norms
   DevBuf<T> theta;    // current Ritz values (device)
+  DevBuf<T> theta_prev;  // Ritz values before the last speculative update
   DevBuf<T> eigw;
   int lwork = 0;
 

@@ -71,45 +71,53 @@ __device__ __forceinline__ T warp_sum(T v) {
 // Householder reduction of the b x m tile (column-major, ld b) in shared
 // memory.  On exit the upper triangle holds R.  A column whose remaining
 // norm is zero gets no reflector (R(j,j) = 0; rank is judged on the final R).
+// The reflector scalars (norm, beta = 2 / v^T v, the projection coefficient)
+// are formed in fp64 even for an fp32 tile: beta = 2/|v|^2 overflows binary32
+// once a column norm drops below ~1e-19, which happens for residual columns
+// of converged Ritz pairs.
 template <typename Tq>
 __device__ void householder_tile(Tq* t, int b, int m) {
-  __shared__ Tq red[kThreads / 32];
-  __shared__ Tq sh_beta, sh_diag;
+  __shared__ double red[kThreads / 32];
+  __shared__ double sh_beta;
+  __shared__ Tq sh_diag;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int steps = min(b, m);
   for (int j = 0; j < steps; ++j) {
     Tq* cj = t + static_cast<int64_t>(j) * b;
-    Tq part = Tq(0);
-    for (int i = j + 1 + tid; i < b; i += kThreads) part = fma(cj[i], cj[i], part);
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < b; i += kThreads) {
+      const double v = static_cast<double>(cj[i]);
+      part = fma(v, v, part);
+    }
     part = warp_sum(part);
     if (lane == 0) red[warp] = part;
     __syncthreads();
     if (tid == 0) {
-      Tq tail2 = Tq(0);
+      double tail2 = 0.0;
 #pragma unroll
       for (int w = 0; w < kThreads / 32; ++w) tail2 += red[w];
-      const Tq x0 = cj[j];
-      const Tq nrm = sqrt(fma(x0, x0, tail2));
-      if (nrm == Tq(0)) {
-        sh_beta = Tq(0);
+      const double x0 = static_cast<double>(cj[j]);
+      const double nrm = sqrt(fma(x0, x0, tail2));
+      if (nrm == 0.0) {
+        sh_beta = 0.0;
         sh_diag = Tq(0);
       } else {
-        const Tq phase = x0 >= Tq(0) ? Tq(1) : Tq(-1);
-        const Tq v0 = x0 + phase * nrm;
-        sh_beta = Tq(2) / fma(v0, v0, tail2);
-        sh_diag = -phase * nrm;
-        cj[j] = v0;
+        const double phase = x0 >= 0.0 ? 1.0 : -1.0;
+        const double v0 = x0 + phase * nrm;
+        sh_beta = 2.0 / fma(v0, v0, tail2);
+        sh_diag = static_cast<Tq>(-phase * nrm);
+        cj[j] = static_cast<Tq>(v0);
       }
     }
     __syncthreads();
-    const Tq beta = sh_beta;
-    if (beta != Tq(0)) {
+    const double beta = sh_beta;
+    if (beta != 0.0) {
       for (int c = j + 1 + warp; c < m; c += kThreads / 32) {
         Tq* cc = t + static_cast<int64_t>(c) * b;
         Tq s = Tq(0);
         for (int i = j + lane; i < b; i += 32) s = fma(cj[i], cc[i], s);
         s = warp_sum(s);
-        s = __shfl_sync(0xffffffffu, s, 0) * beta;
+        s = static_cast<Tq>(static_cast<double>(__shfl_sync(0xffffffffu, s, 0)) * beta);
         for (int i = j + lane; i < b; i += 32) cc[i] = fma(-s, cj[i], cc[i]);
       }
     }
@@ -178,7 +186,7 @@ k_tsqr_node(int64_t nR, int m, int group, const Tq* __restrict__ Rin, Tq* __rest
 // positive diagonal (fix_diagonal_phases), rank check, copy to R (ld ldr)
 template <typename Tq>
 __global__ void k_tsqr_finish(int m, const Tq* __restrict__ Rin, Tq* __restrict__ R, int64_t ldr,
-                              int* status) {
+                              int* status, int numeric_rank_check) {
   for (int64_t idx = threadIdx.x; idx < static_cast<int64_t>(m) * m; idx += blockDim.x) {
     const int i = static_cast<int>(idx % m), j = static_cast<int>(idx / m);
     const Tq d = Rin[i + static_cast<int64_t>(i) * m];
@@ -186,12 +194,29 @@ __global__ void k_tsqr_finish(int m, const Tq* __restrict__ Rin, Tq* __restrict_
     R[i + static_cast<int64_t>(j) * ldr] = d < Tq(0) ? -v : v;
   }
   if (threadIdx.x == 0 && status[0] == 0) {
-    for (int j = 0; j < m; ++j)
-      if (Rin[j + static_cast<int64_t>(j) * m] == Tq(0)) {
+    // Exact zero pivot: the reference's householder_reduce throws
+    // RankDeficient (ortho.hpp:43-45).  A non-finite pivot is overflow.  With
+    // numeric_rank_check (Householder-equivalent QR, R and the block in one
+    // precision) a pivot below m*eps*max|R_ii| also counts as rank deficient:
+    // Q = W R^-1 cannot represent the null directions a Householder Q fills
+    // with rounding noise, so the caller takes the reference's rank-dropping
+    // fallback (orthonormalize_dropping, ortho.hpp:205-250) instead.
+    Tq dmax = Tq(0);
+    for (int j = 0; j < m; ++j) dmax = fmax(dmax, fabs(Rin[j + static_cast<int64_t>(j) * m]));
+    const Tq eps = sizeof(Tq) == 8 ? Tq(2.220446049250313e-16) : Tq(1.1920929e-7f);
+    for (int j = 0; j < m; ++j) {
+      const Tq d = fabs(Rin[j + static_cast<int64_t>(j) * m]);
+      if (!isfinite(static_cast<double>(d))) {
+        status[0] = MPEIG_E_OVERFLOW;
+        status[1] = j;
+        break;
+      }
+      if (d == Tq(0) || (numeric_rank_check && d <= Tq(m) * eps * dmax)) {
         status[0] = MPEIG_E_RANK_DEFICIENT;
         status[1] = j;
         break;
       }
+    }
   }
 }
 
@@ -230,7 +255,7 @@ void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr,
     std::swap(bufA, bufB);
     nR = nout;
   }
-  k_tsqr_finish<Tq><<<1, 256, 0, s>>>(mi, bufA, R, ldr, status);
+  k_tsqr_finish<Tq><<<1, 256, 0, s>>>(mi, bufA, R, ldr, status, sizeof(Tin) == sizeof(Tq));
   MPB_LAUNCH_CHECK();
 }
 

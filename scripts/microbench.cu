@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
@@ -160,7 +162,7 @@ int main(int argc, char** argv) {
     cusolverDnHandle_t h;
     cusolverDnCreate(&h);
     cusolverDnSetStream(h, s);
-    for (int sdim : {48, 144, 240, 576}) {
+    for (int sdim : {18, 48, 96, 144, 240, 576}) {
       std::vector<double> Mh((size_t)sdim * sdim);
       for (int j = 0; j < sdim; ++j)
         for (int i = 0; i < sdim; ++i) Mh[i + (size_t)j * sdim] = (i == j) ? 1.0 + i : 1.0 / (1 + i + j);
@@ -210,6 +212,72 @@ int main(int argc, char** argv) {
       }, 10, s);
       snprintf(name, sizeof name, "XsyevBatched(1) s=%d", sdim);
       report(name, ms, 0, 0);
+      if (small_syev_supported<double>(sdim)) {
+        ms = time_ms([&] {
+          cudaMemcpyAsync(Mw, M, Mh.size() * 8, cudaMemcpyDeviceToDevice, s);
+          small_syev<double>(sdim, Mw, sdim, W, info, s);
+        }, 10, s);
+        long long* dprof;
+        CK(cudaMalloc(&dprof, 64));
+        CK(cudaMemset(dprof, 0, 64));
+        cudaMemcpyAsync(Mw, M, Mh.size() * 8, cudaMemcpyDeviceToDevice, s);
+        small_syev_prof<double>(sdim, Mw, sdim, W, info, dprof, s);
+        long long hp[5];
+        CK(cudaMemcpy(hp, dprof, sizeof hp, cudaMemcpyDeviceToHost));
+        snprintf(name, sizeof name, "mpb small_syev<double> s=%d", sdim);
+        report(name, ms, 0, 0);
+        printf("  phases (cycles): tridiag %lld  QL %lld  sort %lld  sweeps %lld  chain %lld\n", hp[0], hp[1],
+               hp[2], hp[3], hp[4]);
+        cudaFree(dprof);
+        {  // correctness of both precisions on the same matrix
+          std::vector<double> V((size_t)sdim * sdim), lam(sdim);
+          CK(cudaMemcpy(V.data(), Mw, V.size() * 8, cudaMemcpyDeviceToHost));
+          CK(cudaMemcpy(lam.data(), W, sdim * 8, cudaMemcpyDeviceToHost));
+          double orth = 0, res = 0;
+          for (int a = 0; a < sdim; ++a)
+            for (int b = 0; b < sdim; ++b) {
+              double o = 0, r = 0;
+              for (int i = 0; i < sdim; ++i) {
+                o += V[i + (size_t)a * sdim] * V[i + (size_t)b * sdim];
+                r += Mh[a + (size_t)i * sdim] * V[i + (size_t)b * sdim];
+              }
+              orth = std::max(orth, std::fabs(o - (a == b)));
+              res = std::max(res, std::fabs(r - lam[b] * V[a + (size_t)b * sdim]));
+            }
+          printf("  f64 check s=%d: orth %.2e resid %.2e\n", sdim, orth, res);
+          std::vector<float> Mf(Mh.begin(), Mh.end());
+          float *Mfd, *Wf;
+          CK(cudaMalloc(&Mfd, Mf.size() * 4));
+          CK(cudaMalloc(&Wf, sdim * 4));
+          CK(cudaMemcpy(Mfd, Mf.data(), Mf.size() * 4, cudaMemcpyHostToDevice));
+          small_syev<float>(sdim, Mfd, sdim, Wf, info, s);
+          std::vector<float> Vf((size_t)sdim * sdim), lf(sdim);
+          CK(cudaMemcpy(Vf.data(), Mfd, Vf.size() * 4, cudaMemcpyDeviceToHost));
+          CK(cudaMemcpy(lf.data(), Wf, sdim * 4, cudaMemcpyDeviceToHost));
+          orth = res = 0;
+          int nan = 0;
+          for (int a = 0; a < sdim; ++a)
+            for (int b = 0; b < sdim; ++b) {
+              double o = 0, r = 0;
+              for (int i = 0; i < sdim; ++i) {
+                o += (double)Vf[i + (size_t)a * sdim] * Vf[i + (size_t)b * sdim];
+                r += (double)Mf[a + (size_t)i * sdim] * Vf[i + (size_t)b * sdim];
+              }
+              if (std::isnan(o) || std::isnan(r)) ++nan;
+              orth = std::max(orth, std::fabs(o - (a == b)));
+              res = std::max(res, std::fabs(r - lf[b] * Vf[a + (size_t)b * sdim]));
+            }
+          printf("  f32 check s=%d: orth %.2e resid %.2e nan %d lam0 %g\n", sdim, orth, res, nan, lf[0]);
+          cudaFree(Mfd);
+          cudaFree(Wf);
+        }
+        ms = time_ms([&] {
+          cudaMemcpyAsync(Mw, M, Mh.size() * 8, cudaMemcpyDeviceToDevice, s);
+          small_syev<float>(sdim, (float*)Mw, sdim, (float*)W, info, s);
+        }, 10, s);
+        snprintf(name, sizeof name, "mpb small_syev<float> s=%d", sdim);
+        report(name, ms, 0, 0);
+      }
       CK(cudaFree(dw));
       CK(cudaFree(M));
       CK(cudaFree(Mw));
