@@ -28,8 +28,8 @@ GramPlan gram_plan(int64_t n, int64_t ka, int64_t kb) {
   p.tiles_n = ceil_div(kb, kTile);
   const int64_t ntiles = p.tiles_m * p.tiles_n;
   int64_t nchunk = ceil_div(kTargetCTAs, ntiles);
-  // >= 512 rows per chunk: the chunk partials are summed sequentially per entry
-  const int64_t max_chunks = ceil_div(n, 512);
+  // >= 256 rows per chunk (the partials are re-read by the reduction)
+  const int64_t max_chunks = ceil_div(n, 256);
   if (nchunk > max_chunks) nchunk = max_chunks;
   if (nchunk < 1) nchunk = 1;
   p.rows_per_chunk = round_up(ceil_div(n, nchunk), kGramBK);
@@ -92,23 +92,231 @@ k_gram_partial(int64_t n, int ka, int kb, const T* __restrict__ A, int64_t lda,
     }
 }
 
-template <typename T>
-__global__ void k_gram_reduce(int64_t nchunk, int ka, int kb, const T* __restrict__ part,
-                              T* __restrict__ G, int64_t ldg, int sym) {
-  const int64_t total = static_cast<int64_t>(ka) * kb;
-  const int64_t stride = static_cast<int64_t>(ka) * kb;
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int i = static_cast<int>(idx % ka), j = static_cast<int>(idx / ka);
-    T s = T(0);
-    for (int64_t c = 0; c < nchunk; ++c) s += part[c * stride + idx];
-    if (sym) {
-      T t = T(0);
-      const int64_t tidx = j + static_cast<int64_t>(i) * ka;
-      for (int64_t c = 0; c < nchunk; ++c) t += part[c * stride + tidx];
-      s = (s + t) / T(2);
+// ---- fp64 tensor-core (DMMA) partial Gram ---------------------------------
+// mma.sync.m8n8k4.f64: the legacy fp64 tensor path (tcgen05 has no f64 kind).
+// CTA = 4 warps, 64 x 64 output tile, each warp 32 x 32 (4 x 4 MMA tiles);
+// K (= the row dimension n) streamed in 16-row panels through a cp.async
+// double buffer.  Column-major panels are copied verbatim (16-B chunks of
+// contiguous rows); the smem row pitch 20 (doubles) makes the fragment reads
+// 2-way (the minimum for 8-B lanes).
+constexpr int kDBK = 16;
+constexpr int kDPitch = kDBK + 4;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Load a 16-row x 64-column panel of a column-major matrix (rows r0.., cols
+// c0..) into smem [col][row]; out-of-range rows/cols are zero-filled.
+__device__ __forceinline__ void load_panel(double (*dst)[kDPitch], const double* __restrict__ M,
+                                           int64_t ld, int64_t r0, int64_t r_end, int c0, int ncols) {
+  // 64 cols x 8 chunks of 2 doubles = 512 chunks, 128 threads -> 4 each
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int e = threadIdx.x + 128 * t;
+    const int col = e >> 3, ch = e & 7;
+    const int64_t row = r0 + 2 * ch;
+    const bool cin = c0 + col < ncols;
+    int bytes = 0;
+    if (cin && row < r_end) bytes = row + 1 < r_end ? 16 : 8;
+    const double* src = bytes ? M + row + static_cast<int64_t>(c0 + col) * ld : M;
+    cp_async16(&dst[col][2 * ch], src, bytes);
+  }
+}
+
+__global__ void __launch_bounds__(128)
+k_gram_dmma(int64_t n, int ka, int kb, const double* __restrict__ A, int64_t lda,
+            const double* __restrict__ B, int64_t ldb, int64_t rows_per_chunk, int tiles_n,
+            double* __restrict__ part) {
+  __shared__ __align__(16) double As[2][kTile][kDPitch];
+  __shared__ __align__(16) double Bs[2][kTile][kDPitch];
+  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
+  const int i0 = tm * kTile, j0 = tn * kTile;
+  const int64_t r_begin = static_cast<int64_t>(blockIdx.y) * rows_per_chunk;
+  const int64_t r_end = min(n, r_begin + rows_per_chunk);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  const int npanel = static_cast<int>((r_end - r_begin + kDBK - 1) / kDBK);
+  if (npanel > 0) {
+    load_panel(As[0], A, lda, r_begin, r_end, i0, ka);
+    load_panel(Bs[0], B, ldb, r_begin, r_end, j0, kb);
+  }
+  cp_async_commit();
+  for (int p = 0; p < npanel; ++p) {
+    const int buf = p & 1;
+    if (p + 1 < npanel) {
+      const int64_t r1 = r_begin + static_cast<int64_t>(p + 1) * kDBK;
+      load_panel(As[buf ^ 1], A, lda, r1, r_end, i0, ka);
+      load_panel(Bs[buf ^ 1], B, ldb, r1, r_end, j0, kb);
     }
-    G[i + static_cast<int64_t>(j) * ldg] = s;
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kDBK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        af[q] = As[buf][wm + 8 * q + g][kk + t4];
+        bf[q] = Bs[buf][wn + 8 * q + g][kk + t4];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+    __syncthreads();
+  }
+  double* out = part + static_cast<int64_t>(blockIdx.y) * ka * kb;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = i0 + wm + 8 * a + g, j = j0 + wn + 8 * b + 2 * t4 + h;
+        if (i < ka && j < kb) out[i + static_cast<int64_t>(j) * ka] = acc[a][b][h];
+      }
+}
+
+// ---- fp64 tensor-core (DMMA) block update Y = beta Z + alpha A C ------------
+// A: n x k column-major (the tall operand), C: k x c (small).  CTA = 4 warps,
+// 64 rows x 64 cols of Y, each warp 32 x 32; K in 16-wide panels through a
+// cp.async double buffer.  A panel smem layout [k][row] with pitch 72
+// (fragment reads 2-way), C panel [col][k] with pitch 20.
+constexpr int kAPitch = kTile + 8;
+
+__global__ void __launch_bounds__(128)
+k_gemm_dmma(int64_t n, int k, int c, double alpha, const double* __restrict__ A, int64_t lda,
+            const double* __restrict__ Cm, int64_t ldc, double beta, const double* Z, int64_t ldz,
+            double* Y, int64_t ldy) {
+  __shared__ __align__(16) double As[2][kDBK][kAPitch];
+  __shared__ __align__(16) double Cs[2][kTile][kDPitch];
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kTile;
+  const int j0 = blockIdx.y * kTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  auto load = [&](int buf, int k0) {
+    // A panel: 16 k-columns x 64 rows = 16 x 32 chunks of 2 doubles
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int e = threadIdx.x + 128 * t;
+      const int kc = e >> 5, ch = e & 31;
+      const int64_t row = i0 + 2 * ch;
+      int bytes = 0;
+      if (k0 + kc < k && row < n) bytes = row + 1 < n ? 16 : 8;
+      const double* src = bytes ? A + row + static_cast<int64_t>(k0 + kc) * lda : A;
+      cp_async16(&As[buf][kc][2 * ch], src, bytes);
+    }
+    // C panel: 64 cols x 16 k = 64 x 8 chunks
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int e = threadIdx.x + 128 * t;
+      const int col = e >> 3, ch = e & 7;
+      const int kr = k0 + 2 * ch;
+      int bytes = 0;
+      if (j0 + col < c && kr < k) bytes = kr + 1 < k ? 16 : 8;
+      const double* src = bytes ? Cm + kr + static_cast<int64_t>(j0 + col) * ldc : Cm;
+      cp_async16(&Cs[buf][col][2 * ch], src, bytes);
+    }
+  };
+
+  const int npanel = (k + kDBK - 1) / kDBK;
+  load(0, 0);
+  cp_async_commit();
+  for (int p = 0; p < npanel; ++p) {
+    const int buf = p & 1;
+    if (p + 1 < npanel) load(buf ^ 1, (p + 1) * kDBK);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kDBK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        af[q] = As[buf][kk + t4][wm + 8 * q + g];
+        bf[q] = Cs[buf][wn + 8 * q + g][kk + t4];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t i = i0 + wm + 8 * a + g;
+        const int j = j0 + wn + 8 * b + 2 * t4 + h;
+        if (i < n && j < c) {
+          double v = alpha * acc[a][b][h];
+          if (beta != 0.0) v = beta * Z[i + j * ldz] + v;
+          Y[i + j * ldy] = v;
+        }
+      }
+}
+
+// Deterministic reduction of the chunk partials: a CTA owns 32 entries; warp
+// w sums chunks w, w+8, w+16, ... in order, then the 8 warp sums are added in
+// warp order.  `sym` also averages with the transposed entry (hermitize).
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_gram_reduce(int64_t nchunk, int ka, int kb, const T* __restrict__ part, T* __restrict__ G,
+              int64_t ldg, int sym) {
+  __shared__ T red[8][32][2];
+  const int64_t total = static_cast<int64_t>(ka) * kb;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  T s = T(0), t = T(0);
+  if (idx < total) {
+    const int i = static_cast<int>(idx % ka), j = static_cast<int>(idx / ka);
+    const int64_t tidx = j + static_cast<int64_t>(i) * ka;
+    for (int64_t c = w; c < nchunk; c += 8) {
+      s += part[c * total + idx];
+      if (sym) t += part[c * total + tidx];
+    }
+  }
+  red[w][lane][0] = s;
+  red[w][lane][1] = t;
+  __syncthreads();
+  if (w == 0 && idx < total) {
+    T a = T(0), b = T(0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      a += red[q][lane][0];
+      b += red[q][lane][1];
+    }
+    const int i = static_cast<int>(idx % ka), j = static_cast<int>(idx / ka);
+    G[i + static_cast<int64_t>(j) * ldg] = sym ? (a + b) / T(2) : a;
   }
 }
 
@@ -271,11 +479,26 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
                  2.0 * n * ka * kb);
   const GramPlan p = gram_plan(n, ka, kb);
   dim3 grid(static_cast<unsigned>(p.tiles_m * p.tiles_n), static_cast<unsigned>(p.nchunk));
-  k_gram_partial<T><<<grid, 256, 0, s>>>(n, static_cast<int>(ka), static_cast<int>(kb), A, lda, B,
-                                         ldb, p.rows_per_chunk, static_cast<int>(p.tiles_n), work);
+  const bool aligned = (lda % 2 == 0) && (ldb % 2 == 0) &&
+                       (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(B) % 16 == 0);
+  if constexpr (sizeof(T) == 8) {
+    if (aligned) {
+      k_gram_dmma<<<grid, 128, 0, s>>>(n, static_cast<int>(ka), static_cast<int>(kb), A, lda, B,
+                                       ldb, p.rows_per_chunk, static_cast<int>(p.tiles_n), work);
+    } else {
+      k_gram_partial<T><<<grid, 256, 0, s>>>(n, static_cast<int>(ka), static_cast<int>(kb), A, lda,
+                                             B, ldb, p.rows_per_chunk, static_cast<int>(p.tiles_n),
+                                             work);
+    }
+  } else {
+    (void)aligned;
+    k_gram_partial<T><<<grid, 256, 0, s>>>(n, static_cast<int>(ka), static_cast<int>(kb), A, lda, B,
+                                           ldb, p.rows_per_chunk, static_cast<int>(p.tiles_n), work);
+  }
   MPB_LAUNCH_CHECK();
-  k_gram_reduce<T><<<grid_for(ka * kb), 256, 0, s>>>(p.nchunk, static_cast<int>(ka),
-                                                     static_cast<int>(kb), work, G, ldg, sym);
+  k_gram_reduce<T><<<static_cast<unsigned>(ceil_div(ka * kb, 32)), 256, 0, s>>>(
+      p.nchunk, static_cast<int>(ka), static_cast<int>(kb), work, G, ldg, sym);
   MPB_LAUNCH_CHECK();
 }
 
@@ -295,6 +518,17 @@ void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, 
   ProfScope prof("gemm", s, double(sizeof(T)) * n * (k + (beta != T(0) ? 2 : 1) * c),
                  2.0 * n * k * c);
   dim3 grid(static_cast<unsigned>(ceil_div(n, kTile)), static_cast<unsigned>(ceil_div(c, kTile)));
+  if constexpr (sizeof(T) == 8) {
+    const bool aligned = (lda % 2 == 0) && (ldc % 2 == 0) &&
+                         (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(C) % 16 == 0);
+    if (aligned) {
+      k_gemm_dmma<<<grid, 128, 0, s>>>(n, static_cast<int>(k), static_cast<int>(c), alpha, A, lda, C,
+                                       ldc, beta, Z, ldz, Y, ldy);
+      MPB_LAUNCH_CHECK();
+      return;
+    }
+  }
   k_gemm_tn<T><<<grid, 256, 0, s>>>(n, static_cast<int>(k), static_cast<int>(c), alpha, A, lda, C,
                                     ldc, beta, Z, ldz, Y, ldy);
   MPB_LAUNCH_CHECK();

@@ -95,6 +95,32 @@ __global__ void k_dmma16(double* out, int iters) {
   if (s == 1234.5) out[0] = 1;
 }
 
+// single-thread dependent-chain latencies (cycles per op)
+__global__ void k_lat(double* out, long long* cyc, double x0) {
+  double x = x0, y = x0 * 0.5 + 1.0;
+  float xf = static_cast<float>(x0);
+  long long t0 = clock64();
+  for (int i = 0; i < 256; ++i) x = fma(x, 0.999999, 1e-7);
+  long long t1 = clock64();
+  for (int i = 0; i < 256; ++i) x = rsqrt(x + 1.0);
+  long long t2 = clock64();
+  for (int i = 0; i < 256; ++i) x = 1.0 / (x + 1.0);
+  long long t3 = clock64();
+  for (int i = 0; i < 256; ++i) x = sqrt(x + 1.0);
+  long long t4 = clock64();
+  for (int i = 0; i < 256; ++i) xf = fmaf(xf, 0.999999f, 1e-7f);
+  long long t5 = clock64();
+  for (int i = 0; i < 256; ++i) y = y * x + 0.5;
+  long long t6 = clock64();
+  out[0] = x + y + xf;
+  cyc[0] = (t1 - t0) / 256;
+  cyc[1] = (t2 - t1) / 256;
+  cyc[2] = (t3 - t2) / 256;
+  cyc[3] = (t4 - t3) / 256;
+  cyc[4] = (t5 - t4) / 256;
+  cyc[5] = (t6 - t5) / 256;
+}
+
 __global__ void k_copy(const double4* __restrict__ a, double4* __restrict__ b, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     b[i] = a[i];
@@ -106,6 +132,16 @@ int main(int argc, char** argv) {
   CK(cudaStreamCreate(&s));
   double* dummy;
   CK(cudaMalloc(&dummy, 64));
+  {
+    long long* cyc;
+    CK(cudaMalloc(&cyc, 64));
+    k_lat<<<1, 1, 0, s>>>(dummy, cyc, 0.5);
+    CK(cudaStreamSynchronize(s));
+    long long h[6];
+    CK(cudaMemcpy(h, cyc, sizeof h, cudaMemcpyDeviceToHost));
+    printf("latency (cycles/op): dfma %lld  drsqrt %lld  ddiv %lld  dsqrt %lld  ffma %lld  dmul+dadd %lld\n", h[0],
+           h[1] - 1, h[2] - 1, h[3] - 1, h[4], h[5]);
+  }
   // ---- peaks
   {
     const int iters = 4096;
