@@ -11,6 +11,7 @@
 // The fp64 -> fp32 narrowing of mixed_qr's to_lower (precision.hpp:102-107)
 // happens as the leaf loads W, with the overflow check.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -220,21 +221,314 @@ __global__ void k_tsqr_finish(int m, const Tq* __restrict__ Rin, Tq* __restrict_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident TSQR: one launch for the whole tree.
+//
+// A CTA of NW warps holds a b x m tile (b = 32*RPL) in registers: warp w owns
+// columns c = w + NW*q (q < MPW), lane l owns rows l + 32*i (i < RPL).  Step j
+// of the Householder reduction is formed by the warp owning column j (warp
+// reductions, fp64 scalars), published through a double-buffered shared
+// vector, and applied by every warp to its own columns with one barrier per
+// step.  Leaves factor row blocks of W; the last leaf of each group of G
+// (atomic counter, self-resetting) stacks the G leaf R factors into its tile
+// and factors them again, and so on up to the root, which also applies the
+// positive-diagonal and rank checks of k_tsqr_finish.
+// ---------------------------------------------------------------------------
+template <typename Tq, int NW, int RPL, int MPW>
+struct RegTile {
+  static constexpr int B = 32 * RPL;
+  Tq a[MPW][RPL];
+
+  template <typename T>
+  static __device__ __forceinline__ T xor_sum(T v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+  }
+
+  // Householder reduction of the tile; on exit rows <= c of column c hold R
+  // and the rows below are zero.
+  __device__ void factor(int m, Tq (*vbuf)[B], double* sbeta) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int j = 0; j < m; ++j) {
+      const int buf = j & 1;
+      if (warp == (j % NW)) {
+        const int qj = j / NW;
+        Tq x[RPL];
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          x[i] = Tq(0);
+#pragma unroll
+          for (int q = 0; q < MPW; ++q)
+            if (q == qj) x[i] = a[q][i];
+        }
+        double tail = 0.0, xj = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          const int r = lane + 32 * i;
+          const double v = static_cast<double>(x[i]);
+          if (r > j) tail = fma(v, v, tail);
+          if (r == j) xj = v;
+        }
+        tail = xor_sum(tail);
+        const double x0 = __shfl_sync(0xffffffffu, xj, j & 31);
+        const double nrm = sqrt(fma(x0, x0, tail));
+        double beta = 0.0, diag = 0.0, v0 = 0.0;
+        if (nrm != 0.0) {
+          const double phase = x0 >= 0.0 ? 1.0 : -1.0;
+          v0 = x0 + phase * nrm;
+          beta = 2.0 / fma(v0, v0, tail);
+          diag = -phase * nrm;
+        }
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          const int r = lane + 32 * i;
+          vbuf[buf][r] = r < j ? Tq(0) : (r == j ? static_cast<Tq>(v0) : x[i]);
+          const Tq nv = r < j ? x[i] : (r == j ? static_cast<Tq>(diag) : Tq(0));
+#pragma unroll
+          for (int q = 0; q < MPW; ++q)
+            if (q == qj) a[q][i] = nv;
+        }
+        if (lane == 0) sbeta[buf] = beta;
+      }
+      __syncthreads();
+      const double beta = sbeta[buf];
+      if (beta == 0.0) continue;
+      Tq v[RPL];
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) v[i] = vbuf[buf][lane + 32 * i];
+      const int i0 = j >> 5;  // row blocks above j hold zeros of v
+#pragma unroll
+      for (int q = 0; q < MPW; ++q) {
+        const int c = warp + NW * q;
+        if (c > j && c < m) {
+          Tq s = Tq(0);
+#pragma unroll
+          for (int i = 0; i < RPL; ++i)
+            if (i >= i0) s = fma(v[i], a[q][i], s);
+          s = xor_sum(s);
+          const Tq f = static_cast<Tq>(static_cast<double>(s) * beta);
+#pragma unroll
+          for (int i = 0; i < RPL; ++i)
+            if (i >= i0) a[q][i] = fma(-f, v[i], a[q][i]);
+        }
+      }
+    }
+  }
+
+  __device__ void store_r(int m, Tq* __restrict__ R) const {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < MPW; ++q) {
+      const int c = warp + NW * q;
+      if (c >= m) continue;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = lane + 32 * i;
+        if (r < m) R[r + static_cast<int64_t>(c) * m] = a[q][i];
+      }
+    }
+  }
+};
+
+template <typename Tin, typename Tq, int NW, int RPL, int MPW>
+__global__ void __launch_bounds__(NW * 32)
+k_tsqr_reg(int64_t n, int m, const Tin* __restrict__ W, int64_t ldw, Tq* __restrict__ Rbuf,
+           int* __restrict__ counters, int64_t nleaf, int G, Tq* __restrict__ Rfinal, int64_t ldr,
+           int* status, int numeric_rank_check) {
+  using Tile = RegTile<Tq, NW, RPL, MPW>;
+  constexpr int B = Tile::B;
+  __shared__ __align__(16) Tq vbuf[2][B];
+  __shared__ double sbeta[2];
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Tile t;
+  {
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * B;
+    int ovf = 0;
+#pragma unroll
+    for (int q = 0; q < MPW; ++q) {
+      const int c = warp + NW * q;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int64_t row = r0 + lane + 32 * i;
+        t.a[q][i] = (c < m && row < n) ? narrow<Tin, Tq>(__ldg(W + row + c * ldw), &ovf) : Tq(0);
+      }
+    }
+    if (ovf) atomicCAS(status, 0, MPEIG_E_OVERFLOW);
+  }
+  t.factor(m, vbuf, sbeta);
+  const int64_t mm = static_cast<int64_t>(m) * m;
+  int64_t idx = blockIdx.x, cnt = nleaf;
+  Tq* level = Rbuf;   // R factors of the current level
+  int* ctr = counters;
+  while (cnt > 1) {
+    t.store_r(m, level + idx * mm);
+    const int64_t parent = idx / G;
+    const int nchild = static_cast<int>(min(static_cast<int64_t>(G), cnt - parent * G));
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int old = atomicAdd(ctr + parent, 1);
+      s_last = old == nchild - 1;
+      if (s_last) ctr[parent] = 0;  // ready for the next call / graph replay
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const Tq* kids = level + parent * G * mm;
+#pragma unroll
+    for (int q = 0; q < MPW; ++q) {
+      const int c = warp + NW * q;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = lane + 32 * i;
+        const int g = r / m, rr = r - g * m;
+        t.a[q][i] = (c < m && g < nchild && rr <= c) ? __ldcg(kids + g * mm + rr + c * m) : Tq(0);
+      }
+    }
+    level += cnt * mm;
+    ctr += ceil_div(cnt, static_cast<int64_t>(G));
+    cnt = ceil_div(cnt, static_cast<int64_t>(G));
+    idx = parent;
+    t.factor(m, vbuf, sbeta);
+  }
+  // root: this CTA holds R of the whole block
+  t.store_r(m, level);
+  __syncthreads();
+  const Tq* Rr = level;
+  for (int64_t e = threadIdx.x; e < mm; e += blockDim.x) {
+    const int i = static_cast<int>(e % m), j = static_cast<int>(e / m);
+    const Tq d = Rr[i + static_cast<int64_t>(i) * m];
+    const Tq v = i <= j ? Rr[e] : Tq(0);
+    Rfinal[i + static_cast<int64_t>(j) * ldr] = d < Tq(0) ? -v : v;
+  }
+  if (threadIdx.x == 0 && *reinterpret_cast<volatile int*>(status) == 0) {
+    Tq dmax = Tq(0);
+    for (int j = 0; j < m; ++j) dmax = fmax(dmax, fabs(Rr[j + static_cast<int64_t>(j) * m]));
+    const Tq eps = sizeof(Tq) == 8 ? Tq(2.220446049250313e-16) : Tq(1.1920929e-7f);
+    for (int j = 0; j < m; ++j) {
+      const Tq d = fabs(Rr[j + static_cast<int64_t>(j) * m]);
+      if (!isfinite(static_cast<double>(d))) {
+        status[0] = MPEIG_E_OVERFLOW;
+        status[1] = j;
+        break;
+      }
+      if (d == Tq(0) || (numeric_rank_check && d <= Tq(m) * eps * dmax)) {
+        status[0] = MPEIG_E_RANK_DEFICIENT;
+        status[1] = j;
+        break;
+      }
+    }
+  }
+}
+
+struct RegCfg {
+  int nw, rpl, mpw;  // 0 = not supported
+};
+
+// tile shape per (precision, width): b = 32*RPL >= 2m so a tree node stacks
+// at least two R factors; the register tile stays <= 96 32-bit registers.
+template <typename Tq>
+RegCfg reg_cfg(int64_t m) {
+  if (sizeof(Tq) == 4) {
+    if (m <= 16) return {8, 4, 2};
+    if (m <= 32) return {8, 8, 4};
+    if (m <= 48) return {8, 8, 6};
+    if (m <= 64) return {8, 8, 8};
+    if (m <= 96) return {16, 8, 6};
+    if (m <= 128) return {16, 8, 8};
+  } else {
+    if (m <= 16) return {8, 4, 2};
+    if (m <= 32) return {8, 8, 4};
+    if (m <= 48) return {8, 8, 6};
+    if (m <= 64) return {16, 8, 4};
+    if (m <= 96) return {16, 6, 6};
+  }
+  return {0, 0, 0};
+}
+
+template <typename Tin, typename Tq>
+using RegKernel = void (*)(int64_t, int, const Tin*, int64_t, Tq*, int*, int64_t, int, Tq*, int64_t,
+                           int*, int);
+
+template <typename Tin, typename Tq>
+RegKernel<Tin, Tq> reg_kernel(const RegCfg& c) {
+#define MPB_REG(NW, RPL, MPW) \
+  if (c.nw == NW && c.rpl == RPL && c.mpw == MPW) return k_tsqr_reg<Tin, Tq, NW, RPL, MPW>;
+  if constexpr (sizeof(Tq) == 4) {
+    MPB_REG(8, 4, 2) MPB_REG(8, 8, 4) MPB_REG(8, 8, 6) MPB_REG(8, 8, 8) MPB_REG(16, 8, 6)
+    MPB_REG(16, 8, 8)
+  } else {
+    MPB_REG(8, 4, 2) MPB_REG(8, 8, 4) MPB_REG(8, 8, 6) MPB_REG(16, 8, 4) MPB_REG(16, 6, 6)
+  }
+#undef MPB_REG
+  return nullptr;
+}
+
+struct RegPlan {
+  RegCfg cfg;
+  int64_t nleaf, G, r_elems, n_ctr;
+};
+
+template <typename Tq>
+RegPlan reg_plan(int64_t n, int64_t m) {
+  RegPlan p{};
+  p.cfg = reg_cfg<Tq>(m);
+  if (p.cfg.nw == 0) return p;
+  const int64_t b = 32 * p.cfg.rpl;
+  p.G = b / m;
+  p.nleaf = std::max<int64_t>(1, ceil_div(n, b));
+  int64_t cnt = p.nleaf;
+  p.r_elems = m * m;  // root
+  p.n_ctr = 0;
+  while (cnt > 1) {
+    p.r_elems += cnt * m * m;
+    cnt = ceil_div(cnt, p.G);
+    p.n_ctr += cnt;
+  }
+  return p;
+}
+
+bool tsqr_reg_enabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("MPEIG_TSQR_SMEM");
+    return e && e[0] == '1';
+  }();
+  return !off;
+}
+
 }  // namespace
 
 template <typename Tin, typename Tq>
 int64_t tsqr_workspace_elems(int64_t n, int64_t m) {
   const TsqrPlan<Tq> p = tsqr_plan<Tq>(n, m);
-  return (p.nleaf + ceil_div(p.nleaf, p.group) + 1) * m * m;
+  const int64_t smem_path = (p.nleaf + ceil_div(p.nleaf, p.group) + 1) * m * m;
+  const RegPlan r = reg_plan<Tq>(n, m);
+  const int64_t reg_path = r.r_elems + ceil_div(r.n_ctr * static_cast<int64_t>(sizeof(int)),
+                                                static_cast<int64_t>(sizeof(Tq))) + 2;
+  return std::max(smem_path, reg_path);
 }
 
 template <typename Tin, typename Tq>
 void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr, Tq* work,
             int* status, cudaStream_t s) {
+  const int mi = static_cast<int>(m);
+  const RegPlan rp = reg_plan<Tq>(n, m);
+  const RegKernel<Tin, Tq> rk = rp.cfg.nw ? reg_kernel<Tin, Tq>(rp.cfg) : nullptr;
+  if (rk && tsqr_reg_enabled()) {
+    ProfScope prof("tsqr", s, double(sizeof(Tin)) * n * m, 2.0 * n * m * m);
+    int* ctr = reinterpret_cast<int*>(work + rp.r_elems);
+    if (rp.n_ctr) MPB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int) * rp.n_ctr, s));
+    rk<<<static_cast<unsigned>(rp.nleaf), rp.cfg.nw * 32, 0, s>>>(
+        n, mi, W, ldw, work, ctr, rp.nleaf, static_cast<int>(rp.G), R, ldr, status,
+        sizeof(Tin) == sizeof(Tq));
+    MPB_LAUNCH_CHECK();
+    return;
+  }
   const TsqrPlan<Tq> p = tsqr_plan<Tq>(n, m);
   if (!p.ok) throw Error(MPEIG_E_CONFIG, "tsqr: block too wide for the shared-memory leaf");
   ProfScope prof("tsqr", s, double(sizeof(Tin)) * n * m, 2.0 * n * m * m);
-  const int mi = static_cast<int>(m);
   const size_t leaf_smem = static_cast<size_t>(p.leaf_rows * m * sizeof(Tq));
   MPB_CUDA(cudaFuncSetAttribute(k_tsqr_leaf<Tin, Tq>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(std::max<size_t>(leaf_smem, 48 * 1024))));
