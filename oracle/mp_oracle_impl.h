@@ -337,6 +337,7 @@ static void SFX(tridiag_ql)(int64_t n, R* d, R* e, R* V) {
   }
 }
 
+#ifndef MPORC_EIG_JACOBI
 /* full eigendecomposition: Householder tridiagonalisation, QL, stable sort */
 static void SFX(small_herm_eig)(int64_t n, const R* M, R* vals, R* vecs) {
   if (n == 0) return;
@@ -432,6 +433,74 @@ static void SFX(small_herm_eig)(int64_t n, const R* M, R* vals, R* vecs) {
   free(w);
   free(u);
 }
+#else
+/* Sensitivity build only (tests/golden/make_sensitivity.py, -DMPORC_EIG_JACOBI):
+ * the same eigendecomposition by cyclic two-sided Jacobi -- a different,
+ * equally valid small symmetric eigensolver -- to measure how the reference
+ * algorithm's iteration counts react to the rounding of the Rayleigh-Ritz
+ * eigenvectors.  Not the reference's algorithm; never used for parity. */
+static void SFX(small_herm_eig)(int64_t n, const R* M, R* vals, R* vecs) {
+  if (n == 0) return;
+  R* W = (R*)xmalloc((size_t)(n * n) * sizeof(R));
+  R* V = (R*)xcalloc((size_t)(n * n), sizeof(R));
+  for (int64_t j = 0; j < n; ++j) {
+    V[j + j * n] = 1;
+    for (int64_t i = 0; i < n; ++i) W[i + j * n] = (M[i + j * n] + M[j + i * n]) / (R)2;
+  }
+  const R eps = sizeof(R) == 8 ? (R)DBL_EPSILON : (R)FLT_EPSILON;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    R off = 0, tot = 0;
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t i = 0; i < n; ++i) {
+        const R a = W[i + j * n] * W[i + j * n];
+        tot += a;
+        if (i != j) off += a;
+      }
+    if (off <= eps * eps * tot) break;
+    for (int64_t p = 0; p + 1 < n; ++p)
+      for (int64_t q = p + 1; q < n; ++q) {
+        const R apq = W[p + q * n];
+        if (apq == 0) continue;
+        const R th = (W[q + q * n] - W[p + p * n]) / (2 * apq);
+        const R t = (th >= 0 ? (R)1 : (R)-1) / ((R)fabs((double)th) + (R)sqrt((double)(th * th + 1)));
+        const R c = (R)1 / (R)sqrt((double)(t * t + 1)), sn = t * c;
+        for (int64_t k = 0; k < n; ++k) { /* columns p, q */
+          const R wp = W[k + p * n], wq = W[k + q * n];
+          W[k + p * n] = c * wp - sn * wq;
+          W[k + q * n] = sn * wp + c * wq;
+        }
+        for (int64_t k = 0; k < n; ++k) { /* rows p, q */
+          const R wp = W[p + k * n], wq = W[q + k * n];
+          W[p + k * n] = c * wp - sn * wq;
+          W[q + k * n] = sn * wp + c * wq;
+        }
+        for (int64_t k = 0; k < n; ++k) {
+          const R vp = V[k + p * n], vq = V[k + q * n];
+          V[k + p * n] = c * vp - sn * vq;
+          V[k + q * n] = sn * vp + c * vq;
+        }
+      }
+  }
+  int64_t* idx = (int64_t*)xmalloc((size_t)n * sizeof(int64_t));
+  for (int64_t i = 0; i < n; ++i) idx[i] = i;
+  for (int64_t i = 1; i < n; ++i) {
+    const int64_t key = idx[i];
+    int64_t j = i - 1;
+    while (j >= 0 && W[key + key * n] < W[idx[j] + idx[j] * n]) {
+      idx[j + 1] = idx[j];
+      --j;
+    }
+    idx[j + 1] = key;
+  }
+  for (int64_t j = 0; j < n; ++j) {
+    vals[j] = W[idx[j] + idx[j] * n];
+    memcpy(vecs + j * n, V + idx[j] * n, (size_t)n * sizeof(R));
+  }
+  free(idx);
+  free(W);
+  free(V);
+}
+#endif
 
 /* ---- Hetmaniuk-Lehoucq update (eigensolvers.hpp:148-174) ------------------- */
 /* coefficients only: cx = C(:,0:m) (s x m), cpv = C(:,m:m+p) V (s x p) */

@@ -146,6 +146,7 @@ int mpeig_ctx_set_option(mpeig_ctx* ctx, const char* key, int value) {
   else if (k == "spec_mode") ctx->spec_mode = value;
   else if (k == "use_graphs") ctx->use_graphs = value;
   else if (k == "syev_method") g_syev_method = value;
+  else if (k == "ql_exact") g_ql_exact = value;
   else return MPEIG_E_CONFIG;
   return MPEIG_OK;
 }
@@ -490,7 +491,8 @@ int mpeig_gram_f64(mpeig_ctx* ctx, int64_t n, int64_t ka, const double* A, int64
                    const double* B, int64_t ldb, double* G) {
   return guard(ctx, [&] {
     set_device(ctx);
-    DevBuf<double> wk(static_cast<size_t>(gram_workspace_elems<double>(n, ka, kb)), ctx->stream);
+    DevBuf<double> wk;
+    wk.alloc_zero(static_cast<size_t>(gram_workspace_elems<double>(n, ka, kb)), ctx->stream);
     gram<double>(n, ka, A, lda, kb, B, ldb, G, ka, 0, wk.p, ctx->stream);
     MPB_CUDA(cudaStreamSynchronize(ctx->stream));
   });

@@ -71,6 +71,11 @@ struct DevBuf {
     count = n;
     if (n) MPB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), st));
   }
+  // workspaces holding self-resetting tree counters (gram, tsqr) start zeroed
+  void alloc_zero(size_t n, cudaStream_t st) {
+    alloc(n, st);
+    if (n) MPB_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), st));
+  }
   void release() {
     if (p) cudaFreeAsync(p, s);
     p = nullptr;

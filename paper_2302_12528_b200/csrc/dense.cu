@@ -7,6 +7,9 @@
 // thread) with shared-memory staged K panels.  The Gram splits n into a fixed
 // number of chunks and reduces the partials in chunk order, so results are
 // bitwise reproducible run to run (SURVEY §8e determinism).
+#include <algorithm>
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -16,91 +19,249 @@ namespace {
 constexpr int kTile = 64;
 constexpr int kGramBK = 32;
 constexpr int kGemmBK = 16;
-constexpr int kTargetCTAs = kNumSMs * 4;
+
+// ---- Gram G = A^T B ---------------------------------------------------------
+// One CTA per (output tile, row chunk).  The output tile is 16*MT square
+// (MT = 1..4) so that narrow blocks (k = 16, 32, 48) waste no MMA / FMA work
+// on zero padding.  Chunk partials are summed by a tree of groups of
+// kGramGroup inside the kernel itself: the last CTA of a group (atomic
+// counter) adds the group's partials in chunk order, so the result does not
+// depend on CTA timing and is bitwise reproducible.  Counters live at the
+// head of the workspace, are zeroed when the workspace is allocated and are
+// reset by the CTA that consumes them.
+constexpr int kGramGroup = 16;
+constexpr int64_t kGramCtrInts = 8192;
 
 struct GramPlan {
-  int64_t tiles_m, tiles_n, nchunk, rows_per_chunk;
+  int mt;  // output tile = 16 * mt
+  int64_t tiles_m, tiles_n, nchunk, rows_per_chunk, level_elems;
 };
 
 GramPlan gram_plan(int64_t n, int64_t ka, int64_t kb) {
   GramPlan p;
-  p.tiles_m = ceil_div(ka, kTile);
-  p.tiles_n = ceil_div(kb, kTile);
+  const int64_t kmax = std::max(ka, kb);
+  p.mt = kmax <= 16 ? 1 : kmax <= 32 ? 2 : kmax <= 48 ? 3 : 4;
+  const int64_t tile = 16 * p.mt;
+  p.tiles_m = ceil_div(ka, tile);
+  p.tiles_n = ceil_div(kb, tile);
   const int64_t ntiles = p.tiles_m * p.tiles_n;
-  int64_t nchunk = ceil_div(kTargetCTAs, ntiles);
-  // >= 256 rows per chunk (the partials are re-read by the reduction)
-  const int64_t max_chunks = ceil_div(n, 256);
+  // one wave: a single-tile Gram uses one CTA per SM (two reduction levels),
+  // multi-tile Grams two CTAs per SM
+  int64_t nchunk = ntiles == 1 ? kNumSMs : ceil_div(kNumSMs * 2, ntiles);
+  const int64_t max_chunks = ceil_div(n, 64);  // >= 64 rows per chunk
   if (nchunk > max_chunks) nchunk = max_chunks;
   if (nchunk < 1) nchunk = 1;
   p.rows_per_chunk = round_up(ceil_div(n, nchunk), kGramBK);
-  if (p.rows_per_chunk < kGramBK) p.rows_per_chunk = kGramBK;
   p.nchunk = ceil_div(n, p.rows_per_chunk);
   if (p.nchunk < 1) p.nchunk = 1;
+  // level buffers (the last level writes G directly)
+  p.level_elems = 0;
+  int64_t ctrs = 1;
+  for (int64_t cnt = p.nchunk; cnt > 1; cnt = ceil_div(cnt, kGramGroup)) {
+    p.level_elems += cnt * ka * kb;
+    ctrs += ntiles * ceil_div(cnt, kGramGroup);
+  }
+  if (ctrs > kGramCtrInts) throw Error(MPEIG_E_CONFIG, "gram: reduction tree too large");
   return p;
 }
 
-template <typename T>
+// Called by every CTA after writing its chunk partial (tile at i0, j0, edge
+// TILE) to level 0 of `part` (or straight to G when there is a single chunk).
+// scratch: >= TILE*TILE elements of shared memory no longer in use; with a
+// single tile the final sums are hermitized there instead of through a pass
+// over G after a grid-wide counter.
+template <typename T, int TILE>
+__device__ void gram_tree(int ka, int kb, int i0, int j0, int tile, int ntiles, int64_t chunk,
+                          int64_t nchunk, T* __restrict__ part, int* __restrict__ ctr, T* G,
+                          int64_t ldg, int sym, T* scratch) {
+  __shared__ int s_last;
+  const bool local_sym = sym && ntiles == 1;
+  const int64_t tot = static_cast<int64_t>(ka) * kb;
+  int64_t idx = chunk, cnt = nchunk;
+  T* lvl = part;
+  int* c = ctr;
+  while (cnt > 1) {
+    const int64_t ng = ceil_div(cnt, static_cast<int64_t>(kGramGroup));
+    const int64_t grp = idx / kGramGroup;
+    const int nchild = static_cast<int>(min(static_cast<int64_t>(kGramGroup), cnt - grp * kGramGroup));
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int* cp = c + tile * ng + grp;
+      s_last = atomicAdd(cp, 1) == nchild - 1;
+      if (s_last) *cp = 0;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const T* src = lvl + grp * kGramGroup * tot;
+    T* next = lvl + cnt * tot;
+    // valid entries of this tile, kEl per thread per round so that
+    // kEl * kGramGroup independent L2 loads are in flight
+    constexpr int kEl = 2;
+    const int vm = min(TILE, ka - i0), vn = min(TILE, kb - j0), nv = vm * vn;
+    for (int base = 0; base < nv; base += kEl * blockDim.x) {
+      T v[kEl][kGramGroup];
+      int64_t off[kEl];
+#pragma unroll
+      for (int u = 0; u < kEl; ++u) {
+        const int e = base + u * blockDim.x + threadIdx.x;
+        const int ee = e < nv ? e : 0;
+        off[u] = (i0 + ee % vm) + static_cast<int64_t>(j0 + ee / vm) * ka;
+#pragma unroll
+        for (int q = 0; q < kGramGroup; ++q)
+          v[u][q] = (e < nv && q < nchild) ? __ldcg(src + q * tot + off[u]) : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < kEl; ++u) {
+        const int e = base + u * blockDim.x + threadIdx.x;
+        if (e >= nv) continue;
+        T sum = v[u][0];
+#pragma unroll
+        for (int q = 1; q < kGramGroup; ++q)
+          if (q < nchild) sum += v[u][q];
+        if (ng == 1) {
+          if (local_sym) {
+            scratch[e] = sum;
+          } else {
+            const int i = i0 + e % vm, j = j0 + e / vm;
+            G[i + static_cast<int64_t>(j) * ldg] = sum;
+          }
+        } else {
+          next[grp * tot + off[u]] = sum;
+        }
+      }
+    }
+    lvl = next;
+    c += ntiles * ng;
+    cnt = ng;
+    idx = grp;
+  }
+  if (!sym) return;
+  if (local_sym) {
+    // ka == kb here; scratch holds the summed matrix, column-major (ld ka)
+    if (nchunk == 1) {
+      // single chunk: the CTA wrote its partial straight to G
+      __syncthreads();
+      for (int64_t e = threadIdx.x; e < tot; e += blockDim.x)
+        scratch[e] = G[(e % ka) + static_cast<int64_t>(e / ka) * ldg];
+    }
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+      const int i = static_cast<int>(e % ka), j = static_cast<int>(e / ka);
+      G[i + static_cast<int64_t>(j) * ldg] =
+          (scratch[e] + scratch[j + static_cast<int64_t>(i) * ka]) / T(2);
+    }
+    return;
+  }
+  // hermitize once every tile is final: G = (G + G^T) / 2 (eigensolvers.hpp:292-297)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_last = atomicAdd(c, 1) == ntiles - 1;
+    if (s_last) *c = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int i = static_cast<int>(e % ka), j = static_cast<int>(e / ka);
+    if (i > j) continue;
+    const T a = __ldcg(G + i + static_cast<int64_t>(j) * ldg);
+    const T b = __ldcg(G + j + static_cast<int64_t>(i) * ldg);
+    const T v = (a + b) / T(2);
+    G[i + static_cast<int64_t>(j) * ldg] = v;
+    G[j + static_cast<int64_t>(i) * ldg] = v;
+  }
+}
+
+// SIMT Gram (fp32, and fp64 operands that are not 16-B aligned): 256 threads
+// as 16 x 16, TM x TM outputs per thread, 32-row panels staged through
+// registers so the next panel's loads overlap this one's FMAs.
+template <typename T, int TM>
 __global__ void __launch_bounds__(256)
 k_gram_partial(int64_t n, int ka, int kb, const T* __restrict__ A, int64_t lda,
                const T* __restrict__ B, int64_t ldb, int64_t rows_per_chunk, int tiles_n,
-               T* __restrict__ part) {
-  __shared__ T As[kGramBK][kTile + 1];
-  __shared__ T Bs[kGramBK][kTile + 1];
+               int64_t nchunk, T* __restrict__ part, int* __restrict__ ctr, T* G, int64_t ldg,
+               int sym) {
+  constexpr int TILE = 16 * TM;
+  constexpr int kSm = 2 * kGramBK * (TILE + 1) > TILE * TILE ? 2 * kGramBK * (TILE + 1) : TILE * TILE;
+  __shared__ T sm[kSm];  // also gram_tree's scratch
+  auto As = reinterpret_cast<T(*)[TILE + 1]>(sm);
+  auto Bs = reinterpret_cast<T(*)[TILE + 1]>(sm + kGramBK * (TILE + 1));
   const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
-  const int i0 = tm * kTile, j0 = tn * kTile;
+  const int i0 = tm * TILE, j0 = tn * TILE;
   const int64_t r_begin = static_cast<int64_t>(blockIdx.y) * rows_per_chunk;
   const int64_t r_end = min(n, r_begin + rows_per_chunk);
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  T acc[4][4];
+  T acc[TM][TM];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < TM; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = T(0);
+    for (int b = 0; b < TM; ++b) acc[a][b] = T(0);
 
-  for (int64_t r0 = r_begin; r0 < r_end; r0 += kGramBK) {
+  constexpr int kPer = kGramBK * TILE / 256;
+  T ra[kPer], rb[kPer];
+  auto fetch = [&](int64_t r0) {
 #pragma unroll
-    for (int e = threadIdx.x; e < kGramBK * kTile; e += 256) {
+    for (int t = 0; t < kPer; ++t) {
+      const int e = threadIdx.x + 256 * t;
       const int r = e % kGramBK, c = e / kGramBK;
       const int64_t row = r0 + r;
       const bool rin = row < r_end;
-      As[r][c] = (rin && i0 + c < ka) ? A[row + static_cast<int64_t>(i0 + c) * lda] : T(0);
-      Bs[r][c] = (rin && j0 + c < kb) ? B[row + static_cast<int64_t>(j0 + c) * ldb] : T(0);
+      ra[t] = (rin && i0 + c < ka) ? __ldg(A + row + static_cast<int64_t>(i0 + c) * lda) : T(0);
+      rb[t] = (rin && j0 + c < kb) ? __ldg(B + row + static_cast<int64_t>(j0 + c) * ldb) : T(0);
+    }
+  };
+  if (r_begin < r_end) fetch(r_begin);
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += kGramBK) {
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int e = threadIdx.x + 256 * t;
+      As[e % kGramBK][e / kGramBK] = ra[t];
+      Bs[e % kGramBK][e / kGramBK] = rb[t];
     }
     __syncthreads();
+    if (r0 + kGramBK < r_end) fetch(r0 + kGramBK);
 #pragma unroll 8
     for (int r = 0; r < kGramBK; ++r) {
-      T av[4], bv[4];
+      T av[TM], bv[TM];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < TM; ++q) {
         av[q] = As[r][ty + 16 * q];
         bv[q] = Bs[r][tx + 16 * q];
       }
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < TM; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+        for (int b = 0; b < TM; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
     }
     __syncthreads();
   }
-  T* out = part + static_cast<int64_t>(blockIdx.y) * ka * kb;
+  const bool direct = nchunk == 1;
+  T* out = direct ? G : part + static_cast<int64_t>(blockIdx.y) * ka * kb;
+  const int64_t ldo = direct ? ldg : ka;
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < TM; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < TM; ++b) {
       const int i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
-      if (i < ka && j < kb) out[i + static_cast<int64_t>(j) * ka] = acc[a][b];
+      if (i < ka && j < kb) out[i + static_cast<int64_t>(j) * ldo] = acc[a][b];
     }
+  gram_tree<T, TILE>(ka, kb, i0, j0, blockIdx.x, gridDim.x, blockIdx.y, nchunk, part, ctr, G, ldg,
+                     sym, sm);
 }
 
-// ---- fp64 tensor-core (DMMA) partial Gram ---------------------------------
+// ---- fp64 tensor-core (DMMA) Gram -------------------------------------------
 // mma.sync.m8n8k4.f64: the legacy fp64 tensor path (tcgen05 has no f64 kind).
-// CTA = 4 warps, 64 x 64 output tile, each warp 32 x 32 (4 x 4 MMA tiles);
-// K (= the row dimension n) streamed in 16-row panels through a cp.async
-// double buffer.  Column-major panels are copied verbatim (16-B chunks of
-// contiguous rows); the smem row pitch 20 (doubles) makes the fragment reads
-// 2-way (the minimum for 8-B lanes).
+// CTA = 4 warps (2 x 2), output tile 16*MT, each warp (8 MT)^2 = MT x MT MMA
+// tiles; K (= the row dimension n) streamed in 16-row panels through a
+// kGramStages-deep cp.async ring.  Column-major panels are copied verbatim
+// (16-B chunks of contiguous rows); the smem row pitch 20 (doubles) makes the
+// fragment reads 2-way (the minimum for 8-B lanes).
 constexpr int kDBK = 16;
 constexpr int kDPitch = kDBK + 4;
+constexpr int kGramStages = 4;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -116,13 +277,14 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-// Load a 16-row x 64-column panel of a column-major matrix (rows r0.., cols
-// c0..) into smem [col][row]; out-of-range rows/cols are zero-filled.
+// Load a 16-row x TILE-column panel of a column-major matrix (rows r0..,
+// cols c0..) into smem [col][row]; out-of-range rows/cols are zero-filled.
+template <int TILE>
 __device__ __forceinline__ void load_panel(double (*dst)[kDPitch], const double* __restrict__ M,
                                            int64_t ld, int64_t r0, int64_t r_end, int c0, int ncols) {
-  // 64 cols x 8 chunks of 2 doubles = 512 chunks, 128 threads -> 4 each
+  // TILE cols x 8 chunks of 2 doubles, 128 threads
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
+  for (int t = 0; t < TILE / 16; ++t) {
     const int e = threadIdx.x + 128 * t;
     const int col = e >> 3, ch = e & 7;
     const int64_t row = r0 + 2 * ch;
@@ -134,66 +296,90 @@ __device__ __forceinline__ void load_panel(double (*dst)[kDPitch], const double*
   }
 }
 
+template <int MT>
+constexpr size_t gram_dmma_smem() {
+  constexpr size_t ring = sizeof(double) * 2 * kGramStages * (16 * MT) * kDPitch;
+  constexpr size_t scratch = sizeof(double) * (16 * MT) * (16 * MT);
+  return ring > scratch ? ring : scratch;
+}
+
+template <int MT>
 __global__ void __launch_bounds__(128)
 k_gram_dmma(int64_t n, int ka, int kb, const double* __restrict__ A, int64_t lda,
             const double* __restrict__ B, int64_t ldb, int64_t rows_per_chunk, int tiles_n,
-            double* __restrict__ part) {
-  __shared__ __align__(16) double As[2][kTile][kDPitch];
-  __shared__ __align__(16) double Bs[2][kTile][kDPitch];
+            int64_t nchunk, double* __restrict__ part, int* __restrict__ ctr, double* G,
+            int64_t ldg, int sym) {
+  constexpr int TILE = 16 * MT;
+  extern __shared__ __align__(16) unsigned char gsm[];
+  auto As = reinterpret_cast<double(*)[TILE][kDPitch]>(gsm);
+  auto Bs = As + kGramStages;
   const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
-  const int i0 = tm * kTile, j0 = tn * kTile;
+  const int i0 = tm * TILE, j0 = tn * TILE;
   const int64_t r_begin = static_cast<int64_t>(blockIdx.y) * rows_per_chunk;
   const int64_t r_end = min(n, r_begin + rows_per_chunk);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-  double acc[4][4][2];
+  const int wm = (warp >> 1) * 8 * MT, wn = (warp & 1) * 8 * MT;
+  double acc[MT][MT][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < MT; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < MT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
+  // kGramStages-deep cp.async ring: stages-1 panels in flight ahead of the MMA
   const int npanel = static_cast<int>((r_end - r_begin + kDBK - 1) / kDBK);
-  if (npanel > 0) {
-    load_panel(As[0], A, lda, r_begin, r_end, i0, ka);
-    load_panel(Bs[0], B, ldb, r_begin, r_end, j0, kb);
-  }
-  cp_async_commit();
-  for (int p = 0; p < npanel; ++p) {
-    const int buf = p & 1;
-    if (p + 1 < npanel) {
-      const int64_t r1 = r_begin + static_cast<int64_t>(p + 1) * kDBK;
-      load_panel(As[buf ^ 1], A, lda, r1, r_end, i0, ka);
-      load_panel(Bs[buf ^ 1], B, ldb, r1, r_end, j0, kb);
+#pragma unroll
+  for (int q = 0; q < kGramStages - 1; ++q) {
+    if (q < npanel) {
+      const int64_t r1 = r_begin + static_cast<int64_t>(q) * kDBK;
+      load_panel<TILE>(As[q], A, lda, r1, r_end, i0, ka);
+      load_panel<TILE>(Bs[q], B, ldb, r1, r_end, j0, kb);
     }
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  for (int p = 0; p < npanel; ++p) {
+    const int buf = p % kGramStages;
+    cp_async_wait<kGramStages - 2>();
     __syncthreads();
+    {
+      const int q = p + kGramStages - 1;
+      if (q < npanel) {
+        const int64_t r1 = r_begin + static_cast<int64_t>(q) * kDBK;
+        load_panel<TILE>(As[q % kGramStages], A, lda, r1, r_end, i0, ka);
+        load_panel<TILE>(Bs[q % kGramStages], B, ldb, r1, r_end, j0, kb);
+      }
+      cp_async_commit();
+    }
 #pragma unroll
     for (int kk = 0; kk < kDBK; kk += 4) {
-      double af[4], bf[4];
+      double af[MT], bf[MT];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < MT; ++q) {
         af[q] = As[buf][wm + 8 * q + g][kk + t4];
         bf[q] = Bs[buf][wn + 8 * q + g][kk + t4];
       }
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < MT; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        for (int b = 0; b < MT; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
-    __syncthreads();
   }
-  double* out = part + static_cast<int64_t>(blockIdx.y) * ka * kb;
+  const bool direct = nchunk == 1;
+  double* out = direct ? G : part + static_cast<int64_t>(blockIdx.y) * ka * kb;
+  const int64_t ldo = direct ? ldg : ka;
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < MT; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
+    for (int b = 0; b < MT; ++b)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int i = i0 + wm + 8 * a + g, j = j0 + wn + 8 * b + 2 * t4 + h;
-        if (i < ka && j < kb) out[i + static_cast<int64_t>(j) * ka] = acc[a][b][h];
+        if (i < ka && j < kb) out[i + static_cast<int64_t>(j) * ldo] = acc[a][b][h];
       }
+  cp_async_wait<0>();
+  __syncthreads();  // the ring becomes gram_tree's scratch
+  gram_tree<double, TILE>(ka, kb, i0, j0, blockIdx.x, gridDim.x, blockIdx.y, nchunk, part, ctr, G,
+                          ldg, sym, reinterpret_cast<double*>(gsm));
 }
 
 // ---- fp64 tensor-core (DMMA) block update Y = beta Z + alpha A C ------------
@@ -283,41 +469,6 @@ k_gemm_dmma(int64_t n, int k, int c, double alpha, const double* __restrict__ A,
           Y[i + j * ldy] = v;
         }
       }
-}
-
-// Deterministic reduction of the chunk partials: a CTA owns 32 entries; warp
-// w sums chunks w, w+8, w+16, ... in order, then the 8 warp sums are added in
-// warp order.  `sym` also averages with the transposed entry (hermitize).
-template <typename T>
-__global__ void __launch_bounds__(256)
-k_gram_reduce(int64_t nchunk, int ka, int kb, const T* __restrict__ part, T* __restrict__ G,
-              int64_t ldg, int sym) {
-  __shared__ T red[8][32][2];
-  const int64_t total = static_cast<int64_t>(ka) * kb;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * 32 + lane;
-  T s = T(0), t = T(0);
-  if (idx < total) {
-    const int i = static_cast<int>(idx % ka), j = static_cast<int>(idx / ka);
-    const int64_t tidx = j + static_cast<int64_t>(i) * ka;
-    for (int64_t c = w; c < nchunk; c += 8) {
-      s += part[c * total + idx];
-      if (sym) t += part[c * total + tidx];
-    }
-  }
-  red[w][lane][0] = s;
-  red[w][lane][1] = t;
-  __syncthreads();
-  if (w == 0 && idx < total) {
-    T a = T(0), b = T(0);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      a += red[q][lane][0];
-      b += red[q][lane][1];
-    }
-    const int i = static_cast<int>(idx % ka), j = static_cast<int>(idx / ka);
-    G[i + static_cast<int64_t>(j) * ldg] = sym ? (a + b) / T(2) : a;
-  }
 }
 
 template <typename T>
@@ -463,7 +614,7 @@ int grid_for(int64_t total, int threads = 256, int64_t cap = kNumSMs * 8) {
 template <typename T>
 int64_t gram_workspace_elems(int64_t n, int64_t ka, int64_t kb) {
   const GramPlan p = gram_plan(n, ka, kb);
-  return p.nchunk * ka * kb;
+  return ceil_div(kGramCtrInts * static_cast<int64_t>(sizeof(int)), sizeof(T)) + p.level_elems;
 }
 
 template <typename T>
@@ -478,27 +629,56 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
   ProfScope prof("gram", s, double(sizeof(T)) * n * (A == B ? ka : ka + kb),
                  2.0 * n * ka * kb);
   const GramPlan p = gram_plan(n, ka, kb);
+  int* ctr = reinterpret_cast<int*>(work);
+  T* part = work + ceil_div(kGramCtrInts * static_cast<int64_t>(sizeof(int)), sizeof(T));
   dim3 grid(static_cast<unsigned>(p.tiles_m * p.tiles_n), static_cast<unsigned>(p.nchunk));
   const bool aligned = (lda % 2 == 0) && (ldb % 2 == 0) &&
                        (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(B) % 16 == 0);
+  const int kai = static_cast<int>(ka), kbi = static_cast<int>(kb), tn = static_cast<int>(p.tiles_n);
   if constexpr (sizeof(T) == 8) {
     if (aligned) {
-      k_gram_dmma<<<grid, 128, 0, s>>>(n, static_cast<int>(ka), static_cast<int>(kb), A, lda, B,
-                                       ldb, p.rows_per_chunk, static_cast<int>(p.tiles_n), work);
-    } else {
-      k_gram_partial<T><<<grid, 256, 0, s>>>(n, static_cast<int>(ka), static_cast<int>(kb), A, lda,
-                                             B, ldb, p.rows_per_chunk, static_cast<int>(p.tiles_n),
-                                             work);
+      auto launch = [&](auto mt_tag) {
+        constexpr int MT = decltype(mt_tag)::value;
+        constexpr size_t smem = gram_dmma_smem<MT>();
+        static bool attr = false;
+        if (!attr) {
+          MPB_CUDA(cudaFuncSetAttribute(k_gram_dmma<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+          attr = true;
+        }
+        k_gram_dmma<MT><<<grid, 128, smem, s>>>(n, kai, kbi, A, lda, B, ldb, p.rows_per_chunk, tn,
+                                                p.nchunk, part, ctr, G, ldg, sym);
+      };
+      switch (p.mt) {
+        case 1: launch(std::integral_constant<int, 1>()); break;
+        case 2: launch(std::integral_constant<int, 2>()); break;
+        case 3: launch(std::integral_constant<int, 3>()); break;
+        default: launch(std::integral_constant<int, 4>()); break;
+      }
+      MPB_LAUNCH_CHECK();
+      return;
     }
-  } else {
-    (void)aligned;
-    k_gram_partial<T><<<grid, 256, 0, s>>>(n, static_cast<int>(ka), static_cast<int>(kb), A, lda, B,
-                                           ldb, p.rows_per_chunk, static_cast<int>(p.tiles_n), work);
   }
-  MPB_LAUNCH_CHECK();
-  k_gram_reduce<T><<<static_cast<unsigned>(ceil_div(ka * kb, 32)), 256, 0, s>>>(
-      p.nchunk, static_cast<int>(ka), static_cast<int>(kb), work, G, ldg, sym);
+  (void)aligned;
+  switch (p.mt) {
+    case 1:
+      k_gram_partial<T, 1><<<grid, 256, 0, s>>>(n, kai, kbi, A, lda, B, ldb, p.rows_per_chunk, tn,
+                                                p.nchunk, part, ctr, G, ldg, sym);
+      break;
+    case 2:
+      k_gram_partial<T, 2><<<grid, 256, 0, s>>>(n, kai, kbi, A, lda, B, ldb, p.rows_per_chunk, tn,
+                                                p.nchunk, part, ctr, G, ldg, sym);
+      break;
+    case 3:
+      k_gram_partial<T, 3><<<grid, 256, 0, s>>>(n, kai, kbi, A, lda, B, ldb, p.rows_per_chunk, tn,
+                                                p.nchunk, part, ctr, G, ldg, sym);
+      break;
+    default:
+      k_gram_partial<T, 4><<<grid, 256, 0, s>>>(n, kai, kbi, A, lda, B, ldb, p.rows_per_chunk, tn,
+                                                p.nchunk, part, ctr, G, ldg, sym);
+      break;
+  }
   MPB_LAUNCH_CHECK();
 }
 

@@ -18,7 +18,8 @@ int64_t gram_workspace_elems(int64_t n, int64_t ka, int64_t kb);
 // dense_kernels.hpp:36-52).  Split-n partial products reduced in a fixed
 // order -> bitwise deterministic for a given n.  `sym` != 0 additionally
 // symmetrises G in place like hermitize (dense_kernels.hpp:77-88); needs
-// ka == kb.  work: gram_workspace_elems<T>() elements.
+// ka == kb.  work: gram_workspace_elems<T>() elements, zeroed before first
+// use (its head holds the reduction-tree counters, which reset themselves).
 template <typename T>
 void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B,
           int64_t ldb, T* G, int64_t ldg, int sym, T* work, cudaStream_t s);
@@ -128,6 +129,7 @@ void small_syev(int64_t s, T* G, int64_t ldg, T* vals, int* info, cudaStream_t s
 template <typename T>
 void small_syev_prof(int64_t s, T* G, int64_t ldg, T* vals, int* info, long long* prof,
                      cudaStream_t st);
+extern int g_ql_exact;
 extern int g_syev_method;  // 0: tridiagonal + QL (default), 1: tridiagonal + Jacobi
 
 // ------------------------------------------------------------------ TSQR

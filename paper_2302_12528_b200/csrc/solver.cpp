@@ -175,10 +175,10 @@ Work<T>::Work(mpeig_ctx* c, int64_t n_, int64_t m_, int64_t smax_) : ctx(c), n(n
   gw = std::max(gw, gram_workspace_elems<T>(n, 2 * m, m));
   gw = std::max(gw, gram_workspace_elems<T>(n, m, m));
   gw = std::max(gw, gram_workspace_elems<T>(n, m, 1));
-  gramw.alloc(static_cast<size_t>(gw), s);
-  tsqr_w.alloc(static_cast<size_t>(tsqr_workspace_elems<T, T>(n, m)), s);
+  gramw.alloc_zero(static_cast<size_t>(gw), s);
+  tsqr_w.alloc_zero(static_cast<size_t>(tsqr_workspace_elems<T, T>(n, m)), s);
   if constexpr (sizeof(T) == 8)
-    tsqr_f.alloc(static_cast<size_t>(tsqr_workspace_elems<double, float>(n, m)), s);
+    tsqr_f.alloc_zero(static_cast<size_t>(tsqr_workspace_elems<double, float>(n, m)), s);
   rw.alloc(static_cast<size_t>(std::max<int64_t>(resid_workspace_elems(n, m), kNumSMs * 2) + 4 * m + 8), s);
   theta.alloc(static_cast<size_t>(smax), s);
   theta_prev.alloc(static_cast<size_t>(smax), s);

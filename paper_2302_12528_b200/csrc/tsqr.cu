@@ -230,7 +230,8 @@ __global__ void k_tsqr_finish(int m, const Tq* __restrict__ Rin, Tq* __restrict_
 // reductions, fp64 scalars), published through a double-buffered shared
 // vector, and applied by every warp to its own columns with one barrier per
 // step.  Leaves factor row blocks of W; the last leaf of each group of G
-// (atomic counter, self-resetting) stacks the G leaf R factors into its tile
+// (atomic counter; the workspace starts zeroed and each counter is reset
+// by the CTA that consumes it) stacks the G leaf R factors into its tile
 // and factors them again, and so on up to the root, which also applies the
 // positive-diagonal and rank checks of k_tsqr_finish.
 // ---------------------------------------------------------------------------
@@ -519,7 +520,6 @@ void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr,
   if (rk && tsqr_reg_enabled()) {
     ProfScope prof("tsqr", s, double(sizeof(Tin)) * n * m, 2.0 * n * m * m);
     int* ctr = reinterpret_cast<int*>(work + rp.r_elems);
-    if (rp.n_ctr) MPB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int) * rp.n_ctr, s));
     rk<<<static_cast<unsigned>(rp.nleaf), rp.cfg.nw * 32, 0, s>>>(
         n, mi, W, ldw, work, ctr, rp.nleaf, static_cast<int>(rp.G), R, ldr, status,
         sizeof(Tin) == sizeof(Tq));

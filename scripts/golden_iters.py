@@ -1,0 +1,37 @@
+"""Iteration counts of the GPU solver on every golden case vs the reference
+(and the reference's own FMA-rounding spread).  GPU box helper:
+
+    python scripts/golden_iters.py [name-substring ...]
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
+
+import paper_2302_12528_b200 as mp  # noqa: E402
+from conftest import load_golden  # noqa: E402
+from test_gpu_solver import iteration_band, make_op, sensitivity  # noqa: E402
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+names = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and f != "pcg64.npz")
+flt = sys.argv[1:]
+for name in names:
+    if flt and not any(s in name for s in flt):
+        continue
+    g = load_golden(name)
+    kw = eval(str(g["kw"]))
+    cfg = mp.SolverConfig(variant=str(g["variant"]), **kw)
+    r = mp.solve(make_op(mp, name), cfg)
+    ref = (int(g["iters_lower"]), int(g["iters_working"]))
+    tot = sum(ref)
+    sens = sensitivity(name) or {}
+    fma = (sens.get("fma_iters_lower"), sens.get("fma_iters_working"))
+    got = (r.iterations_lower, r.iterations_working)
+    rel = float(np.max(np.abs(r.theta - g["theta"]) / np.abs(g["theta"])))
+    band = iteration_band(name, tot)
+    ok = abs(sum(got) - tot) <= band
+    print(f"{name:28s} ref {ref[0]:5d}+{ref[1]:5d}  fma {fma}  gpu {got[0]:5d}+{got[1]:5d}  "
+          f"d={sum(got) - tot:+5d} band {band:4d} {'ok' if ok else 'OUT'}  theta {rel:.1e}", flush=True)

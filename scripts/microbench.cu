@@ -341,6 +341,7 @@ int main(int argc, char** argv) {
       CK(cudaMemset(AS, 0, n * k * 8));
       const int64_t gw = gram_workspace_elems<double>(n, k, k);
       CK(cudaMalloc(&work, gw * 8 + 64));
+      CK(cudaMemset(work, 0, gw * 8 + 64));
       char name[96];
       double ms = time_ms([&] { gram<double>(n, k, S, n, k, AS, n, G, k, 1, work, s); }, 5, s);
       snprintf(name, sizeof name, "gram S^T AS %s", sh.tag);
@@ -348,6 +349,18 @@ int main(int argc, char** argv) {
       ms = time_ms([&] { gram<double>(n, 2 * m, S, n, m, S + 2 * m * n, n, G, 2 * m, 0, work, s); }, 5, s);
       snprintf(name, sizeof name, "gram B^T W (2m x m) %s", sh.tag);
       report(name, ms, 3.0 * n * m * 8, 2.0 * n * 2 * m * m);
+      {
+        float* wf;
+        const int64_t gwf = gram_workspace_elems<float>(n, k, k);
+        CK(cudaMalloc(&wf, gwf * 4 + 64));
+        CK(cudaMemset(wf, 0, gwf * 4 + 64));
+        const float* Sf = reinterpret_cast<const float*>(S);
+        const float* ASf = reinterpret_cast<const float*>(AS);
+        ms = time_ms([&] { gram<float>(n, k, Sf, n, k, ASf, n, reinterpret_cast<float*>(G), k, 1, wf, s); }, 5, s);
+        snprintf(name, sizeof name, "gram<float> S^T AS %s", sh.tag);
+        report(name, ms, 2.0 * n * k * 4, 2.0 * n * k * k);
+        CK(cudaFree(wf));
+      }
       ms = time_ms([&] { gemm_tn<double>(n, k, 2 * m, 1.0, S, n, G, k, 0.0, nullptr, 0, Y, n, s); }, 5, s);
       snprintf(name, sizeof name, "gemm S C (s -> 2m) %s", sh.tag);
       report(name, ms, (double)(n * k + n * 2 * m) * 8, 2.0 * n * k * 2 * m);
@@ -369,6 +382,7 @@ int main(int argc, char** argv) {
       float* tw;
       const int64_t tws = tsqr_workspace_elems<double, float>(n, m);
       CK(cudaMalloc(&tw, tws * 4 + 64));
+      CK(cudaMemset(tw, 0, tws * 4 + 64));
       float* Rf;
       CK(cudaMalloc(&Rf, m * m * 4));
       ms = time_ms([&] { tsqr_r<double, float>(n, m, S, n, Rf, m, tw, st, s); }, 5, s);
@@ -377,6 +391,7 @@ int main(int argc, char** argv) {
       double* tw64;
       const int64_t tws64 = tsqr_workspace_elems<double, double>(n, m);
       CK(cudaMalloc(&tw64, tws64 * 8 + 64));
+      CK(cudaMemset(tw64, 0, tws64 * 8 + 64));
       ms = time_ms([&] { tsqr_r<double, double>(n, m, S, n, Rt, m, tw64, st, s); }, 5, s);
       snprintf(name, sizeof name, "tsqr fp64 %s", sh.tag);
       report(name, ms, (double)n * m * 8, 2.0 * n * m * m);
