@@ -1,13 +1,15 @@
 // small.cu -- single-CTA kernels for the small (<= 3m x 3m) dense steps.
 //
-// These run once or twice per iteration on matrices of order <= 576.  They
-// are latency-bound, so each stages its matrices in shared memory (global
-// scratch only when they do not fit) and keeps the reference's sequential
-// inner-product order with separately rounded operations: for identical
-// inputs they reproduce the reference's small factorizations
-// (dense_cholesky, dense_kernels.hpp:128-152; householder_qr_square,
-// ortho.hpp:30-121; matmul :20-34) bit for bit.
+// These run once or twice per iteration on matrices of order <= 576 and are
+// latency-bound: each stages its matrices in shared memory (global scratch
+// only when they do not fit) and spreads every step over the CTA (warp
+// reductions, trailing updates in parallel) so that the serial chain is one
+// barrier and one scalar op (sqrt / reciprocal) per column.  They follow the
+// reference's small factorizations step for step (dense_cholesky,
+// dense_kernels.hpp:128-152; householder_qr_square, ortho.hpp:30-121;
+// matmul :20-34); sums are formed in parallel, so results agree to rounding.
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -33,27 +35,36 @@ __global__ void k_symmetrize(int64_t s, T* G, int64_t ldg) {
   }
 }
 
-// Left-looking Cholesky G = L L^T: column j after columns < j, rows of a
-// column in parallel; then Uinv = L^{-T} by forward substitution (thread per
-// column of L^{-1}).  status = {code, index}, first error wins.
+template <typename T>
+__device__ __forceinline__ T warp_sum_s(T v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// Right-looking Cholesky G = L L^T (dense_cholesky, dense_kernels.hpp:128-152)
+// with the trailing update spread over the CTA, then Uinv = L^{-T}: L^{-1}
+// by forward substitution, one thread per column.  status = {code, index},
+// first error wins.
 template <typename T>
 __global__ void __launch_bounds__(kSmallThreads)
 k_cholesky_inv(int m, const T* __restrict__ G, int64_t ldg, T* __restrict__ L,
                T* __restrict__ Uinv, int* status, int use_smem) {
   extern __shared__ __align__(16) unsigned char raw[];
-  T* Ls = use_smem ? reinterpret_cast<T*>(raw) : L;
-  T* Us = use_smem ? Ls + m * m : Uinv;
+  T* As = use_smem ? reinterpret_cast<T*>(raw) : L;  // working lower triangle -> L
+  T* Us = use_smem ? As + m * m : Uinv;
   __shared__ int fail;
-  if (threadIdx.x == 0) fail = 0;
-  for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) Ls[idx] = T(0);
+  __shared__ T sh_rd;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) fail = 0;
+  for (int idx = tid; idx < m * m; idx += nt) {
+    const int i = idx % m, j = idx / m;
+    As[idx] = i >= j ? G[i + static_cast<int64_t>(j) * ldg] : T(0);
+  }
   __syncthreads();
   for (int j = 0; j < m; ++j) {
-    if (threadIdx.x == 0) {
-      T s = G[j + static_cast<int64_t>(j) * ldg];
-      for (int k = 0; k < j; ++k) {
-        const T ljk = Ls[j + k * m];
-        s = sub_rn(s, mul_rn(ljk, ljk));
-      }
+    if (tid == 0) {
+      const T s = As[j + j * m];
       if (!isfinite(static_cast<double>(s))) {
         fail = 1;
         if (status[0] == 0) {
@@ -67,38 +78,54 @@ k_cholesky_inv(int m, const T* __restrict__ G, int64_t ldg, T* __restrict__ L,
           status[1] = j;
         }
       } else {
-        Ls[j + j * m] = sqrt(s);
+        const T d = sqrt(s);
+        As[j + j * m] = d;
+        sh_rd = T(1) / d;
       }
     }
     __syncthreads();
     if (fail) return;
-    const T djj = Ls[j + j * m];
-    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) {
-      T s = G[i + static_cast<int64_t>(j) * ldg];
-      for (int k = 0; k < j; ++k) s = sub_rn(s, mul_rn(Ls[i + k * m], Ls[j + k * m]));
-      Ls[i + j * m] = s / djj;
+    const T rd = sh_rd;
+    // trailing lower triangle (i >= k > j): A(i,k) -= A(i,j) A(k,j) / d^2;
+    // column j is scaled after (it is read here)
+    const int len = m - j - 1;
+    for (int idx = tid; idx < len * len; idx += nt) {
+      const int i = j + 1 + idx % len, k = j + 1 + idx / len;
+      if (i >= k) As[i + k * m] = fma(-(As[i + j * m] * rd), As[k + j * m] * rd, As[i + k * m]);
     }
+    __syncthreads();
+    for (int i = j + 1 + tid; i < m; i += nt) As[i + j * m] *= rd;
     __syncthreads();
   }
   if (Uinv) {
-    for (int c = threadIdx.x; c < m; c += blockDim.x) {
-      for (int k = 0; k < m; ++k) Us[c + k * m] = T(0);
-      for (int k = c; k < m; ++k) {
-        T s = (k == c) ? T(1) : T(0);
-        for (int l = c; l < k; ++l) s = sub_rn(s, mul_rn(Ls[k + l * m], Us[c + l * m]));
-        Us[c + k * m] = s / Ls[k + k * m];
+    // X = L^{-1} (lower), column c by thread c; Uinv = X^T (upper)
+    for (int c = tid; c < m; c += nt) {
+      for (int k = 0; k < c; ++k) Us[c + k * m] = T(0);
+      const T xc = T(1) / As[c + c * m];
+      Us[c + c * m] = xc;  // Us(c, k) holds X(k, c)
+      for (int k = c + 1; k < m; ++k) {
+        T s0 = T(0), s1 = T(0);
+        int l = c;
+        for (; l + 1 < k; l += 2) {
+          s0 = fma(As[k + l * m], Us[c + l * m], s0);
+          s1 = fma(As[k + (l + 1) * m], Us[c + (l + 1) * m], s1);
+        }
+        if (l < k) s0 = fma(As[k + l * m], Us[c + l * m], s0);
+        Us[c + k * m] = -(s0 + s1) / As[k + k * m];
       }
     }
   }
   if (use_smem) {
     __syncthreads();
-    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-      L[idx] = Ls[idx];
+    for (int idx = tid; idx < m * m; idx += nt) {
+      L[idx] = As[idx];
       if (Uinv) Uinv[idx] = Us[idx];
     }
   }
 }
 
+// R^{-1} of an upper-triangular R: column c of R^{-1} by thread c (back
+// substitution).  A zero or subnormal pivot is SingularTriangular.
 template <typename T>
 __global__ void __launch_bounds__(kSmallThreads)
 k_upper_inverse(int m, const T* __restrict__ R, int64_t ldr, T* __restrict__ Rinv, int* status,
@@ -106,41 +133,53 @@ k_upper_inverse(int m, const T* __restrict__ R, int64_t ldr, T* __restrict__ Rin
   extern __shared__ __align__(16) unsigned char raw[];
   T* Rs = reinterpret_cast<T*>(raw);
   T* Is = use_smem ? Rs + m * m : Rinv;
+  T* rdiag = use_smem ? Is + m * m : nullptr;
   __shared__ int fail;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) fail = 0;
+  __syncthreads();
+  const T tiny = sizeof(T) == 8 ? T(DBL_MIN) : T(FLT_MIN);
   if (use_smem)
-    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x)
-      Rs[idx] = R[(idx % m) + static_cast<int64_t>(idx / m) * ldr];
-  if (threadIdx.x == 0) {
-    fail = 0;
-    const T tiny = sizeof(T) == 8 ? T(DBL_MIN) : T(FLT_MIN);
-    for (int j = 0; j < m; ++j) {
-      const T a = fabs(R[j + static_cast<int64_t>(j) * ldr]);
-      if (a == T(0) || a < tiny) {
-        fail = 1;
-        if (status[0] == 0) {
-          status[0] = MPEIG_E_SINGULAR_TRI;
-          status[1] = j;
-        }
-        break;
-      }
-    }
+    for (int idx = tid; idx < m * m; idx += nt) Rs[idx] = R[(idx % m) + static_cast<int64_t>(idx / m) * ldr];
+  for (int j = tid; j < m; j += nt) {
+    const T a = R[j + static_cast<int64_t>(j) * ldr];
+    if (fabs(a) == T(0) || fabs(a) < tiny) fail = 1;
+    if (rdiag) rdiag[j] = T(1) / a;
   }
   __syncthreads();
-  if (fail) return;
+  if (fail) {
+    if (tid == 0 && status[0] == 0) {
+      for (int j = 0; j < m; ++j) {
+        const T a = fabs(R[j + static_cast<int64_t>(j) * ldr]);
+        if (a == T(0) || a < tiny) {
+          status[0] = MPEIG_E_SINGULAR_TRI;
+          status[1] = j;
+          break;
+        }
+      }
+    }
+    return;
+  }
   const T* Rr = use_smem ? Rs : R;
   const int64_t ld = use_smem ? m : ldr;
-  for (int c = threadIdx.x; c < m; c += blockDim.x) {
+  for (int c = tid; c < m; c += nt) {
     for (int k = c + 1; k < m; ++k) Is[k + c * m] = T(0);
-    Is[c + c * m] = T(1) / Rr[c + c * ld];
+    const T rc = rdiag ? rdiag[c] : T(1) / Rr[c + c * ld];
+    Is[c + c * m] = rc;
     for (int k = c - 1; k >= 0; --k) {
-      T s = T(0);
-      for (int l = k + 1; l <= c; ++l) s = add_rn(s, mul_rn(Rr[k + l * ld], Is[l + c * m]));
-      Is[k + c * m] = -s / Rr[k + k * ld];
+      T s0 = T(0), s1 = T(0);
+      int l = k + 1;
+      for (; l + 1 <= c; l += 2) {
+        s0 = fma(Rr[k + l * ld], Is[l + c * m], s0);
+        s1 = fma(Rr[k + (l + 1) * ld], Is[l + 1 + c * m], s1);
+      }
+      if (l <= c) s0 = fma(Rr[k + l * ld], Is[l + c * m], s0);
+      Is[k + c * m] = -(s0 + s1) * (rdiag ? rdiag[k] : T(1) / Rr[k + k * ld]);
     }
   }
   if (use_smem) {
     __syncthreads();
-    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) Rinv[idx] = Is[idx];
+    for (int idx = tid; idx < m * m; idx += nt) Rinv[idx] = Is[idx];
   }
 }
 
@@ -202,51 +241,48 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
     M[a + b * p] = C[b + static_cast<int64_t>(m + a) * ldc];
   }
   __syncthreads();
-  // householder_reduce (ortho.hpp:30-76) on the p x m block, steps = p
+  // householder_reduce (ortho.hpp:30-76) on the p x m block, steps = p;
+  // warp 0 forms each reflector, the 8 warps apply it (a column per warp,
+  // rows over lanes)
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   for (int j = 0; j < p; ++j) {
     const int len = p - j;
-    if (tid == 0) {
-      double nrm2 = 0.0;
-      for (int i = j; i < p; ++i) {
-        const double a = fabs(static_cast<double>(M[i + j * p]));
-        nrm2 = add_rn(nrm2, mul_rn(a, a));
+    if (warp == 0) {
+      double part = 0.0;
+      for (int i = j + 1 + lane; i < p; i += 32) {
+        const double a = static_cast<double>(M[i + j * p]);
+        part = fma(a, a, part);
       }
-      const double nrm = sqrt(nrm2);
+      const double tail = warp_sum_s(part);
+      const double x0 = static_cast<double>(M[j + j * p]);
+      const double nrm = sqrt(fma(x0, x0, tail));
       if (nrm == 0.0) {
-        fb = 1;
+        if (lane == 0) fb = 1;
       } else {
-        const double x0 = static_cast<double>(M[j + j * p]);
-        const double ax0 = fabs(x0);
-        const double phase = ax0 > 0.0 ? x0 / ax0 : 1.0;
+        const double phase = x0 > 0.0 ? 1.0 : (x0 < 0.0 ? -1.0 : 1.0);
+        const double v0 = x0 + phase * nrm;
         T* v = V + j * p + j;
-        v[0] = static_cast<T>(add_rn(x0, mul_rn(phase, nrm)));
-        for (int i = 1; i < len; ++i) v[i] = M[j + i + j * p];
-        double vn2 = 0.0;
-        for (int i = 0; i < len; ++i) {
-          const double a = fabs(static_cast<double>(v[i]));
-          vn2 = add_rn(vn2, mul_rn(a, a));
+        for (int i = lane; i < len; i += 32) v[i] = i == 0 ? static_cast<T>(v0) : M[j + i + j * p];
+        if (lane == 0) {
+          sh_beta = 2.0 / fma(v0, v0, tail);
+          beta[j] = sh_beta;
+          sh_diag = static_cast<T>(-phase * nrm);  // R(j,j) after the reflection (ortho.hpp:72)
         }
-        sh_beta = 2.0 / vn2;
-        beta[j] = sh_beta;
-        sh_diag = static_cast<T>(-phase * nrm);  // R(j,j) after the reflection (ortho.hpp:72)
       }
     }
     __syncthreads();
     if (fb) break;
     const double b = sh_beta;
     const T* v = V + j * p + j;
-    for (int c = j + tid; c < m; c += nt) {
+    for (int c = j + 1 + warp; c < m; c += nw) {
       T* col = M + c * p + j;
-      T sdot = T(0);
-      for (int i = 0; i < len; ++i) sdot = add_rn(sdot, mul_rn(v[i], col[i]));
-      sdot = static_cast<T>(mul_rn(static_cast<double>(sdot), b));
-      for (int i = 0; i < len; ++i) col[i] = sub_rn(col[i], mul_rn(sdot, v[i]));
+      T part = T(0);
+      for (int i = lane; i < len; i += 32) part = fma(v[i], col[i], part);
+      const T f = static_cast<T>(static_cast<double>(warp_sum_s(part)) * b);
+      for (int i = lane; i < len; i += 32) col[i] = fma(-f, v[i], col[i]);
     }
-    __syncthreads();
-    if (tid == 0) {
-      M[j + j * p] = sh_diag;
-      for (int i = j + 1; i < p; ++i) M[i + j * p] = T(0);
-    }
+    if (warp == 0)
+      for (int i = j + lane; i < p; i += 32) M[i + j * p] = i == j ? sh_diag : T(0);
     __syncthreads();
   }
   if (!fb) {
@@ -257,12 +293,12 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
       const int len = p - jj;
       const T* v = V + jj * p + jj;
       const double b = beta[jj];
-      for (int c = tid; c < p; c += nt) {
-        T* qc = Q + c * p + (p - len);
-        T sdot = T(0);
-        for (int i = 0; i < len; ++i) sdot = add_rn(sdot, mul_rn(v[i], qc[i]));
-        sdot = static_cast<T>(mul_rn(static_cast<double>(sdot), b));
-        for (int i = 0; i < len; ++i) qc[i] = sub_rn(qc[i], mul_rn(sdot, v[i]));
+      for (int c = warp; c < p; c += nw) {
+        T* qc = Q + c * p + jj;
+        T part = T(0);
+        for (int i = lane; i < len; i += 32) part = fma(v[i], qc[i], part);
+        const T f = static_cast<T>(static_cast<double>(warp_sum_s(part)) * b);
+        for (int i = lane; i < len; i += 32) qc[i] = fma(-f, v[i], qc[i]);
       }
       __syncthreads();
     }
@@ -288,13 +324,242 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
     if (fb) {
       acc = C[i + static_cast<int64_t>(m + j) * ldc];
     } else {
-      // matmul(cp, Q): ascending l, separately rounded (dense_kernels.hpp:20-34)
-      acc = T(0);
-      for (int l = 0; l < p; ++l)
-        acc = add_rn(acc, mul_rn(C[i + static_cast<int64_t>(m + l) * ldc], Q[l + j * p]));
+      // matmul(cp, Q) (dense_kernels.hpp:20-34)
+      T a0 = T(0), a1 = T(0);
+      int l = 0;
+      for (; l + 1 < p; l += 2) {
+        a0 = fma(C[i + static_cast<int64_t>(m + l) * ldc], Q[l + j * p], a0);
+        a1 = fma(C[i + static_cast<int64_t>(m + l + 1) * ldc], Q[l + 1 + j * p], a1);
+      }
+      if (l < p) a0 = fma(C[i + static_cast<int64_t>(m + l) * ldc], Q[l + j * p], a0);
+      acc = a0 + a1;
     }
     coef[i + static_cast<int64_t>(m + j) * s] = acc;
   }
+}
+
+// ---- one-warp forms for m <= 32 ---------------------------------------------
+// Lane i holds row i in registers; the per-column serial chain is a shuffle
+// broadcast and one sqrt / reciprocal, with no CTA barrier at all.
+
+// G = L L^T and Uinv = L^{-T} (dense_cholesky, dense_kernels.hpp:128-152)
+template <typename T, int MAXM>
+__global__ void __launch_bounds__(32)
+k_cholesky_inv_warp(int m, const T* __restrict__ G, int64_t ldg, T* __restrict__ L,
+                    T* __restrict__ Uinv, int* status) {
+  const int lane = threadIdx.x;
+  T a[MAXM];
+#pragma unroll
+  for (int j = 0; j < MAXM; ++j)
+    a[j] = (lane < m && j < m && lane >= j) ? G[lane + static_cast<int64_t>(j) * ldg] : T(0);
+#pragma unroll
+  for (int j = 0; j < MAXM; ++j) {
+    if (j >= m) break;
+    const T d2 = __shfl_sync(0xffffffffu, a[j], j);
+    if (!isfinite(static_cast<double>(d2)) || !(d2 > T(0))) {
+      if (lane == 0 && status[0] == 0) {
+        status[0] = isfinite(static_cast<double>(d2)) ? MPEIG_E_NOT_PD : MPEIG_E_OVERFLOW;
+        status[1] = j;
+      }
+      return;
+    }
+    const T d = sqrt(d2), rd = T(1) / d;
+    const T lij = lane > j ? a[j] * rd : (lane == j ? d : T(0));
+    a[j] = lij;
+#pragma unroll
+    for (int k = j + 1; k < MAXM; ++k) {
+      const T lkj = __shfl_sync(0xffffffffu, lij, k);
+      if (lane >= k) a[k] = fma(-lij, lkj, a[k]);
+    }
+  }
+  if (lane < m) {
+#pragma unroll
+    for (int j = 0; j < MAXM; ++j)
+      if (j < m) L[lane + j * m] = a[j];
+  }
+  if (!Uinv) return;
+  // X = L^{-1}: column c by lane c (forward substitution); Uinv(c, i) = X(i, c)
+  T x[MAXM];
+  const int c = lane;
+#pragma unroll
+  for (int i = 0; i < MAXM; ++i) {
+    if (i >= m) break;
+    T s = i == c ? T(1) : T(0);
+#pragma unroll
+    for (int l = 0; l < i; ++l) s = fma(-__shfl_sync(0xffffffffu, a[l], i), x[l], s);
+    const T dii = __shfl_sync(0xffffffffu, a[i], i);
+    x[i] = i >= c ? s / dii : T(0);
+  }
+  if (c < m) {
+#pragma unroll
+    for (int i = 0; i < MAXM; ++i)
+      if (i < m) Uinv[c + i * m] = x[i];
+  }
+}
+
+// R^{-1} of an upper-triangular R: column c by lane c (back substitution).
+template <typename T, int MAXM>
+__global__ void __launch_bounds__(32)
+k_upper_inverse_warp(int m, const T* __restrict__ R, int64_t ldr, T* __restrict__ Rinv,
+                     int* status) {
+  const int lane = threadIdx.x;
+  const T tiny = sizeof(T) == 8 ? T(DBL_MIN) : T(FLT_MIN);
+  T r[MAXM];  // row `lane` of R
+#pragma unroll
+  for (int l = 0; l < MAXM; ++l)
+    r[l] = (lane < m && l < m && l >= lane) ? R[lane + static_cast<int64_t>(l) * ldr] : T(0);
+  T rdl = T(0);
+#pragma unroll
+  for (int l = 0; l < MAXM; ++l)
+    if (l == lane) rdl = r[l];
+  const bool bad = lane < m && (fabs(rdl) == T(0) || fabs(rdl) < tiny);
+  const unsigned badm = __ballot_sync(0xffffffffu, bad);
+  if (badm) {
+    if (lane == 0 && status[0] == 0) {
+      status[0] = MPEIG_E_SINGULAR_TRI;
+      status[1] = __ffs(badm) - 1;
+    }
+    return;
+  }
+  const T rinv_l = lane < m ? T(1) / rdl : T(0);
+  T y[MAXM];
+  const int c = lane;
+#pragma unroll
+  for (int k = MAXM - 1; k >= 0; --k) {
+    y[k] = T(0);
+    if (k >= m) continue;
+    T s = k == c ? T(1) : T(0);
+#pragma unroll
+    for (int l = k + 1; l < MAXM; ++l) {
+      if (l >= m) break;
+      s = fma(-__shfl_sync(0xffffffffu, r[l], k), y[l], s);
+    }
+    const T rk = __shfl_sync(0xffffffffu, rinv_l, k);  // all lanes take part
+    y[k] = k <= c ? s * rk : T(0);
+  }
+  if (c < m) {
+#pragma unroll
+    for (int k = 0; k < MAXM; ++k)
+      if (k < m) Rinv[k + c * m] = y[k];
+  }
+}
+
+// Hetmaniuk-Lehoucq coefficients (hl_update, eigensolvers.hpp:148-174) for
+// m, p <= MAXM: warp 0 runs householder_qr_square of top^* with the rows in
+// lanes (reflector scalars in fp64), the CTA forms c_x and c_pv = C_p Q.
+template <typename T, int MAXM>
+__global__ void __launch_bounds__(kSmallThreads)
+k_hl_coeffs_warp(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __restrict__ coef,
+                 int* fallback) {
+  __shared__ T Qs[MAXM * MAXM];
+  __shared__ int fb;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int64_t idx = tid; idx < static_cast<int64_t>(s) * m; idx += nt) {
+    const int i = static_cast<int>(idx % s), j = static_cast<int>(idx / s);
+    coef[i + static_cast<int64_t>(j) * s] = C[i + static_cast<int64_t>(j) * ldc];
+  }
+  if (p == 0) return;
+  if (tid < 32) {
+    const int lane = tid;
+    // row `lane` of M = top^*: M(a, b) = C(b, m + a)
+    T mr[MAXM], v[MAXM], q[MAXM];
+    double beta[MAXM];
+#pragma unroll
+    for (int b = 0; b < MAXM; ++b)
+      mr[b] = (lane < p && b < m) ? C[b + static_cast<int64_t>(m + lane) * ldc] : T(0);
+    int bad = 0;
+#pragma unroll
+    for (int j = 0; j < MAXM; ++j) {
+      v[j] = T(0);
+      beta[j] = 0.0;
+      if (j >= p || bad) continue;
+      const double xl = static_cast<double>(mr[j]);
+      double tail = lane > j && lane < p ? xl * xl : 0.0;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) tail += __shfl_xor_sync(0xffffffffu, tail, off);
+      const double x0 = __shfl_sync(0xffffffffu, xl, j);
+      const double nrm = sqrt(fma(x0, x0, tail));
+      if (nrm == 0.0) {
+        bad = 1;
+        continue;
+      }
+      const double phase = x0 < 0.0 ? -1.0 : 1.0;
+      const double v0 = x0 + phase * nrm;
+      beta[j] = 2.0 / fma(v0, v0, tail);
+      v[j] = lane == j ? static_cast<T>(v0) : (lane > j && lane < p ? mr[j] : T(0));
+#pragma unroll
+      for (int c = j + 1; c < MAXM; ++c) {
+        if (c >= m) break;
+        T part = v[j] * mr[c];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+        const T f = static_cast<T>(static_cast<double>(part) * beta[j]);
+        mr[c] = fma(-f, v[j], mr[c]);
+      }
+      mr[j] = lane == j ? static_cast<T>(-phase * nrm) : (lane > j ? T(0) : mr[j]);
+    }
+    // Q = H_0 ... H_{p-1} applied to I last to first (ortho.hpp:78-92); row `lane`
+#pragma unroll
+    for (int c = 0; c < MAXM; ++c) q[c] = (c == lane && lane < p) ? T(1) : T(0);
+    if (!bad) {
+#pragma unroll
+      for (int jj = MAXM - 1; jj >= 0; --jj) {
+        if (jj >= p) continue;
+#pragma unroll
+        for (int c = 0; c < MAXM; ++c) {
+          if (c >= p) break;
+          T part = v[jj] * q[c];
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+          const T f = static_cast<T>(static_cast<double>(part) * beta[jj]);
+          q[c] = fma(-f, v[jj], q[c]);
+        }
+      }
+    }
+    // fix_diagonal_phases (ortho.hpp:95-110): column j of Q by sign(R(j,j))
+    T rjj = T(1);
+#pragma unroll
+    for (int j = 0; j < MAXM; ++j)
+      if (j == lane) rjj = mr[j];
+    const unsigned zero = __ballot_sync(0xffffffffu, lane < p && rjj == T(0));
+    if (zero) bad = 1;
+#pragma unroll
+    for (int j = 0; j < MAXM; ++j) {
+      const T sj = __shfl_sync(0xffffffffu, rjj, j);
+      if (lane < p && j < p) Qs[lane + j * MAXM] = sj < T(0) ? -q[j] : q[j];
+    }
+    if (lane == 0) {
+      fb = bad;
+      *fallback = bad;
+    }
+  }
+  __syncthreads();
+  const bool use_q = !fb;
+  for (int64_t idx = tid; idx < static_cast<int64_t>(s) * p; idx += nt) {
+    const int i = static_cast<int>(idx % s), j = static_cast<int>(idx / s);
+    T acc;
+    if (!use_q) {
+      acc = C[i + static_cast<int64_t>(m + j) * ldc];
+    } else {
+      T a0 = T(0), a1 = T(0);
+      int l = 0;
+      for (; l + 1 < p; l += 2) {
+        a0 = fma(C[i + static_cast<int64_t>(m + l) * ldc], Qs[l + j * MAXM], a0);
+        a1 = fma(C[i + static_cast<int64_t>(m + l + 1) * ldc], Qs[l + 1 + j * MAXM], a1);
+      }
+      if (l < p) a0 = fma(C[i + static_cast<int64_t>(m + l) * ldc], Qs[l + j * MAXM], a0);
+      acc = a0 + a1;
+    }
+    coef[i + static_cast<int64_t>(m + j) * s] = acc;
+  }
+}
+
+int warp_forms() {  // bitmask of the one-warp forms in use (1 chol, 2 trinv, 4 hl)
+  static const int v = [] {
+    const char* e = std::getenv("MPEIG_SMALL_WARP");
+    return e ? std::atoi(e) : 7;
+  }();
+  return v;
 }
 
 template <typename K>
@@ -309,6 +574,18 @@ void hl_coeffs_t(int64_t s, int64_t m, int64_t p, const T* C, int64_t ldc, T* co
                  int* fallback, cudaStream_t st) {
   ProfScope prof("hl_coeffs", st, 0, 0);
   if (p > kMaxHlP) throw Error(MPEIG_E_CONFIG, "hl_update: block size above 256 not supported");
+  if ((warp_forms() & 4) && m <= 16 && p <= 16) {
+    k_hl_coeffs_warp<T, 16><<<1, kSmallThreads, 0, st>>>(static_cast<int>(s), static_cast<int>(m),
+                                                        static_cast<int>(p), C, ldc, coef, fallback);
+    MPB_LAUNCH_CHECK();
+    return;
+  }
+  if ((warp_forms() & 4) && sizeof(T) == 4 && m <= 32 && p <= 32) {
+    k_hl_coeffs_warp<T, 32><<<1, kSmallThreads, 0, st>>>(static_cast<int>(s), static_cast<int>(m),
+                                                        static_cast<int>(p), C, ldc, coef, fallback);
+    MPB_LAUNCH_CHECK();
+    return;
+  }
   const size_t bytes = static_cast<size_t>(p * m + 2 * p * p + p) * sizeof(T);
   const int use = bytes <= kSmemCap;
   if (use) allow_smem(k_hl_coeffs<T>, bytes);
@@ -333,6 +610,14 @@ void small_cholesky_inv(int64_t m, const T* G, int64_t ldg, T* L, T* Uinv, int* 
                         cudaStream_t st) {
   if (m <= 0) return;
   ProfScope prof("small_chol", st, 0, 0);
+  if ((warp_forms() & 1) && (m <= 16 || (sizeof(T) == 4 && m <= 32))) {
+    if (m <= 16)
+      k_cholesky_inv_warp<T, 16><<<1, 32, 0, st>>>(static_cast<int>(m), G, ldg, L, Uinv, status);
+    else
+      k_cholesky_inv_warp<T, 32><<<1, 32, 0, st>>>(static_cast<int>(m), G, ldg, L, Uinv, status);
+    MPB_LAUNCH_CHECK();
+    return;
+  }
   const size_t bytes = static_cast<size_t>(2 * m * m) * sizeof(T);
   const int use = bytes <= kSmemCap;
   if (use) allow_smem(k_cholesky_inv<T>, bytes);
@@ -346,7 +631,15 @@ void small_upper_inverse(int64_t m, const T* R, int64_t ldr, T* Rinv, int* statu
                          cudaStream_t st) {
   if (m <= 0) return;
   ProfScope prof("small_trinv", st, 0, 0);
-  const size_t bytes = static_cast<size_t>(2 * m * m) * sizeof(T);
+  if ((warp_forms() & 2) && (m <= 16 || (sizeof(T) == 4 && m <= 32))) {
+    if (m <= 16)
+      k_upper_inverse_warp<T, 16><<<1, 32, 0, st>>>(static_cast<int>(m), R, ldr, Rinv, status);
+    else
+      k_upper_inverse_warp<T, 32><<<1, 32, 0, st>>>(static_cast<int>(m), R, ldr, Rinv, status);
+    MPB_LAUNCH_CHECK();
+    return;
+  }
+  const size_t bytes = static_cast<size_t>(2 * m * m + m) * sizeof(T);
   const int use = bytes <= kSmemCap;
   if (use) allow_smem(k_upper_inverse<T>, bytes);
   k_upper_inverse<T><<<1, kSmallThreads, use ? bytes : 0, st>>>(static_cast<int>(m), R, ldr, Rinv,

@@ -255,63 +255,55 @@ struct RegTile {
       const int buf = j & 1;
       if (warp == (j % NW)) {
         const int qj = j / NW;
-        Tq x[RPL];
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-          x[i] = Tq(0);
+        for (int q = 0; q < MPW; ++q) {
+          if (q != qj) continue;  // compile-time q: the tile stays in registers
+          // 4 independent partial sums: the reduction is on the serial path
+          double tp[4] = {0.0, 0.0, 0.0, 0.0}, xj = 0.0;
 #pragma unroll
-          for (int q = 0; q < MPW; ++q)
-            if (q == qj) x[i] = a[q][i];
+          for (int i = 0; i < RPL; ++i) {
+            const int r = lane + 32 * i;
+            const double v = static_cast<double>(a[q][i]);
+            if (r > j) tp[i & 3] = fma(v, v, tp[i & 3]);
+            if (r == j) xj = v;
+          }
+          double tail = xor_sum((tp[0] + tp[1]) + (tp[2] + tp[3]));
+          const double x0 = __shfl_sync(0xffffffffu, xj, j & 31);
+          const double nrm = sqrt(fma(x0, x0, tail));
+          double beta = 0.0, diag = 0.0, v0 = 0.0;
+          if (nrm != 0.0) {
+            const double phase = x0 >= 0.0 ? 1.0 : -1.0;
+            v0 = x0 + phase * nrm;
+            beta = 2.0 / fma(v0, v0, tail);
+            diag = -phase * nrm;
+          }
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            const int r = lane + 32 * i;
+            vbuf[buf][r] = r < j ? Tq(0) : (r == j ? static_cast<Tq>(v0) : a[q][i]);
+            a[q][i] = r < j ? a[q][i] : (r == j ? static_cast<Tq>(diag) : Tq(0));
+          }
+          if (lane == 0) sbeta[buf] = beta;
         }
-        double tail = 0.0, xj = 0.0;
-#pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-          const int r = lane + 32 * i;
-          const double v = static_cast<double>(x[i]);
-          if (r > j) tail = fma(v, v, tail);
-          if (r == j) xj = v;
-        }
-        tail = xor_sum(tail);
-        const double x0 = __shfl_sync(0xffffffffu, xj, j & 31);
-        const double nrm = sqrt(fma(x0, x0, tail));
-        double beta = 0.0, diag = 0.0, v0 = 0.0;
-        if (nrm != 0.0) {
-          const double phase = x0 >= 0.0 ? 1.0 : -1.0;
-          v0 = x0 + phase * nrm;
-          beta = 2.0 / fma(v0, v0, tail);
-          diag = -phase * nrm;
-        }
-#pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-          const int r = lane + 32 * i;
-          vbuf[buf][r] = r < j ? Tq(0) : (r == j ? static_cast<Tq>(v0) : x[i]);
-          const Tq nv = r < j ? x[i] : (r == j ? static_cast<Tq>(diag) : Tq(0));
-#pragma unroll
-          for (int q = 0; q < MPW; ++q)
-            if (q == qj) a[q][i] = nv;
-        }
-        if (lane == 0) sbeta[buf] = beta;
       }
       __syncthreads();
       const double beta = sbeta[buf];
       if (beta == 0.0) continue;
-      Tq v[RPL];
-#pragma unroll
-      for (int i = 0; i < RPL; ++i) v[i] = vbuf[buf][lane + 32 * i];
+      const Tq* v = vbuf[buf] + lane;
       const int i0 = j >> 5;  // row blocks above j hold zeros of v
 #pragma unroll
       for (int q = 0; q < MPW; ++q) {
         const int c = warp + NW * q;
         if (c > j && c < m) {
-          Tq s = Tq(0);
+          Tq sp[4] = {Tq(0), Tq(0), Tq(0), Tq(0)};
 #pragma unroll
           for (int i = 0; i < RPL; ++i)
-            if (i >= i0) s = fma(v[i], a[q][i], s);
-          s = xor_sum(s);
-          const Tq f = static_cast<Tq>(static_cast<double>(s) * beta);
+            if (i >= i0) sp[i & 3] = fma(v[32 * i], a[q][i], sp[i & 3]);
+          const Tq sacc = xor_sum((sp[0] + sp[1]) + (sp[2] + sp[3]));
+          const Tq f = static_cast<Tq>(static_cast<double>(sacc) * beta);
 #pragma unroll
           for (int i = 0; i < RPL; ++i)
-            if (i >= i0) a[q][i] = fma(-f, v[i], a[q][i]);
+            if (i >= i0) a[q][i] = fma(-f, v[32 * i], a[q][i]);
         }
       }
     }
@@ -432,17 +424,25 @@ struct RegCfg {
 // at least two R factors; the register tile stays <= 96 32-bit registers.
 template <typename Tq>
 RegCfg reg_cfg(int64_t m) {
+  static const int rpl16 = [] {
+    const char* e = std::getenv("MPEIG_TSQR_RPL16");  // tuning experiments only
+    return e ? std::atoi(e) : 0;
+  }();
+  if (m <= 16 && (rpl16 == 8 || rpl16 == 16 || (rpl16 == 32 && sizeof(Tq) == 4))) return {16, rpl16, 1};
+  // The per-column step is a latency chain (two warp reductions, sqrt, a
+  // barrier), so the tree is kept shallow: tall tiles (b = 32*RPL rows) and
+  // wide fan-in G = b/m.  One column per warp where m allows.
   if (sizeof(Tq) == 4) {
-    if (m <= 16) return {8, 4, 2};
-    if (m <= 32) return {8, 8, 4};
-    if (m <= 48) return {8, 8, 6};
-    if (m <= 64) return {8, 8, 8};
+    if (m <= 16) return {16, 8, 1};
+    if (m <= 32) return {16, 16, 2};
+    if (m <= 48) return {16, 16, 3};
+    if (m <= 64) return {16, 16, 4};
     if (m <= 96) return {16, 8, 6};
     if (m <= 128) return {16, 8, 8};
   } else {
-    if (m <= 16) return {8, 4, 2};
-    if (m <= 32) return {8, 8, 4};
-    if (m <= 48) return {8, 8, 6};
+    if (m <= 16) return {16, 8, 1};
+    if (m <= 32) return {16, 16, 2};
+    if (m <= 48) return {16, 8, 3};
     if (m <= 64) return {16, 8, 4};
     if (m <= 96) return {16, 6, 6};
   }
@@ -458,10 +458,12 @@ RegKernel<Tin, Tq> reg_kernel(const RegCfg& c) {
 #define MPB_REG(NW, RPL, MPW) \
   if (c.nw == NW && c.rpl == RPL && c.mpw == MPW) return k_tsqr_reg<Tin, Tq, NW, RPL, MPW>;
   if constexpr (sizeof(Tq) == 4) {
-    MPB_REG(8, 4, 2) MPB_REG(8, 8, 4) MPB_REG(8, 8, 6) MPB_REG(8, 8, 8) MPB_REG(16, 8, 6)
+    MPB_REG(16, 32, 1) MPB_REG(16, 16, 1) MPB_REG(16, 8, 1) MPB_REG(16, 16, 2) MPB_REG(16, 16, 3)
+    MPB_REG(16, 16, 4) MPB_REG(16, 8, 6)
     MPB_REG(16, 8, 8)
   } else {
-    MPB_REG(8, 4, 2) MPB_REG(8, 8, 4) MPB_REG(8, 8, 6) MPB_REG(16, 8, 4) MPB_REG(16, 6, 6)
+    MPB_REG(16, 16, 1) MPB_REG(16, 8, 1) MPB_REG(16, 16, 2) MPB_REG(16, 8, 3) MPB_REG(16, 8, 4)
+    MPB_REG(16, 6, 6)
   }
 #undef MPB_REG
   return nullptr;
