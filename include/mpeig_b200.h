@@ -142,8 +142,11 @@ void* mpeig_ctx_stream(mpeig_ctx* ctx);
  *   "spec_mode"   1 (default): one host sync per iteration, breakdowns rolled
  *                 back to the careful path; 0: eager, one sync per decision
  *   "use_graphs"  1 (default): replay the steady-state iteration as a CUDA graph
- *   "eig_backend" 0 (default): one-CTA syev for 3m <= 96, cuSOLVER above;
- *                 1: cuSOLVER syevd always (different rounding) */
+ *   "eig_backend" 0 (default): one-CTA tridiagonal + QL eigensolver (the
+ *                 reference's algorithm) for 3m <= 96, cuSOLVER syevd above;
+ *                 1: cuSOLVER syevd always; 2: cuSOLVER syevj (diagnostic)
+ *   "syev_method", "ql_exact": eigensolver variants for experiments
+ *                 (process-wide; default 0) */
 int mpeig_ctx_set_option(mpeig_ctx* ctx, const char* key, int value);
 
 /* ------------------------------------------------------------ operators */

@@ -819,9 +819,14 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
     const void* S;
     int64_t p;
   };
-  std::vector<std::pair<GraphKey, cudaGraphExec_t>> graphs;
+  struct CachedGraph {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    int64_t kernels;  // library kernels per replay (counted into g_launches)
+  };
+  std::vector<CachedGraph> graphs;
   auto cleanup = [&] {
-    for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     graphs.clear();
   };
 
@@ -874,11 +879,16 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
       // ---- speculative body (graph in the steady state)
       cudaGraphExec_t exec = nullptr;
       if (use_graphs && p == m) {
+        int64_t nk = 0;
         for (auto& g : graphs)
-          if (g.first.S == w.S.p && g.first.p == p) exec = g.second;
+          if (g.key.S == w.S.p && g.key.p == p) {
+            exec = g.exec;
+            nk = g.kernels;
+          }
         if (!exec) {
           cudaGraph_t graph;
           ev.on = false;
+          const int64_t c0 = g_launches.load();
           MPB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
           try {
             spec_body<T>(w, A, T_op, p, mixed, w.S.p, w.AS.p, w.S2.p, w.AS2.p, ev);
@@ -889,10 +899,14 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
           MPB_CUDA(cudaStreamEndCapture(s, &graph));
           MPB_CUDA(cudaGraphInstantiate(&exec, graph, 0));
           cudaGraphDestroy(graph);
-          graphs.push_back({{w.S.p, p}, exec});
+          // capture records launches without running them: count them per replay
+          nk = g_launches.load() - c0;
+          g_launches.fetch_sub(nk);
+          graphs.push_back({{w.S.p, p}, exec, nk});
         }
         MPB_CUDA(cudaEventRecord(ev.e[0], s));
         MPB_CUDA(cudaGraphLaunch(exec, s));
+        g_launches.fetch_add(nk);
         MPB_CUDA(cudaEventRecord(ev.e[3], s));
         MPB_CUDA(cudaStreamSynchronize(s));
         tm.projected_eig += ev.ms(0, 3) * 1e-3;  // whole body (no phase split in a graph)
