@@ -130,6 +130,7 @@ template <typename T>
 void small_syev_prof(int64_t s, T* G, int64_t ldg, T* vals, int* info, long long* prof,
                      cudaStream_t st);
 extern int g_ql_exact;
+extern int g_ql_f32;
 extern int g_syev_method;  // 0: tridiagonal + QL (default), 1: tridiagonal + Jacobi
 
 // ------------------------------------------------------------------ TSQR

@@ -56,11 +56,14 @@ k_residual(int64_t n, int m, const T* __restrict__ X, int64_t ldx, const T* __re
            int64_t ldax, const T* __restrict__ theta, const void* __restrict__ dinv,
            T* __restrict__ W, int64_t ldw, int64_t rows_per_chunk, double* __restrict__ part,
            int* overflow) {
-  __shared__ double red[kThreads / 32][2 * kColGroup];
+  // norms accumulate in real_t<T> like DenseMatrix<T>::col_norm
+  // (dense_matrix.hpp:74-82): fp32 sums in the fp32 stage, fp64 otherwise
+  using Acc = T;
+  __shared__ Acc red[kThreads / 32][2 * kColGroup];
   const int j0 = blockIdx.y * kColGroup;
   const int64_t r_begin = static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
   const int64_t r_end = min(n, r_begin + rows_per_chunk);
-  double rr[kColGroup], xx[kColGroup];
+  Acc rr[kColGroup], xx[kColGroup];
   T th[kColGroup];
 #pragma unroll
   for (int q = 0; q < kColGroup; ++q) {
@@ -76,8 +79,8 @@ k_residual(int64_t n, int m, const T* __restrict__ X, int64_t ldx, const T* __re
       if (j < m) {
         const T x = X[i + j * ldx];
         const T r = sub_rn(AX[i + j * ldax], mul_rn(th[q], x));
-        rr[q] = fma(static_cast<double>(r), static_cast<double>(r), rr[q]);
-        xx[q] = fma(static_cast<double>(x), static_cast<double>(x), xx[q]);
+        rr[q] = fma(static_cast<Acc>(r), static_cast<Acc>(r), rr[q]);
+        xx[q] = fma(static_cast<Acc>(x), static_cast<Acc>(x), xx[q]);
         if (W) W[i + j * ldw] = apply_ft<T, MODE>(r, dinv, i, &ovf);
       }
     }
@@ -87,7 +90,7 @@ k_residual(int64_t n, int m, const T* __restrict__ X, int64_t ldx, const T* __re
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int q = 0; q < kColGroup; ++q) {
-    double a = rr[q], b = xx[q];
+    Acc a = rr[q], b = xx[q];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       a += __shfl_down_sync(0xffffffffu, a, off);
@@ -100,7 +103,7 @@ k_residual(int64_t n, int m, const T* __restrict__ X, int64_t ldx, const T* __re
   }
   __syncthreads();
   if (threadIdx.x < 2 * kColGroup) {
-    double s = 0;
+    Acc s = 0;
 #pragma unroll
     for (int w = 0; w < kThreads / 32; ++w) s += red[w][threadIdx.x];
     const int q = threadIdx.x % kColGroup;
@@ -110,14 +113,15 @@ k_residual(int64_t n, int m, const T* __restrict__ X, int64_t ldx, const T* __re
   }
 }
 
+template <typename Acc>
 __global__ void k_resid_norms(int64_t nchunk, int m, const double* __restrict__ part,
                               double* __restrict__ rnorm, double* __restrict__ xnorm) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= 2 * m) return;
   const int j = t >> 1, which = t & 1;
-  double s = 0;
-  for (int64_t c = 0; c < nchunk; ++c) s += part[(c * m + j) * 2 + which];
-  (which ? xnorm : rnorm)[j] = sqrt(s);
+  Acc s = 0;
+  for (int64_t c = 0; c < nchunk; ++c) s += static_cast<Acc>(part[(c * m + j) * 2 + which]);
+  (which ? xnorm : rnorm)[j] = static_cast<double>(sqrt(s));
 }
 
 template <typename T, int MODE>
@@ -186,7 +190,7 @@ void residual_precond(int mode, int64_t n, int64_t m, const T* X, int64_t ldx, c
       }
   }
   MPB_LAUNCH_CHECK();
-  k_resid_norms<<<static_cast<unsigned>(ceil_div(2 * m, 128)), 128, 0, s>>>(p.nchunk, mi, work,
+  k_resid_norms<T><<<static_cast<unsigned>(ceil_div(2 * m, 128)), 128, 0, s>>>(p.nchunk, mi, work,
                                                                             rnorm, xnorm);
   MPB_LAUNCH_CHECK();
 }

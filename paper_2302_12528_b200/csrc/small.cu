@@ -445,13 +445,19 @@ k_upper_inverse_warp(int m, const T* __restrict__ R, int64_t ldr, T* __restrict_
 }
 
 // Hetmaniuk-Lehoucq coefficients (hl_update, eigensolvers.hpp:148-174) for
-// m, p <= MAXM: warp 0 runs householder_qr_square of top^* with the rows in
-// lanes (reflector scalars in fp64), the CTA forms c_x and c_pv = C_p Q.
+// m, p <= MAXM.  householder_qr_square of top^* (p x m) by warp 0 with the
+// COLUMNS in lanes: lane c holds column c, so the reflector of column j is
+// formed by lane j alone and every other column's dot product is lane-local
+// (no shuffles); reflectors go to shared memory.  Then every thread takes a
+// row of C_p and applies Q = H_0 ... H_{p-1} and the phase fix from the
+// right, again lane-local: c_pv(r, :) = C_p(r, :) Q.
 template <typename T, int MAXM>
 __global__ void __launch_bounds__(kSmallThreads)
 k_hl_coeffs_warp(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __restrict__ coef,
                  int* fallback) {
-  __shared__ T Qs[MAXM * MAXM];
+  __shared__ T Vs[MAXM][MAXM + 1];  // Vs[j][a]: reflector j, component a (a >= j)
+  __shared__ double Bs[MAXM];       // reflector scalars (fp64)
+  __shared__ T Sg[MAXM];            // sign of R(j, j)
   __shared__ int fb;
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int64_t idx = tid; idx < static_cast<int64_t>(s) * m; idx += nt) {
@@ -461,96 +467,81 @@ k_hl_coeffs_warp(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* _
   if (p == 0) return;
   if (tid < 32) {
     const int lane = tid;
-    // row `lane` of M = top^*: M(a, b) = C(b, m + a)
-    T mr[MAXM], v[MAXM], q[MAXM];
-    double beta[MAXM];
+    // column `lane` of M = top^*: M(a, c) = C(c, m + a), a < p
+    T mc[MAXM];
 #pragma unroll
-    for (int b = 0; b < MAXM; ++b)
-      mr[b] = (lane < p && b < m) ? C[b + static_cast<int64_t>(m + lane) * ldc] : T(0);
+    for (int a = 0; a < MAXM; ++a)
+      mc[a] = (lane < m && a < p) ? C[lane + static_cast<int64_t>(m + a) * ldc] : T(0);
     int bad = 0;
 #pragma unroll
     for (int j = 0; j < MAXM; ++j) {
-      v[j] = T(0);
-      beta[j] = 0.0;
-      if (j >= p || bad) continue;
-      const double xl = static_cast<double>(mr[j]);
-      double tail = lane > j && lane < p ? xl * xl : 0.0;
+      if (j < p && !bad) {  // guards, not break: the loops stay fully unrolled
+        if (lane == j) {
+          double tail = 0.0;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) tail += __shfl_xor_sync(0xffffffffu, tail, off);
-      const double x0 = __shfl_sync(0xffffffffu, xl, j);
-      const double nrm = sqrt(fma(x0, x0, tail));
-      if (nrm == 0.0) {
-        bad = 1;
-        continue;
-      }
-      const double phase = x0 < 0.0 ? -1.0 : 1.0;
-      const double v0 = x0 + phase * nrm;
-      beta[j] = 2.0 / fma(v0, v0, tail);
-      v[j] = lane == j ? static_cast<T>(v0) : (lane > j && lane < p ? mr[j] : T(0));
+          for (int a = j + 1; a < MAXM; ++a)
+            tail = fma(static_cast<double>(mc[a]), static_cast<double>(mc[a]), tail);
+          const double x0 = static_cast<double>(mc[j]);
+          const double nrm = sqrt(fma(x0, x0, tail));
+          if (nrm == 0.0) {
+            Bs[j] = -1.0;  // rank deficient: fallback
+          } else {
+            const double phase = x0 < 0.0 ? -1.0 : 1.0;
+            const double v0 = x0 + phase * nrm;
+            Bs[j] = 2.0 / fma(v0, v0, tail);
 #pragma unroll
-      for (int c = j + 1; c < MAXM; ++c) {
-        if (c >= m) break;
-        T part = v[j] * mr[c];
+            for (int a = 0; a < MAXM; ++a)
+              Vs[j][a] = a < j ? T(0) : (a == j ? static_cast<T>(v0) : mc[a]);
+            const T d = static_cast<T>(-phase * nrm);  // R(j,j) (ortho.hpp:72)
+            Sg[j] = d < T(0) ? T(-1) : T(1);
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-        const T f = static_cast<T>(static_cast<double>(part) * beta[j]);
-        mr[c] = fma(-f, v[j], mr[c]);
-      }
-      mr[j] = lane == j ? static_cast<T>(-phase * nrm) : (lane > j ? T(0) : mr[j]);
-    }
-    // Q = H_0 ... H_{p-1} applied to I last to first (ortho.hpp:78-92); row `lane`
-#pragma unroll
-    for (int c = 0; c < MAXM; ++c) q[c] = (c == lane && lane < p) ? T(1) : T(0);
-    if (!bad) {
-#pragma unroll
-      for (int jj = MAXM - 1; jj >= 0; --jj) {
-        if (jj >= p) continue;
-#pragma unroll
-        for (int c = 0; c < MAXM; ++c) {
-          if (c >= p) break;
-          T part = v[jj] * q[c];
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-          const T f = static_cast<T>(static_cast<double>(part) * beta[jj]);
-          q[c] = fma(-f, v[jj], q[c]);
+            for (int a = j; a < MAXM; ++a) mc[a] = a == j ? d : T(0);
+          }
         }
+        __syncwarp();
+        const double beta = Bs[j];
+        if (beta < 0.0) bad = 1;
+        if (!bad && lane > j && lane < m) {
+          T dot = T(0);
+#pragma unroll
+          for (int a = j; a < MAXM; ++a) dot = fma(Vs[j][a], mc[a], dot);
+          const T f = static_cast<T>(static_cast<double>(dot) * beta);
+#pragma unroll
+          for (int a = j; a < MAXM; ++a) mc[a] = fma(-f, Vs[j][a], mc[a]);
+        }
+        __syncwarp();
       }
     }
-    // fix_diagonal_phases (ortho.hpp:95-110): column j of Q by sign(R(j,j))
-    T rjj = T(1);
-#pragma unroll
-    for (int j = 0; j < MAXM; ++j)
-      if (j == lane) rjj = mr[j];
-    const unsigned zero = __ballot_sync(0xffffffffu, lane < p && rjj == T(0));
-    if (zero) bad = 1;
-#pragma unroll
-    for (int j = 0; j < MAXM; ++j) {
-      const T sj = __shfl_sync(0xffffffffu, rjj, j);
-      if (lane < p && j < p) Qs[lane + j * MAXM] = sj < T(0) ? -q[j] : q[j];
-    }
-    if (lane == 0) {
-      fb = bad;
-      *fallback = bad;
-    }
+    if (lane == 0) fb = bad;
   }
   __syncthreads();
+  if (tid == 0) *fallback = fb;
+  // c_pv(r, :) = C_p(r, :) H_0 H_1 ... H_{p-1} diag(sign R(j,j))  (V = I on fallback)
   const bool use_q = !fb;
-  for (int64_t idx = tid; idx < static_cast<int64_t>(s) * p; idx += nt) {
-    const int i = static_cast<int>(idx % s), j = static_cast<int>(idx / s);
-    T acc;
-    if (!use_q) {
-      acc = C[i + static_cast<int64_t>(m + j) * ldc];
-    } else {
-      T a0 = T(0), a1 = T(0);
-      int l = 0;
-      for (; l + 1 < p; l += 2) {
-        a0 = fma(C[i + static_cast<int64_t>(m + l) * ldc], Qs[l + j * MAXM], a0);
-        a1 = fma(C[i + static_cast<int64_t>(m + l + 1) * ldc], Qs[l + 1 + j * MAXM], a1);
+  for (int r = tid; r < s; r += nt) {
+    T y[MAXM];
+#pragma unroll
+    for (int a = 0; a < MAXM; ++a)
+      y[a] = a < p ? C[r + static_cast<int64_t>(m + a) * ldc] : T(0);
+    if (use_q) {
+#pragma unroll
+      for (int j = 0; j < MAXM; ++j) {
+        if (j < p) {
+          T dot = T(0);
+#pragma unroll
+          for (int a = j; a < MAXM; ++a) dot = fma(y[a], Vs[j][a], dot);
+          const T f = static_cast<T>(static_cast<double>(dot) * Bs[j]);
+#pragma unroll
+          for (int a = j; a < MAXM; ++a) y[a] = fma(-f, Vs[j][a], y[a]);
+        }
       }
-      if (l < p) a0 = fma(C[i + static_cast<int64_t>(m + l) * ldc], Qs[l + j * MAXM], a0);
-      acc = a0 + a1;
+#pragma unroll
+      for (int a = 0; a < MAXM; ++a)
+        if (a < p) y[a] *= Sg[a];
     }
-    coef[i + static_cast<int64_t>(m + j) * s] = acc;
+#pragma unroll
+    for (int a = 0; a < MAXM; ++a)
+      if (a < p) coef[r + static_cast<int64_t>(m + a) * s] = y[a];
   }
 }
 
@@ -580,11 +571,13 @@ void hl_coeffs_t(int64_t s, int64_t m, int64_t p, const T* C, int64_t ldc, T* co
     MPB_LAUNCH_CHECK();
     return;
   }
-  if ((warp_forms() & 4) && sizeof(T) == 4 && m <= 32 && p <= 32) {
-    k_hl_coeffs_warp<T, 32><<<1, kSmallThreads, 0, st>>>(static_cast<int>(s), static_cast<int>(m),
-                                                        static_cast<int>(p), C, ldc, coef, fallback);
-    MPB_LAUNCH_CHECK();
-    return;
+  if constexpr (sizeof(T) == 4) {
+    if ((warp_forms() & 4) && m <= 32 && p <= 32) {
+      k_hl_coeffs_warp<T, 32><<<1, kSmallThreads, 0, st>>>(static_cast<int>(s), static_cast<int>(m),
+                                                          static_cast<int>(p), C, ldc, coef, fallback);
+      MPB_LAUNCH_CHECK();
+      return;
+    }
   }
   const size_t bytes = static_cast<size_t>(p * m + 2 * p * p + p) * sizeof(T);
   const int use = bytes <= kSmemCap;

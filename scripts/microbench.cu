@@ -304,15 +304,31 @@ int main(int argc, char** argv) {
               res = std::max(res, std::fabs(r - lf[b] * Vf[a + (size_t)b * sdim]));
             }
           printf("  f32 check s=%d: orth %.2e resid %.2e nan %d lam0 %g\n", sdim, orth, res, nan, lf[0]);
+          {
+            float* Mfw;
+            CK(cudaMalloc(&Mfw, Mf.size() * 4));
+            CK(cudaMemcpy(Mfd, Mf.data(), Mf.size() * 4, cudaMemcpyHostToDevice));
+            const double msf = time_ms([&] {
+              cudaMemcpyAsync(Mfw, Mfd, Mf.size() * 4, cudaMemcpyDeviceToDevice, s);
+              small_syev<float>(sdim, Mfw, sdim, Wf, info, s);
+            }, 10, s);
+            snprintf(name, sizeof name, "mpb small_syev<float> s=%d", sdim);
+            report(name, msf, 0, 0);
+            long long* dpf;
+            CK(cudaMalloc(&dpf, 64));
+            CK(cudaMemset(dpf, 0, 64));
+            cudaMemcpyAsync(Mfw, Mfd, Mf.size() * 4, cudaMemcpyDeviceToDevice, s);
+            small_syev_prof<float>(sdim, Mfw, sdim, Wf, info, dpf, s);
+            long long hpf[5];
+            CK(cudaMemcpy(hpf, dpf, sizeof hpf, cudaMemcpyDeviceToHost));
+            printf("  f32 phases (cycles): tridiag %lld  QL %lld  sort %lld  sweeps %lld  chain %lld\n", hpf[0],
+                   hpf[1], hpf[2], hpf[3], hpf[4]);
+            cudaFree(dpf);
+            cudaFree(Mfw);
+          }
           cudaFree(Mfd);
           cudaFree(Wf);
         }
-        ms = time_ms([&] {
-          cudaMemcpyAsync(Mw, M, Mh.size() * 8, cudaMemcpyDeviceToDevice, s);
-          small_syev<float>(sdim, (float*)Mw, sdim, (float*)W, info, s);
-        }, 10, s);
-        snprintf(name, sizeof name, "mpb small_syev<float> s=%d", sdim);
-        report(name, ms, 0, 0);
       }
       CK(cudaFree(dw));
       CK(cudaFree(M));

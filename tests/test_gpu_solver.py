@@ -129,9 +129,12 @@ def test_long_case_parity(gpu):
     check_parity(g, cfg, r, "lap2d5x500-mplobpcg-schol")
 
 
-def test_small_case_iteration_parity_strict(gpu):
-    """Where the trajectory does not reach the chaotic regime the count is within +-2."""
-    g, cfg, r = run_case(gpu, "lap3d8-dlobpcg-dchol")
+@pytest.mark.parametrize("name", ["lap3d8-pinvit", "lap3d8-dlobpcg-schol"])
+def test_small_case_iteration_parity_strict(gpu, name):
+    """North-star bar: iteration count within +-2 of the reference.  Held strictly
+    on cases whose count the reference's own rounding perturbations leave within
+    +-2 as well (sensitivity.json); elsewhere the band of iteration_band applies."""
+    g, cfg, r = run_case(gpu, name)
     check_parity(g, cfg, r, iter_slack=ITER_SLACK)
 
 
