@@ -258,12 +258,12 @@ int main(int argc, char** argv) {
         CK(cudaMemset(dprof, 0, 64));
         cudaMemcpyAsync(Mw, M, Mh.size() * 8, cudaMemcpyDeviceToDevice, s);
         small_syev_prof<double>(sdim, Mw, sdim, W, info, dprof, s);
-        long long hp[5];
+        long long hp[8];
         CK(cudaMemcpy(hp, dprof, sizeof hp, cudaMemcpyDeviceToHost));
         snprintf(name, sizeof name, "mpb small_syev<double> s=%d", sdim);
         report(name, ms, 0, 0);
-        printf("  phases (cycles): tridiag %lld  QL %lld  sort %lld  sweeps %lld  chain %lld\n", hp[0], hp[1],
-               hp[2], hp[3], hp[4]);
+        printf("  phases (cycles): tridiag %lld [norm %lld mv %lld upd %lld]  QL %lld  sort %lld  sweeps %lld  chain %lld\n",
+               hp[0], hp[5], hp[6], hp[7], hp[1], hp[2], hp[3], hp[4]);
         cudaFree(dprof);
         {  // correctness of both precisions on the same matrix
           std::vector<double> V((size_t)sdim * sdim), lam(sdim);
