@@ -8,6 +8,7 @@
 // number of chunks and reduces the partials in chunk order, so results are
 // bitwise reproducible run to run (SURVEY §8e determinism).
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -21,16 +22,10 @@ constexpr int kGramBK = 32;
 constexpr int kGemmBK = 16;
 
 // ---- Gram G = A^T B ---------------------------------------------------------
-// One CTA per (output tile, row chunk).  The output tile is 16*MT square
-// (MT = 1..4) so that narrow blocks (k = 16, 32, 48) waste no MMA / FMA work
-// on zero padding.  Chunk partials are summed by a tree of groups of
-// kGramGroup inside the kernel itself: the last CTA of a group (atomic
-// counter) adds the group's partials in chunk order, so the result does not
-// depend on CTA timing and is bitwise reproducible.  Counters live at the
-// head of the workspace, are zeroed when the workspace is allocated and are
-// reset by the CTA that consumes them.
-constexpr int kGramGroup = 16;
-constexpr int64_t kGramCtrInts = 8192;
+// One CTA per (output tile, row chunk) writes its chunk's partial product; a
+// second kernel combines the partials GPU-wide in a fixed order (bitwise
+// reproducible) and hermitizes.  The output tile is 16*MT square (MT = 1..4)
+// so that narrow blocks (k = 16, 32, 48) waste no MMA / FMA work on padding.
 
 struct GramPlan {
   int mt;  // output tile = 16 * mt
@@ -44,134 +39,69 @@ GramPlan gram_plan(int64_t n, int64_t ka, int64_t kb) {
   const int64_t tile = 16 * p.mt;
   p.tiles_m = ceil_div(ka, tile);
   p.tiles_n = ceil_div(kb, tile);
-  const int64_t ntiles = p.tiles_m * p.tiles_n;
   // one wave: a single-tile Gram uses one CTA per SM (two reduction levels),
   // multi-tile Grams two CTAs per SM
-  int64_t nchunk = ntiles == 1 ? kNumSMs : ceil_div(kNumSMs * 2, ntiles);
+  static const int env_chunks = [] {
+    const char* e = std::getenv("MPEIG_GRAM_CHUNKS");  // tuning experiments only
+    return e ? std::atoi(e) : 0;
+  }();
+  // one chunk per SM: measured best from cfg1 (1 tile) to cfg4@8 (16 tiles);
+  // the GPU-wide combine makes the chunk count cheap
+  int64_t nchunk = env_chunks > 0 ? env_chunks : kNumSMs;
   const int64_t max_chunks = ceil_div(n, 64);  // >= 64 rows per chunk
   if (nchunk > max_chunks) nchunk = max_chunks;
   if (nchunk < 1) nchunk = 1;
   p.rows_per_chunk = round_up(ceil_div(n, nchunk), kGramBK);
   p.nchunk = ceil_div(n, p.rows_per_chunk);
   if (p.nchunk < 1) p.nchunk = 1;
-  // level buffers (the last level writes G directly)
-  p.level_elems = 0;
-  int64_t ctrs = 1;
-  for (int64_t cnt = p.nchunk; cnt > 1; cnt = ceil_div(cnt, kGramGroup)) {
-    p.level_elems += cnt * ka * kb;
-    ctrs += ntiles * ceil_div(cnt, kGramGroup);
-  }
-  if (ctrs > kGramCtrInts) throw Error(MPEIG_E_CONFIG, "gram: reduction tree too large");
+  // chunk partials, combined by k_gram_combine
+  p.level_elems = p.nchunk * ka * kb;
   return p;
 }
 
-// Called by every CTA after writing its chunk partial (tile at i0, j0, edge
-// TILE) to level 0 of `part` (or straight to G when there is a single chunk).
-// scratch: >= TILE*TILE elements of shared memory no longer in use; with a
-// single tile the final sums are hermitized there instead of through a pass
-// over G after a grid-wide counter.
-template <typename T, int TILE>
-__device__ void gram_tree(int ka, int kb, int i0, int j0, int tile, int ntiles, int64_t chunk,
-                          int64_t nchunk, T* __restrict__ part, int* __restrict__ ctr, T* G,
-                          int64_t ldg, int sym, T* scratch) {
-  __shared__ int s_last;
-  const bool local_sym = sym && ntiles == 1;
+// Deterministic combine of the chunk partials, spread over the whole GPU: a
+// warp per output entry (per symmetric pair when hermitizing), lanes sum
+// chunks lane, lane+32, ... in order, then a fixed xor tree.  G = sum, or
+// G(i,j) = G(j,i) = (sum_ij + sum_ji) / 2 (hermitize, eigensolvers.hpp:302-308).
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_gram_combine(int64_t nchunk, int ka, int kb, const T* __restrict__ part, T* __restrict__ G,
+               int64_t ldg, int sym) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t tot = static_cast<int64_t>(ka) * kb;
-  int64_t idx = chunk, cnt = nchunk;
-  T* lvl = part;
-  int* c = ctr;
-  while (cnt > 1) {
-    const int64_t ng = ceil_div(cnt, static_cast<int64_t>(kGramGroup));
-    const int64_t grp = idx / kGramGroup;
-    const int nchild = static_cast<int>(min(static_cast<int64_t>(kGramGroup), cnt - grp * kGramGroup));
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int* cp = c + tile * ng + grp;
-      s_last = atomicAdd(cp, 1) == nchild - 1;
-      if (s_last) *cp = 0;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const T* src = lvl + grp * kGramGroup * tot;
-    T* next = lvl + cnt * tot;
-    // valid entries of this tile, kEl per thread per round so that
-    // kEl * kGramGroup independent L2 loads are in flight
-    constexpr int kEl = 2;
-    const int vm = min(TILE, ka - i0), vn = min(TILE, kb - j0), nv = vm * vn;
-    for (int base = 0; base < nv; base += kEl * blockDim.x) {
-      T v[kEl][kGramGroup];
-      int64_t off[kEl];
-#pragma unroll
-      for (int u = 0; u < kEl; ++u) {
-        const int e = base + u * blockDim.x + threadIdx.x;
-        const int ee = e < nv ? e : 0;
-        off[u] = (i0 + ee % vm) + static_cast<int64_t>(j0 + ee / vm) * ka;
-#pragma unroll
-        for (int q = 0; q < kGramGroup; ++q)
-          v[u][q] = (e < nv && q < nchild) ? __ldcg(src + q * tot + off[u]) : T(0);
-      }
-#pragma unroll
-      for (int u = 0; u < kEl; ++u) {
-        const int e = base + u * blockDim.x + threadIdx.x;
-        if (e >= nv) continue;
-        T sum = v[u][0];
-#pragma unroll
-        for (int q = 1; q < kGramGroup; ++q)
-          if (q < nchild) sum += v[u][q];
-        if (ng == 1) {
-          if (local_sym) {
-            scratch[e] = sum;
-          } else {
-            const int i = i0 + e % vm, j = j0 + e / vm;
-            G[i + static_cast<int64_t>(j) * ldg] = sum;
-          }
-        } else {
-          next[grp * tot + off[u]] = sum;
-        }
-      }
-    }
-    lvl = next;
-    c += ntiles * ng;
-    cnt = ng;
-    idx = grp;
+  int i, j;
+  if (sym) {
+    // pair index w -> (i <= j), column-major over the upper triangle
+    if (w >= static_cast<int64_t>(ka) * (ka + 1) / 2) return;
+    j = static_cast<int>((sqrt(8.0 * static_cast<double>(w) + 1.0) - 1.0) / 2.0);
+    while ((static_cast<int64_t>(j) + 1) * (j + 2) / 2 <= w) ++j;
+    while (static_cast<int64_t>(j) * (j + 1) / 2 > w) --j;
+    i = static_cast<int>(w - static_cast<int64_t>(j) * (j + 1) / 2);
+  } else {
+    if (w >= tot) return;
+    i = static_cast<int>(w % ka);
+    j = static_cast<int>(w / ka);
   }
-  if (!sym) return;
-  if (local_sym) {
-    // ka == kb here; scratch holds the summed matrix, column-major (ld ka)
-    if (nchunk == 1) {
-      // single chunk: the CTA wrote its partial straight to G
-      __syncthreads();
-      for (int64_t e = threadIdx.x; e < tot; e += blockDim.x)
-        scratch[e] = G[(e % ka) + static_cast<int64_t>(e / ka) * ldg];
-    }
-    __syncthreads();
-    for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
-      const int i = static_cast<int>(e % ka), j = static_cast<int>(e / ka);
-      G[i + static_cast<int64_t>(j) * ldg] =
-          (scratch[e] + scratch[j + static_cast<int64_t>(i) * ka]) / T(2);
-    }
-    return;
+  const int64_t o1 = i + static_cast<int64_t>(j) * ka, o2 = j + static_cast<int64_t>(i) * ka;
+  T a = T(0), b = T(0);
+  for (int64_t c = lane; c < nchunk; c += 32) {
+    a += __ldg(part + c * tot + o1);
+    if (sym) b += __ldg(part + c * tot + o2);
   }
-  // hermitize once every tile is final: G = (G + G^T) / 2 (eigensolvers.hpp:292-297)
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    s_last = atomicAdd(c, 1) == ntiles - 1;
-    if (s_last) *c = 0;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, off);
+    b += __shfl_xor_sync(0xffffffffu, b, off);
   }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
-    const int i = static_cast<int>(e % ka), j = static_cast<int>(e / ka);
-    if (i > j) continue;
-    const T a = __ldcg(G + i + static_cast<int64_t>(j) * ldg);
-    const T b = __ldcg(G + j + static_cast<int64_t>(i) * ldg);
-    const T v = (a + b) / T(2);
-    G[i + static_cast<int64_t>(j) * ldg] = v;
-    G[j + static_cast<int64_t>(i) * ldg] = v;
+  if (lane == 0) {
+    if (sym) {
+      const T v = (a + b) / T(2);
+      G[i + static_cast<int64_t>(j) * ldg] = v;
+      G[j + static_cast<int64_t>(i) * ldg] = v;
+    } else {
+      G[i + static_cast<int64_t>(j) * ldg] = a;
+    }
   }
 }
 
@@ -186,7 +116,7 @@ k_gram_partial(int64_t n, int ka, int kb, const T* __restrict__ A, int64_t lda,
                int sym) {
   constexpr int TILE = 16 * TM;
   constexpr int kSm = 2 * kGramBK * (TILE + 1) > TILE * TILE ? 2 * kGramBK * (TILE + 1) : TILE * TILE;
-  __shared__ T sm[kSm];  // also gram_tree's scratch
+  __shared__ T sm[kSm];
   auto As = reinterpret_cast<T(*)[TILE + 1]>(sm);
   auto Bs = reinterpret_cast<T(*)[TILE + 1]>(sm + kGramBK * (TILE + 1));
   const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
@@ -238,7 +168,7 @@ k_gram_partial(int64_t n, int ka, int kb, const T* __restrict__ A, int64_t lda,
     }
     __syncthreads();
   }
-  const bool direct = nchunk == 1;
+  const bool direct = nchunk == 1 && !sym;
   T* out = direct ? G : part + static_cast<int64_t>(blockIdx.y) * ka * kb;
   const int64_t ldo = direct ? ldg : ka;
 #pragma unroll
@@ -248,8 +178,6 @@ k_gram_partial(int64_t n, int ka, int kb, const T* __restrict__ A, int64_t lda,
       const int i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
       if (i < ka && j < kb) out[i + static_cast<int64_t>(j) * ldo] = acc[a][b];
     }
-  gram_tree<T, TILE>(ka, kb, i0, j0, blockIdx.x, gridDim.x, blockIdx.y, nchunk, part, ctr, G, ldg,
-                     sym, sm);
 }
 
 // ---- fp64 tensor-core (DMMA) Gram -------------------------------------------
@@ -364,7 +292,7 @@ k_gram_dmma(int64_t n, int ka, int kb, const double* __restrict__ A, int64_t lda
         for (int b = 0; b < MT; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
   }
-  const bool direct = nchunk == 1;
+  const bool direct = nchunk == 1 && !sym;
   double* out = direct ? G : part + static_cast<int64_t>(blockIdx.y) * ka * kb;
   const int64_t ldo = direct ? ldg : ka;
 #pragma unroll
@@ -376,35 +304,36 @@ k_gram_dmma(int64_t n, int ka, int kb, const double* __restrict__ A, int64_t lda
         const int i = i0 + wm + 8 * a + g, j = j0 + wn + 8 * b + 2 * t4 + h;
         if (i < ka && j < kb) out[i + static_cast<int64_t>(j) * ldo] = acc[a][b][h];
       }
-  cp_async_wait<0>();
-  __syncthreads();  // the ring becomes gram_tree's scratch
-  gram_tree<double, TILE>(ka, kb, i0, j0, blockIdx.x, gridDim.x, blockIdx.y, nchunk, part, ctr, G,
-                          ldg, sym, reinterpret_cast<double*>(gsm));
 }
 
 // ---- fp64 tensor-core (DMMA) block update Y = beta Z + alpha A C ------------
-// A: n x k column-major (the tall operand), C: k x c (small).  CTA = 4 warps,
-// 64 rows x 64 cols of Y, each warp 32 x 32; K in 16-wide panels through a
-// cp.async double buffer.  A panel smem layout [k][row] with pitch 72
-// (fragment reads 2-way), C panel [col][k] with pitch 20.
+// A: n x k column-major (the tall operand), C: k x c (small).  CTA = 4 warps
+// (2 x 2), 64 rows x 16*NT columns of Y (NT = 1..4 sized to c), each warp
+// 32 x 8*NT; K in 16-wide panels through a cp.async ring, 4 stages for the
+// k <= 64 products of the hot path every load is in flight at once (deep
+// K uses a 2-stage ring: less shared memory, more CTAs per SM).  A panel
+// smem layout [k][row] with pitch 72 (fragment reads 2-way), C panel [col][k]
+// with pitch 20.
 constexpr int kAPitch = kTile + 8;
-
+template <int NT, int kGemmStages>
 __global__ void __launch_bounds__(128)
 k_gemm_dmma(int64_t n, int k, int c, double alpha, const double* __restrict__ A, int64_t lda,
             const double* __restrict__ Cm, int64_t ldc, double beta, const double* Z, int64_t ldz,
             double* Y, int64_t ldy) {
-  __shared__ __align__(16) double As[2][kDBK][kAPitch];
-  __shared__ __align__(16) double Cs[2][kTile][kDPitch];
+  constexpr int TN = 16 * NT;
+  extern __shared__ __align__(16) unsigned char gemm_sm[];
+  auto As = reinterpret_cast<double(*)[kDBK][kAPitch]>(gemm_sm);
+  auto Cs = reinterpret_cast<double(*)[TN][kDPitch]>(gemm_sm + sizeof(double) * kGemmStages * kDBK * kAPitch);
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kTile;
-  const int j0 = blockIdx.y * kTile;
+  const int j0 = blockIdx.y * TN;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-  double acc[4][4][2];
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 8 * NT;
+  double acc[4][NT][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
   auto load = [&](int buf, int k0) {
     // A panel: 16 k-columns x 64 rows = 16 x 32 chunks of 2 doubles
@@ -418,9 +347,9 @@ k_gemm_dmma(int64_t n, int k, int c, double alpha, const double* __restrict__ A,
       const double* src = bytes ? A + row + static_cast<int64_t>(k0 + kc) * lda : A;
       cp_async16(&As[buf][kc][2 * ch], src, bytes);
     }
-    // C panel: 64 cols x 16 k = 64 x 8 chunks
+    // C panel: TN cols x 16 k = TN x 8 chunks
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < NT; ++t) {
       const int e = threadIdx.x + 128 * t;
       const int col = e >> 3, ch = e & 7;
       const int kr = k0 + 2 * ch;
@@ -432,33 +361,37 @@ k_gemm_dmma(int64_t n, int k, int c, double alpha, const double* __restrict__ A,
   };
 
   const int npanel = (k + kDBK - 1) / kDBK;
-  load(0, 0);
-  cp_async_commit();
-  for (int p = 0; p < npanel; ++p) {
-    const int buf = p & 1;
-    if (p + 1 < npanel) load(buf ^ 1, (p + 1) * kDBK);
+#pragma unroll
+  for (int q = 0; q < kGemmStages - 1; ++q) {
+    if (q < npanel) load(q, q * kDBK);
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  for (int p = 0; p < npanel; ++p) {
+    const int buf = p % kGemmStages;
+    cp_async_wait<kGemmStages - 2>();
     __syncthreads();
+    {
+      const int q = p + kGemmStages - 1;
+      if (q < npanel) load(q % kGemmStages, q * kDBK);
+      cp_async_commit();
+    }
 #pragma unroll
     for (int kk = 0; kk < kDBK; kk += 4) {
-      double af[4], bf[4];
+      double af[4], bf[NT];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        af[q] = As[buf][kk + t4][wm + 8 * q + g];
-        bf[q] = Cs[buf][wn + 8 * q + g][kk + t4];
-      }
+      for (int q = 0; q < 4; ++q) af[q] = As[buf][kk + t4][wm + 8 * q + g];
+#pragma unroll
+      for (int q = 0; q < NT; ++q) bf[q] = Cs[buf][wn + 8 * q + g][kk + t4];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        for (int b = 0; b < NT; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
-    __syncthreads();
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
+    for (int b = 0; b < NT; ++b)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t i = i0 + wm + 8 * a + g;
@@ -612,9 +545,19 @@ int grid_for(int64_t total, int threads = 256, int64_t cap = kNumSMs * 8) {
 }  // namespace
 
 template <typename T>
+void gram_combine(const GramPlan& p, int64_t ka, int64_t kb, const T* part, T* G, int64_t ldg, int sym,
+                  cudaStream_t s) {
+  if (p.nchunk == 1 && !sym) return;  // the kernel wrote G directly
+  const int64_t warps = sym ? ka * (ka + 1) / 2 : ka * kb;
+  k_gram_combine<T><<<static_cast<unsigned>(ceil_div(warps, 8)), 256, 0, s>>>(
+      p.nchunk, static_cast<int>(ka), static_cast<int>(kb), part, G, ldg, sym);
+  MPB_LAUNCH_CHECK();
+}
+
+template <typename T>
 int64_t gram_workspace_elems(int64_t n, int64_t ka, int64_t kb) {
   const GramPlan p = gram_plan(n, ka, kb);
-  return ceil_div(kGramCtrInts * static_cast<int64_t>(sizeof(int)), sizeof(T)) + p.level_elems;
+  return p.level_elems;
 }
 
 template <typename T>
@@ -629,8 +572,8 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
   ProfScope prof("gram", s, double(sizeof(T)) * n * (A == B ? ka : ka + kb),
                  2.0 * n * ka * kb);
   const GramPlan p = gram_plan(n, ka, kb);
-  int* ctr = reinterpret_cast<int*>(work);
-  T* part = work + ceil_div(kGramCtrInts * static_cast<int64_t>(sizeof(int)), sizeof(T));
+  int* ctr = nullptr;  // (unused)
+  T* part = work;
   dim3 grid(static_cast<unsigned>(p.tiles_m * p.tiles_n), static_cast<unsigned>(p.nchunk));
   const bool aligned = (lda % 2 == 0) && (ldb % 2 == 0) &&
                        (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
@@ -657,6 +600,7 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
         default: launch(std::integral_constant<int, 4>()); break;
       }
       MPB_LAUNCH_CHECK();
+      gram_combine<T>(p, ka, kb, part, G, ldg, sym, s);
       return;
     }
   }
@@ -680,6 +624,7 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
       break;
   }
   MPB_LAUNCH_CHECK();
+  gram_combine<T>(p, ka, kb, part, G, ldg, sym, s);
 }
 
 template <typename T>
@@ -703,8 +648,37 @@ void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, 
                          (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(C) % 16 == 0);
     if (aligned) {
-      k_gemm_dmma<<<grid, 128, 0, s>>>(n, static_cast<int>(k), static_cast<int>(c), alpha, A, lda, C,
-                                       ldc, beta, Z, ldz, Y, ldy);
+      const int nt = c <= 16 ? 1 : c <= 32 ? 2 : c <= 48 ? 3 : 4;
+      const dim3 g2(static_cast<unsigned>(ceil_div(n, kTile)),
+                    static_cast<unsigned>(ceil_div(c, 16 * nt)));
+      const int ki = static_cast<int>(k), ci = static_cast<int>(c);
+      const bool shallow = k <= 4 * kDBK;
+      auto launch = [&](auto nt_tag) {
+        constexpr int NT = decltype(nt_tag)::value;
+        auto go = [&](auto st_tag) {
+          constexpr int ST = decltype(st_tag)::value;
+          constexpr size_t smem = sizeof(double) * ST * (kDBK * kAPitch + 16 * NT * kDPitch);
+          static bool attr = false;
+          if (!attr) {
+            MPB_CUDA(cudaFuncSetAttribute(k_gemm_dmma<NT, ST>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem)));
+            attr = true;
+          }
+          k_gemm_dmma<NT, ST><<<g2, 128, smem, s>>>(n, ki, ci, alpha, A, lda, C, ldc, beta, Z, ldz,
+                                                    Y, ldy);
+        };
+        if (shallow)
+          go(std::integral_constant<int, 4>());
+        else
+          go(std::integral_constant<int, 2>());
+      };
+      switch (nt) {
+        case 1: launch(std::integral_constant<int, 1>()); break;
+        case 2: launch(std::integral_constant<int, 2>()); break;
+        case 3: launch(std::integral_constant<int, 3>()); break;
+        default: launch(std::integral_constant<int, 4>()); break;
+      }
       MPB_LAUNCH_CHECK();
       return;
     }
