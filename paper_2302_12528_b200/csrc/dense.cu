@@ -319,8 +319,12 @@ template <int NT, int kGemmStages>
 __global__ void __launch_bounds__(128)
 k_gemm_dmma(int64_t n, int k, int c, double alpha, const double* __restrict__ A, int64_t lda,
             const double* __restrict__ Cm, int64_t ldc, double beta, const double* Z, int64_t ldz,
-            double* Y, int64_t ldy) {
+            double* Y, int64_t ldy, const double* __restrict__ A2, double* Y2) {
   constexpr int TN = 16 * NT;
+  if (blockIdx.z) {  // paired product Y2 = alpha A2 C (same C, k, c; beta = 0)
+    A = A2;
+    Y = Y2;
+  }
   extern __shared__ __align__(16) unsigned char gemm_sm[];
   auto As = reinterpret_cast<double(*)[kDBK][kAPitch]>(gemm_sm);
   auto Cs = reinterpret_cast<double(*)[TN][kDPitch]>(gemm_sm + sizeof(double) * kGemmStages * kDBK * kAPitch);
@@ -408,7 +412,11 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_gemm_tn(int64_t n, int k, int c, T alpha, const T* __restrict__ A, int64_t lda,
           const T* __restrict__ Cm, int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y,
-          int64_t ldy) {
+          int64_t ldy, const T* __restrict__ A2, T* Y2) {
+  if (blockIdx.z) {
+    A = A2;
+    Y = Y2;
+  }
   __shared__ T As[kGemmBK][kTile + 1];
   __shared__ T Cs[kGemmBK][kTile + 1];
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kTile;
@@ -628,8 +636,10 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
 }
 
 template <typename T>
-void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, const T* C,
-             int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y, int64_t ldy, cudaStream_t s) {
+static void gemm_impl(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, const T* C,
+                      int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y, int64_t ldy, const T* A2,
+                      T* Y2, cudaStream_t s) {
+  const unsigned nz = A2 ? 2u : 1u;
   if (n <= 0 || c <= 0) return;
   if (k <= 0) {
     // Y = beta Z
@@ -642,7 +652,7 @@ void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, 
   }
   ProfScope prof("gemm", s, double(sizeof(T)) * n * (k + (beta != T(0) ? 2 : 1) * c),
                  2.0 * n * k * c);
-  dim3 grid(static_cast<unsigned>(ceil_div(n, kTile)), static_cast<unsigned>(ceil_div(c, kTile)));
+  dim3 grid(static_cast<unsigned>(ceil_div(n, kTile)), static_cast<unsigned>(ceil_div(c, kTile)), nz);
   if constexpr (sizeof(T) == 8) {
     const bool aligned = (lda % 2 == 0) && (ldc % 2 == 0) &&
                          (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
@@ -650,7 +660,7 @@ void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, 
     if (aligned) {
       const int nt = c <= 16 ? 1 : c <= 32 ? 2 : c <= 48 ? 3 : 4;
       const dim3 g2(static_cast<unsigned>(ceil_div(n, kTile)),
-                    static_cast<unsigned>(ceil_div(c, 16 * nt)));
+                    static_cast<unsigned>(ceil_div(c, 16 * nt)), nz);
       const int ki = static_cast<int>(k), ci = static_cast<int>(c);
       const bool shallow = k <= 4 * kDBK;
       auto launch = [&](auto nt_tag) {
@@ -666,7 +676,7 @@ void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, 
             attr = true;
           }
           k_gemm_dmma<NT, ST><<<g2, 128, smem, s>>>(n, ki, ci, alpha, A, lda, C, ldc, beta, Z, ldz,
-                                                    Y, ldy);
+                                                    Y, ldy, A2, Y2);
         };
         if (shallow)
           go(std::integral_constant<int, 4>());
@@ -684,8 +694,25 @@ void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, 
     }
   }
   k_gemm_tn<T><<<grid, 256, 0, s>>>(n, static_cast<int>(k), static_cast<int>(c), alpha, A, lda, C,
-                                    ldc, beta, Z, ldz, Y, ldy);
+                                    ldc, beta, Z, ldz, Y, ldy, A2, Y2);
   MPB_LAUNCH_CHECK();
+}
+
+template <typename T>
+void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, const T* C,
+             int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y, int64_t ldy, cudaStream_t s) {
+  gemm_impl<T>(n, k, c, alpha, A, lda, C, ldc, beta, Z, ldz, Y, ldy, nullptr, nullptr, s);
+}
+
+template <typename T>
+void gemm_tn_pair(int64_t n, int64_t k, int64_t c, const T* A1, const T* A2, int64_t lda,
+                  const T* C, int64_t ldc, T* Y1, T* Y2, int64_t ldy, cudaStream_t s) {
+  if (k <= 0) {
+    gemm_tn<T>(n, k, c, T(1), A1, lda, C, ldc, T(0), nullptr, 0, Y1, ldy, s);
+    gemm_tn<T>(n, k, c, T(1), A2, lda, C, ldc, T(0), nullptr, 0, Y2, ldy, s);
+    return;
+  }
+  gemm_impl<T>(n, k, c, T(1), A1, lda, C, ldc, T(0), nullptr, 0, Y1, ldy, A2, Y2, s);
 }
 
 void convert_f64_to_f32(int64_t n, int64_t c, const double* src, int64_t lds, float* dst,
@@ -738,6 +765,8 @@ void frob_sq(int64_t n, int64_t c, const T* X, int64_t ldx, double* out, double*
                         int64_t, int, T*, cudaStream_t);                                        \
   template void gemm_tn<T>(int64_t, int64_t, int64_t, T, const T*, int64_t, const T*, int64_t, \
                            T, const T*, int64_t, T*, int64_t, cudaStream_t);                    \
+  template void gemm_tn_pair<T>(int64_t, int64_t, int64_t, const T*, const T*, int64_t, const T*, \
+                                int64_t, T*, T*, int64_t, cudaStream_t);                          \
   template void copy_block<T>(int64_t, int64_t, const T*, int64_t, T*, int64_t, cudaStream_t); \
   template void frob_sq<T>(int64_t, int64_t, const T*, int64_t, double*, double*, cudaStream_t); \
   template void scale_block<T>(int64_t, int64_t, T, const T*, int64_t, T*, int64_t, cudaStream_t);

@@ -29,6 +29,10 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
 template <typename T>
 void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, const T* C,
              int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y, int64_t ldy, cudaStream_t s);
+// Y1 = A1 C and Y2 = A2 C in one launch (the S C / AS C update pair)
+template <typename T>
+void gemm_tn_pair(int64_t n, int64_t k, int64_t c, const T* A1, const T* A2, int64_t lda,
+                  const T* C, int64_t ldc, T* Y1, T* Y2, int64_t ldy, cudaStream_t s);
 
 // dst = (To) src, elementwise over an n x c block; to_lower() narrowing sets
 // *overflow_flag = 1 on finite -> inf (precision.hpp:102-107).
@@ -142,6 +146,8 @@ template <typename Tin, typename Tq>
 int64_t tsqr_workspace_elems(int64_t n, int64_t m);
 template <typename Tin, typename Tq>
 void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr, Tq* work,
-            int* status, cudaStream_t s);
+            int* status, cudaStream_t s, Tin* Rw_out = nullptr, Tin* Rinv_out = nullptr);
+// (Rinv_out != nullptr: also R in Tin (Rw_out, m x m) and R^{-1} (m x m) --
+//  fused into the TSQR root for m <= 16)
 
 }  // namespace mpb

@@ -26,7 +26,7 @@ struct ResidPlan {
 ResidPlan resid_plan(int64_t n, int64_t m) {
   const int64_t groups = ceil_div(m, kColGroup);
   int64_t nchunk = ceil_div(static_cast<int64_t>(kNumSMs) * 8, groups);
-  const int64_t maxc = ceil_div(n, 4 * kThreads);  // >= 1024 rows per chunk
+  const int64_t maxc = ceil_div(n, 2 * kThreads);  // >= 512 rows per chunk
   if (nchunk > maxc) nchunk = maxc;
   if (nchunk < 1) nchunk = 1;
   ResidPlan p;
@@ -113,15 +113,19 @@ k_residual(int64_t n, int m, const T* __restrict__ X, int64_t ldx, const T* __re
   }
 }
 
+// a warp per (column, r|x): lanes take chunks lane, lane+32, ... in order,
+// then a fixed xor tree -> deterministic
 template <typename Acc>
 __global__ void k_resid_norms(int64_t nchunk, int m, const double* __restrict__ part,
                               double* __restrict__ rnorm, double* __restrict__ xnorm) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (t >= 2 * m) return;
   const int j = t >> 1, which = t & 1;
   Acc s = 0;
-  for (int64_t c = 0; c < nchunk; ++c) s += static_cast<Acc>(part[(c * m + j) * 2 + which]);
-  (which ? xnorm : rnorm)[j] = static_cast<double>(sqrt(s));
+  for (int64_t c = lane; c < nchunk; c += 32) s += static_cast<Acc>(part[(c * m + j) * 2 + which]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) (which ? xnorm : rnorm)[j] = static_cast<double>(sqrt(s));
 }
 
 template <typename T, int MODE>
@@ -190,8 +194,8 @@ void residual_precond(int mode, int64_t n, int64_t m, const T* X, int64_t ldx, c
       }
   }
   MPB_LAUNCH_CHECK();
-  k_resid_norms<T><<<static_cast<unsigned>(ceil_div(2 * m, 128)), 128, 0, s>>>(p.nchunk, mi, work,
-                                                                            rnorm, xnorm);
+  k_resid_norms<T><<<static_cast<unsigned>(ceil_div(2 * m, 4)), 128, 0, s>>>(p.nchunk, mi, work,
+                                                                          rnorm, xnorm);
   MPB_LAUNCH_CHECK();
 }
 

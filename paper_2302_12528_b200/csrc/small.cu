@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "rn.cuh"
+#include "smallwarp.cuh"
 
 namespace mpb {
 namespace {
@@ -397,51 +398,12 @@ k_cholesky_inv_warp(int m, const T* __restrict__ G, int64_t ldg, T* __restrict__
   }
 }
 
-// R^{-1} of an upper-triangular R: column c by lane c (back substitution).
+// R^{-1} of an upper-triangular R, one warp (smallwarp.cuh)
 template <typename T, int MAXM>
 __global__ void __launch_bounds__(32)
 k_upper_inverse_warp(int m, const T* __restrict__ R, int64_t ldr, T* __restrict__ Rinv,
                      int* status) {
-  const int lane = threadIdx.x;
-  const T tiny = sizeof(T) == 8 ? T(DBL_MIN) : T(FLT_MIN);
-  T r[MAXM];  // row `lane` of R
-#pragma unroll
-  for (int l = 0; l < MAXM; ++l)
-    r[l] = (lane < m && l < m && l >= lane) ? R[lane + static_cast<int64_t>(l) * ldr] : T(0);
-  T rdl = T(0);
-#pragma unroll
-  for (int l = 0; l < MAXM; ++l)
-    if (l == lane) rdl = r[l];
-  const bool bad = lane < m && (fabs(rdl) == T(0) || fabs(rdl) < tiny);
-  const unsigned badm = __ballot_sync(0xffffffffu, bad);
-  if (badm) {
-    if (lane == 0 && status[0] == 0) {
-      status[0] = MPEIG_E_SINGULAR_TRI;
-      status[1] = __ffs(badm) - 1;
-    }
-    return;
-  }
-  const T rinv_l = lane < m ? T(1) / rdl : T(0);
-  T y[MAXM];
-  const int c = lane;
-#pragma unroll
-  for (int k = MAXM - 1; k >= 0; --k) {
-    y[k] = T(0);
-    if (k >= m) continue;
-    T s = k == c ? T(1) : T(0);
-#pragma unroll
-    for (int l = k + 1; l < MAXM; ++l) {
-      if (l >= m) break;
-      s = fma(-__shfl_sync(0xffffffffu, r[l], k), y[l], s);
-    }
-    const T rk = __shfl_sync(0xffffffffu, rinv_l, k);  // all lanes take part
-    y[k] = k <= c ? s * rk : T(0);
-  }
-  if (c < m) {
-#pragma unroll
-    for (int k = 0; k < MAXM; ++k)
-      if (k < m) Rinv[k + c * m] = y[k];
-  }
+  warp_upper_inverse<T, T, MAXM>(m, R, ldr, nullptr, Rinv, status);
 }
 
 // Hetmaniuk-Lehoucq coefficients (hl_update, eigensolvers.hpp:148-174) for

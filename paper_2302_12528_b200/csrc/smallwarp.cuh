@@ -1,0 +1,69 @@
+// smallwarp.cuh -- one-warp triangular routines shared by several kernels.
+#pragma once
+
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace mpb {
+
+// R^{-1} of an upper-triangular m x m R (m <= MAXM <= 32) by one warp:
+// column c of R^{-1} by lane c (back substitution), row k of R broadcast from
+// lane k.  R is read as TS and converted to T; Rw (optional) receives that
+// converted copy.  A zero or subnormal pivot is SingularTriangular
+// (tri_solve, dense_kernels.hpp:177-194): status = {code, index}, first error
+// wins; returns false then.  Called by all 32 lanes of one warp.
+template <typename T, typename TS, int MAXM>
+__device__ __forceinline__ bool warp_upper_inverse(int m, const TS* __restrict__ R, int64_t ldr,
+                                                   T* __restrict__ Rw, T* __restrict__ Rinv,
+                                                   int* status) {
+  const int lane = threadIdx.x & 31;
+  const T tiny = sizeof(T) == 8 ? T(DBL_MIN) : T(FLT_MIN);
+  T r[MAXM];  // row `lane` of R
+#pragma unroll
+  for (int l = 0; l < MAXM; ++l)
+    r[l] = (lane < m && l < m && l >= lane) ? static_cast<T>(R[lane + static_cast<int64_t>(l) * ldr])
+                                            : T(0);
+  if (Rw && lane < m) {
+#pragma unroll
+    for (int l = 0; l < MAXM; ++l)
+      if (l < m) Rw[lane + l * m] = r[l];
+  }
+  T rdl = T(0);
+#pragma unroll
+  for (int l = 0; l < MAXM; ++l)
+    if (l == lane) rdl = r[l];
+  const bool bad = lane < m && (fabs(rdl) == T(0) || fabs(rdl) < tiny);
+  const unsigned badm = __ballot_sync(0xffffffffu, bad);
+  if (badm) {
+    if (lane == 0 && status[0] == 0) {
+      status[0] = MPEIG_E_SINGULAR_TRI;
+      status[1] = __ffs(badm) - 1;
+    }
+    return false;
+  }
+  const T rinv_l = lane < m ? T(1) / rdl : T(0);
+  T y[MAXM];
+  const int c = lane;
+#pragma unroll
+  for (int k = MAXM - 1; k >= 0; --k) {
+    y[k] = T(0);
+    if (k >= m) continue;
+    T s = k == c ? T(1) : T(0);
+#pragma unroll
+    for (int l = k + 1; l < MAXM; ++l) {
+      if (l >= m) break;
+      s = fma(-__shfl_sync(0xffffffffu, r[l], k), y[l], s);
+    }
+    const T rk = __shfl_sync(0xffffffffu, rinv_l, k);  // all lanes take part
+    y[k] = k <= c ? s * rk : T(0);
+  }
+  if (c < m) {
+#pragma unroll
+    for (int k = 0; k < MAXM; ++k)
+      if (k < m) Rinv[k + c * m] = y[k];
+  }
+  return true;
+}
+
+}  // namespace mpb

@@ -281,16 +281,15 @@ static int qr_core(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, T* Rout
   status_clear(ctx);
   if constexpr (sizeof(T) == 8) {
     if (lower) {
-      tsqr_r<double, float>(n, m, W, ldw, w.smallf.p, m, w.tsqr_f.p, ctx->d_status, s);
-      convert_f32_to_f64(m, m, w.smallf.p, m, w.Rw(), m, s);
+      // fp32 R_l, then R_l in fp64 and R_l^-1 (fused into the TSQR root)
+      tsqr_r<double, float>(n, m, W, ldw, w.smallf.p, m, w.tsqr_f.p, ctx->d_status, s, w.Rw(), w.Rinv());
     } else {
-      tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, ctx->d_status, s);
+      tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, ctx->d_status, s, nullptr, w.Rinv());
     }
   } else {
     (void)lower;
-    tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, ctx->d_status, s);
+    tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, ctx->d_status, s, nullptr, w.Rinv());
   }
-  small_upper_inverse<T>(m, w.Rw(), m, w.Rinv(), ctx->d_status, s);
   gemm_tn<T>(n, m, m, T(1), W, ldw, w.Rinv(), m, T(0), nullptr, 0, w.V.p, w.ld, s);
   gram<T>(n, m, w.V.p, w.ld, m, w.V.p, w.ld, w.G.p, m, 1, w.gramw.p, s);
   small_cholesky_inv<T>(m, w.G.p, m, w.L(), w.Uinv(), ctx->d_status, s);
@@ -396,8 +395,7 @@ void ritz_rotate(Work<T>& w) {
   const int64_t m = w.m;
   gram<T>(w.n, m, w.S.p, w.ld, m, w.AS.p, w.ld, w.G.p, m, 1, w.gramw.p, w.s);
   small_eig<T>(w, m, w.G.p, m, w.evals.p);
-  gemm_tn<T>(w.n, m, m, T(1), w.S.p, w.ld, w.G.p, m, T(0), nullptr, 0, w.S2.p, w.ld, w.s);
-  gemm_tn<T>(w.n, m, m, T(1), w.AS.p, w.ld, w.G.p, m, T(0), nullptr, 0, w.AS2.p, w.ld, w.s);
+  gemm_tn_pair<T>(w.n, m, m, w.S.p, w.AS.p, w.ld, w.G.p, m, w.S2.p, w.AS2.p, w.ld, w.s);
   MPB_CUDA(cudaMemcpyAsync(w.theta.p, w.evals.p, sizeof(T) * m, cudaMemcpyDeviceToDevice, w.s));
   std::swap(w.S, w.S2);
   std::swap(w.AS, w.AS2);
@@ -639,9 +637,8 @@ StageResult lobpcg_stage_eager(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, con
     else
       hl_coeffs_f32(sdim, m, pn, w.G.p, sdim, w.coef.p, w.scratch(), ctx->d_status + 4, s);
     // X, P = S [c_x c_pv]; AX, AP = AS [c_x c_pv] (eigensolvers.hpp:315-319)
-    gemm_tn<T>(n, sdim, m + pn, T(1), w.S.p, w.ld, w.coef.p, sdim, T(0), nullptr, 0, w.S2.p, w.ld, s);
-    gemm_tn<T>(n, sdim, m + pn, T(1), w.AS.p, w.ld, w.coef.p, sdim, T(0), nullptr, 0, w.AS2.p, w.ld,
-               s);
+    gemm_tn_pair<T>(n, sdim, m + pn, w.S.p, w.AS.p, w.ld, w.coef.p, sdim, w.S2.p, w.AS2.p, w.ld,
+                    s);
     MPB_CUDA(cudaMemcpyAsync(w.theta.p, w.evals.p, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
     status_fetch(ctx);
     tm.projected_eig += timer.stop();
@@ -668,16 +665,15 @@ static void qr_spec(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, int* s
   const int64_t n = w.n;
   if constexpr (sizeof(T) == 8) {
     if (lower) {
-      tsqr_r<double, float>(n, m, W, ldw, w.smallf.p, m, w.tsqr_f.p, status, s);
-      convert_f32_to_f64(m, m, w.smallf.p, m, w.Rw(), m, s);
+      // fp32 R_l, then R_l in fp64 and R_l^-1 (fused into the TSQR root)
+      tsqr_r<double, float>(n, m, W, ldw, w.smallf.p, m, w.tsqr_f.p, status, s, w.Rw(), w.Rinv());
     } else {
-      tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, status, s);
+      tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, status, s, nullptr, w.Rinv());
     }
   } else {
     (void)lower;
-    tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, status, s);
+    tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, status, s, nullptr, w.Rinv());
   }
-  small_upper_inverse<T>(m, w.Rw(), m, w.Rinv(), status, s);
   gemm_tn<T>(n, m, m, T(1), W, ldw, w.Rinv(), m, T(0), nullptr, 0, w.V.p, w.ld, s);
   gram<T>(n, m, w.V.p, w.ld, m, w.V.p, w.ld, w.G.p, m, 1, w.gramw.p, s);
   small_cholesky_inv<T>(m, w.G.p, m, w.L(), w.Uinv(), status, s);
@@ -764,8 +760,7 @@ static void spec_body(Work<T>& w, const mpeig_op* A, const mpeig_op* T_op, int64
     hl_coeffs(sdim, m, pn, w.G.p, sdim, w.coef.p, w.scratch(), ctx->d_status + kSlotHl, s);
   else
     hl_coeffs_f32(sdim, m, pn, w.G.p, sdim, w.coef.p, w.scratch(), ctx->d_status + kSlotHl, s);
-  gemm_tn<T>(n, sdim, m + pn, T(1), S, ld, w.coef.p, sdim, T(0), nullptr, 0, S2, ld, s);
-  gemm_tn<T>(n, sdim, m + pn, T(1), AS, ld, w.coef.p, sdim, T(0), nullptr, 0, AS2, ld, s);
+  gemm_tn_pair<T>(n, sdim, m + pn, S, AS, ld, w.coef.p, sdim, S2, AS2, ld, s);
   MPB_CUDA(cudaMemcpyAsync(w.theta.p, w.evals.p, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
   if (ev.on) MPB_CUDA(cudaEventRecord(ev.e[2], s));
   resid_launch<T>(w, T_op, S2, AS2, S2 + (m + pn) * ld);
@@ -961,10 +956,8 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
           hl_coeffs(sdim, m, pn, w.G.p, sdim, w.coef.p, w.scratch(), ctx->d_status + kSlotHl, s);
         else
           hl_coeffs_f32(sdim, m, pn, w.G.p, sdim, w.coef.p, w.scratch(), ctx->d_status + kSlotHl, s);
-        gemm_tn<T>(n, sdim, m + pn, T(1), w.S.p, w.ld, w.coef.p, sdim, T(0), nullptr, 0, w.S2.p,
-                   w.ld, s);
-        gemm_tn<T>(n, sdim, m + pn, T(1), w.AS.p, w.ld, w.coef.p, sdim, T(0), nullptr, 0, w.AS2.p,
-                   w.ld, s);
+        gemm_tn_pair<T>(n, sdim, m + pn, w.S.p, w.AS.p, w.ld, w.coef.p, sdim, w.S2.p, w.AS2.p,
+                        w.ld, s);
         MPB_CUDA(cudaMemcpyAsync(w.theta.p, w.evals.p, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
         status_fetch(ctx);
         tm.projected_eig += timer.stop();

@@ -15,6 +15,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "smallwarp.cuh"
 
 namespace mpb {
 namespace {
@@ -325,10 +326,10 @@ struct RegTile {
 };
 
 template <typename Tin, typename Tq, int NW, int RPL, int MPW>
-__global__ void __launch_bounds__(NW * 32)
+__global__ void __launch_bounds__(NW * 32, 1)
 k_tsqr_reg(int64_t n, int m, const Tin* __restrict__ W, int64_t ldw, Tq* __restrict__ Rbuf,
            int* __restrict__ counters, int64_t nleaf, int G, Tq* __restrict__ Rfinal, int64_t ldr,
-           int* status, int numeric_rank_check) {
+           int* status, int numeric_rank_check, Tin* __restrict__ Rw_out, Tin* __restrict__ Rinv_out) {
   using Tile = RegTile<Tq, NW, RPL, MPW>;
   constexpr int B = Tile::B;
   __shared__ __align__(16) Tq vbuf[2][B];
@@ -414,6 +415,13 @@ k_tsqr_reg(int64_t n, int m, const Tin* __restrict__ W, int64_t ldw, Tq* __restr
       }
     }
   }
+  if (Rinv_out) {
+    // fused epilogue of the QR's next two steps for m <= 16: R in the
+    // working precision (Rw_out) and R^{-1} (Rinv_out), by warp 0
+    __syncthreads();
+    if (warp == 0 && *reinterpret_cast<volatile int*>(status) == 0)
+      warp_upper_inverse<Tin, Tq, 16>(m, Rfinal, ldr, Rw_out, Rinv_out, status);
+  }
 }
 
 struct RegCfg {
@@ -451,7 +459,7 @@ RegCfg reg_cfg(int64_t m) {
 
 template <typename Tin, typename Tq>
 using RegKernel = void (*)(int64_t, int, const Tin*, int64_t, Tq*, int*, int64_t, int, Tq*, int64_t,
-                           int*, int);
+                           int*, int, Tin*, Tin*);
 
 template <typename Tin, typename Tq>
 RegKernel<Tin, Tq> reg_kernel(const RegCfg& c) {
@@ -503,6 +511,19 @@ bool tsqr_reg_enabled() {
 
 }  // namespace
 
+// R -> Rw (working precision) and R^{-1} when the epilogue is not fused
+template <typename Tin, typename Tq>
+void tsqr_epilogue(int64_t m, const Tq* R, int64_t ldr, Tin* Rw, Tin* Rinv, int* status,
+                   cudaStream_t s) {
+  if constexpr (sizeof(Tin) != sizeof(Tq)) {
+    convert_f32_to_f64(m, m, R, ldr, Rw, m, s);
+    small_upper_inverse<Tin>(m, Rw, m, Rinv, status, s);
+  } else {
+    if (Rw && Rw != R) copy_block<Tin>(m, m, R, ldr, Rw, m, s);
+    small_upper_inverse<Tin>(m, R, ldr, Rinv, status, s);
+  }
+}
+
 template <typename Tin, typename Tq>
 int64_t tsqr_workspace_elems(int64_t n, int64_t m) {
   const TsqrPlan<Tq> p = tsqr_plan<Tq>(n, m);
@@ -515,17 +536,19 @@ int64_t tsqr_workspace_elems(int64_t n, int64_t m) {
 
 template <typename Tin, typename Tq>
 void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr, Tq* work,
-            int* status, cudaStream_t s) {
+            int* status, cudaStream_t s, Tin* Rw_out, Tin* Rinv_out) {
   const int mi = static_cast<int>(m);
   const RegPlan rp = reg_plan<Tq>(n, m);
   const RegKernel<Tin, Tq> rk = rp.cfg.nw ? reg_kernel<Tin, Tq>(rp.cfg) : nullptr;
   if (rk && tsqr_reg_enabled()) {
     ProfScope prof("tsqr", s, double(sizeof(Tin)) * n * m, 2.0 * n * m * m);
     int* ctr = reinterpret_cast<int*>(work + rp.r_elems);
+    const bool fuse = Rinv_out && m <= 16;
     rk<<<static_cast<unsigned>(rp.nleaf), rp.cfg.nw * 32, 0, s>>>(
         n, mi, W, ldw, work, ctr, rp.nleaf, static_cast<int>(rp.G), R, ldr, status,
-        sizeof(Tin) == sizeof(Tq));
+        sizeof(Tin) == sizeof(Tq), fuse ? Rw_out : nullptr, fuse ? Rinv_out : nullptr);
     MPB_LAUNCH_CHECK();
+    if (Rinv_out && !fuse) tsqr_epilogue<Tin, Tq>(m, R, ldr, Rw_out, Rinv_out, status, s);
     return;
   }
   const TsqrPlan<Tq> p = tsqr_plan<Tq>(n, m);
@@ -553,16 +576,17 @@ void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr,
   }
   k_tsqr_finish<Tq><<<1, 256, 0, s>>>(mi, bufA, R, ldr, status, sizeof(Tin) == sizeof(Tq));
   MPB_LAUNCH_CHECK();
+  if (Rinv_out) tsqr_epilogue<Tin, Tq>(m, R, ldr, Rw_out, Rinv_out, status, s);
 }
 
 template int64_t tsqr_workspace_elems<double, double>(int64_t, int64_t);
 template int64_t tsqr_workspace_elems<double, float>(int64_t, int64_t);
 template int64_t tsqr_workspace_elems<float, float>(int64_t, int64_t);
 template void tsqr_r<double, double>(int64_t, int64_t, const double*, int64_t, double*, int64_t,
-                                     double*, int*, cudaStream_t);
+                                     double*, int*, cudaStream_t, double*, double*);
 template void tsqr_r<double, float>(int64_t, int64_t, const double*, int64_t, float*, int64_t,
-                                    float*, int*, cudaStream_t);
+                                    float*, int*, cudaStream_t, double*, double*);
 template void tsqr_r<float, float>(int64_t, int64_t, const float*, int64_t, float*, int64_t,
-                                   float*, int*, cudaStream_t);
+                                   float*, int*, cudaStream_t, float*, float*);
 
 }  // namespace mpb
