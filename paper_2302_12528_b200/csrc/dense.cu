@@ -13,6 +13,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "smallwarp.cuh"
 
 namespace mpb {
 namespace {
@@ -26,6 +27,9 @@ constexpr int kGemmBK = 16;
 // second kernel combines the partials GPU-wide in a fixed order (bitwise
 // reproducible) and hermitizes.  The output tile is 16*MT square (MT = 1..4)
 // so that narrow blocks (k = 16, 32, 48) waste no MMA / FMA work on padding.
+
+template <typename T>
+constexpr int64_t kGramHead = 16 / sizeof(T);  // elements before the partials
 
 struct GramPlan {
   int mt;  // output tile = 16 * mt
@@ -59,14 +63,10 @@ GramPlan gram_plan(int64_t n, int64_t ka, int64_t kb) {
   return p;
 }
 
-// Deterministic combine of the chunk partials, spread over the whole GPU: a
-// warp per output entry (per symmetric pair when hermitizing), lanes sum
-// chunks lane, lane+32, ... in order, then a fixed xor tree.  G = sum, or
-// G(i,j) = G(j,i) = (sum_ij + sum_ji) / 2 (hermitize, eigensolvers.hpp:302-308).
 template <typename T>
-__global__ void __launch_bounds__(256)
-k_gram_combine(int64_t nchunk, int ka, int kb, const T* __restrict__ part, T* __restrict__ G,
-               int64_t ldg, int sym) {
+__device__ __forceinline__ void combine_body(int64_t nchunk, int ka, int kb,
+                                             const T* __restrict__ part, T* __restrict__ G,
+                                             int64_t ldg, int sym) {
   const int lane = threadIdx.x & 31;
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t tot = static_cast<int64_t>(ka) * kb;
@@ -104,6 +104,36 @@ k_gram_combine(int64_t nchunk, int ka, int kb, const T* __restrict__ part, T* __
     }
   }
 }
+
+// Deterministic combine of the chunk partials, spread over the whole GPU: a
+// warp per output entry (per symmetric pair when hermitizing), lanes sum
+// chunks lane, lane+32, ... in order, then a fixed xor tree.  G = sum, or
+// G(i,j) = G(j,i) = (sum_ij + sum_ji) / 2 (hermitize, eigensolvers.hpp:302-308).
+//
+// chol != 0 (CholQR, ka = kb <= 16): the last CTA to finish (ticket) also
+// factors G = L L^T and forms L^{-T} (warp_cholesky_inv), saving the
+// separate small-kernel launch of the reference's cholesky_qr step.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_gram_combine(int64_t nchunk, int ka, int kb, const T* __restrict__ part, T* __restrict__ G,
+               int64_t ldg, int sym, int* __restrict__ ticket, T* __restrict__ L,
+               T* __restrict__ Uinv, int* status) {
+  combine_body(nchunk, ka, kb, part, G, ldg, sym);
+  if (!ticket) return;
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_last = atomicAdd(ticket, 1) == static_cast<int>(gridDim.x) - 1;
+    if (s_last) *ticket = 0;  // ready for the next call / graph replay
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if ((threadIdx.x >> 5) == 0 && *reinterpret_cast<volatile int*>(status) == 0)
+    warp_cholesky_inv<T, 16>(ka, G, ldg, L, Uinv, status);
+}
+
 
 // SIMT Gram (fp32, and fp64 operands that are not 16-B aligned): 256 threads
 // as 16 x 16, TM x TM outputs per thread, 32-row panels staged through
@@ -554,23 +584,26 @@ int grid_for(int64_t total, int threads = 256, int64_t cap = kNumSMs * 8) {
 
 template <typename T>
 void gram_combine(const GramPlan& p, int64_t ka, int64_t kb, const T* part, T* G, int64_t ldg, int sym,
-                  cudaStream_t s) {
+                  cudaStream_t s, int* ticket = nullptr, T* L = nullptr, T* Uinv = nullptr,
+                  int* status = nullptr) {
   if (p.nchunk == 1 && !sym) return;  // the kernel wrote G directly
   const int64_t warps = sym ? ka * (ka + 1) / 2 : ka * kb;
   k_gram_combine<T><<<static_cast<unsigned>(ceil_div(warps, 8)), 256, 0, s>>>(
-      p.nchunk, static_cast<int>(ka), static_cast<int>(kb), part, G, ldg, sym);
+      p.nchunk, static_cast<int>(ka), static_cast<int>(kb), part, G, ldg, sym, ticket, L, Uinv,
+      status);
   MPB_LAUNCH_CHECK();
 }
 
 template <typename T>
 int64_t gram_workspace_elems(int64_t n, int64_t ka, int64_t kb) {
   const GramPlan p = gram_plan(n, ka, kb);
-  return p.level_elems;
+  return p.level_elems + kGramHead<T>;  // + the CholQR ticket (zero at allocation)
 }
 
 template <typename T>
-void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B, int64_t ldb,
-          T* G, int64_t ldg, int sym, T* work, cudaStream_t s) {
+static void gram_impl(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B,
+                      int64_t ldb, T* G, int64_t ldg, int sym, T* work, cudaStream_t s, T* L,
+                      T* Uinv, int* status) {
   if (ka <= 0 || kb <= 0) return;
   if (n <= 0) {
     for (int64_t j = 0; j < kb; ++j)
@@ -580,8 +613,10 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
   ProfScope prof("gram", s, double(sizeof(T)) * n * (A == B ? ka : ka + kb),
                  2.0 * n * ka * kb);
   const GramPlan p = gram_plan(n, ka, kb);
+  // workspace: [CholQR ticket (16 B, fixed place for every shape) | partials]
   int* ctr = nullptr;  // (unused)
-  T* part = work;
+  int* ticket = reinterpret_cast<int*>(work);
+  T* part = work + kGramHead<T>;
   dim3 grid(static_cast<unsigned>(p.tiles_m * p.tiles_n), static_cast<unsigned>(p.nchunk));
   const bool aligned = (lda % 2 == 0) && (ldb % 2 == 0) &&
                        (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
@@ -608,7 +643,7 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
         default: launch(std::integral_constant<int, 4>()); break;
       }
       MPB_LAUNCH_CHECK();
-      gram_combine<T>(p, ka, kb, part, G, ldg, sym, s);
+      gram_combine<T>(p, ka, kb, part, G, ldg, sym, s, L ? ticket : nullptr, L, Uinv, status);
       return;
     }
   }
@@ -632,7 +667,21 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
       break;
   }
   MPB_LAUNCH_CHECK();
-  gram_combine<T>(p, ka, kb, part, G, ldg, sym, s);
+  gram_combine<T>(p, ka, kb, part, G, ldg, sym, s, L ? ticket : nullptr, L, Uinv, status);
+}
+
+template <typename T>
+void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B, int64_t ldb,
+          T* G, int64_t ldg, int sym, T* work, cudaStream_t s) {
+  gram_impl<T>(n, ka, A, lda, kb, B, ldb, G, ldg, sym, work, s, nullptr, nullptr, nullptr);
+}
+
+template <typename T>
+bool gram_cholesky(int64_t n, int64_t m, const T* V, int64_t ldv, T* G, T* work, T* L, T* Uinv,
+                   int* status, cudaStream_t s) {
+  if (m > 16 || n <= 0) return false;
+  gram_impl<T>(n, m, V, ldv, m, V, ldv, G, m, 1, work, s, L, Uinv, status);
+  return true;
 }
 
 template <typename T>
@@ -765,6 +814,8 @@ void frob_sq(int64_t n, int64_t c, const T* X, int64_t ldx, double* out, double*
                         int64_t, int, T*, cudaStream_t);                                        \
   template void gemm_tn<T>(int64_t, int64_t, int64_t, T, const T*, int64_t, const T*, int64_t, \
                            T, const T*, int64_t, T*, int64_t, cudaStream_t);                    \
+  template bool gram_cholesky<T>(int64_t, int64_t, const T*, int64_t, T*, T*, T*, T*, int*,   \
+                                 cudaStream_t);                                                \
   template void gemm_tn_pair<T>(int64_t, int64_t, int64_t, const T*, const T*, int64_t, const T*, \
                                 int64_t, T*, T*, int64_t, cudaStream_t);                          \
   template void copy_block<T>(int64_t, int64_t, const T*, int64_t, T*, int64_t, cudaStream_t); \

@@ -29,6 +29,13 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
 template <typename T>
 void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, const T* C,
              int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y, int64_t ldy, cudaStream_t s);
+// CholQR's Gram and factorization in one pass (m <= 16): G = V^T V
+// (hermitized), then L L^T = G and Uinv = L^{-T} by the last CTA of the
+// combine; returns false (nothing launched) when m > 16.
+template <typename T>
+bool gram_cholesky(int64_t n, int64_t m, const T* V, int64_t ldv, T* G, T* work, T* L, T* Uinv,
+                   int* status, cudaStream_t s);
+
 // Y1 = A1 C and Y2 = A2 C in one launch (the S C / AS C update pair)
 template <typename T>
 void gemm_tn_pair(int64_t n, int64_t k, int64_t c, const T* A1, const T* A2, int64_t lda,

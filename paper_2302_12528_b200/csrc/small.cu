@@ -348,54 +348,7 @@ template <typename T, int MAXM>
 __global__ void __launch_bounds__(32)
 k_cholesky_inv_warp(int m, const T* __restrict__ G, int64_t ldg, T* __restrict__ L,
                     T* __restrict__ Uinv, int* status) {
-  const int lane = threadIdx.x;
-  T a[MAXM];
-#pragma unroll
-  for (int j = 0; j < MAXM; ++j)
-    a[j] = (lane < m && j < m && lane >= j) ? G[lane + static_cast<int64_t>(j) * ldg] : T(0);
-#pragma unroll
-  for (int j = 0; j < MAXM; ++j) {
-    if (j >= m) break;
-    const T d2 = __shfl_sync(0xffffffffu, a[j], j);
-    if (!isfinite(static_cast<double>(d2)) || !(d2 > T(0))) {
-      if (lane == 0 && status[0] == 0) {
-        status[0] = isfinite(static_cast<double>(d2)) ? MPEIG_E_NOT_PD : MPEIG_E_OVERFLOW;
-        status[1] = j;
-      }
-      return;
-    }
-    const T d = sqrt(d2), rd = T(1) / d;
-    const T lij = lane > j ? a[j] * rd : (lane == j ? d : T(0));
-    a[j] = lij;
-#pragma unroll
-    for (int k = j + 1; k < MAXM; ++k) {
-      const T lkj = __shfl_sync(0xffffffffu, lij, k);
-      if (lane >= k) a[k] = fma(-lij, lkj, a[k]);
-    }
-  }
-  if (lane < m) {
-#pragma unroll
-    for (int j = 0; j < MAXM; ++j)
-      if (j < m) L[lane + j * m] = a[j];
-  }
-  if (!Uinv) return;
-  // X = L^{-1}: column c by lane c (forward substitution); Uinv(c, i) = X(i, c)
-  T x[MAXM];
-  const int c = lane;
-#pragma unroll
-  for (int i = 0; i < MAXM; ++i) {
-    if (i >= m) break;
-    T s = i == c ? T(1) : T(0);
-#pragma unroll
-    for (int l = 0; l < i; ++l) s = fma(-__shfl_sync(0xffffffffu, a[l], i), x[l], s);
-    const T dii = __shfl_sync(0xffffffffu, a[i], i);
-    x[i] = i >= c ? s / dii : T(0);
-  }
-  if (c < m) {
-#pragma unroll
-    for (int i = 0; i < MAXM; ++i)
-      if (i < m) Uinv[c + i * m] = x[i];
-  }
+  warp_cholesky_inv<T, MAXM>(m, G, ldg, L, Uinv, status);
 }
 
 // R^{-1} of an upper-triangular R, one warp (smallwarp.cuh)

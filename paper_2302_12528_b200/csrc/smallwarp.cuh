@@ -66,4 +66,63 @@ __device__ __forceinline__ bool warp_upper_inverse(int m, const TS* __restrict__
   return true;
 }
 
+// G = L L^T and Uinv = L^{-T} (dense_cholesky, dense_kernels.hpp:128-152) by
+// one warp for m <= MAXM <= 32: lane i holds row i.  G is read through L2
+// (__ldcg: it may have been written by other CTAs of the calling kernel).
+// Failure -> status {NOT_PD | OVERFLOW, column}, returns false.
+template <typename T, int MAXM>
+__device__ __forceinline__ bool warp_cholesky_inv(int m, const T* __restrict__ G, int64_t ldg,
+                                                  T* __restrict__ L, T* __restrict__ Uinv,
+                                                  int* status) {
+  const int lane = threadIdx.x & 31;
+  T a[MAXM];
+#pragma unroll
+  for (int j = 0; j < MAXM; ++j)
+    a[j] = (lane < m && j < m && lane >= j) ? __ldcg(G + lane + static_cast<int64_t>(j) * ldg) : T(0);
+#pragma unroll
+  for (int j = 0; j < MAXM; ++j) {
+    if (j >= m) break;
+    const T d2 = __shfl_sync(0xffffffffu, a[j], j);
+    if (!isfinite(static_cast<double>(d2)) || !(d2 > T(0))) {
+      if (lane == 0 && status[0] == 0) {
+        status[0] = isfinite(static_cast<double>(d2)) ? MPEIG_E_NOT_PD : MPEIG_E_OVERFLOW;
+        status[1] = j;
+      }
+      return false;
+    }
+    const T d = sqrt(d2), rd = T(1) / d;
+    const T lij = lane > j ? a[j] * rd : (lane == j ? d : T(0));
+    a[j] = lij;
+#pragma unroll
+    for (int k = j + 1; k < MAXM; ++k) {
+      const T lkj = __shfl_sync(0xffffffffu, lij, k);
+      if (lane >= k) a[k] = fma(-lij, lkj, a[k]);
+    }
+  }
+  if (lane < m) {
+#pragma unroll
+    for (int j = 0; j < MAXM; ++j)
+      if (j < m) L[lane + j * m] = a[j];
+  }
+  if (!Uinv) return true;
+  // X = L^{-1}: column c by lane c (forward substitution); Uinv(c, i) = X(i, c)
+  T x[MAXM];
+  const int c = lane;
+#pragma unroll
+  for (int i = 0; i < MAXM; ++i) {
+    if (i >= m) break;
+    T s = i == c ? T(1) : T(0);
+#pragma unroll
+    for (int l = 0; l < i; ++l) s = fma(-__shfl_sync(0xffffffffu, a[l], i), x[l], s);
+    const T dii = __shfl_sync(0xffffffffu, a[i], i);
+    x[i] = i >= c ? s / dii : T(0);
+  }
+  if (c < m) {
+#pragma unroll
+    for (int i = 0; i < MAXM; ++i)
+      if (i < m) Uinv[c + i * m] = x[i];
+  }
+  return true;
+}
+
 }  // namespace mpb

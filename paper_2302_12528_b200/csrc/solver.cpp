@@ -291,8 +291,10 @@ static int qr_core(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, T* Rout
     tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, ctx->d_status, s, nullptr, w.Rinv());
   }
   gemm_tn<T>(n, m, m, T(1), W, ldw, w.Rinv(), m, T(0), nullptr, 0, w.V.p, w.ld, s);
-  gram<T>(n, m, w.V.p, w.ld, m, w.V.p, w.ld, w.G.p, m, 1, w.gramw.p, s);
-  small_cholesky_inv<T>(m, w.G.p, m, w.L(), w.Uinv(), ctx->d_status, s);
+  if (!gram_cholesky<T>(n, m, w.V.p, w.ld, w.G.p, w.gramw.p, w.L(), w.Uinv(), ctx->d_status, s)) {
+    gram<T>(n, m, w.V.p, w.ld, m, w.V.p, w.ld, w.G.p, m, 1, w.gramw.p, s);
+    small_cholesky_inv<T>(m, w.G.p, m, w.L(), w.Uinv(), ctx->d_status, s);
+  }
   status_fetch(ctx);
   const int code = ctx->h_status[0];
   *idx = ctx->h_status[1];
@@ -675,8 +677,10 @@ static void qr_spec(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, int* s
     tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, status, s, nullptr, w.Rinv());
   }
   gemm_tn<T>(n, m, m, T(1), W, ldw, w.Rinv(), m, T(0), nullptr, 0, w.V.p, w.ld, s);
-  gram<T>(n, m, w.V.p, w.ld, m, w.V.p, w.ld, w.G.p, m, 1, w.gramw.p, s);
-  small_cholesky_inv<T>(m, w.G.p, m, w.L(), w.Uinv(), status, s);
+  if (!gram_cholesky<T>(n, m, w.V.p, w.ld, w.G.p, w.gramw.p, w.L(), w.Uinv(), status, s)) {
+    gram<T>(n, m, w.V.p, w.ld, m, w.V.p, w.ld, w.G.p, m, 1, w.gramw.p, s);
+    small_cholesky_inv<T>(m, w.G.p, m, w.L(), w.Uinv(), status, s);
+  }
   gemm_tn<T>(n, m, m, T(1), w.V.p, w.ld, w.Uinv(), m, T(0), nullptr, 0, W, ldw, s);
 }
 
