@@ -149,6 +149,21 @@ void* mpeig_ctx_stream(mpeig_ctx* ctx);
  *                 (process-wide; default 0) */
 int mpeig_ctx_set_option(mpeig_ctx* ctx, const char* key, int value);
 
+/* -------------------------------------------------------- row sharding */
+/* the n x . blocks are row-sharded over the ranks (z-slabs of
+ * the stencil).  Per iteration the ranks sum-allreduce the small Gram
+ * matrices and column norms, allgather their TSQR R factors, exchange the
+ * stencil's boundary planes with the slab neighbours and max-reduce the
+ * status words; the Rayleigh-Ritz step and all small factorisations run
+ * replicated.  A context attached to a communicator solves its rank's rows.
+ * NCCL (one process per GPU; rank 0 creates the id, broadcasts it):        */
+int mpeig_nccl_unique_id(void* out, int64_t cap);  /* cap >= 128 bytes */
+int mpeig_ctx_attach_nccl(mpeig_ctx* ctx, int rank, int nranks, const void* unique_id);
+/* ranks as threads of one process, host-staged sums in rank order (tests) */
+int mpeig_host_group_create(int nranks, void** out);
+void mpeig_host_group_destroy(void* group);
+int mpeig_ctx_attach_host_comm(mpeig_ctx* ctx, void* group, int rank);
+
 /* ------------------------------------------------------------ operators */
 /* BlockOperator<T> (dense_kernels.hpp:15-16).  Device callback: Y = op(X),
  * X/Y device column-major n_local x ncols, stream-ordered on `stream`,
@@ -168,6 +183,11 @@ typedef int (*mpeig_host_apply_fn)(void* user, int64_t n, int64_t ncols,
  * entries summed in ascending column order like spmv_block
  * (sparse_kernels.hpp:16-33) -> bitwise equal to the reference's CSR apply */
 int mpeig_op_lap3d(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, mpeig_op** out);
+/* this rank's z-slab [z0, z0 + nz_local) of the nx x ny x nz_global 7-point
+ * Laplacian (rows row0 = nx ny z0 ...), halo planes exchanged through the
+ * context's communicator; sharded rank r must hold slab r in z order */
+int mpeig_op_lap3d_slab(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz_global, int64_t z0,
+                        int64_t nz_local, mpeig_op** out);
 /* gen_laplace2d (generators.cpp:13-30) applied matrix-free */
 int mpeig_op_lap2d(mpeig_ctx* ctx, int64_t nx, int64_t ny, mpeig_op** out);
 /* CsrMatrix<double> (csr_matrix.hpp:13-146): int64 row_ptr/col_idx, sorted
@@ -254,6 +274,10 @@ int mpeig_run_variant(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T,
 /* gaussian_matrix<double> (dense_matrix.hpp:144-161) drawn on the host with
  * the reference stream, written to a host array (rows x cols) */
 int mpeig_gaussian_matrix_host(int64_t rows, int64_t cols, uint64_t seed, double* out_host);
+/* rows [row0, row0 + rows) of gaussian_matrix<double>(n_global, cols, seed):
+ * a row-shard's part of the start block / sketch (rows x cols, column-major) */
+int mpeig_gaussian_matrix_rows_host(int64_t n_global, int64_t cols, uint64_t seed, int64_t row0,
+                                    int64_t rows, double* out_host);
 /* detail::orthonormal_q (eigensolvers.hpp:55-70): mixed_qr with Householder
  * fallback (use_mixed, fp64) or Householder-equivalent QR.  In place on W. */
 int mpeig_orthonormal_q_f64(mpeig_ctx* ctx, int64_t n, int64_t m, double* W, int64_t ldw,

@@ -6,7 +6,9 @@ in ``include/mpeig_b200.h``); this package is the thin Python mirror of the
 reference interface used by the tests and the benchmark.
 """
 from .api import (  # noqa: F401
-    LOWER, WORKING, CallbackError, ConfigError, Context, CudaError, DimensionMismatch,
+    LOWER, WORKING, CallbackError, CommError, ConfigError, Context, CudaError, DimensionMismatch,
+    HostGroup, broadcast_unique_id, gaussian_matrix_rows, laplace3d_slab, nccl_unique_id,
+    slab_partition,
     EigResult, IterationRecord, MpeigError, NoConvergence, NotPositiveDefinite, Operator,
     OverflowError_, RankCollapse, RankDeficient, SingularTriangular, SolverConfig,
     StageOptions, StageOutcome, StageTimings, build_precision_for, converged_count, csr_matrix,

@@ -77,6 +77,9 @@ SYMBOLS = [
     "mpeig_project_out_f64", "mpeig_small_eig_f64", "mpeig_hl_coeffs_f64",
     "mpeig_residual_precond_f64", "mpeig_solve_prepared", "mpeig_profile_enable",
     "mpeig_profile_reset", "mpeig_profile_names", "mpeig_profile_query",
+    "mpeig_nccl_unique_id", "mpeig_ctx_attach_nccl", "mpeig_host_group_create",
+    "mpeig_host_group_destroy", "mpeig_ctx_attach_host_comm", "mpeig_op_lap3d_slab",
+    "mpeig_gaussian_matrix_rows_host",
 ]
 
 _lib = None
@@ -123,6 +126,7 @@ def load() -> C.CDLL:
         "mpeig_run_variant": (C.c_int, [vp, vp, vp, C.POINTER(Cfg), vp, i64, dbl, SINK, vp,
                                         C.POINTER(Result)]),
         "mpeig_gaussian_matrix_host": (C.c_int, [i64, i64, u64, vp]),
+        "mpeig_gaussian_matrix_rows_host": (C.c_int, [i64, i64, u64, i64, i64, vp]),
         "mpeig_orthonormal_q_f64": (C.c_int, [vp, i64, i64, vp, i64, i32]),
         "mpeig_orthonormal_q_f32": (C.c_int, [vp, i64, i64, vp, i64]),
         "mpeig_mixed_qr_f64": (C.c_int, [vp, i64, i64, vp, i64, vp]),
@@ -138,6 +142,12 @@ def load() -> C.CDLL:
                                                  vp, vp]),
         "mpeig_solve_prepared": (C.c_int, [vp, vp, vp, C.POINTER(Cfg), vp, i64, vp, i64, dbl, SINK,
                                            vp, C.POINTER(Result)]),
+        "mpeig_nccl_unique_id": (C.c_int, [vp, i64]),
+        "mpeig_ctx_attach_nccl": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+        "mpeig_host_group_create": (C.c_int, [C.c_int, pvp]),
+        "mpeig_host_group_destroy": (None, [vp]),
+        "mpeig_ctx_attach_host_comm": (C.c_int, [vp, vp, C.c_int]),
+        "mpeig_op_lap3d_slab": (C.c_int, [vp, i64, i64, i64, i64, i64, pvp]),
         "mpeig_profile_enable": (None, [C.c_int]),
         "mpeig_profile_reset": (None, []),
         "mpeig_profile_names": (C.c_int, [C.c_char_p, i64]),

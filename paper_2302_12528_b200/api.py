@@ -91,9 +91,13 @@ class CudaError(MpeigError, RuntimeError):
     code = L.E_CUDA
 
 
+class CommError(MpeigError, RuntimeError):
+    code = 32  # MPEIG_E_COMM
+
+
 _ERRORS = {c.code: c for c in (DimensionMismatch, ConfigError, NotPositiveDefinite,
                                SingularTriangular, RankDeficient, RankCollapse, NoConvergence,
-                               OverflowError_, CallbackError, CudaError)}
+                               OverflowError_, CallbackError, CudaError, CommError)}
 
 # ----------------------------------------------------------------- types
 
@@ -220,6 +224,78 @@ class Context:
     def launches(self, reset=False) -> int:
         return int(self.lib.mpeig_launch_count(self.h, 1 if reset else 0))
 
+    # -- row sharding: rank r solves its rows; see include/mpeig_b200.h
+    def attach_nccl(self, rank: int, nranks: int, unique_id: bytes):
+        """NCCL communicator over the ranks' GPUs (one process per GPU)."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        self.check(self.lib.mpeig_ctx_attach_nccl(self.h, int(rank), int(nranks), buf))
+
+    def attach_host(self, group: "HostGroup", rank: int):
+        """Rank `rank` of a HostGroup (ranks as threads of this process)."""
+        self._group = group  # keep alive
+        self.check(self.lib.mpeig_ctx_attach_host_comm(self.h, group.h, int(rank)))
+
+
+class HostGroup:
+    """A group of ranks running as threads of one process; exchanges are
+    staged through host memory and reduced in rank order (deterministic)."""
+
+    def __init__(self, nranks: int):
+        self.lib = L.load()
+        h = C.c_void_p()
+        if self.lib.mpeig_host_group_create(int(nranks), C.byref(h)) != 0:
+            raise ConfigError("host group: bad size")
+        self.h, self.nranks = h, nranks
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.mpeig_host_group_destroy(self.h)
+            self.h = None
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0); broadcast it to the other ranks."""
+    lib = L.load()
+    buf = C.create_string_buffer(128)
+    rc = lib.mpeig_nccl_unique_id(buf, 128)
+    if rc != 0:
+        raise CommError("NCCL unavailable", -1)
+    return buf.raw
+
+
+def gaussian_matrix_rows(n_global: int, cols: int, seed: int, row0: int, rows: int) -> np.ndarray:
+    """Rows [row0, row0 + rows) of gaussian_matrix(n_global, cols, seed)."""
+    lib = L.load()
+    out = np.empty((rows, cols), dtype=np.float64, order="F")
+    rc = lib.mpeig_gaussian_matrix_rows_host(n_global, cols, seed, row0, rows,
+                                             out.ctypes.data_as(C.c_void_p))
+    if rc != 0:
+        raise ConfigError("gaussian_matrix_rows: bad row range", -1)
+    return out
+
+
+def broadcast_unique_id(rank: int, group=None) -> bytes:
+    """NCCL id from rank 0 to every rank through torch.distributed (any
+    backend, e.g. gloo), for Context.attach_nccl."""
+    import torch
+    import torch.distributed as dist_
+    buf = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        buf[:] = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8)
+    dist_.broadcast(buf, src=0, group=group)
+    return bytes(buf.tolist())
+
+
+def slab_partition(nz: int, nranks: int):
+    """Balanced z-slabs [(z0, nz_local)] in rank order (rank r holds slab r)."""
+    base, extra = divmod(nz, nranks)
+    out, z0 = [], 0
+    for r in range(nranks):
+        nl = base + (1 if r < extra else 0)
+        out.append((z0, nl))
+        z0 += nl
+    return out
+
 
 _default_ctx: dict = {}
 
@@ -271,6 +347,15 @@ def laplace3d(nx: int, ny: int = None, nz: int = None, ctx: Context = None) -> O
     ny = nx if ny is None else ny
     nz = nx if nz is None else nz
     return Operator(ctx, _mk(ctx, ctx.lib.mpeig_op_lap3d, nx, ny, nz), nx * ny * nz, "lap3d")
+
+
+def laplace3d_slab(nx: int, ny: int, nz_global: int, z0: int, nz_local: int,
+                   ctx: Context = None) -> Operator:
+    """This rank's z-slab of the 7-point Laplacian (row-sharded; the context
+    must be attached to a communicator for more than one rank)."""
+    ctx = ctx or default_context()
+    h = _mk(ctx, ctx.lib.mpeig_op_lap3d_slab, nx, ny, nz_global, z0, nz_local)
+    return Operator(ctx, h, nx * ny * nz_local, "lap3d_slab")
 
 
 def laplace2d(nx: int, ny: int = None, ctx: Context = None) -> Operator:

@@ -123,6 +123,7 @@ void mpeig_ctx_destroy(mpeig_ctx* ctx) {
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx->comm;
   delete ctx;
 }
 
@@ -138,6 +139,44 @@ int64_t mpeig_launch_count(mpeig_ctx* ctx, int reset) {
 }
 
 void* mpeig_ctx_stream(mpeig_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+// ---- row sharding (comm.hpp)
+int mpeig_host_group_create(int nranks, void** out) {
+  if (!out || nranks < 1) return MPEIG_E_CONFIG;
+  *out = new mpb::HostGroup(nranks);
+  return MPEIG_OK;
+}
+
+void mpeig_host_group_destroy(void* group) { delete static_cast<mpb::HostGroup*>(group); }
+
+int mpeig_ctx_attach_host_comm(mpeig_ctx* ctx, void* group, int rank) {
+  return guard(ctx, [&] {
+    auto* g = static_cast<mpb::HostGroup*>(group);
+    if (!g || rank < 0 || rank >= g->nranks) throw Error(MPEIG_E_CONFIG, "bad host group / rank");
+    delete ctx->comm;
+    ctx->comm = new mpb::HostComm(g, rank);
+  });
+}
+
+int mpeig_nccl_unique_id(void* out, int64_t cap) {
+  if (!out || cap < 128) return MPEIG_E_CONFIG;
+  try {
+    mpb::nccl_unique_id(out);
+  } catch (const Error& e) {
+    return e.code;
+  }
+  return MPEIG_OK;
+}
+
+int mpeig_ctx_attach_nccl(mpeig_ctx* ctx, int rank, int nranks, const void* id) {
+  return guard(ctx, [&] {
+    if (!id || rank < 0 || rank >= nranks) throw Error(MPEIG_E_CONFIG, "bad NCCL rank / id");
+    MPB_CUDA(cudaSetDevice(ctx->device));
+    mpb::Comm* c = mpb::make_nccl_comm(rank, nranks, id);
+    delete ctx->comm;
+    ctx->comm = c;
+  });
+}
 
 int mpeig_ctx_set_option(mpeig_ctx* ctx, const char* key, int value) {
   if (!ctx || !key) return MPEIG_E_CONFIG;
@@ -160,6 +199,24 @@ int mpeig_op_lap3d(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, mpeig_op*
     op->nx = nx;
     op->ny = ny;
     op->nz = nz;
+    *out = op;
+  });
+}
+
+int mpeig_op_lap3d_slab(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz_global, int64_t z0,
+                        int64_t nz_local, mpeig_op** out) {
+  return guard(ctx, [&] {
+    if (nx < 1 || ny < 1 || nz_local < 1 || z0 < 0 || z0 + nz_local > nz_global)
+      throw Error(MPEIG_E_CONFIG, "lap3d_slab: bad slab");
+    mpeig_op* op = new_op(ctx, kOpLap3d, nx * ny * nz_local);
+    op->nx = nx;
+    op->ny = ny;
+    op->nz = nz_local;
+    op->slab = true;
+    op->z0 = z0;
+    op->nz_global = nz_global;
+    op->n_global = nx * ny * nz_global;
+    op->row0 = nx * ny * z0;
     *out = op;
   });
 }
@@ -308,6 +365,7 @@ void mpeig_op_destroy(mpeig_op* op) {
   cudaFree(op->Al);
   cudaFree(op->dinv);
   cudaFree(op->dinvf);
+  if (op->halo) cudaFree(op->halo);
   delete op;
 }
 
@@ -431,6 +489,14 @@ int mpeig_run_variant(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T, cons
 // ----------------------------------------------------- kernel-level entries
 int mpeig_gaussian_matrix_host(int64_t rows, int64_t cols, uint64_t seed, double* out_host) {
   return guard(nullptr, [&] { gaussian_fill(rows, cols, seed, out_host); });
+}
+
+int mpeig_gaussian_matrix_rows_host(int64_t n_global, int64_t cols, uint64_t seed, int64_t row0,
+                                    int64_t rows, double* out_host) {
+  return guard(nullptr, [&] {
+    if (row0 < 0 || rows < 0 || row0 + rows > n_global) throw Error(MPEIG_E_CONFIG, "bad row range");
+    gaussian_fill_rows(n_global, cols, seed, row0, rows, out_host);
+  });
 }
 
 int mpeig_orthonormal_q_f64(mpeig_ctx* ctx, int64_t n, int64_t m, double* W, int64_t ldw,

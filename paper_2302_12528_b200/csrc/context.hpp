@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.hpp"
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -27,6 +28,7 @@ struct mpeig_ctx {
   int eig_backend = 0;          // 0 auto (one-CTA syev for s <= kSyevMax), 1 cuSOLVER
   int spec_mode = 1;            // speculative iteration (1 host sync / iteration)
   int use_graphs = 1;           // replay the steady-state iteration as a CUDA graph
+  mpb::Comm* comm = nullptr;    // row-sharded mode (owned), nullptr: single GPU
 };
 
 enum OpKind { kOpLap3d, kOpLap2d, kOpCsr, kOpDense, kOpDeviceCb, kOpHostCb, kOpJacobi };
@@ -35,6 +37,12 @@ struct mpeig_op {
   OpKind kind;
   mpeig_ctx* ctx = nullptr;
   int64_t n = 0, nx = 0, ny = 0, nz = 0;
+  // row sharding: this rank holds global rows [row0, row0 + n) of n_global
+  // (z-slab [z0, z0 + nz) of nz_global for the stencil)
+  int64_t n_global = 0, row0 = 0, z0 = 0, nz_global = 0;
+  bool slab = false;
+  mutable void* halo = nullptr;  // send/recv planes of the slab exchange
+  mutable size_t halo_bytes = 0;
   // CSR (device)
   int64_t* rp = nullptr;
   int64_t* ci = nullptr;
@@ -99,6 +107,14 @@ struct DevBuf {
 
 // host-side gaussian block generation (rng.cpp)
 void gaussian_fill(int64_t rows, int64_t cols, uint64_t seed, double* out);
+// rows [row0, row0 + rows) of the n_global x cols block gaussian_fill draws
+void gaussian_fill_rows(int64_t n_global, int64_t cols, uint64_t seed, int64_t row0, int64_t rows,
+                        double* out);
+
+// the communicator when the context runs row-sharded over > 1 rank
+inline Comm* dist(const mpeig_ctx* ctx) {
+  return ctx->comm && ctx->comm->nranks > 1 ? ctx->comm : nullptr;
+}
 uint64_t pcg64_draw(uint64_t seed, uint64_t index);
 
 // operator application (ops dispatch in solver.cpp)

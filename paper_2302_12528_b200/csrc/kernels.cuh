@@ -76,7 +76,10 @@ template <typename T>
 void residual_precond(int mode, int64_t n, int64_t m, const T* X, int64_t ldx, const T* AX,
                       int64_t ldax, const T* theta, const void* dinv, T* W, int64_t ldw,
                       double* rnorm, double* xnorm, int* overflow_flag, double* work,
-                      cudaStream_t s);
+                      cudaStream_t s, int raw_sums = 0);
+// v = sqrt(v) in real_t<T> (after the row-sharded sums of squares were reduced)
+template <typename T>
+void norms_sqrt(int64_t count, double* v, cudaStream_t s);
 // W = f_T(R) without residual (generic Jacobi apply on a block)
 template <typename T>
 void jacobi_apply(int mode, int64_t n, int64_t c, const T* R, int64_t ldr, const void* dinv,
@@ -88,9 +91,11 @@ void subtract(int64_t n, int64_t c, const T* X, int64_t ldx, const T* W, int64_t
 
 // ------------------------------------------------------------- operators
 // 3-D 7-point / 2-D 5-point Laplacian, matrix-free, reference summation order
+// (hlo / hhi: the neighbouring ranks' adjacent z-planes of a row-sharded
+//  slab, nx*ny per column contiguous; nullptr at the domain boundary)
 template <typename T>
 void stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t c, const T* X, int64_t ldx, T* Y,
-              int64_t ldy, cudaStream_t s);
+              int64_t ldy, cudaStream_t s, const T* hlo = nullptr, const T* hhi = nullptr);
 template <typename T>
 void stencil5(int64_t nx, int64_t ny, int64_t c, const T* X, int64_t ldx, T* Y, int64_t ldy,
               cudaStream_t s);
@@ -153,7 +158,14 @@ template <typename Tin, typename Tq>
 int64_t tsqr_workspace_elems(int64_t n, int64_t m);
 template <typename Tin, typename Tq>
 void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr, Tq* work,
-            int* status, cudaStream_t s, Tin* Rw_out = nullptr, Tin* Rinv_out = nullptr);
+            int* status, cudaStream_t s, Tin* Rw_out = nullptr, Tin* Rinv_out = nullptr,
+            int rank_check = -1);
+// (rank_check: -1 numeric check iff Tin == Tq (default), 0 exact zeros only,
+//  1 numeric; a row-shard's local R factor uses 0 -- only the global R counts)
+// R (Tq) -> Rw (Tin, m x m) and Rinv = R^-1 (Tin), for an R already formed
+template <typename Tin, typename Tq>
+void tsqr_epilogue(int64_t m, const Tq* R, int64_t ldr, Tin* Rw, Tin* Rinv, int* status,
+                   cudaStream_t s);
 // (Rinv_out != nullptr: also R in Tin (Rw_out, m x m) and R^{-1} (m x m) --
 //  fused into the TSQR root for m <= 16)
 

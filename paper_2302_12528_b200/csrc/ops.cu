@@ -22,10 +22,13 @@ __device__ __forceinline__ T acc_neg(T s, T x) {  // s += (-1) * x
 // One thread per (row, column); rows of a column are consecutive threads so
 // every neighbour load of a warp is a contiguous 256-B segment (L1/L2 absorb
 // the 7-fold reuse; HBM traffic stays ~ read X + write Y).
+// Row-sharded z-slab: hlo / hhi are the neighbour ranks' adjacent planes
+// (nx*ny per column, contiguous), nullptr at the domain boundary; the sum
+// order is unchanged, so a sharded apply is bitwise the global one.
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_stencil7(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t ldx,
-           T* __restrict__ Y, int64_t ldy) {
+           T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi) {
   const int64_t n = nx * ny * nz;
   const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (p >= n) return;
@@ -37,13 +40,19 @@ k_stencil7(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t 
   const int64_t zi = yz / ny;
   const int64_t sy = nx, sz = nx * ny;
   T s = T(0);
-  if (zi > 0) s = acc_neg(s, x[p - sz]);
+  if (zi > 0)
+    s = acc_neg(s, x[p - sz]);
+  else if (hlo)
+    s = acc_neg(s, hlo[p + j * sz]);
   if (yi > 0) s = acc_neg(s, x[p - sy]);
   if (xi > 0) s = acc_neg(s, x[p - 1]);
   s = add_rn(s, mul_rn(T(6), x[p]));
   if (xi + 1 < nx) s = acc_neg(s, x[p + 1]);
   if (yi + 1 < ny) s = acc_neg(s, x[p + sy]);
-  if (zi + 1 < nz) s = acc_neg(s, x[p + sz]);
+  if (zi + 1 < nz)
+    s = acc_neg(s, x[p + sz]);
+  else if (hhi)
+    s = acc_neg(s, hhi[p - (nz - 1) * sz + j * sz]);
   Y[p + j * ldy] = s;
 }
 
@@ -86,12 +95,12 @@ k_csr_spmm(int64_t n, const int64_t* __restrict__ rp, const int64_t* __restrict_
 
 template <typename T>
 void stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t c, const T* X, int64_t ldx, T* Y,
-              int64_t ldy, cudaStream_t s) {
+              int64_t ldy, cudaStream_t s, const T* hlo, const T* hhi) {
   const int64_t n = nx * ny * nz;
   if (n <= 0 || c <= 0) return;
   ProfScope prof("stencil", s, 2.0 * sizeof(T) * n * c, 13.0 * n * c);
   dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(c));
-  k_stencil7<T><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy);
+  k_stencil7<T><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi);
   MPB_LAUNCH_CHECK();
 }
 
@@ -118,7 +127,7 @@ void csr_spmm(int64_t n, const int64_t* row_ptr, const int64_t* col_idx, const T
 
 #define MPB_INST(T)                                                                          \
   template void stencil7<T>(int64_t, int64_t, int64_t, int64_t, const T*, int64_t, T*,       \
-                            int64_t, cudaStream_t);                                          \
+                            int64_t, cudaStream_t, const T*, const T*);                      \
   template void stencil5<T>(int64_t, int64_t, int64_t, const T*, int64_t, T*, int64_t,       \
                             cudaStream_t);                                                   \
   template void csr_spmm<T>(int64_t, const int64_t*, const int64_t*, const T*, int64_t,      \

@@ -117,7 +117,7 @@ k_residual(int64_t n, int m, const T* __restrict__ X, int64_t ldx, const T* __re
 // then a fixed xor tree -> deterministic
 template <typename Acc>
 __global__ void k_resid_norms(int64_t nchunk, int m, const double* __restrict__ part,
-                              double* __restrict__ rnorm, double* __restrict__ xnorm) {
+                              double* __restrict__ rnorm, double* __restrict__ xnorm, int raw) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (t >= 2 * m) return;
   const int j = t >> 1, which = t & 1;
@@ -125,7 +125,14 @@ __global__ void k_resid_norms(int64_t nchunk, int m, const double* __restrict__ 
   for (int64_t c = lane; c < nchunk; c += 32) s += static_cast<Acc>(part[(c * m + j) * 2 + which]);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if (lane == 0) (which ? xnorm : rnorm)[j] = static_cast<double>(sqrt(s));
+  if (lane == 0) (which ? xnorm : rnorm)[j] = raw ? static_cast<double>(s) : static_cast<double>(sqrt(s));
+}
+
+// sqrt in real_t<T> after the row-sharded sums were allreduced
+template <typename Acc>
+__global__ void k_norms_sqrt(int64_t count, double* __restrict__ v) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < count) v[i] = static_cast<double>(sqrt(static_cast<Acc>(v[i])));
 }
 
 template <typename T, int MODE>
@@ -170,7 +177,7 @@ template <typename T>
 void residual_precond(int mode, int64_t n, int64_t m, const T* X, int64_t ldx, const T* AX,
                       int64_t ldax, const T* theta, const void* dinv, T* W, int64_t ldw,
                       double* rnorm, double* xnorm, int* overflow_flag, double* work,
-                      cudaStream_t s) {
+                      cudaStream_t s, int raw_sums) {
   if (m <= 0) return;
   ProfScope prof("residual_ft", s, double(sizeof(T)) * n * m * (W ? 3 : 2), 6.0 * n * m);
   const ResidPlan p = resid_plan(n, m);
@@ -195,7 +202,14 @@ void residual_precond(int mode, int64_t n, int64_t m, const T* X, int64_t ldx, c
   }
   MPB_LAUNCH_CHECK();
   k_resid_norms<T><<<static_cast<unsigned>(ceil_div(2 * m, 4)), 128, 0, s>>>(p.nchunk, mi, work,
-                                                                          rnorm, xnorm);
+                                                                          rnorm, xnorm, raw_sums);
+  MPB_LAUNCH_CHECK();
+}
+
+template <typename T>
+void norms_sqrt(int64_t count, double* v, cudaStream_t s) {
+  if (count <= 0) return;
+  k_norms_sqrt<T><<<static_cast<unsigned>(ceil_div(count, 128)), 128, 0, s>>>(count, v);
   MPB_LAUNCH_CHECK();
 }
 
@@ -231,7 +245,8 @@ void subtract(int64_t n, int64_t c, const T* X, int64_t ldx, const T* W, int64_t
 #define MPB_INST(T)                                                                             \
   template void residual_precond<T>(int, int64_t, int64_t, const T*, int64_t, const T*, int64_t, \
                                     const T*, const void*, T*, int64_t, double*, double*, int*,  \
-                                    double*, cudaStream_t);                                      \
+                                    double*, cudaStream_t, int);                                 \
+  template void norms_sqrt<T>(int64_t, double*, cudaStream_t);                                  \
   template void jacobi_apply<T>(int, int64_t, int64_t, const T*, int64_t, const void*, T*,       \
                                 int64_t, int*, cudaStream_t);                                    \
   template void subtract<T>(int64_t, int64_t, const T*, int64_t, const T*, int64_t, T*, int64_t, \

@@ -55,9 +55,11 @@ u128 jump(u128 s, uint64_t k) {
   return acc_mult * s + acc_plus;
 }
 
-void fill_range(uint64_t seed, int64_t begin, int64_t end, double* out) {
+// stream elements [begin, end) into out[e - base]
+void fill_range(uint64_t seed, int64_t begin, int64_t end, double* out, int64_t base = 0) {
   // begin is even: element 2p/2p+1 use draws 2p, 2p+1
   u128 s = jump(seed_state(seed), static_cast<uint64_t>(begin));
+  out -= base;
   constexpr double two_pi = 6.283185307179586476925286766559;
   for (int64_t e = begin; e < end; e += 2) {
     s = s * kA + kC;
@@ -73,6 +75,18 @@ void fill_range(uint64_t seed, int64_t begin, int64_t end, double* out) {
 }
 
 }  // namespace
+
+void gaussian_fill_rows(int64_t n_global, int64_t cols, uint64_t seed, int64_t row0, int64_t rows,
+                        double* out) {
+  if (rows <= 0 || cols <= 0) return;
+  std::vector<double> tmp(static_cast<size_t>(rows + 2));
+  for (int64_t j = 0; j < cols; ++j) {
+    // column j of the local rows = stream elements [row0 + n j, row0 + rows + n j)
+    const int64_t s = row0 + n_global * j, e = s + rows, s2 = s & ~int64_t{1};
+    fill_range(seed, s2, e, tmp.data(), s2);
+    for (int64_t i = 0; i < rows; ++i) out[i + rows * j] = tmp[static_cast<size_t>(s - s2 + i)];
+  }
+}
 
 uint64_t pcg64_draw(uint64_t seed, uint64_t index) {
   return out_xslrr(jump(seed_state(seed), index + 1));
@@ -93,7 +107,7 @@ void gaussian_fill(int64_t rows, int64_t cols, uint64_t seed, double* out) {
     const int64_t b = static_cast<int64_t>(t) * per;
     if (b >= total) break;
     const int64_t e = b + per < total ? b + per : total;
-    th.emplace_back(fill_range, seed, b, e, out);
+    th.emplace_back(fill_range, seed, b, e, out, int64_t{0});
   }
   for (auto& x : th) x.join();
 }

@@ -37,6 +37,8 @@ void status_clear(mpeig_ctx* ctx) {
 }
 
 void status_fetch(mpeig_ctx* ctx) {
+  // row-sharded: every rank sees every rank's failures, so all take the same branch
+  if (Comm* c = dist(ctx)) c->allreduce_max(ctx->d_status, 16, ctx->stream);
   MPB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->d_status, 16 * sizeof(int), cudaMemcpyDeviceToHost,
                            ctx->stream));
   MPB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -62,9 +64,35 @@ void op_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* X, int
   cudaStream_t s = ctx->stream;
   if (ncols <= 0) return;
   switch (op->kind) {
-    case kOpLap3d:
-      stencil7<T>(op->nx, op->ny, op->nz, ncols, X, ldx, Y, ldy, s);
+    case kOpLap3d: {
+      Comm* c = dist(ctx);
+      if (!op->slab || !c) {
+        stencil7<T>(op->nx, op->ny, op->nz, ncols, X, ldx, Y, ldy, s);
+        return;
+      }
+      // z-slab of a row-sharded Laplacian: swap the boundary planes with
+      // the neighbouring ranks (SURVEY §8e halo exchange), then one pass
+      const int64_t sz = op->nx * op->ny;
+      const size_t plane = sizeof(T) * static_cast<size_t>(sz * ncols);
+      if (op->halo_bytes < 4 * plane) {
+        if (op->halo) MPB_CUDA(cudaFreeAsync(op->halo, s));
+        MPB_CUDA(cudaMallocAsync(&op->halo, 4 * plane, s));
+        op->halo_bytes = 4 * plane;
+      }
+      char* h = static_cast<char*>(op->halo);
+      T* slo = reinterpret_cast<T*>(h);
+      T* shi = reinterpret_cast<T*>(h + plane);
+      T* rlo = reinterpret_cast<T*>(h + 2 * plane);
+      T* rhi = reinterpret_cast<T*>(h + 3 * plane);
+      MPB_CUDA(cudaMemcpy2DAsync(slo, sizeof(T) * sz, X, sizeof(T) * ldx, sizeof(T) * sz, ncols,
+                                 cudaMemcpyDeviceToDevice, s));
+      MPB_CUDA(cudaMemcpy2DAsync(shi, sizeof(T) * sz, X + (op->nz - 1) * sz, sizeof(T) * ldx,
+                                 sizeof(T) * sz, ncols, cudaMemcpyDeviceToDevice, s));
+      c->exchange(slo, shi, rlo, rhi, static_cast<int64_t>(plane), s);
+      stencil7<T>(op->nx, op->ny, op->nz, ncols, X, ldx, Y, ldy, s, c->rank > 0 ? rlo : nullptr,
+                  c->rank + 1 < c->nranks ? rhi : nullptr);
       return;
+    }
     case kOpLap2d:
       stencil5<T>(op->nx, op->ny, ncols, X, ldx, Y, ldy, s);
       return;
@@ -196,6 +224,15 @@ Work<T>::Work(mpeig_ctx* c, int64_t n_, int64_t m_, int64_t smax_) : ctx(c), n(n
                    "syevd_bufferSize");
   lwork = lw;
   eigw.alloc(static_cast<size_t>(lw > 0 ? lw : 1), s);
+  if (Comm* c = dist(ctx)) {
+    const int64_t P = c->nranks, mm = m * m;
+    rstk.alloc(static_cast<size_t>(P * mm), s);
+    rstk2.alloc(static_cast<size_t>(P * mm), s);
+    tsqr_w2.alloc_zero(static_cast<size_t>(tsqr_workspace_elems<T, T>(P * m, m)), s);
+    rstkf.alloc(static_cast<size_t>(P * mm), s);
+    rstk2f.alloc(static_cast<size_t>(P * mm), s);
+    tsqr_f2.alloc_zero(static_cast<size_t>(tsqr_workspace_elems<float, float>(P * m, m)), s);
+  }
 }
 
 template <typename T>
@@ -265,6 +302,96 @@ void small_eig(Work<T>& w, int64_t sdim, T* G, int64_t ldg, T* vals) {
                    "cusolverDnSsyevd");
 }
 
+// ---------------------------------------------------- row-sharded helpers
+// G = A^T B summed over the ranks' rows (then hermitized): the Gram products
+// are the solver's only O(n)-reductions besides the column norms.
+template <typename T>
+static void dgram(Work<T>& w, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B,
+                  int64_t ldb, T* G, int64_t ldg, int sym) {
+  Comm* c = dist(w.ctx);
+  if (!c) {
+    gram<T>(w.n, ka, A, lda, kb, B, ldb, G, ldg, sym, w.gramw.p, w.s);
+    return;
+  }
+  if (ldg != ka) throw Error(MPEIG_E_OTHER, "dgram: Gram leading dimension must equal its rows");
+  gram<T>(w.n, ka, A, lda, kb, B, ldb, G, ldg, 0, w.gramw.p, w.s);
+  c->allreduce_sum(G, ka * kb, w.s);
+  if (sym) small_symmetrize<T>(ka, G, ldg, w.s);
+}
+
+// ||x||^2 of one column, summed over the ranks
+template <typename T>
+static void dfrob(Work<T>& w, int64_t n, const T* v, int64_t ld, double* d2) {
+  frob_sq<T>(n, 1, v, ld, d2, w.rw.p, w.s);
+  if (Comm* c = dist(w.ctx)) c->allreduce_sum(d2, 1, w.s);
+}
+
+// residual + norms (+ fused f_T); the norms' sums of squares are reduced over
+// the ranks before the square root
+template <typename T>
+static void dresidual(Work<T>& w, int mode, int64_t m, const T* X, const T* AX, const void* dinv,
+                      T* Wdst, int* ovf) {
+  Comm* c = dist(w.ctx);
+  residual_precond<T>(mode, w.n, m, X, w.ld, AX, w.ld, w.theta.p, dinv, Wdst, w.ld, w.rnorm(),
+                      w.xnorm(), ovf, w.rw.p, w.s, c ? 1 : 0);
+  if (c) {
+    c->allreduce_sum(w.rnorm(), 2 * m, w.s);  // rnorm, xnorm are adjacent
+    norms_sqrt<T>(2 * m, w.rnorm(), w.s);
+  }
+}
+
+// R of the row-sharded block: each rank's TSQR R, gathered, stacked and
+// factored again (a TSQR tree whose top level spans the ranks); every rank
+// computes the same global R, then Rw = R (working precision), Rinv = R^-1.
+template <typename T>
+static void tsqr_R(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, int* status) {
+  const int64_t n = w.n;
+  cudaStream_t s = w.s;
+  Comm* c = dist(w.ctx);
+  if (!c) {
+    if constexpr (sizeof(T) == 8) {
+      if (lower) {
+        // fp32 R_l, then R_l in fp64 and R_l^-1 (fused into the TSQR root)
+        tsqr_r<double, float>(n, m, W, ldw, w.smallf.p, m, w.tsqr_f.p, status, s, w.Rw(), w.Rinv());
+        return;
+      }
+    }
+    tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, status, s, nullptr, w.Rinv());
+    return;
+  }
+  const int64_t P = c->nranks, mm = m * m;
+  if constexpr (sizeof(T) == 8) {
+    if (lower) {
+      tsqr_r<double, float>(n, m, W, ldw, w.smallf.p, m, w.tsqr_f.p, status, s, nullptr, nullptr, 0);
+      c->allgather(w.smallf.p, w.rstkf.p, static_cast<int64_t>(sizeof(float)) * mm, s);
+      for (int64_t r = 0; r < P; ++r)
+        MPB_CUDA(cudaMemcpy2DAsync(w.rstk2f.p + r * m, sizeof(float) * P * m, w.rstkf.p + r * mm,
+                                   sizeof(float) * m, sizeof(float) * m, m, cudaMemcpyDeviceToDevice,
+                                   s));
+      tsqr_r<float, float>(P * m, m, w.rstk2f.p, P * m, w.smallf.p, m, w.tsqr_f2.p, status, s,
+                           nullptr, nullptr, 0);
+      tsqr_epilogue<double, float>(m, w.smallf.p, m, w.Rw(), w.Rinv(), status, s);
+      return;
+    }
+  }
+  tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, status, s, nullptr, nullptr, 0);
+  c->allgather(w.Rw(), w.rstk.p, static_cast<int64_t>(sizeof(T)) * mm, s);
+  for (int64_t r = 0; r < P; ++r)
+    MPB_CUDA(cudaMemcpy2DAsync(w.rstk2.p + r * m, sizeof(T) * P * m, w.rstk.p + r * mm,
+                               sizeof(T) * m, sizeof(T) * m, m, cudaMemcpyDeviceToDevice, s));
+  tsqr_r<T, T>(P * m, m, w.rstk2.p, P * m, w.Rw(), m, w.tsqr_w2.p, status, s, nullptr, w.Rinv());
+}
+
+// CholQR's Gram + Cholesky (fused on one GPU)
+template <typename T>
+static void gram_chol(Work<T>& w, int64_t m, int* status) {
+  if (!dist(w.ctx) &&
+      gram_cholesky<T>(w.n, m, w.V.p, w.ld, w.G.p, w.gramw.p, w.L(), w.Uinv(), status, w.s))
+    return;
+  dgram<T>(w, m, w.V.p, w.ld, m, w.V.p, w.ld, w.G.p, m, 1);
+  small_cholesky_inv<T>(m, w.G.p, m, w.L(), w.Uinv(), status, w.s);
+}
+
 // ------------------------------------------------------------- QR family
 // Q (in place) by "R from a Householder TSQR, then Cholesky-QR of W R^-1":
 //   lower = true  (T = double): Alg. 2 / mixed_qr (ortho.hpp:173-186) --
@@ -279,22 +406,9 @@ static int qr_core(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, T* Rout
   cudaStream_t s = w.s;
   const int64_t n = w.n;
   status_clear(ctx);
-  if constexpr (sizeof(T) == 8) {
-    if (lower) {
-      // fp32 R_l, then R_l in fp64 and R_l^-1 (fused into the TSQR root)
-      tsqr_r<double, float>(n, m, W, ldw, w.smallf.p, m, w.tsqr_f.p, ctx->d_status, s, w.Rw(), w.Rinv());
-    } else {
-      tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, ctx->d_status, s, nullptr, w.Rinv());
-    }
-  } else {
-    (void)lower;
-    tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, ctx->d_status, s, nullptr, w.Rinv());
-  }
+  tsqr_R<T>(w, m, W, ldw, lower, ctx->d_status);
   gemm_tn<T>(n, m, m, T(1), W, ldw, w.Rinv(), m, T(0), nullptr, 0, w.V.p, w.ld, s);
-  if (!gram_cholesky<T>(n, m, w.V.p, w.ld, w.G.p, w.gramw.p, w.L(), w.Uinv(), ctx->d_status, s)) {
-    gram<T>(n, m, w.V.p, w.ld, m, w.V.p, w.ld, w.G.p, m, 1, w.gramw.p, s);
-    small_cholesky_inv<T>(m, w.G.p, m, w.L(), w.Uinv(), ctx->d_status, s);
-  }
+  gram_chol<T>(w, m, ctx->d_status);
   status_fetch(ctx);
   const int code = ctx->h_status[0];
   *idx = ctx->h_status[1];
@@ -342,16 +456,16 @@ int64_t ortho_dropping(Work<T>& w, int64_t m, T* W, int64_t ldw, T drop_tol) {
   int64_t kept = 0;
   for (int64_t j = 0; j < m; ++j) {
     copy_block<T>(n, 1, W + j * ldw, ldw, v, w.ld, s);
-    frob_sq<T>(n, 1, v, w.ld, d2, w.rw.p, s);
+    dfrob<T>(w, n, v, w.ld, d2);
     MPB_CUDA(cudaMemcpyAsync(&h2, d2, sizeof(double), cudaMemcpyDeviceToHost, s));
     MPB_CUDA(cudaStreamSynchronize(s));
     const T n0 = static_cast<T>(std::sqrt(h2));
     if (n0 == T(0)) continue;
     for (int pass = 0; pass < 2 && kept > 0; ++pass) {
-      gram<T>(n, kept, W, ldw, 1, v, w.ld, g, kept, 0, w.gramw.p, s);
+      dgram<T>(w, kept, W, ldw, 1, v, w.ld, g, kept, 0);
       gemm_tn<T>(n, kept, 1, T(-1), W, ldw, g, kept, T(1), v, w.ld, v, w.ld, s);
     }
-    frob_sq<T>(n, 1, v, w.ld, d2, w.rw.p, s);
+    dfrob<T>(w, n, v, w.ld, d2);
     MPB_CUDA(cudaMemcpyAsync(&h2, d2, sizeof(double), cudaMemcpyDeviceToHost, s));
     MPB_CUDA(cudaStreamSynchronize(s));
     const T nv = static_cast<T>(std::sqrt(h2));
@@ -385,7 +499,7 @@ void project_out(Work<T>& w, const T* B, int64_t b, int64_t ldb, T* W, int64_t w
                  int passes) {
   if (b == 0 || wc == 0) return;
   for (int p = 0; p < passes; ++p) {
-    gram<T>(w.n, b, B, ldb, wc, W, ldw, w.G.p, b, 0, w.gramw.p, w.s);
+    dgram<T>(w, b, B, ldb, wc, W, ldw, w.G.p, b, 0);
     gemm_tn<T>(w.n, b, wc, T(-1), B, ldb, w.G.p, b, T(1), W, ldw, W, ldw, w.s);
   }
 }
@@ -395,7 +509,7 @@ void project_out(Work<T>& w, const T* B, int64_t b, int64_t ldb, T* W, int64_t w
 template <typename T>
 void ritz_rotate(Work<T>& w) {
   const int64_t m = w.m;
-  gram<T>(w.n, m, w.S.p, w.ld, m, w.AS.p, w.ld, w.G.p, m, 1, w.gramw.p, w.s);
+  dgram<T>(w, m, w.S.p, w.ld, m, w.AS.p, w.ld, w.G.p, m, 1);
   small_eig<T>(w, m, w.G.p, m, w.evals.p);
   gemm_tn_pair<T>(w.n, m, m, w.S.p, w.AS.p, w.ld, w.G.p, m, w.S2.p, w.AS2.p, w.ld, w.s);
   MPB_CUDA(cudaMemcpyAsync(w.theta.p, w.evals.p, sizeof(T) * m, cudaMemcpyDeviceToDevice, w.s));
@@ -417,9 +531,7 @@ static bool residual_step(Work<T>& w, const mpeig_op* T_op, const T* X, const T*
   int mode = kResidPlain;
   if (fused) mode = jacobi_mode<T>(T_op, &dinv);
   status_clear(ctx);
-  residual_precond<T>(mode, w.n, m, X, w.ld, AX, w.ld, w.theta.p, dinv,
-                      fused ? Wdst : w.V.p, w.ld, w.rnorm(), w.xnorm(), ctx->d_status + 2,
-                      w.rw.p, w.s);
+  dresidual<T>(w, mode, m, X, AX, dinv, fused ? Wdst : w.V.p, ctx->d_status + 2);
   std::vector<T> th(static_cast<size_t>(m));
   MPB_CUDA(cudaMemcpyAsync(th.data(), w.theta.p, sizeof(T) * m, cudaMemcpyDeviceToHost, w.s));
   MPB_CUDA(cudaMemcpyAsync(ctx->h_pinned, w.rnorm(), sizeof(double) * 2 * m, cudaMemcpyDeviceToHost,
@@ -595,7 +707,7 @@ StageResult lobpcg_stage_eager(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, con
     timer.start();
     const int64_t sdim = m + p + wc;
     status_clear(ctx);
-    gram<T>(n, sdim, w.S.p, w.ld, sdim, w.AS.p, w.ld, w.G.p, sdim, 1, w.gramw.p, s);
+    dgram<T>(w, sdim, w.S.p, w.ld, sdim, w.AS.p, w.ld, w.G.p, sdim, 1);
     std::vector<T> dbgG;
     if (getenv("MPEIG_DUMP_G_ITER") &&
         (atol(getenv("MPEIG_DUMP_G_ITER")) == iter || atol(getenv("MPEIG_DUMP_G_ITER")) < 0)) {
@@ -665,22 +777,9 @@ template <typename T>
 static void qr_spec(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, int* status) {
   cudaStream_t s = w.s;
   const int64_t n = w.n;
-  if constexpr (sizeof(T) == 8) {
-    if (lower) {
-      // fp32 R_l, then R_l in fp64 and R_l^-1 (fused into the TSQR root)
-      tsqr_r<double, float>(n, m, W, ldw, w.smallf.p, m, w.tsqr_f.p, status, s, w.Rw(), w.Rinv());
-    } else {
-      tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, status, s, nullptr, w.Rinv());
-    }
-  } else {
-    (void)lower;
-    tsqr_r<T, T>(n, m, W, ldw, w.Rw(), m, w.tsqr_w.p, status, s, nullptr, w.Rinv());
-  }
+  tsqr_R<T>(w, m, W, ldw, lower, status);
   gemm_tn<T>(n, m, m, T(1), W, ldw, w.Rinv(), m, T(0), nullptr, 0, w.V.p, w.ld, s);
-  if (!gram_cholesky<T>(n, m, w.V.p, w.ld, w.G.p, w.gramw.p, w.L(), w.Uinv(), status, s)) {
-    gram<T>(n, m, w.V.p, w.ld, m, w.V.p, w.ld, w.G.p, m, 1, w.gramw.p, s);
-    small_cholesky_inv<T>(m, w.G.p, m, w.L(), w.Uinv(), status, s);
-  }
+  gram_chol<T>(w, m, status);
   gemm_tn<T>(n, m, m, T(1), w.V.p, w.ld, w.Uinv(), m, T(0), nullptr, 0, W, ldw, s);
 }
 
@@ -695,12 +794,12 @@ static void resid_launch(Work<T>& w, const mpeig_op* T_op, const T* S, const T* 
   const void* dinv = nullptr;
   int mode = kResidPlain;
   if (fused) mode = jacobi_mode<T>(T_op, &dinv);
-  residual_precond<T>(mode, w.n, m, S, w.ld, AS, w.ld, w.theta.p, dinv, fused ? Wslot : w.V.p,
-                      w.ld, w.rnorm(), w.xnorm(), ctx->d_status + kSlotOvf, w.rw.p, w.s);
+  dresidual<T>(w, mode, m, S, AS, dinv, fused ? Wslot : w.V.p, ctx->d_status + kSlotOvf);
   MPB_CUDA(cudaMemcpyAsync(ctx->h_pinned, w.rnorm(), sizeof(double) * 2 * m,
                            cudaMemcpyDeviceToHost, w.s));
   MPB_CUDA(cudaMemcpyAsync(ctx->h_pinned + 2 * m, w.theta.p, sizeof(T) * m, cudaMemcpyDeviceToHost,
                            w.s));
+  if (Comm* c = dist(ctx)) c->allreduce_max(ctx->d_status, 16, w.s);
   MPB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->d_status, 16 * sizeof(int), cudaMemcpyDeviceToHost,
                            w.s));
 }
@@ -757,7 +856,7 @@ static void spec_body(Work<T>& w, const mpeig_op* A, const mpeig_op* T_op, int64
   if (ev.on) MPB_CUDA(cudaEventRecord(ev.e[1], s));
   op_apply<T>(ctx, A, m, Wslot, ld, AS + (m + p) * ld, ld);
   const int64_t sdim = 2 * m + p;
-  gram<T>(n, sdim, S, ld, sdim, AS, ld, w.G.p, sdim, 1, w.gramw.p, s);
+  dgram<T>(w, sdim, S, ld, sdim, AS, ld, w.G.p, sdim, 1);
   small_syev<T>(sdim, w.G.p, sdim, w.evals.p, ctx->d_status + kSlotEig, s);
   const int64_t pn = std::min(m, sdim - m);
   if constexpr (sizeof(T) == 8)
@@ -802,7 +901,8 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
   mpeig_timings local{};
   mpeig_timings& tm = tim ? *tim : local;
   const bool mixed = opt.use_mixed_qr != 0;
-  const bool use_graphs = ctx->use_graphs != 0 && !g_prof_on;
+  // (row-sharded runs exchange through the host or NCCL inside the body: no graph)
+  const bool use_graphs = ctx->use_graphs != 0 && !g_prof_on && !dist(ctx);
 
   copy_block<T>(n, m, X0, ldx0, w.S.p, w.ld, s);
   op_apply<T>(ctx, A, m, w.S.p, w.ld, w.AS.p, w.ld);
@@ -930,8 +1030,7 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
         T* Wslot = w.S.p + (m + p) * w.ld;
         const void* dinv = nullptr;
         const int mode = jacobi_mode<T>(T_op, &dinv);
-        residual_precond<T>(mode, n, m, w.S.p, w.ld, w.AS.p, w.ld, w.theta.p, dinv, Wslot, w.ld,
-                            w.rnorm(), w.xnorm(), ctx->d_status + kSlotOvf, w.rw.p, s);
+        dresidual<T>(w, mode, m, w.S.p, w.AS.p, dinv, Wslot, ctx->d_status + kSlotOvf);
         timer.start();
         const int64_t b = m + p;
         int64_t wc = m;
@@ -953,7 +1052,7 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
         timer.start();
         const int64_t sdim = m + p + wc;
         status_clear(ctx);
-        gram<T>(n, sdim, w.S.p, w.ld, sdim, w.AS.p, w.ld, w.G.p, sdim, 1, w.gramw.p, s);
+        dgram<T>(w, sdim, w.S.p, w.ld, sdim, w.AS.p, w.ld, w.G.p, sdim, 1);
         small_eig<T>(w, sdim, w.G.p, sdim, w.evals.p);
         pn = std::min(m, sdim - m);
         if constexpr (sizeof(T) == 8)
@@ -1054,10 +1153,12 @@ double spectral_norm_estimate(mpeig_ctx* ctx, const mpeig_op* A, int64_t sketch_
   const int64_t n = A->n;
   const int64_t ld = padded_ld(n);
   std::vector<double> om(static_cast<size_t>(n * sketch_rows));
-  gaussian_fill(n, sketch_rows, seed, om.data());
+  if (A->n_global > n)  // this rank's rows of the global sketch
+    gaussian_fill_rows(A->n_global, sketch_rows, seed, A->row0, n, om.data());
+  else
+    gaussian_fill(n, sketch_rows, seed, om.data());
   double den2 = 0;  // frobenius_norm, sequential like the reference
   for (double v : om) den2 += std::abs(v) * std::abs(v);
-  const double denom = std::sqrt(den2);
   cudaStream_t s = ctx->stream;
   DevBuf<double> O(static_cast<size_t>(ld * sketch_rows), s), Y(static_cast<size_t>(ld * sketch_rows), s),
       wk(kNumSMs * 2 + 2, s);
@@ -1065,11 +1166,18 @@ double spectral_norm_estimate(mpeig_ctx* ctx, const mpeig_op* A, int64_t sketch_
                              sizeof(double) * n, sketch_rows, cudaMemcpyHostToDevice, s));
   op_apply<double>(ctx, A, sketch_rows, O.p, ld, Y.p, ld);
   frob_sq<double>(n, sketch_rows, Y.p, ld, wk.p + kNumSMs * 2, wk.p, s);
-  double y2 = 0;
-  MPB_CUDA(cudaMemcpyAsync(&y2, wk.p + kNumSMs * 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+  double h[2] = {0, den2};
+  if (Comm* c = dist(ctx)) {
+    MPB_CUDA(cudaMemcpyAsync(wk.p + kNumSMs * 2 + 1, &h[1], sizeof(double), cudaMemcpyHostToDevice, s));
+    c->allreduce_sum(wk.p + kNumSMs * 2, 2, s);
+    MPB_CUDA(cudaMemcpyAsync(h, wk.p + kNumSMs * 2, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  } else {
+    MPB_CUDA(cudaMemcpyAsync(h, wk.p + kNumSMs * 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
   MPB_CUDA(cudaStreamSynchronize(s));
+  const double denom = std::sqrt(h[1]);
   if (denom == 0) return 0;
-  return std::sqrt(y2) / denom;
+  return std::sqrt(h[0]) / denom;
 }
 
 // run_variant (drivers.hpp:57-111) on a device start block
@@ -1130,13 +1238,16 @@ void run_variant(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T_op, const 
 void solve(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T_op, const mpeig_cfg& cfg,
            mpeig_history_sink sink, void* sink_user, mpeig_result* out) {
   const int64_t n = A->n;
-  validate_cfg(cfg, n);
+  validate_cfg(cfg, A->n_global > n ? A->n_global : n);
   const int64_t m = cfg.block != 0 ? cfg.block : (3 * cfg.k + 1) / 2;
   const auto t0 = std::chrono::steady_clock::now();
   const double est =
       spectral_norm_estimate(ctx, A, cfg.sketch_rows, cfg.seed ^ 0x9e3779b97f4a7c15ULL);
   std::vector<double> g(static_cast<size_t>(n * m));
-  gaussian_fill(n, m, cfg.seed, g.data());
+  if (A->n_global > n)  // this rank's rows of the global start block
+    gaussian_fill_rows(A->n_global, m, cfg.seed, A->row0, n, g.data());
+  else
+    gaussian_fill(n, m, cfg.seed, g.data());
   const int64_t ld = padded_ld(n);
   cudaStream_t s = ctx->stream;
   DevBuf<double> X0(static_cast<size_t>(ld * m), s);
@@ -1160,7 +1271,7 @@ void solve_prepared(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T_op, con
                     const double* X0raw, int64_t ldx0, const double* omega, int64_t ldo,
                     double omega_fro, mpeig_history_sink sink, void* sink_user, mpeig_result* out) {
   const int64_t n = A->n;
-  validate_cfg(cfg, n);
+  validate_cfg(cfg, A->n_global > n ? A->n_global : n);
   const int64_t m = cfg.block != 0 ? cfg.block : (3 * cfg.k + 1) / 2;
   const auto t0 = std::chrono::steady_clock::now();
   cudaStream_t s = ctx->stream;
@@ -1172,6 +1283,7 @@ void solve_prepared(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T_op, con
     op_apply<double>(ctx, A, sr, omega, ldo, Y.p, ld);
     frob_sq<double>(n, sr, Y.p, ld, wk.p + kNumSMs * 2, wk.p, s);
     if (omega_fro <= 0) frob_sq<double>(n, sr, omega, ldo, wk.p + kNumSMs * 2 + 1, wk.p, s);
+    if (Comm* c = dist(ctx)) c->allreduce_sum(wk.p + kNumSMs * 2, omega_fro <= 0 ? 2 : 1, s);
     double h[2] = {0, 0};
     MPB_CUDA(cudaMemcpyAsync(h, wk.p + kNumSMs * 2, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
     MPB_CUDA(cudaStreamSynchronize(s));

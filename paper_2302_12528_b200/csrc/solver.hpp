@@ -29,6 +29,10 @@ struct Work {
   DevBuf<T> theta_prev;  // Ritz values before the last speculative update
   DevBuf<T> eigw;
   int lwork = 0;
+  // row-sharded mode: gathered per-rank R factors, stacked, and the TSQR
+  // workspace of the (nranks m) x m stack
+  DevBuf<T> rstk, rstk2, tsqr_w2;
+  DevBuf<float> rstkf, rstk2f, tsqr_f2;
 
   Work(mpeig_ctx* c, int64_t n_, int64_t m_, int64_t smax_);
   T* L();

@@ -536,7 +536,8 @@ int64_t tsqr_workspace_elems(int64_t n, int64_t m) {
 
 template <typename Tin, typename Tq>
 void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr, Tq* work,
-            int* status, cudaStream_t s, Tin* Rw_out, Tin* Rinv_out) {
+            int* status, cudaStream_t s, Tin* Rw_out, Tin* Rinv_out, int rank_check) {
+  const int numeric = rank_check < 0 ? (sizeof(Tin) == sizeof(Tq) ? 1 : 0) : rank_check;
   const int mi = static_cast<int>(m);
   const RegPlan rp = reg_plan<Tq>(n, m);
   const RegKernel<Tin, Tq> rk = rp.cfg.nw ? reg_kernel<Tin, Tq>(rp.cfg) : nullptr;
@@ -545,8 +546,8 @@ void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr,
     int* ctr = reinterpret_cast<int*>(work + rp.r_elems);
     const bool fuse = Rinv_out && m <= 16;
     rk<<<static_cast<unsigned>(rp.nleaf), rp.cfg.nw * 32, 0, s>>>(
-        n, mi, W, ldw, work, ctr, rp.nleaf, static_cast<int>(rp.G), R, ldr, status,
-        sizeof(Tin) == sizeof(Tq), fuse ? Rw_out : nullptr, fuse ? Rinv_out : nullptr);
+        n, mi, W, ldw, work, ctr, rp.nleaf, static_cast<int>(rp.G), R, ldr, status, numeric,
+        fuse ? Rw_out : nullptr, fuse ? Rinv_out : nullptr);
     MPB_LAUNCH_CHECK();
     if (Rinv_out && !fuse) tsqr_epilogue<Tin, Tq>(m, R, ldr, Rw_out, Rinv_out, status, s);
     return;
@@ -574,7 +575,7 @@ void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr,
     std::swap(bufA, bufB);
     nR = nout;
   }
-  k_tsqr_finish<Tq><<<1, 256, 0, s>>>(mi, bufA, R, ldr, status, sizeof(Tin) == sizeof(Tq));
+  k_tsqr_finish<Tq><<<1, 256, 0, s>>>(mi, bufA, R, ldr, status, numeric);
   MPB_LAUNCH_CHECK();
   if (Rinv_out) tsqr_epilogue<Tin, Tq>(m, R, ldr, Rw_out, Rinv_out, status, s);
 }
@@ -583,10 +584,16 @@ template int64_t tsqr_workspace_elems<double, double>(int64_t, int64_t);
 template int64_t tsqr_workspace_elems<double, float>(int64_t, int64_t);
 template int64_t tsqr_workspace_elems<float, float>(int64_t, int64_t);
 template void tsqr_r<double, double>(int64_t, int64_t, const double*, int64_t, double*, int64_t,
-                                     double*, int*, cudaStream_t, double*, double*);
+                                     double*, int*, cudaStream_t, double*, double*, int);
 template void tsqr_r<double, float>(int64_t, int64_t, const double*, int64_t, float*, int64_t,
-                                    float*, int*, cudaStream_t, double*, double*);
+                                    float*, int*, cudaStream_t, double*, double*, int);
 template void tsqr_r<float, float>(int64_t, int64_t, const float*, int64_t, float*, int64_t,
-                                   float*, int*, cudaStream_t, float*, float*);
+                                   float*, int*, cudaStream_t, float*, float*, int);
+template void tsqr_epilogue<double, double>(int64_t, const double*, int64_t, double*, double*, int*,
+                                            cudaStream_t);
+template void tsqr_epilogue<double, float>(int64_t, const float*, int64_t, double*, double*, int*,
+                                           cudaStream_t);
+template void tsqr_epilogue<float, float>(int64_t, const float*, int64_t, float*, float*, int*,
+                                          cudaStream_t);
 
 }  // namespace mpb

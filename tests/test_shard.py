@@ -1,0 +1,153 @@
+"""Row-sharded (multi-GPU) path, SURVEY.md §8(e).
+
+CPU: the sharding arithmetic that must agree across ranks (start-block row
+slices bit for bit, slab partition) and the N > 1 launcher plumbing (NCCL id
+creation + broadcast over a world-size-2 gloo group).
+GPU: the sharded solver with ranks as threads of one process (host-staged
+exchanges, rank-ordered sums) against the single-GPU solve and the global
+operator.  NCCL itself needs one GPU per rank and is exercised by the
+multi-GPU bench (bench.py --shard).
+"""
+import os
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2302_12528_b200 as mp
+
+
+@pytest.mark.parametrize("n,cols,parts", [(97, 5, 3), (1000, 3, 4), (64, 2, 1), (33, 7, 5)])
+def test_gaussian_row_slices_bitwise(n, cols, parts):
+    """Each rank draws exactly its rows of gaussian_matrix (dense_matrix.hpp:144-161)."""
+    G = mp.gaussian_matrix(n, cols, 11)
+    bounds = np.linspace(0, n, parts + 1).astype(int)
+    got = np.vstack([mp.gaussian_matrix_rows(n, cols, 11, a, b - a)
+                     for a, b in zip(bounds[:-1], bounds[1:])])
+    assert np.array_equal(got, G)
+
+
+def test_slab_partition():
+    for nz, p in [(32, 3), (8, 8), (256, 8), (7, 2)]:
+        sl = mp.slab_partition(nz, p)
+        assert sum(n for _, n in sl) == nz and sl[0][0] == 0
+        assert all(a + n == b for (a, n), (b, _) in zip(sl, sl[1:]))
+        assert max(n for _, n in sl) - min(n for _, n in sl) <= 1
+
+
+def _gloo_worker(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    uid = mp.broadcast_unique_id(rank)
+    out.put((rank, uid, mp.slab_partition(32, world)[rank]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_nccl_id_broadcast_world2():
+    """The N > 1 launcher path: rank 0's NCCL id reaches rank 1 (gloo, CPU)."""
+    import socket
+
+    import torch.multiprocessing as tmp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (u, sl)) for r, u, sl in (q.get(timeout=120) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert len(res[0][0]) == 128 and res[0][0] == res[1][0]
+    assert res[0][1] == (0, 16) and res[1][1] == (16, 16)
+
+
+# ------------------------------------------------------------------ GPU
+
+
+def _run_ranks(nranks, dims, fn):
+    """fn(rank, ctx, op_slab) on `nranks` threads sharing one HostGroup."""
+    import torch
+    nx, ny, nz = dims
+    group = mp.HostGroup(nranks)
+    slabs = mp.slab_partition(nz, nranks)
+    out, errs = [None] * nranks, []
+
+    def work(r):
+        try:
+            ctx = mp.Context(0, stream=torch.cuda.Stream())
+            ctx.attach_host(group, r)
+            z0, nl = slabs[r]
+            A = mp.laplace3d_slab(nx, ny, nz, z0, nl, ctx=ctx)
+            out[r] = fn(r, ctx, A)
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_sharded_stencil_apply_bitwise(gpu, nranks):
+    """Halo exchange + slab apply == the global apply, bit for bit."""
+    dims = (9, 8, 13)
+    n = int(np.prod(dims))
+    X = np.asfortranarray(np.random.default_rng(3).standard_normal((n, 4)))
+    Y = mp.to_host(gpu.laplace3d(*dims).apply(mp.to_device(X)))
+    sl = mp.slab_partition(dims[2], nranks)
+    plane = dims[0] * dims[1]
+
+    def fn(r, ctx, A):
+        z0, nl = sl[r]
+        Xl = np.asfortranarray(X[z0 * plane:(z0 + nl) * plane])
+        return mp.to_host(A.apply(mp.to_device(Xl)))
+
+    parts = _run_ranks(nranks, dims, fn)
+    assert np.array_equal(np.vstack(parts), Y)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["dlobpcg-dchol", "mplobpcg-schol"])
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_sharded_solve_matches_single_gpu(gpu, nranks, variant):
+    """Row-sharded solve == single-GPU solve: theta to 1e-10, residual contract
+    on the gathered X, iteration count within the rounding band."""
+    dims = (10, 11, 12)
+    cfg = mp.SolverConfig(k=5, tol=1e-10, maxit=1500, variant=variant)
+    prec = mp.WORKING if variant == "dlobpcg-dchol" else mp.LOWER
+    A1 = gpu.laplace3d(*dims)
+    r1 = gpu.solve(A1, cfg, T=gpu.jacobi(A1, prec))
+
+    def fn(r, ctx, A):
+        res = mp.solve(A, cfg, T=mp.jacobi(A, prec))
+        return res, mp.to_host(res.X)
+
+    outs = _run_ranks(nranks, dims, fn)
+    th0 = outs[0][0].theta
+    for res, _ in outs:  # every rank holds the same replicated results
+        assert np.array_equal(res.theta, th0)
+        assert (res.iterations_lower, res.iterations_working) == (
+            outs[0][0].iterations_lower, outs[0][0].iterations_working)
+    res = outs[0][0]
+    assert res.converged
+    assert np.abs(res.theta - r1.theta).max() <= 1e-10 * np.abs(r1.theta).max()
+    tot1 = r1.iterations_lower + r1.iterations_working
+    tot = res.iterations_lower + res.iterations_working
+    assert abs(tot - tot1) <= max(2, int(0.1 * tot1)), (tot, tot1)
+    X = np.vstack([x for _, x in outs])
+    assert np.linalg.norm(X.T @ X - np.eye(cfg.k)) < 1e-10
+    AX = mp.to_host(A1.apply(mp.to_device(np.asfortranarray(X))))
+    rn = np.linalg.norm(AX - X * res.theta, axis=0)
+    assert np.all(rn <= 10 * cfg.tol * (res.a_norm_estimate + res.theta))
