@@ -35,6 +35,11 @@ sys.path.insert(0, ROOT)
 WORKLOADS = {
     "cfg1": dict(dims=(32, 32, 32), k=10, block=16, tol=1e-10, maxit=2000, seed=0,
                  desc="3-D 7-pt Laplacian 32^3 (n=32768), k=10, m=16, tol 1e-10, Jacobi f_T"),
+    # larger row-sharded workloads (bench.py --shard under torchrun)
+    "lap3d128": dict(dims=(128, 128, 128), k=32, block=48, tol=1e-10, maxit=20000, seed=0,
+                     desc="3-D 7-pt Laplacian 128^3 (n=2.1M), k=32, m=48, tol 1e-10, Jacobi f_T"),
+    "cfg4": dict(dims=(256, 256, 256), k=64, block=80, tol=1e-10, maxit=20000, seed=0,
+                 desc="3-D 7-pt Laplacian 256^3 (n=16.8M), k=64, m=80, tol 1e-10, Jacobi f_T"),
 }
 METRIC = "LOBPCG time-to-solution (k eigpairs, tol 1e-10)"
 REF_SAMPLE_ITERS = 10  # per stage, per reference sample
@@ -173,18 +178,36 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     w = WORKLOADS[args.workload]
+    shard = args.shard and world > 1
     ctx = mp.Context(local)
-    A = mp.laplace3d(*w["dims"], ctx=ctx)
     cfg = mp.SolverConfig(k=w["k"], block=w["block"], tol=w["tol"], maxit=w["maxit"], seed=w["seed"],
                           variant=args.variant)
+    m, k, sr = cfg.block_size(), cfg.k, cfg.sketch_rows
+    if shard:
+        # row-sharded solve: rank r owns z-slab r; Gram / norm
+        # allreduce, R allgather and halo planes over NCCL (NVLink / NVSwitch)
+        ctx.attach_nccl(rank, world, mp.broadcast_unique_id(rank))
+        nx, ny, nz = w["dims"]
+        z0, nzl = mp.slab_partition(nz, world)[rank]
+        A = mp.laplace3d_slab(nx, ny, nz, z0, nzl, ctx=ctx)
+        n_glob, row0 = nx * ny * nz, nx * ny * z0
+    else:
+        A = mp.laplace3d(*w["dims"], ctx=ctx)
+        n_glob, row0 = A.n, 0
     T = mp.jacobi(A, mp.build_precision_for(args.variant))
-    n, m, k, sr = A.n, cfg.block_size(), cfg.k, cfg.sketch_rows
+    n = A.n
     dev = f"cuda:{local}"
 
-    # inputs: gaussian_matrix(n, m, seed) and the sketch Omega, drawn once on the host
-    X0h = mp.gaussian_matrix(n, m, cfg.seed)
-    Omh = mp.gaussian_matrix(n, sr, cfg.seed ^ 0x9E3779B97F4A7C15)
-    om_fro = float(np.sqrt(np.sum(np.abs(Omh.ravel(order="F")) ** 2)))
+    # inputs: gaussian_matrix(n, m, seed) and the sketch Omega (this rank's
+    # rows when sharded), drawn once on the host
+    if shard:
+        X0h = mp.gaussian_matrix_rows(n_glob, m, cfg.seed, row0, n)
+        Omh = mp.gaussian_matrix_rows(n_glob, sr, cfg.seed ^ 0x9E3779B97F4A7C15, row0, n)
+        om_fro = 0.0  # ||Omega||_F reduced over the ranks on the device
+    else:
+        X0h = mp.gaussian_matrix(n, m, cfg.seed)
+        Omh = mp.gaussian_matrix(n, sr, cfg.seed ^ 0x9E3779B97F4A7C15)
+        om_fro = float(np.sqrt(np.sum(np.abs(Omh.ravel(order="F")) ** 2)))
     X0pin = torch.from_numpy(np.ascontiguousarray(X0h.T)).pin_memory()
     Ompin = torch.from_numpy(np.ascontiguousarray(Omh.T)).pin_memory()
     X0d, Omd = X0pin.to(dev), Ompin.to(dev)
@@ -279,7 +302,7 @@ def run_ours(args):
                 "launches": v["count"], "share_of_solve": kernels[top]["share"]}
     gi = golden_iters(args.workload, args.variant)
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and args.workload == "cfg1":
         v, sample, kind = reference_sample(args.workload, args.variant)
         cpu = {"value": v, "unit": "s", "cores": 1, "kind": kind, "sample": sample}
     theta_err = None
@@ -288,11 +311,13 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(args.variant),
+        "scaling": "strong" if shard else "weak", "vs_baseline": None,
+        "dtype": dtype_of(args.variant),
         "data": "synthetic (deterministic Laplacian, seeded PCG64 start block)",
         "config": {"workload": f"{args.workload}: {w['desc']}", "variant": args.variant,
                    "l2": "flushed (256 MB write) before every solve",
-                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "parallelism": (f"row-sharded over {world} GPUs (NCCL)" if shard else
+                                   "replicas" if world > 1 else "single GPU"),
                    "iterations": {"lower": iters[-1][0], "working": iters[-1][1]},
                    "reference_iterations": {"lower": gi["lower"], "working": gi["working"]} if gi else None,
                    "theta_max_rel_err_vs_reference": theta_err,
@@ -320,6 +345,9 @@ def main():
     ap.add_argument("--variant", default="mplobpcg-schol",
                     choices=["mplobpcg-schol", "dlobpcg-schol", "dlobpcg-dchol", "pinvit"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="N > 1: one row-sharded solve over the N GPUs (strong scaling) "
+                         "instead of N independent replicas")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

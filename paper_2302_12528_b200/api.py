@@ -279,11 +279,13 @@ def broadcast_unique_id(rank: int, group=None) -> bytes:
     backend, e.g. gloo), for Context.attach_nccl."""
     import torch
     import torch.distributed as dist_
-    buf = torch.zeros(128, dtype=torch.uint8)
+    on_gpu = dist_.get_backend(group) == "nccl"
+    buf = torch.zeros(128, dtype=torch.uint8,
+                      device=f"cuda:{torch.cuda.current_device()}" if on_gpu else "cpu")
     if rank == 0:
-        buf[:] = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8)
+        buf[:] = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8).to(buf.device)
     dist_.broadcast(buf, src=0, group=group)
-    return bytes(buf.tolist())
+    return bytes(buf.cpu().tolist())
 
 
 def slab_partition(nz: int, nranks: int):
