@@ -56,6 +56,74 @@ k_stencil7(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t 
   Y[p + j * ldy] = s;
 }
 
+// Vectorised form (nx a multiple of V): a thread computes V consecutive x
+// points with V-wide loads of its own, the y +- 1 and z +- 1 rows, plus the
+// two scalar x neighbours -- 5 vector + 2 scalar loads for V points instead
+// of 7 V scalar loads.  Per-point summation order unchanged (bitwise equal).
+template <typename T, int V>
+struct VecT;
+template <>
+struct VecT<double, 2> {
+  using type = double2;
+};
+template <>
+struct VecT<float, 4> {
+  using type = float4;
+};
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256)
+k_stencil7_vec(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t ldx,
+               T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi) {
+  using VT = typename VecT<T, V>::type;
+  const int64_t nv = nx * ny * nz / V;
+  const int64_t pv = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (pv >= nv) return;
+  const int64_t j = blockIdx.y;
+  const int64_t p = pv * V;
+  const T* x = X + j * ldx;
+  const int64_t xi = p % nx;
+  const int64_t yz = p / nx;
+  const int64_t yi = yz % ny;
+  const int64_t zi = yz / ny;
+  const int64_t sy = nx, sz = nx * ny;
+  auto ldv = [](const T* a) {
+    const VT v = *reinterpret_cast<const VT*>(a);
+    return v;
+  };
+  const VT c = ldv(x + p);
+  VT zm{}, ym{}, yp{}, zp{};
+  const bool hz_m = zi > 0 || hlo, hz_p = zi + 1 < nz || hhi;
+  if (zi > 0) zm = ldv(x + p - sz);
+  else if (hlo) zm = ldv(hlo + p + j * sz);
+  if (yi > 0) ym = ldv(x + p - sy);
+  if (yi + 1 < ny) yp = ldv(x + p + sy);
+  if (zi + 1 < nz) zp = ldv(x + p + sz);
+  else if (hhi) zp = ldv(hhi + p - (nz - 1) * sz + j * sz);
+  const T xl = xi > 0 ? x[p - 1] : T(0);
+  const T xr = xi + V < nx ? x[p + V] : T(0);
+  const T* cv = reinterpret_cast<const T*>(&c);
+  const T* zmv = reinterpret_cast<const T*>(&zm);
+  const T* ymv = reinterpret_cast<const T*>(&ym);
+  const T* ypv = reinterpret_cast<const T*>(&yp);
+  const T* zpv = reinterpret_cast<const T*>(&zp);
+  VT out;
+  T* o = reinterpret_cast<T*>(&out);
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    T s = T(0);
+    if (hz_m) s = acc_neg(s, zmv[u]);
+    if (yi > 0) s = acc_neg(s, ymv[u]);
+    if (xi + u > 0) s = acc_neg(s, u == 0 ? xl : cv[u - 1]);
+    s = add_rn(s, mul_rn(T(6), cv[u]));
+    if (xi + u + 1 < nx) s = acc_neg(s, u + 1 == V ? xr : cv[u + 1]);
+    if (yi + 1 < ny) s = acc_neg(s, ypv[u]);
+    if (hz_p) s = acc_neg(s, zpv[u]);
+    o[u] = s;
+  }
+  *reinterpret_cast<VT*>(Y + j * ldy + p) = out;
+}
+
 // gen_laplace2d (generators.cpp:13-30): row p = i + nx*j, diag 4
 template <typename T>
 __global__ void __launch_bounds__(256)
@@ -99,6 +167,18 @@ void stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t c, const T* X, int64_t
   const int64_t n = nx * ny * nz;
   if (n <= 0 || c <= 0) return;
   ProfScope prof("stencil", s, 2.0 * sizeof(T) * n * c, 13.0 * n * c);
+  constexpr int V = sizeof(T) == 8 ? 2 : 4;
+  const bool aligned = nx % V == 0 && ldx % V == 0 && ldy % V == 0 &&
+                       reinterpret_cast<uintptr_t>(X) % (V * sizeof(T)) == 0 &&
+                       reinterpret_cast<uintptr_t>(Y) % (V * sizeof(T)) == 0 &&
+                       reinterpret_cast<uintptr_t>(hlo) % (V * sizeof(T)) == 0 &&
+                       reinterpret_cast<uintptr_t>(hhi) % (V * sizeof(T)) == 0;
+  if (aligned) {
+    dim3 grid(static_cast<unsigned>(ceil_div(n / V, 256)), static_cast<unsigned>(c));
+    k_stencil7_vec<T, V><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi);
+    MPB_LAUNCH_CHECK();
+    return;
+  }
   dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(c));
   k_stencil7<T><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi);
   MPB_LAUNCH_CHECK();
