@@ -499,6 +499,71 @@ k_gemm_tn(int64_t n, int k, int c, T alpha, const T* __restrict__ A, int64_t lda
   }
 }
 
+// Tall-skinny times small, fp32 (and unaligned fp64): one thread per row of Y
+// with all c <= CT outputs in registers; C (k x c) staged once in shared
+// memory and read as broadcasts; the row's k values of A are independent,
+// coalesced loads (8 in flight).  Pair mode via blockIdx.z as k_gemm_tn.
+template <typename T, int CT>
+__global__ void __launch_bounds__(128)
+k_gemm_rows(int64_t n, int k, int c, T alpha, const T* __restrict__ A, int64_t lda,
+            const T* __restrict__ Cm, int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y,
+            int64_t ldy, const T* __restrict__ A2, T* Y2) {
+  extern __shared__ __align__(16) unsigned char rows_sm[];
+  T* Cs = reinterpret_cast<T*>(rows_sm);  // k x CT, row l contiguous
+  if (blockIdx.z) {
+    A = A2;
+    Y = Y2;
+  }
+  for (int e = threadIdx.x; e < k * CT; e += blockDim.x) {
+    const int l = e / CT, jj = e % CT;
+    Cs[e] = jj < c ? Cm[l + static_cast<int64_t>(jj) * ldc] : T(0);
+  }
+  __syncthreads();
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  T acc[CT];
+#pragma unroll
+  for (int jj = 0; jj < CT; ++jj) acc[jj] = T(0);
+  const T* a = A + i;
+  int l = 0;
+  // 16 loads in flight: the next batch is requested before this one is used
+  constexpr int B = 16;
+  T nxt[B];
+  if (k >= B) {
+#pragma unroll
+    for (int u = 0; u < B; ++u) nxt[u] = __ldg(a + static_cast<int64_t>(u) * lda);
+  }
+  for (; l + B <= k; l += B) {
+    T av[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) av[u] = nxt[u];
+    if (l + 2 * B <= k) {
+#pragma unroll
+      for (int u = 0; u < B; ++u) nxt[u] = __ldg(a + static_cast<int64_t>(l + B + u) * lda);
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const T* cr = Cs + (l + u) * CT;
+#pragma unroll
+      for (int jj = 0; jj < CT; ++jj) acc[jj] = fma(av[u], cr[jj], acc[jj]);
+    }
+  }
+  for (; l < k; ++l) {
+    const T av = __ldg(a + static_cast<int64_t>(l) * lda);
+    const T* cr = Cs + l * CT;
+#pragma unroll
+    for (int jj = 0; jj < CT; ++jj) acc[jj] = fma(av, cr[jj], acc[jj]);
+  }
+#pragma unroll
+  for (int jj = 0; jj < CT; ++jj) {
+    if (jj < c) {
+      T v = alpha * acc[jj];
+      if (beta != T(0)) v = beta * Z[i + jj * ldz] + v;
+      Y[i + jj * ldy] = v;
+    }
+  }
+}
+
 __global__ void k_f64_to_f32(int64_t n, int64_t c, const double* __restrict__ src, int64_t lds,
                              float* __restrict__ dst, int64_t ldd, int* overflow) {
   const int64_t total = n * c;
@@ -741,6 +806,28 @@ static void gemm_impl(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int6
       MPB_LAUNCH_CHECK();
       return;
     }
+  }
+  if (c <= 64 && k <= 1024) {
+    const int ct = c <= 16 ? 16 : c <= 32 ? 32 : c <= 48 ? 48 : 64;
+    const size_t smem = sizeof(T) * static_cast<size_t>(k) * ct;
+    const dim3 g3(static_cast<unsigned>(ceil_div(n, 128)), 1, nz);
+    const int ki = static_cast<int>(k), ci = static_cast<int>(c);
+    auto go = [&](auto ct_tag) {
+      constexpr int CT = decltype(ct_tag)::value;
+      if (smem > 48 * 1024)
+        MPB_CUDA(cudaFuncSetAttribute(k_gemm_rows<T, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+      k_gemm_rows<T, CT><<<g3, 128, smem, s>>>(n, ki, ci, alpha, A, lda, C, ldc, beta, Z, ldz, Y,
+                                               ldy, A2, Y2);
+    };
+    switch (ct) {
+      case 16: go(std::integral_constant<int, 16>()); break;
+      case 32: go(std::integral_constant<int, 32>()); break;
+      case 48: go(std::integral_constant<int, 48>()); break;
+      default: go(std::integral_constant<int, 64>()); break;
+    }
+    MPB_LAUNCH_CHECK();
+    return;
   }
   k_gemm_tn<T><<<grid, 256, 0, s>>>(n, static_cast<int>(k), static_cast<int>(c), alpha, A, lda, C,
                                     ldc, beta, Z, ldz, Y, ldy, A2, Y2);

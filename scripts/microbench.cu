@@ -383,6 +383,14 @@ int main(int argc, char** argv) {
       ms = time_ms([&] { gemm_tn<double>(n, 2 * m, m, -1.0, S, n, G, 2 * m, 1.0, Y, n, Y, n, s); }, 5, s);
       snprintf(name, sizeof name, "gemm W -= B G %s", sh.tag);
       report(name, ms, (double)(n * 2 * m + 2 * n * m) * 8, 2.0 * n * 2 * m * m);
+      {
+        const float* Sf = reinterpret_cast<const float*>(S);
+        const float* Gf = reinterpret_cast<const float*>(G);
+        float* Yf = reinterpret_cast<float*>(Y);
+        ms = time_ms([&] { gemm_tn<float>(n, k, 2 * m, 1.f, Sf, n, Gf, k, 0.f, nullptr, 0, Yf, n, s); }, 5, s);
+        snprintf(name, sizeof name, "gemm<float> S C (s -> 2m) %s", sh.tag);
+        report(name, ms, (double)(n * k + n * 2 * m) * 4, 2.0 * n * k * 2 * m);
+      }
       double* Rt;
       CK(cudaMalloc(&Rt, m * m * 8));
       int* st;
