@@ -9,6 +9,8 @@
 // precision.hpp:102-107, overflow flagged), scaled in fp32 and widened back
 // (to_working, :113-117), so R never exists in HBM.  The elementwise
 // arithmetic is explicitly rounded -> bitwise equal to the reference's.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "rn.cuh"
@@ -50,7 +52,7 @@ __device__ __forceinline__ T apply_ft(T r, const void* dinv, int64_t i, int* ove
   }
 }
 
-template <typename T, int MODE>
+template <typename T, int MODE, bool VEC>
 __global__ void __launch_bounds__(kThreads)
 k_residual(int64_t n, int m, const T* __restrict__ X, int64_t ldx, const T* __restrict__ AX,
            int64_t ldax, const T* __restrict__ theta, const void* __restrict__ dinv,
@@ -72,16 +74,47 @@ k_residual(int64_t n, int m, const T* __restrict__ X, int64_t ldx, const T* __re
     th[q] = (j0 + q < m) ? theta[j0 + q] : T(0);
   }
   int ovf = 0;
-  for (int64_t i = r_begin + threadIdx.x; i < r_end; i += kThreads) {
+  // two consecutive rows per thread with 2-wide loads / stores (rows are
+  // contiguous per column; chunks start at multiples of 256 rows, ld % 32 == 0)
+  using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  constexpr int kStep = VEC ? 2 : 1;
+  for (int64_t i = r_begin + kStep * threadIdx.x; i < r_end; i += kStep * kThreads) {
+    const bool pair = VEC && i + 1 < r_end;
 #pragma unroll
     for (int q = 0; q < kColGroup; ++q) {
       const int j = j0 + q;
       if (j < m) {
-        const T x = X[i + j * ldx];
-        const T r = sub_rn(AX[i + j * ldax], mul_rn(th[q], x));
-        rr[q] = fma(static_cast<Acc>(r), static_cast<Acc>(r), rr[q]);
-        xx[q] = fma(static_cast<Acc>(x), static_cast<Acc>(x), xx[q]);
-        if (W) W[i + j * ldw] = apply_ft<T, MODE>(r, dinv, i, &ovf);
+        T x0, x1 = T(0), a0, a1 = T(0);
+        if (pair) {
+          const V2 xv = *reinterpret_cast<const V2*>(X + i + j * ldx);
+          const V2 av = *reinterpret_cast<const V2*>(AX + i + j * ldax);
+          x0 = xv.x;
+          x1 = xv.y;
+          a0 = av.x;
+          a1 = av.y;
+        } else {
+          x0 = X[i + j * ldx];
+          a0 = AX[i + j * ldax];
+        }
+        const T r0 = sub_rn(a0, mul_rn(th[q], x0));
+        const T r1 = sub_rn(a1, mul_rn(th[q], x1));
+        rr[q] = fma(static_cast<Acc>(r0), static_cast<Acc>(r0), rr[q]);
+        xx[q] = fma(static_cast<Acc>(x0), static_cast<Acc>(x0), xx[q]);
+        if (pair) {
+          rr[q] = fma(static_cast<Acc>(r1), static_cast<Acc>(r1), rr[q]);
+          xx[q] = fma(static_cast<Acc>(x1), static_cast<Acc>(x1), xx[q]);
+        }
+        if (W) {
+          const T w0 = apply_ft<T, MODE>(r0, dinv, i, &ovf);
+          if (pair) {
+            V2 wv;
+            wv.x = w0;
+            wv.y = apply_ft<T, MODE>(r1, dinv, i + 1, &ovf);
+            *reinterpret_cast<V2*>(W + i + j * ldw) = wv;
+          } else {
+            W[i + j * ldw] = w0;
+          }
+        }
       }
     }
   }
@@ -169,6 +202,14 @@ int ew_grid(int64_t total) {
 
 }  // namespace
 
+template <typename T, int MODE, typename... Args>
+void launch_resid(bool vec, dim3 grid, cudaStream_t s, Args... args) {
+  if (vec)
+    k_residual<T, MODE, true><<<grid, kThreads, 0, s>>>(args...);
+  else
+    k_residual<T, MODE, false><<<grid, kThreads, 0, s>>>(args...);
+}
+
 int64_t resid_workspace_elems(int64_t n, int64_t m) {
   return resid_plan(n, m).nchunk * m * 2;
 }
@@ -182,19 +223,24 @@ void residual_precond(int mode, int64_t n, int64_t m, const T* X, int64_t ldx, c
   ProfScope prof("residual_ft", s, double(sizeof(T)) * n * m * (W ? 3 : 2), 6.0 * n * m);
   const ResidPlan p = resid_plan(n, m);
   dim3 grid(static_cast<unsigned>(p.nchunk), static_cast<unsigned>(ceil_div(m, kColGroup)));
+  const size_t al = 2 * sizeof(T);
+  const bool vec = ldx % 2 == 0 && ldax % 2 == 0 && (W == nullptr || ldw % 2 == 0) &&
+                   reinterpret_cast<uintptr_t>(X) % al == 0 &&
+                   reinterpret_cast<uintptr_t>(AX) % al == 0 &&
+                   reinterpret_cast<uintptr_t>(W) % al == 0;
   const int mi = static_cast<int>(m);
   switch (mode) {
     case kResidPlain:
-      k_residual<T, kResidPlain><<<grid, kThreads, 0, s>>>(n, mi, X, ldx, AX, ldax, theta, dinv, W,
+      launch_resid<T, kResidPlain>(vec, grid, s, n, mi, X, ldx, AX, ldax, theta, dinv, W,
                                                            ldw, p.rows_per_chunk, work, overflow_flag);
       break;
     case kResidJacobiT:
-      k_residual<T, kResidJacobiT><<<grid, kThreads, 0, s>>>(
+      launch_resid<T, kResidJacobiT>(vec, grid, s, 
           n, mi, X, ldx, AX, ldax, theta, dinv, W, ldw, p.rows_per_chunk, work, overflow_flag);
       break;
     default:
       if constexpr (sizeof(T) == 8) {
-        k_residual<T, kResidSandwich><<<grid, kThreads, 0, s>>>(
+        launch_resid<T, kResidSandwich>(vec, grid, s, 
             n, mi, X, ldx, AX, ldax, theta, dinv, W, ldw, p.rows_per_chunk, work, overflow_flag);
       } else {
         throw Error(MPEIG_E_CONFIG, "sandwich f_T needs a working-precision block");
