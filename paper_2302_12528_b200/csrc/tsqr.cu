@@ -12,6 +12,7 @@
 // happens as the leaf loads W, with the overflow check.
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -424,6 +425,137 @@ k_tsqr_reg(int64_t n, int m, const Tin* __restrict__ W, int64_t ldw, Tq* __restr
   }
 }
 
+// ---------------------------------------------------------------------------
+// Throughput leaves for long blocks: one WARP factors one b x m leaf (b =
+// 32*RPL) held in shared memory, with warp-synchronous steps only (no CTA
+// barrier) and the dot products of four columns interleaved, so many leaves'
+// latency chains overlap on each SM.  Each leaf writes its R (m x m) into a
+// stacked, column-major (nleaf m) x m block, which the next pass (or the
+// register TSQR above) factors again.
+// ---------------------------------------------------------------------------
+template <typename Tin, typename Tq, int RPL>
+__global__ void __launch_bounds__(128)
+k_tsqr_warpleaf(int64_t rows, int m, const Tin* __restrict__ W, int64_t ldw, int64_t nleaf,
+                Tq* __restrict__ out, int* status) {
+  constexpr int B = 32 * RPL;
+  extern __shared__ __align__(16) unsigned char wl_sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t leaf = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
+  if (leaf >= nleaf) return;
+  Tq* t = reinterpret_cast<Tq*>(wl_sm) + static_cast<int64_t>(warp) * B * m;
+  const int64_t r0 = leaf * B;
+  int ovf = 0;
+  // four columns' loads in flight before their stores (one DRAM round trip
+  // per four columns, not per column)
+  for (int c0 = 0; c0 < m; c0 += 4) {
+    Tin buf[4][RPL];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int64_t row = r0 + lane + 32 * i;
+        buf[u][i] = (c0 + u < m && row < rows) ? __ldg(W + row + (c0 + u) * ldw) : Tin(0);
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (c0 + u < m)
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) t[(c0 + u) * B + lane + 32 * i] = narrow<Tin, Tq>(buf[u][i], &ovf);
+  }
+  if (ovf) atomicCAS(status, 0, MPEIG_E_OVERFLOW);
+  __syncwarp();
+  const int steps = m < B ? m : B;
+  for (int j = 0; j < steps; ++j) {
+    Tq v[RPL];
+    double tail = 0.0, xj = 0.0;
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = lane + 32 * i;
+      v[i] = t[j * B + r];
+      const double x = static_cast<double>(v[i]);
+      if (r > j) tail = fma(x, x, tail);
+      if (r == j) xj = x;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) tail += __shfl_xor_sync(0xffffffffu, tail, off);
+    const double x0 = __shfl_sync(0xffffffffu, xj, j & 31);
+    const double nrm = sqrt(fma(x0, x0, tail));
+    double beta = 0.0, diag = 0.0, v0 = 0.0;
+    if (nrm != 0.0) {
+      const double phase = x0 >= 0.0 ? 1.0 : -1.0;
+      v0 = x0 + phase * nrm;
+      beta = 2.0 / fma(v0, v0, tail);
+      diag = -phase * nrm;
+    }
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = lane + 32 * i;
+      v[i] = r < j ? Tq(0) : (r == j ? static_cast<Tq>(v0) : v[i]);
+      if (r >= j) t[j * B + r] = r == j ? static_cast<Tq>(diag) : Tq(0);
+    }
+    if (beta != 0.0) {
+      for (int c = j + 1; c < m; c += 4) {
+        Tq d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          d[u] = Tq(0);
+          if (c + u < m) {
+            const Tq* col = t + (c + u) * B + lane;
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) d[u] = fma(v[i], col[32 * i], d[u]);
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], off);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (c + u < m) {
+            const Tq f = static_cast<Tq>(static_cast<double>(d[u]) * beta);
+            Tq* col = t + (c + u) * B + lane;
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) col[32 * i] = fma(-f, v[i], col[32 * i]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // R (rows < m of the tile) -> rows [leaf m, leaf m + m) of the stack
+  const int64_t ldo = nleaf * m;
+  for (int c = 0; c < m; ++c)
+    for (int r = lane; r < m; r += 32)
+      out[leaf * m + r + c * ldo] = r <= c && r < B ? t[c * B + r] : Tq(0);
+}
+
+constexpr int kWarpLeafRPL = 8;  // b = 256 rows per leaf
+
+template <typename Tq>
+int warpleaf_warps(int64_t m) {  // warps (leaves) per CTA within 200 KB of shared memory
+  const int64_t per = 32 * kWarpLeafRPL * m * static_cast<int64_t>(sizeof(Tq));
+  int64_t w = (200 * 1024) / std::max<int64_t>(per, 1);
+  return static_cast<int>(std::min<int64_t>(4, w));
+}
+
+// passes of the warp-leaf reduction for an n x m block: rows of each pass's
+// input (the last entry is what the register TSQR finishes)
+template <typename Tq>
+std::vector<int64_t> warpleaf_passes(int64_t n, int64_t m) {
+  std::vector<int64_t> rows{n};
+  static const bool off = [] {
+    const char* e = std::getenv("MPEIG_TSQR_WARPLEAF");
+    return e && e[0] == '0';
+  }();
+  // (fp64 leaves: the register TSQR is faster -- 2.5 vs 3.6 ms at n = 1 M, m = 48)
+  if (off || sizeof(Tq) != 4 || m > 64 || warpleaf_warps<Tq>(m) < 1) return rows;
+  const int64_t b = 32 * kWarpLeafRPL;
+  // worth it once there are several leaves per warp slot of the GPU
+  while (rows.back() >= 8 * kNumSMs * b && b >= 2 * m)
+    rows.push_back(ceil_div(rows.back(), b) * m);
+  return rows;
+}
+
 struct RegCfg {
   int nw, rpl, mpw;  // 0 = not supported
 };
@@ -526,6 +658,19 @@ void tsqr_epilogue(int64_t m, const Tq* R, int64_t ldr, Tin* Rw, Tin* Rinv, int*
 
 template <typename Tin, typename Tq>
 int64_t tsqr_workspace_elems(int64_t n, int64_t m) {
+  const std::vector<int64_t> passes = warpleaf_passes<Tq>(n, m);
+  if (passes.size() > 1) {
+    // two ping-pong stacks (the first pass's output is the largest), then the
+    // register TSQR of the last stack
+    int64_t st = passes[1] * m;
+    const int64_t last = passes.back();
+    const TsqrPlan<Tq> p = tsqr_plan<Tq>(last, m);
+    const int64_t smem_path = (p.nleaf + ceil_div(p.nleaf, p.group) + 1) * m * m;
+    const RegPlan r = reg_plan<Tq>(last, m);
+    const int64_t reg_path = r.r_elems + ceil_div(r.n_ctr * static_cast<int64_t>(sizeof(int)),
+                                                  static_cast<int64_t>(sizeof(Tq))) + 2;
+    return 2 * st + std::max(smem_path, reg_path) + 4;
+  }
   const TsqrPlan<Tq> p = tsqr_plan<Tq>(n, m);
   const int64_t smem_path = (p.nleaf + ceil_div(p.nleaf, p.group) + 1) * m * m;
   const RegPlan r = reg_plan<Tq>(n, m);
@@ -539,6 +684,41 @@ void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr,
             int* status, cudaStream_t s, Tin* Rw_out, Tin* Rinv_out, int rank_check) {
   const int numeric = rank_check < 0 ? (sizeof(Tin) == sizeof(Tq) ? 1 : 0) : rank_check;
   const int mi = static_cast<int>(m);
+  const std::vector<int64_t> passes = warpleaf_passes<Tq>(n, m);
+  if (passes.size() > 1) {
+    ProfScope prof("tsqr", s, double(sizeof(Tin)) * n * m, 2.0 * n * m * m);
+    const int64_t st = passes[1] * m;
+    Tq* stk[2] = {work, work + st};
+    Tq* rest = work + 2 * st;
+    const int wpc = warpleaf_warps<Tq>(m);
+    const size_t smem = static_cast<size_t>(wpc) * 32 * kWarpLeafRPL * m * sizeof(Tq);
+    const Tq* in_q = nullptr;
+    for (size_t p = 0; p + 1 < passes.size(); ++p) {
+      const int64_t rows = passes[p], nleaf = ceil_div(rows, 32 * kWarpLeafRPL);
+      Tq* out = stk[p & 1];
+      if (p == 0) {
+        auto k = k_tsqr_warpleaf<Tin, Tq, kWarpLeafRPL>;
+        MPB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        k<<<static_cast<unsigned>(ceil_div(nleaf, wpc)), 32 * wpc, smem, s>>>(rows, mi, W, ldw,
+                                                                                nleaf, out, status);
+      } else {
+        auto k = k_tsqr_warpleaf<Tq, Tq, kWarpLeafRPL>;
+        MPB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        k<<<static_cast<unsigned>(ceil_div(nleaf, wpc)), 32 * wpc, smem, s>>>(rows, mi, in_q, rows,
+                                                                                nleaf, out, status);
+      }
+      MPB_LAUNCH_CHECK();
+      in_q = out;
+    }
+    // the last stack: register TSQR with the original rank-check semantics;
+    // R / R^-1 in the working precision formed after
+    tsqr_r<Tq, Tq>(passes.back(), m, in_q, passes.back(), R, ldr, rest, status, s, nullptr,
+                   nullptr, numeric);
+    if (Rinv_out) tsqr_epilogue<Tin, Tq>(m, R, ldr, Rw_out, Rinv_out, status, s);
+    return;
+  }
   const RegPlan rp = reg_plan<Tq>(n, m);
   const RegKernel<Tin, Tq> rk = rp.cfg.nw ? reg_kernel<Tin, Tq>(rp.cfg) : nullptr;
   if (rk && tsqr_reg_enabled()) {

@@ -195,7 +195,9 @@ def test_mixed_qr_orthogonality(gpu, kappa):
 
 
 @pytest.mark.parametrize("n,m", [(3001, 16), (100, 7), (40000, 16), (5000, 32), (20000, 48),
-                                 (9000, 64), (7000, 80), (3000, 96), (2000, 112)])
+                                 (9000, 64), (7000, 80), (3000, 96), (2000, 112),
+                                 # long blocks: warp-leaf passes before the register TSQR
+                                 (400000, 16), (330000, 48)])
 def test_householder_qr_matches_reference(gpu, n, m):
     """TSQR tree shapes: one leaf, several tree levels, every register-tile width
     class and the shared-memory fallback (m > 96 in fp64)."""
