@@ -45,13 +45,7 @@ GramPlan gram_plan(int64_t n, int64_t ka, int64_t kb) {
   p.tiles_n = ceil_div(kb, tile);
   // one wave: a single-tile Gram uses one CTA per SM (two reduction levels),
   // multi-tile Grams two CTAs per SM
-  static const int env_chunks = [] {
-    const char* e = std::getenv("MPEIG_GRAM_CHUNKS");  // tuning experiments only
-    return e ? std::atoi(e) : 0;
-  }();
-  // one chunk per SM: measured best from cfg1 (1 tile) to cfg4@8 (16 tiles);
-  // the GPU-wide combine makes the chunk count cheap
-  int64_t nchunk = env_chunks > 0 ? env_chunks : kNumSMs;
+  int64_t nchunk = kNumSMs;
   const int64_t max_chunks = ceil_div(n, 64);  // >= 64 rows per chunk
   if (nchunk > max_chunks) nchunk = max_chunks;
   if (nchunk < 1) nchunk = 1;

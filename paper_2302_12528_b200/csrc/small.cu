@@ -460,13 +460,6 @@ k_hl_coeffs_warp(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* _
   }
 }
 
-int warp_forms() {  // bitmask of the one-warp forms in use (1 chol, 2 trinv, 4 hl)
-  static const int v = [] {
-    const char* e = std::getenv("MPEIG_SMALL_WARP");
-    return e ? std::atoi(e) : 7;
-  }();
-  return v;
-}
 
 template <typename K>
 void allow_smem(K kernel, size_t bytes) {
@@ -480,14 +473,14 @@ void hl_coeffs_t(int64_t s, int64_t m, int64_t p, const T* C, int64_t ldc, T* co
                  int* fallback, cudaStream_t st) {
   ProfScope prof("hl_coeffs", st, 0, 0);
   if (p > kMaxHlP) throw Error(MPEIG_E_CONFIG, "hl_update: block size above 256 not supported");
-  if ((warp_forms() & 4) && m <= 16 && p <= 16) {
+  if (m <= 16 && p <= 16) {
     k_hl_coeffs_warp<T, 16><<<1, kSmallThreads, 0, st>>>(static_cast<int>(s), static_cast<int>(m),
                                                         static_cast<int>(p), C, ldc, coef, fallback);
     MPB_LAUNCH_CHECK();
     return;
   }
   if constexpr (sizeof(T) == 4) {
-    if ((warp_forms() & 4) && m <= 32 && p <= 32) {
+    if (m <= 32 && p <= 32) {
       k_hl_coeffs_warp<T, 32><<<1, kSmallThreads, 0, st>>>(static_cast<int>(s), static_cast<int>(m),
                                                           static_cast<int>(p), C, ldc, coef, fallback);
       MPB_LAUNCH_CHECK();
@@ -518,7 +511,7 @@ void small_cholesky_inv(int64_t m, const T* G, int64_t ldg, T* L, T* Uinv, int* 
                         cudaStream_t st) {
   if (m <= 0) return;
   ProfScope prof("small_chol", st, 0, 0);
-  if ((warp_forms() & 1) && (m <= 16 || (sizeof(T) == 4 && m <= 32))) {
+  if ((m <= 16 || (sizeof(T) == 4 && m <= 32))) {
     if (m <= 16)
       k_cholesky_inv_warp<T, 16><<<1, 32, 0, st>>>(static_cast<int>(m), G, ldg, L, Uinv, status);
     else
@@ -539,7 +532,7 @@ void small_upper_inverse(int64_t m, const T* R, int64_t ldr, T* Rinv, int* statu
                          cudaStream_t st) {
   if (m <= 0) return;
   ProfScope prof("small_trinv", st, 0, 0);
-  if ((warp_forms() & 2) && (m <= 16 || (sizeof(T) == 4 && m <= 32))) {
+  if ((m <= 16 || (sizeof(T) == 4 && m <= 32))) {
     if (m <= 16)
       k_upper_inverse_warp<T, 16><<<1, 32, 0, st>>>(static_cast<int>(m), R, ldr, Rinv, status);
     else

@@ -671,28 +671,12 @@ StageResult lobpcg_stage_eager(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, con
     timer.start();
     const int64_t b = m + p;
     int64_t dropped = 0, wc = m;
-    auto dbg = [&](const T* ptr, int64_t cols, const char* label) {
-      if (!getenv("MPEIG_DEBUG_NAN")) return;
-      std::vector<T> h(static_cast<size_t>(w.ld * cols));
-      MPB_CUDA(cudaMemcpyAsync(h.data(), ptr, sizeof(T) * h.size(), cudaMemcpyDeviceToHost, s));
-      MPB_CUDA(cudaStreamSynchronize(s));
-      int64_t bad = 0;
-      for (int64_t j = 0; j < cols; ++j)
-        for (int64_t i = 0; i < n; ++i) bad += !std::isfinite(static_cast<double>(h[i + j * w.ld]));
-      if (bad) fprintf(stderr, "iter %ld: %ld non-finite after %s (cols %ld, p %ld)\n", (long)iter, (long)bad, label, (long)cols, (long)p);
-    };
-    dbg(w.S.p, m + p, "S[X P] at start");
-    dbg(Wslot, m, "W = T(R)");
     project_out<T>(w, w.S.p, b, w.ld, Wslot, wc, w.ld, 2);
-    dbg(Wslot, m, "project 2");
     wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, opt.use_mixed_qr != 0, &dropped);
-    dbg(Wslot, wc, "QR1");
     if (wc > 0) {
       int64_t more = 0;
       project_out<T>(w, w.S.p, b, w.ld, Wslot, wc, w.ld, 1);
-      dbg(Wslot, wc, "project 1");
       wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, opt.use_mixed_qr != 0, &more);
-      dbg(Wslot, wc, "QR2");
       dropped += more;
     }
     rec.w_columns_dropped = dropped;
@@ -708,43 +692,7 @@ StageResult lobpcg_stage_eager(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, con
     const int64_t sdim = m + p + wc;
     status_clear(ctx);
     dgram<T>(w, sdim, w.S.p, w.ld, sdim, w.AS.p, w.ld, w.G.p, sdim, 1);
-    std::vector<T> dbgG;
-    if (getenv("MPEIG_DUMP_G_ITER") &&
-        (atol(getenv("MPEIG_DUMP_G_ITER")) == iter || atol(getenv("MPEIG_DUMP_G_ITER")) < 0)) {
-      std::vector<T> h(sdim * sdim);
-      MPB_CUDA(cudaMemcpyAsync(h.data(), w.G.p, sizeof(T) * sdim * sdim, cudaMemcpyDeviceToHost, s));
-      MPB_CUDA(cudaStreamSynchronize(s));
-      FILE* f = fopen(getenv("MPEIG_DUMP_G_FILE"), "wb");
-      if (f) {
-        fwrite(h.data(), sizeof(T), h.size(), f);
-        fclose(f);
-      }
-    }
-    if (getenv("MPEIG_DEBUG_NAN")) {
-      dbgG.resize(sdim * sdim);
-      MPB_CUDA(cudaMemcpyAsync(dbgG.data(), w.G.p, sizeof(T) * sdim * sdim, cudaMemcpyDeviceToHost, s));
-    }
     small_eig<T>(w, sdim, w.G.p, sdim, w.evals.p);
-    if (getenv("MPEIG_DEBUG_NAN")) {
-      std::vector<T> ev(sdim), vv(sdim * sdim);
-      MPB_CUDA(cudaMemcpyAsync(ev.data(), w.evals.p, sizeof(T) * sdim, cudaMemcpyDeviceToHost, s));
-      MPB_CUDA(cudaMemcpyAsync(vv.data(), w.G.p, sizeof(T) * sdim * sdim, cudaMemcpyDeviceToHost, s));
-      MPB_CUDA(cudaStreamSynchronize(s));
-      bool bad = false;
-      for (auto v : ev) bad |= !std::isfinite(static_cast<double>(v));
-      for (auto v : vv) bad |= !std::isfinite(static_cast<double>(v));
-      bool badin = false;
-      for (auto v : dbgG) badin |= !std::isfinite(static_cast<double>(v));
-      if (bad) {
-        fprintf(stderr, "NaN after eig: sdim=%ld input_bad=%d\n", (long)sdim, badin);
-        FILE* f = fopen(getenv("MPEIG_DEBUG_NAN"), "wb");
-        if (f) {
-          fwrite(dbgG.data(), sizeof(T), dbgG.size(), f);
-          fclose(f);
-        }
-        getenv("MPEIG_DEBUG_NAN_STOP") ? (void)0 : (void)0;
-      }
-    }
     const int64_t pn = std::min(m, sdim - m);
     if constexpr (sizeof(T) == 8)
       hl_coeffs(sdim, m, pn, w.G.p, sdim, w.coef.p, w.scratch(), ctx->d_status + 4, s);
@@ -1021,10 +969,6 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
                           ctx->h_status[kSlotEig];
       int64_t dropped = 0, pn = std::min(m, m + p);
       if (failed) {
-        if (getenv("MPEIG_DEBUG_SPEC"))
-          fprintf(stderr, "iter %ld: speculative body failed (qr1 %d/%d qr2 %d/%d eig %d), rolling back\n",
-                  (long)iter, ctx->h_status[kSlotQr1], ctx->h_status[kSlotQr1 + 1],
-                  ctx->h_status[kSlotQr2], ctx->h_status[kSlotQr2 + 1], ctx->h_status[kSlotEig]);
         // ---- roll back and repeat on the careful path
         MPB_CUDA(cudaMemcpyAsync(w.theta.p, w.theta_prev.p, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
         T* Wslot = w.S.p + (m + p) * w.ld;

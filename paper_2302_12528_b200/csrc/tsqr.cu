@@ -543,12 +543,8 @@ int warpleaf_warps(int64_t m) {  // warps (leaves) per CTA within 200 KB of shar
 template <typename Tq>
 std::vector<int64_t> warpleaf_passes(int64_t n, int64_t m) {
   std::vector<int64_t> rows{n};
-  static const bool off = [] {
-    const char* e = std::getenv("MPEIG_TSQR_WARPLEAF");
-    return e && e[0] == '0';
-  }();
   // (fp64 leaves: the register TSQR is faster -- 2.5 vs 3.6 ms at n = 1 M, m = 48)
-  if (off || sizeof(Tq) != 4 || m > 64 || warpleaf_warps<Tq>(m) < 1) return rows;
+  if (sizeof(Tq) != 4 || m > 64 || warpleaf_warps<Tq>(m) < 1) return rows;
   const int64_t b = 32 * kWarpLeafRPL;
   // worth it once there are several leaves per warp slot of the GPU
   while (rows.back() >= 8 * kNumSMs * b && b >= 2 * m)
@@ -564,11 +560,6 @@ struct RegCfg {
 // at least two R factors; the register tile stays <= 96 32-bit registers.
 template <typename Tq>
 RegCfg reg_cfg(int64_t m) {
-  static const int rpl16 = [] {
-    const char* e = std::getenv("MPEIG_TSQR_RPL16");  // tuning experiments only
-    return e ? std::atoi(e) : 0;
-  }();
-  if (m <= 16 && (rpl16 == 8 || rpl16 == 16 || (rpl16 == 32 && sizeof(Tq) == 4))) return {16, rpl16, 1};
   // The per-column step is a latency chain (two warp reductions, sqrt, a
   // barrier), so the tree is kept shallow: tall tiles (b = 32*RPL rows) and
   // wide fan-in G = b/m.  One column per warp where m allows.
@@ -633,13 +624,6 @@ RegPlan reg_plan(int64_t n, int64_t m) {
   return p;
 }
 
-bool tsqr_reg_enabled() {
-  static const bool off = [] {
-    const char* e = std::getenv("MPEIG_TSQR_SMEM");
-    return e && e[0] == '1';
-  }();
-  return !off;
-}
 
 }  // namespace
 
@@ -721,7 +705,7 @@ void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr,
   }
   const RegPlan rp = reg_plan<Tq>(n, m);
   const RegKernel<Tin, Tq> rk = rp.cfg.nw ? reg_kernel<Tin, Tq>(rp.cfg) : nullptr;
-  if (rk && tsqr_reg_enabled()) {
+  if (rk) {
     ProfScope prof("tsqr", s, double(sizeof(Tin)) * n * m, 2.0 * n * m * m);
     int* ctr = reinterpret_cast<int*>(work + rp.r_elems);
     const bool fuse = Rinv_out && m <= 16;
