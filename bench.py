@@ -178,7 +178,7 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     w = WORKLOADS[args.workload]
-    shard = args.shard and world > 1
+    shard = args.shard  # at N = 1: the sharded code path over a 1-rank NCCL comm
     ctx = mp.Context(local)
     cfg = mp.SolverConfig(k=w["k"], block=w["block"], tol=w["tol"], maxit=w["maxit"], seed=w["seed"],
                           variant=args.variant)
@@ -186,7 +186,8 @@ def run_ours(args):
     if shard:
         # row-sharded solve: rank r owns z-slab r; Gram / norm
         # allreduce, R allgather and halo planes over NCCL (NVLink / NVSwitch)
-        ctx.attach_nccl(rank, world, mp.broadcast_unique_id(rank))
+        ctx.attach_nccl(rank, world,
+                        mp.broadcast_unique_id(rank) if world > 1 else mp.nccl_unique_id())
         nx, ny, nz = w["dims"]
         z0, nzl = mp.slab_partition(nz, world)[rank]
         A = mp.laplace3d_slab(nx, ny, nz, z0, nzl, ctx=ctx)
@@ -346,7 +347,8 @@ def main():
                     choices=["mplobpcg-schol", "dlobpcg-schol", "dlobpcg-dchol", "pinvit"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", action="store_true",
-                    help="N > 1: one row-sharded solve over the N GPUs (strong scaling) "
+                    help="one row-sharded solve over the N GPUs (strong scaling; N = 1 runs "
+                         "the sharded path over a 1-rank NCCL comm) "
                          "instead of N independent replicas")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -130,6 +130,8 @@ typedef struct {
 /* ------------------------------------------------------------- context */
 /* One context per (GPU, stream); not thread-safe per context, independent
  * contexts may run concurrently (SPEC.md:526 / SURVEY §8b threading). */
+/* cuda_stream NULL: the context creates its own stream and orders every call
+ * after earlier, and before later, work on the legacy default stream. */
 int mpeig_ctx_create(int device, void* cuda_stream, mpeig_ctx** out);
 void mpeig_ctx_destroy(mpeig_ctx* ctx);
 /* message of the last failure on this context; *index gets the payload */

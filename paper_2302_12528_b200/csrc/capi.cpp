@@ -18,9 +18,25 @@ using namespace mpb;
 
 namespace {
 
+// a context on its own stream joins the legacy default stream around each call
+struct LegacyOrder {
+  mpeig_ctx* ctx;
+  explicit LegacyOrder(mpeig_ctx* c) : ctx(c && c->own_stream && c->ev_in ? c : nullptr) {
+    if (!ctx) return;
+    cudaEventRecord(ctx->ev_in, cudaStreamLegacy);
+    cudaStreamWaitEvent(ctx->stream, ctx->ev_in, 0);
+  }
+  ~LegacyOrder() {
+    if (!ctx) return;
+    cudaEventRecord(ctx->ev_out, ctx->stream);
+    cudaStreamWaitEvent(cudaStreamLegacy, ctx->ev_out, 0);
+  }
+};
+
 template <typename F>
 int guard(mpeig_ctx* ctx, F&& f) {
   try {
+    LegacyOrder order(ctx);
     f();
     if (ctx) {
       ctx->last_msg.clear();
@@ -85,6 +101,8 @@ int mpeig_ctx_create(int device, void* cuda_stream, mpeig_ctx** out) {
       ctx->stream = static_cast<cudaStream_t>(cuda_stream);
     } else {
       MPB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      MPB_CUDA(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
+      MPB_CUDA(cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming));
       ctx->own_stream = true;
     }
     if (cusolverDnCreate(&ctx->cusolver) != CUSOLVER_STATUS_SUCCESS)
@@ -123,6 +141,8 @@ void mpeig_ctx_destroy(mpeig_ctx* ctx) {
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+  if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
   delete ctx->comm;
   delete ctx;
 }

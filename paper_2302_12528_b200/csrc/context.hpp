@@ -17,6 +17,10 @@ struct mpeig_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // own stream (created for a NULL stream argument): every C-ABI call is
+  // ordered after prior work on the legacy default stream and before later
+  // work there, through these two events
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cusolverDnHandle_t cusolver = nullptr;
   cublasHandle_t cublas = nullptr;
   std::string last_msg;
@@ -111,10 +115,9 @@ void gaussian_fill(int64_t rows, int64_t cols, uint64_t seed, double* out);
 void gaussian_fill_rows(int64_t n_global, int64_t cols, uint64_t seed, int64_t row0, int64_t rows,
                         double* out);
 
-// the communicator when the context runs row-sharded over > 1 rank
-inline Comm* dist(const mpeig_ctx* ctx) {
-  return ctx->comm && ctx->comm->nranks > 1 ? ctx->comm : nullptr;
-}
+// the communicator when the context runs row-sharded (any attached comm,
+// a 1-rank one included: that runs the sharded code path on one GPU)
+inline Comm* dist(const mpeig_ctx* ctx) { return ctx->comm; }
 uint64_t pcg64_draw(uint64_t seed, uint64_t index);
 
 // operator application (ops dispatch in solver.cpp)

@@ -289,3 +289,21 @@ def test_hl_coeffs_match_reference(gpu):
     assert p.value == m and fb.value == fb_r == 0
     assert np.array_equal(cf[:, :m], Cm[:, :m])
     assert np.abs(cf[:, m:] - cpv_r).max() <= 1e-13
+
+
+@pytest.mark.gpu
+def test_default_context_orders_with_torch_default_stream(gpu):
+    """A Context on torch's default stream runs on its own stream; each call
+    must still wait for earlier default-stream work (a non-blocking H2D copy)
+    and finish before later default-stream work (the D2H read)."""
+    import torch
+    A = gpu.laplace3d(256, 256, 128)
+    n = A.n
+    Xh = torch.from_numpy(np.random.default_rng(1).standard_normal((2, n))).pin_memory()
+    Xd = Xh.to("cuda:0")
+    torch.cuda.synchronize()
+    ref = A.apply(Xd).cpu()
+    for _ in range(3):
+        xd = Xh.to("cuda:0", non_blocking=True)  # still in flight on the default stream
+        got = A.apply(xd).cpu()
+        assert torch.equal(got, ref)
