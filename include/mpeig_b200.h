@@ -147,9 +147,19 @@ void* mpeig_ctx_stream(mpeig_ctx* ctx);
  *   "eig_backend" 0 (default): one-CTA tridiagonal + QL eigensolver (the
  *                 reference's algorithm) for 3m <= 96, cuSOLVER syevd above;
  *                 1: cuSOLVER syevd always; 2: cuSOLVER syevj (diagnostic)
+ *   "spec_qr"     1 (default): the speculative body orthonormalises W by
+ *                 Cholesky-QR twice with a conditioning guard (a column with
+ *                 < 1e-5 (fp64) / 1e-2 (fp32) of its norm outside the span of
+ *                 the columns before it fails the guard and the iteration is
+ *                 repeated on the careful path with the reference's QR);
+ *                 0: the TSQR-based QR in the speculative body too.  Same
+ *                 results to rounding (not bitwise).
  *   "syev_method", "ql_exact": eigensolver variants for experiments
  *                 (process-wide; default 0) */
 int mpeig_ctx_set_option(mpeig_ctx* ctx, const char* key, int value);
+/* speculative iterations this context repeated on the careful path (a
+ * breakdown or a failed guard inside the speculative body) */
+int64_t mpeig_spec_rollbacks(mpeig_ctx* ctx, int reset);
 
 /* -------------------------------------------------------- row sharding */
 /* the n x . blocks are row-sharded over the ranks (z-slabs of

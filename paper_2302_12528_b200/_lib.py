@@ -67,7 +67,7 @@ HOST_APPLY = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, 
 # exported symbols declared by include/mpeig_b200.h (checked by tests)
 SYMBOLS = [
     "mpeig_ctx_create", "mpeig_ctx_destroy", "mpeig_last_error", "mpeig_launch_count",
-    "mpeig_ctx_stream", "mpeig_ctx_set_option", "mpeig_op_lap3d", "mpeig_op_lap2d", "mpeig_op_csr", "mpeig_op_dense",
+    "mpeig_ctx_stream", "mpeig_ctx_set_option", "mpeig_spec_rollbacks", "mpeig_op_lap3d", "mpeig_op_lap2d", "mpeig_op_csr", "mpeig_op_dense",
     "mpeig_op_device_callback", "mpeig_op_host_callback", "mpeig_precond_jacobi",
     "mpeig_op_destroy", "mpeig_op_n", "mpeig_op_apply", "mpeig_spectral_norm_estimate",
     "mpeig_lobpcg_stage_f64", "mpeig_lobpcg_stage_f32", "mpeig_pinvit_f64", "mpeig_solve",
@@ -101,6 +101,7 @@ def load() -> C.CDLL:
         "mpeig_ctx_destroy": (None, [vp]),
         "mpeig_last_error": (C.c_char_p, [vp, C.POINTER(i64)]),
         "mpeig_launch_count": (i64, [vp, C.c_int]),
+        "mpeig_spec_rollbacks": (i64, [vp, C.c_int]),
         "mpeig_ctx_stream": (vp, [vp]),
         "mpeig_ctx_set_option": (C.c_int, [vp, C.c_char_p, C.c_int]),
         "mpeig_op_lap3d": (C.c_int, [vp, i64, i64, i64, pvp]),

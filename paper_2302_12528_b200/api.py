@@ -224,6 +224,10 @@ class Context:
     def launches(self, reset=False) -> int:
         return int(self.lib.mpeig_launch_count(self.h, 1 if reset else 0))
 
+    def spec_rollbacks(self, reset=False) -> int:
+        """Speculative iterations repeated on the careful path since creation / reset."""
+        return int(self.lib.mpeig_spec_rollbacks(self.h, 1 if reset else 0))
+
     # -- row sharding (SURVEY §8e): rank r solves its rows; see include/mpeig_b200.h
     def attach_nccl(self, rank: int, nranks: int, unique_id: bytes):
         """NCCL communicator over the ranks' GPUs (one process per GPU)."""

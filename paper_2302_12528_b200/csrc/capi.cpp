@@ -198,12 +198,20 @@ int mpeig_ctx_attach_nccl(mpeig_ctx* ctx, int rank, int nranks, const void* id) 
   });
 }
 
+int64_t mpeig_spec_rollbacks(mpeig_ctx* ctx, int reset) {
+  if (!ctx) return 0;
+  const int64_t v = ctx->spec_rollbacks;
+  if (reset) ctx->spec_rollbacks = 0;
+  return v;
+}
+
 int mpeig_ctx_set_option(mpeig_ctx* ctx, const char* key, int value) {
   if (!ctx || !key) return MPEIG_E_CONFIG;
   const std::string k(key);
   if (k == "eig_backend") ctx->eig_backend = value;
   else if (k == "spec_mode") ctx->spec_mode = value;
   else if (k == "use_graphs") ctx->use_graphs = value;
+  else if (k == "spec_qr") ctx->spec_qr = value;
   else if (k == "syev_method") g_syev_method = value;
   else if (k == "ql_exact") g_ql_exact = value;
   else if (k == "ql_f32") g_ql_f32 = value;

@@ -32,6 +32,8 @@ struct mpeig_ctx {
   int eig_backend = 0;          // 0 auto (one-CTA syev for s <= kSyevMax), 1 cuSOLVER
   int spec_mode = 1;            // speculative iteration (1 host sync / iteration)
   int use_graphs = 1;           // replay the steady-state iteration as a CUDA graph
+  int spec_qr = 10;             // speculative body's QR: k > 0 guarded CholQR2 (fp64 guard 1e-k), 0 TSQR
+  int64_t spec_rollbacks = 0;   // speculative iterations repeated on the careful path
   mpb::Comm* comm = nullptr;    // row-sharded mode (owned), nullptr: single GPU
 };
 

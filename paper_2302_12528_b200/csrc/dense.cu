@@ -111,7 +111,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_gram_combine(int64_t nchunk, int ka, int kb, const T* __restrict__ part, T* __restrict__ G,
                int64_t ldg, int sym, int* __restrict__ ticket, T* __restrict__ L,
-               T* __restrict__ Uinv, int* status) {
+               T* __restrict__ Uinv, int* status, T tau2) {
   combine_body(nchunk, ka, kb, part, G, ldg, sym);
   if (!ticket) return;
   __shared__ int s_last;
@@ -125,7 +125,7 @@ k_gram_combine(int64_t nchunk, int ka, int kb, const T* __restrict__ part, T* __
   if (!s_last) return;
   __threadfence();
   if ((threadIdx.x >> 5) == 0 && *reinterpret_cast<volatile int*>(status) == 0)
-    warp_cholesky_inv<T, 16>(ka, G, ldg, L, Uinv, status);
+    warp_cholesky_inv<T, 16>(ka, G, ldg, L, Uinv, status, tau2);
 }
 
 
@@ -644,12 +644,12 @@ int grid_for(int64_t total, int threads = 256, int64_t cap = kNumSMs * 8) {
 template <typename T>
 void gram_combine(const GramPlan& p, int64_t ka, int64_t kb, const T* part, T* G, int64_t ldg, int sym,
                   cudaStream_t s, int* ticket = nullptr, T* L = nullptr, T* Uinv = nullptr,
-                  int* status = nullptr) {
+                  int* status = nullptr, T tau2 = T(0)) {
   if (p.nchunk == 1 && !sym) return;  // the kernel wrote G directly
   const int64_t warps = sym ? ka * (ka + 1) / 2 : ka * kb;
   k_gram_combine<T><<<static_cast<unsigned>(ceil_div(warps, 8)), 256, 0, s>>>(
       p.nchunk, static_cast<int>(ka), static_cast<int>(kb), part, G, ldg, sym, ticket, L, Uinv,
-      status);
+      status, tau2);
   MPB_LAUNCH_CHECK();
 }
 
@@ -662,7 +662,7 @@ int64_t gram_workspace_elems(int64_t n, int64_t ka, int64_t kb) {
 template <typename T>
 static void gram_impl(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B,
                       int64_t ldb, T* G, int64_t ldg, int sym, T* work, cudaStream_t s, T* L,
-                      T* Uinv, int* status) {
+                      T* Uinv, int* status, T tau2 = T(0)) {
   if (ka <= 0 || kb <= 0) return;
   if (n <= 0) {
     for (int64_t j = 0; j < kb; ++j)
@@ -702,7 +702,7 @@ static void gram_impl(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb
         default: launch(std::integral_constant<int, 4>()); break;
       }
       MPB_LAUNCH_CHECK();
-      gram_combine<T>(p, ka, kb, part, G, ldg, sym, s, L ? ticket : nullptr, L, Uinv, status);
+      gram_combine<T>(p, ka, kb, part, G, ldg, sym, s, L ? ticket : nullptr, L, Uinv, status, tau2);
       return;
     }
   }
@@ -726,7 +726,7 @@ static void gram_impl(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb
       break;
   }
   MPB_LAUNCH_CHECK();
-  gram_combine<T>(p, ka, kb, part, G, ldg, sym, s, L ? ticket : nullptr, L, Uinv, status);
+  gram_combine<T>(p, ka, kb, part, G, ldg, sym, s, L ? ticket : nullptr, L, Uinv, status, tau2);
 }
 
 template <typename T>
@@ -737,9 +737,9 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
 
 template <typename T>
 bool gram_cholesky(int64_t n, int64_t m, const T* V, int64_t ldv, T* G, T* work, T* L, T* Uinv,
-                   int* status, cudaStream_t s) {
+                   int* status, cudaStream_t s, T tau2) {
   if (m > 16 || n <= 0) return false;
-  gram_impl<T>(n, m, V, ldv, m, V, ldv, G, m, 1, work, s, L, Uinv, status);
+  gram_impl<T>(n, m, V, ldv, m, V, ldv, G, m, 1, work, s, L, Uinv, status, tau2);
   return true;
 }
 
@@ -896,7 +896,7 @@ void frob_sq(int64_t n, int64_t c, const T* X, int64_t ldx, double* out, double*
   template void gemm_tn<T>(int64_t, int64_t, int64_t, T, const T*, int64_t, const T*, int64_t, \
                            T, const T*, int64_t, T*, int64_t, cudaStream_t);                    \
   template bool gram_cholesky<T>(int64_t, int64_t, const T*, int64_t, T*, T*, T*, T*, int*,   \
-                                 cudaStream_t);                                                \
+                                 cudaStream_t, T);                                             \
   template void gemm_tn_pair<T>(int64_t, int64_t, int64_t, const T*, const T*, int64_t, const T*, \
                                 int64_t, T*, T*, int64_t, cudaStream_t);                          \
   template void copy_block<T>(int64_t, int64_t, const T*, int64_t, T*, int64_t, cudaStream_t); \

@@ -34,7 +34,7 @@ void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, 
 // combine; returns false (nothing launched) when m > 16.
 template <typename T>
 bool gram_cholesky(int64_t n, int64_t m, const T* V, int64_t ldv, T* G, T* work, T* L, T* Uinv,
-                   int* status, cudaStream_t s);
+                   int* status, cudaStream_t s, T tau2 = T(0));
 
 // Y1 = A1 C and Y2 = A2 C in one launch (the S C / AS C update pair)
 template <typename T>
@@ -113,7 +113,7 @@ void small_symmetrize(int64_t s, T* G, int64_t ldg, cudaStream_t st);
 // Uinv = L^{-T} (upper).  On failure status = {NOT_PD|OVERFLOW, index}.
 template <typename T>
 void small_cholesky_inv(int64_t m, const T* G, int64_t ldg, T* L, T* Uinv, int* status,
-                        cudaStream_t st);
+                        cudaStream_t st, T tau2 = T(0));
 // Rinv = R^{-1} for upper-triangular R (check_tri_diag, dense_kernels.hpp:163-170)
 template <typename T>
 void small_upper_inverse(int64_t m, const T* R, int64_t ldr, T* Rinv, int* status,

@@ -50,7 +50,7 @@ __device__ __forceinline__ T warp_sum_s(T v) {
 template <typename T>
 __global__ void __launch_bounds__(kSmallThreads)
 k_cholesky_inv(int m, const T* __restrict__ G, int64_t ldg, T* __restrict__ L,
-               T* __restrict__ Uinv, int* status, int use_smem) {
+               T* __restrict__ Uinv, int* status, int use_smem, T tau2) {
   extern __shared__ __align__(16) unsigned char raw[];
   T* As = use_smem ? reinterpret_cast<T*>(raw) : L;  // working lower triangle -> L
   T* Us = use_smem ? As + m * m : Uinv;
@@ -72,7 +72,7 @@ k_cholesky_inv(int m, const T* __restrict__ G, int64_t ldg, T* __restrict__ L,
           status[0] = MPEIG_E_OVERFLOW;
           status[1] = j;
         }
-      } else if (!(s > T(0))) {
+      } else if (!(s > T(0)) || (tau2 > T(0) && !(s >= tau2 * G[j + static_cast<int64_t>(j) * ldg]))) {
         fail = 1;
         if (status[0] == 0) {
           status[0] = MPEIG_E_NOT_PD;
@@ -347,8 +347,8 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
 template <typename T, int MAXM>
 __global__ void __launch_bounds__(32)
 k_cholesky_inv_warp(int m, const T* __restrict__ G, int64_t ldg, T* __restrict__ L,
-                    T* __restrict__ Uinv, int* status) {
-  warp_cholesky_inv<T, MAXM>(m, G, ldg, L, Uinv, status);
+                    T* __restrict__ Uinv, int* status, T tau2) {
+  warp_cholesky_inv<T, MAXM>(m, G, ldg, L, Uinv, status, tau2);
 }
 
 // R^{-1} of an upper-triangular R, one warp (smallwarp.cuh)
@@ -508,14 +508,14 @@ void small_symmetrize(int64_t s, T* G, int64_t ldg, cudaStream_t st) {
 
 template <typename T>
 void small_cholesky_inv(int64_t m, const T* G, int64_t ldg, T* L, T* Uinv, int* status,
-                        cudaStream_t st) {
+                        cudaStream_t st, T tau2) {
   if (m <= 0) return;
   ProfScope prof("small_chol", st, 0, 0);
   if ((m <= 16 || (sizeof(T) == 4 && m <= 32))) {
     if (m <= 16)
-      k_cholesky_inv_warp<T, 16><<<1, 32, 0, st>>>(static_cast<int>(m), G, ldg, L, Uinv, status);
+      k_cholesky_inv_warp<T, 16><<<1, 32, 0, st>>>(static_cast<int>(m), G, ldg, L, Uinv, status, tau2);
     else
-      k_cholesky_inv_warp<T, 32><<<1, 32, 0, st>>>(static_cast<int>(m), G, ldg, L, Uinv, status);
+      k_cholesky_inv_warp<T, 32><<<1, 32, 0, st>>>(static_cast<int>(m), G, ldg, L, Uinv, status, tau2);
     MPB_LAUNCH_CHECK();
     return;
   }
@@ -523,7 +523,7 @@ void small_cholesky_inv(int64_t m, const T* G, int64_t ldg, T* L, T* Uinv, int* 
   const int use = bytes <= kSmemCap;
   if (use) allow_smem(k_cholesky_inv<T>, bytes);
   k_cholesky_inv<T><<<1, kSmallThreads, use ? bytes : 0, st>>>(static_cast<int>(m), G, ldg, L, Uinv,
-                                                               status, use);
+                                                               status, use, tau2);
   MPB_LAUNCH_CHECK();
 }
 
@@ -582,7 +582,7 @@ void hl_coeffs_f32(int64_t s, int64_t m, int64_t p, const float* C, int64_t ldc,
 
 #define MPB_INST(T)                                                                            \
   template void small_symmetrize<T>(int64_t, T*, int64_t, cudaStream_t);                       \
-  template void small_cholesky_inv<T>(int64_t, const T*, int64_t, T*, T*, int*, cudaStream_t); \
+  template void small_cholesky_inv<T>(int64_t, const T*, int64_t, T*, T*, int*, cudaStream_t, T); \
   template void small_upper_inverse<T>(int64_t, const T*, int64_t, T*, int*, cudaStream_t);    \
   template void small_matmul<T>(int64_t, int64_t, int64_t, const T*, int64_t, const T*,        \
                                 int64_t, T*, int64_t, cudaStream_t);                            \

@@ -69,21 +69,29 @@ __device__ __forceinline__ bool warp_upper_inverse(int m, const TS* __restrict__
 // G = L L^T and Uinv = L^{-T} (dense_cholesky, dense_kernels.hpp:128-152) by
 // one warp for m <= MAXM <= 32: lane i holds row i.  G is read through L2
 // (__ldcg: it may have been written by other CTAs of the calling kernel).
-// Failure -> status {NOT_PD | OVERFLOW, column}, returns false.
+// Failure -> status {NOT_PD | OVERFLOW, column}, returns false.  tau2 > 0
+// (conditioning guard of the speculative CholQR): a pivot below tau2 * G_jj,
+// i.e. column j with less than sqrt(tau2) of its norm outside the span of the
+// columns before it, also fails as NOT_PD.
 template <typename T, int MAXM>
 __device__ __forceinline__ bool warp_cholesky_inv(int m, const T* __restrict__ G, int64_t ldg,
                                                   T* __restrict__ L, T* __restrict__ Uinv,
-                                                  int* status) {
+                                                  int* status, T tau2 = T(0)) {
   const int lane = threadIdx.x & 31;
   T a[MAXM];
 #pragma unroll
   for (int j = 0; j < MAXM; ++j)
     a[j] = (lane < m && j < m && lane >= j) ? __ldcg(G + lane + static_cast<int64_t>(j) * ldg) : T(0);
+  T gdiag = T(0);  // G(lane, lane) before the elimination
+#pragma unroll
+  for (int j = 0; j < MAXM; ++j)
+    if (j == lane) gdiag = a[j];
 #pragma unroll
   for (int j = 0; j < MAXM; ++j) {
     if (j >= m) break;
     const T d2 = __shfl_sync(0xffffffffu, a[j], j);
-    if (!isfinite(static_cast<double>(d2)) || !(d2 > T(0))) {
+    const T gjj = __shfl_sync(0xffffffffu, gdiag, j);
+    if (!isfinite(static_cast<double>(d2)) || !(d2 > T(0)) || (tau2 > T(0) && !(d2 >= tau2 * gjj))) {
       if (lane == 0 && status[0] == 0) {
         status[0] = isfinite(static_cast<double>(d2)) ? MPEIG_E_NOT_PD : MPEIG_E_OVERFLOW;
         status[1] = j;

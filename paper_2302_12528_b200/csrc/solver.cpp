@@ -382,14 +382,26 @@ static void tsqr_R(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, int* st
   tsqr_r<T, T>(P * m, m, w.rstk2.p, P * m, w.Rw(), m, w.tsqr_w2.p, status, s, nullptr, w.Rinv());
 }
 
-// CholQR's Gram + Cholesky (fused on one GPU)
+// CholQR's Gram + Cholesky of X (default w.V), fused on one GPU; tau2 > 0 is
+// the conditioning guard of the speculative CholQR (warp_cholesky_inv)
 template <typename T>
-static void gram_chol(Work<T>& w, int64_t m, int* status) {
+static void gram_chol(Work<T>& w, int64_t m, int* status, const T* X = nullptr, int64_t ldx = 0,
+                      T tau2 = T(0)) {
+  if (!X) {
+    X = w.V.p;
+    ldx = w.ld;
+  }
   if (!dist(w.ctx) &&
-      gram_cholesky<T>(w.n, m, w.V.p, w.ld, w.G.p, w.gramw.p, w.L(), w.Uinv(), status, w.s))
+      gram_cholesky<T>(w.n, m, X, ldx, w.G.p, w.gramw.p, w.L(), w.Uinv(), status, w.s, tau2))
     return;
-  dgram<T>(w, m, w.V.p, w.ld, m, w.V.p, w.ld, w.G.p, m, 1);
-  small_cholesky_inv<T>(m, w.G.p, m, w.L(), w.Uinv(), status, w.s);
+  dgram<T>(w, m, X, ldx, m, X, ldx, w.G.p, m, 1);
+  small_cholesky_inv<T>(m, w.G.p, m, w.L(), w.Uinv(), status, w.s, tau2);
+}
+
+// guard of the CholQR first pass (option "spec_qr" = k > 0: fp64 1e-k)
+template <typename T>
+static T cholqr_tau2(const mpeig_ctx* ctx) {
+  return sizeof(T) == 8 ? T(std::pow(10.0, -std::max(1, ctx->spec_qr))) : T(1e-4);
 }
 
 // ------------------------------------------------------------- QR family
@@ -481,6 +493,21 @@ template <typename T>
 int64_t orthonormal_q_dropping(Work<T>& w, int64_t m, T* W, int64_t ldw, bool use_mixed,
                                int64_t* dropped) {
   *dropped = 0;
+  if (w.ctx->spec_qr && m > 0) {
+    // the guarded Cholesky-QR of qr_spec first (so the eager, careful and
+    // speculative paths take identical steps); W is overwritten only when
+    // both passes succeed, else the reference's QR chain below runs on it
+    cudaStream_t s = w.s;
+    status_clear(w.ctx);
+    gram_chol<T>(w, m, w.ctx->d_status, W, ldw, cholqr_tau2<T>(w.ctx));
+    gemm_tn<T>(w.n, m, m, T(1), W, ldw, w.Uinv(), m, T(0), nullptr, 0, w.V.p, w.ld, s);
+    gram_chol<T>(w, m, w.ctx->d_status);
+    status_fetch(w.ctx);
+    if (w.ctx->h_status[0] == 0) {
+      gemm_tn<T>(w.n, m, m, T(1), w.V.p, w.ld, w.Uinv(), m, T(0), nullptr, 0, W, ldw, s);
+      return m;
+    }
+  }
   try {
     orthonormal_q<T>(w, m, W, ldw, use_mixed);
     return m;
@@ -725,8 +752,21 @@ template <typename T>
 static void qr_spec(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, int* status) {
   cudaStream_t s = w.s;
   const int64_t n = w.n;
-  tsqr_R<T>(w, m, W, ldw, lower, status);
-  gemm_tn<T>(n, m, m, T(1), W, ldw, w.Rinv(), m, T(0), nullptr, 0, w.V.p, w.ld, s);
+  if (w.ctx->spec_qr) {
+    // First pass as a guarded Cholesky-QR instead of the TSQR R: one Gram
+    // (no column-serial reduction chain).  Cholesky is invariant to column
+    // scaling, so the guard tests the equilibrated pivots: every column must
+    // keep >= 1e-5 (fp64) / 1e-2 (fp32) of its norm outside the span of the
+    // ones before it.  Then V = W R1^-1 is orthonormal to ~eps * cond^2 <<
+    // 1 and the second pass makes Q orthonormal to rounding, as the
+    // reference's QR does.  A failed guard rolls the iteration back to the
+    // careful path (the reference's mixed_qr / householder_qr).
+    gram_chol<T>(w, m, status, W, ldw, cholqr_tau2<T>(w.ctx));
+    gemm_tn<T>(n, m, m, T(1), W, ldw, w.Uinv(), m, T(0), nullptr, 0, w.V.p, w.ld, s);
+  } else {
+    tsqr_R<T>(w, m, W, ldw, lower, status);
+    gemm_tn<T>(n, m, m, T(1), W, ldw, w.Rinv(), m, T(0), nullptr, 0, w.V.p, w.ld, s);
+  }
   gram_chol<T>(w, m, status);
   gemm_tn<T>(n, m, m, T(1), w.V.p, w.ld, w.Uinv(), m, T(0), nullptr, 0, W, ldw, s);
 }
@@ -969,6 +1009,7 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
                           ctx->h_status[kSlotEig];
       int64_t dropped = 0, pn = std::min(m, m + p);
       if (failed) {
+        ++ctx->spec_rollbacks;
         // ---- roll back and repeat on the careful path
         MPB_CUDA(cudaMemcpyAsync(w.theta.p, w.theta_prev.p, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
         T* Wslot = w.S.p + (m + p) * w.ld;

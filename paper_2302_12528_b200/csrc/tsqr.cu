@@ -388,40 +388,81 @@ k_tsqr_reg(int64_t n, int m, const Tin* __restrict__ W, int64_t ldw, Tq* __restr
     idx = parent;
     t.factor(m, vbuf, sbeta);
   }
-  // root: this CTA holds R of the whole block
-  t.store_r(m, level);
+  // root: this CTA holds R of the whole block in registers.  Diagonal to
+  // shared memory, then R with rows of positive diagonal (fix_diagonal_phases)
+  // straight from the registers, and the k_tsqr_finish checks by one warp.
+  Tq* sdiag = vbuf[0];  // the reflector buffers are free now (b >= m)
   __syncthreads();
-  const Tq* Rr = level;
-  for (int64_t e = threadIdx.x; e < mm; e += blockDim.x) {
-    const int i = static_cast<int>(e % m), j = static_cast<int>(e / m);
-    const Tq d = Rr[i + static_cast<int64_t>(i) * m];
-    const Tq v = i <= j ? Rr[e] : Tq(0);
-    Rfinal[i + static_cast<int64_t>(j) * ldr] = d < Tq(0) ? -v : v;
+#pragma unroll
+  for (int q = 0; q < MPW; ++q) {
+    const int c = warp + NW * q;
+    if (c < m) {
+#pragma unroll
+      for (int i = 0; i < RPL; ++i)
+        if (lane + 32 * i == c) sdiag[c] = t.a[q][i];
+    }
   }
-  if (threadIdx.x == 0 && *reinterpret_cast<volatile int*>(status) == 0) {
+  __syncthreads();
+  Tq* sR = vbuf[1];  // signed R for the fused epilogue (m <= 16: m*m <= b)
+  const bool stage = Rinv_out != nullptr && m * m <= B;
+#pragma unroll
+  for (int q = 0; q < MPW; ++q) {
+    const int c = warp + NW * q;
+    if (c >= m) continue;
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = lane + 32 * i;
+      if (r < m) {
+        const Tq v = r <= c ? (sdiag[r] < Tq(0) ? -t.a[q][i] : t.a[q][i]) : Tq(0);
+        Rfinal[r + static_cast<int64_t>(c) * ldr] = v;
+        if (stage) sR[r + c * m] = v;
+      }
+    }
+  }
+  if (warp == 0 && *reinterpret_cast<volatile int*>(status) == 0) {
     Tq dmax = Tq(0);
-    for (int j = 0; j < m; ++j) dmax = fmax(dmax, fabs(Rr[j + static_cast<int64_t>(j) * m]));
+    for (int j = lane; j < m; j += 32) dmax = fmax(dmax, fabs(sdiag[j]));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, off));
     const Tq eps = sizeof(Tq) == 8 ? Tq(2.220446049250313e-16) : Tq(1.1920929e-7f);
-    for (int j = 0; j < m; ++j) {
-      const Tq d = fabs(Rr[j + static_cast<int64_t>(j) * m]);
-      if (!isfinite(static_cast<double>(d))) {
-        status[0] = MPEIG_E_OVERFLOW;
-        status[1] = j;
-        break;
+    // the first failing column decides the code, as the serial scan would
+    int first = 0x7fffffff, code = 0;
+    for (int j = lane; j < m; j += 32) {
+      const Tq d = fabs(sdiag[j]);
+      int cj = 0;
+      if (!isfinite(static_cast<double>(d)))
+        cj = MPEIG_E_OVERFLOW;
+      else if (d == Tq(0) || (numeric_rank_check && d <= Tq(m) * eps * dmax))
+        cj = MPEIG_E_RANK_DEFICIENT;
+      if (cj && j < first) {
+        first = j;
+        code = cj;
       }
-      if (d == Tq(0) || (numeric_rank_check && d <= Tq(m) * eps * dmax)) {
-        status[0] = MPEIG_E_RANK_DEFICIENT;
-        status[1] = j;
-        break;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const int of = __shfl_xor_sync(0xffffffffu, first, off);
+      const int oc = __shfl_xor_sync(0xffffffffu, code, off);
+      if (of < first) {
+        first = of;
+        code = oc;
       }
+    }
+    if (lane == 0 && code) {
+      status[0] = code;
+      status[1] = first;
     }
   }
   if (Rinv_out) {
     // fused epilogue of the QR's next two steps for m <= 16: R in the
     // working precision (Rw_out) and R^{-1} (Rinv_out), by warp 0
     __syncthreads();
-    if (warp == 0 && *reinterpret_cast<volatile int*>(status) == 0)
-      warp_upper_inverse<Tin, Tq, 16>(m, Rfinal, ldr, Rw_out, Rinv_out, status);
+    if (warp == 0 && *reinterpret_cast<volatile int*>(status) == 0) {
+      if (stage)
+        warp_upper_inverse<Tin, Tq, 16>(m, sR, m, Rw_out, Rinv_out, status);
+      else
+        warp_upper_inverse<Tin, Tq, 16>(m, Rfinal, ldr, Rw_out, Rinv_out, status);
+    }
   }
 }
 

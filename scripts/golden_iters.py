@@ -2,6 +2,7 @@
 (and the reference's own FMA-rounding spread).  GPU box helper:
 
     python scripts/golden_iters.py [name-substring ...]
+    MPEIG_OPTS="spec_qr=0,..." selects execution options of the default context.
 """
 import os
 import sys
@@ -18,13 +19,19 @@ from test_gpu_solver import iteration_band, make_op, sensitivity  # noqa: E402
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 names = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and f != "pcg64.npz")
 flt = sys.argv[1:]
+ctx = mp.default_context()
+for kv in filter(None, os.environ.get("MPEIG_OPTS", "").split(",")):
+    k, v = kv.split("=")
+    ctx.set_option(k, int(v))
 for name in names:
     if flt and not any(s in name for s in flt):
         continue
     g = load_golden(name)
     kw = eval(str(g["kw"]))
     cfg = mp.SolverConfig(variant=str(g["variant"]), **kw)
+    ctx.spec_rollbacks(reset=True)
     r = mp.solve(make_op(mp, name), cfg)
+    rb = ctx.spec_rollbacks()
     ref = (int(g["iters_lower"]), int(g["iters_working"]))
     tot = sum(ref)
     sens = sensitivity(name) or {}
@@ -34,4 +41,5 @@ for name in names:
     band = iteration_band(name, tot)
     ok = abs(sum(got) - tot) <= band
     print(f"{name:28s} ref {ref[0]:5d}+{ref[1]:5d}  fma {fma}  gpu {got[0]:5d}+{got[1]:5d}  "
-          f"d={sum(got) - tot:+5d} band {band:4d} {'ok' if ok else 'OUT'}  theta {rel:.1e}", flush=True)
+          f"d={sum(got) - tot:+5d} band {band:4d} {'ok' if ok else 'OUT'}  theta {rel:.1e}  rollbacks {rb}",
+          flush=True)

@@ -46,7 +46,7 @@ int main() {
     CK(cudaMemcpy(dG, G.data(), m * m * 8, cudaMemcpyHostToDevice));
     small_upper_inverse<double>(m, dR, m, dRi, st, s);
     CK(cudaStreamSynchronize(s));
-    small_cholesky_inv<double>(m, dG, m, dL, dU, st, s);
+    small_cholesky_inv<double>(m, dG, m, dL, dU, st, s, 0.0);
     CK(cudaStreamSynchronize(s));
     std::vector<double> Ri(m * m), L(m * m), U(m * m);
     int hs[2];
