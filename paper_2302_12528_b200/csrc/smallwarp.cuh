@@ -83,6 +83,7 @@ __device__ __forceinline__ bool warp_cholesky_inv(int m, const T* __restrict__ G
   for (int j = 0; j < MAXM; ++j)
     a[j] = (lane < m && j < m && lane >= j) ? __ldcg(G + lane + static_cast<int64_t>(j) * ldg) : T(0);
   T gdiag = T(0);  // G(lane, lane) before the elimination
+  T rdiag = T(0);  // 1 / L(lane, lane)
 #pragma unroll
   for (int j = 0; j < MAXM; ++j)
     if (j == lane) gdiag = a[j];
@@ -98,8 +99,16 @@ __device__ __forceinline__ bool warp_cholesky_inv(int m, const T* __restrict__ G
       }
       return false;
     }
-    const T d = sqrt(d2), rd = T(1) / d;
+    // one reciprocal square root on the serial chain (not sqrt + divide)
+    T rd = rsqrt(d2);
+    if constexpr (sizeof(T) == 4) {
+      // rsqrtf: a 2-ulp approximation with a one-sided bias; one Newton step
+      const T h = d2 * rd;
+      rd = rd * fma(T(-0.5) * h, rd, T(1.5));
+    }
+    const T d = d2 * rd;
     const T lij = lane > j ? a[j] * rd : (lane == j ? d : T(0));
+    if (lane == j) rdiag = rd;
     a[j] = lij;
 #pragma unroll
     for (int k = j + 1; k < MAXM; ++k) {
@@ -113,22 +122,24 @@ __device__ __forceinline__ bool warp_cholesky_inv(int m, const T* __restrict__ G
       if (j < m) L[lane + j * m] = a[j];
   }
   if (!Uinv) return true;
-  // X = L^{-1}: column c by lane c (forward substitution); Uinv(c, i) = X(i, c)
-  T x[MAXM];
+  // X = L^{-1}, column c by lane c, right-looking: x_l is final once the
+  // updates of rows < l are in, then every later row's sum takes its term
+  // at once (independent FMAs), so the serial chain is one multiply and one
+  // FMA per row.  The L(i, l) broadcasts do not depend on x.  Uinv(c, i) = X(i, c).
   const int c = lane;
+  T acc[MAXM];
 #pragma unroll
-  for (int i = 0; i < MAXM; ++i) {
-    if (i >= m) break;
-    T s = i == c ? T(1) : T(0);
+  for (int i = 0; i < MAXM; ++i) acc[i] = i == c ? T(1) : T(0);
 #pragma unroll
-    for (int l = 0; l < i; ++l) s = fma(-__shfl_sync(0xffffffffu, a[l], i), x[l], s);
-    const T dii = __shfl_sync(0xffffffffu, a[i], i);
-    x[i] = i >= c ? s / dii : T(0);
-  }
-  if (c < m) {
+  for (int l = 0; l < MAXM; ++l) {
+    if (l >= m) break;
+    const T xl = acc[l] * __shfl_sync(0xffffffffu, rdiag, l);
+    if (c < m) Uinv[c + l * m] = xl;
 #pragma unroll
-    for (int i = 0; i < MAXM; ++i)
-      if (i < m) Uinv[c + i * m] = x[i];
+    for (int i = l + 1; i < MAXM; ++i) {
+      const T lil = __shfl_sync(0xffffffffu, a[l], i);
+      if (i < m) acc[i] = fma(-lil, xl, acc[i]);
+    }
   }
   return true;
 }
