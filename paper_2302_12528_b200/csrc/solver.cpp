@@ -403,6 +403,14 @@ template <typename T>
 static T cholqr_tau2(const mpeig_ctx* ctx) {
   return sizeof(T) == 8 ? T(std::pow(10.0, -std::max(1, ctx->spec_qr))) : T(1e-4);
 }
+// guard of the single CholQR pass of the second project + QR round (fp64
+// stage): every equilibrated pivot >= 1/2, i.e. cond(W) ~ 1, so one pass is
+// orthonormal to ~eps * cond^2 ~ eps (W is the first round's Q minus an
+// O(u cond) overlap).  The fp32 stage keeps both passes: its length is set by
+// how well the fp32 iteration holds orthogonality, and one
+// fp32 pass measurably lengthens it (lap2d 5x500: 880 vs 797 iterations).
+template <typename T>
+constexpr T kCholQrSingleTau2 = T(0.25);
 
 // ------------------------------------------------------------- QR family
 // Q (in place) by "R from a Householder TSQR, then Cholesky-QR of W R^-1":
@@ -491,9 +499,19 @@ int64_t ortho_dropping(Work<T>& w, int64_t m, T* W, int64_t ldw, T drop_tol) {
 // detail::orthonormal_q_dropping (eigensolvers.hpp:74-85)
 template <typename T>
 int64_t orthonormal_q_dropping(Work<T>& w, int64_t m, T* W, int64_t ldw, bool use_mixed,
-                               int64_t* dropped) {
+                               int64_t* dropped, bool second) {
   *dropped = 0;
-  if (w.ctx->spec_qr && m > 0) {
+  if (w.ctx->spec_qr && m > 0 && second && sizeof(T) == 8) {
+    // second round (qr_spec): one guarded CholQR pass, in place
+    cudaStream_t s = w.s;
+    status_clear(w.ctx);
+    gram_chol<T>(w, m, w.ctx->d_status, W, ldw, kCholQrSingleTau2<T>);
+    status_fetch(w.ctx);
+    if (w.ctx->h_status[0] == 0) {
+      gemm_tn<T>(w.n, m, m, T(1), W, ldw, w.Uinv(), m, T(0), nullptr, 0, W, ldw, s);
+      return m;
+    }
+  } else if (w.ctx->spec_qr && m > 0) {
     // the guarded Cholesky-QR of qr_spec first (so the eager, careful and
     // speculative paths take identical steps); W is overwritten only when
     // both passes succeed, else the reference's QR chain below runs on it
@@ -703,7 +721,7 @@ StageResult lobpcg_stage_eager(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, con
     if (wc > 0) {
       int64_t more = 0;
       project_out<T>(w, w.S.p, b, w.ld, Wslot, wc, w.ld, 1);
-      wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, opt.use_mixed_qr != 0, &more);
+      wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, opt.use_mixed_qr != 0, &more, true);
       dropped += more;
     }
     rec.w_columns_dropped = dropped;
@@ -749,9 +767,18 @@ enum : int { kSlotOvf = 2, kSlotEig = 3, kSlotHl = 4, kSlotQr1 = 6, kSlotQr2 = 8
 // written unconditionally and failures only land in `status` (the caller
 // rolls the iteration back and repeats it on the careful path).
 template <typename T>
-static void qr_spec(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, int* status) {
+static void qr_spec(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, int* status,
+                    bool second = false) {
   cudaStream_t s = w.s;
   const int64_t n = w.n;
+  if (w.ctx->spec_qr && second && sizeof(T) == 8) {
+    // second round: W is already orthonormal up to the scrubbed overlap, so
+    // one guarded CholQR pass (in place: every GEMM kernel reads all of a
+    // row's inputs before it writes the row)
+    gram_chol<T>(w, m, status, W, ldw, kCholQrSingleTau2<T>);
+    gemm_tn<T>(n, m, m, T(1), W, ldw, w.Uinv(), m, T(0), nullptr, 0, W, ldw, s);
+    return;
+  }
   if (w.ctx->spec_qr) {
     // First pass as a guarded Cholesky-QR instead of the TSQR R: one Gram
     // (no column-serial reduction chain).  Cholesky is invariant to column
@@ -840,7 +867,7 @@ static void spec_body(Work<T>& w, const mpeig_op* A, const mpeig_op* T_op, int64
   project_out<T>(w, S, m + p, ld, Wslot, m, ld, 2);
   qr_spec<T>(w, m, Wslot, ld, mixed, ctx->d_status + kSlotQr1);
   project_out<T>(w, S, m + p, ld, Wslot, m, ld, 1);
-  qr_spec<T>(w, m, Wslot, ld, mixed, ctx->d_status + kSlotQr2);
+  qr_spec<T>(w, m, Wslot, ld, mixed, ctx->d_status + kSlotQr2, true);
   if (ev.on) MPB_CUDA(cudaEventRecord(ev.e[1], s));
   op_apply<T>(ctx, A, m, Wslot, ld, AS + (m + p) * ld, ld);
   const int64_t sdim = 2 * m + p;
@@ -1024,7 +1051,7 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
         if (wc > 0) {
           int64_t more = 0;
           project_out<T>(w, w.S.p, b, w.ld, Wslot, wc, w.ld, 1);
-          wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, mixed, &more);
+          wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, mixed, &more, true);
           dropped += more;
         }
         tm.orthogonalize += timer.stop();
@@ -1315,7 +1342,7 @@ template struct Work<float>;
 template void orthonormal_q<double>(Work<double>&, int64_t, double*, int64_t, bool);
 template void orthonormal_q<float>(Work<float>&, int64_t, float*, int64_t, bool);
 template int64_t orthonormal_q_dropping<double>(Work<double>&, int64_t, double*, int64_t, bool,
-                                                int64_t*);
+                                                int64_t*, bool);
 template void project_out<double>(Work<double>&, const double*, int64_t, int64_t, double*, int64_t,
                                   int64_t, int);
 template void small_eig<double>(Work<double>&, int64_t, double*, int64_t, double*);

@@ -61,7 +61,7 @@ template <typename T>
 void orthonormal_q(Work<T>& w, int64_t m, T* W, int64_t ldw, bool use_mixed);
 template <typename T>
 int64_t orthonormal_q_dropping(Work<T>& w, int64_t m, T* W, int64_t ldw, bool use_mixed,
-                               int64_t* dropped);
+                               int64_t* dropped, bool second = false);
 template <typename T>
 void project_out(Work<T>& w, const T* B, int64_t b, int64_t ldb, T* W, int64_t wc, int64_t ldw,
                  int passes);
