@@ -255,3 +255,24 @@ def test_execution_modes_bitwise_identical(gpu, variant):
         assert np.array_equal(r.theta, out[0].theta)
         assert np.array_equal(r.residual_norms, out[0].residual_norms)
         assert [h.ritz_values for h in r.history] == [h.ritz_values for h in out[0].history]
+
+
+@pytest.mark.parametrize("variant", ["mplobpcg-schol", "dlobpcg-dchol"])
+def test_guarded_cholqr_matches_tsqr_path(gpu, variant):
+    """The speculative body's guarded Cholesky-QR (option spec_qr, default on)
+    and the TSQR-based QR give the same eigenpairs and iteration counts within
+    the rounding band, including a block wider than the one-warp kernels
+    (m = 48: CTA Cholesky with the guard)."""
+    import torch
+    res = {}
+    for opt in (10, 0):
+        ctx = gpu.Context(0, stream=torch.cuda.Stream())
+        ctx.set_option("spec_qr", opt)
+        A = gpu.laplace3d(24, ctx=ctx)
+        cfg = gpu.SolverConfig(k=32, block=48, tol=1e-10, maxit=5000, variant=variant)
+        res[opt] = gpu.solve(A, cfg, want_X=False)
+    a, b = res[10], res[0]
+    assert a.converged and b.converged
+    assert np.abs(a.theta - b.theta).max() <= 1e-10 * np.abs(b.theta).max()
+    ta, tb = a.iterations_lower + a.iterations_working, b.iterations_lower + b.iterations_working
+    assert abs(ta - tb) <= max(4, int(0.08 * tb)), (ta, tb)
