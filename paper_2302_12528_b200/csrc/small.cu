@@ -392,10 +392,12 @@ k_hl_coeffs_warp(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* _
     for (int j = 0; j < MAXM; ++j) {
       if (j < p && !bad) {  // guards, not break: the loops stay fully unrolled
         if (lane == j) {
-          double tail = 0.0;
+          // four partial sums: the reduction is on the serial path
+          double tp[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
           for (int a = j + 1; a < MAXM; ++a)
-            tail = fma(static_cast<double>(mc[a]), static_cast<double>(mc[a]), tail);
+            tp[a & 3] = fma(static_cast<double>(mc[a]), static_cast<double>(mc[a]), tp[a & 3]);
+          const double tail = (tp[0] + tp[1]) + (tp[2] + tp[3]);
           const double x0 = static_cast<double>(mc[j]);
           const double nrm = sqrt(fma(x0, x0, tail));
           if (nrm == 0.0) {
@@ -417,9 +419,10 @@ k_hl_coeffs_warp(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* _
         const double beta = Bs[j];
         if (beta < 0.0) bad = 1;
         if (!bad && lane > j && lane < m) {
-          T dot = T(0);
+          T dp[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
-          for (int a = j; a < MAXM; ++a) dot = fma(Vs[j][a], mc[a], dot);
+          for (int a = j; a < MAXM; ++a) dp[a & 3] = fma(Vs[j][a], mc[a], dp[a & 3]);
+          const T dot = (dp[0] + dp[1]) + (dp[2] + dp[3]);
           const T f = static_cast<T>(static_cast<double>(dot) * beta);
 #pragma unroll
           for (int a = j; a < MAXM; ++a) mc[a] = fma(-f, Vs[j][a], mc[a]);
@@ -442,9 +445,10 @@ k_hl_coeffs_warp(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* _
 #pragma unroll
       for (int j = 0; j < MAXM; ++j) {
         if (j < p) {
-          T dot = T(0);
+          T dp[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
-          for (int a = j; a < MAXM; ++a) dot = fma(y[a], Vs[j][a], dot);
+          for (int a = j; a < MAXM; ++a) dp[a & 3] = fma(y[a], Vs[j][a], dp[a & 3]);
+          const T dot = (dp[0] + dp[1]) + (dp[2] + dp[3]);
           const T f = static_cast<T>(static_cast<double>(dot) * Bs[j]);
 #pragma unroll
           for (int a = j; a < MAXM; ++a) y[a] = fma(-f, Vs[j][a], y[a]);
