@@ -114,10 +114,6 @@ void small_symmetrize(int64_t s, T* G, int64_t ldg, cudaStream_t st);
 template <typename T>
 void small_cholesky_inv(int64_t m, const T* G, int64_t ldg, T* L, T* Uinv, int* status,
                         cudaStream_t st, T tau2 = T(0));
-// second project + QR round coefficients (fp64, m <= 16, b <= 32; small.cu)
-void proj_cholqr_coeffs(int64_t b, int64_t m, const double* G, int64_t ldg, double* C, int64_t ldc,
-                        double* L, double* Uinv, int* status, double tau2, double g2max,
-                        cudaStream_t st);
 // Rinv = R^{-1} for upper-triangular R (check_tri_diag, dense_kernels.hpp:163-170)
 template <typename T>
 void small_upper_inverse(int64_t m, const T* R, int64_t ldr, T* Rinv, int* status,

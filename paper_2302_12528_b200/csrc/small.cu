@@ -584,87 +584,6 @@ void hl_coeffs_f32(int64_t s, int64_t m, int64_t p, const float* C, int64_t ldc,
   hl_coeffs_t<float>(s, m, p, C, ldc, coef, scratch, fallback, st);
 }
 
-// Second project + QR round of W in one small step (fp64, m <= 16, b <= 32):
-// from G = [B W]^T W ((b + m) x m: G2 = B^T W on top, H = W^T W below) form
-// the Gram of the projected block W' = W - B G2 without re-reading it,
-//   W'^T W' = H - G2^T G2        (B^T B = I to rounding; |G2| <= g2max),
-// factor it (guarded: pivots >= tau2 of the diagonal), and emit the
-// coefficients C = [-G2 U; U] (U = L^-T) so that ONE GEMM, W <- [B W] C,
-// applies the projection and the CholQR at once.  |G2| > g2max (the overlap
-// is not small: the Pythagorean Gram would cancel) fails as NOT_PD.
-__global__ void __launch_bounds__(256)
-k_proj_cholqr(int b, int m, const double* __restrict__ G, int64_t ldg, double* __restrict__ C,
-              int64_t ldc, double* __restrict__ L, double* __restrict__ Uinv, int* status,
-              double tau2, double g2max) {
-  __shared__ double G2[32 * 16], Ms[16 * 16], Us[16 * 16];
-  __shared__ double wmax[8];
-  __shared__ int ok;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double amax = 0.0;
-  for (int e = tid; e < b * m; e += blockDim.x) {
-    const int r = e % b, c = e / b;
-    const double v = G[r + static_cast<int64_t>(c) * ldg];
-    G2[e] = v;  // column-major b x m
-    amax = fmax(amax, isfinite(v) ? fabs(v) : INFINITY);
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, off));
-  if (lane == 0) wmax[warp] = amax;
-  __syncthreads();
-  if (tid == 0) {
-    double mx = 0.0;
-    for (int w2 = 0; w2 < 8; ++w2) mx = fmax(mx, wmax[w2]);
-    ok = mx <= g2max;
-    if (!ok && status[0] == 0) {
-      status[0] = MPEIG_E_NOT_PD;
-      status[1] = -1;
-    }
-  }
-  // M(i, j) = H(i, j) - sum_l G2(l, i) G2(l, j), lower triangle, one entry
-  // per thread (four chains over l)
-  const int np = m * (m + 1) / 2;
-  for (int e = tid; e < np; e += blockDim.x) {
-    int j = static_cast<int>((sqrt(8.0 * e + 1.0) - 1.0) / 2.0);
-    while ((j + 1) * (j + 2) / 2 <= e) ++j;
-    while (j * (j + 1) / 2 > e) --j;
-    const int i = e - j * (j + 1) / 2;  // i <= j: entry (row j, col i) of the lower triangle
-    double a[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int l = 0; l < b; ++l) a[l & 3] = fma(G2[l + j * b], G2[l + i * b], a[l & 3]);
-    Ms[j + i * m] = G[(b + j) + static_cast<int64_t>(i) * ldg] - ((a[0] + a[1]) + (a[2] + a[3]));
-  }
-  __syncthreads();
-  if (!ok) return;
-  if (warp == 0) {
-    const bool good = warp_cholesky_inv<double, 16, false>(m, Ms, m, L, Us, status, tau2);
-    if (lane == 0) ok = good;
-  }
-  __syncthreads();
-  if (!ok) return;
-  // C = [-G2 U; U], (b + m) x m, one entry per thread
-  for (int e = tid; e < (b + m) * m; e += blockDim.x) {
-    const int r = e % (b + m), j = e / (b + m);
-    double v;
-    if (r < b) {
-      double a[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int k = 0; k < m; ++k) a[k & 3] = fma(G2[r + k * b], Us[k + j * m], a[k & 3]);
-      v = -((a[0] + a[1]) + (a[2] + a[3]));
-    } else {
-      v = Us[(r - b) + j * m];
-      Uinv[(r - b) + j * m] = v;
-    }
-    C[r + static_cast<int64_t>(j) * ldc] = v;
-  }
-}
-
-void proj_cholqr_coeffs(int64_t b, int64_t m, const double* G, int64_t ldg, double* C, int64_t ldc,
-                        double* L, double* Uinv, int* status, double tau2, double g2max,
-                        cudaStream_t st) {
-  ProfScope prof("small_chol", st, 0, 0);
-  k_proj_cholqr<<<1, 256, 0, st>>>(static_cast<int>(b), static_cast<int>(m), G, ldg, C, ldc, L,
-                                   Uinv, status, tau2, g2max);
-  MPB_LAUNCH_CHECK();
-}
-
 #define MPB_INST(T)                                                                            \
   template void small_symmetrize<T>(int64_t, T*, int64_t, cudaStream_t);                       \
   template void small_cholesky_inv<T>(int64_t, const T*, int64_t, T*, T*, int*, cudaStream_t, T); \

@@ -73,21 +73,15 @@ __device__ __forceinline__ bool warp_upper_inverse(int m, const TS* __restrict__
 // (conditioning guard of the speculative CholQR): a pivot below tau2 * G_jj,
 // i.e. column j with less than sqrt(tau2) of its norm outside the span of the
 // columns before it, also fails as NOT_PD.
-template <typename T, int MAXM, bool kGlobalG = true>
+template <typename T, int MAXM>
 __device__ __forceinline__ bool warp_cholesky_inv(int m, const T* __restrict__ G, int64_t ldg,
                                                   T* __restrict__ L, T* __restrict__ Uinv,
                                                   int* status, T tau2 = T(0)) {
   const int lane = threadIdx.x & 31;
   T a[MAXM];
 #pragma unroll
-  for (int j = 0; j < MAXM; ++j) {
-    const bool in = lane < m && j < m && lane >= j;
-    const T* gp = G + lane + static_cast<int64_t>(j) * ldg;
-    if constexpr (kGlobalG)
-      a[j] = in ? __ldcg(gp) : T(0);
-    else
-      a[j] = in ? *gp : T(0);  // G in shared memory
-  }
+  for (int j = 0; j < MAXM; ++j)
+    a[j] = (lane < m && j < m && lane >= j) ? __ldcg(G + lane + static_cast<int64_t>(j) * ldg) : T(0);
   T gdiag = T(0);  // G(lane, lane) before the elimination
   T rdiag = T(0);  // 1 / L(lane, lane)
 #pragma unroll

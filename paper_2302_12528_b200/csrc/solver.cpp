@@ -538,50 +538,6 @@ int64_t orthonormal_q_dropping(Work<T>& w, int64_t m, T* W, int64_t ldw, bool us
   return kept;
 }
 
-// The second project + QR round (eigensolvers.hpp:284-288) fused for fp64 on
-// one GPU with m <= 16: one Gram [B W]^T W, the small step of
-// k_proj_cholqr_warp (Gram of the projected block by Pythagoras, guarded
-// Cholesky, coefficients C = [-G2 U; U]) and ONE GEMM W <- [B W] C, in place
-// (each GEMM row tile reads all of its inputs before it writes).  W sits
-// right after the basis in S (W = B + b ld).  Falls back to the separate
-// projection + QR when not applicable or when the guards fail.
-constexpr double kProjG2Max = 1e-3;
-template <typename T>
-static bool proj_qr2_fusable(const Work<T>& w, int64_t b, int64_t wc) {
-  return sizeof(T) == 8 && w.ctx->spec_qr != 0 && !dist(w.ctx) && wc > 0 && wc <= 16 && b > 0 &&
-         b <= 32;
-}
-
-template <typename T>
-static void proj_qr2_launch(Work<T>& w, int64_t b, T* W, int64_t wc, int* status, bool apply) {
-  if constexpr (sizeof(T) == 8) {
-    const T* S = W - b * w.ld;
-    const int64_t ka = b + wc;
-    dgram<T>(w, ka, S, w.ld, wc, W, w.ld, w.G.p, ka, 0);
-    proj_cholqr_coeffs(b, wc, w.G.p, ka, w.coef.p, ka, w.L(), w.Uinv(), status,
-                       kCholQrSingleTau2<T>, kProjG2Max, w.s);
-    if (apply) gemm_tn<T>(w.n, ka, wc, T(1), S, w.ld, w.coef.p, ka, T(0), nullptr, 0, W, w.ld, w.s);
-  }
-}
-
-template <typename T>
-static int64_t project_qr_second(Work<T>& w, int64_t b, T* W, int64_t wc, bool use_mixed,
-                                 int64_t* dropped) {
-  *dropped = 0;
-  if (proj_qr2_fusable(w, b, wc)) {
-    status_clear(w.ctx);
-    proj_qr2_launch<T>(w, b, W, wc, w.ctx->d_status, false);
-    status_fetch(w.ctx);
-    if (w.ctx->h_status[0] == 0) {
-      gemm_tn<T>(w.n, b + wc, wc, T(1), W - b * w.ld, w.ld, w.coef.p, b + wc, T(0), nullptr, 0, W,
-                 w.ld, w.s);
-      return wc;
-    }
-  }
-  project_out<T>(w, W - b * w.ld, b, w.ld, W, wc, w.ld, 1);
-  return orthonormal_q_dropping<T>(w, wc, W, w.ld, use_mixed, dropped, true);
-}
-
 // block_project_out (ortho.hpp:190-200): W -= B (B^T W), `passes` times
 template <typename T>
 void project_out(Work<T>& w, const T* B, int64_t b, int64_t ldb, T* W, int64_t wc, int64_t ldw,
@@ -764,7 +720,8 @@ StageResult lobpcg_stage_eager(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, con
     wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, opt.use_mixed_qr != 0, &dropped);
     if (wc > 0) {
       int64_t more = 0;
-      wc = project_qr_second<T>(w, b, Wslot, wc, opt.use_mixed_qr != 0, &more);
+      project_out<T>(w, w.S.p, b, w.ld, Wslot, wc, w.ld, 1);
+      wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, opt.use_mixed_qr != 0, &more, true);
       dropped += more;
     }
     rec.w_columns_dropped = dropped;
@@ -909,12 +866,8 @@ static void spec_body(Work<T>& w, const mpeig_op* A, const mpeig_op* T_op, int64
   MPB_CUDA(cudaMemcpyAsync(w.theta_prev.p, w.theta.p, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
   project_out<T>(w, S, m + p, ld, Wslot, m, ld, 2);
   qr_spec<T>(w, m, Wslot, ld, mixed, ctx->d_status + kSlotQr1);
-  if (proj_qr2_fusable(w, m + p, m)) {
-    proj_qr2_launch<T>(w, m + p, Wslot, m, ctx->d_status + kSlotQr2, true);
-  } else {
-    project_out<T>(w, S, m + p, ld, Wslot, m, ld, 1);
-    qr_spec<T>(w, m, Wslot, ld, mixed, ctx->d_status + kSlotQr2, true);
-  }
+  project_out<T>(w, S, m + p, ld, Wslot, m, ld, 1);
+  qr_spec<T>(w, m, Wslot, ld, mixed, ctx->d_status + kSlotQr2, true);
   if (ev.on) MPB_CUDA(cudaEventRecord(ev.e[1], s));
   op_apply<T>(ctx, A, m, Wslot, ld, AS + (m + p) * ld, ld);
   const int64_t sdim = 2 * m + p;
@@ -1097,7 +1050,8 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
         wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, mixed, &dropped);
         if (wc > 0) {
           int64_t more = 0;
-          wc = project_qr_second<T>(w, b, Wslot, wc, mixed, &more);
+          project_out<T>(w, w.S.p, b, w.ld, Wslot, wc, w.ld, 1);
+          wc = orthonormal_q_dropping<T>(w, wc, Wslot, w.ld, mixed, &more, true);
           dropped += more;
         }
         tm.orthogonalize += timer.stop();
