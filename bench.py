@@ -331,9 +331,50 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
+    if world == 1 and not shard and args.workload == "cfg1" and not args.no_at_scale:
+        try:
+            line["kernels_at_scale"] = at_scale_kernels(mp, peak)
+        except Exception as exc:  # evidence only: never fail the bench line
+            line["kernels_at_scale"] = {"error": f"{type(exc).__name__}: {exc}"}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+DMMA_PEAK_TFS = 37.1  # fp64 mma.sync m8n8k4, measured in-repo (profiles/r01_microbench_b200.txt)
+
+
+def at_scale_kernels(mp, peak_gbs):
+    """Per-kernel-family efficiency at the north-star target's per-GPU shape
+    (256^3 rows / 8 GPUs = a 256 x 256 x 32 grid, k = 64, m = 80): a capped
+    mixed-precision solve (8 iterations per stage) in profiling mode, algorithmic
+    bytes / flops per family over its event-timed launches.  Evidence for the
+    kernels' HBM / DMMA roofline at sizes where they are bandwidth- or
+    compute-bound (cfg1's are latency-bound); not part of the timed metric."""
+    import torch
+    A = mp.laplace3d(256, 256, 32)
+    cfg = mp.SolverConfig(k=64, block=80, tol=1e-10, maxit=8, variant="mplobpcg-schol")
+    mp.solve(A, cfg, want_X=False, history=False)  # warm-up (allocations, attributes)
+    torch.cuda.synchronize()
+    with mp.profile():
+        mp.solve(A, cfg, want_X=False, history=False)
+        torch.cuda.synchronize()
+        rep = mp.profile.report()
+    out = {"workload": "3-D 7-pt Laplacian 256x256x32 (n=2.1M, the per-GPU rows of 256^3 on 8 GPUs), "
+                       "k=64, m=80, mplobpcg-schol capped at 8+8 iterations, profiling pass",
+           "hbm_peak_gbs": peak_gbs, "dmma_peak_tfs": DMMA_PEAK_TFS, "kernels": {}}
+    for name, v in sorted(rep.items(), key=lambda kv: -kv[1]["ms"]):
+        if v["ms"] <= 0 or v["count"] == 0:
+            continue
+        gbs = v["bytes"] / (v["ms"] * 1e6) if v["bytes"] > 0 else None
+        tfs = v["flops"] / (v["ms"] * 1e9) if v["flops"] > 0 else None
+        out["kernels"][name] = {
+            "launches": v["count"], "ms_per_launch": round(v["ms"] / v["count"], 4),
+            "GBps": round(gbs, 1) if gbs else None,
+            "hbm_frac": round(gbs / peak_gbs, 3) if gbs else None,
+            "TFps": round(tfs, 2) if tfs else None,
+            "dmma_frac_if_fp64": round(tfs / DMMA_PEAK_TFS, 3) if tfs else None}
+    return out
 
 
 def main():
@@ -346,6 +387,8 @@ def main():
     ap.add_argument("--variant", default="mplobpcg-schol",
                     choices=["mplobpcg-schol", "dlobpcg-schol", "dlobpcg-dchol", "pinvit"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-at-scale", action="store_true",
+                    help="skip the per-kernel efficiency pass at the 256^3 / 8-GPU per-rank shape")
     ap.add_argument("--shard", action="store_true",
                     help="one row-sharded solve over the N GPUs (strong scaling; N = 1 runs "
                          "the sharded path over a 1-rank NCCL comm) "
