@@ -82,10 +82,22 @@ k_stencil7_vec(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int6
   const int64_t j = blockIdx.y;
   const int64_t p = pv * V;
   const T* x = X + j * ldx;
-  const int64_t xi = p % nx;
-  const int64_t yz = p / nx;
-  const int64_t yi = yz % ny;
-  const int64_t zi = yz / ny;
+  // grid coordinates: 32-bit division when the grid allows (a 64-bit
+  // div / mod pair per point was the kernel's integer-pipe bottleneck)
+  int64_t xi, yi, zi;
+  if (nx * ny * nz <= 0xffffffffLL) {
+    const uint32_t p32 = static_cast<uint32_t>(p), nx32 = static_cast<uint32_t>(nx),
+                   ny32 = static_cast<uint32_t>(ny);
+    const uint32_t yz32 = p32 / nx32;
+    xi = p32 - yz32 * nx32;
+    zi = yz32 / ny32;
+    yi = yz32 - static_cast<uint32_t>(zi) * ny32;
+  } else {
+    const int64_t yz = p / nx;
+    xi = p - yz * nx;
+    yi = yz % ny;
+    zi = yz / ny;
+  }
   const int64_t sy = nx, sz = nx * ny;
   auto ldv = [](const T* a) {
     const VT v = *reinterpret_cast<const VT*>(a);
