@@ -136,6 +136,68 @@ k_stencil7_vec(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int6
   *reinterpret_cast<VT*>(Y + j * ldy + p) = out;
 }
 
+// Large grids: each thread marches V points of one (x, y) row position through
+// ZC consecutive z-planes, so the z-1 / z+1 neighbours come from registers
+// (the previous centre / the prefetched next plane) instead of two more L2
+// reads per point; y +- 1 and x +- 1 hit L1 (the CTA covers whole rows).
+// Same per-point summation order as k_stencil7_vec: bitwise equal.
+template <typename T, int V, int ZC>
+__global__ void __launch_bounds__(256)
+k_stencil7_zm(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t ldx,
+              T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi) {
+  using VT = typename VecT<T, V>::type;
+  const int64_t sz = nx * ny;
+  const int64_t npv = sz / V;
+  const int64_t pv = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (pv >= npv) return;
+  const int64_t j = blockIdx.z;
+  const int64_t q = pv * V;  // position within the plane
+  const uint32_t q32 = static_cast<uint32_t>(q), nx32 = static_cast<uint32_t>(nx);
+  const int64_t yi = q32 / nx32, xi = q32 - static_cast<uint32_t>(yi) * nx32;
+  const int64_t sy = nx;
+  const T* x = X + j * ldx;
+  auto ldv = [](const T* a) { return *reinterpret_cast<const VT*>(a); };
+  const int64_t z0 = static_cast<int64_t>(blockIdx.y) * ZC;
+  const int64_t z1 = min(nz, z0 + ZC);
+  if (z0 >= nz) return;
+  VT zm{}, c = ldv(x + q + z0 * sz);
+  if (z0 > 0) zm = ldv(x + q + (z0 - 1) * sz);
+  else if (hlo) zm = ldv(hlo + q + j * sz);
+  for (int64_t zi = z0; zi < z1; ++zi) {
+    const int64_t p = q + zi * sz;
+    VT zp{}, ym{}, yp{};
+    if (zi + 1 < nz) zp = ldv(x + p + sz);
+    else if (hhi) zp = ldv(hhi + q + j * sz);
+    if (yi > 0) ym = ldv(x + p - sy);
+    if (yi + 1 < ny) yp = ldv(x + p + sy);
+    const T xl = xi > 0 ? x[p - 1] : T(0);
+    const T xr = xi + V < nx ? x[p + V] : T(0);
+    const bool hz_m = zi > 0 || hlo, hz_p = zi + 1 < nz || hhi;
+    const T* cv = reinterpret_cast<const T*>(&c);
+    const T* zmv = reinterpret_cast<const T*>(&zm);
+    const T* ymv = reinterpret_cast<const T*>(&ym);
+    const T* ypv = reinterpret_cast<const T*>(&yp);
+    const T* zpv = reinterpret_cast<const T*>(&zp);
+    VT out;
+    T* o = reinterpret_cast<T*>(&out);
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      T s = T(0);
+      if (hz_m) s = acc_neg(s, zmv[u]);
+      if (yi > 0) s = acc_neg(s, ymv[u]);
+      if (xi + u > 0) s = acc_neg(s, u == 0 ? xl : cv[u - 1]);
+      s = add_rn(s, mul_rn(T(6), cv[u]));
+      if (xi + u + 1 < nx) s = acc_neg(s, u + 1 == V ? xr : cv[u + 1]);
+      if (yi + 1 < ny) s = acc_neg(s, ypv[u]);
+      if (hz_p) s = acc_neg(s, zpv[u]);
+      o[u] = s;
+    }
+    *reinterpret_cast<VT*>(Y + j * ldy + p) = out;
+    zm = c;
+    c = zp;
+  }
+}
+
 // gen_laplace2d (generators.cpp:13-30): row p = i + nx*j, diag 4
 template <typename T>
 __global__ void __launch_bounds__(256)
@@ -185,6 +247,15 @@ void stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t c, const T* X, int64_t
                        reinterpret_cast<uintptr_t>(Y) % (V * sizeof(T)) == 0 &&
                        reinterpret_cast<uintptr_t>(hlo) % (V * sizeof(T)) == 0 &&
                        reinterpret_cast<uintptr_t>(hhi) % (V * sizeof(T)) == 0;
+  constexpr int ZC = 16;
+  if (aligned && n >= (int64_t(1) << 21) && nx * ny >= 256 * V && nx * ny <= 0xffffffffLL &&
+      (nx * ny) % V == 0) {
+    dim3 grid(static_cast<unsigned>(ceil_div(nx * ny / V, 256)),
+              static_cast<unsigned>(ceil_div(nz, int64_t(ZC))), static_cast<unsigned>(c));
+    k_stencil7_zm<T, V, ZC><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi);
+    MPB_LAUNCH_CHECK();
+    return;
+  }
   if (aligned) {
     dim3 grid(static_cast<unsigned>(ceil_div(n / V, 256)), static_cast<unsigned>(c));
     k_stencil7_vec<T, V><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi);

@@ -28,8 +28,9 @@ def rand(n, m, seed, dtype=np.float64):
     (Problem.lap3d(8, 7, 6), lambda mp: mp.laplace3d(8, 7, 6)),
     (Problem.lap3d(5), lambda mp: mp.laplace3d(5)),
     (Problem.lap2d(9, 8), lambda mp: mp.laplace2d(9, 8)),
-    # z-marching kernel (nx >= 32, nz >= 64), ragged x / y tiles and z chunks
     (Problem.lap3d(37, 9, 70), lambda mp: mp.laplace3d(37, 9, 70)),
+    # z-marching kernel (n >= 2^21): ragged last z-chunk, plane not a multiple of the CTA
+    (Problem.lap3d(64, 50, 700), lambda mp: mp.laplace3d(64, 50, 700)),
 ])
 def test_stencil_apply_bitwise(gpu, prob, mk):
     mp = gpu

@@ -99,10 +99,11 @@ def _run_ranks(nranks, dims, fn):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nranks,dims", [(2, (9, 8, 13)), (3, (9, 8, 13)), (2, (33, 5, 140))])
+@pytest.mark.parametrize("nranks,dims", [(2, (9, 8, 13)), (3, (9, 8, 13)), (2, (33, 5, 140)),
+                                          (2, (64, 64, 1100))])
 def test_sharded_stencil_apply_bitwise(gpu, nranks, dims):
-    """Halo exchange + slab apply == the global apply, bit for bit (both the
-    thread-per-point and the z-marching kernel)."""
+    """Halo exchange + slab apply == the global apply, bit for bit (the
+    vectorised per-point kernel and, on the large slabs, the z-marching one)."""
     n = int(np.prod(dims))
     X = np.asfortranarray(np.random.default_rng(3).standard_normal((n, 4)))
     Y = mp.to_host(gpu.laplace3d(*dims).apply(mp.to_device(X)))
