@@ -31,6 +31,8 @@ def rand(n, m, seed, dtype=np.float64):
     (Problem.lap3d(37, 9, 70), lambda mp: mp.laplace3d(37, 9, 70)),
     # z-marching kernel (n >= 2^21): ragged last z-chunk, plane not a multiple of the CTA
     (Problem.lap3d(64, 50, 700), lambda mp: mp.laplace3d(64, 50, 700)),
+    # y-marching 2-D kernel (n >= 2^20): row not a multiple of the CTA, ragged last chunk
+    (Problem.lap2d(1030, 1021), lambda mp: mp.laplace2d(1030, 1021)),
 ])
 def test_stencil_apply_bitwise(gpu, prob, mk):
     mp = gpu
