@@ -223,6 +223,20 @@ int mpeig_op_host_callback(mpeig_ctx* ctx, int64_t n, mpeig_host_apply_fn apply_
  * The solver fuses it with the residual and the conversions (one HBM pass). */
 int mpeig_precond_jacobi(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision,
                          mpeig_op** out);
+/* Dense Cholesky preconditioner f_T = L^-T L^-1 of an explicit dense operator
+ * (Preconditioner<T>::build(DenseMatrix, prec), precond.hpp:33-50; the
+ * reference's own preconditioner for dense systems):
+ *   WORKING: L = chol(A) in fp64; apply(R) = L^-T L^-1 R        (precond.hpp:98)
+ *   LOWER:   L = chol(to_lower(A)) in fp32, on NotPositiveDefinite / Overflow
+ *            one retry with A + 10 u_l ||A||_est I (retry_dense, :140-146);
+ *            apply(R) = to_working(L^-T L^-1 to_lower(R))        (:99)
+ *            apply_lower(R) = L^-T L^-1 R                        (:103-109)
+ * A must come from mpeig_op_dense. Errors: MPEIG_E_NOT_PD (index = pivot),
+ * MPEIG_E_OVERFLOW, MPEIG_E_SINGULAR_TRI on apply (check_tri_diag). */
+int mpeig_precond_dense_chol(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision,
+                             mpeig_op** out);
+/* Preconditioner::shift_applied() (precond.hpp:114): the retry shift, else 0 */
+double mpeig_precond_shift(const mpeig_op* op);
 void mpeig_op_destroy(mpeig_op* op);
 int64_t mpeig_op_n(const mpeig_op* op);
 /* Y = op(X) in working (fp64) or lower (fp32) precision, device arrays */

@@ -154,7 +154,11 @@ class Oracle:
     # ------------------------------------------------------------------ solve
     def solve(self, prob: Problem, variant: str, k: int, block: int = 0, maxit: int = 2000,
               tol: float = 1e-12, lower_tol: float = 5e-6, seed: int = 0,
-              sketch_rows: int = 8, want_X: bool = False, hist_cap: int | None = None):
+              sketch_rows: int = 8, want_X: bool = False, hist_cap: int | None = None,
+              native: bool = False):
+        """native=True (reference library only, dense problems): the reference's
+        stock solve(DenseMatrix, cfg) with its own Cholesky preconditioner
+        (drivers.hpp:158-181) instead of the Jacobi-callback harness."""
         m = block if block else (3 * k + 1) // 2
         cfg = MpCfg(k, block, maxit, tol, lower_tol, seed, sketch_rows)
         hc = hist_cap if hist_cap is not None else 2 * maxit + 4
@@ -175,7 +179,7 @@ class Oracle:
         r.hist_dropped, r.hist_fallback = _ptr(hd, C.c_int64), _ptr(hf, C.c_int32)
         r.hist_ritz, r.hist_resid = _ptr(hr, C.c_double), _ptr(hq, C.c_double)
         pc = prob.to_c()
-        f = self.fn("solve")
+        f = self.fn("solve_native" if native else "solve")
         f.argtypes = [C.POINTER(MpProblem), C.c_int, C.POINTER(MpCfg), C.POINTER(MpResult)]
         f(C.byref(pc), VARIANTS[variant], C.byref(cfg), C.byref(r))
         L = min(r.hist_len, hc)

@@ -331,6 +331,35 @@ int mpref_solve(const mp_problem* prob, int variant, const mp_cfg* c, mp_result*
   return out->status;
 }
 
+// The reference's stock driver on a dense system: solve(DenseMatrix, cfg)
+// (drivers.hpp:158-181) with its own Cholesky preconditioner
+// (Preconditioner<T>::build, precond.hpp:33-50) -- the golden source for the
+// device dense-Cholesky f_T.  Same outputs as mpref_solve.
+int mpref_solve_native(const mp_problem* prob, int variant, const mp_cfg* c, mp_result* out) {
+  out->status = guarded([&] {
+    const SolverConfig cfg = to_cfg(c, variant);
+    auto sys = make_system(prob, false);
+    if (!sys->dense) throw ConfigError("solve_native: dense problems only");
+    const std::size_t m = cfg.block_size();
+    const auto t0 = clk::now();
+    EigResult<double> r = solve(sys->D, cfg);
+    out->t_total = secs(t0);
+    out->t_setup = r.timings.factorize;
+    out->t_stage1 = r.precond_shift;  // (field reused: the retry shift)
+    out->converged = r.converged ? 1 : 0;
+    out->iters_lower = static_cast<int64_t>(r.iterations_lower);
+    out->iters_working = static_cast<int64_t>(r.iterations_working);
+    out->a_norm_est = r.a_norm_estimate;
+    for (std::size_t j = 0; j < cfg.k && j < r.theta.size(); ++j) {
+      out->theta[j] = r.theta[j];
+      out->resid[j] = r.residual_norms[j];
+    }
+    unwrap(r.X, out->X);
+    export_history(r.history, m, out);
+  }, out->msg);
+  return out->status;
+}
+
 void mpref_pcg64_u64(uint64_t seed, int64_t count, uint64_t* o) {
   Pcg64 g(seed);
   for (int64_t i = 0; i < count; ++i) o[i] = g.next_u64();

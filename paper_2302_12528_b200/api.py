@@ -15,6 +15,10 @@ this module                    reference
 ``pinvit``                     ``pinvit<T>``         eigensolvers.hpp:326-390
 ``mixed_lobpcg``               ``mixed_lobpcg``      drivers.hpp:122-152
 ``solve``                      ``solve``             drivers.hpp:158-210
+``jacobi``                     diagonal f_T (the north star's preconditioner)
+``dense_cholesky``             ``Preconditioner<T>::build(DenseMatrix, prec)``
+                               precond.hpp:33-50 (pass as ``T=`` for the
+                               reference's stock dense ``solve``)
 ``spectral_norm_estimate``     norm_estimate.hpp:15-24
 ``converged_count``            eigensolvers.hpp:25-43
 exceptions                     errors.hpp:10-62
@@ -424,6 +428,17 @@ def jacobi(A: Operator, precision: int = LOWER) -> Operator:
     return Operator(A.ctx, h, A.n, "jacobi")
 
 
+def dense_cholesky(A: Operator, precision: int = LOWER) -> Operator:
+    """Dense Cholesky f_T = L^-T L^-1 (Preconditioner<T>::build(DenseMatrix, prec),
+    precond.hpp:33-50): fp64 factor at WORKING, fp32 factor of to_lower(A) at
+    LOWER with retry_dense's one shifted retry (:140-146).  `A` must be a
+    dense_matrix() operator.  `.shift` mirrors Preconditioner::shift_applied()."""
+    h = _mk(A.ctx, A.ctx.lib.mpeig_precond_dense_chol, A.h, precision)
+    op = Operator(A.ctx, h, A.n, "dense_chol", keep=(A,))
+    op.shift = float(A.ctx.lib.mpeig_precond_shift(h))
+    return op
+
+
 def build_precision_for(variant: str) -> int:
     """drivers.hpp:113-116."""
     return WORKING if variant == "dlobpcg-dchol" else LOWER
@@ -558,11 +573,12 @@ def run_variant(A: Operator, X0, cfg: SolverConfig, a_norm_est: float, T: Operat
                      bool(res.converged), _timings(res.timings), res.a_norm_estimate)
 
 
-def mixed_lobpcg(A: Operator, X0, cfg: SolverConfig) -> EigResult:
-    """mixed_lobpcg (drivers.hpp:122-152): forces MPLOBPCG_schol, fp32 Jacobi."""
+def mixed_lobpcg(A: Operator, X0, cfg: SolverConfig, T: Operator = None) -> EigResult:
+    """mixed_lobpcg (drivers.hpp:122-152): forces MPLOBPCG_schol; f_T built at LOWER
+    precision (fp32 Jacobi unless T is given, e.g. dense_cholesky(A, LOWER))."""
     cfg = SolverConfig(**{**cfg.__dict__, "variant": "mplobpcg-schol"})
     est = spectral_norm_estimate(A, cfg.sketch_rows, cfg.seed ^ 0x9E3779B97F4A7C15)
-    return run_variant(A, X0, cfg, est, jacobi(A, LOWER))
+    return run_variant(A, X0, cfg, est, T if T is not None else jacobi(A, LOWER))
 
 
 def lobpcg_stage(A: Operator, n: int, X0, cfg: SolverConfig, T: Operator, a_norm_est: float,

@@ -382,6 +382,25 @@ int mpeig_precond_jacobi(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision, m
   });
 }
 
+int mpeig_precond_dense_chol(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision, mpeig_op** out) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    if (!A) throw Error(MPEIG_E_CONFIG, "dense_chol: null operator");
+    if (precision != MPEIG_WORKING && precision != MPEIG_LOWER)
+      throw Error(MPEIG_E_CONFIG, "dense_chol: unknown precision");
+    mpeig_op* op = new_op(ctx, kOpDenseChol, A->n);
+    try {
+      dense_chol_build(ctx, A, precision, op);
+    } catch (...) {
+      mpeig_op_destroy(op);
+      throw;
+    }
+    *out = op;
+  });
+}
+
+double mpeig_precond_shift(const mpeig_op* op) { return op ? op->shift : 0.0; }
+
 void mpeig_op_destroy(mpeig_op* op) {
   if (!op) return;
   if (op->ctx && op->ctx->stream) cudaStreamSynchronize(op->ctx->stream);
@@ -393,6 +412,9 @@ void mpeig_op_destroy(mpeig_op* op) {
   cudaFree(op->Al);
   cudaFree(op->dinv);
   cudaFree(op->dinvf);
+  cudaFree(op->Lw);
+  cudaFree(op->Ll);
+  cudaFree(op->scratch);
   if (op->halo) cudaFree(op->halo);
   delete op;
 }

@@ -37,7 +37,7 @@ struct mpeig_ctx {
   mpb::Comm* comm = nullptr;    // row-sharded mode (owned), nullptr: single GPU
 };
 
-enum OpKind { kOpLap3d, kOpLap2d, kOpCsr, kOpDense, kOpDeviceCb, kOpHostCb, kOpJacobi };
+enum OpKind { kOpLap3d, kOpLap2d, kOpCsr, kOpDense, kOpDeviceCb, kOpHostCb, kOpJacobi, kOpDenseChol };
 
 struct mpeig_op {
   OpKind kind;
@@ -67,6 +67,14 @@ struct mpeig_op {
   double* dinv = nullptr;   // 1 / diag, fp64
   float* dinvf = nullptr;   // to_lower(1 / diag)
   bool lower_overflow = false;  // to_lower of the coefficients overflowed
+  // dense Cholesky f_T (Preconditioner::Kind::DenseChol, precond.hpp:33-50):
+  // lower factor L (n x n, ld n) in the build precision
+  double* Lw = nullptr;
+  float* Ll = nullptr;
+  double shift = 0.0;          // retry_dense's diagonal shift (precond.hpp:140-146)
+  int64_t tri_singular = -1;   // first zero / subnormal diag(L) (check_tri_diag)
+  mutable float* scratch = nullptr;  // to_lower(R) of a working-precision apply
+  mutable size_t scratch_elems = 0;
 };
 
 namespace mpb {

@@ -852,6 +852,18 @@ void convert_f64_to_f32(int64_t n, int64_t c, const double* src, int64_t lds, fl
   MPB_LAUNCH_CHECK();
 }
 
+__global__ void k_add_diag(int64_t n, double* __restrict__ A, int64_t lda, double shift) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) A[i + i * lda] = __dadd_rn(A[i + i * lda], shift);
+}
+
+// A(i, i) += shift (retry_dense, precond.hpp:140-146)
+void add_diag_f64(int64_t n, double* A, int64_t lda, double shift, cudaStream_t s) {
+  if (n <= 0) return;
+  k_add_diag<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(n, A, lda, shift);
+  MPB_LAUNCH_CHECK();
+}
+
 void convert_f32_to_f64(int64_t n, int64_t c, const float* src, int64_t lds, double* dst,
                         int64_t ldd, cudaStream_t s) {
   if (n * c <= 0) return;

@@ -57,6 +57,153 @@ static void cublas_check(cublasStatus_t st, const char* what) {
 }
 
 // --------------------------------------------------------------- operators
+// ------------------------------------------- dense Cholesky f_T
+// Preconditioner<T>::Kind::DenseChol (precond.hpp:33-50, 92-109, 121-126):
+// T(R) = L^-T L^-1 R with L the lower Cholesky factor of A (or of to_lower(A)).
+// The factor is built once per solve (cuSOLVER potrf); each apply is the two
+// triangular solves (cuBLAS trsm, no TF32) with the lower()/working()
+// conversions of a lower-precision factor fused into the copy in / out.
+
+// dense_cholesky (dense_kernels.hpp:128-152) on L in place: failure index and
+// the reference's error types (non-finite pivot -> OverflowError, nonpositive
+// -> NotPositiveDefinite(j)); check_tri_diag (:163-170) recorded for the applies
+template <typename F>
+static void chol_factor(mpeig_ctx* ctx, F* L, int64_t n, mpeig_op* op) {
+  cudaStream_t s = ctx->stream;
+  const int ni = static_cast<int>(n);
+  int lwork = 0;
+  if constexpr (sizeof(F) == 8)
+    cusolver_check(cusolverDnDpotrf_bufferSize(ctx->cusolver, CUBLAS_FILL_MODE_LOWER, ni, L, ni, &lwork),
+                   "cusolverDnDpotrf_bufferSize");
+  else
+    cusolver_check(cusolverDnSpotrf_bufferSize(ctx->cusolver, CUBLAS_FILL_MODE_LOWER, ni, L, ni, &lwork),
+                   "cusolverDnSpotrf_bufferSize");
+  DevBuf<F> work(static_cast<size_t>(std::max(lwork, 1)), s);
+  DevBuf<int> info(1, s);
+  if constexpr (sizeof(F) == 8)
+    cusolver_check(cusolverDnDpotrf(ctx->cusolver, CUBLAS_FILL_MODE_LOWER, ni, L, ni, work.p, lwork, info.p),
+                   "cusolverDnDpotrf");
+  else
+    cusolver_check(cusolverDnSpotrf(ctx->cusolver, CUBLAS_FILL_MODE_LOWER, ni, L, ni, work.p, lwork, info.p),
+                   "cusolverDnSpotrf");
+  int h_info = 0;
+  std::vector<F> d(static_cast<size_t>(n));
+  MPB_CUDA(cudaMemcpyAsync(&h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  MPB_CUDA(cudaMemcpy2DAsync(d.data(), sizeof(F), L, sizeof(F) * (n + 1), sizeof(F), n,
+                             cudaMemcpyDeviceToHost, s));
+  MPB_CUDA(cudaStreamSynchronize(s));
+  const int64_t fail = h_info > 0 ? h_info - 1 : n;
+  for (int64_t j = 0; j < fail; ++j)
+    if (!std::isfinite(static_cast<double>(d[j])))
+      throw Error(MPEIG_E_OVERFLOW, "dense_cholesky: pivot " + std::to_string(j) + " is not finite", j);
+  if (h_info > 0)
+    throw Error(MPEIG_E_NOT_PD, "dense_cholesky: nonpositive pivot at " + std::to_string(fail), fail);
+  op->tri_singular = -1;
+  for (int64_t j = 0; j < n; ++j) {
+    const F a = std::abs(d[j]);
+    if (a == 0 || a < std::numeric_limits<F>::min()) {
+      op->tri_singular = j;
+      break;
+    }
+  }
+}
+
+void dense_chol_build(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision, mpeig_op* op) {
+  if (!A || A->kind != kOpDense)
+    throw Error(MPEIG_E_CONFIG, "dense_chol: operator is not an explicit dense matrix");
+  const int64_t n = A->n;
+  cudaStream_t s = ctx->stream;
+  op->precision = precision;
+  if (precision == MPEIG_WORKING) {  // precond.hpp:38-41: no retry in working precision
+    MPB_CUDA(cudaMalloc(reinterpret_cast<void**>(&op->Lw), sizeof(double) * n * n));
+    copy_block<double>(n, n, A->A, A->lda, op->Lw, n, s);
+    chol_factor<double>(ctx, op->Lw, n, op);
+    return;
+  }
+  MPB_CUDA(cudaMalloc(reinterpret_cast<void**>(&op->Ll), sizeof(float) * n * n));
+  auto attempt = [&](double shift) {
+    if (shift == 0.0) {  // dense_cholesky(to_lower(A))
+      if (A->lower_overflow) throw Error(MPEIG_E_OVERFLOW, "to_lower: matrix exceeds binary32 range");
+      copy_block<float>(n, n, A->Al, A->lda, op->Ll, n, s);
+    } else {  // retry_dense: to_lower(A + shift I), the shift added in fp64
+      DevBuf<double> As(static_cast<size_t>(n * n), s);
+      copy_block<double>(n, n, A->A, A->lda, As.p, n, s);
+      add_diag_f64(n, As.p, n, shift, s);
+      status_clear(ctx);
+      convert_f64_to_f32(n, n, As.p, n, op->Ll, n, ctx->d_status + 2, s);
+      status_fetch(ctx);
+      if (ctx->h_status[2]) throw Error(MPEIG_E_OVERFLOW, "to_lower: matrix exceeds binary32 range");
+    }
+    chol_factor<float>(ctx, op->Ll, n, op);
+  };
+  try {
+    attempt(0.0);
+  } catch (const Error& e) {  // precond.hpp:42-48: one retry on NotPositiveDefinite / OverflowError
+    if (e.code != MPEIG_E_NOT_PD && e.code != MPEIG_E_OVERFLOW) throw;
+    // retry_shift (precond.hpp:128-132): 10 u_l ||A||_est, sketch seed kShiftSeed (:161)
+    op->shift = 10.0 * 0x1p-24 * spectral_norm_estimate(ctx, A, 8, 0x5eed0123ULL);
+    attempt(op->shift);
+  }
+}
+
+// two triangular solves in place on B (n x c): L Y = B, then L^T X = Y
+// (dense_solve, precond.hpp:115-120; tri_solve Forward / BackwardAdjoint)
+template <typename F>
+static void chol_solve(mpeig_ctx* ctx, const F* L, int64_t n, int64_t c, F* B, int64_t ldb) {
+  const int ni = static_cast<int>(n), ci = static_cast<int>(c), lb = static_cast<int>(ldb);
+  const F one = 1;
+  for (cublasOperation_t t : {CUBLAS_OP_N, CUBLAS_OP_T}) {
+    if constexpr (sizeof(F) == 8)
+      cublas_check(cublasDtrsm(ctx->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, t,
+                               CUBLAS_DIAG_NON_UNIT, ni, ci, &one, L, ni, B, lb),
+                   "cublasDtrsm");
+    else
+      cublas_check(cublasStrsm(ctx->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, t,
+                               CUBLAS_DIAG_NON_UNIT, ni, ci, &one, L, ni, B, lb),
+                   "cublasStrsm");
+  }
+}
+
+// Preconditioner::apply (T = double) / apply_lower (T = float), precond.hpp:92-109
+template <typename T>
+static void dense_chol_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* R,
+                             int64_t ldr, T* W, int64_t ldw) {
+  const int64_t n = op->n;
+  cudaStream_t s = ctx->stream;
+  if (op->tri_singular >= 0)
+    throw Error(MPEIG_E_SINGULAR_TRI, "tri_solve: zero or subnormal diagonal", op->tri_singular);
+  if (op->precision == MPEIG_WORKING) {
+    if constexpr (sizeof(T) == 4) {
+      throw Error(MPEIG_E_CONFIG, "precond apply_lower: factor was built at working precision");
+    } else {
+      copy_block<double>(n, ncols, R, ldr, W, ldw, s);
+      chol_solve<double>(ctx, op->Lw, n, ncols, W, ldw);
+    }
+    return;
+  }
+  if constexpr (sizeof(T) == 4) {
+    copy_block<float>(n, ncols, R, ldr, W, ldw, s);
+    chol_solve<float>(ctx, op->Ll, n, ncols, W, ldw);
+  } else {  // to_working(dense_solve(L, to_lower(R)))
+    const size_t need = static_cast<size_t>(n * ncols);
+    if (op->scratch_elems < need) {
+      if (op->scratch) {
+        MPB_CUDA(cudaStreamSynchronize(s));
+        MPB_CUDA(cudaFree(op->scratch));
+        op->scratch = nullptr;
+      }
+      MPB_CUDA(cudaMalloc(reinterpret_cast<void**>(&op->scratch), sizeof(float) * need));
+      op->scratch_elems = need;
+    }
+    status_clear(ctx);
+    convert_f64_to_f32(n, ncols, R, ldr, op->scratch, n, ctx->d_status + 2, s);
+    status_fetch(ctx);
+    if (ctx->h_status[2]) throw Error(MPEIG_E_OVERFLOW, "to_lower: value exceeds binary32 range");
+    chol_solve<float>(ctx, op->Ll, n, ncols, op->scratch, n);
+    convert_f32_to_f64(n, ncols, op->scratch, n, W, ldw, s);
+  }
+}
+
 template <typename T>
 void op_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* X, int64_t ldx, T* Y,
               int64_t ldy) {
@@ -146,6 +293,9 @@ void op_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* X, int
     }
     case kOpJacobi:
       precond_apply<T>(ctx, op, ncols, X, ldx, Y, ldy);
+      return;
+    case kOpDenseChol:
+      dense_chol_apply<T>(ctx, op, ncols, X, ldx, Y, ldy);
       return;
   }
 }

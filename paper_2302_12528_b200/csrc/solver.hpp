@@ -87,6 +87,8 @@ void solve(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T_op, const mpeig_
 void solve_prepared(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T_op, const mpeig_cfg& cfg,
                     const double* X0raw, int64_t ldx0, const double* omega, int64_t ldo,
                     double omega_fro, mpeig_history_sink sink, void* sink_user, mpeig_result* out);
+// Preconditioner<T>::build(DenseMatrix, prec) (precond.hpp:33-50): fills op (kOpDenseChol)
+void dense_chol_build(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision, mpeig_op* op);
 void validate_cfg(const mpeig_cfg& cfg, int64_t n);
 
 }  // namespace mpb

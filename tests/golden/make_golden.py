@@ -46,6 +46,15 @@ CASES = {
     "dense256-dlobpcg-dchol": (lambda: Problem.dense_matrix(spd_dense(256, 1e3, 5)[0]), "dlobpcg-dchol", dict(k=8, tol=1e-10, maxit=2000, seed=3)),
     "dense256-mplobpcg-schol": (lambda: Problem.dense_matrix(spd_dense(256, 1e3, 5)[0]), "mplobpcg-schol", dict(k=8, tol=1e-10, maxit=2000, seed=3)),
     "lap2d32-pinvit": (lambda: Problem.lap2d(32), "pinvit", dict(k=4, block=6, tol=1e-8, maxit=400)),
+    # the reference's own dense Cholesky preconditioner (stock solve(DenseMatrix),
+    # drivers.hpp:158-181): fp64 factor (dchol), fp32 factor (schol,
+    # mixed, PINVIT), and an ill-conditioned case whose fp32 factor needs
+    # retry_dense's shift (precond.hpp:140-146)
+    "dense256chol-dlobpcg-dchol": (lambda: Problem.dense_matrix(spd_dense(256, 1e3, 5)[0]), "dlobpcg-dchol", dict(k=8, tol=1e-10, maxit=500, seed=3, native=True)),
+    "dense256chol-dlobpcg-schol": (lambda: Problem.dense_matrix(spd_dense(256, 1e3, 5)[0]), "dlobpcg-schol", dict(k=8, tol=1e-10, maxit=500, seed=3, native=True)),
+    "dense256chol-mplobpcg-schol": (lambda: Problem.dense_matrix(spd_dense(256, 1e3, 5)[0]), "mplobpcg-schol", dict(k=8, tol=1e-10, maxit=500, seed=3, native=True)),
+    "dense256chol-pinvit": (lambda: Problem.dense_matrix(spd_dense(256, 1e3, 5)[0]), "pinvit", dict(k=8, tol=1e-10, maxit=500, seed=3, native=True)),
+    "dense256chol-k1e10-dlobpcg-schol": (lambda: Problem.dense_matrix(spd_dense(256, 1e10, 5)[0]), "dlobpcg-schol", dict(k=8, tol=1e-10, maxit=12, seed=3, native=True)),
     # cfg 1 (BASELINE.json configs[0]) -- minutes each on one core
     "cfg1-dlobpcg-dchol": (lambda: Problem.lap3d(32), "dlobpcg-dchol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
     "cfg1-dlobpcg-schol": (lambda: Problem.lap3d(32), "dlobpcg-schol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
@@ -64,7 +73,8 @@ def run(name: str) -> None:
         iters_lower=r.iters_lower, iters_working=r.iters_working, a_norm_est=r.a_norm_est,
         theta=r.theta, resid=r.resid, hist_stage=r.hist_stage, hist_nc=r.hist_nc,
         hist_dropped=r.hist_dropped, hist_fallback=r.hist_fallback,
-        hist_ritz=r.hist_ritz, hist_resid=r.hist_resid, t_total=r.t_total)
+        hist_ritz=r.hist_ritz, hist_resid=r.hist_resid, t_total=r.t_total,
+        precond_shift=r.extra["t_stage1"] if kw.get("native") else 0.0)
     print(f"{name}: status={r.status} conv={r.converged} iters={r.iters_lower}+{r.iters_working} "
           f"theta0={r.theta[0]!r} t={r.t_total:.2f}s", flush=True)
 
