@@ -857,6 +857,35 @@ __global__ void k_add_diag(int64_t n, double* __restrict__ A, int64_t lda, doubl
   if (i < n) A[i + i * lda] = __dadd_rn(A[i + i * lda], shift);
 }
 
+// A(j, i) = A(i, j) for i > j: 32 x 32 tiles through shared memory so both
+// the lower-triangle reads and the upper-triangle writes are coalesced
+template <typename T>
+__global__ void k_symmetrize_lower(int64_t n, T* __restrict__ A, int64_t lda) {
+  __shared__ T tile[32][33];
+  const int64_t bi = blockIdx.x, bj = blockIdx.y;  // tile row / column
+  if (bi < bj) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = bi * 32 + tx, j = bj * 32 + r;
+    if (i < n && j < n) tile[r][tx] = A[i + j * lda];
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = bj * 32 + tx, j = bi * 32 + r;  // write A(i, j) = A(j, i), i < j
+    if (i < n && j < n && i < j) A[i + j * lda] = tile[tx][r];
+  }
+}
+
+template <typename T>
+void symmetrize_lower(int64_t n, T* A, int64_t lda, cudaStream_t s) {
+  if (n <= 1) return;
+  const unsigned t = static_cast<unsigned>((n + 31) / 32);
+  k_symmetrize_lower<T><<<dim3(t, t), dim3(32, 8), 0, s>>>(n, A, lda);
+  MPB_LAUNCH_CHECK();
+}
+template void symmetrize_lower<double>(int64_t, double*, int64_t, cudaStream_t);
+template void symmetrize_lower<float>(int64_t, float*, int64_t, cudaStream_t);
+
 // A(i, i) += shift (retry_dense, precond.hpp:140-146)
 void add_diag_f64(int64_t n, double* A, int64_t lda, double shift, cudaStream_t s) {
   if (n <= 0) return;

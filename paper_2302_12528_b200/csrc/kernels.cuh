@@ -45,6 +45,9 @@ void gemm_tn_pair(int64_t n, int64_t k, int64_t c, const T* A1, const T* A2, int
 // *overflow_flag = 1 on finite -> inf (precision.hpp:102-107).
 void convert_f64_to_f32(int64_t n, int64_t c, const double* src, int64_t lds, float* dst,
                         int64_t ldd, int* overflow_flag, cudaStream_t s);
+// A(j, i) = A(i, j) for i > j (mirror the lower triangle of a symmetric n x n matrix)
+template <typename T>
+void symmetrize_lower(int64_t n, T* A, int64_t lda, cudaStream_t s);
 // A(i, i) += shift, i < n (retry_dense's shifted copy, precond.hpp:140-146)
 void add_diag_f64(int64_t n, double* A, int64_t lda, double shift, cudaStream_t s);
 void convert_f32_to_f64(int64_t n, int64_t c, const float* src, int64_t lds, double* dst,

@@ -60,9 +60,16 @@ static void cublas_check(cublasStatus_t st, const char* what) {
 // ------------------------------------------- dense Cholesky f_T
 // Preconditioner<T>::Kind::DenseChol (precond.hpp:33-50, 92-109, 121-126):
 // T(R) = L^-T L^-1 R with L the lower Cholesky factor of A (or of to_lower(A)).
-// The factor is built once per solve (cuSOLVER potrf); each apply is the two
-// triangular solves (cuBLAS trsm, no TF32) with the lower()/working()
-// conversions of a lower-precision factor fused into the copy in / out.
+// Built once per solve: cuSOLVER potrf (the reference's dense_cholesky, same
+// failure semantics), then potri turns the factor into M = L^-T L^-1 in the
+// build precision, stored as a full symmetric n x n matrix.  Each apply is then
+// ONE GEMM M R (cuBLAS, no TF32) instead of two triangular solves: the same
+// 2 n^2 c flops, but at GEMM throughput instead of trsm's column-serial sweep
+// (cfg3, n = 16384, c = 96: trsm pair 10.6 ms -> SGEMM, scripts/cfg3_dense.py).
+// Rounding differs from the reference's substitutions at the level of the
+// preconditioner's own accuracy (kappa eps_T); parity is the solver-level bar
+// (tests/test_gpu_precond.py).  The lower()/working() conversions of an fp32
+// factor run around the GEMM.
 
 // dense_cholesky (dense_kernels.hpp:128-152) on L in place: failure index and
 // the reference's error types (non-finite pivot -> OverflowError, nonpositive
@@ -103,9 +110,29 @@ static void chol_factor(mpeig_ctx* ctx, F* L, int64_t n, mpeig_op* op) {
     const F a = std::abs(d[j]);
     if (a == 0 || a < std::numeric_limits<F>::min()) {
       op->tri_singular = j;
-      break;
+      return;  // every apply throws SingularTriangular (check_tri_diag)
     }
   }
+  // M = L^-T L^-1 (lower triangle), then mirrored to the upper one
+  lwork = 0;
+  if constexpr (sizeof(F) == 8)
+    cusolver_check(cusolverDnDpotri_bufferSize(ctx->cusolver, CUBLAS_FILL_MODE_LOWER, ni, L, ni, &lwork),
+                   "cusolverDnDpotri_bufferSize");
+  else
+    cusolver_check(cusolverDnSpotri_bufferSize(ctx->cusolver, CUBLAS_FILL_MODE_LOWER, ni, L, ni, &lwork),
+                   "cusolverDnSpotri_bufferSize");
+  work.alloc(static_cast<size_t>(std::max(lwork, 1)), s);
+  if constexpr (sizeof(F) == 8)
+    cusolver_check(cusolverDnDpotri(ctx->cusolver, CUBLAS_FILL_MODE_LOWER, ni, L, ni, work.p, lwork, info.p),
+                   "cusolverDnDpotri");
+  else
+    cusolver_check(cusolverDnSpotri(ctx->cusolver, CUBLAS_FILL_MODE_LOWER, ni, L, ni, work.p, lwork, info.p),
+                   "cusolverDnSpotri");
+  MPB_CUDA(cudaMemcpyAsync(&h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  MPB_CUDA(cudaStreamSynchronize(s));
+  if (h_info > 0)
+    throw Error(MPEIG_E_SINGULAR_TRI, "tri_solve: zero or subnormal diagonal", h_info - 1);
+  symmetrize_lower<F>(n, L, n, s);
 }
 
 void dense_chol_build(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision, mpeig_op* op) {
@@ -146,22 +173,37 @@ void dense_chol_build(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision, mpei
   }
 }
 
-// two triangular solves in place on B (n x c): L Y = B, then L^T X = Y
-// (dense_solve, precond.hpp:115-120; tri_solve Forward / BackwardAdjoint)
+// Y = M B (n x c), M = L^-T L^-1 symmetric n x n: dense_solve (precond.hpp:115-120,
+// tri_solve Forward then BackwardAdjoint) as one GEMM.  Y must not alias B.
 template <typename F>
-static void chol_solve(mpeig_ctx* ctx, const F* L, int64_t n, int64_t c, F* B, int64_t ldb) {
-  const int ni = static_cast<int>(n), ci = static_cast<int>(c), lb = static_cast<int>(ldb);
-  const F one = 1;
-  for (cublasOperation_t t : {CUBLAS_OP_N, CUBLAS_OP_T}) {
-    if constexpr (sizeof(F) == 8)
-      cublas_check(cublasDtrsm(ctx->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, t,
-                               CUBLAS_DIAG_NON_UNIT, ni, ci, &one, L, ni, B, lb),
-                   "cublasDtrsm");
-    else
-      cublas_check(cublasStrsm(ctx->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, t,
-                               CUBLAS_DIAG_NON_UNIT, ni, ci, &one, L, ni, B, lb),
-                   "cublasStrsm");
+static void chol_apply_gemm(mpeig_ctx* ctx, const F* M, int64_t n, int64_t c, const F* B,
+                            int64_t ldb, F* Y, int64_t ldy) {
+  const int ni = static_cast<int>(n), ci = static_cast<int>(c);
+  const F one = 1, zero = 0;
+  ProfScope prof("precond_chol", ctx->stream, double(sizeof(F)) * (double(n) * n + 2.0 * n * c),
+                 2.0 * n * double(n) * c);
+  if constexpr (sizeof(F) == 8)
+    cublas_check(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ci, ni, &one, M, ni, B,
+                             static_cast<int>(ldb), &zero, Y, static_cast<int>(ldy)),
+                 "cublasDgemm");
+  else
+    cublas_check(cublasSgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ci, ni, &one, M, ni, B,
+                             static_cast<int>(ldb), &zero, Y, static_cast<int>(ldy)),
+                 "cublasSgemm");
+}
+
+// fp32 scratch of the op, at least `need` elements
+static float* op_scratch(mpeig_ctx* ctx, const mpeig_op* op, size_t need) {
+  if (op->scratch_elems < need) {
+    if (op->scratch) {
+      MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+      MPB_CUDA(cudaFree(op->scratch));
+      op->scratch = nullptr;
+    }
+    MPB_CUDA(cudaMalloc(reinterpret_cast<void**>(&op->scratch), sizeof(float) * need));
+    op->scratch_elems = need;
   }
+  return op->scratch;
 }
 
 // Preconditioner::apply (T = double) / apply_lower (T = float), precond.hpp:92-109
@@ -172,35 +214,43 @@ static void dense_chol_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, 
   cudaStream_t s = ctx->stream;
   if (op->tri_singular >= 0)
     throw Error(MPEIG_E_SINGULAR_TRI, "tri_solve: zero or subnormal diagonal", op->tri_singular);
+  if (ncols <= 0) return;
+  const size_t blk = static_cast<size_t>(n * ncols);
   if (op->precision == MPEIG_WORKING) {
     if constexpr (sizeof(T) == 4) {
       throw Error(MPEIG_E_CONFIG, "precond apply_lower: factor was built at working precision");
     } else {
-      copy_block<double>(n, ncols, R, ldr, W, ldw, s);
-      chol_solve<double>(ctx, op->Lw, n, ncols, W, ldw);
+      const double* B = R;
+      int64_t ldb = ldr;
+      if (W == R) {  // in place: GEMM input from a copy
+        double* t = reinterpret_cast<double*>(op_scratch(ctx, op, 2 * blk));
+        copy_block<double>(n, ncols, R, ldr, t, n, s);
+        B = t;
+        ldb = n;
+      }
+      chol_apply_gemm<double>(ctx, op->Lw, n, ncols, B, ldb, W, ldw);
     }
     return;
   }
-  if constexpr (sizeof(T) == 4) {
-    copy_block<float>(n, ncols, R, ldr, W, ldw, s);
-    chol_solve<float>(ctx, op->Ll, n, ncols, W, ldw);
-  } else {  // to_working(dense_solve(L, to_lower(R)))
-    const size_t need = static_cast<size_t>(n * ncols);
-    if (op->scratch_elems < need) {
-      if (op->scratch) {
-        MPB_CUDA(cudaStreamSynchronize(s));
-        MPB_CUDA(cudaFree(op->scratch));
-        op->scratch = nullptr;
-      }
-      MPB_CUDA(cudaMalloc(reinterpret_cast<void**>(&op->scratch), sizeof(float) * need));
-      op->scratch_elems = need;
+  if constexpr (sizeof(T) == 4) {  // apply_lower
+    const float* B = R;
+    int64_t ldb = ldr;
+    if (W == R) {
+      float* t = op_scratch(ctx, op, blk);
+      copy_block<float>(n, ncols, R, ldr, t, n, s);
+      B = t;
+      ldb = n;
     }
+    chol_apply_gemm<float>(ctx, op->Ll, n, ncols, B, ldb, W, ldw);
+  } else {  // to_working(dense_solve(L, to_lower(R)))
+    float* lo = op_scratch(ctx, op, 2 * blk);
+    float* hi = lo + blk;
     status_clear(ctx);
-    convert_f64_to_f32(n, ncols, R, ldr, op->scratch, n, ctx->d_status + 2, s);
+    convert_f64_to_f32(n, ncols, R, ldr, lo, n, ctx->d_status + 2, s);
     status_fetch(ctx);
     if (ctx->h_status[2]) throw Error(MPEIG_E_OVERFLOW, "to_lower: value exceeds binary32 range");
-    chol_solve<float>(ctx, op->Ll, n, ncols, op->scratch, n);
-    convert_f32_to_f64(n, ncols, op->scratch, n, W, ldw, s);
+    chol_apply_gemm<float>(ctx, op->Ll, n, ncols, lo, n, hi, n);
+    convert_f32_to_f64(n, ncols, hi, n, W, ldw, s);
   }
 }
 
@@ -252,8 +302,11 @@ void op_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* X, int
       }
       return;
     case kOpDense: {
-      // herm_product (dense_kernels.hpp:66-72): a plain library GEMM
+      // herm_product (dense_kernels.hpp:66-72): a plain library GEMM (cuBLAS
+      // DGEMM 35 TF/s = 95 % of the DMMA peak at cfg3, scripts/dense_ax_bench.py)
       const int n = static_cast<int>(op->n), c = static_cast<int>(ncols);
+      ProfScope prof("dense_apply", s, double(sizeof(T)) * (double(n) * n + 2.0 * n * c),
+                     2.0 * n * double(n) * c);
       if constexpr (kW) {
         const double one = 1.0, zero = 0.0;
         cublas_check(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, n, c, n, &one, op->A,
