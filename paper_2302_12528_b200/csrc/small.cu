@@ -21,6 +21,8 @@ namespace {
 
 constexpr int kSmallThreads = 256;
 constexpr size_t kSmemCap = 200 * 1024;
+// k_hl_coeffs's dynamic shared memory (p = m = 96: 217 KB) + its ~2 KB static
+constexpr size_t kHlSmemCap = 224 * 1024;
 constexpr int kMaxHlP = 256;  // largest P block (block size m) of the HL update
 
 template <typename T>
@@ -215,7 +217,7 @@ __global__ void k_small_matmul(int r, int k, int c, const T* __restrict__ A, int
 template <typename T>
 __global__ void __launch_bounds__(kSmallThreads)
 k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __restrict__ coef,
-            T* __restrict__ scratch, int* fallback, int use_smem) {
+            T* __restrict__ scratch, int* fallback, int use_smem, T* __restrict__ qout) {
   extern __shared__ __align__(16) unsigned char raw[];
   T* M = use_smem ? reinterpret_cast<T*>(raw) : scratch;
   T* V = M + p * m;
@@ -318,6 +320,11 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
     __syncthreads();
   }
   if (tid == 0) *fallback = fb;
+  if (qout) {  // c_pv by k_hl_cpv across the GPU
+    if (Q != qout && !fb)
+      for (int idx = tid; idx < p * p; idx += nt) qout[idx] = Q[idx];
+    return;
+  }
   // c_pv = C(:, m:m+p) V  (V = I on fallback)
   for (int64_t idx = tid; idx < static_cast<int64_t>(s) * p; idx += nt) {
     const int i = static_cast<int>(idx % s), j = static_cast<int>(idx / s);
@@ -337,6 +344,34 @@ k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __rest
     }
     coef[i + static_cast<int64_t>(m + j) * s] = acc;
   }
+}
+
+// c_pv = C(:, m:m+p) Q (V = I on fallback) for k_hl_coeffs's Q: a thread per
+// entry, rows in consecutive lanes (coalesced C columns), Q broadcast; the same
+// two-way split sum as the single-CTA loop above, so results are identical.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_hl_cpv(int s, int m, int p, const T* __restrict__ C, int64_t ldc, const T* __restrict__ Q,
+         T* __restrict__ coef, const int* fallback) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<int64_t>(s) * p) return;
+  const int i = static_cast<int>(idx % s), j = static_cast<int>(idx / s);
+  const T* cp = C + static_cast<int64_t>(m) * ldc + i;
+  T acc;
+  if (*fallback) {
+    acc = cp[static_cast<int64_t>(j) * ldc];
+  } else {
+    const T* q = Q + static_cast<int64_t>(j) * p;
+    T a0 = T(0), a1 = T(0);
+    int l = 0;
+    for (; l + 1 < p; l += 2) {
+      a0 = fma(cp[static_cast<int64_t>(l) * ldc], q[l], a0);
+      a1 = fma(cp[static_cast<int64_t>(l + 1) * ldc], q[l + 1], a1);
+    }
+    if (l < p) a0 = fma(cp[static_cast<int64_t>(l) * ldc], q[l], a0);
+    acc = a0 + a1;
+  }
+  coef[i + static_cast<int64_t>(m + j) * s] = acc;
 }
 
 // ---- one-warp forms for m <= 32 ---------------------------------------------
@@ -492,11 +527,16 @@ void hl_coeffs_t(int64_t s, int64_t m, int64_t p, const T* C, int64_t ldc, T* co
     }
   }
   const size_t bytes = static_cast<size_t>(p * m + 2 * p * p + p) * sizeof(T);
-  const int use = bytes <= kSmemCap;
+  const int use = bytes <= kHlSmemCap;
   if (use) allow_smem(k_hl_coeffs<T>, bytes);
+  // Q lands where the global-memory layout keeps it (scratch + p m + p p)
+  T* qout = scratch + static_cast<int64_t>(p) * m + static_cast<int64_t>(p) * p;
   k_hl_coeffs<T><<<1, kSmallThreads, use ? bytes : 0, st>>>(
       static_cast<int>(s), static_cast<int>(m), static_cast<int>(p), C, ldc, coef, scratch,
-      fallback, use);
+      fallback, use, qout);
+  MPB_LAUNCH_CHECK();
+  k_hl_cpv<T><<<static_cast<unsigned>(ceil_div(s * p, 256)), 256, 0, st>>>(
+      static_cast<int>(s), static_cast<int>(m), static_cast<int>(p), C, ldc, qout, coef, fallback);
   MPB_LAUNCH_CHECK();
 }
 
