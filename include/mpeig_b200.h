@@ -237,6 +237,22 @@ int mpeig_precond_dense_chol(mpeig_ctx* ctx, const mpeig_op* A, int32_t precisio
                              mpeig_op** out);
 /* Preconditioner::shift_applied() (precond.hpp:114): the retry shift, else 0 */
 double mpeig_precond_shift(const mpeig_op* op);
+/* Sparse Cholesky preconditioner f_T = Pi L^-T L^-1 Pi^T of a CSR operator
+ * (Preconditioner<T>::build(CsrMatrix, prec[, perm]), precond.hpp:55-77):
+ * ordering 0 = reverse Cuthill-McKee (rcm_ordering, rcm.cpp:8-57), 1 = identity
+ * (the system was permuted upstream, drivers.hpp:195-197), 2 = `perm` (n entries,
+ * perm[k] = original index of factored row k).  Up-looking factorisation on the
+ * host (sparse_kernels.hpp:92-170): fp64 at WORKING; fp32 of to_lower(A) at LOWER
+ * with retry_sparse's one shifted retry (precond.hpp:148-159).  Each apply runs the
+ * two triangular sweeps on the device, permutation and lower()/working() fused
+ * (sparse_tri_solve, sparse_kernels.hpp:178-225).  A must come from mpeig_op_csr. */
+int mpeig_precond_sparse_chol(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision,
+                              int32_t ordering, const int64_t* perm, mpeig_op** out);
+/* Preconditioner::factor_nnz() (precond.hpp:116-119) */
+int64_t mpeig_precond_factor_nnz(const mpeig_op* op);
+/* rcm_ordering_pattern (rcm.cpp:8-57), host arrays; perm_out has n entries */
+int mpeig_rcm_ordering(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                       int64_t* perm_out);
 void mpeig_op_destroy(mpeig_op* op);
 int64_t mpeig_op_n(const mpeig_op* op);
 /* Y = op(X) in working (fp64) or lower (fp32) precision, device arrays */

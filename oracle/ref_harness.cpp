@@ -331,18 +331,18 @@ int mpref_solve(const mp_problem* prob, int variant, const mp_cfg* c, mp_result*
   return out->status;
 }
 
-// The reference's stock driver on a dense system: solve(DenseMatrix, cfg)
-// (drivers.hpp:158-181) with its own Cholesky preconditioner
-// (Preconditioner<T>::build, precond.hpp:33-50) -- the golden source for the
-// device dense-Cholesky f_T.  Same outputs as mpref_solve.
+// The reference's stock drivers: solve(DenseMatrix, cfg) (drivers.hpp:158-181)
+// and solve(CsrMatrix, cfg) (:183-210) with their own Cholesky preconditioners
+// (Preconditioner<T>::build, precond.hpp:33-77) -- the golden source for the
+// device dense / sparse Cholesky f_T.  Same outputs as mpref_solve.
 int mpref_solve_native(const mp_problem* prob, int variant, const mp_cfg* c, mp_result* out) {
   out->status = guarded([&] {
     const SolverConfig cfg = to_cfg(c, variant);
     auto sys = make_system(prob, false);
-    if (!sys->dense) throw ConfigError("solve_native: dense problems only");
     const std::size_t m = cfg.block_size();
     const auto t0 = clk::now();
-    EigResult<double> r = solve(sys->D, cfg);
+    // dense: Cholesky f_T; CSR: RCM-permuted system + sparse Cholesky f_T
+    EigResult<double> r = sys->dense ? solve(sys->D, cfg) : solve(sys->A, cfg);
     out->t_total = secs(t0);
     out->t_setup = r.timings.factorize;
     out->t_stage1 = r.precond_shift;  // (field reused: the retry shift)
@@ -358,6 +358,13 @@ int mpref_solve_native(const mp_problem* prob, int variant, const mp_cfg* c, mp_
     export_history(r.history, m, out);
   }, out->msg);
   return out->status;
+}
+
+// rcm_ordering_pattern (rcm.cpp:8-57) on a CSR pattern
+void mpref_rcm(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* out) {
+  std::vector<index_t> r(rp, rp + n + 1), c(ci, ci + rp[n]);
+  const std::vector<index_t> p = rcm_ordering_pattern(static_cast<std::size_t>(n), r, c);
+  for (int64_t k = 0; k < n; ++k) out[k] = p[k];
 }
 
 void mpref_pcg64_u64(uint64_t seed, int64_t count, uint64_t* o) {

@@ -69,6 +69,7 @@ SYMBOLS = [
     "mpeig_ctx_create", "mpeig_ctx_destroy", "mpeig_last_error", "mpeig_launch_count",
     "mpeig_ctx_stream", "mpeig_ctx_set_option", "mpeig_spec_rollbacks", "mpeig_op_lap3d", "mpeig_op_lap2d", "mpeig_op_csr", "mpeig_op_dense",
     "mpeig_op_device_callback", "mpeig_op_host_callback", "mpeig_precond_jacobi", "mpeig_precond_dense_chol", "mpeig_precond_shift",
+    "mpeig_precond_sparse_chol", "mpeig_precond_factor_nnz", "mpeig_rcm_ordering",
     "mpeig_op_destroy", "mpeig_op_n", "mpeig_op_apply", "mpeig_spectral_norm_estimate",
     "mpeig_lobpcg_stage_f64", "mpeig_lobpcg_stage_f32", "mpeig_pinvit_f64", "mpeig_solve",
     "mpeig_run_variant", "mpeig_gaussian_matrix_host", "mpeig_orthonormal_q_f64",
@@ -113,6 +114,9 @@ def load() -> C.CDLL:
         "mpeig_precond_jacobi": (C.c_int, [vp, vp, i32, pvp]),
         "mpeig_precond_dense_chol": (C.c_int, [vp, vp, i32, pvp]),
         "mpeig_precond_shift": (C.c_double, [vp]),
+        "mpeig_precond_sparse_chol": (C.c_int, [vp, vp, i32, i32, vp, pvp]),
+        "mpeig_precond_factor_nnz": (i64, [vp]),
+        "mpeig_rcm_ordering": (C.c_int, [i64, vp, vp, vp]),
         "mpeig_op_destroy": (None, [vp]),
         "mpeig_op_n": (i64, [vp]),
         "mpeig_op_apply": (C.c_int, [vp, vp, i32, i64, vp, i64, vp, i64]),

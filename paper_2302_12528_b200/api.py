@@ -439,6 +439,80 @@ def dense_cholesky(A: Operator, precision: int = LOWER) -> Operator:
     return op
 
 
+def rcm_ordering(row_ptr, col_idx) -> np.ndarray:
+    """rcm_ordering_pattern (rcm.cpp:8-57): perm[k] = original index of row k."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int64)
+    n = rp.size - 1
+    perm = np.empty(n, np.int64)
+    rc = L.load().mpeig_rcm_ordering(n, rp.ctypes.data, ci.ctypes.data, perm.ctypes.data)
+    if rc != 0:
+        raise MpeigError("rcm_ordering failed")
+    return perm
+
+
+def sparse_cholesky(A: Operator, precision: int = LOWER, perm="rcm") -> Operator:
+    """Sparse Cholesky f_T = Pi L^-T L^-1 Pi^T (Preconditioner<T>::build(CsrMatrix,
+    prec[, perm]), precond.hpp:55-77).  perm: "rcm" (the reference's default
+    ordering), None (identity: the system was permuted upstream), or an array.
+    `A` must be a csr_matrix() operator.  `.shift` = shift_applied(), `.factor_nnz`."""
+    keep = ()
+    if isinstance(perm, str):
+        if perm != "rcm":
+            raise ConfigError(f"unknown ordering {perm!r}")
+        h = _mk(A.ctx, A.ctx.lib.mpeig_precond_sparse_chol, A.h, precision, 0, None)
+    elif perm is None:
+        h = _mk(A.ctx, A.ctx.lib.mpeig_precond_sparse_chol, A.h, precision, 1, None)
+    else:
+        p = np.ascontiguousarray(perm, dtype=np.int64)
+        if p.size != A.n:
+            raise DimensionMismatch("sparse_cholesky: bad permutation length")
+        keep = (p,)
+        h = _mk(A.ctx, A.ctx.lib.mpeig_precond_sparse_chol, A.h, precision, 2, p.ctypes.data)
+    op = Operator(A.ctx, h, A.n, "sparse_chol", keep=(A,) + keep)
+    op.shift = float(A.ctx.lib.mpeig_precond_shift(h))
+    op.factor_nnz = int(A.ctx.lib.mpeig_precond_factor_nnz(h))
+    return op
+
+
+def solve_csr(row_ptr, col_idx, vals, cfg: "SolverConfig", ctx: Context = None,
+              want_X: bool = True) -> "EigResult":
+    """The reference's stock sparse driver solve(CsrMatrix, cfg) (drivers.hpp:183-210):
+    one RCM permutation of the system, the sparse Cholesky preconditioner at the
+    variant's precision on the permuted system (identity ordering), the solve, and
+    the eigenvectors returned in the original row order."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int64)
+    v = np.ascontiguousarray(vals, dtype=np.float64)
+    n = rp.size - 1
+    perm = rcm_ordering(rp, ci)
+    inv = np.empty(n, np.int64)
+    inv[perm] = np.arange(n)
+    # As = A(perm, perm), columns ascending per row (CsrMatrix::permuted)
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    nr, nc = inv[rows], inv[ci]
+    order = np.lexsort((nc, nr))
+    prp = np.zeros(n + 1, np.int64)
+    np.add.at(prp, nr + 1, 1)
+    prp = np.cumsum(prp)
+    As = csr_matrix(prp, nc[order], v[order], ctx=ctx)
+    T = sparse_cholesky(As, build_precision_for(cfg.variant), perm=None)
+    r = solve(As, cfg, T=T, want_X=want_X)
+    r.precond_shift = T.shift
+    if want_X and r.X is not None:  # unpermute_rows (drivers.hpp:209)
+        X = r.X
+        if hasattr(X, "cpu"):
+            X = X.cpu().numpy()
+        X = np.asarray(X)
+        out = np.empty_like(X)
+        if X.shape[0] == n:
+            out[perm] = X
+        else:  # (k, n): row j = column j
+            out[:, perm] = X
+        r.X = out
+    return r
+
+
 def build_precision_for(variant: str) -> int:
     """drivers.hpp:113-116."""
     return WORKING if variant == "dlobpcg-dchol" else LOWER

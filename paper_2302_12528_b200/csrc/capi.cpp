@@ -13,6 +13,7 @@
 
 #include "context.hpp"
 #include "solver.hpp"
+#include "spchol.hpp"
 
 using namespace mpb;
 
@@ -401,6 +402,41 @@ int mpeig_precond_dense_chol(mpeig_ctx* ctx, const mpeig_op* A, int32_t precisio
 
 double mpeig_precond_shift(const mpeig_op* op) { return op ? op->shift : 0.0; }
 
+int mpeig_precond_sparse_chol(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision,
+                              int32_t ordering, const int64_t* perm, mpeig_op** out) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    if (!A) throw Error(MPEIG_E_CONFIG, "sparse_chol: null operator");
+    if (precision != MPEIG_WORKING && precision != MPEIG_LOWER)
+      throw Error(MPEIG_E_CONFIG, "sparse_chol: unknown precision");
+    mpeig_op* op = new_op(ctx, kOpSparseChol, A->n);
+    try {
+      sparse_chol_build(ctx, A, precision, ordering, perm, op);
+    } catch (...) {
+      mpeig_op_destroy(op);
+      throw;
+    }
+    *out = op;
+  });
+}
+
+int64_t mpeig_precond_factor_nnz(const mpeig_op* op) {
+  if (!op) return 0;
+  if (op->kind == kOpSparseChol) return op->sp_nnz;
+  if (op->kind == kOpDenseChol) return op->n * (op->n + 1) / 2;
+  return 0;
+}
+
+int mpeig_rcm_ordering(int64_t n, const int64_t* row_ptr, const int64_t* col_idx, int64_t* perm_out) {
+  try {
+    const std::vector<int64_t> p = rcm_ordering(n, row_ptr, col_idx);
+    std::copy(p.begin(), p.end(), perm_out);
+    return MPEIG_OK;
+  } catch (const std::exception&) {
+    return MPEIG_E_OTHER;
+  }
+}
+
 void mpeig_op_destroy(mpeig_op* op) {
   if (!op) return;
   if (op->ctx && op->ctx->stream) cudaStreamSynchronize(op->ctx->stream);
@@ -415,6 +451,13 @@ void mpeig_op_destroy(mpeig_op* op) {
   cudaFree(op->Lw);
   cudaFree(op->Ll);
   cudaFree(op->scratch);
+  cudaFree(op->sp_Lrp);
+  cudaFree(op->sp_Lci);
+  cudaFree(op->sp_Urp);
+  cudaFree(op->sp_Uci);
+  cudaFree(op->sp_perm);
+  cudaFree(op->sp_Lv);
+  cudaFree(op->sp_Uv);
   if (op->halo) cudaFree(op->halo);
   delete op;
 }

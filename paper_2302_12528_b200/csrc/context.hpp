@@ -37,7 +37,7 @@ struct mpeig_ctx {
   mpb::Comm* comm = nullptr;    // row-sharded mode (owned), nullptr: single GPU
 };
 
-enum OpKind { kOpLap3d, kOpLap2d, kOpCsr, kOpDense, kOpDeviceCb, kOpHostCb, kOpJacobi, kOpDenseChol };
+enum OpKind { kOpLap3d, kOpLap2d, kOpCsr, kOpDense, kOpDeviceCb, kOpHostCb, kOpJacobi, kOpDenseChol, kOpSparseChol };
 
 struct mpeig_op {
   OpKind kind;
@@ -75,6 +75,17 @@ struct mpeig_op {
   int64_t tri_singular = -1;   // first zero / subnormal diag(L) (check_tri_diag)
   mutable float* scratch = nullptr;  // to_lower(R) of a working-precision apply
   mutable size_t scratch_elems = 0;
+  // sparse Cholesky f_T (Kind::SparseCholKind, precond.hpp:55-77): L rows with
+  // the diagonal last, U = L^T rows with the diagonal first, int32 indices;
+  // values in the build precision; perm[k] = original index of row k
+  int* sp_Lrp = nullptr;
+  int* sp_Lci = nullptr;
+  int* sp_Urp = nullptr;
+  int* sp_Uci = nullptr;
+  int* sp_perm = nullptr;
+  void* sp_Lv = nullptr;
+  void* sp_Uv = nullptr;
+  int64_t sp_nnz = 0;
 };
 
 namespace mpb {

@@ -26,6 +26,7 @@
 
 #include "context.hpp"
 #include "solver.hpp"
+#include "spchol.hpp"
 
 namespace mpb {
 
@@ -207,6 +208,172 @@ static float* op_scratch(mpeig_ctx* ctx, const mpeig_op* op, size_t need) {
 }
 
 // Preconditioner::apply (T = double) / apply_lower (T = float), precond.hpp:92-109
+// ------------------------------------------- sparse Cholesky f_T
+// Preconditioner<T>::build(CsrMatrix, prec[, perm]) (precond.hpp:55-77): the
+// ordering (RCM by default, rcm.cpp:8-57) and the up-looking factorisation run
+// on the host once per solve (spchol_host.cpp), as in the reference; the factor
+// lives on the device and every apply is the two sweeps of spchol.cu.
+template <typename V>
+static V* sp_upload(const V* host, size_t count, cudaStream_t s) {
+  V* d = nullptr;
+  MPB_CUDA(cudaMalloc(reinterpret_cast<void**>(&d), count * sizeof(V)));
+  MPB_CUDA(cudaMemcpyAsync(d, host, count * sizeof(V), cudaMemcpyHostToDevice, s));
+  return d;
+}
+
+template <typename F>
+static void upload_sparse_factor(mpeig_ctx* ctx, const HostFactor<F>& L, int64_t n, mpeig_op* op) {
+  const int64_t nnz = static_cast<int64_t>(L.ci.size());
+  if (nnz > INT32_MAX) throw Error(MPEIG_E_CONFIG, "sparse_chol: factor above 2^31 entries");
+  std::vector<int> lrp(static_cast<size_t>(n + 1)), lci(static_cast<size_t>(nnz));
+  std::vector<int> urp(static_cast<size_t>(n + 1), 0), uci(static_cast<size_t>(nnz));
+  std::vector<F> uv(static_cast<size_t>(nnz));
+  op->tri_singular = -1;
+  for (int64_t i = 0; i < n; ++i) {
+    lrp[i] = static_cast<int>(L.rp[i]);
+    for (int64_t p = L.rp[i]; p < L.rp[i + 1]; ++p) {
+      lci[p] = static_cast<int>(L.ci[p]);
+      ++urp[L.ci[p] + 1];
+    }
+    const F d = std::abs(L.v[L.rp[i + 1] - 1]);  // check_tri_diag (sparse_kernels.hpp:186-192)
+    if (op->tri_singular < 0 && (d == F(0) || d < std::numeric_limits<F>::min())) op->tri_singular = i;
+  }
+  lrp[n] = static_cast<int>(nnz);
+  for (int64_t j = 0; j < n; ++j) urp[j + 1] += urp[j];
+  std::vector<int> fill(urp.begin(), urp.end() - 1);
+  for (int64_t i = 0; i < n; ++i)  // rows ascending: U row j starts with L(j, j)
+    for (int64_t p = L.rp[i]; p < L.rp[i + 1]; ++p) {
+      const int q = fill[L.ci[p]]++;
+      uci[q] = static_cast<int>(i);
+      uv[q] = L.v[p];
+    }
+  cudaStream_t s = ctx->stream;
+  op->sp_Lrp = sp_upload(lrp.data(), lrp.size(), s);
+  op->sp_Lci = sp_upload(lci.data(), lci.size(), s);
+  op->sp_Urp = sp_upload(urp.data(), urp.size(), s);
+  op->sp_Uci = sp_upload(uci.data(), uci.size(), s);
+  op->sp_Lv = sp_upload(L.v.data(), L.v.size(), s);
+  op->sp_Uv = sp_upload(uv.data(), uv.size(), s);
+  op->sp_nnz = nnz;
+  MPB_CUDA(cudaStreamSynchronize(s));
+}
+
+void sparse_chol_build(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision, int32_t ordering,
+                       const int64_t* user_perm, mpeig_op* op) {
+  if (!A || A->kind != kOpCsr)
+    throw Error(MPEIG_E_CONFIG, "sparse_chol: operator is not an explicit CSR matrix");
+  const int64_t n = A->n;
+  if (n > INT32_MAX) throw Error(MPEIG_E_CONFIG, "sparse_chol: n above 2^31");
+  cudaStream_t s = ctx->stream;
+  std::vector<int64_t> rp(static_cast<size_t>(n + 1));
+  MPB_CUDA(cudaMemcpyAsync(rp.data(), A->rp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+  MPB_CUDA(cudaStreamSynchronize(s));
+  std::vector<int64_t> ci(static_cast<size_t>(rp[n]));
+  std::vector<double> v(static_cast<size_t>(rp[n]));
+  MPB_CUDA(cudaMemcpyAsync(ci.data(), A->ci, sizeof(int64_t) * rp[n], cudaMemcpyDeviceToHost, s));
+  MPB_CUDA(cudaMemcpyAsync(v.data(), A->vals, sizeof(double) * rp[n], cudaMemcpyDeviceToHost, s));
+  MPB_CUDA(cudaStreamSynchronize(s));
+  std::vector<int64_t> perm;
+  if (ordering == 0) {
+    perm = rcm_ordering(n, rp.data(), ci.data());
+  } else if (ordering == 2) {
+    if (!user_perm) throw Error(MPEIG_E_CONFIG, "sparse_chol: null permutation");
+    perm.assign(user_perm, user_perm + n);
+    std::vector<char> hit(static_cast<size_t>(n), 0);
+    for (int64_t k = 0; k < n; ++k) {
+      if (perm[k] < 0 || perm[k] >= n || hit[perm[k]])
+        throw Error(MPEIG_E_DIMENSION, "sparse_cholesky: bad permutation");
+      hit[perm[k]] = 1;
+    }
+  } else if (ordering != 1) {
+    throw Error(MPEIG_E_CONFIG, "sparse_chol: unknown ordering");
+  }
+  std::vector<int64_t> brp, bci;
+  std::vector<double> bv;
+  csr_permute<double>(n, rp.data(), ci.data(), v.data(), perm, brp, bci, bv);
+  op->precision = precision;
+  if (precision == MPEIG_WORKING) {  // no retry in working precision (precond.hpp:64-67)
+    upload_sparse_factor(ctx, sparse_cholesky_host<double>(n, brp, bci, bv), n, op);
+  } else {
+    auto attempt = [&](double shift) {
+      std::vector<double> sv = bv;
+      if (shift != 0.0) {  // retry_sparse (precond.hpp:148-159): A + shift I, every diagonal present
+        for (int64_t k = 0; k < n; ++k) {
+          int64_t d = -1;
+          for (int64_t p = brp[k]; p < brp[k + 1]; ++p)
+            if (bci[p] == k) d = p;
+          const int64_t orig = perm.empty() ? k : perm[k];
+          if (d < 0)
+            throw Error(MPEIG_E_NOT_PD, "precond: missing diagonal entry at " + std::to_string(orig), orig);
+          sv[d] += shift;
+        }
+      }
+      std::vector<float> fv(sv.size());
+      for (size_t q = 0; q < sv.size(); ++q) {  // to_lower (precision.hpp:102-107)
+        fv[q] = static_cast<float>(sv[q]);
+        if (std::isinf(fv[q]) && !std::isinf(sv[q]))
+          throw Error(MPEIG_E_OVERFLOW, "to_lower: matrix exceeds binary32 range");
+      }
+      upload_sparse_factor(ctx, sparse_cholesky_host<float>(n, brp, bci, fv), n, op);
+    };
+    try {
+      attempt(0.0);
+    } catch (const Error& e) {
+      if (e.code != MPEIG_E_NOT_PD && e.code != MPEIG_E_OVERFLOW) throw;
+      op->shift = 10.0 * 0x1p-24 * spectral_norm_estimate(ctx, A, 8, 0x5eed0123ULL);
+      attempt(op->shift);
+    }
+  }
+  if (!perm.empty()) {
+    std::vector<int> p32(perm.begin(), perm.end());
+    op->sp_perm = sp_upload(p32.data(), p32.size(), s);
+    MPB_CUDA(cudaStreamSynchronize(s));
+  }
+}
+
+// sparse_tri_solve(F, R, true) (sparse_kernels.hpp:178-225) as Preconditioner::apply
+// (T = double) / apply_lower (T = float)
+template <typename T>
+static void sparse_chol_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* R,
+                              int64_t ldr, T* W, int64_t ldw) {
+  const int64_t n = op->n;
+  cudaStream_t s = ctx->stream;
+  if (op->tri_singular >= 0)
+    throw Error(MPEIG_E_SINGULAR_TRI, "sparse_tri_solve: bad diagonal", op->tri_singular);
+  if (ncols <= 0) return;
+  const int ni = static_cast<int>(n), ci = static_cast<int>(ncols);
+  const bool wide = op->precision == MPEIG_WORKING;
+  // global-memory column scratch only when a column exceeds shared memory
+  const size_t fbytes = wide ? sizeof(double) : sizeof(float);
+  float* gy = fbytes * n > 200 * 1024 ? op_scratch(ctx, op, (fbytes / 4) * n * ncols) : nullptr;
+  ProfScope prof("precond_spchol", s, double(fbytes) * 2.0 * (op->sp_nnz * 2 + n) +
+                 2.0 * sizeof(T) * n * ncols, 4.0 * op->sp_nnz * ncols);
+  if (wide) {
+    if constexpr (sizeof(T) == 4) {
+      throw Error(MPEIG_E_CONFIG, "precond apply_lower: factor was built at working precision");
+    } else {
+      spchol_solve<double, double, double>(ni, ci, op->sp_Lrp, op->sp_Lci,
+                                           static_cast<const double*>(op->sp_Lv), op->sp_Urp,
+                                           op->sp_Uci, static_cast<const double*>(op->sp_Uv),
+                                           op->sp_perm, R, ldr, W, ldw, ctx->d_status + 2,
+                                           reinterpret_cast<double*>(gy), s);
+    }
+    return;
+  }
+  const float* lv = static_cast<const float*>(op->sp_Lv);
+  const float* uv = static_cast<const float*>(op->sp_Uv);
+  if constexpr (sizeof(T) == 4) {
+    spchol_solve<float, float, float>(ni, ci, op->sp_Lrp, op->sp_Lci, lv, op->sp_Urp, op->sp_Uci,
+                                      uv, op->sp_perm, R, ldr, W, ldw, ctx->d_status + 2, gy, s);
+  } else {  // to_working(sparse_tri_solve(L, to_lower(R))), conversions fused
+    status_clear(ctx);
+    spchol_solve<double, float, double>(ni, ci, op->sp_Lrp, op->sp_Lci, lv, op->sp_Urp, op->sp_Uci,
+                                        uv, op->sp_perm, R, ldr, W, ldw, ctx->d_status + 2, gy, s);
+    status_fetch(ctx);
+    if (ctx->h_status[2]) throw Error(MPEIG_E_OVERFLOW, "to_lower: value exceeds binary32 range");
+  }
+}
+
 template <typename T>
 static void dense_chol_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* R,
                              int64_t ldr, T* W, int64_t ldw) {
@@ -349,6 +516,9 @@ void op_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* X, int
       return;
     case kOpDenseChol:
       dense_chol_apply<T>(ctx, op, ncols, X, ldx, Y, ldy);
+      return;
+    case kOpSparseChol:
+      sparse_chol_apply<T>(ctx, op, ncols, X, ldx, Y, ldy);
       return;
   }
 }

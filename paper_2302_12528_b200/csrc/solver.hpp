@@ -89,6 +89,10 @@ void solve_prepared(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T_op, con
                     double omega_fro, mpeig_history_sink sink, void* sink_user, mpeig_result* out);
 // Preconditioner<T>::build(DenseMatrix, prec) (precond.hpp:33-50): fills op (kOpDenseChol)
 void dense_chol_build(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision, mpeig_op* op);
+// Preconditioner<T>::build(CsrMatrix, prec[, perm]) (precond.hpp:55-77): fills op (kOpSparseChol)
+// ordering: 0 = RCM (rcm_ordering), 1 = identity, 2 = `perm`
+void sparse_chol_build(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision, int32_t ordering,
+                       const int64_t* perm, mpeig_op* op);
 void validate_cfg(const mpeig_cfg& cfg, int64_t n);
 
 }  // namespace mpb

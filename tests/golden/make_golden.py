@@ -15,6 +15,7 @@ values, residual norms) and the reference's own wall time.
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import os
 import sys
 
@@ -26,7 +27,7 @@ sys.path.insert(0, ROOT)
 from oracle import Oracle, Problem  # noqa: E402
 
 sys.path.insert(0, os.path.join(ROOT, "tests"))
-from problems import spd_dense  # noqa: E402
+from problems import lap_csr, random_spd_csr, spd_dense  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 
@@ -55,6 +56,16 @@ CASES = {
     "dense256chol-mplobpcg-schol": (lambda: Problem.dense_matrix(spd_dense(256, 1e3, 5)[0]), "mplobpcg-schol", dict(k=8, tol=1e-10, maxit=500, seed=3, native=True)),
     "dense256chol-pinvit": (lambda: Problem.dense_matrix(spd_dense(256, 1e3, 5)[0]), "pinvit", dict(k=8, tol=1e-10, maxit=500, seed=3, native=True)),
     "dense256chol-k1e10-dlobpcg-schol": (lambda: Problem.dense_matrix(spd_dense(256, 1e10, 5)[0]), "dlobpcg-schol", dict(k=8, tol=1e-10, maxit=12, seed=3, native=True)),
+    # the reference's stock sparse driver solve(CsrMatrix) (drivers.hpp:183-210): RCM
+    # permutation + its own sparse Cholesky preconditioner; the last
+    # case is shifted to lambda_min = -1e-6, so the fp32 factor needs retry_sparse's shift
+    "splap3d16-dlobpcg-dchol": (lambda: Problem.csr(*lap_csr(16, 16, 16)), "dlobpcg-dchol", dict(k=10, block=16, tol=1e-10, maxit=500, native=True)),
+    "splap3d16-dlobpcg-schol": (lambda: Problem.csr(*lap_csr(16, 16, 16)), "dlobpcg-schol", dict(k=10, block=16, tol=1e-10, maxit=500, native=True)),
+    "splap3d16-mplobpcg-schol": (lambda: Problem.csr(*lap_csr(16, 16, 16)), "mplobpcg-schol", dict(k=10, block=16, tol=1e-10, maxit=500, native=True)),
+    "splap3d16-pinvit": (lambda: Problem.csr(*lap_csr(16, 16, 16)), "pinvit", dict(k=10, block=16, tol=1e-10, maxit=500, native=True)),
+    "splap2d50-mplobpcg-schol": (lambda: Problem.csr(*lap_csr(50, 50)), "mplobpcg-schol", dict(k=10, block=15, tol=1e-12, maxit=500, seed=7, native=True)),
+    "sprand2000-mplobpcg-schol": (lambda: Problem.csr(*random_spd_csr(2000, 3, 11)), "mplobpcg-schol", dict(k=8, tol=1e-10, maxit=500, seed=2, native=True)),
+    "splap3d8indef-dlobpcg-schol": (lambda: Problem.csr(*lap_csr(8, 8, 8, shift=0.3618452752845494)), "dlobpcg-schol", dict(k=4, tol=1e-10, maxit=6, native=True)),
     # cfg 1 (BASELINE.json configs[0]) -- minutes each on one core
     "cfg1-dlobpcg-dchol": (lambda: Problem.lap3d(32), "dlobpcg-dchol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
     "cfg1-dlobpcg-schol": (lambda: Problem.lap3d(32), "dlobpcg-schol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
@@ -82,12 +93,25 @@ def run(name: str) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", action="append")
+    ap.add_argument("--rcm", action="store_true", help="also write rcm.npz with --case")
     a = ap.parse_args()
     for name in a.case or FAST:
         run(name)
     # PCG64 golden outputs (tests/test_precision.cpp:56-71 values are asserted
     # in tests/test_oracle.py; these are the longer streams)
     o = Oracle("ref")
+    if a.rcm or not a.case:
+        rcm = {}
+        for nm, (rp, ci, _) in (("lap3d8", lap_csr(8, 8, 8)), ("lap2d5x500", lap_csr(5, 500)),
+                                ("lap3d12x7x5", lap_csr(12, 7, 5)),
+                                ("rand2000", random_spd_csr(2000, 3, 11))):
+            perm = np.zeros(rp.size - 1, np.int64)
+            o.fn("rcm")(C.c_int64(rp.size - 1), rp.ctypes.data_as(C.c_void_p),
+                        ci.ctypes.data_as(C.c_void_p), perm.ctypes.data_as(C.c_void_p))
+            rcm[nm] = perm
+        np.savez_compressed(os.path.join(OUT, "rcm.npz"), **rcm)
+    if a.case:
+        return
     np.savez_compressed(os.path.join(OUT, "pcg64.npz"),
                         s0=o.pcg64(0, 64), s42=o.pcg64(42, 64), s2026=o.pcg64(2026, 64),
                         gauss_0_33x5=o.gaussian(33, 5, 0),

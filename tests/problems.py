@@ -20,3 +20,64 @@ def spd_dense(n: int, kappa: float, seed: int):
     A = (Q * lam) @ Q.T
     A = 0.5 * (A + A.T)
     return np.asfortranarray(A), lam
+
+
+def lap_csr(nx: int, ny: int, nz: int = 1, shift: float = 0.0):
+    """7-pt (nz > 1) / 5-pt (nz = 1) Dirichlet Laplacian as CSR, row = x + nx (y + ny z),
+    columns ascending, diagonal 6 (4) - shift, off-diagonals -1 (the reference's
+    gen_laplace2d, generators.cpp:13-30, and its 3-D analogue)."""
+    import numpy as np
+    n = nx * ny * nz
+    d = (6.0 if nz > 1 else 4.0) - shift
+    rp, ci, v = [0], [], []
+    for z in range(nz):
+        for y in range(ny):
+            for x in range(nx):
+                i = x + nx * (y + ny * z)
+                ent = []
+                if z > 0:
+                    ent.append((i - nx * ny, -1.0))
+                if y > 0:
+                    ent.append((i - nx, -1.0))
+                if x > 0:
+                    ent.append((i - 1, -1.0))
+                ent.append((i, d))
+                if x < nx - 1:
+                    ent.append((i + 1, -1.0))
+                if y < ny - 1:
+                    ent.append((i + nx, -1.0))
+                if z < nz - 1:
+                    ent.append((i + nx * ny, -1.0))
+                for c, val in ent:
+                    ci.append(c)
+                    v.append(val)
+                rp.append(len(ci))
+    return np.array(rp, np.int64), np.array(ci, np.int64), np.array(v)
+
+
+def random_spd_csr(n: int, per_row: int, seed: int):
+    """Random symmetric sparse pattern (per_row off-diagonals per row before
+    symmetrisation), diagonally dominant values: an RCM / sparse-Cholesky test case."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    rows = np.repeat(np.arange(n), per_row)
+    cols = rng.integers(0, n, n * per_row)
+    keep = rows != cols
+    r = np.concatenate([rows[keep], cols[keep]])
+    c = np.concatenate([cols[keep], rows[keep]])
+    val = -rng.random(keep.sum())
+    val = np.concatenate([val, val])
+    A = {}
+    for a, b, x in zip(r.tolist(), c.tolist(), val.tolist()):
+        A[(a, b)] = A.get((a, b), 0.0) + x
+    off = np.zeros(n)
+    for (a, b), x in A.items():
+        off[a] += abs(x)
+    for i in range(n):
+        A[(i, i)] = off[i] + 1.0
+    keys = sorted(A)
+    rp = np.zeros(n + 1, np.int64)
+    for a, _ in keys:
+        rp[a + 1] += 1
+    return (np.cumsum(rp), np.array([b for _, b in keys], np.int64),
+            np.array([A[k] for k in keys]))
