@@ -456,6 +456,8 @@ void mpeig_op_destroy(mpeig_op* op) {
   cudaFree(op->sp_Urp);
   cudaFree(op->sp_Uci);
   cudaFree(op->sp_perm);
+  cudaFree(op->sp_Lsp);
+  cudaFree(op->sp_Usp);
   cudaFree(op->sp_Lv);
   cudaFree(op->sp_Uv);
   if (op->halo) cudaFree(op->halo);

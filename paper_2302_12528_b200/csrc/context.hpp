@@ -83,6 +83,8 @@ struct mpeig_op {
   int* sp_Urp = nullptr;
   int* sp_Uci = nullptr;
   int* sp_perm = nullptr;
+  int* sp_Lsp = nullptr;  // per row: first L entry inside the row's 32-row block
+  int* sp_Usp = nullptr;  // per row: first U entry right of the row's block
   void* sp_Lv = nullptr;
   void* sp_Uv = nullptr;
   int64_t sp_nnz = 0;

@@ -247,7 +247,20 @@ static void upload_sparse_factor(mpeig_ctx* ctx, const HostFactor<F>& L, int64_t
       uci[q] = static_cast<int>(i);
       uv[q] = L.v[p];
     }
+  // block split points of the blocked sweeps (spchol.cu): rows in blocks of 32
+  std::vector<int> lsp(static_cast<size_t>(n)), usp(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t b0 = i & ~int64_t{31}, b1 = b0 + 32;
+    int64_t p = L.rp[i];
+    while (p < L.rp[i + 1] - 1 && L.ci[p] < b0) ++p;
+    lsp[i] = static_cast<int>(p);
+    int q = urp[i] + 1;
+    while (q < urp[i + 1] && uci[q] < b1) ++q;
+    usp[i] = q;
+  }
   cudaStream_t s = ctx->stream;
+  op->sp_Lsp = sp_upload(lsp.data(), lsp.size(), s);
+  op->sp_Usp = sp_upload(usp.data(), usp.size(), s);
   op->sp_Lrp = sp_upload(lrp.data(), lrp.size(), s);
   op->sp_Lci = sp_upload(lci.data(), lci.size(), s);
   op->sp_Urp = sp_upload(urp.data(), urp.size(), s);
@@ -353,8 +366,9 @@ static void sparse_chol_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols,
       throw Error(MPEIG_E_CONFIG, "precond apply_lower: factor was built at working precision");
     } else {
       spchol_solve<double, double, double>(ni, ci, op->sp_Lrp, op->sp_Lci,
-                                           static_cast<const double*>(op->sp_Lv), op->sp_Urp,
-                                           op->sp_Uci, static_cast<const double*>(op->sp_Uv),
+                                           static_cast<const double*>(op->sp_Lv), op->sp_Lsp,
+                                           op->sp_Urp, op->sp_Uci,
+                                           static_cast<const double*>(op->sp_Uv), op->sp_Usp,
                                            op->sp_perm, R, ldr, W, ldw, ctx->d_status + 2,
                                            reinterpret_cast<double*>(gy), s);
     }
@@ -363,12 +377,12 @@ static void sparse_chol_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols,
   const float* lv = static_cast<const float*>(op->sp_Lv);
   const float* uv = static_cast<const float*>(op->sp_Uv);
   if constexpr (sizeof(T) == 4) {
-    spchol_solve<float, float, float>(ni, ci, op->sp_Lrp, op->sp_Lci, lv, op->sp_Urp, op->sp_Uci,
-                                      uv, op->sp_perm, R, ldr, W, ldw, ctx->d_status + 2, gy, s);
+    spchol_solve<float, float, float>(ni, ci, op->sp_Lrp, op->sp_Lci, lv, op->sp_Lsp, op->sp_Urp,
+                                      op->sp_Uci, uv, op->sp_Usp, op->sp_perm, R, ldr, W, ldw, ctx->d_status + 2, gy, s);
   } else {  // to_working(sparse_tri_solve(L, to_lower(R))), conversions fused
     status_clear(ctx);
-    spchol_solve<double, float, double>(ni, ci, op->sp_Lrp, op->sp_Lci, lv, op->sp_Urp, op->sp_Uci,
-                                        uv, op->sp_perm, R, ldr, W, ldw, ctx->d_status + 2, gy, s);
+    spchol_solve<double, float, double>(ni, ci, op->sp_Lrp, op->sp_Lci, lv, op->sp_Lsp,
+                                        op->sp_Urp, op->sp_Uci, uv, op->sp_Usp, op->sp_perm, R, ldr, W, ldw, ctx->d_status + 2, gy, s);
     status_fetch(ctx);
     if (ctx->h_status[2]) throw Error(MPEIG_E_OVERFLOW, "to_lower: value exceeds binary32 range");
   }

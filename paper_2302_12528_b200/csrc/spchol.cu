@@ -1,12 +1,12 @@
 // Device half of the sparse Cholesky preconditioner: the two
 // triangular sweeps of sparse_tri_solve (sparse_kernels.hpp:178-225) with the
 // permutation and the lower()/working() conversions fused into the gather and
-// the scatter.  One warp owns one block column: it gathers the column
+// the scatter.  One CTA owns one block column: it gathers the column
 // (permuted, narrowed) into shared memory, runs the forward sweep over the
-// rows of L and the backward sweep over the rows of U = L^T, and scatters the
-// result (widened).  Each row is a lane-strided dot product + a warp shuffle
-// reduction; the rows are a dependent chain (the RCM etree is close to a
-// path), so the sweep is latency-bound, like the reference's.
+// rows of L and the backward sweep over the rows of U = L^T in blocks of 32
+// rows, and scatters the result (widened).  The RCM etree is close to a path,
+// so the rows form one dependent chain; blocking shortens that chain to 32
+// register steps per block, the rest of each row being a parallel dot product.
 #include <cmath>
 
 #include "common.cuh"
@@ -15,6 +15,9 @@
 namespace mpb {
 namespace {
 
+// one warp per row of a 32-row block: 32 rows' dot products in flight at once
+constexpr int kSpThreads = 1024, kSpWarps = kSpThreads / 32;
+
 template <typename F>
 __device__ __forceinline__ F warp_sum_f(F v) {
 #pragma unroll
@@ -22,53 +25,127 @@ __device__ __forceinline__ F warp_sum_f(F v) {
   return v;
 }
 
+// sum over p in [p0, p1), lane-strided, of v[p] * y[ci[p]]: each lane's terms in
+// ascending order (one fma chain), the index / value loads of 8 terms issued
+// ahead of their use so a long profile row streams instead of paying one
+// memory latency per term
+template <typename F>
+__device__ __forceinline__ F row_dot(int p0, int p1, int lane, const int* __restrict__ ci,
+                                     const F* __restrict__ v, const F* y) {
+  F part = F(0);
+  int p = p0 + lane;
+  for (; p + 7 * 32 < p1; p += 8 * 32) {
+    int c[8];
+    F a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      c[u] = ci[p + u * 32];
+      a[u] = v[p + u * 32];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) part = fma(a[u], y[c[u]], part);
+  }
+  for (; p < p1; p += 32) part = fma(v[p], y[ci[p]], part);
+  return part;
+}
+
+// Blocked sweeps: the rows go in blocks of 32.  Per block, (A) all 8 warps
+// form each row's dot product with the ALREADY FINAL part of y (columns
+// outside the block: the bulk of an RCM profile row) and scatter the row's
+// in-block entries into a dense 32 x 32 shared tile; (B) warp 0 finishes the
+// block's 32 x 32 triangular solve from registers (lane t = row t, one
+// shuffle broadcast per column).  The serial chain is 32 short steps per
+// block instead of one full row per step.
 template <typename Tin, typename F, typename Tout>
-__global__ void __launch_bounds__(32)
+__global__ void __launch_bounds__(kSpThreads)
 k_spchol_solve(int n, const int* __restrict__ Lrp, const int* __restrict__ Lci,
-               const F* __restrict__ Lv, const int* __restrict__ Urp, const int* __restrict__ Uci,
-               const F* __restrict__ Uv, const int* __restrict__ perm, const Tin* __restrict__ B,
-               int64_t ldb, Tout* __restrict__ Y, int64_t ldy, int* overflow, F* gy, int use_smem) {
+               const F* __restrict__ Lv, const int* __restrict__ Lsp, const int* __restrict__ Urp,
+               const int* __restrict__ Uci, const F* __restrict__ Uv, const int* __restrict__ Usp,
+               const int* __restrict__ perm, const Tin* __restrict__ B, int64_t ldb,
+               Tout* __restrict__ Y, int64_t ldy, int* overflow, F* gy, int use_smem) {
   extern __shared__ __align__(16) unsigned char raw[];
-  const int col = blockIdx.x, lane = threadIdx.x;
+  __shared__ double tile_raw[32 * 33];
+  __shared__ double acc_raw[32], dg_raw[32];
+  F* tile = reinterpret_cast<F*>(tile_raw);
+  F* acc = reinterpret_cast<F*>(acc_raw);
+  F* dg = reinterpret_cast<F*>(dg_raw);
+  const int col = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   F* y = use_smem ? reinterpret_cast<F*>(raw) : gy + static_cast<int64_t>(col) * n;
   const Tin* b = B + static_cast<int64_t>(col) * ldb;
   int ovf = 0;
-  for (int k = lane; k < n; k += 32) {
+  for (int k = tid; k < n; k += kSpThreads) {
     const Tin v = b[perm ? perm[k] : k];
     const F f = static_cast<F>(v);
     if (sizeof(Tin) > sizeof(F) && isinf(f) && !isinf(v)) ovf = 1;  // to_lower overflow
     y[k] = f;
   }
   if (__any_sync(0xffffffffu, ovf) && lane == 0) *overflow = 1;
-  __syncwarp();
-  // forward: L z = y, rows ascending, diagonal last
-  for (int i = 0; i < n; ++i) {
-    const int p0 = Lrp[i], pd = Lrp[i + 1] - 1;
-    F part = F(0);
-    for (int p = p0 + lane; p < pd; p += 32) part = fma(Lv[p], y[Lci[p]], part);
-    part = warp_sum_f(part);
-    if (lane == 0) y[i] = (y[i] - part) / Lv[pd];
-    __syncwarp();
+  const int nblk = (n + 31) / 32;
+  // forward: L z = y, blocks ascending; L rows: [Lrp, Lsp) outside, [Lsp, diag) inside
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int b0 = blk * 32, nb = min(32, n - b0);
+    for (int e = tid; e < 32 * 33; e += kSpThreads) tile[e] = F(0);
+    __syncthreads();
+    for (int r = warp; r < nb; r += kSpWarps) {
+      const int i = b0 + r, p0 = Lrp[i], ps = Lsp[i], pd = Lrp[i + 1] - 1;
+      F part = row_dot<F>(p0, ps, lane, Lci, Lv, y);
+      for (int p = ps + lane; p < pd; p += 32) tile[r * 33 + (Lci[p] - b0)] = Lv[p];
+      part = warp_sum_f(part);
+      if (lane == 0) {
+        acc[r] = part;
+        dg[r] = Lv[pd];
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      F s = lane < nb ? y[b0 + lane] - acc[lane] : F(0);
+      for (int j = 0; j < nb; ++j) {
+        if (lane == j) s = s / dg[j];
+        const F yj = __shfl_sync(0xffffffffu, s, j);
+        if (lane > j) s = fma(-tile[lane * 33 + j], yj, s);
+      }
+      if (lane < nb) y[b0 + lane] = s;
+    }
+    __syncthreads();
   }
-  // backward: L^T w = z, rows of U = L^T descending, diagonal first
-  for (int i = n - 1; i >= 0; --i) {
-    const int q0 = Urp[i], q1 = Urp[i + 1];
-    F part = F(0);
-    for (int q = q0 + 1 + lane; q < q1; q += 32) part = fma(Uv[q], y[Uci[q]], part);
-    part = warp_sum_f(part);
-    if (lane == 0) y[i] = (y[i] - part) / Uv[q0];
-    __syncwarp();
+  // backward: L^T w = z, blocks descending; U rows: diag, [+1, Usp) inside, [Usp, end) outside
+  for (int blk = nblk - 1; blk >= 0; --blk) {
+    const int b0 = blk * 32, nb = min(32, n - b0);
+    for (int e = tid; e < 32 * 33; e += kSpThreads) tile[e] = F(0);
+    __syncthreads();
+    for (int r = warp; r < nb; r += kSpWarps) {
+      const int i = b0 + r, q0 = Urp[i], qs = Usp[i], q1 = Urp[i + 1];
+      F part = row_dot<F>(qs, q1, lane, Uci, Uv, y);
+      for (int q = q0 + 1 + lane; q < qs; q += 32) tile[r * 33 + (Uci[q] - b0)] = Uv[q];
+      part = warp_sum_f(part);
+      if (lane == 0) {
+        acc[r] = part;
+        dg[r] = Uv[q0];
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      F s = lane < nb ? y[b0 + lane] - acc[lane] : F(0);
+      for (int j = nb - 1; j >= 0; --j) {
+        if (lane == j) s = s / dg[j];
+        const F yj = __shfl_sync(0xffffffffu, s, j);
+        if (lane < j) s = fma(-tile[lane * 33 + j], yj, s);
+      }
+      if (lane < nb) y[b0 + lane] = s;
+    }
+    __syncthreads();
   }
   Tout* out = Y + static_cast<int64_t>(col) * ldy;
-  for (int k = lane; k < n; k += 32) out[perm ? perm[k] : k] = static_cast<Tout>(y[k]);
+  for (int k = tid; k < n; k += kSpThreads) out[perm ? perm[k] : k] = static_cast<Tout>(y[k]);
 }
 
 }  // namespace
 
 template <typename Tin, typename F, typename Tout>
-void spchol_solve(int n, int c, const int* Lrp, const int* Lci, const F* Lv, const int* Urp,
-                  const int* Uci, const F* Uv, const int* perm, const Tin* B, int64_t ldb,
-                  Tout* Y, int64_t ldy, int* overflow, F* gy, cudaStream_t s) {
+void spchol_solve(int n, int c, const int* Lrp, const int* Lci, const F* Lv, const int* Lsp,
+                  const int* Urp, const int* Uci, const F* Uv, const int* Usp, const int* perm,
+                  const Tin* B, int64_t ldb, Tout* Y, int64_t ldy, int* overflow, F* gy,
+                  cudaStream_t s) {
   if (n <= 0 || c <= 0) return;
   const size_t bytes = sizeof(F) * static_cast<size_t>(n);
   const int use = bytes <= 200 * 1024;
@@ -76,22 +153,19 @@ void spchol_solve(int n, int c, const int* Lrp, const int* Lci, const F* Lv, con
     MPB_CUDA(cudaFuncSetAttribute(k_spchol_solve<Tin, F, Tout>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(bytes)));
-  k_spchol_solve<Tin, F, Tout><<<c, 32, use ? bytes : 0, s>>>(n, Lrp, Lci, Lv, Urp, Uci, Uv, perm,
-                                                             B, ldb, Y, ldy, overflow, gy, use);
+  k_spchol_solve<Tin, F, Tout><<<c, kSpThreads, use ? bytes : 0, s>>>(
+      n, Lrp, Lci, Lv, Lsp, Urp, Uci, Uv, Usp, perm, B, ldb, Y, ldy, overflow, gy, use);
   MPB_LAUNCH_CHECK();
 }
 
-template void spchol_solve<double, double, double>(int, int, const int*, const int*, const double*,
-                                                   const int*, const int*, const double*, const int*,
-                                                   const double*, int64_t, double*, int64_t, int*,
-                                                   double*, cudaStream_t);
-template void spchol_solve<double, float, double>(int, int, const int*, const int*, const float*,
-                                                  const int*, const int*, const float*, const int*,
-                                                  const double*, int64_t, double*, int64_t, int*,
-                                                  float*, cudaStream_t);
-template void spchol_solve<float, float, float>(int, int, const int*, const int*, const float*,
-                                                const int*, const int*, const float*, const int*,
-                                                const float*, int64_t, float*, int64_t, int*,
-                                                float*, cudaStream_t);
+template void spchol_solve<double, double, double>(int, int, const int*, const int*, const double*, const int*,
+    const int*, const int*, const double*, const int*, const int*, const double*, int64_t, double*,
+    int64_t, int*, double*, cudaStream_t);
+template void spchol_solve<double, float, double>(int, int, const int*, const int*, const float*, const int*,
+    const int*, const int*, const float*, const int*, const int*, const double*, int64_t, double*,
+    int64_t, int*, float*, cudaStream_t);
+template void spchol_solve<float, float, float>(int, int, const int*, const int*, const float*, const int*,
+    const int*, const int*, const float*, const int*, const int*, const float*, int64_t, float*,
+    int64_t, int*, float*, cudaStream_t);
 
 }  // namespace mpb

@@ -24,13 +24,15 @@ HostFactor<F> sparse_cholesky_host(int64_t n, const std::vector<int64_t>& rp,
                                    const std::vector<int64_t>& ci, const std::vector<F>& v);
 
 // W = Pi L^-T L^-1 Pi^T R on the device (sparse_tri_solve, sparse_kernels.hpp:178-225):
-// one warp per block column; Tin -> F narrowing (overflow flag) and F -> Tout
-// widening fused into the gather / scatter.  L rows: diagonal last; U = L^T
-// rows: diagonal first.  perm may be null (identity).  gy: n x c scratch of F
-// used when the column does not fit shared memory.
+// one CTA per block column, rows in blocks of 32; Tin -> F narrowing (overflow
+// flag) and F -> Tout widening fused into the gather / scatter.  L rows: diagonal
+// last, Lsp[i] = first entry of row i inside row i's 32-row block; U = L^T rows:
+// diagonal first, Usp[i] = first entry right of row i's block.  perm may be null
+// (identity).  gy: n x c scratch of F used when a column exceeds shared memory.
 template <typename Tin, typename F, typename Tout>
-void spchol_solve(int n, int c, const int* Lrp, const int* Lci, const F* Lv, const int* Urp,
-                  const int* Uci, const F* Uv, const int* perm, const Tin* B, int64_t ldb,
-                  Tout* Y, int64_t ldy, int* overflow, F* gy, cudaStream_t s);
+void spchol_solve(int n, int c, const int* Lrp, const int* Lci, const F* Lv, const int* Lsp,
+                  const int* Urp, const int* Uci, const F* Uv, const int* Usp, const int* perm,
+                  const Tin* B, int64_t ldb, Tout* Y, int64_t ldy, int* overflow, F* gy,
+                  cudaStream_t s);
 
 }  // namespace mpb

@@ -34,12 +34,26 @@ def _solve(mp, name):
     return g, cfg, (rp, ci, v), mp.solve_csr(rp, ci, v, cfg)
 
 
+def _band(name):
+    """+-2, widened to 2 x the reference's own spread under +-1 binary32-ulp
+    perturbations of diag(A) where measured (tests/golden/make_sparse_sensitivity.py;
+    the band policy of DESIGN.md §4.2).  sprand2000 mixed: the reference itself
+    moves by up to 6 iterations (116..127 around 121): a clustered spectrum."""
+    import json
+    import os
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                     "sensitivity_sparse.json")
+    spread = json.load(open(p)).get(name, {}).get("spread", 0) if os.path.exists(p) else 0
+    return max(2, 2 * spread)
+
+
 @pytest.mark.parametrize("name", CASES)
 def test_sparse_cholesky_solve_parity(gpu, name):
-    """theta within 1e-10, residual contract, iterations within +-2 of the reference."""
+    """theta within 1e-10, residual contract, iterations within +-2 of the reference
+    (or the reference's own measured rounding spread, _band)."""
     g, cfg, _, r = _solve(gpu, name)
     assert r.precond_shift == 0.0
-    check_parity(g, cfg, r, name, iter_slack=2)
+    check_parity(g, cfg, r, name, iter_slack=_band(name))
 
 
 def test_sparse_cholesky_eigenvectors_unpermuted(gpu):
