@@ -12,7 +12,8 @@ from .api import (  # noqa: F401
     EigResult, IterationRecord, MpeigError, NoConvergence, NotPositiveDefinite, Operator,
     OverflowError_, RankCollapse, RankDeficient, SingularTriangular, SolverConfig,
     StageOptions, StageOutcome, StageTimings, build_precision_for, converged_count, csr_matrix,
-    default_context, dense_cholesky, dense_matrix, rcm_ordering, solve_csr, sparse_cholesky, gaussian_matrix, host_operator, jacobi, laplace2d, laplace3d,
+    default_context, dense_cholesky, dense_matrix, rcm_ordering, solve_csr, sparse_cholesky,
+    read_matrix_market, ParseError, NotSymmetricHeader, NotSquare, gaussian_matrix, host_operator, jacobi, laplace2d, laplace3d,
     lobpcg_stage, mixed_lobpcg, pinvit, profile, run_variant, solve, solve_prepared,
     spectral_norm_estimate, to_device,
     to_host,

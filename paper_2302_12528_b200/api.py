@@ -439,6 +439,119 @@ def dense_cholesky(A: Operator, precision: int = LOWER) -> Operator:
     return op
 
 
+class ParseError(MpeigError, ValueError):
+    """matrix_market.cpp ParseError(line, col, msg)."""
+
+    def __init__(self, line, col, msg):
+        super().__init__(f"{line}:{col}: {msg}")
+        self.line, self.col = line, col
+
+
+class NotSymmetricHeader(MpeigError, ValueError):
+    """matrix_market.cpp NotSymmetricHeader: only symmetric real input is accepted."""
+
+
+class NotSquare(MpeigError, ValueError):
+    """matrix_market.cpp NotSquare."""
+
+
+def read_matrix_market(path: str):
+    """read_matrix_market_real (matrix_market.cpp:128-157, 204-215) -> (row_ptr, col_idx,
+    vals) CSR: banner `%%MatrixMarket matrix coordinate real symmetric` (case-insensitive),
+    %-comments and blank lines skipped, 1-based entries mirrored across the diagonal,
+    duplicates accumulated (CsrMatrix::from_triplets, csr_matrix.hpp:31-58), columns
+    ascending.  Host-side ingestion; feed the result to csr_matrix() or solve_csr()."""
+    try:
+        f = open(path)
+    except OSError:
+        raise ParseError(0, 0, f"cannot open '{path}'")
+    with f:
+        lines = f.read().split("\n")
+    if not lines or not lines[0].strip():
+        raise ParseError(1, 1, "empty file")
+    tok = lines[0].split()
+    low = [t.lower() for t in tok]
+    if not low or low[0] != "%%matrixmarket":
+        raise ParseError(1, 1, "missing %%MatrixMarket banner")
+    if len(low) < 2 or low[1] != "matrix":
+        raise ParseError(1, 1, "object must be 'matrix'")
+    if len(low) < 3 or low[2] != "coordinate":
+        raise ParseError(1, 1, "format must be 'coordinate'")
+    field = low[3] if len(low) > 3 else ""
+    sym = low[4] if len(low) > 4 else ""
+    if field != "real":
+        raise ParseError(1, 1, f"'{path}' is not a real matrix")
+    if sym != "symmetric":
+        raise NotSymmetricHeader(sym)
+    ln = 1
+    size = None
+    while ln < len(lines):
+        t = lines[ln]
+        ln += 1
+        if t.startswith("%") or not t.strip():
+            continue
+        parts = t.split()
+        if len(parts) != 3:
+            raise ParseError(ln, 1, "expected rows cols nnz")
+        try:
+            rows, cols, nnz = (int(x) for x in parts)
+        except ValueError:
+            raise ParseError(ln, 1, "expected an integer")
+        if rows != cols:
+            raise NotSquare(f"matrix is {rows}x{cols}")
+        if rows < 0 or nnz < 0:
+            raise ParseError(ln, 1, "negative size")
+        size = (rows, nnz)
+        break
+    if size is None:
+        raise ParseError(ln + 1, 1, "missing size line")
+    n, nnz = size
+    I, J, V = [], [], []
+    seen = 0
+    while ln < len(lines):
+        t = lines[ln]
+        ln += 1
+        if t.startswith("%") or not t.strip():
+            continue
+        parts = t.split()
+        if len(parts) != 3:
+            raise ParseError(ln, 1, "expected i j value")
+        try:
+            i, j = int(parts[0]), int(parts[1])
+        except ValueError:
+            raise ParseError(ln, 1, "expected an integer")
+        try:
+            v = float(parts[2])
+        except ValueError:
+            raise ParseError(ln, 1, "expected a number")
+        if i < 1 or i > n or j < 1 or j > n:
+            raise ParseError(ln, 1, "index out of range")
+        seen += 1
+        if seen > nnz:
+            raise ParseError(ln, 1, "more entries than declared")
+        I.append(i - 1), J.append(j - 1), V.append(v)
+        if i != j:
+            I.append(j - 1), J.append(i - 1), V.append(v)
+    if seen != nnz:
+        raise ParseError(ln + 1, 1, "fewer entries than declared")
+    I, J, V = np.array(I, np.int64), np.array(J, np.int64), np.array(V, np.float64)
+    order = np.lexsort((J, I))  # stable: duplicates summed in file order
+    I, J, V = I[order], J[order], V[order]
+    if I.size:
+        new = np.ones(I.size, bool)
+        new[1:] = (I[1:] != I[:-1]) | (J[1:] != J[:-1])
+        idx = np.cumsum(new) - 1
+        vals = np.zeros(int(idx[-1]) + 1)
+        for q in range(I.size):  # sequential accumulation (from_triplets order)
+            vals[idx[q]] += V[q]
+        I, J = I[new], J[new]
+    else:
+        vals = V
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, I + 1, 1)
+    return np.cumsum(rp), J, vals
+
+
 def rcm_ordering(row_ptr, col_idx) -> np.ndarray:
     """rcm_ordering_pattern (rcm.cpp:8-57): perm[k] = original index of row k."""
     rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
