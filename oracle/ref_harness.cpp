@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "mpeig/drivers.hpp"
+#include "mpeig/run_record.hpp"
 #include "mpeig/eigensolvers.hpp"
 #include "mpeig/generators.hpp"
 #include "mpeig/norm_estimate.hpp"
@@ -358,6 +359,13 @@ int mpref_solve_native(const mp_problem* prob, int variant, const mp_cfg* c, mp_
     export_history(r.history, m, out);
   }, out->msg);
   return out->status;
+}
+
+// format_shortest (run_record.cpp:97-102): std::to_chars shortest round trip
+int mpref_format_shortest(double v, char* buf, int cap) {
+  const std::string t = format_shortest(v);
+  std::snprintf(buf, static_cast<std::size_t>(cap), "%s", t.c_str());
+  return static_cast<int>(t.size());
 }
 
 // rcm_ordering_pattern (rcm.cpp:8-57) on a CSR pattern
