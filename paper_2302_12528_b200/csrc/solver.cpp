@@ -248,15 +248,21 @@ static void upload_sparse_factor(mpeig_ctx* ctx, const HostFactor<F>& L, int64_t
       uv[q] = L.v[p];
     }
   // block split points of the blocked sweeps (spchol.cu): rows in blocks of 32
-  std::vector<int> lsp(static_cast<size_t>(n)), usp(static_cast<size_t>(n));
+  // lsp = [Lsp | Lsp2], usp = [Usp | Usp2] (n each): Lsp2 / Usp2 bound the entries
+  // of the neighbouring block (previous for L, next for U)
+  std::vector<int> lsp(static_cast<size_t>(2 * n)), usp(static_cast<size_t>(2 * n));
   for (int64_t i = 0; i < n; ++i) {
     const int64_t b0 = i & ~int64_t{31}, b1 = b0 + 32;
     int64_t p = L.rp[i];
+    while (p < L.rp[i + 1] - 1 && L.ci[p] < b0 - 32) ++p;
+    lsp[n + i] = static_cast<int>(p);
     while (p < L.rp[i + 1] - 1 && L.ci[p] < b0) ++p;
     lsp[i] = static_cast<int>(p);
     int q = urp[i] + 1;
     while (q < urp[i + 1] && uci[q] < b1) ++q;
     usp[i] = q;
+    while (q < urp[i + 1] && uci[q] < b1 + 32) ++q;
+    usp[n + i] = q;
   }
   cudaStream_t s = ctx->stream;
   op->sp_Lsp = sp_upload(lsp.data(), lsp.size(), s);

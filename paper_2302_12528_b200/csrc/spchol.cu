@@ -26,15 +26,27 @@ __device__ __forceinline__ F warp_sum_f(F v) {
 }
 
 // sum over p in [p0, p1), lane-strided, of v[p] * y[ci[p]]: each lane's terms in
-// ascending order (one fma chain), the index / value loads of 8 terms issued
+// ascending order (one fma chain), the index / value loads of 16 terms issued
 // ahead of their use so a long profile row streams instead of paying one
 // memory latency per term
 template <typename F>
 __device__ __forceinline__ F row_dot(int p0, int p1, int lane, const int* __restrict__ ci,
                                      const F* __restrict__ v, const F* y) {
+  constexpr int U = 16;
   F part = F(0);
   int p = p0 + lane;
-  for (; p + 7 * 32 < p1; p += 8 * 32) {
+  for (; p + (U - 1) * 32 < p1; p += U * 32) {
+    int c[U];
+    F a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      c[u] = ci[p + u * 32];
+      a[u] = v[p + u * 32];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) part = fma(a[u], y[c[u]], part);
+  }
+  if (p + 7 * 32 < p1) {
     int c[8];
     F a[8];
 #pragma unroll
@@ -44,6 +56,7 @@ __device__ __forceinline__ F row_dot(int p0, int p1, int lane, const int* __rest
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) part = fma(a[u], y[c[u]], part);
+    p += 8 * 32;
   }
   for (; p < p1; p += 32) part = fma(v[p], y[ci[p]], part);
   return part;
@@ -54,14 +67,16 @@ __device__ __forceinline__ F row_dot(int p0, int p1, int lane, const int* __rest
 // outside the block: the bulk of an RCM profile row) and scatter the row's
 // in-block entries into a dense 32 x 32 shared tile; (B) warp 0 finishes the
 // block's 32 x 32 triangular solve from registers (lane t = row t, one
-// shuffle broadcast per column).  The serial chain is 32 short steps per
+// shuffle broadcast per column) while warps 1..31 already stream the next
+// block's products with the entries that are final (all but the current
+// block's), so phase A's bulk hides behind phase B.  The serial chain is 32 short steps per
 // block instead of one full row per step.
 template <typename Tin, typename F, typename Tout>
 __global__ void __launch_bounds__(kSpThreads)
 k_spchol_solve(int n, const int* __restrict__ Lrp, const int* __restrict__ Lci,
-               const F* __restrict__ Lv, const int* __restrict__ Lsp, const int* __restrict__ Urp,
-               const int* __restrict__ Uci, const F* __restrict__ Uv, const int* __restrict__ Usp,
-               const int* __restrict__ perm, const Tin* __restrict__ B, int64_t ldb,
+               const F* __restrict__ Lv, const int* __restrict__ Lsp, const int* __restrict__ Lsp2,
+               const int* __restrict__ Urp, const int* __restrict__ Uci, const F* __restrict__ Uv,
+               const int* __restrict__ Usp, const int* __restrict__ Usp2, const int* __restrict__ perm, const Tin* __restrict__ B, int64_t ldb,
                Tout* __restrict__ Y, int64_t ldy, int* overflow, F* gy, int use_smem) {
   extern __shared__ __align__(16) unsigned char raw[];
   __shared__ double tile_raw[32 * 33];
@@ -81,18 +96,27 @@ k_spchol_solve(int n, const int* __restrict__ Lrp, const int* __restrict__ Lci,
   }
   if (__any_sync(0xffffffffu, ovf) && lane == 0) *overflow = 1;
   const int nblk = (n + 31) / 32;
-  // forward: L z = y, blocks ascending; L rows: [Lrp, Lsp) outside, [Lsp, diag) inside
+  // accE[buf][r]: row r's product with the entries two or more blocks back,
+  // formed by warps 1..31 while warp 0 runs the previous block's phase B
+  __shared__ double accE_raw[2][32];
+  F* accE0 = reinterpret_cast<F*>(accE_raw[0]);
+  F* accE1 = reinterpret_cast<F*>(accE_raw[1]);
+  if (tid < 32) accE0[tid] = F(0);
+  // forward: L z = y, blocks ascending; row i: [Lrp, Lsp2) two+ blocks back,
+  // [Lsp2, Lsp) the previous block, [Lsp, diag) inside, diag last
   for (int blk = 0; blk < nblk; ++blk) {
     const int b0 = blk * 32, nb = min(32, n - b0);
+    F* accE = (blk & 1) ? accE1 : accE0;
+    F* accN = (blk & 1) ? accE0 : accE1;
     for (int e = tid; e < 32 * 33; e += kSpThreads) tile[e] = F(0);
     __syncthreads();
     for (int r = warp; r < nb; r += kSpWarps) {
-      const int i = b0 + r, p0 = Lrp[i], ps = Lsp[i], pd = Lrp[i + 1] - 1;
-      F part = row_dot<F>(p0, ps, lane, Lci, Lv, y);
+      const int i = b0 + r, ps2 = Lsp2[i], ps = Lsp[i], pd = Lrp[i + 1] - 1;
+      F part = row_dot<F>(ps2, ps, lane, Lci, Lv, y);
       for (int p = ps + lane; p < pd; p += 32) tile[r * 33 + (Lci[p] - b0)] = Lv[p];
       part = warp_sum_f(part);
       if (lane == 0) {
-        acc[r] = part;
+        acc[r] = accE[r] + part;
         dg[r] = Lv[pd];
       }
     }
@@ -105,21 +129,34 @@ k_spchol_solve(int n, const int* __restrict__ Lrp, const int* __restrict__ Lci,
         if (lane > j) s = fma(-tile[lane * 33 + j], yj, s);
       }
       if (lane < nb) y[b0 + lane] = s;
+    } else if (blk + 1 < nblk) {  // next block's rows: entries before this block (final)
+      const int c0 = b0 + 32, nc = min(32, n - c0);
+      for (int r = warp - 1; r < nc; r += kSpWarps - 1) {
+        const int i = c0 + r;
+        F part = warp_sum_f(row_dot<F>(Lrp[i], Lsp2[i], lane, Lci, Lv, y));
+        if (lane == 0) accN[r] = part;
+      }
     }
     __syncthreads();
   }
-  // backward: L^T w = z, blocks descending; U rows: diag, [+1, Usp) inside, [Usp, end) outside
-  for (int blk = nblk - 1; blk >= 0; --blk) {
+  // backward: L^T w = z, blocks descending; U row i: diag, [+1, Usp) inside,
+  // [Usp, Usp2) the next block, [Usp2, end) two+ blocks ahead
+  if (tid < 32) accE0[tid] = F(0);
+  __syncthreads();
+  for (int k = 0; k < nblk; ++k) {
+    const int blk = nblk - 1 - k;
     const int b0 = blk * 32, nb = min(32, n - b0);
+    F* accE = (k & 1) ? accE1 : accE0;
+    F* accN = (k & 1) ? accE0 : accE1;
     for (int e = tid; e < 32 * 33; e += kSpThreads) tile[e] = F(0);
     __syncthreads();
     for (int r = warp; r < nb; r += kSpWarps) {
-      const int i = b0 + r, q0 = Urp[i], qs = Usp[i], q1 = Urp[i + 1];
-      F part = row_dot<F>(qs, q1, lane, Uci, Uv, y);
+      const int i = b0 + r, q0 = Urp[i], qs = Usp[i], qs2 = Usp2[i];
+      F part = row_dot<F>(qs, qs2, lane, Uci, Uv, y);
       for (int q = q0 + 1 + lane; q < qs; q += 32) tile[r * 33 + (Uci[q] - b0)] = Uv[q];
       part = warp_sum_f(part);
       if (lane == 0) {
-        acc[r] = part;
+        acc[r] = accE[r] + part;
         dg[r] = Uv[q0];
       }
     }
@@ -132,6 +169,13 @@ k_spchol_solve(int n, const int* __restrict__ Lrp, const int* __restrict__ Lci,
         if (lane < j) s = fma(-tile[lane * 33 + j], yj, s);
       }
       if (lane < nb) y[b0 + lane] = s;
+    } else if (blk > 0) {  // previous block's rows: entries after this block (final)
+      const int c0 = b0 - 32;
+      for (int r = warp - 1; r < 32; r += kSpWarps - 1) {
+        const int i = c0 + r;
+        F part = warp_sum_f(row_dot<F>(Usp2[i], Urp[i + 1], lane, Uci, Uv, y));
+        if (lane == 0) accN[r] = part;
+      }
     }
     __syncthreads();
   }
@@ -154,7 +198,8 @@ void spchol_solve(int n, int c, const int* Lrp, const int* Lci, const F* Lv, con
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(bytes)));
   k_spchol_solve<Tin, F, Tout><<<c, kSpThreads, use ? bytes : 0, s>>>(
-      n, Lrp, Lci, Lv, Lsp, Urp, Uci, Uv, Usp, perm, B, ldb, Y, ldy, overflow, gy, use);
+      n, Lrp, Lci, Lv, Lsp, Lsp + n, Urp, Uci, Uv, Usp, Usp + n, perm, B, ldb, Y, ldy, overflow,
+      gy, use);
   MPB_LAUNCH_CHECK();
 }
 

@@ -26,8 +26,9 @@ HostFactor<F> sparse_cholesky_host(int64_t n, const std::vector<int64_t>& rp,
 // W = Pi L^-T L^-1 Pi^T R on the device (sparse_tri_solve, sparse_kernels.hpp:178-225):
 // one CTA per block column, rows in blocks of 32; Tin -> F narrowing (overflow
 // flag) and F -> Tout widening fused into the gather / scatter.  L rows: diagonal
-// last, Lsp[i] = first entry of row i inside row i's 32-row block; U = L^T rows:
-// diagonal first, Usp[i] = first entry right of row i's block.  perm may be null
+// last, Lsp[i] = first entry of row i inside row i's 32-row block (Lsp[n + i]: first
+// entry of the previous block); U = L^T rows: diagonal first, Usp[i] = first entry
+// right of row i's block (Usp[n + i]: first entry two blocks right).  perm may be null
 // (identity).  gy: n x c scratch of F used when a column exceeds shared memory.
 template <typename Tin, typename F, typename Tout>
 void spchol_solve(int n, int c, const int* Lrp, const int* Lci, const F* Lv, const int* Lsp,
