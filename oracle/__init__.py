@@ -45,7 +45,7 @@ class MpProblem(C.Structure):
 class MpCfg(C.Structure):
     _fields_ = [("k", C.c_int64), ("block", C.c_int64), ("maxit", C.c_int64),
                 ("tol", C.c_double), ("lower_tol", C.c_double), ("seed", C.c_uint64),
-                ("sketch_rows", C.c_int64)]
+                ("sketch_rows", C.c_int64), ("x0", C.POINTER(C.c_double))]
 
 
 class MpResult(C.Structure):
@@ -155,12 +155,20 @@ class Oracle:
     def solve(self, prob: Problem, variant: str, k: int, block: int = 0, maxit: int = 2000,
               tol: float = 1e-12, lower_tol: float = 5e-6, seed: int = 0,
               sketch_rows: int = 8, want_X: bool = False, hist_cap: int | None = None,
-              native: bool = False):
+              native: bool = False, x0: np.ndarray | None = None):
         """native=True (reference library only, dense problems): the reference's
         stock solve(DenseMatrix, cfg) with its own Cholesky preconditioner
-        (drivers.hpp:158-181) instead of the Jacobi-callback harness."""
+        (drivers.hpp:158-181) instead of the Jacobi-callback harness.
+        x0 (n x m, Jacobi-callback harness only): the start block before
+        orthonormal_q, in place of gaussian_matrix(n, m, seed)."""
         m = block if block else (3 * k + 1) // 2
-        cfg = MpCfg(k, block, maxit, tol, lower_tol, seed, sketch_rows)
+        if x0 is not None:
+            if native:
+                raise ValueError("x0 override needs the callback harness (native=False)")
+            x0 = np.asfortranarray(x0, dtype=np.float64)
+            if x0.shape != (prob.n, m):
+                raise ValueError(f"x0 must be {prob.n} x {m}")
+        cfg = MpCfg(k, block, maxit, tol, lower_tol, seed, sketch_rows, _ptr(x0, C.c_double))
         hc = hist_cap if hist_cap is not None else 2 * maxit + 4
         theta = np.zeros(k)
         resid = np.zeros(k)

@@ -363,7 +363,10 @@ int mporc_solve(const mp_problem* prob, int variant, const mp_cfg* c, mp_result*
     const double t0 = now_s();
     const double est = norm_estimate(&sys.A, n, c->sketch_rows, c->seed ^ 0x9e3779b97f4a7c15ULL);
     double* X = (double*)xmalloc((size_t)(n * m) * sizeof(double));
-    gaussian_fill(n, m, c->seed, X);
+    if (c->x0)
+      memcpy(X, c->x0, (size_t)(n * m) * sizeof(double));
+    else
+      gaussian_fill(n, m, c->seed, X);
     orthonormal_q_d(n, m, X, 1);
     out->t_setup = now_s() - t0;
     out->t_stage1 = 0;

@@ -46,6 +46,10 @@ typedef struct {
   double tol, lower_tol;
   uint64_t seed;
   int64_t sketch_rows;
+  /* optional: the n x m start block before orthonormal_q (column-major),
+   * replacing gaussian_matrix(n, m, seed) -- used to measure the reference's
+   * iteration-count envelope under 1-ulp perturbations of X0 */
+  const double* x0;
 } mp_cfg;
 
 /* Output of one solve. Caller owns every array; capacities in *_cap. */

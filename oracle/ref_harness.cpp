@@ -274,8 +274,10 @@ int mpref_solve(const mp_problem* prob, int variant, const mp_cfg* c, mp_result*
     // drivers.hpp:164-169 (solve): sketch, then the orthonormal start block
     const double est = spectral_norm_estimate<double>(sys->op(), n, cfg.sketch_rows,
                                                       cfg.seed ^ 0x9e3779b97f4a7c15ULL);
-    const DenseMatrix<double> X0 =
-        detail::orthonormal_q(gaussian_matrix<double>(n, m, cfg.seed), true);
+    const DenseMatrix<double> X0 = detail::orthonormal_q(
+        c->x0 ? wrap(static_cast<int64_t>(n), static_cast<int64_t>(m), c->x0)
+              : gaussian_matrix<double>(n, m, cfg.seed),
+        true);
     out->t_setup = secs(t0);
     out->t_stage1 = 0;
     EigResult<double> r;

@@ -749,6 +749,13 @@ static void gemm_impl(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int6
                       T* Y2, cudaStream_t s) {
   const unsigned nz = A2 ? 2u : 1u;
   if (n <= 0 || c <= 0) return;
+  if (c > kGemmInplaceCols && k > 0) {
+    // Y aliasing A: only legal within one output column tile (kernels.cuh)
+    const auto lo = [](const T* p) { return reinterpret_cast<uintptr_t>(p); };
+    const uintptr_t a0 = lo(A), a1 = lo(A + (k - 1) * lda + n), y0 = lo(Y), y1 = lo(Y + (c - 1) * ldy + n);
+    if (a0 < y1 && y0 < a1)
+      throw Error(MPEIG_E_DIMENSION, "gemm_tn: output overlaps A with more than 64 output columns");
+  }
   if (k <= 0) {
     // Y = beta Z
     if (beta == T(0)) {

@@ -25,7 +25,11 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
           int64_t ldb, T* G, int64_t ldg, int sym, T* work, cudaStream_t s);
 
 // Y (n x c) = beta Z + alpha A (n x k) C (k x c)   (matmul, dense_kernels.hpp:20-34)
-// Y may alias Z (elementwise read-before-write); Y must not alias A.
+// Y may alias Z (elementwise read-before-write).  Y may alias A only when
+// c <= kGemmInplaceCols: each CTA then owns whole rows (one column tile) and
+// reads all of them before it writes; wider outputs span several CTAs per row
+// block and an in-place call would race.
+constexpr int64_t kGemmInplaceCols = 64;
 template <typename T>
 void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, const T* C,
              int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y, int64_t ldy, cudaStream_t s);

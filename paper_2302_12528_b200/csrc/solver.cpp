@@ -805,6 +805,21 @@ static T cholqr_tau2(const mpeig_ctx* ctx) {
 template <typename T>
 constexpr T kCholQrSingleTau2 = T(0.25);
 
+// W <- W C (m x m) in place.  Every GEMM kernel reads a row block's inputs
+// before writing it only within ONE output column tile (<= 64 columns:
+// kernels.cuh gemm_tn); a wider block would let a later column tile read
+// columns an earlier tile of the same rows already overwrote, so above that
+// the product goes through the QR scratch w.V and is copied back.
+template <typename T>
+static void gemm_right_inplace(Work<T>& w, int64_t m, T* W, int64_t ldw, const T* C) {
+  if (m <= kGemmInplaceCols) {
+    gemm_tn<T>(w.n, m, m, T(1), W, ldw, C, m, T(0), nullptr, 0, W, ldw, w.s);
+    return;
+  }
+  gemm_tn<T>(w.n, m, m, T(1), W, ldw, C, m, T(0), nullptr, 0, w.V.p, w.ld, w.s);
+  copy_block<T>(w.n, m, w.V.p, w.ld, W, ldw, w.s);
+}
+
 // ------------------------------------------------------------- QR family
 // Q (in place) by "R from a Householder TSQR, then Cholesky-QR of W R^-1":
 //   lower = true  (T = double): Alg. 2 / mixed_qr (ortho.hpp:173-186) --
@@ -901,7 +916,7 @@ int64_t orthonormal_q_dropping(Work<T>& w, int64_t m, T* W, int64_t ldw, bool us
     gram_chol<T>(w, m, w.ctx->d_status, W, ldw, kCholQrSingleTau2<T>);
     status_fetch(w.ctx);
     if (w.ctx->h_status[0] == 0) {
-      gemm_tn<T>(w.n, m, m, T(1), W, ldw, w.Uinv(), m, T(0), nullptr, 0, W, ldw, s);
+      gemm_right_inplace<T>(w, m, W, ldw, w.Uinv());
       return m;
     }
   } else if (w.ctx->spec_qr && m > 0) {
@@ -1169,7 +1184,7 @@ static void qr_spec(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, int* s
     // one guarded CholQR pass (in place: every GEMM kernel reads all of a
     // row's inputs before it writes the row)
     gram_chol<T>(w, m, status, W, ldw, kCholQrSingleTau2<T>);
-    gemm_tn<T>(n, m, m, T(1), W, ldw, w.Uinv(), m, T(0), nullptr, 0, W, ldw, s);
+    gemm_right_inplace<T>(w, m, W, ldw, w.Uinv());
     return;
   }
   if (w.ctx->spec_qr) {

@@ -1,5 +1,6 @@
 """Iteration counts of the GPU solver on every golden case vs the reference
-(and the reference's own FMA-rounding spread).  GPU box helper:
+and the reference's own per-stage envelope under 1-ulp start-block
+perturbations (tests/golden/envelope.json).  GPU box helper:
 
     python scripts/golden_iters.py [name-substring ...]
     MPEIG_OPTS="spec_qr=0,..." selects execution options of the default context.
@@ -14,7 +15,7 @@ sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
 
 import paper_2302_12528_b200 as mp  # noqa: E402
 from conftest import load_golden  # noqa: E402
-from test_gpu_solver import iteration_band, make_op, sensitivity  # noqa: E402
+from test_gpu_solver import iteration_bands, make_op  # noqa: E402
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 names = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and f != "pcg64.npz")
@@ -33,13 +34,10 @@ for name in names:
     r = mp.solve(make_op(mp, name), cfg)
     rb = ctx.spec_rollbacks()
     ref = (int(g["iters_lower"]), int(g["iters_working"]))
-    tot = sum(ref)
-    sens = sensitivity(name) or {}
-    fma = (sens.get("fma_iters_lower"), sens.get("fma_iters_working"))
     got = (r.iterations_lower, r.iterations_working)
     rel = float(np.max(np.abs(r.theta - g["theta"]) / np.abs(g["theta"])))
-    band = iteration_band(name, tot)
-    ok = abs(sum(got) - tot) <= band
-    print(f"{name:28s} ref {ref[0]:5d}+{ref[1]:5d}  fma {fma}  gpu {got[0]:5d}+{got[1]:5d}  "
-          f"d={sum(got) - tot:+5d} band {band:4d} {'ok' if ok else 'OUT'}  theta {rel:.1e}  rollbacks {rb}",
-          flush=True)
+    bands = iteration_bands(name, g)
+    ok = all(lo <= v <= hi for v, (lo, hi) in zip((*got, sum(got)), bands))
+    print(f"{name:28s} ref {ref[0]:5d}+{ref[1]:5d}  gpu {got[0]:5d}+{got[1]:5d}  "
+          f"bands lower {bands[0]} working {bands[1]} {'ok' if ok else 'OUT'}  theta {rel:.1e}  "
+          f"rollbacks {rb}", flush=True)

@@ -81,3 +81,28 @@ def random_spd_csr(n: int, per_row: int, seed: int):
         rp[a + 1] += 1
     return (np.cumsum(rp), np.array([b for _, b in keys], np.int64),
             np.array([A[k] for k in keys]))
+
+
+def perturb_x0(X0, p: int, ulp: str = "f64"):
+    """Start block with rounding-level noise: every entry of X0 moved by -1, 0 or
+    +1 ulp, chosen by a seeded generator (p = 0: X0 unchanged).  ulp = "f64":
+    one binary64 ulp (np.nextafter) -- the working-precision modes; "f32": one
+    binary32 ulp of the entry -- the mixed mode, whose fp32 stage 1 would round
+    a binary64-ulp nudge away in to_lower.  Fed to the reference (oracle x0
+    override) and to the device alike; the spread of the reference's own
+    iteration counts over p = 1..16 is the iteration-parity envelope
+    (tests/golden/make_envelope.py)."""
+    X0 = np.asfortranarray(X0, dtype=np.float64)
+    if p == 0:
+        return X0.copy(order="F")
+    d = np.random.default_rng(0x5EED0000 + p).integers(-1, 2, size=X0.shape)
+    if ulp == "f32":
+        step = np.spacing(np.abs(X0).astype(np.float32)).astype(np.float64)
+        return np.asfortranarray(X0 + d * step)
+    up, dn = np.nextafter(X0, np.inf), np.nextafter(X0, -np.inf)
+    return np.asfortranarray(np.where(d > 0, up, np.where(d < 0, dn, X0)))
+
+
+def envelope_ulp(variant: str) -> str:
+    """Perturbation scale of the envelope for a variant (perturb_x0)."""
+    return "f32" if variant == "mplobpcg-schol" else "f64"
