@@ -161,6 +161,14 @@ int mpeig_ctx_set_option(mpeig_ctx* ctx, const char* key, int value);
  * breakdown or a failed guard inside the speculative body) */
 int64_t mpeig_spec_rollbacks(mpeig_ctx* ctx, int reset);
 
+/* device memory for callers without the CUDA runtime headers (the C++ layer
+ * include/mpeig_b200.hpp): allocation on the context's device, and a copy in
+ * any direction (cudaMemcpyDefault; unified addressing) ordered on the
+ * context's stream and complete on return */
+int mpeig_buffer_alloc(mpeig_ctx* ctx, int64_t bytes, void** out);
+void mpeig_buffer_free(mpeig_ctx* ctx, void* p);
+int mpeig_copy(mpeig_ctx* ctx, void* dst, const void* src, int64_t bytes);
+
 /* -------------------------------------------------------- row sharding */
 /* the n x . blocks are row-sharded over the ranks (z-slabs of
  * the stencil).  Per iteration the ranks sum-allreduce the small Gram
@@ -303,6 +311,19 @@ int mpeig_solve_prepared(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T,
                          const mpeig_cfg* cfg, const double* X0raw, int64_t ldx0,
                          const double* omega, int64_t ldo, double omega_fro,
                          mpeig_history_sink sink, void* sink_user, mpeig_result* out);
+
+/* solve(CsrMatrix, cfg) (drivers.hpp:183-210): the reference's stock sparse
+ * driver.  One RCM permutation of the system (rcm.cpp:8-57), the sparse
+ * Cholesky preconditioner of the permuted system at the variant's precision
+ * (Preconditioner::build(As, prec, {}), precond.hpp:59-77, with retry_sparse's
+ * shift), the norm sketch and seeded start block on the permuted system, then
+ * run_variant; out->X (device, optional) comes back in the ORIGINAL row order
+ * (unpermute_rows).  Host CSR arrays, columns sorted per row.  *precond_shift
+ * (optional) = P.shift_applied(); out->timings.factorize = the factor time. */
+int mpeig_solve_csr(mpeig_ctx* ctx, int64_t n, const int64_t* row_ptr_host,
+                    const int64_t* col_idx_host, const double* vals_host, const mpeig_cfg* cfg,
+                    mpeig_history_sink sink, void* sink_user, mpeig_result* out,
+                    double* precond_shift);
 
 /* run_variant on an explicit start block X0 (device fp64, n x m) with a
  * precomputed norm estimate (drivers.hpp:57-111; mixed_lobpcg :122-152) */

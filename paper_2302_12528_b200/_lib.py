@@ -76,7 +76,8 @@ SYMBOLS = [
     "mpeig_orthonormal_q_f32", "mpeig_mixed_qr_f64", "mpeig_householder_qr_f64",
     "mpeig_orthonormal_q_dropping_f64", "mpeig_gram_f64", "mpeig_gemm_f64",
     "mpeig_project_out_f64", "mpeig_small_eig_f64", "mpeig_hl_coeffs_f64",
-    "mpeig_residual_precond_f64", "mpeig_solve_prepared", "mpeig_profile_enable",
+    "mpeig_residual_precond_f64", "mpeig_solve_prepared", "mpeig_solve_csr",
+    "mpeig_buffer_alloc", "mpeig_buffer_free", "mpeig_copy", "mpeig_profile_enable",
     "mpeig_profile_reset", "mpeig_profile_names", "mpeig_profile_query",
     "mpeig_nccl_unique_id", "mpeig_ctx_attach_nccl", "mpeig_host_group_create",
     "mpeig_host_group_destroy", "mpeig_ctx_attach_host_comm", "mpeig_op_lap3d_slab",
@@ -149,6 +150,11 @@ def load() -> C.CDLL:
                                                  vp, vp]),
         "mpeig_solve_prepared": (C.c_int, [vp, vp, vp, C.POINTER(Cfg), vp, i64, vp, i64, dbl, SINK,
                                            vp, C.POINTER(Result)]),
+        "mpeig_solve_csr": (C.c_int, [vp, i64, vp, vp, vp, C.POINTER(Cfg), SINK, vp,
+                                      C.POINTER(Result), C.POINTER(dbl)]),
+        "mpeig_buffer_alloc": (C.c_int, [vp, i64, pvp]),
+        "mpeig_buffer_free": (None, [vp, vp]),
+        "mpeig_copy": (C.c_int, [vp, vp, vp, i64]),
         "mpeig_nccl_unique_id": (C.c_int, [vp, i64]),
         "mpeig_ctx_attach_nccl": (C.c_int, [vp, C.c_int, C.c_int, vp]),
         "mpeig_host_group_create": (C.c_int, [C.c_int, pvp]),

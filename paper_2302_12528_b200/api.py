@@ -589,40 +589,36 @@ def sparse_cholesky(A: Operator, precision: int = LOWER, perm="rcm") -> Operator
 
 
 def solve_csr(row_ptr, col_idx, vals, cfg: "SolverConfig", ctx: Context = None,
-              want_X: bool = True) -> "EigResult":
-    """The reference's stock sparse driver solve(CsrMatrix, cfg) (drivers.hpp:183-210):
-    one RCM permutation of the system, the sparse Cholesky preconditioner at the
-    variant's precision on the permuted system (identity ordering), the solve, and
-    the eigenvectors returned in the original row order."""
+              want_X: bool = True, history: bool = True) -> "EigResult":
+    """The reference's stock sparse driver solve(CsrMatrix, cfg) (drivers.hpp:183-210)
+    through mpeig_solve_csr: one RCM permutation of the system, the sparse Cholesky
+    preconditioner at the variant's precision on the permuted system (identity
+    ordering), the solve, and the eigenvectors returned in the original row order."""
+    torch = _torch()
+    ctx = ctx or default_context()
     rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
     ci = np.ascontiguousarray(col_idx, dtype=np.int64)
     v = np.ascontiguousarray(vals, dtype=np.float64)
     n = rp.size - 1
-    perm = rcm_ordering(rp, ci)
-    inv = np.empty(n, np.int64)
-    inv[perm] = np.arange(n)
-    # As = A(perm, perm), columns ascending per row (CsrMatrix::permuted)
-    rows = np.repeat(np.arange(n), np.diff(rp))
-    nr, nc = inv[rows], inv[ci]
-    order = np.lexsort((nc, nr))
-    prp = np.zeros(n + 1, np.int64)
-    np.add.at(prp, nr + 1, 1)
-    prp = np.cumsum(prp)
-    As = csr_matrix(prp, nc[order], v[order], ctx=ctx)
-    T = sparse_cholesky(As, build_precision_for(cfg.variant), perm=None)
-    r = solve(As, cfg, T=T, want_X=want_X)
-    r.precond_shift = T.shift
-    if want_X and r.X is not None:  # unpermute_rows (drivers.hpp:209)
-        X = r.X
-        if hasattr(X, "cpu"):
-            X = X.cpu().numpy()
-        X = np.asarray(X)
-        out = np.empty_like(X)
-        if X.shape[0] == n:
-            out[perm] = X
-        else:  # (k, n): row j = column j
-            out[:, perm] = X
-        r.X = out
+    k = cfg.k
+    theta, resid = np.zeros(k), np.zeros(k)
+    res = L.Result()
+    res.theta = theta.ctypes.data_as(C.POINTER(C.c_double))
+    res.residual_norms = resid.ctypes.data_as(C.POINTER(C.c_double))
+    X = None
+    if want_X:
+        X = torch.empty((k, n), dtype=torch.float64, device=f"cuda:{ctx.device}")
+        res.X, res.ldx = C.c_void_p(X.data_ptr()), n
+    hist = _History()
+    shift = C.c_double(0.0)
+    c = cfg.to_c()
+    ctx.check(ctx.lib.mpeig_solve_csr(ctx.h, n, rp.ctypes.data, ci.ctypes.data, v.ctypes.data,
+                                      C.byref(c), hist.cb if history else L.SINK(), None,
+                                      C.byref(res), C.byref(shift)))
+    r = EigResult(theta, X.cpu().numpy() if X is not None else None, resid,
+                  res.iterations_lower, res.iterations_working, hist.records, bool(res.converged),
+                  _timings(res.timings), res.a_norm_estimate)
+    r.precond_shift = shift.value
     return r
 
 

@@ -6,6 +6,7 @@
 #include <cublas_v2.h>
 #include <cusolverDn.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -36,6 +37,11 @@ struct LegacyOrder {
 
 template <typename F>
 int guard(mpeig_ctx* ctx, F&& f) {
+  // A non-sticky error left in the runtime's per-thread slot by a call outside
+  // this entry point (another library, a context torn down by the garbage
+  // collector) must not be reported by this call's launch checks; sticky
+  // errors still surface on the next runtime call.
+  (void)cudaGetLastError();
   try {
     LegacyOrder order(ctx);
     f();
@@ -146,6 +152,7 @@ void mpeig_ctx_destroy(mpeig_ctx* ctx) {
   if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
   delete ctx->comm;
   delete ctx;
+  (void)cudaGetLastError();  // teardown must not leave an error for the next caller
 }
 
 const char* mpeig_last_error(mpeig_ctx* ctx, int64_t* index) {
@@ -567,6 +574,75 @@ int mpeig_solve_prepared(mpeig_ctx* ctx, const mpeig_op* A, const mpeig_op* T,
     set_device(ctx);
     out->timings = mpeig_timings{};
     solve_prepared(ctx, A, T, *cfg, X0raw, ldx0, omega, ldo, omega_fro, sink, sink_user, out);
+  });
+}
+
+int mpeig_buffer_alloc(mpeig_ctx* ctx, int64_t bytes, void** out) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    *out = nullptr;
+    if (bytes > 0) MPB_CUDA(cudaMalloc(out, static_cast<size_t>(bytes)));
+  });
+}
+
+void mpeig_buffer_free(mpeig_ctx* ctx, void* p) {
+  if (!p) return;
+  if (ctx) {
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+  }
+  cudaFree(p);
+}
+
+int mpeig_copy(mpeig_ctx* ctx, void* dst, const void* src, int64_t bytes) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    if (bytes <= 0) return;
+    MPB_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault, ctx->stream));
+    MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int mpeig_solve_csr(mpeig_ctx* ctx, int64_t n, const int64_t* row_ptr_host,
+                    const int64_t* col_idx_host, const double* vals_host, const mpeig_cfg* cfg,
+                    mpeig_history_sink sink, void* sink_user, mpeig_result* out,
+                    double* precond_shift) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    if (!cfg || !out || !row_ptr_host || n < 1) throw Error(MPEIG_E_CONFIG, "solve_csr: null argument");
+    validate_cfg(*cfg, n);  // cfg.validate(n) first (drivers.hpp:185-186)
+    // one RCM permutation of the system (drivers.hpp:187-188)
+    const std::vector<int64_t> perm = rcm_ordering(n, row_ptr_host, col_idx_host);
+    std::vector<int64_t> brp, bci;
+    std::vector<double> bv;
+    csr_permute<double>(n, row_ptr_host, col_idx_host, vals_host, perm, brp, bci, bv);
+    auto rethrow = [&](int rc) {
+      if (rc != MPEIG_OK) throw Error(rc, ctx->last_msg, ctx->last_index);
+    };
+    struct OpPtr {
+      mpeig_op* p = nullptr;
+      ~OpPtr() { mpeig_op_destroy(p); }
+    } As, T;
+    rethrow(mpeig_op_csr(ctx, n, brp.data(), bci.data(), bv.data(), &As.p));
+    // the preconditioner on the permuted system, identity ordering (:190-192)
+    const int32_t prec = cfg->variant == MPEIG_DLOBPCG_DCHOL ? MPEIG_WORKING : MPEIG_LOWER;
+    const auto t0 = std::chrono::steady_clock::now();
+    rethrow(mpeig_precond_sparse_chol(ctx, As.p, prec, 1, nullptr, &T.p));
+    const double t_factor =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (precond_shift) *precond_shift = T.p->shift;
+    out->timings = mpeig_timings{};
+    solve(ctx, As.p, T.p, *cfg, sink, sink_user, out);
+    out->timings.factorize = t_factor;
+    if (out->X) {  // unpermute_rows (drivers.hpp:209): X(perm[i], :) = Xs(i, :)
+      cudaStream_t s = ctx->stream;
+      DevBuf<double> Xs(static_cast<size_t>(n * cfg->k), s);
+      DevBuf<int64_t> dp(static_cast<size_t>(n), s);
+      copy_block<double>(n, cfg->k, out->X, out->ldx, Xs.p, n, s);
+      MPB_CUDA(cudaMemcpyAsync(dp.p, perm.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+      scatter_rows_f64(n, cfg->k, Xs.p, n, dp.p, out->X, out->ldx, s);
+      MPB_CUDA(cudaStreamSynchronize(s));
+    }
   });
 }
 

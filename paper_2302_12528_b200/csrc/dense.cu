@@ -919,6 +919,22 @@ void copy_block(int64_t n, int64_t c, const T* src, int64_t lds, T* dst, int64_t
                              cudaMemcpyDeviceToDevice, s));
 }
 
+__global__ void k_scatter_rows(int64_t n, int64_t c, const double* __restrict__ src, int64_t lds,
+                               const int64_t* __restrict__ perm, double* __restrict__ dst,
+                               int64_t ldd) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= n * c) return;
+  const int64_t i = t % n, j = t / n;
+  dst[perm[i] + j * ldd] = src[i + j * lds];
+}
+
+void scatter_rows_f64(int64_t n, int64_t c, const double* src, int64_t lds, const int64_t* perm,
+                      double* dst, int64_t ldd, cudaStream_t s) {
+  if (n * c <= 0) return;
+  k_scatter_rows<<<grid_for(n * c), 256, 0, s>>>(n, c, src, lds, perm, dst, ldd);
+  MPB_LAUNCH_CHECK();
+}
+
 template <typename T>
 void scale_block(int64_t n, int64_t c, T alpha, const T* X, int64_t ldx, T* Y, int64_t ldy,
                  cudaStream_t s) {

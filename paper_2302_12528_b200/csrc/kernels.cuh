@@ -61,6 +61,9 @@ void copy_block(int64_t n, int64_t c, const T* src, int64_t lds, T* dst, int64_t
                 cudaStream_t s);
 
 // Y = alpha X (elementwise; Y may alias X)
+// dst(perm[i], j) = src(i, j): unpermute_rows (drivers.hpp:209) of an n x c block
+void scatter_rows_f64(int64_t n, int64_t c, const double* src, int64_t lds, const int64_t* perm,
+                      double* dst, int64_t ldd, cudaStream_t s);
 template <typename T>
 void scale_block(int64_t n, int64_t c, T alpha, const T* X, int64_t ldx, T* Y, int64_t ldy,
                  cudaStream_t s);

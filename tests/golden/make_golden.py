@@ -66,12 +66,22 @@ CASES = {
     "splap2d50-mplobpcg-schol": (lambda: Problem.csr(*lap_csr(50, 50)), "mplobpcg-schol", dict(k=10, block=15, tol=1e-12, maxit=500, seed=7, native=True)),
     "sprand2000-mplobpcg-schol": (lambda: Problem.csr(*random_spd_csr(2000, 3, 11)), "mplobpcg-schol", dict(k=8, tol=1e-10, maxit=500, seed=2, native=True)),
     "splap3d8indef-dlobpcg-schol": (lambda: Problem.csr(*lap_csr(8, 8, 8, shift=0.3618452752845494)), "dlobpcg-schol", dict(k=4, tol=1e-10, maxit=6, native=True)),
+    # north-star block sizes (SURVEY §8d ladder): m = 48 (cfg2 family, 3m = 144 > 96:
+    # the large-block path) and m = 96 with the reference's dense Cholesky (cfg3 family)
+    "lap2d64k32-dlobpcg-dchol": (lambda: Problem.lap2d(64), "dlobpcg-dchol", dict(k=32, block=48, tol=1e-10, maxit=5000)),
+    "lap2d64k32-mplobpcg-schol": (lambda: Problem.lap2d(64), "mplobpcg-schol", dict(k=32, block=48, tol=1e-10, maxit=5000)),
+    "lap2d64k32-pinvit": (lambda: Problem.lap2d(64), "pinvit", dict(k=32, block=48, tol=1e-10, maxit=150)),
+    "lap2d128k32-dlobpcg-dchol": (lambda: Problem.lap2d(128), "dlobpcg-dchol", dict(k=32, block=48, tol=1e-10, maxit=8000)),
+    "dense2048chol-dlobpcg-dchol": (lambda: Problem.dense_matrix(spd_dense(2048, 1e3, 9)[0]), "dlobpcg-dchol", dict(k=64, tol=1e-10, maxit=500, seed=5, native=True)),
+    "dense2048chol-mplobpcg-schol": (lambda: Problem.dense_matrix(spd_dense(2048, 1e3, 9)[0]), "mplobpcg-schol", dict(k=64, tol=1e-10, maxit=500, seed=5, native=True)),
     # cfg 1 (BASELINE.json configs[0]) -- minutes each on one core
     "cfg1-dlobpcg-dchol": (lambda: Problem.lap3d(32), "dlobpcg-dchol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
     "cfg1-dlobpcg-schol": (lambda: Problem.lap3d(32), "dlobpcg-schol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
     "cfg1-mplobpcg-schol": (lambda: Problem.lap3d(32), "mplobpcg-schol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
 }
-FAST = [c for c in CASES if not c.startswith("cfg1")]
+LARGE = ["lap2d64k32-dlobpcg-dchol", "lap2d64k32-mplobpcg-schol", "lap2d64k32-pinvit",
+         "lap2d128k32-dlobpcg-dchol", "dense2048chol-dlobpcg-dchol", "dense2048chol-mplobpcg-schol"]
+FAST = [c for c in CASES if not c.startswith("cfg1") and c not in LARGE]
 
 
 def run(name: str) -> None:

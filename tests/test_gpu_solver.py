@@ -335,7 +335,10 @@ def test_wide_block_inplace_cholqr(gpu, variant):
         cfg = gpu.SolverConfig(k=64, block=80, tol=1e-10, maxit=4, variant=variant)
         res[opt] = gpu.solve(A, cfg, want_X=True, history=False)
     a, b = res[10], res[0]
-    assert np.abs(a.theta - b.theta).max() <= 1e-8 * np.abs(b.theta).max()
+    # capped runs: the two QR paths differ by rounding (fp32 stage 1 in mixed
+    # mode); a raced in-place product would corrupt columns 64.. at O(1)
+    tol = 1e-5 if variant == "mplobpcg-schol" else 1e-8
+    assert np.abs(a.theta - b.theta).max() <= tol * np.abs(b.theta).max()
     X = a.X.double()
     G = (X @ X.T).cpu().numpy()
     assert np.abs(G - np.eye(G.shape[0])).max() <= 1e-10
