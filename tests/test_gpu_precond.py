@@ -94,3 +94,19 @@ def test_dense_cholesky_errors(gpu):
     T = mp.dense_cholesky(mp.dense_matrix(np.eye(16) * 2.0), mp.WORKING)
     with pytest.raises(mp.ConfigError):
         T.apply(torch.ones((1, 16), dtype=torch.float32, device="cuda"), precision=mp.LOWER)
+
+
+@pytest.mark.parametrize("name", ["dense2048chol-dlobpcg-dchol", "dense2048chol-mplobpcg-schol"])
+def test_dense_cholesky_m96(gpu, name):
+    """cfg3's block (k = 64, m = 96, s = 288) with the reference's dense Cholesky
+    preconditioner on a 2048 x 2048 SPD matrix: the stock solve(DenseMatrix)."""
+    mp = gpu
+    g = load_golden(name)
+    kw = eval(str(g["kw"]))
+    kw.pop("native", None)
+    variant = str(g["variant"])
+    A = mp.dense_matrix(spd_dense(2048, 1e3, 9)[0])
+    T = mp.dense_cholesky(A, mp.build_precision_for(variant))
+    cfg = mp.SolverConfig(variant=variant, **kw)
+    r = mp.solve(A, cfg, T=T)
+    check_parity(g, cfg, r, name, iter_slack=2)

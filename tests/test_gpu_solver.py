@@ -32,6 +32,10 @@ def make_op(mp, name):
         return mp.laplace2d(5, 500)
     if name.startswith("lap2d32"):
         return mp.laplace2d(32)
+    if name.startswith("lap2d64"):
+        return mp.laplace2d(64)
+    if name.startswith("lap2d128"):
+        return mp.laplace2d(128)
     if name.startswith("dense256"):
         return mp.dense_matrix(spd_dense(256, 1e3, 5)[0])
     raise KeyError(name)
@@ -124,6 +128,29 @@ def test_cfg1_parity(gpu, name):
     """BASELINE.json configs[0]: 3-D Laplacian 32^3, k=10, m=16, tol 1e-10."""
     g, cfg, r = run_case(gpu, name)
     check_parity(g, cfg, r, name)
+
+
+LARGE_BLOCK = ["lap2d64k32-dlobpcg-dchol", "lap2d64k32-mplobpcg-schol", "lap2d128k32-dlobpcg-dchol"]
+
+
+@pytest.mark.parametrize("name", LARGE_BLOCK)
+def test_large_block_parity(gpu, name):
+    """The north-star block sizes' path: k = 32, m = 48, s = 3m = 144 > 96 (the
+    cfg2 family; SURVEY §8d ladder), against the reference's own fixtures."""
+    g, cfg, r = run_case(gpu, name)
+    check_parity(g, cfg, r, name)
+
+
+def test_large_block_pinvit_capped(gpu):
+    """PINVIT at m = 48 capped at 150 iterations (cfg2's PINVIT arm): the same
+    iteration count and Ritz values as the reference's capped run."""
+    g, cfg, r = run_case(gpu, "lap2d64k32-pinvit")
+    assert not r.converged and r.iterations_working == int(g["iters_working"])
+    rel = np.abs(r.theta - g["theta"]) / np.abs(g["theta"])
+    assert rel.max() <= 1e-9
+    ref = g["hist_ritz"][:, :cfg.k]
+    got = np.array([h.ritz_values[:cfg.k] for h in r.history])
+    assert np.abs(got - ref).max() <= 1e-9 * np.abs(ref).max()
 
 
 def test_long_case_parity(gpu):
