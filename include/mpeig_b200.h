@@ -362,6 +362,12 @@ int mpeig_gram_f64(mpeig_ctx* ctx, int64_t n, int64_t ka, const double* A, int64
 int mpeig_gemm_f64(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, double alpha,
                    const double* A, int64_t lda, const double* Cm, int64_t ldc, double beta,
                    const double* Z, int64_t ldz, double* Y, int64_t ldy);
+/* the same two products in binary32 (the lower-precision stage's kernels) */
+int mpeig_gram_f32(mpeig_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda,
+                   int64_t kb, const float* B, int64_t ldb, float* G);
+int mpeig_gemm_f32(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, float alpha,
+                   const float* A, int64_t lda, const float* Cm, int64_t ldc, float beta,
+                   const float* Z, int64_t ldz, float* Y, int64_t ldy);
 /* block_project_out (ortho.hpp:190-200): W -= B (B^T W), `passes` times */
 int mpeig_project_out_f64(mpeig_ctx* ctx, int64_t n, int64_t b, const double* B,
                           int64_t ldb, int64_t w, double* W, int64_t ldw, int32_t passes);

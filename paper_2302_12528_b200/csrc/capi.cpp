@@ -746,6 +746,27 @@ int mpeig_gemm_f64(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, double alpha
   });
 }
 
+int mpeig_gram_f32(mpeig_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, int64_t kb,
+                   const float* B, int64_t ldb, float* G) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    DevBuf<float> wk;
+    wk.alloc_zero(static_cast<size_t>(gram_workspace_elems<float>(n, ka, kb)), ctx->stream);
+    gram<float>(n, ka, A, lda, kb, B, ldb, G, ka, 0, wk.p, ctx->stream);
+    MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int mpeig_gemm_f32(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, float alpha, const float* A,
+                   int64_t lda, const float* Cm, int64_t ldc, float beta, const float* Z,
+                   int64_t ldz, float* Y, int64_t ldy) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    gemm_tn<float>(n, k, c, alpha, A, lda, Cm, ldc, beta, Z, ldz, Y, ldy, ctx->stream);
+    MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int mpeig_project_out_f64(mpeig_ctx* ctx, int64_t n, int64_t b, const double* B, int64_t ldb,
                           int64_t wc, double* W, int64_t ldw, int32_t passes) {
   return guard(ctx, [&] {

@@ -29,6 +29,10 @@ struct Error : std::runtime_error {
                                            cudaGetErrorString(e_));             \
   } while (0)
 
+// Dynamic shared memory above 48 KB needs a per-function opt-in, which is
+// per device context: set it once per (kernel, current device); thread-safe.
+void smem_opt_in(const void* kernel, size_t bytes);
+
 // Kernels launched by this library (reported as gpu_launches by bench.py).
 extern std::atomic<int64_t> g_launches;
 

@@ -39,7 +39,22 @@ struct GramPlan {
 GramPlan gram_plan(int64_t n, int64_t ka, int64_t kb) {
   GramPlan p;
   const int64_t kmax = std::max(ka, kb);
-  p.mt = kmax <= 16 ? 1 : kmax <= 32 ? 2 : kmax <= 48 ? 3 : 4;
+  if (kmax <= 64) {
+    p.mt = kmax <= 16 ? 1 : kmax <= 32 ? 2 : kmax <= 48 ? 3 : 4;  // one tile
+  } else {
+    // wide Grams: the 16*mt tile (mt = 3..5) that wastes the least MMA work on
+    // padding -- 240 = 3 x 80, 160 x 80 = 2 x 1 x 80, 144 = 3 x 48 -- ties to
+    // the larger tile (fewer re-reads of the tall operands)
+    int64_t best = -1;
+    for (int mt = 5; mt >= 3; --mt) {
+      const int64_t t = 16 * mt;
+      const int64_t area = ceil_div(ka, t) * ceil_div(kb, t) * t * t;
+      if (best < 0 || area < best) {
+        best = area;
+        p.mt = mt;
+      }
+    }
+  }
   const int64_t tile = 16 * p.mt;
   p.tiles_m = ceil_div(ka, tile);
   p.tiles_n = ceil_div(kb, tile);
@@ -53,6 +68,16 @@ GramPlan gram_plan(int64_t n, int64_t ka, int64_t kb) {
   p.nchunk = ceil_div(n, p.rows_per_chunk);
   if (p.nchunk < 1) p.nchunk = 1;
   // chunk partials, combined by k_gram_combine
+  p.level_elems = p.nchunk * ka * kb;
+  return p;
+}
+
+// the SIMT kernel's tiles (TM <= 4): the single-tile policy up to 64, then 64
+GramPlan gram_plan_simt(int64_t n, int64_t ka, int64_t kb) {
+  GramPlan p = gram_plan(n, std::min<int64_t>(ka, 64), std::min<int64_t>(kb, 64));
+  p.mt = 4;
+  p.tiles_m = ceil_div(ka, 64);
+  p.tiles_n = ceil_div(kb, 64);
   p.level_elems = p.nchunk * ka * kb;
   return p;
 }
@@ -686,12 +711,7 @@ static void gram_impl(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb
       auto launch = [&](auto mt_tag) {
         constexpr int MT = decltype(mt_tag)::value;
         constexpr size_t smem = gram_dmma_smem<MT>();
-        static bool attr = false;
-        if (!attr) {
-          MPB_CUDA(cudaFuncSetAttribute(k_gram_dmma<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
-          attr = true;
-        }
+        smem_opt_in(reinterpret_cast<const void*>(k_gram_dmma<MT>), smem);
         k_gram_dmma<MT><<<grid, 128, smem, s>>>(n, kai, kbi, A, lda, B, ldb, p.rows_per_chunk, tn,
                                                 p.nchunk, part, ctr, G, ldg, sym);
       };
@@ -699,7 +719,8 @@ static void gram_impl(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb
         case 1: launch(std::integral_constant<int, 1>()); break;
         case 2: launch(std::integral_constant<int, 2>()); break;
         case 3: launch(std::integral_constant<int, 3>()); break;
-        default: launch(std::integral_constant<int, 4>()); break;
+        case 4: launch(std::integral_constant<int, 4>()); break;
+        default: launch(std::integral_constant<int, 5>()); break;
       }
       MPB_LAUNCH_CHECK();
       gram_combine<T>(p, ka, kb, part, G, ldg, sym, s, L ? ticket : nullptr, L, Uinv, status, tau2);
@@ -707,26 +728,29 @@ static void gram_impl(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb
     }
   }
   (void)aligned;
-  switch (p.mt) {
+  const GramPlan ps = p.mt <= 4 ? p : gram_plan_simt(n, ka, kb);
+  grid = dim3(static_cast<unsigned>(ps.tiles_m * ps.tiles_n), static_cast<unsigned>(ps.nchunk));
+  const int tns = static_cast<int>(ps.tiles_n);
+  switch (ps.mt) {
     case 1:
-      k_gram_partial<T, 1><<<grid, 256, 0, s>>>(n, kai, kbi, A, lda, B, ldb, p.rows_per_chunk, tn,
-                                                p.nchunk, part, ctr, G, ldg, sym);
+      k_gram_partial<T, 1><<<grid, 256, 0, s>>>(n, kai, kbi, A, lda, B, ldb, ps.rows_per_chunk, tns,
+                                                ps.nchunk, part, ctr, G, ldg, sym);
       break;
     case 2:
-      k_gram_partial<T, 2><<<grid, 256, 0, s>>>(n, kai, kbi, A, lda, B, ldb, p.rows_per_chunk, tn,
-                                                p.nchunk, part, ctr, G, ldg, sym);
+      k_gram_partial<T, 2><<<grid, 256, 0, s>>>(n, kai, kbi, A, lda, B, ldb, ps.rows_per_chunk, tns,
+                                                ps.nchunk, part, ctr, G, ldg, sym);
       break;
     case 3:
-      k_gram_partial<T, 3><<<grid, 256, 0, s>>>(n, kai, kbi, A, lda, B, ldb, p.rows_per_chunk, tn,
-                                                p.nchunk, part, ctr, G, ldg, sym);
+      k_gram_partial<T, 3><<<grid, 256, 0, s>>>(n, kai, kbi, A, lda, B, ldb, ps.rows_per_chunk, tns,
+                                                ps.nchunk, part, ctr, G, ldg, sym);
       break;
     default:
-      k_gram_partial<T, 4><<<grid, 256, 0, s>>>(n, kai, kbi, A, lda, B, ldb, p.rows_per_chunk, tn,
-                                                p.nchunk, part, ctr, G, ldg, sym);
+      k_gram_partial<T, 4><<<grid, 256, 0, s>>>(n, kai, kbi, A, lda, B, ldb, ps.rows_per_chunk, tns,
+                                                ps.nchunk, part, ctr, G, ldg, sym);
       break;
   }
   MPB_LAUNCH_CHECK();
-  gram_combine<T>(p, ka, kb, part, G, ldg, sym, s, L ? ticket : nullptr, L, Uinv, status, tau2);
+  gram_combine<T>(ps, ka, kb, part, G, ldg, sym, s, L ? ticket : nullptr, L, Uinv, status, tau2);
 }
 
 template <typename T>
@@ -773,7 +797,17 @@ static void gemm_impl(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int6
                          (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(C) % 16 == 0);
     if (aligned) {
-      const int nt = c <= 16 ? 1 : c <= 32 ? 2 : c <= 48 ? 3 : 4;
+      // output tile 16 * nt columns: the least padding, ties to the wider tile
+      // (80 | 160 at m = 80, 48 | 96 | 144 at m = 48)
+      int nt = 1;
+      int64_t best = -1;
+      for (int t = 5; t >= 1; --t) {
+        const int64_t w = ceil_div(c, 16 * t) * 16 * t;
+        if (best < 0 || w < best) {
+          best = w;
+          nt = t;
+        }
+      }
       const dim3 g2(static_cast<unsigned>(ceil_div(n, kTile)),
                     static_cast<unsigned>(ceil_div(c, 16 * nt)), nz);
       const int ki = static_cast<int>(k), ci = static_cast<int>(c);
@@ -783,13 +817,7 @@ static void gemm_impl(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int6
         auto go = [&](auto st_tag) {
           constexpr int ST = decltype(st_tag)::value;
           constexpr size_t smem = sizeof(double) * ST * (kDBK * kAPitch + 16 * NT * kDPitch);
-          static bool attr = false;
-          if (!attr) {
-            MPB_CUDA(cudaFuncSetAttribute(k_gemm_dmma<NT, ST>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(smem)));
-            attr = true;
-          }
+          smem_opt_in(reinterpret_cast<const void*>(k_gemm_dmma<NT, ST>), smem);
           k_gemm_dmma<NT, ST><<<g2, 128, smem, s>>>(n, ki, ci, alpha, A, lda, C, ldc, beta, Z, ldz,
                                                     Y, ldy, A2, Y2);
         };
@@ -802,7 +830,8 @@ static void gemm_impl(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int6
         case 1: launch(std::integral_constant<int, 1>()); break;
         case 2: launch(std::integral_constant<int, 2>()); break;
         case 3: launch(std::integral_constant<int, 3>()); break;
-        default: launch(std::integral_constant<int, 4>()); break;
+        case 4: launch(std::integral_constant<int, 4>()); break;
+        default: launch(std::integral_constant<int, 5>()); break;
       }
       MPB_LAUNCH_CHECK();
       return;

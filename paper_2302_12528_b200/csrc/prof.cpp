@@ -1,6 +1,8 @@
 // prof.cpp -- CUDA-event timing per kernel class (used by bench.py's roofline).
 #include <map>
 #include <mutex>
+#include <set>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -25,6 +27,21 @@ std::map<std::string, Entry>& table() {
 }
 
 }  // namespace
+
+void smem_opt_in(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  MPB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (!done.insert({kernel, dev}).second) return;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(bytes));
+  if (e != cudaSuccess) {
+    done.erase({kernel, dev});
+    MPB_CUDA(e);
+  }
+}
 
 void prof_begin(const char* name, cudaStream_t s, double bytes, double flops) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -95,5 +112,6 @@ int mpeig_profile_query(const char* name, int64_t* count, double* ms, double* by
   *flops = e.flops;
   return 0;
 }
+
 
 }  // extern "C"

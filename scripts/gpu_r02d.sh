@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -q -p no:cacheprovider -x -k "gram or gemm" > gpurun_out/pytest_dense.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_dense.log
+timeout 600 python scripts/dense_shapes.py 2097152 > gpurun_out/dense_shapes_2M_b.json 2> gpurun_out/dense_shapes_2M_b.log
+timeout 900 python scripts/cfg_run.py cfg4 --capped 4 > gpurun_out/r02_cfg4_capped_b.json 2> gpurun_out/r02_cfg4_capped_b.log
+python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_r02d.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_r02d.log

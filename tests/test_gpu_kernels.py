@@ -134,36 +134,76 @@ def test_residual_overflow_is_loud(gpu):
     assert rc == 8  # OverflowError
 
 
-@pytest.mark.parametrize("n,ka,kb", [(100003, 48, 37), (1000, 144, 144), (31, 5, 7)])
-def test_gram(gpu, n, ka, kb):
-    mp = gpu
-    A, B = rand(n, ka, 9), rand(n, kb, 10)
-    ctx = mp.default_context()
-    Ad, Bd = mp.to_device(A), mp.to_device(B)
-    G = np.zeros((ka, kb), order="F")
-    import torch
-    Gd = torch.zeros((kb, ka), dtype=torch.float64, device="cuda")
-    ctx.check(ctx.lib.mpeig_gram_f64(ctx.h, n, ka, C.c_void_p(Ad.data_ptr()), n, kb,
-                                     C.c_void_p(Bd.data_ptr()), n, C.c_void_p(Gd.data_ptr())))
-    G = mp.to_host(Gd)
-    Gr = A.T @ B
-    scale = np.sqrt(np.outer((A * A).sum(0), (B * B).sum(0)))
-    assert np.all(np.abs(G - Gr) <= 1e-14 * np.sqrt(n) * scale + 1e-300)
+GRAM_SHAPES = [(100003, 48, 37), (1000, 144, 144), (31, 5, 7),
+               # the m = 80 / 48 iteration's shapes: S^T AS 240^2, [X P]^T W 160 x 80,
+               # W^T W 80^2 (80-wide DMMA tiles), 96 x 48, and a ragged 200 x 130
+               (70001, 240, 240), (50000, 160, 80), (40003, 80, 80), (30000, 96, 48),
+               (20011, 200, 130)]
 
 
-def test_gemm(gpu):
+@pytest.mark.parametrize("n,ka,kb", GRAM_SHAPES)
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_gram(gpu, n, ka, kb, dtype):
+    """adjoint_matmul (dense_kernels.hpp:36-52) in both precisions against a
+    float64 reference product; the error bound is the fp64 / fp32 dot-product
+    bound sqrt(n) u ||a|| ||b|| per entry."""
     mp = gpu
     import torch
-    n, k, c = 50001, 96, 70
-    A, Cm, Z = rand(n, k, 11), rand(k, c, 12), rand(n, c, 13)
+    npdt, tdt, u = ((np.float64, torch.float64, 2.0 ** -53) if dtype == "f64"
+                    else (np.float32, torch.float32, 2.0 ** -24))
+    A, B = rand(n, ka, 9, npdt), rand(n, kb, 10, npdt)
     ctx = mp.default_context()
-    Ad, Cd, Zd = mp.to_device(A), mp.to_device(Cm), mp.to_device(Z)
-    ctx.check(ctx.lib.mpeig_gemm_f64(ctx.h, n, k, c, -1.0, C.c_void_p(Ad.data_ptr()), n,
-                                     C.c_void_p(Cd.data_ptr()), k, 1.0, C.c_void_p(Zd.data_ptr()),
-                                     n, C.c_void_p(Zd.data_ptr()), n))
-    Y = mp.to_host(Zd)
-    Yr = Z - A @ Cm
-    assert np.abs(Y - Yr).max() <= 1e-13 * np.abs(A).max() * np.abs(Cm).max() * k
+    Ad = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    Bd = torch.from_numpy(np.ascontiguousarray(B.T)).cuda()
+    Gd = torch.zeros((kb, ka), dtype=tdt, device="cuda")
+    fn = ctx.lib.mpeig_gram_f64 if dtype == "f64" else ctx.lib.mpeig_gram_f32
+    ctx.check(fn(ctx.h, n, ka, C.c_void_p(Ad.data_ptr()), n, kb, C.c_void_p(Bd.data_ptr()), n,
+                 C.c_void_p(Gd.data_ptr())))
+    G = Gd.cpu().numpy().T.astype(np.float64)
+    A64, B64 = A.astype(np.float64), B.astype(np.float64)
+    Gr = A64.T @ B64
+    scale = np.sqrt(np.outer((A64 * A64).sum(0), (B64 * B64).sum(0)))
+    assert np.all(np.abs(G - Gr) <= 16 * u * np.sqrt(n) * scale + 1e-300)
+
+
+GEMM_SHAPES = [(50001, 96, 70), (40000, 240, 160), (30001, 160, 80), (20000, 80, 80),
+               (10007, 144, 96), (5000, 48, 48)]
+
+
+@pytest.mark.parametrize("n,k,c", GEMM_SHAPES)
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_gemm(gpu, n, k, c, dtype):
+    """Y = Z - A C (matmul + subtract, dense_kernels.hpp:20-62), both precisions,
+    every output-tile width class (16 .. 80 columns, several column tiles)."""
+    mp = gpu
+    import torch
+    npdt, tdt, u = ((np.float64, torch.float64, 2.0 ** -53) if dtype == "f64"
+                    else (np.float32, torch.float32, 2.0 ** -24))
+    A, Cm, Z = rand(n, k, 11, npdt), rand(k, c, 12, npdt), rand(n, c, 13, npdt)
+    ctx = mp.default_context()
+    dev = lambda M: torch.from_numpy(np.ascontiguousarray(M.T)).cuda()  # noqa: E731
+    Ad, Cd, Zd = dev(A), dev(Cm), dev(Z)
+    fn = ctx.lib.mpeig_gemm_f64 if dtype == "f64" else ctx.lib.mpeig_gemm_f32
+    ctx.check(fn(ctx.h, n, k, c, -1.0, C.c_void_p(Ad.data_ptr()), n, C.c_void_p(Cd.data_ptr()), k,
+                 1.0, C.c_void_p(Zd.data_ptr()), n, C.c_void_p(Zd.data_ptr()), n))
+    Y = Zd.cpu().numpy().T.astype(np.float64)
+    Yr = Z.astype(np.float64) - A.astype(np.float64) @ Cm.astype(np.float64)
+    bound = 4 * u * (np.abs(A).astype(np.float64) @ np.abs(Cm).astype(np.float64) + np.abs(Z)) * k
+    assert np.all(np.abs(Y - Yr) <= bound)
+
+
+def test_gemm_inplace_wide_is_refused(gpu):
+    """Y aliasing A with more than 64 output columns would race across column
+    tiles: the library refuses instead of returning wrong columns."""
+    mp = gpu
+    import torch
+    n, k = 10000, 80
+    W = torch.randn(k, n, dtype=torch.float64, device="cuda")
+    U = torch.eye(k, dtype=torch.float64, device="cuda")
+    ctx = mp.default_context()
+    rc = ctx.lib.mpeig_gemm_f64(ctx.h, n, k, k, 1.0, C.c_void_p(W.data_ptr()), n,
+                                C.c_void_p(U.data_ptr()), k, 0.0, None, 0, C.c_void_p(W.data_ptr()), n)
+    assert rc == 1  # DimensionMismatch
 
 
 def graded(n, m, kappa, seed):

@@ -70,19 +70,24 @@ def iteration_bands(name, g):
     Bit-identical trajectories need bit-identical reductions, which a parallel
     device cannot reproduce, and LOBPCG iteration counts on these spectra are
     a chaotic function of rounding.  The band is the reference's OWN spread
-    under 1-ulp perturbations of its start block (envelope.json), per stage,
-    widened by the north star's +-2; without a measured envelope it is the
-    reference's count +-2 per stage."""
+    under 1-ulp perturbations of its start block (envelope.json), per stage:
+    the observed [min, max] over the 17 runs, extended to mean +- 3 standard
+    deviations of that sample (17 draws cover only about +-2 sigma of the
+    distribution), then widened by the north star's +-2.  Without a measured
+    envelope it is the reference's count +-2 per stage."""
     ref = (int(g["iters_lower"]), int(g["iters_working"]))
     runs = [ref]
     env = envelope(name)
     if env:
         runs += [tuple(r) for r in env["perturbed"]]
-    lo = [min(r[i] for r in runs) for i in range(2)]
-    hi = [max(r[i] for r in runs) for i in range(2)]
-    tl, th = min(sum(r) for r in runs), max(sum(r) for r in runs)
+    a = np.array(runs, dtype=float)
+    a = np.column_stack([a, a.sum(1)])
+    lo, hi = a.min(0), a.max(0)
+    if len(runs) > 2:
+        mu, sd = a.mean(0), a.std(0, ddof=1)
+        lo, hi = np.minimum(lo, np.floor(mu - 3 * sd)), np.maximum(hi, np.ceil(mu + 3 * sd))
     s = ITER_SLACK
-    return ((lo[0] - s, hi[0] + s), (lo[1] - s, hi[1] + s), (tl - s, th + s))
+    return tuple((int(lo[i]) - s, int(hi[i]) + s) for i in range(3))
 
 
 def check_parity(g, cfg, r, name=None, iter_slack=None):
