@@ -362,6 +362,13 @@ int mpeig_gram_f64(mpeig_ctx* ctx, int64_t n, int64_t ka, const double* A, int64
 int mpeig_gemm_f64(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, double alpha,
                    const double* A, int64_t lda, const double* Cm, int64_t ldc, double beta,
                    const double* Z, int64_t ldz, double* Y, int64_t ldy);
+/* Process-wide kernel-selection knobs (diagnostics and tests; NOT per
+ * context -- set them before any solve runs):
+ *   "gram_tc" / "gemm_tc" / "tc" (both): the binary32 Gram / block update
+ *              on the tcgen05 tensor cores (exact 3-way bf16 split, fp32
+ *              accumulation): 1 = for products with n * k * c >= 2^28
+ *              (default), 0 = never (SIMT FFMA kernels), 2 = always. */
+int mpeig_set_process_option(const char* key, int value);
 /* the same two products in binary32 (the lower-precision stage's kernels) */
 int mpeig_gram_f32(mpeig_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda,
                    int64_t kb, const float* B, int64_t ldb, float* G);

@@ -77,7 +77,8 @@ SYMBOLS = [
     "mpeig_orthonormal_q_dropping_f64", "mpeig_gram_f64", "mpeig_gemm_f64",
     "mpeig_project_out_f64", "mpeig_small_eig_f64", "mpeig_hl_coeffs_f64",
     "mpeig_residual_precond_f64", "mpeig_solve_prepared", "mpeig_solve_csr",
-    "mpeig_buffer_alloc", "mpeig_buffer_free", "mpeig_copy", "mpeig_gram_f32", "mpeig_gemm_f32", "mpeig_profile_enable",
+    "mpeig_buffer_alloc", "mpeig_buffer_free", "mpeig_copy", "mpeig_gram_f32", "mpeig_gemm_f32",
+    "mpeig_set_process_option", "mpeig_profile_enable",
     "mpeig_profile_reset", "mpeig_profile_names", "mpeig_profile_query",
     "mpeig_nccl_unique_id", "mpeig_ctx_attach_nccl", "mpeig_host_group_create",
     "mpeig_host_group_destroy", "mpeig_ctx_attach_host_comm", "mpeig_op_lap3d_slab",
@@ -143,6 +144,7 @@ def load() -> C.CDLL:
         "mpeig_gram_f64": (C.c_int, [vp, i64, i64, vp, i64, i64, vp, i64, vp]),
         "mpeig_gemm_f64": (C.c_int, [vp, i64, i64, i64, dbl, vp, i64, vp, i64, dbl, vp, i64, vp,
                                      i64]),
+        "mpeig_set_process_option": (C.c_int, [C.c_char_p, C.c_int]),
         "mpeig_gram_f32": (C.c_int, [vp, i64, i64, vp, i64, i64, vp, i64, vp]),
         "mpeig_gemm_f32": (C.c_int, [vp, i64, i64, i64, C.c_float, vp, i64, vp, i64, C.c_float, vp,
                                      i64, vp, i64]),

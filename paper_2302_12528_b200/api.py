@@ -32,6 +32,7 @@ fallback.
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional
 
@@ -143,6 +144,7 @@ class IterationRecord:
     n_converged: int
     w_columns_dropped: int
     basis_rotation_fallback: bool
+    host_time: float = 0.0  # time.perf_counter() when the record reached the host (diagnostic)
 
 
 @dataclass
@@ -640,7 +642,7 @@ class _History:
             self.records.append(IterationRecord(
                 int(r.stage), [r.ritz_values[j] for j in range(m)],
                 [r.residual_norms[j] for j in range(m)], int(r.n_converged),
-                int(r.w_columns_dropped), bool(r.basis_rotation_fallback)))
+                int(r.w_columns_dropped), bool(r.basis_rotation_fallback), time.perf_counter()))
         self.cb = L.SINK(sink)
 
 

@@ -746,6 +746,19 @@ int mpeig_gemm_f64(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, double alpha
   });
 }
 
+int mpeig_set_process_option(const char* key, int value) {
+  const std::string k = key ? key : "";
+  if (k == "tc_nprod") { g_tc_nprod = value; return MPEIG_OK; }
+  if (k == "tc_store") { g_tc_store = value; return MPEIG_OK; }
+  if (k == "gram_tc" || k == "gemm_tc" || k == "tc") {
+    if (value < 0 || value > 2) return MPEIG_E_CONFIG;
+    if (k != "gemm_tc") g_gram_tc = value;
+    if (k != "gram_tc") g_gemm_tc = value;
+    return MPEIG_OK;
+  }
+  return MPEIG_E_CONFIG;
+}
+
 int mpeig_gram_f32(mpeig_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, int64_t kb,
                    const float* B, int64_t ldb, float* G) {
   return guard(ctx, [&] {

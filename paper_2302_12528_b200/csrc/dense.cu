@@ -669,8 +669,8 @@ int grid_for(int64_t total, int threads = 256, int64_t cap = kNumSMs * 8) {
 template <typename T>
 void gram_combine(const GramPlan& p, int64_t ka, int64_t kb, const T* part, T* G, int64_t ldg, int sym,
                   cudaStream_t s, int* ticket = nullptr, T* L = nullptr, T* Uinv = nullptr,
-                  int* status = nullptr, T tau2 = T(0)) {
-  if (p.nchunk == 1 && !sym) return;  // the kernel wrote G directly
+                  int* status = nullptr, T tau2 = T(0), bool force = false) {
+  if (p.nchunk == 1 && !sym && !force) return;  // the kernel wrote G directly
   const int64_t warps = sym ? ka * (ka + 1) / 2 : ka * kb;
   k_gram_combine<T><<<static_cast<unsigned>(ceil_div(warps, 8)), 256, 0, s>>>(
       p.nchunk, static_cast<int>(ka), static_cast<int>(kb), part, G, ldg, sym, ticket, L, Uinv,
@@ -724,6 +724,16 @@ static void gram_impl(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb
       }
       MPB_LAUNCH_CHECK();
       gram_combine<T>(p, ka, kb, part, G, ldg, sym, s, L ? ticket : nullptr, L, Uinv, status, tau2);
+      return;
+    }
+  }
+  if constexpr (sizeof(T) == 4) {
+    // binary32 on the tcgen05 tensor cores (tc.cu: exact 3-way bf16 split)
+    if (gram_tc_wanted(n, ka, kb) && gram_tc_eligible(n, ka, kb, lda, ldb, A, B)) {
+      GramPlan pt = p;
+      pt.nchunk = gram_tc_f32(n, ka, A, lda, kb, B, ldb, p.nchunk, part, s);
+      gram_combine<T>(pt, ka, kb, part, G, ldg, sym, s, L ? ticket : nullptr, L, Uinv, status, tau2,
+                      /*force=*/true);
       return;
     }
   }
@@ -834,6 +844,17 @@ static void gemm_impl(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int6
         default: launch(std::integral_constant<int, 5>()); break;
       }
       MPB_LAUNCH_CHECK();
+      return;
+    }
+  }
+  if constexpr (sizeof(T) == 4) {
+    // binary32 on the tcgen05 tensor cores (tc.cu: exact 3-way bf16 split);
+    // one CTA covers whole rows of every column tile it writes after reading
+    // all of its rows of A, so the Y = A in-place contract (c <= 64) holds
+    if (gemm_tc_wanted(n, k, c) && gemm_tc_eligible(n, k, c, lda, ldc, A, C) &&
+        (!A2 || gemm_tc_eligible(n, k, c, lda, ldc, A2, C)) &&
+        (c <= 128 || (Y != A && (!A2 || Y2 != A2)))) {
+      gemm_tc_f32(n, k, c, alpha, A, lda, C, ldc, beta, Z, ldz, Y, ldy, A2, Y2, s);
       return;
     }
   }

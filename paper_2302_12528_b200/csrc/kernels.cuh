@@ -33,6 +33,29 @@ constexpr int64_t kGemmInplaceCols = 64;
 template <typename T>
 void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, const T* C,
              int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y, int64_t ldy, cudaStream_t s);
+// binary32 Gram chunk partials on the tcgen05 tensor cores (tc.cu); the
+// caller combines the returned number of chunks
+bool gram_tc_eligible(int64_t n, int64_t ka, int64_t kb, int64_t lda, int64_t ldb, const float* A,
+                      const float* B);
+int64_t gram_tc_f32(int64_t n, int64_t ka, const float* A, int64_t lda, int64_t kb, const float* B,
+                    int64_t ldb, int64_t max_chunks, float* part, cudaStream_t s);
+// binary32 Y = beta Z + alpha A C (+ the paired A2 C) on tcgen05 (tc.cu)
+bool gemm_tc_eligible(int64_t n, int64_t k, int64_t c, int64_t lda, int64_t ldc, const float* A,
+                      const float* C);
+void gemm_tc_f32(int64_t n, int64_t k, int64_t c, float alpha, const float* A, int64_t lda,
+                 const float* C, int64_t ldc, float beta, const float* Z, int64_t ldz, float* Y,
+                 int64_t ldy, const float* A2, float* Y2, cudaStream_t s);
+// policy: the tensor-core path for Grams big enough to be bandwidth/compute
+// bound (the m = 16 cfg1 shapes stay on the latency-lean SIMT kernel);
+// g_gram_tc: 1 = by size (default), 0 = never, 2 = always (tests)
+extern int g_gram_tc, g_gemm_tc;
+extern int g_tc_nprod, g_tc_store;
+inline bool gram_tc_wanted(int64_t n, int64_t ka, int64_t kb) {
+  return g_gram_tc == 2 || (g_gram_tc == 1 && n * ka * kb >= (int64_t(1) << 28));
+}
+inline bool gemm_tc_wanted(int64_t n, int64_t k, int64_t c) {
+  return g_gemm_tc == 2 || (g_gemm_tc == 1 && n * k * c >= (int64_t(1) << 28));
+}
 // CholQR's Gram and factorization in one pass (m <= 16): G = V^T V
 // (hermitized), then L L^T = G and Uinv = L^{-T} by the last CTA of the
 // combine; returns false (nothing launched) when m > 16.

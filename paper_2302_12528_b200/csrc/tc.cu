@@ -1,0 +1,651 @@
+// tc.cu -- binary32 Gram products on the 5th-generation tensor cores (tcgen05).
+//
+// The lower-precision stage's Gram G = A^T B (adjoint_matmul<float>,
+// dense_kernels.hpp:36-52) on B200's tcgen05 MMA.  tcgen05 has no fp32
+// multiplicand kind, so each binary32 operand is split exactly into three
+// bfloat16 parts, x = hi + mid + lo (8 + 8 + 8 significand bits: every split
+// is exact, bf16 has binary32's exponent range), and the part products are
+// accumulated in fp32 in tensor memory.  Each bf16 x bf16 product is exact
+// in fp32, so the result carries only fp32 accumulation rounding -- the same
+// order of error as the reference's binary32 dot products, at tensor-core
+// throughput instead of the FFMA pipe's.
+//
+// CTA (256 threads) = one 128 x N output tile x one row chunk of n:
+//   * all 8 warps stream the fp32 columns of A and B (32 rows per stage,
+//     prefetched two stages ahead into registers; the column-major operands
+//     are K-major here), split them by truncation into the bf16 hi/mid/lo
+//     operand tiles and store those in the canonical K-major no-swizzle
+//     core-matrix layout (8 rows x 16 B);
+//   * thread 0 issues 8 part products (all but lo x lo, ~2^-32 relative) x 2
+//     K-steps of tcgen05.mma (M = 128, N = the B tile width <= 256, K = 16)
+//     into one TMEM accumulator and commits them to an mbarrier, so the split
+//     of the next stage overlaps the MMAs of this one (double-buffered);
+//   * epilogue: tcgen05.ld (32x32b) -- thread = output row -- to the chunk's
+//     partial, reduced GPU-wide by the deterministic combine of dense.cu.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mpb {
+namespace {
+
+constexpr int kTcM = 128;       // MMA M (output rows: columns of A)
+constexpr int kTcThreads = 256;  // producer warps; + 1 MMA-issue warp
+constexpr int kTcRing = 3;       // fp32 cp.async stages
+constexpr int kTcProducts = 8;   // all part products but lo x lo (~2^-32 relative)
+
+// Tile configuration: NMAX = widest B tile (MMA N), KC = rows of n per stage.
+// <128, 32> for narrow products; <256, 16> keeps a 240-wide S^T AS in one tile
+// (B read once per A tile) within shared memory.
+template <int NMAX, int KC>
+struct TcCfg {
+  static constexpr int kHQ = KC / 16;                      // float4-quads per column
+  static constexpr int kSlots = (kTcM + NMAX) / 8 * kHQ / (kTcThreads / 32);
+  static constexpr int kSbo = (KC / 8) * 128;              // core-matrix group step along M/N
+  static constexpr int kPartA = kTcM * KC * 2;             // one bf16 part of the A tile
+  static constexpr int kBufBytes = 3 * (kTcM + NMAX) * KC * 2;
+  static constexpr int kPitch = KC + 4;                    // fp32 ring column pitch (floats)
+  static constexpr int kRingBytes = kTcRing * (kTcM + NMAX) * kPitch * 4;
+  static constexpr int kSmem = 2 * kBufBytes + kRingBytes + 64;  // + 4 mbarriers, TMEM address
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// shared-memory matrix descriptor, K-major, no swizzle: core matrices of 8
+// rows x 16 B; lbo = byte step between core matrices along K, sbo = along M/N
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFF) |
+         (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);  // version 1 (sm_100)
+}
+
+// instruction descriptor: kind::f16, A/B bf16 (K-major), D fp32, M = 128, N
+__device__ __forceinline__ uint32_t idesc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(kTcM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+      smem_u32(bar)));
+}
+
+// x = hi + mid + lo exactly, each part a bfloat16 (its binary32 pattern has a
+// zero low half): truncation splits, so every step is an exact subtraction
+__device__ __forceinline__ void split3(float x, uint32_t& h, uint32_t& m, uint32_t& l) {
+  h = __float_as_uint(x) & 0xFFFF0000u;
+  const float r = x - __uint_as_float(h);
+  m = __float_as_uint(r) & 0xFFFF0000u;
+  l = __float_as_uint(r - __uint_as_float(m));
+}
+__device__ __forceinline__ uint32_t pack_hi(uint32_t a, uint32_t b) {  // bf16(a) | bf16(b) << 16
+  return __byte_perm(a, b, 0x7632);
+}
+
+template <int NMAX, int KC>
+__global__ void __launch_bounds__(kTcThreads + 32, 1)
+k_gram_tc(int64_t n, int ka, int kb, const float* __restrict__ A, int64_t lda,
+          const float* __restrict__ B, int64_t ldb, int64_t rows_per_chunk, int tiles_n, int ntile,
+          float* __restrict__ part, int nprod, int do_store) {
+  using Cf = TcCfg<NMAX, KC>;
+  constexpr int kTcSlots = Cf::kSlots, kTcSbo = Cf::kSbo, kTcPartA = Cf::kPartA;
+  constexpr int kTcBufBytes = Cf::kBufBytes, kTcPitch = Cf::kPitch, kTcRingBytes = Cf::kRingBytes;
+  constexpr int kTcNMax = NMAX, kTcKC = KC, kHQ = Cf::kHQ;
+  constexpr uint32_t kAcc1 = NMAX;  // TMEM column of the small-products accumulator
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  float* ring = reinterpret_cast<float*>(tsm + 2 * kTcBufBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm + 2 * kTcBufBytes + kTcRingBytes);  // split stored
+  uint64_t* empty = full + 2;                                             // stage MMAs done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full + 4);
+
+  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
+  const int i0 = tm * kTcM, j0 = tn * ntile;
+  const int N = ntile;  // MMA N (multiple of 16)
+  // Row blocks of kTcKC rows are dealt round-robin to the chunks (chunk c
+  // takes blocks c, c + nchunk, ...): at any moment every SM streams the same
+  // window of rows, so the operands' pages (one per column of a tall
+  // column-major block) are shared GPU-wide instead of one set per chunk.
+  const int64_t nchunk = gridDim.y;
+  const int64_t r_end = n;
+  (void)rows_per_chunk;
+  auto stage_row = [&](int st) -> int64_t {
+    return (static_cast<int64_t>(st) * nchunk + blockIdx.y) * kTcKC;
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(2 * kTcNMax));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], kTcThreads);
+    mbar_init(&full[1], kTcThreads);
+    mbar_init(&empty[0], 1);
+    mbar_init(&empty[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  // never-written columns (beyond ka / kb) of both split buffers stay zero
+  for (int e = threadIdx.x; e < 2 * kTcBufBytes / 16; e += blockDim.x)
+    reinterpret_cast<uint4*>(tsm)[e] = make_uint4(0, 0, 0, 0);
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = *tmem_slot;
+
+  // Work items: (8-column group g, row half hq) -> one warp instruction.  Lane
+  // l: column g*8 + (l & 7), float4 index ch = (l >> 3) + 4 hq (rows 4ch..4ch+3
+  // of the stage): a lane octet reads 64 contiguous bytes of one column, and
+  // the 32 lanes' 8-byte bf16 stores land on 256 contiguous bytes of a core
+  // matrix pair (conflict-free).
+  const int ncols = kTcM + N;
+  const int nitems = ncols / 8 * kHQ;
+  const int cl = lane & 7, jl = lane >> 3;
+  const float* src[kTcSlots];
+  int soff[kTcSlots];  // byte offset of the 8-byte store inside one part
+  int sprt[kTcSlots];  // part stride (bytes) of this column's operand
+  int roff[kTcSlots];  // float offset of the item in one ring stage
+  int rrow[kTcSlots];  // row of the item inside the stage (4 ch)
+#pragma unroll
+  for (int q = 0; q < kTcSlots; ++q) {
+    const int it = warp + (kTcThreads / 32) * q;
+    src[q] = nullptr;
+    soff[q] = sprt[q] = roff[q] = rrow[q] = 0;
+    if (it < nitems) {
+      const int g = it / kHQ, hq = it % kHQ;
+      const int col = g * 8 + cl, ch = jl + 4 * hq;
+      const bool isa = col < kTcM;
+      const int c = isa ? col : col - kTcM;
+      const int gc = isa ? i0 + c : j0 + c;
+      if (gc < (isa ? ka : kb))
+        src[q] = isa ? A + static_cast<int64_t>(gc) * lda : B + static_cast<int64_t>(gc) * ldb;
+      // A parts at 0, 1, 2 x kTcPartA; B parts after them, N * kTcKC * 2 apart
+      soff[q] = (isa ? 0 : 3 * kTcPartA) + (c >> 3) * kTcSbo + (ch >> 1) * 128 + (c & 7) * 16 +
+                (ch & 1) * 8;
+      sprt[q] = isa ? kTcPartA : N * kTcKC * 2;
+      roff[q] = col * kTcPitch + 4 * ch;
+      rrow[q] = 4 * ch;
+    }
+  }
+  // Each thread stages (cp.async) exactly the items it later splits, so the
+  // ring needs no CTA barrier: cp.async.wait_group orders each thread's own data.
+  auto fetch = [&](int slot, int64_t row0) {
+    float* rs = ring + slot * (kTcM + kTcNMax) * kTcPitch;
+#pragma unroll
+    for (int q = 0; q < kTcSlots; ++q) {
+      if (!src[q]) continue;
+      const int64_t row = row0 + rrow[q];
+      int bytes = 0;
+      if (row < r_end) bytes = static_cast<int>(r_end - row < 4 ? r_end - row : 4) * 4;
+      const float* p = bytes ? src[q] + row : src[q];
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(rs + roff[q])),
+                   "l"(p), "r"(bytes));
+    }
+    asm volatile("cp.async.commit_group;\n");
+  };
+  auto store = [&](int slot, unsigned char* buf) {
+    const float* rs = ring + slot * (kTcM + kTcNMax) * kTcPitch;
+#pragma unroll
+    for (int q = 0; q < kTcSlots; ++q) {
+      if (!src[q]) continue;  // padding column: stays zero
+      const float4 v = *reinterpret_cast<const float4*>(rs + roff[q]);
+      uint32_t h0, m0, l0, h1, m1, l1, h2, m2, l2, h3, m3, l3;
+      split3(v.x, h0, m0, l0);
+      split3(v.y, h1, m1, l1);
+      split3(v.z, h2, m2, l2);
+      split3(v.w, h3, m3, l3);
+      unsigned char* d = buf + soff[q];
+      *reinterpret_cast<uint2*>(d) = make_uint2(pack_hi(h0, h1), pack_hi(h2, h3));
+      *reinterpret_cast<uint2*>(d + sprt[q]) = make_uint2(pack_hi(m0, m1), pack_hi(m2, m3));
+      *reinterpret_cast<uint2*>(d + 2 * sprt[q]) = make_uint2(pack_hi(l0, l1), pack_hi(l2, l3));
+    }
+  };
+
+  const int64_t nblk = (n + kTcKC - 1) / kTcKC;
+  static_assert(kTcKC % 16 == 0, "stage rows: whole MMA K-steps");
+  const int nst = static_cast<int>(blockIdx.y < nblk ? (nblk - blockIdx.y + nchunk - 1) / nchunk : 0);
+  const uint32_t idesc = idesc_bf16(N);
+  const int part_b = N * kTcKC * 2;
+  if (warp == kTcThreads / 32) {
+    // MMA issue warp: one elected lane per stage, full -> MMAs -> commit(empty)
+    if (lane == 0) {
+      for (int st = 0; st < nst; ++st) {
+        const int buf = st & 1;
+        mbar_wait(&full[buf], (st >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        const uint32_t a0 = smem_u32(tsm + buf * kTcBufBytes), b0 = a0 + 3 * kTcPartA;
+        // part pairs (hi, mid, lo) x (hi, mid, lo) without lo x lo
+        constexpr int pa_of[kTcProducts] = {0, 0, 1, 0, 1, 2, 1, 2};
+        constexpr int pb_of[kTcProducts] = {0, 1, 0, 2, 1, 0, 2, 1};
+#pragma unroll
+        for (int pr = 0; pr < kTcProducts; ++pr)
+#pragma unroll
+          for (int kk = 0; kk < kTcKC / 16; ++kk) {
+            if (pr >= nprod) continue;
+            const uint64_t ad = umma_desc(a0 + pa_of[pr] * kTcPartA + kk * 256, 128, kTcSbo);
+            const uint64_t bd = umma_desc(b0 + pb_of[pr] * part_b + kk * 256, 128, kTcSbo);
+            // hi x hi into accumulator 0; the small part products into
+            // accumulator 1, so the tensor core's accumulation rounding acts
+            // on each sum at its own magnitude (summed once in the epilogue)
+            if (pr == 0)
+              mma_bf16(tmem, ad, bd, idesc, (st | kk) != 0);
+            else
+              mma_bf16(tmem + kAcc1, ad, bd, idesc, (st | (pr - 1) | kk) != 0);
+          }
+        mma_commit(&empty[buf]);
+      }
+    }
+  } else {
+    // producer warps: prefetch stage st+2 -> wait for stage st's data and for
+    // the MMAs of stage st-2 (empty) -> split + store -> arrive(full)
+    for (int q = 0; q < kTcRing - 1; ++q)
+      if (q < nst) fetch(q, stage_row(q));
+      else asm volatile("cp.async.commit_group;\n");
+    for (int st = 0; st < nst; ++st) {
+      const int buf = st & 1;
+      if (st + kTcRing - 1 < nst)
+        fetch((st + kTcRing - 1) % kTcRing, stage_row(st + kTcRing - 1));
+      else
+        asm volatile("cp.async.commit_group;\n");
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kTcRing - 1));
+      if (st >= 2) mbar_wait(&empty[buf], ((st >> 1) - 1) & 1);  // MMAs of stage st-2 done
+      if (do_store) store(st % kTcRing, tsm + buf * kTcBufBytes);
+      asm volatile("fence.proxy.async.shared::cta;\n");
+      mbar_arrive(&full[buf]);
+    }
+    if (nst >= 1) mbar_wait(&empty[(nst - 1) & 1], ((nst - 1) >> 1) & 1);
+    if (nst >= 2) mbar_wait(&empty[(nst - 2) & 1], ((nst - 2) >> 1) & 1);
+  }
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+
+  // epilogue (producer warps): TMEM lane = output row; warp w reads lane
+  // quarter w % 4 and the column half w / 4 (8 columns per tcgen05.ld)
+  if (warp < kTcThreads / 32) {
+  float* out = part + static_cast<int64_t>(blockIdx.y) * ka * kb;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int i = i0 + 32 * quarter + lane;
+  const int cbeg = half * (N / 2), cend = cbeg + N / 2;
+  for (int c0 = cbeg; c0 < cend; c0 += 8) {
+    uint32_t v[8], w[8];
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + c0;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                   "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
+                   "=r"(w[6]), "=r"(w[7])
+                 : "r"(taddr + kAcc1));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+    if (i < ka) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = j0 + c0 + q;
+        if (j < kb && c0 + q < N)
+          out[i + static_cast<int64_t>(j) * ka] = __uint_as_float(v[q]) + __uint_as_float(w[q]);
+      }
+    }
+  }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "r"(2 * kTcNMax));
+}
+
+
+// ---- Y = beta Z + alpha A C on tcgen05 ---------------------------------------
+// CTA = 128 rows of Y (MMA M) x one N-wide column tile (N <= 128); K (= k,
+// the columns of A) in stages of 32.  A's tile is M-contiguous in memory, so
+// its bf16 parts go to the MN-major core-matrix layout (8 K-rows x 16 B of 8
+// consecutive rows); C's columns are K-contiguous (K-major, as in the Gram).
+constexpr int kGmN = 128, kGmKC = 32;
+constexpr int kGmApitch = kTcM + 4;    // fp32 ring: A [k][128 rows]
+constexpr int kGmCpitch = kGmKC + 4;   // fp32 ring: C [col][32 k]
+constexpr int kGmRingStage = kGmKC * kGmApitch + kGmN * kGmCpitch;  // floats
+constexpr int kGmPartA = kTcM * kGmKC * 2, kGmPartC = kGmN * kGmKC * 2;
+constexpr int kGmBuf = 3 * (kGmPartA + kGmPartC);
+constexpr int kGmSmem = 2 * kGmBuf + kTcRing * kGmRingStage * 4 + 64;
+constexpr int kGmAItems = kGmKC * (kTcM / 4) / kTcThreads;  // float4 of A per thread per stage
+constexpr int kGmCSlots = kGmN / 8 * 2 / (kTcThreads / 32);  // C items per thread (Gram mapping)
+constexpr int kGmSplitA = kGmKC * (kTcM / 8) / kTcThreads;   // (k, 8-row group) items per thread
+
+__global__ void __launch_bounds__(kTcThreads + 32, 1)
+k_gemm_tc(int64_t n, int k, int c, int ntile, int tiles_n, int64_t ntiles, float alpha,
+          const float* __restrict__ A, int64_t lda, const float* __restrict__ Cm, int64_t ldc,
+          float beta, const float* Z, int64_t ldz, float* Y, int64_t ldy,
+          const float* __restrict__ A2, float* Y2) {
+  if (blockIdx.z) {
+    A = A2;
+    Y = Y2;
+  }
+  extern __shared__ __align__(1024) unsigned char gsm[];
+  float* ring = reinterpret_cast<float*>(gsm + 2 * kGmBuf);
+  uint64_t* full = reinterpret_cast<uint64_t*>(gsm + 2 * kGmBuf + kTcRing * kGmRingStage * 4);
+  uint64_t* empty = full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full + 4);
+  const int N = ntile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t kAcc1 = kGmN;  // TMEM column of the small-products accumulator
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(2 * kGmN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], kTcThreads);
+    mbar_init(&full[1], kTcThreads);
+    mbar_init(&empty[0], 1);
+    mbar_init(&empty[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  for (int e = threadIdx.x; e < 2 * kGmBuf / 16; e += blockDim.x)
+    reinterpret_cast<uint4*>(gsm)[e] = make_uint4(0, 0, 0, 0);
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = *tmem_slot;
+  const int nst = (k + kGmKC - 1) / kGmKC;
+  // persistent: this CTA's tiles are blockIdx.x, + gridDim.x, ...; the stage
+  // pipeline runs over the flattened (tile, K stage) sequence
+  const int64_t my_tiles =
+      blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t total = my_tiles * nst;
+  // instruction descriptor: bf16 x bf16 -> f32, A MN-major (bit 15), B K-major
+  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
+                         (static_cast<uint32_t>(N >> 3) << 17) |
+                         (static_cast<uint32_t>(kTcM >> 4) << 24);
+
+  if (warp == kTcThreads / 32) {
+    if (lane == 0) {
+      for (int64_t g = 0; g < total; ++g) {
+        const int buf = static_cast<int>(g & 1);
+        const int st = static_cast<int>(g % nst);
+        mbar_wait(&full[buf], static_cast<uint32_t>((g >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        const uint32_t a0 = smem_u32(gsm + buf * kGmBuf), c0 = a0 + 3 * kGmPartA;
+        constexpr int pa_of[kTcProducts] = {0, 0, 1, 0, 1, 2, 1, 2};
+        constexpr int pb_of[kTcProducts] = {0, 1, 0, 2, 1, 0, 2, 1};
+#pragma unroll
+        for (int pr = 0; pr < kTcProducts; ++pr)
+#pragma unroll
+          for (int kk = 0; kk < kGmKC / 16; ++kk) {
+            // A: MN-major, k-groups (8 k) 128 B apart (lbo), row groups 512 B (sbo)
+            const uint64_t ad = umma_desc(a0 + pa_of[pr] * kGmPartA + kk * 256, 128, 512);
+            const uint64_t bd = umma_desc(c0 + pb_of[pr] * kGmPartC + kk * 256, 128, 512);
+            // hi x hi into accumulator 0; the small part products into
+            // accumulator 1, so the tensor core's accumulation rounding acts
+            // on each sum at its own magnitude (summed once in the epilogue)
+            if (pr == 0)
+              mma_bf16(tmem, ad, bd, idesc, (st | kk) != 0);
+            else
+              mma_bf16(tmem + kAcc1, ad, bd, idesc, (st | (pr - 1) | kk) != 0);
+          }
+        mma_commit(&empty[buf]);
+      }
+    }
+  } else {
+    const int cl = lane & 7, jl = lane >> 3;
+    // C items of this thread (the Gram's K-major mapping), per column tile
+    int ccol[kGmCSlots], coff[kGmCSlots], croff[kGmCSlots], cch[kGmCSlots];
+#pragma unroll
+    for (int q = 0; q < kGmCSlots; ++q) {
+      const int it = warp + (kTcThreads / 32) * q;
+      const int g = it >> 1, hq = it & 1;
+      const int col = 8 * g + cl, ch = jl + 4 * hq;
+      ccol[q] = col;
+      coff[q] = (col >> 3) * 512 + (ch >> 1) * 128 + (col & 7) * 16 + (ch & 1) * 8;
+      croff[q] = kGmKC * kGmApitch + col * kGmCpitch + 4 * ch;
+      cch[q] = 4 * ch;
+    }
+    auto tile_of = [&](int64_t g) { return blockIdx.x + (g / nst) * gridDim.x; };
+    auto fetch = [&](int slot, int64_t g) {
+      float* rs = ring + slot * kGmRingStage;
+      const int64_t t = tile_of(g);
+      const int64_t i0 = (t / tiles_n) * kTcM;
+      const int j0 = static_cast<int>(t % tiles_n) * N;
+      const int k0 = static_cast<int>(g % nst) * kGmKC;
+#pragma unroll
+      for (int q = 0; q < kGmAItems; ++q) {
+        const int e = threadIdx.x + kTcThreads * q;
+        const int kc = e / (kTcM / 4), ch = e % (kTcM / 4);
+        const int64_t row = i0 + 4 * ch;
+        int bytes = 0;
+        if (k0 + kc < k && row < n) bytes = static_cast<int>(n - row < 4 ? n - row : 4) * 4;
+        const float* p = bytes ? A + row + static_cast<int64_t>(k0 + kc) * lda : A;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                         smem_u32(rs + kc * kGmApitch + 4 * ch)),
+                     "l"(p), "r"(bytes));
+      }
+#pragma unroll
+      for (int q = 0; q < kGmCSlots; ++q) {
+        if (ccol[q] >= N) continue;
+        const int kr = k0 + cch[q];
+        const int j = j0 + ccol[q];
+        int bytes = 0;
+        if (kr < k && j < c) bytes = (k - kr < 4 ? k - kr : 4) * 4;
+        const float* p = bytes ? Cm + kr + static_cast<int64_t>(j) * ldc : Cm;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(rs + croff[q])),
+                     "l"(p), "r"(bytes));
+      }
+      asm volatile("cp.async.commit_group;\n");
+    };
+    auto store = [&](int slot, unsigned char* buf) {
+      const float* rs = ring + slot * kGmRingStage;
+      // A -> MN-major: item (k, 8-row group gm): 8 consecutive rows of column k
+#pragma unroll
+      for (int q = 0; q < kGmSplitA; ++q) {
+        const int e = threadIdx.x + kTcThreads * q;
+        const int kc = e % kGmKC, gm = e / kGmKC;
+        const float4 v0 = *reinterpret_cast<const float4*>(rs + kc * kGmApitch + 8 * gm);
+        const float4 v1 = *reinterpret_cast<const float4*>(rs + kc * kGmApitch + 8 * gm + 4);
+        const float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        uint32_t h[8], m[8], l[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) split3(f[t], h[t], m[t], l[t]);
+        const int off = gm * 512 + (kc >> 3) * 128 + (kc & 7) * 16;
+        *reinterpret_cast<uint4*>(buf + off) =
+            make_uint4(pack_hi(h[0], h[1]), pack_hi(h[2], h[3]), pack_hi(h[4], h[5]), pack_hi(h[6], h[7]));
+        *reinterpret_cast<uint4*>(buf + kGmPartA + off) =
+            make_uint4(pack_hi(m[0], m[1]), pack_hi(m[2], m[3]), pack_hi(m[4], m[5]), pack_hi(m[6], m[7]));
+        *reinterpret_cast<uint4*>(buf + 2 * kGmPartA + off) =
+            make_uint4(pack_hi(l[0], l[1]), pack_hi(l[2], l[3]), pack_hi(l[4], l[5]), pack_hi(l[6], l[7]));
+      }
+      unsigned char* cb = buf + 3 * kGmPartA;
+#pragma unroll
+      for (int q = 0; q < kGmCSlots; ++q) {
+        if (ccol[q] >= N) continue;
+        const float4 v = *reinterpret_cast<const float4*>(rs + croff[q]);
+        uint32_t h0, m0, l0, h1, m1, l1, h2, m2, l2, h3, m3, l3;
+        split3(v.x, h0, m0, l0);
+        split3(v.y, h1, m1, l1);
+        split3(v.z, h2, m2, l2);
+        split3(v.w, h3, m3, l3);
+        unsigned char* d = cb + coff[q];
+        *reinterpret_cast<uint2*>(d) = make_uint2(pack_hi(h0, h1), pack_hi(h2, h3));
+        *reinterpret_cast<uint2*>(d + kGmPartC) = make_uint2(pack_hi(m0, m1), pack_hi(m2, m3));
+        *reinterpret_cast<uint2*>(d + 2 * kGmPartC) = make_uint2(pack_hi(l0, l1), pack_hi(l2, l3));
+      }
+    };
+    auto epilogue = [&](int64_t t) {
+      const int64_t i0 = (t / tiles_n) * kTcM;
+      const int j0 = static_cast<int>(t % tiles_n) * N;
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      // TMEM lane = row of the tile; warp w: lane quarter w % 4, column half w / 4
+      const int quarter = warp & 3, half = warp >> 2;
+      const int64_t i = i0 + 32 * quarter + lane;
+      const int cbeg = half * (N / 2), cend = cbeg + N / 2;
+      for (int cc = cbeg; cc < cend; cc += 16) {
+        // 16 columns: both TMEM loads and every Z load in flight before use
+        uint32_t v[16];
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + cc;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                       "=r"(v[6]), "=r"(v[7])
+                     : "r"(taddr));
+        if (cc + 8 < cend)
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                       : "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                         "=r"(v[14]), "=r"(v[15])
+                       : "r"(taddr + 8));
+        uint32_t w[16];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
+                       "=r"(w[6]), "=r"(w[7])
+                     : "r"(taddr + kAcc1));
+        if (cc + 8 < cend)
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                       : "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]),
+                         "=r"(w[14]), "=r"(w[15])
+                       : "r"(taddr + kAcc1 + 8));
+        float z[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int j = j0 + cc + q;
+          z[q] = (beta != 0.f && i < n && j < c && cc + q < cend) ? Z[i + static_cast<int64_t>(j) * ldz] : 0.f;
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+        if (i < n) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int j = j0 + cc + q;
+            if (j < c && cc + q < cend) {
+              float y = alpha * (__uint_as_float(v[q]) + __uint_as_float(w[q]));
+              if (beta != 0.f) y = fmaf(beta, z[q], y);
+              Y[i + static_cast<int64_t>(j) * ldy] = y;
+            }
+          }
+        }
+      }
+      // the next tile's first MMA overwrites the accumulator: order these reads first
+      asm volatile("tcgen05.fence::before_thread_sync;\n");
+    };
+    for (int q = 0; q < kTcRing - 1; ++q)
+      if (q < total) fetch(q, q);
+      else asm volatile("cp.async.commit_group;\n");
+    for (int64_t g = 0; g < total; ++g) {
+      const int buf = static_cast<int>(g & 1);
+      if (g + kTcRing - 1 < total)
+        fetch(static_cast<int>((g + kTcRing - 1) % kTcRing), g + kTcRing - 1);
+      else
+        asm volatile("cp.async.commit_group;\n");
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kTcRing - 1));
+      // the A tile is shared by all producers (row groups x k): a barrier
+      // makes every thread's cp.async data visible before the split reads it
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kTcThreads));
+      if (g >= 2) mbar_wait(&empty[buf], static_cast<uint32_t>(((g >> 1) - 1) & 1));
+      store(static_cast<int>(g % kTcRing), gsm + buf * kGmBuf);
+      asm volatile("fence.proxy.async.shared::cta;\n");
+      mbar_arrive(&full[buf]);
+      // the ring slot read here is refilled two stages later: order the reads
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kTcThreads));
+      if (g % nst == nst - 1) {
+        // last K stage of a tile: its MMAs done -> epilogue
+        mbar_wait(&empty[buf], static_cast<uint32_t>((g >> 1) & 1));
+        epilogue(tile_of(g));
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "r"(2 * kGmN));
+}
+
+}  // namespace
+
+int g_gram_tc = 1, g_gemm_tc = 1;
+int g_tc_nprod = kTcProducts, g_tc_store = 1;  // experiment knobs
+
+bool gram_tc_eligible(int64_t n, int64_t ka, int64_t kb, int64_t lda, int64_t ldb, const float* A,
+                      const float* B) {
+  return n >= 32 && (lda % 4 == 0) && (ldb % 4 == 0) &&
+         (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
+         ka >= 1 && kb >= 1;
+}
+
+// Chunk partials of G = A^T B (ka x kb each, column-major, ld ka) into part,
+// nchunk row chunks; returns nchunk (the caller's deterministic combine sums them).
+int64_t gram_tc_f32(int64_t n, int64_t ka, const float* A, int64_t lda, int64_t kb, const float* B,
+                    int64_t ldb, int64_t max_chunks, float* part, cudaStream_t s) {
+  auto go = [&](auto nmax_tag, auto kc_tag) -> int64_t {
+    constexpr int NMAX = decltype(nmax_tag)::value, KC = decltype(kc_tag)::value;
+    const int64_t tiles_m = ceil_div(ka, kTcM);
+    const int64_t tiles_n = ceil_div(kb, NMAX);
+    const int64_t ntile = round_up(ceil_div(kb, tiles_n), 16);  // MMA N: multiple of 16
+    const int64_t tiles = tiles_m * tiles_n;
+    int64_t nchunk = std::max<int64_t>(1, kNumSMs / tiles);
+    nchunk = std::min(nchunk, std::max<int64_t>(1, max_chunks));
+    nchunk = std::min(nchunk, ceil_div(n, KC));
+    constexpr int smem = TcCfg<NMAX, KC>::kSmem;
+    smem_opt_in(reinterpret_cast<const void*>(k_gram_tc<NMAX, KC>), smem);
+    const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(nchunk));
+    k_gram_tc<NMAX, KC><<<grid, kTcThreads + 32, smem, s>>>(
+        n, static_cast<int>(ka), static_cast<int>(kb), A, lda, B, ldb, 0, static_cast<int>(tiles_n),
+        static_cast<int>(ntile), part, g_tc_nprod, g_tc_store);
+    MPB_LAUNCH_CHECK();
+    return nchunk;
+  };
+  if (kb <= 128) return go(std::integral_constant<int, 128>(), std::integral_constant<int, 32>());
+  return go(std::integral_constant<int, 256>(), std::integral_constant<int, 16>());
+}
+
+bool gemm_tc_eligible(int64_t n, int64_t k, int64_t c, int64_t lda, int64_t ldc, const float* A,
+                      const float* C) {
+  return n >= kTcM && k >= 1 && c >= 1 && (lda % 4 == 0) && (ldc % 4 == 0) &&
+         (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
+}
+
+void gemm_tc_f32(int64_t n, int64_t k, int64_t c, float alpha, const float* A, int64_t lda,
+                 const float* C, int64_t ldc, float beta, const float* Z, int64_t ldz, float* Y,
+                 int64_t ldy, const float* A2, float* Y2, cudaStream_t s) {
+  const int64_t tiles_n = ceil_div(c, kGmN);
+  const int64_t ntile = round_up(ceil_div(c, tiles_n), 16);
+  const int64_t tiles = ceil_div(n, kTcM) * tiles_n;
+  smem_opt_in(reinterpret_cast<const void*>(k_gemm_tc), kGmSmem);
+  // persistent: one CTA per SM (per product of the pair)
+  const int64_t ctas = std::min<int64_t>(tiles, A2 ? kNumSMs / 2 : kNumSMs);
+  const dim3 grid(static_cast<unsigned>(ctas), 1, A2 ? 2u : 1u);
+  k_gemm_tc<<<grid, kTcThreads + 32, kGmSmem, s>>>(n, static_cast<int>(k), static_cast<int>(c),
+                                                   static_cast<int>(ntile), static_cast<int>(tiles_n),
+                                                   tiles, alpha, A, lda, C, ldc, beta, Z, ldz, Y, ldy,
+                                                   A2, Y2);
+  MPB_LAUNCH_CHECK();
+}
+
+}  // namespace mpb

@@ -77,7 +77,19 @@ def capped(name, variant, iters):
                     "ms_per_launch": round(v["ms"] / v["count"], 4),
                     "GBps": round(v["bytes"] / (v["ms"] * 1e6), 1) if v["bytes"] > 0 and v["ms"] > 0 else None,
                     "TFps": round(v["flops"] / (v["ms"] * 1e9), 2) if v["flops"] > 0 and v["ms"] > 0 else None}
+    # per-stage iteration times from the host arrival of the per-iteration records
+    cfg2 = mp.SolverConfig(k=c["k"], block=c["block"], tol=1e-10, maxit=2 * iters, variant=variant)
+    rh = mp.solve(A, cfg2, want_X=False, history=True)
+    per_stage = {}
+    h = rh.history
+    for st in sorted({x.stage for x in h}):
+        ts = [x.host_time for x in h if x.stage == st]
+        if len(ts) > 2:
+            d = np.diff(ts)[1:]  # skip the stage's first (setup) interval
+            per_stage["fp32" if st == 1 else "fp64"] = {"ms_per_iteration_median": 1e3 * float(np.median(d)),
+                                                        "iterations": len(d)}
     return {"variant": variant, "iterations": [r.iterations_lower, r.iterations_working],
+            "per_stage_from_records": per_stage,
             "method": f"(t[{2 * iters}/stage] - t[{iters}/stage]) / extra iterations",
             "ms_per_iteration": 1e3 * dt / max(di, 1), "iters_per_s": di / dt,
             "kernels_profiling_pass": kern}

@@ -166,6 +166,43 @@ def test_gram(gpu, n, ka, kb, dtype):
     assert np.all(np.abs(G - Gr) <= 16 * u * np.sqrt(n) * scale + 1e-300)
 
 
+@pytest.mark.parametrize("n,ka,kb", [(70001, 240, 240), (50000, 160, 80), (40003, 80, 80),
+                                     (30000, 96, 48), (20011, 200, 130), (1000, 16, 16),
+                                     (4099, 130, 7)])
+def test_gram_f32_tensor_cores(gpu, n, ka, kb):
+    """The binary32 Gram on tcgen05 (tc.cu, forced for every shape): the exact
+    3-way bf16 split + fp32 accumulation matches the float64 product within the
+    binary32 dot-product bound, and agrees with the SIMT FFMA kernel to the
+    same level."""
+    mp = gpu
+    import torch
+    A, B = rand(n, ka, 19, np.float32), rand(n, kb, 20, np.float32)
+    A[::97, :] *= 1e-3  # dynamic range inside a column
+    ctx = mp.default_context()
+    Ad = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    Bd = torch.from_numpy(np.ascontiguousarray(B.T)).cuda()
+    out = {}
+    for opt in (2, 0):
+        assert ctx.lib.mpeig_set_process_option(b"gram_tc", opt) == 0
+        try:
+            Gd = torch.zeros((kb, ka), dtype=torch.float32, device="cuda")
+            ctx.check(ctx.lib.mpeig_gram_f32(ctx.h, n, ka, C.c_void_p(Ad.data_ptr()), n, kb,
+                                             C.c_void_p(Bd.data_ptr()), n, C.c_void_p(Gd.data_ptr())))
+            out[opt] = Gd.cpu().numpy().T.astype(np.float64)
+        finally:
+            ctx.lib.mpeig_set_process_option(b"gram_tc", 1)
+    A64, B64 = A.astype(np.float64), B.astype(np.float64)
+    Gr = A64.T @ B64
+    bound = 16 * 2.0 ** -24 * np.sqrt(n) * np.sqrt(np.outer((A64 * A64).sum(0), (B64 * B64).sum(0)))
+    assert np.all(np.abs(out[2] - Gr) <= bound)
+    assert np.all(np.abs(out[2] - out[0]) <= 2 * bound)
+    # as accurate as the FFMA kernel (the tensor core's accumulation rounding
+    # must not add up over the part products: ADR in tc.cu)
+    sc = np.abs(A64).T @ np.abs(B64)
+    e_tc, e_simt = np.max(np.abs(out[2] - Gr) / sc), np.max(np.abs(out[0] - Gr) / sc)
+    assert e_tc <= 1.5 * e_simt + 2 * 2.0 ** -24, (e_tc, e_simt)
+
+
 GEMM_SHAPES = [(50001, 96, 70), (40000, 240, 160), (30001, 160, 80), (20000, 80, 80),
                (10007, 144, 96), (5000, 48, 48)]
 
@@ -190,6 +227,41 @@ def test_gemm(gpu, n, k, c, dtype):
     Yr = Z.astype(np.float64) - A.astype(np.float64) @ Cm.astype(np.float64)
     bound = 4 * u * (np.abs(A).astype(np.float64) @ np.abs(Cm).astype(np.float64) + np.abs(Z)) * k
     assert np.all(np.abs(Y - Yr) <= bound)
+
+
+@pytest.mark.parametrize("n,k,c", [(40000, 240, 160), (30001, 160, 80), (20000, 80, 80),
+                                   (10007, 144, 96), (5000, 48, 48), (4099, 37, 13),
+                                   (1000, 16, 200)])
+@pytest.mark.parametrize("beta", [0.0, 1.0])
+def test_gemm_f32_tensor_cores(gpu, n, k, c, beta):
+    """The binary32 block update on tcgen05 (tc.cu, forced for every shape):
+    exact 3-way bf16 split, fp32 accumulation; against float64 and against the
+    SIMT FFMA kernel, with and without the beta Z term."""
+    mp = gpu
+    import torch
+    A, Cm, Z = rand(n, k, 31, np.float32), rand(k, c, 32, np.float32), rand(n, c, 33, np.float32)
+    ctx = mp.default_context()
+    dev = lambda M: torch.from_numpy(np.ascontiguousarray(M.T)).cuda()  # noqa: E731
+    Ad, Cd = dev(A), dev(Cm)
+    out = {}
+    for opt in (2, 0):
+        assert ctx.lib.mpeig_set_process_option(b"gemm_tc", opt) == 0
+        try:
+            Zd = dev(Z)
+            Yd = torch.zeros_like(Zd)
+            ctx.check(ctx.lib.mpeig_gemm_f32(ctx.h, n, k, c, -1.0, C.c_void_p(Ad.data_ptr()), n,
+                                             C.c_void_p(Cd.data_ptr()), k, beta,
+                                             C.c_void_p(Zd.data_ptr()), n, C.c_void_p(Yd.data_ptr()), n))
+            out[opt] = Yd.cpu().numpy().T.astype(np.float64)
+        finally:
+            ctx.lib.mpeig_set_process_option(b"gemm_tc", 1)
+    Yr = beta * Z.astype(np.float64) - A.astype(np.float64) @ Cm.astype(np.float64)
+    sc = np.abs(A).astype(np.float64) @ np.abs(Cm).astype(np.float64) + np.abs(Z)
+    bound = 4 * 2.0 ** -24 * sc * k
+    assert np.all(np.abs(out[2] - Yr) <= bound)
+    assert np.all(np.abs(out[2] - out[0]) <= 2 * bound)
+    e_tc, e_simt = np.max(np.abs(out[2] - Yr) / sc), np.max(np.abs(out[0] - Yr) / sc)
+    assert e_tc <= 1.5 * e_simt + 2 * 2.0 ** -24, (e_tc, e_simt)
 
 
 def test_gemm_inplace_wide_is_refused(gpu):

@@ -146,6 +146,20 @@ def test_large_block_parity(gpu, name):
     check_parity(g, cfg, r, name)
 
 
+@pytest.mark.parametrize("name", ["lap3d16-mplobpcg-schol", "lap2d64k32-mplobpcg-schol"])
+def test_tensor_core_fp32_stage_parity(gpu, name):
+    """The fp32 stage with every Gram and block update on the tcgen05 path
+    (forced; by default it serves products with n k c >= 2^28, i.e. the
+    north-star sizes): same parity bar against the reference."""
+    ctx = gpu.default_context()
+    assert ctx.lib.mpeig_set_process_option(b"tc", 2) == 0
+    try:
+        g, cfg, r = run_case(gpu, name)
+    finally:
+        ctx.lib.mpeig_set_process_option(b"tc", 1)
+    check_parity(g, cfg, r, name)
+
+
 def test_large_block_pinvit_capped(gpu):
     """PINVIT at m = 48 capped at 150 iterations (cfg2's PINVIT arm): the same
     iteration count and Ritz values as the reference's capped run."""
