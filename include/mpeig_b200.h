@@ -154,8 +154,8 @@ void* mpeig_ctx_stream(mpeig_ctx* ctx);
  *                 repeated on the careful path with the reference's QR);
  *                 0: the TSQR-based QR in the speculative body too.  Same
  *                 results to rounding (not bitwise).
- *   "syev_method", "ql_exact": eigensolver variants for experiments
- *                 (process-wide; default 0) */
+ *   "ql_exact"    QL rotation formulas of the one-CTA Rayleigh-Ritz
+ *                 eigensolver (-1 default; see syev.cu); per context */
 int mpeig_ctx_set_option(mpeig_ctx* ctx, const char* key, int value);
 /* speculative iterations this context repeated on the careful path (a
  * breakdown or a failed guard inside the speculative body) */

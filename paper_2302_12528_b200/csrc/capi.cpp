@@ -220,9 +220,7 @@ int mpeig_ctx_set_option(mpeig_ctx* ctx, const char* key, int value) {
   else if (k == "spec_mode") ctx->spec_mode = value;
   else if (k == "use_graphs") ctx->use_graphs = value;
   else if (k == "spec_qr") ctx->spec_qr = value;
-  else if (k == "syev_method") g_syev_method = value;
-  else if (k == "ql_exact") g_ql_exact = value;
-  else if (k == "ql_f32") g_ql_f32 = value;
+  else if (k == "ql_exact") ctx->ql_exact = value;
   else return MPEIG_E_CONFIG;
   return MPEIG_OK;
 }

@@ -33,6 +33,7 @@ struct mpeig_ctx {
   int spec_mode = 1;            // speculative iteration (1 host sync / iteration)
   int use_graphs = 1;           // replay the steady-state iteration as a CUDA graph
   int spec_qr = 10;             // speculative body's QR: k > 0 guarded CholQR2 (fp64 guard 1e-k), 0 TSQR
+  int ql_exact = -1;            // QL rotation formulas of the one-CTA eigensolver (syev.cu)
   int64_t spec_rollbacks = 0;   // speculative iterations repeated on the careful path
   mpb::Comm* comm = nullptr;    // row-sharded mode (owned), nullptr: single GPU
 };

@@ -175,14 +175,11 @@ constexpr int64_t kSyevMax = 96;
 template <typename T>
 bool small_syev_supported(int64_t s);
 template <typename T>
-void small_syev(int64_t s, T* G, int64_t ldg, T* vals, int* info, cudaStream_t st);
+void small_syev(int64_t s, T* G, int64_t ldg, T* vals, int* info, cudaStream_t st, int exact = -1);
 // same, with per-phase clock64 counters (tridiag, QL, sort, sweeps, chain) into prof
 template <typename T>
 void small_syev_prof(int64_t s, T* G, int64_t ldg, T* vals, int* info, long long* prof,
-                     cudaStream_t st);
-extern int g_ql_exact;
-extern int g_ql_f32;
-extern int g_syev_method;  // 0: tridiagonal + QL (default), 1: tridiagonal + Jacobi
+                     cudaStream_t st, int exact = -1);
 
 // ------------------------------------------------------------------ TSQR
 // R factor (m x m, upper, positive diagonal) of a tall n x m block by a

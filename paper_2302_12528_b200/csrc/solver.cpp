@@ -654,7 +654,7 @@ template <typename T>
 void small_eig(Work<T>& w, int64_t sdim, T* G, int64_t ldg, T* vals) {
   mpeig_ctx* ctx = w.ctx;
   if (ctx->eig_backend == 0 && small_syev_supported<T>(sdim)) {
-    small_syev<T>(sdim, G, ldg, vals, ctx->d_status + 3, w.s);
+    small_syev<T>(sdim, G, ldg, vals, ctx->d_status + 3, w.s, ctx->ql_exact);
     return;
   }
   ProfScope prof("small_eig_cusolver", w.s, 0, 0);
@@ -1280,7 +1280,7 @@ static void spec_body(Work<T>& w, const mpeig_op* A, const mpeig_op* T_op, int64
   op_apply<T>(ctx, A, m, Wslot, ld, AS + (m + p) * ld, ld);
   const int64_t sdim = 2 * m + p;
   dgram<T>(w, sdim, S, ld, sdim, AS, ld, w.G.p, sdim, 1);
-  small_syev<T>(sdim, w.G.p, sdim, w.evals.p, ctx->d_status + kSlotEig, s);
+  small_syev<T>(sdim, w.G.p, sdim, w.evals.p, ctx->d_status + kSlotEig, s, ctx->ql_exact);
   const int64_t pn = std::min(m, sdim - m);
   if constexpr (sizeof(T) == 8)
     hl_coeffs(sdim, m, pn, w.G.p, sdim, w.coef.p, w.scratch(), ctx->d_status + kSlotHl, s);

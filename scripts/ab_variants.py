@@ -13,8 +13,8 @@ name = sys.argv[1] if len(sys.argv) > 1 else "dense256-dlobpcg-dchol"
 g = load_golden(name)
 kw = eval(str(g["kw"]))
 print(name, "ref", int(g["iters_lower"]), int(g["iters_working"]))
-opts = [{}, {"ql_exact": 1}, {"ql_exact": 3}, {"ql_exact": 2}, {"spec_mode": 0}, {"eig_backend": 1}, {"eig_backend": 2},
-        {"syev_method": 4}, {"syev_method": 3}, {"syev_method": 1}]
+opts = [{}, {"ql_exact": 1}, {"ql_exact": 3}, {"ql_exact": 2}, {"spec_mode": 0}, {"eig_backend": 1},
+        {"eig_backend": 2}]
 for o in opts:
     ctx = mp.Context(0)
     for k, v in o.items():
@@ -31,6 +31,3 @@ for o in opts:
         A = mp.laplace3d(8, ctx=ctx)
     r = mp.solve(A, mp.SolverConfig(variant=str(g["variant"]), **kw))
     print(o, r.iterations_lower, r.iterations_working, r.converged, flush=True)
-    for key, dflt in (("syev_method", 0), ("ql_exact", -1), ("ql_f32", 0)):  # process-wide switches
-        if key in o:
-            ctx.set_option(key, dflt)
