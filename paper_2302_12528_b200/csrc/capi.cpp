@@ -283,8 +283,17 @@ int mpeig_op_csr(mpeig_ctx* ctx, int64_t n, const int64_t* row_ptr_host,
     }
     mpeig_op* op = new_op(ctx, kOpCsr, n);
     cudaStream_t s = ctx->stream;
+    if (n >= INT32_MAX || nnz >= INT32_MAX)
+      throw Error(MPEIG_E_CONFIG, "csr: n and nnz must stay below 2^31 (int32 device indices)");
     op->rp = upload(row_ptr_host, static_cast<size_t>(n + 1), s);
     op->ci = upload(col_idx_host, static_cast<size_t>(nnz), s);
+    op->nnz = nnz;
+    {
+      std::vector<int> rp32(row_ptr_host, row_ptr_host + n + 1), ci32(col_idx_host, col_idx_host + nnz);
+      op->rp32 = upload(rp32.data(), rp32.size(), s);
+      op->ci32 = upload(ci32.data(), ci32.size(), s);
+      MPB_CUDA(cudaStreamSynchronize(s));  // the host staging vectors go out of scope
+    }
     op->vals = upload(vals_host, static_cast<size_t>(nnz), s);
     std::vector<float> vl;
     op->lower_overflow = !narrow(vals_host, static_cast<size_t>(nnz), vl);
@@ -447,6 +456,8 @@ void mpeig_op_destroy(mpeig_op* op) {
   if (op->ctx && op->ctx->stream) cudaStreamSynchronize(op->ctx->stream);
   cudaFree(op->rp);
   cudaFree(op->ci);
+  cudaFree(op->rp32);
+  cudaFree(op->ci32);
   cudaFree(op->vals);
   cudaFree(op->vals_l);
   cudaFree(op->A);

@@ -53,6 +53,9 @@ struct mpeig_op {
   // CSR (device)
   int64_t* rp = nullptr;
   int64_t* ci = nullptr;
+  int* rp32 = nullptr;  // the same pattern with int32 indices (the SpMM's; n, nnz < 2^31)
+  int* ci32 = nullptr;
+  int64_t nnz = 0;
   double* vals = nullptr;
   float* vals_l = nullptr;
   // dense (device)

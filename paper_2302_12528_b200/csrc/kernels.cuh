@@ -136,7 +136,7 @@ void stencil5(int64_t nx, int64_t ny, int64_t c, const T* X, int64_t ldx, T* Y, 
               cudaStream_t s);
 // CSR SpMM (spmv_block, sparse_kernels.hpp:16-33), ascending-column order
 template <typename T>
-void csr_spmm(int64_t n, const int64_t* row_ptr, const int64_t* col_idx, const T* vals,
+void csr_spmm(int64_t n, const int* row_ptr, const int* col_idx, const T* vals, int64_t nnz,
               int64_t c, const T* X, int64_t ldx, T* Y, int64_t ldy, cudaStream_t s);
 
 // ---------------------------------------------------------- small dense

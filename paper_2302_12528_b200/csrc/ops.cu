@@ -264,19 +264,35 @@ k_stencil5_ym(int64_t nx, int64_t ny, const T* __restrict__ X, int64_t ldx, T* _
   }
 }
 
-template <typename T>
+// CSR SpMM, Y = A X (spmv_block, sparse_kernels.hpp:16-33): a thread per row
+// and CB block columns at once, so each row's entries (int32 column index +
+// value) are read once per CB columns instead of once per column; the X
+// gathers and Y stores are coalesced across the warp's consecutive rows.
+// Every output entry sums its row's products in ascending column order with
+// separately rounded multiplies and adds: bitwise the reference's sums.
+template <typename T, int CB>
 __global__ void __launch_bounds__(256)
-k_csr_spmm(int64_t n, const int64_t* __restrict__ rp, const int64_t* __restrict__ ci,
-           const T* __restrict__ v, const T* __restrict__ X, int64_t ldx, T* __restrict__ Y,
-           int64_t ldy) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+k_csr_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ v,
+           int c, const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int64_t c = blockIdx.y;
-  const T* x = X + c * ldx;
-  T s = T(0);
-  const int64_t e = rp[i + 1];
-  for (int64_t q = rp[i]; q < e; ++q) s = add_rn(s, mul_rn(v[q], x[ci[q]]));
-  Y[i + c * ldy] = s;
+  const int c0 = blockIdx.y * CB;
+  const int nc = min(CB, c - c0);
+  const T* x = X + c0 * ldx;
+  T acc[CB];
+#pragma unroll
+  for (int u = 0; u < CB; ++u) acc[u] = T(0);
+  const int e = __ldg(rp + i + 1);
+  for (int q = __ldg(rp + i); q < e; ++q) {
+    const int col = __ldg(ci + q);
+    const T a = __ldg(v + q);
+#pragma unroll
+    for (int u = 0; u < CB; ++u)
+      if (u < nc) acc[u] = add_rn(acc[u], mul_rn(a, __ldg(x + u * ldx + col)));
+  }
+#pragma unroll
+  for (int u = 0; u < CB; ++u)
+    if (u < nc) Y[i + (c0 + u) * ldy] = acc[u];
 }
 
 }  // namespace
@@ -336,12 +352,27 @@ void stencil5(int64_t nx, int64_t ny, int64_t c, const T* X, int64_t ldx, T* Y, 
 }
 
 template <typename T>
-void csr_spmm(int64_t n, const int64_t* row_ptr, const int64_t* col_idx, const T* vals,
+void csr_spmm(int64_t n, const int* row_ptr, const int* col_idx, const T* vals, int64_t nnz,
               int64_t c, const T* X, int64_t ldx, T* Y, int64_t ldy, cudaStream_t s) {
   if (n <= 0 || c <= 0) return;
-  ProfScope prof("spmm", s, 0.0, 0.0);
-  dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(c));
-  k_csr_spmm<T><<<grid, 256, 0, s>>>(n, row_ptr, col_idx, vals, X, ldx, Y, ldy);
+  // algorithmic bytes: the matrix once (value + int32 index per entry, the
+  // row pointers) and X, Y once each (SURVEY §8(d) K1 CSR)
+  ProfScope prof("spmm", s, double(sizeof(T) + 4) * nnz + 4.0 * (n + 1) + 2.0 * sizeof(T) * n * c,
+                 2.0 * nnz * c);
+  // CB block columns per thread: each row's entries are read once per CB
+  // columns.  Measured at 5-pt 1024^2 x 48 (scripts/spmm_bw.py): fp64 best at
+  // 16 (the gathers' 8-B loads keep enough bytes in flight), fp32 at 4 (its
+  // 4-B gathers need more threads in flight per byte)
+  auto go = [&](auto cb_tag) {
+    constexpr int CB = decltype(cb_tag)::value;
+    const dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(ceil_div(c, CB)));
+    k_csr_spmm<T, CB><<<grid, 256, 0, s>>>(static_cast<int>(n), row_ptr, col_idx, vals,
+                                           static_cast<int>(c), X, ldx, Y, ldy);
+  };
+  if constexpr (sizeof(T) == 8)
+    go(std::integral_constant<int, 16>());
+  else
+    go(std::integral_constant<int, 4>());
   MPB_LAUNCH_CHECK();
 }
 
@@ -350,7 +381,7 @@ void csr_spmm(int64_t n, const int64_t* row_ptr, const int64_t* col_idx, const T
                             int64_t, cudaStream_t, const T*, const T*);                      \
   template void stencil5<T>(int64_t, int64_t, int64_t, const T*, int64_t, T*, int64_t,       \
                             cudaStream_t);                                                   \
-  template void csr_spmm<T>(int64_t, const int64_t*, const int64_t*, const T*, int64_t,      \
+  template void csr_spmm<T>(int64_t, const int*, const int*, const T*, int64_t, int64_t,     \
                             const T*, int64_t, T*, int64_t, cudaStream_t);
 MPB_INST(double)
 MPB_INST(float)

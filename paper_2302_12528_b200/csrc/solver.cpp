@@ -482,10 +482,10 @@ void op_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* X, int
       return;
     case kOpCsr:
       if constexpr (kW) {
-        csr_spmm<double>(op->n, op->rp, op->ci, op->vals, ncols, X, ldx, Y, ldy, s);
+        csr_spmm<double>(op->n, op->rp32, op->ci32, op->vals, op->nnz, ncols, X, ldx, Y, ldy, s);
       } else {
         if (op->lower_overflow) throw Error(MPEIG_E_OVERFLOW, "to_lower: matrix exceeds binary32 range");
-        csr_spmm<float>(op->n, op->rp, op->ci, op->vals_l, ncols, X, ldx, Y, ldy, s);
+        csr_spmm<float>(op->n, op->rp32, op->ci32, op->vals_l, op->nnz, ncols, X, ldx, Y, ldy, s);
       }
       return;
     case kOpDense: {
