@@ -208,6 +208,12 @@ int mpeig_op_lap3d(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, mpeig_op*
  * context's communicator; sharded rank r must hold slab r in z order */
 int mpeig_op_lap3d_slab(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz_global, int64_t z0,
                         int64_t nz_local, mpeig_op** out);
+/* the same 7-point stencil with a variable diagonal: H = -Laplacian + V, row
+ * i's diagonal diag_host[i] = 6 + V_i (the KS-like cfg5 family; host array of
+ * n values), off-diagonals -1, sums in the CSR column order (bitwise the
+ * reference's spmv_block on the CSR form) */
+int mpeig_op_lap3d_diag(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz,
+                        const double* diag_host, mpeig_op** out);
 /* gen_laplace2d (generators.cpp:13-30) applied matrix-free */
 int mpeig_op_lap2d(mpeig_ctx* ctx, int64_t nx, int64_t ny, mpeig_op** out);
 /* CsrMatrix<double> (csr_matrix.hpp:13-146): int64 row_ptr/col_idx, sorted

@@ -361,6 +361,19 @@ def laplace3d(nx: int, ny: int = None, nz: int = None, ctx: Context = None) -> O
     return Operator(ctx, _mk(ctx, ctx.lib.mpeig_op_lap3d, nx, ny, nz), nx * ny * nz, "lap3d")
 
 
+def ks_hamiltonian(nx: int, ny: int = None, nz: int = None, seed: int = 0, ctx: Context = None,
+                   **kw) -> Operator:
+    """cfg5's Kohn-Sham-like H = -Laplacian_7pt + V (generators.ks_potential)
+    as a matrix-free stencil with a variable diagonal (mpeig_op_lap3d_diag)."""
+    from .generators import ks_diagonal
+    ctx = ctx or default_context()
+    ny = nx if ny is None else ny
+    nz = nx if nz is None else nz
+    d = np.ascontiguousarray(ks_diagonal(nx, ny, nz, seed=seed, **kw), dtype=np.float64)
+    h = _mk(ctx, ctx.lib.mpeig_op_lap3d_diag, nx, ny, nz, d.ctypes.data)
+    return Operator(ctx, h, nx * ny * nz, "ks")
+
+
 def laplace3d_slab(nx: int, ny: int, nz_global: int, z0: int, nz_local: int,
                    ctx: Context = None) -> Operator:
     """This rank's z-slab of the 7-point Laplacian (row-sharded; the context

@@ -255,6 +255,28 @@ int mpeig_op_lap3d_slab(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz_globa
   });
 }
 
+int mpeig_op_lap3d_diag(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, const double* diag_host,
+                        mpeig_op** out) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    if (nx < 1 || ny < 1 || nz < 1) throw Error(MPEIG_E_CONFIG, "lap3d: grid sides must be >= 1");
+    if (!diag_host) throw Error(MPEIG_E_CONFIG, "lap3d_diag: null diagonal");
+    const int64_t n = nx * ny * nz;
+    mpeig_op* op = new_op(ctx, kOpLap3d, n);
+    op->nx = nx;
+    op->ny = ny;
+    op->nz = nz;
+    op->dg_host.assign(diag_host, diag_host + n);
+    cudaStream_t s = ctx->stream;
+    op->dgw = upload(diag_host, static_cast<size_t>(n), s);
+    std::vector<float> dl;
+    op->lower_overflow = !narrow(diag_host, static_cast<size_t>(n), dl);
+    op->dgl = upload(dl.data(), dl.size(), s);
+    MPB_CUDA(cudaStreamSynchronize(s));
+    *out = op;
+  });
+}
+
 int mpeig_op_lap2d(mpeig_ctx* ctx, int64_t nx, int64_t ny, mpeig_op** out) {
   return guard(ctx, [&] {
     if (nx < 1 || ny < 1) throw Error(MPEIG_E_CONFIG, "gen_laplace2d: grid sides must be >= 1");
@@ -351,7 +373,10 @@ int mpeig_precond_jacobi(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision, m
     cudaStream_t s = ctx->stream;
     switch (A->kind) {
       case kOpLap3d:
-        std::fill(d.begin(), d.end(), 6.0);
+        if (!A->dg_host.empty())
+          d = A->dg_host;
+        else
+          std::fill(d.begin(), d.end(), 6.0);
         break;
       case kOpLap2d:
         std::fill(d.begin(), d.end(), 4.0);
@@ -458,6 +483,8 @@ void mpeig_op_destroy(mpeig_op* op) {
   cudaFree(op->ci);
   cudaFree(op->rp32);
   cudaFree(op->ci32);
+  cudaFree(op->dgw);
+  cudaFree(op->dgl);
   cudaFree(op->vals);
   cudaFree(op->vals_l);
   cudaFree(op->A);

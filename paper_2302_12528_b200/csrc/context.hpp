@@ -53,6 +53,9 @@ struct mpeig_op {
   // CSR (device)
   int64_t* rp = nullptr;
   int64_t* ci = nullptr;
+  double* dgw = nullptr;  // 7-pt stencil with a variable diagonal (-Laplacian + V): 6 + V_i
+  float* dgl = nullptr;   // to_lower of it
+  std::vector<double> dg_host;
   int* rp32 = nullptr;  // the same pattern with int32 indices (the SpMM's; n, nnz < 2^31)
   int* ci32 = nullptr;
   int64_t nnz = 0;

@@ -130,7 +130,8 @@ void subtract(int64_t n, int64_t c, const T* X, int64_t ldx, const T* W, int64_t
 //  slab, nx*ny per column contiguous; nullptr at the domain boundary)
 template <typename T>
 void stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t c, const T* X, int64_t ldx, T* Y,
-              int64_t ldy, cudaStream_t s, const T* hlo = nullptr, const T* hhi = nullptr);
+              int64_t ldy, cudaStream_t s, const T* hlo = nullptr, const T* hhi = nullptr,
+              const T* dg = nullptr);
 template <typename T>
 void stencil5(int64_t nx, int64_t ny, int64_t c, const T* X, int64_t ldx, T* Y, int64_t ldy,
               cudaStream_t s);
@@ -188,6 +189,8 @@ void small_syev_prof(int64_t s, T* G, int64_t ldg, T* vals, int* info, long long
 // status: [0] = RANK_DEFICIENT / OVERFLOW, [1] = column index.
 template <typename Tin, typename Tq>
 int64_t tsqr_workspace_elems(int64_t n, int64_t m);
+template <typename Tin, typename Tq>
+bool tsqr_fits(int64_t n, int64_t m);
 template <typename Tin, typename Tq>
 void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr, Tq* work,
             int* status, cudaStream_t s, Tin* Rw_out = nullptr, Tin* Rinv_out = nullptr,

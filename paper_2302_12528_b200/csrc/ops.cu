@@ -28,7 +28,8 @@ __device__ __forceinline__ T acc_neg(T s, T x) {  // s += (-1) * x
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_stencil7(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t ldx,
-           T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi) {
+           T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi,
+           const T* __restrict__ dg) {
   const int64_t n = nx * ny * nz;
   const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (p >= n) return;
@@ -46,7 +47,7 @@ k_stencil7(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t 
     s = acc_neg(s, hlo[p + j * sz]);
   if (yi > 0) s = acc_neg(s, x[p - sy]);
   if (xi > 0) s = acc_neg(s, x[p - 1]);
-  s = add_rn(s, mul_rn(T(6), x[p]));
+  s = add_rn(s, mul_rn(dg ? dg[p] : T(6), x[p]));
   if (xi + 1 < nx) s = acc_neg(s, x[p + 1]);
   if (yi + 1 < ny) s = acc_neg(s, x[p + sy]);
   if (zi + 1 < nz)
@@ -74,7 +75,8 @@ struct VecT<float, 4> {
 template <typename T, int V>
 __global__ void __launch_bounds__(256)
 k_stencil7_vec(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t ldx,
-               T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi) {
+               T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi,
+           const T* __restrict__ dg) {
   using VT = typename VecT<T, V>::type;
   const int64_t nv = nx * ny * nz / V;
   const int64_t pv = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -114,6 +116,9 @@ k_stencil7_vec(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int6
   else if (hhi) zp = ldv(hhi + p - (nz - 1) * sz + j * sz);
   const T xl = xi > 0 ? x[p - 1] : T(0);
   const T xr = xi + V < nx ? x[p + V] : T(0);
+  VT dd;
+  if (dg) dd = ldv(dg + p);
+  const T* dv = reinterpret_cast<const T*>(&dd);
   const T* cv = reinterpret_cast<const T*>(&c);
   const T* zmv = reinterpret_cast<const T*>(&zm);
   const T* ymv = reinterpret_cast<const T*>(&ym);
@@ -127,7 +132,7 @@ k_stencil7_vec(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int6
     if (hz_m) s = acc_neg(s, zmv[u]);
     if (yi > 0) s = acc_neg(s, ymv[u]);
     if (xi + u > 0) s = acc_neg(s, u == 0 ? xl : cv[u - 1]);
-    s = add_rn(s, mul_rn(T(6), cv[u]));
+    s = add_rn(s, mul_rn(dg ? dv[u] : T(6), cv[u]));
     if (xi + u + 1 < nx) s = acc_neg(s, u + 1 == V ? xr : cv[u + 1]);
     if (yi + 1 < ny) s = acc_neg(s, ypv[u]);
     if (hz_p) s = acc_neg(s, zpv[u]);
@@ -144,7 +149,8 @@ k_stencil7_vec(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int6
 template <typename T, int V, int ZC>
 __global__ void __launch_bounds__(256)
 k_stencil7_zm(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t ldx,
-              T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi) {
+              T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi,
+           const T* __restrict__ dg) {
   using VT = typename VecT<T, V>::type;
   const int64_t sz = nx * ny;
   const int64_t npv = sz / V;
@@ -173,6 +179,9 @@ k_stencil7_zm(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64
     const T xl = xi > 0 ? x[p - 1] : T(0);
     const T xr = xi + V < nx ? x[p + V] : T(0);
     const bool hz_m = zi > 0 || hlo, hz_p = zi + 1 < nz || hhi;
+    VT dd;
+    if (dg) dd = ldv(dg + p);
+    const T* dv = reinterpret_cast<const T*>(&dd);
     const T* cv = reinterpret_cast<const T*>(&c);
     const T* zmv = reinterpret_cast<const T*>(&zm);
     const T* ymv = reinterpret_cast<const T*>(&ym);
@@ -186,7 +195,7 @@ k_stencil7_zm(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64
       if (hz_m) s = acc_neg(s, zmv[u]);
       if (yi > 0) s = acc_neg(s, ymv[u]);
       if (xi + u > 0) s = acc_neg(s, u == 0 ? xl : cv[u - 1]);
-      s = add_rn(s, mul_rn(T(6), cv[u]));
+      s = add_rn(s, mul_rn(dg ? dv[u] : T(6), cv[u]));
       if (xi + u + 1 < nx) s = acc_neg(s, u + 1 == V ? xr : cv[u + 1]);
       if (yi + 1 < ny) s = acc_neg(s, ypv[u]);
       if (hz_p) s = acc_neg(s, zpv[u]);
@@ -299,33 +308,35 @@ k_csr_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci, const 
 
 template <typename T>
 void stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t c, const T* X, int64_t ldx, T* Y,
-              int64_t ldy, cudaStream_t s, const T* hlo, const T* hhi) {
+              int64_t ldy, cudaStream_t s, const T* hlo, const T* hhi, const T* dg) {
   const int64_t n = nx * ny * nz;
   if (n <= 0 || c <= 0) return;
-  ProfScope prof("stencil", s, 2.0 * sizeof(T) * n * c, 13.0 * n * c);
+  // algorithmic bytes: X and Y once (+ the diagonal once per column block)
+  ProfScope prof("stencil", s, (2.0 * c + (dg ? 1.0 : 0.0)) * sizeof(T) * n, 13.0 * n * c);
   constexpr int V = sizeof(T) == 8 ? 2 : 4;
   const bool aligned = nx % V == 0 && ldx % V == 0 && ldy % V == 0 &&
                        reinterpret_cast<uintptr_t>(X) % (V * sizeof(T)) == 0 &&
                        reinterpret_cast<uintptr_t>(Y) % (V * sizeof(T)) == 0 &&
                        reinterpret_cast<uintptr_t>(hlo) % (V * sizeof(T)) == 0 &&
-                       reinterpret_cast<uintptr_t>(hhi) % (V * sizeof(T)) == 0;
+                       reinterpret_cast<uintptr_t>(hhi) % (V * sizeof(T)) == 0 &&
+                       reinterpret_cast<uintptr_t>(dg) % (V * sizeof(T)) == 0;
   constexpr int ZC = 16;
   if (aligned && n >= (int64_t(1) << 21) && nx * ny >= 256 * V && nx * ny <= 0xffffffffLL &&
       (nx * ny) % V == 0) {
     dim3 grid(static_cast<unsigned>(ceil_div(nx * ny / V, 256)),
               static_cast<unsigned>(ceil_div(nz, int64_t(ZC))), static_cast<unsigned>(c));
-    k_stencil7_zm<T, V, ZC><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi);
+    k_stencil7_zm<T, V, ZC><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi, dg);
     MPB_LAUNCH_CHECK();
     return;
   }
   if (aligned) {
     dim3 grid(static_cast<unsigned>(ceil_div(n / V, 256)), static_cast<unsigned>(c));
-    k_stencil7_vec<T, V><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi);
+    k_stencil7_vec<T, V><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi, dg);
     MPB_LAUNCH_CHECK();
     return;
   }
   dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(c));
-  k_stencil7<T><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi);
+  k_stencil7<T><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi, dg);
   MPB_LAUNCH_CHECK();
 }
 
@@ -378,7 +389,7 @@ void csr_spmm(int64_t n, const int* row_ptr, const int* col_idx, const T* vals, 
 
 #define MPB_INST(T)                                                                          \
   template void stencil7<T>(int64_t, int64_t, int64_t, int64_t, const T*, int64_t, T*,       \
-                            int64_t, cudaStream_t, const T*, const T*);                      \
+                            int64_t, cudaStream_t, const T*, const T*, const T*);                      \
   template void stencil5<T>(int64_t, int64_t, int64_t, const T*, int64_t, T*, int64_t,       \
                             cudaStream_t);                                                   \
   template void csr_spmm<T>(int64_t, const int*, const int*, const T*, int64_t, int64_t,     \

@@ -450,8 +450,16 @@ void op_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* X, int
   switch (op->kind) {
     case kOpLap3d: {
       Comm* c = dist(ctx);
+      const T* dg = nullptr;  // -Laplacian + V: the row's diagonal 6 + V_i (else 6)
+      if constexpr (kW) {
+        dg = op->dgw;
+      } else {
+        if (op->dgw && op->lower_overflow)
+          throw Error(MPEIG_E_OVERFLOW, "to_lower: matrix exceeds binary32 range");
+        dg = op->dgl;
+      }
       if (!op->slab || !c) {
-        stencil7<T>(op->nx, op->ny, op->nz, ncols, X, ldx, Y, ldy, s);
+        stencil7<T>(op->nx, op->ny, op->nz, ncols, X, ldx, Y, ldy, s, nullptr, nullptr, dg);
         return;
       }
       // z-slab of a row-sharded Laplacian: swap the boundary planes with
@@ -474,7 +482,7 @@ void op_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* X, int
                                  sizeof(T) * sz, ncols, cudaMemcpyDeviceToDevice, s));
       c->exchange(slo, shi, rlo, rhi, static_cast<int64_t>(plane), s);
       stencil7<T>(op->nx, op->ny, op->nz, ncols, X, ldx, Y, ldy, s, c->rank > 0 ? rlo : nullptr,
-                  c->rank + 1 < c->nranks ? rhi : nullptr);
+                  c->rank + 1 < c->nranks ? rhi : nullptr, dg);
       return;
     }
     case kOpLap2d:
@@ -737,10 +745,25 @@ static void dresidual(Work<T>& w, int mode, int64_t m, const T* X, const T* AX, 
 // factored again (a TSQR tree whose top level spans the ranks); every rank
 // computes the same global R, then Rw = R (working precision), Rinv = R^-1.
 template <typename T>
+static void dgram(Work<T>& w, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B,
+                  int64_t ldb, T* G, int64_t ldg, int sym);
+
+template <typename T>
 static void tsqr_R(Work<T>& w, int64_t m, T* W, int64_t ldw, bool lower, int* status) {
   const int64_t n = w.n;
   cudaStream_t s = w.s;
   Comm* c = dist(w.ctx);
+  if (!tsqr_fits<T, T>(n, m) || (lower && !tsqr_fits<T, float>(n, m))) {
+    // blocks too wide for a one-CTA Householder tree (cfg5's m = 192): R from
+    // the Cholesky factor of W^T W, R = L^T, R^-1 = L^-T.  Any R that makes
+    // W R^-1 well conditioned serves the next CholQR pass of qr_core; a
+    // breakdown (cond(W) ~ u^-1/2) is reported as NotPositiveDefinite like
+    // mixed_qr's (ortho.hpp:173-186) and falls back the same way.
+    dgram<T>(w, m, W, ldw, m, W, ldw, w.G.p, m, 1);
+    small_cholesky_inv<T>(m, w.G.p, m, w.L(), w.Rinv(), status, s);
+    small_transpose<T>(m, m, w.L(), m, w.Rw(), m, s);
+    return;
+  }
   if (!c) {
     if constexpr (sizeof(T) == 8) {
       if (lower) {

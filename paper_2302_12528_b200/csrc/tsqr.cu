@@ -704,6 +704,21 @@ int64_t tsqr_workspace_elems(int64_t n, int64_t m) {
   return std::max(smem_path, reg_path);
 }
 
+// Whether some TSQR path handles an n x m block: the register TSQR, or the
+// shared-memory leaf + tree (both the leaf tile and a node's stacked R
+// factors must fit one CTA).  Wider blocks (m > ~110 fp64 / ~160 fp32) get
+// their R from a Cholesky factor instead (solver.cpp tsqr_R).
+template <typename Tin, typename Tq>
+bool tsqr_fits(int64_t n, int64_t m) {
+  const RegPlan rp = reg_plan<Tq>(n, m);
+  if (rp.cfg.nw && reg_kernel<Tin, Tq>(rp.cfg)) return true;
+  const TsqrPlan<Tq> p = tsqr_plan<Tq>(n, m);
+  return p.ok && p.group * m * m * static_cast<int64_t>(sizeof(Tq)) <= 220 * 1024;
+}
+template bool tsqr_fits<double, double>(int64_t, int64_t);
+template bool tsqr_fits<double, float>(int64_t, int64_t);
+template bool tsqr_fits<float, float>(int64_t, int64_t);
+
 template <typename Tin, typename Tq>
 void tsqr_r(int64_t n, int64_t m, const Tin* W, int64_t ldw, Tq* R, int64_t ldr, Tq* work,
             int* status, cudaStream_t s, Tin* Rw_out, Tin* Rinv_out, int rank_check) {

@@ -28,6 +28,7 @@ from oracle import Oracle, Problem  # noqa: E402
 
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 from problems import lap_csr, random_spd_csr, spd_dense  # noqa: E402
+from paper_2302_12528_b200.generators import ks_csr  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 
@@ -74,12 +75,16 @@ CASES = {
     "lap2d128k32-dlobpcg-dchol": (lambda: Problem.lap2d(128), "dlobpcg-dchol", dict(k=32, block=48, tol=1e-10, maxit=8000)),
     "dense2048chol-dlobpcg-dchol": (lambda: Problem.dense_matrix(spd_dense(2048, 1e3, 9)[0]), "dlobpcg-dchol", dict(k=64, tol=1e-10, maxit=500, seed=5, native=True)),
     "dense2048chol-mplobpcg-schol": (lambda: Problem.dense_matrix(spd_dense(2048, 1e3, 9)[0]), "mplobpcg-schol", dict(k=64, tol=1e-10, maxit=500, seed=5, native=True)),
+    # cfg5 family (BASELINE.json configs[4]): the Kohn-Sham-like H = -Laplacian + V
+    # (paper_2302_12528_b200/generators.py), clustered low spectrum, 32^3, k = 16
+    "ks32-dlobpcg-dchol": (lambda: Problem.csr(*ks_csr(32, 32, 32, seed=0)), "dlobpcg-dchol", dict(k=16, block=24, tol=1e-10, maxit=4000)),
+    "ks32-mplobpcg-schol": (lambda: Problem.csr(*ks_csr(32, 32, 32, seed=0)), "mplobpcg-schol", dict(k=16, block=24, tol=1e-10, maxit=4000)),
     # cfg 1 (BASELINE.json configs[0]) -- minutes each on one core
     "cfg1-dlobpcg-dchol": (lambda: Problem.lap3d(32), "dlobpcg-dchol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
     "cfg1-dlobpcg-schol": (lambda: Problem.lap3d(32), "dlobpcg-schol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
     "cfg1-mplobpcg-schol": (lambda: Problem.lap3d(32), "mplobpcg-schol", dict(k=10, block=16, tol=1e-10, maxit=2000)),
 }
-LARGE = ["lap2d64k32-dlobpcg-dchol", "lap2d64k32-mplobpcg-schol", "lap2d64k32-pinvit",
+LARGE = ["ks32-dlobpcg-dchol", "ks32-mplobpcg-schol", "lap2d64k32-dlobpcg-dchol", "lap2d64k32-mplobpcg-schol", "lap2d64k32-pinvit",
          "lap2d128k32-dlobpcg-dchol", "dense2048chol-dlobpcg-dchol", "dense2048chol-mplobpcg-schol"]
 FAST = [c for c in CASES if not c.startswith("cfg1") and c not in LARGE]
 

@@ -38,6 +38,8 @@ def make_op(mp, name):
         return mp.laplace2d(128)
     if name.startswith("dense256"):
         return mp.dense_matrix(spd_dense(256, 1e3, 5)[0])
+    if name.startswith("ks32"):
+        return mp.ks_hamiltonian(32, seed=0)
     raise KeyError(name)
 
 
@@ -158,6 +160,25 @@ def test_tensor_core_fp32_stage_parity(gpu, name):
     finally:
         ctx.lib.mpeig_set_process_option(b"tc", 1)
     check_parity(g, cfg, r, name)
+
+
+@pytest.mark.parametrize("name", ["ks32-dlobpcg-dchol", "ks32-mplobpcg-schol"])
+def test_ks_clustered_parity(gpu, name):
+    """cfg5 family: Kohn-Sham-like H = -Laplacian + V (seeded wells, clustered
+    low spectrum), 32^3, k = 16, m = 24, against the reference's fixture."""
+    g, cfg, r = run_case(gpu, name)
+    check_parity(g, cfg, r, name)
+
+
+def test_ks_stencil_and_csr_trajectories_identical(gpu):
+    """The matrix-free variable-diagonal stencil and the CSR operator are
+    bitwise equal applies, so the whole solve is bit-identical."""
+    from paper_2302_12528_b200.generators import ks_csr
+    cfg = gpu.SolverConfig(k=6, block=9, tol=1e-9, maxit=300, variant="mplobpcg-schol")
+    r1 = gpu.solve(gpu.ks_hamiltonian(12, 10, 9, seed=5), cfg)
+    r2 = gpu.solve(gpu.csr_matrix(*ks_csr(12, 10, 9, seed=5)), cfg)
+    assert (r1.iterations_lower, r1.iterations_working) == (r2.iterations_lower, r2.iterations_working)
+    assert np.array_equal(r1.theta, r2.theta)
 
 
 def test_large_block_pinvit_capped(gpu):
