@@ -11,7 +11,8 @@ see DESIGN.md §Measurement).  A "step" is one complete solve.
     python bench.py                        # N=1, 5 timed solves after 3 warm-ups
     python bench.py --impl reference       # the reference CPU solver (oracle/_ref):
                                            # K complete solves, side by side on the host cores
-    torchrun --nproc-per-node N bench.py --gpus N   # N independent replicas
+    torchrun --nproc-per-node N bench.py --gpus N   # ONE row-sharded solve over the N GPUs
+    torchrun --nproc-per-node N bench.py --gpus N --replicas   # N independent replicas
 
 Prints ONE JSON line (rank 0).  `value` = mean device time of one solve with
 all inputs resident in HBM (seconds, lower is better); `e2e` = the same solve
@@ -249,9 +250,15 @@ def run_ours(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
+        # a fixed NCCL algorithm / protocol keeps the allreduce summation order
+        # (and so the sharded trajectory) reproducible run to run
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        os.environ.setdefault("NCCL_PROTO", "Simple")
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     w = WORKLOADS[args.workload]
-    shard = args.shard  # at N = 1: the sharded code path over a 1-rank NCCL comm
+    # N > 1: one row-sharded solve over the N GPUs (SURVEY §8e, strong scaling)
+    # unless --replicas; at N = 1 --shard runs the sharded path over a 1-rank comm
+    shard = args.shard or (world > 1 and not args.replicas)
     ctx = mp.Context(local)
     cfg = mp.SolverConfig(k=w["k"], block=w["block"], tol=w["tol"], maxit=w["maxit"], seed=w["seed"],
                           variant=args.variant)
@@ -347,6 +354,16 @@ def run_ours(args):
         solve_resident()
         torch.cuda.synchronize()
         prof = mp.profile.report()
+    # ---- the north-star target's per-iteration time at this N (cfg4: 256^3,
+    # k = 64, m = 80, row-sharded over the N GPUs; evidence key, all ranks)
+    cfg4 = None
+    # (N > 1: the per-GPU share of 256^3; at N = 1 the whole 16.8M-row problem
+    # needs ~150 GB of the 180 GB and is measured by scripts/cfg_run.py instead)
+    if (world > 1 or args.cfg4) and not args.no_at_scale and args.workload == "cfg1" and not args.replicas:
+        try:
+            cfg4 = cfg4_per_iteration(mp, ctx, rank, world, dist, shard)
+        except Exception as exc:  # evidence only: never fail the bench line
+            cfg4 = {"error": f"{type(exc).__name__}: {exc}"}
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -417,12 +434,61 @@ def run_ours(args):
             line["kernels_at_scale"] = at_scale_kernels(mp, peak)
         except Exception as exc:  # evidence only: never fail the bench line
             line["kernels_at_scale"] = {"error": f"{type(exc).__name__}: {exc}"}
+    if cfg4 is not None:
+        line["cfg4_per_iteration"] = cfg4
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
 
 
 DMMA_PEAK_TFS = 37.1  # fp64 mma.sync m8n8k4, measured in-repo (profiles/r01_microbench_b200.txt)
+
+
+def cfg4_per_iteration(mp, ctx, rank, world, dist, shard, iters=4):
+    """BASELINE.json configs[3] at this N: 3-D 7-pt Laplacian 256^3 (n = 16.8M),
+    k = 64, m = 80, mixed precision, row-sharded over the N GPUs (z-slabs,
+    overlapped halo exchange, Gram / norm allreduce over NCCL); a capped solve
+    (`iters` per stage).  Per-iteration time = median interval between the
+    per-iteration records reaching the host, per stage, max over ranks.  A
+    full solve to 1e-10 takes thousands of iterations."""
+    import torch
+    nx = ny = nz = 256
+    k, m = 64, 80
+    cfg = mp.SolverConfig(k=k, block=m, tol=1e-10, maxit=iters, variant="mplobpcg-schol")
+    if shard:
+        z0, nzl = mp.slab_partition(nz, world)[rank]
+        A = mp.laplace3d_slab(nx, ny, nz, z0, nzl, ctx=ctx)
+        row0 = nx * ny * z0
+    else:
+        A = mp.laplace3d(nx, ny, nz, ctx=ctx)
+        row0 = 0
+    n_glob, n = nx * ny * nz, A.n
+    dev = f"cuda:{ctx.device}"
+    X0 = torch.from_numpy(np.ascontiguousarray(
+        mp.gaussian_matrix_rows(n_glob, m, cfg.seed, row0, n).T)).to(dev)
+    Om = torch.from_numpy(np.ascontiguousarray(
+        mp.gaussian_matrix_rows(n_glob, cfg.sketch_rows, cfg.seed ^ 0x9E3779B97F4A7C15, row0, n).T)).to(dev)
+    T = mp.jacobi(A, mp.LOWER)
+    mp.solve_prepared(A, cfg, X0, Om, 0.0, T=T)  # warm-up: allocations
+    torch.cuda.synchronize()
+    r = mp.solve_prepared(A, cfg, X0, Om, 0.0, T=T, history=True)
+    torch.cuda.synchronize()
+    med = []
+    for st in (1, 0):  # fp32 stage, fp64 stage
+        ts = [h.host_time for h in r.history if h.stage == st]
+        d = np.diff(ts)[1:] if len(ts) > 2 else np.array([np.nan])
+        med.append(float(np.median(d)) * 1e3)
+    if dist:
+        t = torch.tensor(med, device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        med = t.tolist()
+    del X0, Om
+    torch.cuda.empty_cache()
+    return {"workload": "cfg4: 3-D 7-pt Laplacian 256^3 (n=16.8M), k=64, m=80, mplobpcg-schol, "
+                        f"{'row-sharded over ' + str(world) + ' GPUs' if shard else 'one GPU'}, "
+                        f"capped at {iters}+{iters} iterations",
+            "ms_per_iteration_fp32_stage": med[0], "ms_per_iteration_fp64_stage": med[1],
+            "rows_per_gpu": n, "method": "median interval of the per-iteration records, max over ranks"}
 
 
 def at_scale_kernels(mp, peak_gbs):
@@ -471,9 +537,13 @@ def main():
     ap.add_argument("--no-at-scale", action="store_true",
                     help="skip the per-kernel efficiency pass at the 256^3 / 8-GPU per-rank shape")
     ap.add_argument("--shard", action="store_true",
-                    help="one row-sharded solve over the N GPUs (strong scaling; N = 1 runs "
-                         "the sharded path over a 1-rank NCCL comm) "
-                         "instead of N independent replicas")
+                    help="at N = 1: the row-sharded code path over a 1-rank NCCL comm "
+                         "(N > 1 is sharded by default)")
+    ap.add_argument("--cfg4", action="store_true",
+                    help="also time cfg4 (256^3, m = 80) per iteration at N = 1")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: N independent single-GPU solves (weak scaling) instead of "
+                         "one row-sharded solve")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -504,6 +504,9 @@ void mpeig_op_destroy(mpeig_op* op) {
   cudaFree(op->sp_Lv);
   cudaFree(op->sp_Uv);
   if (op->halo) cudaFree(op->halo);
+  if (op->halo_stream) cudaStreamDestroy(op->halo_stream);
+  if (op->ev_packed) cudaEventDestroy(op->ev_packed);
+  if (op->ev_halo) cudaEventDestroy(op->ev_halo);
   delete op;
 }
 

@@ -50,6 +50,8 @@ struct mpeig_op {
   bool slab = false;
   mutable void* halo = nullptr;  // send/recv planes of the slab exchange
   mutable size_t halo_bytes = 0;
+  mutable cudaStream_t halo_stream = nullptr;  // the overlapped halo exchange
+  mutable cudaEvent_t ev_packed = nullptr, ev_halo = nullptr;
   // CSR (device)
   int64_t* rp = nullptr;
   int64_t* ci = nullptr;

@@ -126,12 +126,14 @@ void subtract(int64_t n, int64_t c, const T* X, int64_t ldx, const T* W, int64_t
 
 // ------------------------------------------------------------- operators
 // 3-D 7-point / 2-D 5-point Laplacian, matrix-free, reference summation order
-// (hlo / hhi: the neighbouring ranks' adjacent z-planes of a row-sharded
-//  slab, nx*ny per column contiguous; nullptr at the domain boundary)
+// (hlo / hhi: the z-planes adjacent to the slab -- the neighbouring ranks'
+//  received planes, column j at + j * ldl / ldu (0: nx*ny, packed), or planes
+//  of X itself when a sub-slab is applied; nullptr at the domain boundary;
+//  dg: the variable diagonal, else 6)
 template <typename T>
 void stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t c, const T* X, int64_t ldx, T* Y,
               int64_t ldy, cudaStream_t s, const T* hlo = nullptr, const T* hhi = nullptr,
-              const T* dg = nullptr);
+              const T* dg = nullptr, int64_t ldl = 0, int64_t ldu = 0);
 template <typename T>
 void stencil5(int64_t nx, int64_t ny, int64_t c, const T* X, int64_t ldx, T* Y, int64_t ldy,
               cudaStream_t s);

@@ -29,7 +29,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_stencil7(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t ldx,
            T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi,
-           const T* __restrict__ dg) {
+           const T* __restrict__ dg, int64_t ldl, int64_t ldu) {
   const int64_t n = nx * ny * nz;
   const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (p >= n) return;
@@ -44,7 +44,7 @@ k_stencil7(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t 
   if (zi > 0)
     s = acc_neg(s, x[p - sz]);
   else if (hlo)
-    s = acc_neg(s, hlo[p + j * sz]);
+    s = acc_neg(s, hlo[p + j * ldl]);
   if (yi > 0) s = acc_neg(s, x[p - sy]);
   if (xi > 0) s = acc_neg(s, x[p - 1]);
   s = add_rn(s, mul_rn(dg ? dg[p] : T(6), x[p]));
@@ -53,7 +53,7 @@ k_stencil7(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t 
   if (zi + 1 < nz)
     s = acc_neg(s, x[p + sz]);
   else if (hhi)
-    s = acc_neg(s, hhi[p - (nz - 1) * sz + j * sz]);
+    s = acc_neg(s, hhi[p - (nz - 1) * sz + j * ldu]);
   Y[p + j * ldy] = s;
 }
 
@@ -76,7 +76,7 @@ template <typename T, int V>
 __global__ void __launch_bounds__(256)
 k_stencil7_vec(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t ldx,
                T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi,
-           const T* __restrict__ dg) {
+           const T* __restrict__ dg, int64_t ldl, int64_t ldu) {
   using VT = typename VecT<T, V>::type;
   const int64_t nv = nx * ny * nz / V;
   const int64_t pv = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -109,11 +109,11 @@ k_stencil7_vec(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int6
   VT zm{}, ym{}, yp{}, zp{};
   const bool hz_m = zi > 0 || hlo, hz_p = zi + 1 < nz || hhi;
   if (zi > 0) zm = ldv(x + p - sz);
-  else if (hlo) zm = ldv(hlo + p + j * sz);
+  else if (hlo) zm = ldv(hlo + p + j * ldl);
   if (yi > 0) ym = ldv(x + p - sy);
   if (yi + 1 < ny) yp = ldv(x + p + sy);
   if (zi + 1 < nz) zp = ldv(x + p + sz);
-  else if (hhi) zp = ldv(hhi + p - (nz - 1) * sz + j * sz);
+  else if (hhi) zp = ldv(hhi + p - (nz - 1) * sz + j * ldu);
   const T xl = xi > 0 ? x[p - 1] : T(0);
   const T xr = xi + V < nx ? x[p + V] : T(0);
   VT dd;
@@ -150,7 +150,7 @@ template <typename T, int V, int ZC>
 __global__ void __launch_bounds__(256)
 k_stencil7_zm(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t ldx,
               T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi,
-           const T* __restrict__ dg) {
+           const T* __restrict__ dg, int64_t ldl, int64_t ldu) {
   using VT = typename VecT<T, V>::type;
   const int64_t sz = nx * ny;
   const int64_t npv = sz / V;
@@ -168,12 +168,12 @@ k_stencil7_zm(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64
   if (z0 >= nz) return;
   VT zm{}, c = ldv(x + q + z0 * sz);
   if (z0 > 0) zm = ldv(x + q + (z0 - 1) * sz);
-  else if (hlo) zm = ldv(hlo + q + j * sz);
+  else if (hlo) zm = ldv(hlo + q + j * ldl);
   for (int64_t zi = z0; zi < z1; ++zi) {
     const int64_t p = q + zi * sz;
     VT zp{}, ym{}, yp{};
     if (zi + 1 < nz) zp = ldv(x + p + sz);
-    else if (hhi) zp = ldv(hhi + q + j * sz);
+    else if (hhi) zp = ldv(hhi + q + j * ldu);
     if (yi > 0) ym = ldv(x + p - sy);
     if (yi + 1 < ny) yp = ldv(x + p + sy);
     const T xl = xi > 0 ? x[p - 1] : T(0);
@@ -308,9 +308,12 @@ k_csr_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci, const 
 
 template <typename T>
 void stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t c, const T* X, int64_t ldx, T* Y,
-              int64_t ldy, cudaStream_t s, const T* hlo, const T* hhi, const T* dg) {
+              int64_t ldy, cudaStream_t s, const T* hlo, const T* hhi, const T* dg, int64_t ldl,
+              int64_t ldu) {
   const int64_t n = nx * ny * nz;
   if (n <= 0 || c <= 0) return;
+  if (ldl <= 0) ldl = nx * ny;  // halo planes packed per column
+  if (ldu <= 0) ldu = nx * ny;
   // algorithmic bytes: X and Y once (+ the diagonal once per column block)
   ProfScope prof("stencil", s, (2.0 * c + (dg ? 1.0 : 0.0)) * sizeof(T) * n, 13.0 * n * c);
   constexpr int V = sizeof(T) == 8 ? 2 : 4;
@@ -319,24 +322,24 @@ void stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t c, const T* X, int64_t
                        reinterpret_cast<uintptr_t>(Y) % (V * sizeof(T)) == 0 &&
                        reinterpret_cast<uintptr_t>(hlo) % (V * sizeof(T)) == 0 &&
                        reinterpret_cast<uintptr_t>(hhi) % (V * sizeof(T)) == 0 &&
-                       reinterpret_cast<uintptr_t>(dg) % (V * sizeof(T)) == 0;
+                       reinterpret_cast<uintptr_t>(dg) % (V * sizeof(T)) == 0 && ldl % V == 0 && ldu % V == 0;
   constexpr int ZC = 16;
   if (aligned && n >= (int64_t(1) << 21) && nx * ny >= 256 * V && nx * ny <= 0xffffffffLL &&
       (nx * ny) % V == 0) {
     dim3 grid(static_cast<unsigned>(ceil_div(nx * ny / V, 256)),
               static_cast<unsigned>(ceil_div(nz, int64_t(ZC))), static_cast<unsigned>(c));
-    k_stencil7_zm<T, V, ZC><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi, dg);
+    k_stencil7_zm<T, V, ZC><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi, dg, ldl, ldu);
     MPB_LAUNCH_CHECK();
     return;
   }
   if (aligned) {
     dim3 grid(static_cast<unsigned>(ceil_div(n / V, 256)), static_cast<unsigned>(c));
-    k_stencil7_vec<T, V><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi, dg);
+    k_stencil7_vec<T, V><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi, dg, ldl, ldu);
     MPB_LAUNCH_CHECK();
     return;
   }
   dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(c));
-  k_stencil7<T><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi, dg);
+  k_stencil7<T><<<grid, 256, 0, s>>>(nx, ny, nz, X, ldx, Y, ldy, hlo, hhi, dg, ldl, ldu);
   MPB_LAUNCH_CHECK();
 }
 
@@ -389,7 +392,8 @@ void csr_spmm(int64_t n, const int* row_ptr, const int* col_idx, const T* vals, 
 
 #define MPB_INST(T)                                                                          \
   template void stencil7<T>(int64_t, int64_t, int64_t, int64_t, const T*, int64_t, T*,       \
-                            int64_t, cudaStream_t, const T*, const T*, const T*);                      \
+                            int64_t, cudaStream_t, const T*, const T*, const T*, int64_t,    \
+                            int64_t);                      \
   template void stencil5<T>(int64_t, int64_t, int64_t, const T*, int64_t, T*, int64_t,       \
                             cudaStream_t);                                                   \
   template void csr_spmm<T>(int64_t, const int*, const int*, const T*, int64_t, int64_t,     \

@@ -480,9 +480,36 @@ void op_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* X, int
                                  cudaMemcpyDeviceToDevice, s));
       MPB_CUDA(cudaMemcpy2DAsync(shi, sizeof(T) * sz, X + (op->nz - 1) * sz, sizeof(T) * ldx,
                                  sizeof(T) * sz, ncols, cudaMemcpyDeviceToDevice, s));
-      c->exchange(slo, shi, rlo, rhi, static_cast<int64_t>(plane), s);
-      stencil7<T>(op->nx, op->ny, op->nz, ncols, X, ldx, Y, ldy, s, c->rank > 0 ? rlo : nullptr,
-                  c->rank + 1 < c->nranks ? rhi : nullptr, dg);
+      // the exchange runs on a side stream while the interior planes (every
+      // neighbour inside the slab) are computed; the two boundary planes
+      // follow once the neighbours' planes have arrived.  Each point's sum
+      // order is unchanged, so the sharded apply stays bitwise the global one.
+      if (!op->halo_stream) {
+        MPB_CUDA(cudaStreamCreateWithFlags(&op->halo_stream, cudaStreamNonBlocking));
+        MPB_CUDA(cudaEventCreateWithFlags(&op->ev_packed, cudaEventDisableTiming));
+        MPB_CUDA(cudaEventCreateWithFlags(&op->ev_halo, cudaEventDisableTiming));
+      }
+      MPB_CUDA(cudaEventRecord(op->ev_packed, s));
+      MPB_CUDA(cudaStreamWaitEvent(op->halo_stream, op->ev_packed, 0));
+      c->exchange(slo, shi, rlo, rhi, static_cast<int64_t>(plane), op->halo_stream);
+      MPB_CUDA(cudaEventRecord(op->ev_halo, op->halo_stream));
+      const int64_t nz = op->nz;
+      const T* lo_halo = c->rank > 0 ? rlo : nullptr;
+      const T* hi_halo = c->rank + 1 < c->nranks ? rhi : nullptr;
+      auto dgz = [&](int64_t z) -> const T* { return dg ? dg + z * sz : nullptr; };
+      if (nz >= 3)  // interior planes 1 .. nz-2: z-neighbours are X's own planes
+        stencil7<T>(op->nx, op->ny, nz - 2, ncols, X + sz, ldx, Y + sz, ldy, s, X,
+                    X + (nz - 1) * sz, dgz(1), ldx, ldx);
+      MPB_CUDA(cudaStreamWaitEvent(s, op->ev_halo, 0));
+      if (nz == 1) {
+        stencil7<T>(op->nx, op->ny, 1, ncols, X, ldx, Y, ldy, s, lo_halo, hi_halo, dgz(0));
+      } else {
+        // plane 0: below = the lower neighbour's plane (packed), above = X's plane 1;
+        // plane nz-1: below = X's plane nz-2, above = the upper neighbour's plane
+        stencil7<T>(op->nx, op->ny, 1, ncols, X, ldx, Y, ldy, s, lo_halo, X + sz, dgz(0), 0, ldx);
+        stencil7<T>(op->nx, op->ny, 1, ncols, X + (nz - 1) * sz, ldx, Y + (nz - 1) * sz, ldy, s,
+                    X + (nz - 2) * sz, hi_halo, dgz(nz - 1), ldx, 0);
+      }
       return;
     }
     case kOpLap2d:
