@@ -60,7 +60,7 @@ GramPlan gram_plan(int64_t n, int64_t ka, int64_t kb) {
   p.tiles_n = ceil_div(kb, tile);
   // one wave: a single-tile Gram uses one CTA per SM (two reduction levels),
   // multi-tile Grams two CTAs per SM
-  int64_t nchunk = kNumSMs;
+  int64_t nchunk = kNumSMs;  // combine_body's unrolled loads assume nchunk <= kNumSMs
   const int64_t max_chunks = ceil_div(n, 64);  // >= 64 rows per chunk
   if (nchunk > max_chunks) nchunk = max_chunks;
   if (nchunk < 1) nchunk = 1;
@@ -104,9 +104,19 @@ __device__ __forceinline__ void combine_body(int64_t nchunk, int ka, int kb,
   }
   const int64_t o1 = i + static_cast<int64_t>(j) * ka, o2 = j + static_cast<int64_t>(i) * ka;
   T a = T(0), b = T(0);
-  for (int64_t c = lane; c < nchunk; c += 32) {
-    a += __ldg(part + c * tot + o1);
-    if (sym) b += __ldg(part + c * tot + o2);
+  // nchunk <= kNumSMs: every lane's chunk loads issued before the (ordered) sums
+  constexpr int kPer = (kNumSMs + 31) / 32;
+  T va[kPer], vb[kPer];
+#pragma unroll
+  for (int t = 0; t < kPer; ++t) {
+    const int64_t c = lane + 32 * t;
+    va[t] = c < nchunk ? __ldg(part + c * tot + o1) : T(0);
+    vb[t] = (sym && c < nchunk) ? __ldg(part + c * tot + o2) : T(0);
+  }
+#pragma unroll
+  for (int t = 0; t < kPer; ++t) {
+    a += va[t];
+    b += vb[t];
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -818,10 +828,14 @@ static void gemm_impl(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int6
           nt = t;
         }
       }
+      // deep K (the dense operator A X, K = n): one column tile up to 96 wide,
+      // so the n x n operand streams from HBM once instead of once per tile
+      const bool deep = k > 4 * kDBK;
+      if (deep && c > 16 * nt && c <= 96) nt = static_cast<int>(ceil_div(c, 16));
       const dim3 g2(static_cast<unsigned>(ceil_div(n, kTile)),
                     static_cast<unsigned>(ceil_div(c, 16 * nt)), nz);
       const int ki = static_cast<int>(k), ci = static_cast<int>(c);
-      const bool shallow = k <= 4 * kDBK;
+      const bool shallow = !deep;
       auto launch = [&](auto nt_tag) {
         constexpr int NT = decltype(nt_tag)::value;
         auto go = [&](auto st_tag) {
@@ -831,17 +845,20 @@ static void gemm_impl(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int6
           k_gemm_dmma<NT, ST><<<g2, 128, smem, s>>>(n, ki, ci, alpha, A, lda, C, ldc, beta, Z, ldz,
                                                     Y, ldy, A2, Y2);
         };
+        // shallow K: every panel in flight at once; deep K: a 3-stage ring
+        // (two panels of A in flight from HBM while the third is consumed)
         if (shallow)
           go(std::integral_constant<int, 4>());
         else
-          go(std::integral_constant<int, 2>());
+          go(std::integral_constant<int, 3>());
       };
       switch (nt) {
         case 1: launch(std::integral_constant<int, 1>()); break;
         case 2: launch(std::integral_constant<int, 2>()); break;
         case 3: launch(std::integral_constant<int, 3>()); break;
         case 4: launch(std::integral_constant<int, 4>()); break;
-        default: launch(std::integral_constant<int, 5>()); break;
+        case 5: launch(std::integral_constant<int, 5>()); break;
+        default: launch(std::integral_constant<int, 6>()); break;
       }
       MPB_LAUNCH_CHECK();
       return;

