@@ -50,11 +50,16 @@ void gemm_tc_f32(int64_t n, int64_t k, int64_t c, float alpha, const float* A, i
 // g_gram_tc: 1 = by size (default), 0 = never, 2 = always (tests)
 extern int g_gram_tc, g_gemm_tc;
 extern int g_tc_nprod, g_tc_store;
+// (crossovers measured at n = 2M, scripts/dense_shapes.py: the tensor-core
+// Gram wins from 32 x 16 up, the tensor-core block update once k * c reaches
+// the m = 48 project-out's 96 x 48; narrower updates stay on the FFMA kernel)
 inline bool gram_tc_wanted(int64_t n, int64_t ka, int64_t kb) {
-  return g_gram_tc == 2 || (g_gram_tc == 1 && n * ka * kb >= (int64_t(1) << 28));
+  return g_gram_tc == 2 ||
+         (g_gram_tc == 1 && n * ka * kb >= (int64_t(1) << 28) && ka * kb > 256);
 }
 inline bool gemm_tc_wanted(int64_t n, int64_t k, int64_t c) {
-  return g_gemm_tc == 2 || (g_gemm_tc == 1 && n * k * c >= (int64_t(1) << 28));
+  return g_gemm_tc == 2 ||
+         (g_gemm_tc == 1 && n * k * c >= (int64_t(1) << 28) && k * c >= 96 * 48);
 }
 // CholQR's Gram and factorization in one pass (m <= 16): G = V^T V
 // (hermitized), then L L^T = G and Uinv = L^{-T} by the last CTA of the

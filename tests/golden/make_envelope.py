@@ -36,7 +36,8 @@ FAST = ["lap3d8-dlobpcg-dchol", "lap3d8-dlobpcg-schol", "lap3d8-mplobpcg-schol",
         "dense256-dlobpcg-dchol", "dense256-mplobpcg-schol", "lap2d32-pinvit"]
 SLOW = ["cfg1-mplobpcg-schol", "cfg1-dlobpcg-dchol", "cfg1-dlobpcg-schol"]
 # the large-block path (3m = 144 > 96)
-LARGE = ["lap2d64k32-dlobpcg-dchol", "lap2d64k32-mplobpcg-schol"]
+LARGE = ["lap2d64k32-dlobpcg-dchol", "lap2d64k32-mplobpcg-schol", "lap2d128k32-dlobpcg-dchol",
+         "ks32-dlobpcg-dchol", "ks32-mplobpcg-schol"]
 
 
 def one(args):
