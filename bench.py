@@ -434,8 +434,8 @@ def run_ours(args):
             line["kernels_at_scale"] = at_scale_kernels(mp, peak)
         except Exception as exc:  # evidence only: never fail the bench line
             line["kernels_at_scale"] = {"error": f"{type(exc).__name__}: {exc}"}
-    if cfg4 is not None:
-        line["cfg4_per_iteration"] = cfg4
+    for which, v in at_scale.items():
+        line[f"{which}_per_iteration"] = v
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -444,23 +444,34 @@ def run_ours(args):
 DMMA_PEAK_TFS = 37.1  # fp64 mma.sync m8n8k4, measured in-repo (profiles/r01_microbench_b200.txt)
 
 
-def cfg4_per_iteration(mp, ctx, rank, world, dist, shard, iters=4):
-    """BASELINE.json configs[3] at this N: 3-D 7-pt Laplacian 256^3 (n = 16.8M),
-    k = 64, m = 80, mixed precision, row-sharded over the N GPUs (z-slabs,
-    overlapped halo exchange, Gram / norm allreduce over NCCL); a capped solve
-    (`iters` per stage).  Per-iteration time = median interval between the
+AT_SCALE = {
+    "cfg4": dict(dims=(256, 256, 256), k=64, m=80, ks=False,
+                 desc="cfg4: 3-D 7-pt Laplacian 256^3 (n=16.8M), k=64, m=80"),
+    "cfg5": dict(dims=(256, 128, 128), k=128, m=192, ks=True,
+                 desc="cfg5: Kohn-Sham-like -Laplacian+V 256x128x128 (n=4.2M), k=128, m=192"),
+}
+
+
+def cfg4_per_iteration(mp, ctx, rank, world, dist, shard, iters=4, which="cfg4"):
+    """BASELINE.json configs[3] (cfg4: 3-D 7-pt Laplacian 256^3, k = 64, m = 80)
+    or configs[4] (cfg5: the Kohn-Sham-like operator, n = 4.2M, k = 128) at
+    this N: mixed precision, row-sharded over the N GPUs (z-slabs, overlapped
+    halo exchange, Gram / norm allreduce over NCCL); a capped solve (`iters`
+    per stage).  Per-iteration time = median interval between the
     per-iteration records reaching the host, per stage, max over ranks.  A
     full solve to 1e-10 takes thousands of iterations."""
     import torch
-    nx = ny = nz = 256
-    k, m = 64, 80
+    w = AT_SCALE[which]
+    nx, ny, nz = w["dims"]
+    k, m = w["k"], w["m"]
     cfg = mp.SolverConfig(k=k, block=m, tol=1e-10, maxit=iters, variant="mplobpcg-schol")
     if shard:
         z0, nzl = mp.slab_partition(nz, world)[rank]
-        A = mp.laplace3d_slab(nx, ny, nz, z0, nzl, ctx=ctx)
+        A = (mp.ks_hamiltonian_slab(nx, ny, nz, z0, nzl, seed=0, ctx=ctx) if w["ks"] else
+             mp.laplace3d_slab(nx, ny, nz, z0, nzl, ctx=ctx))
         row0 = nx * ny * z0
     else:
-        A = mp.laplace3d(nx, ny, nz, ctx=ctx)
+        A = mp.ks_hamiltonian(nx, ny, nz, seed=0, ctx=ctx) if w["ks"] else mp.laplace3d(nx, ny, nz, ctx=ctx)
         row0 = 0
     n_glob, n = nx * ny * nz, A.n
     dev = f"cuda:{ctx.device}"
@@ -484,7 +495,7 @@ def cfg4_per_iteration(mp, ctx, rank, world, dist, shard, iters=4):
         med = t.tolist()
     del X0, Om
     torch.cuda.empty_cache()
-    return {"workload": "cfg4: 3-D 7-pt Laplacian 256^3 (n=16.8M), k=64, m=80, mplobpcg-schol, "
+    return {"workload": w["desc"] + ", mplobpcg-schol, "
                         f"{'row-sharded over ' + str(world) + ' GPUs' if shard else 'one GPU'}, "
                         f"capped at {iters}+{iters} iterations",
             "ms_per_iteration_fp32_stage": med[0], "ms_per_iteration_fp64_stage": med[1],

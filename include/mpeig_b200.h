@@ -214,6 +214,10 @@ int mpeig_op_lap3d_slab(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz_globa
  * reference's spmv_block on the CSR form) */
 int mpeig_op_lap3d_diag(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz,
                         const double* diag_host, mpeig_op** out);
+/* this rank's z-slab of the variable-diagonal 7-pt operator; diag_local_host
+ * = the slab's n_local diagonal values (rows row0 .. row0 + n_local) */
+int mpeig_op_lap3d_slab_diag(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz_global, int64_t z0,
+                             int64_t nz_local, const double* diag_local_host, mpeig_op** out);
 /* gen_laplace2d (generators.cpp:13-30) applied matrix-free */
 int mpeig_op_lap2d(mpeig_ctx* ctx, int64_t nx, int64_t ny, mpeig_op** out);
 /* CsrMatrix<double> (csr_matrix.hpp:13-146): int64 row_ptr/col_idx, sorted

@@ -13,7 +13,7 @@ from .api import (  # noqa: F401
     OverflowError_, RankCollapse, RankDeficient, SingularTriangular, SolverConfig,
     StageOptions, StageOutcome, StageTimings, build_precision_for, converged_count, csr_matrix,
     default_context, dense_cholesky, dense_matrix, rcm_ordering, solve_csr, sparse_cholesky,
-    ks_hamiltonian, read_matrix_market, ParseError, NotSymmetricHeader, NotSquare, gaussian_matrix, host_operator, jacobi, laplace2d, laplace3d,
+    ks_hamiltonian, ks_hamiltonian_slab, read_matrix_market, ParseError, NotSymmetricHeader, NotSquare, gaussian_matrix, host_operator, jacobi, laplace2d, laplace3d,
     lobpcg_stage, mixed_lobpcg, pinvit, profile, run_variant, solve, solve_prepared,
     spectral_norm_estimate, to_device,
     to_host,

@@ -374,6 +374,18 @@ def ks_hamiltonian(nx: int, ny: int = None, nz: int = None, seed: int = 0, ctx: 
     return Operator(ctx, h, nx * ny * nz, "ks")
 
 
+def ks_hamiltonian_slab(nx: int, ny: int, nz_global: int, z0: int, nz_local: int, seed: int = 0,
+                        ctx: Context = None, **kw) -> Operator:
+    """This rank's z-slab of cfg5's H = -Laplacian_7pt + V (row-sharded)."""
+    from .generators import ks_diagonal
+    ctx = ctx or default_context()
+    d = ks_diagonal(nx, ny, nz_global, seed=seed, **kw)
+    row0, n = nx * ny * z0, nx * ny * nz_local
+    dl = np.ascontiguousarray(d[row0:row0 + n], dtype=np.float64)
+    h = _mk(ctx, ctx.lib.mpeig_op_lap3d_slab_diag, nx, ny, nz_global, z0, nz_local, dl.ctypes.data)
+    return Operator(ctx, h, n, "ks_slab")
+
+
 def laplace3d_slab(nx: int, ny: int, nz_global: int, z0: int, nz_local: int,
                    ctx: Context = None) -> Operator:
     """This rank's z-slab of the 7-point Laplacian (row-sharded; the context

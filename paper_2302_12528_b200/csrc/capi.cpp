@@ -255,6 +255,39 @@ int mpeig_op_lap3d_slab(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz_globa
   });
 }
 
+namespace {
+// the variable diagonal (6 + V_i) of a 7-pt operator: host copy, fp64 and
+// to_lower'd fp32 device copies
+void attach_diag(mpeig_ctx* ctx, mpeig_op* op, const double* diag_host) {
+  const int64_t n = op->n;
+  op->dg_host.assign(diag_host, diag_host + n);
+  cudaStream_t s = ctx->stream;
+  op->dgw = upload(diag_host, static_cast<size_t>(n), s);
+  std::vector<float> dl;
+  op->lower_overflow = !narrow(diag_host, static_cast<size_t>(n), dl);
+  op->dgl = upload(dl.data(), dl.size(), s);
+  MPB_CUDA(cudaStreamSynchronize(s));
+}
+}  // namespace
+
+int mpeig_op_lap3d_slab_diag(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz_global, int64_t z0,
+                             int64_t nz_local, const double* diag_local_host, mpeig_op** out) {
+  mpeig_op* op = nullptr;
+  int rc = mpeig_op_lap3d_slab(ctx, nx, ny, nz_global, z0, nz_local, &op);
+  if (rc != MPEIG_OK) return rc;
+  rc = guard(ctx, [&] {
+    set_device(ctx);
+    if (!diag_local_host) throw Error(MPEIG_E_CONFIG, "lap3d_slab_diag: null diagonal");
+    attach_diag(ctx, op, diag_local_host);
+  });
+  if (rc != MPEIG_OK) {
+    mpeig_op_destroy(op);
+    return rc;
+  }
+  *out = op;
+  return MPEIG_OK;
+}
+
 int mpeig_op_lap3d_diag(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, const double* diag_host,
                         mpeig_op** out) {
   return guard(ctx, [&] {
@@ -266,13 +299,7 @@ int mpeig_op_lap3d_diag(mpeig_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, cons
     op->nx = nx;
     op->ny = ny;
     op->nz = nz;
-    op->dg_host.assign(diag_host, diag_host + n);
-    cudaStream_t s = ctx->stream;
-    op->dgw = upload(diag_host, static_cast<size_t>(n), s);
-    std::vector<float> dl;
-    op->lower_overflow = !narrow(diag_host, static_cast<size_t>(n), dl);
-    op->dgl = upload(dl.data(), dl.size(), s);
-    MPB_CUDA(cudaStreamSynchronize(s));
+    attach_diag(ctx, op, diag_host);
     *out = op;
   });
 }

@@ -70,8 +70,9 @@ def test_nccl_id_broadcast_world2():
 # ------------------------------------------------------------------ GPU
 
 
-def _run_ranks(nranks, dims, fn):
-    """fn(rank, ctx, op_slab) on `nranks` threads sharing one HostGroup."""
+def _run_ranks(nranks, dims, fn, ks_seed=None):
+    """fn(rank, ctx, op_slab) on `nranks` threads sharing one HostGroup
+    (ks_seed: the slab of cfg5's -Laplacian + V instead of the Laplacian)."""
     import torch
     nx, ny, nz = dims
     group = mp.HostGroup(nranks)
@@ -83,7 +84,8 @@ def _run_ranks(nranks, dims, fn):
             ctx = mp.Context(0, stream=torch.cuda.Stream())
             ctx.attach_host(group, r)
             z0, nl = slabs[r]
-            A = mp.laplace3d_slab(nx, ny, nz, z0, nl, ctx=ctx)
+            A = (mp.laplace3d_slab(nx, ny, nz, z0, nl, ctx=ctx) if ks_seed is None else
+                 mp.ks_hamiltonian_slab(nx, ny, nz, z0, nl, seed=ks_seed, ctx=ctx))
             out[r] = fn(r, ctx, A)
         except Exception as e:  # pragma: no cover - surfaced below
             errs.append(e)
@@ -116,6 +118,26 @@ def test_sharded_stencil_apply_bitwise(gpu, nranks, dims):
         return mp.to_host(A.apply(mp.to_device(Xl)))
 
     parts = _run_ranks(nranks, dims, fn)
+    assert np.array_equal(np.vstack(parts), Y)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nranks,dims", [(2, (9, 8, 13)), (3, (16, 8, 21))])
+def test_sharded_ks_apply_bitwise(gpu, nranks, dims):
+    """The row-sharded variable-diagonal (cfg5) operator == its global apply,
+    bit for bit, with the overlapped halo exchange."""
+    n = int(np.prod(dims))
+    X = np.asfortranarray(np.random.default_rng(4).standard_normal((n, 3)))
+    Y = mp.to_host(gpu.ks_hamiltonian(*dims, seed=2).apply(mp.to_device(X)))
+    sl = mp.slab_partition(dims[2], nranks)
+    plane = dims[0] * dims[1]
+
+    def fn(r, ctx, A):
+        z0, nl = sl[r]
+        Xl = np.asfortranarray(X[z0 * plane:(z0 + nl) * plane])
+        return mp.to_host(A.apply(mp.to_device(Xl)))
+
+    parts = _run_ranks(nranks, dims, fn, ks_seed=2)
     assert np.array_equal(np.vstack(parts), Y)
 
 
