@@ -814,6 +814,7 @@ int mpeig_gemm_f64(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, double alpha
 
 int mpeig_set_process_option(const char* key, int value) {
   const std::string k = key ? key : "";
+  if (k == "gram_tma") { g_gram_tma = value; return MPEIG_OK; }
   if (k == "tc_nprod") { g_tc_nprod = value; return MPEIG_OK; }
   if (k == "tc_store") { g_tc_store = value; return MPEIG_OK; }
   if (k == "gram_tc" || k == "gemm_tc" || k == "tc") {

@@ -22,6 +22,7 @@
 //     of the next stage overlaps the MMAs of this one (double-buffered);
 //   * epilogue: tcgen05.ld (32x32b) -- thread = output row -- to the chunk's
 //     partial, reduced GPU-wide by the deterministic combine of dense.cu.
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -326,6 +327,211 @@ k_gram_tc(int64_t n, int ka, int kb, const float* __restrict__ A, int64_t lda,
 }
 
 
+// ---- the binary32 Gram with TMA-fed stages -----------------------------------
+// Same MMA scheme as k_gram_tc, but the fp32 tiles of A and B are brought in by
+// the Tensor Memory Accelerator: one elected lane of warp 0 issues the 2-D
+// box loads (32 rows x <= 128 columns, 128-B swizzled: conflict-free splits)
+// into a 4-deep ring of fp32 stages, completion tracked by mbarrier
+// transaction counts.  No thread holds in-flight data, so the ring keeps up
+// to four stages (128 KB per SM) in flight -- the register / cp.async
+// loaders topped out near 2.7 TB/s for lack of bytes in flight.
+// Warps 1..8 split a landed stage into the bf16 parts; warp 9 issues the MMAs.
+constexpr int kTmN = 128, kTmKC = 32, kTmRing = 4;
+constexpr int kTmStage = (kTcM + kTmN) * kTmKC * 4;            // fp32 bytes per ring stage
+constexpr int kTmPartA = kTcM * kTmKC * 2, kTmPartB = kTmN * kTmKC * 2;
+constexpr int kTmBuf = 3 * (kTmPartA + kTmPartB);
+constexpr int kTmSmem = kTmRing * kTmStage + 2 * kTmBuf + 1024 + 128;  // + alignment, barriers
+constexpr int kTmSplitThreads = 256;
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes));
+}
+
+__global__ void __launch_bounds__(kTmSplitThreads + 64, 1)
+k_gram_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           int64_t n, int ka, int kb, int tiles_n, int ntile, float* __restrict__ part) {
+  extern __shared__ unsigned char tsm_raw[];
+  // 1024-B alignment for the 128-B swizzled TMA boxes
+  unsigned char* tsm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  unsigned char* ring = tsm;
+  unsigned char* split = tsm + kTmRing * kTmStage;
+  uint64_t* tfull = reinterpret_cast<uint64_t*>(split + 2 * kTmBuf);  // TMA landed
+  uint64_t* tempty = tfull + kTmRing;                                 // stage split
+  uint64_t* sfull = tempty + kTmRing;                                 // split stored
+  uint64_t* sempty = sfull + 2;                                       // MMAs done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 2);
+  constexpr uint32_t kAcc1 = kTmN;
+
+  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
+  const int i0 = tm * kTcM, j0 = tn * ntile;
+  const int N = ntile;
+  const int64_t nchunk = gridDim.y;
+  const int64_t nblk = (n + kTmKC - 1) / kTmKC;
+  const int nst = static_cast<int>(blockIdx.y < nblk ? (nblk - blockIdx.y + nchunk - 1) / nchunk : 0);
+  auto stage_row = [&](int st) -> int { return static_cast<int>((st * nchunk + blockIdx.y) * kTmKC); };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(2 * kTmN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kTmRing; ++q) {
+      mbar_init(&tfull[q], 1);
+      mbar_init(&tempty[q], kTmSplitThreads);
+    }
+    mbar_init(&sfull[0], kTmSplitThreads);
+    mbar_init(&sfull[1], kTmSplitThreads);
+    mbar_init(&sempty[0], 1);
+    mbar_init(&sempty[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)));
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)));
+  }
+  for (int e = threadIdx.x; e < 2 * kTmBuf / 16; e += blockDim.x)
+    reinterpret_cast<uint4*>(split)[e] = make_uint4(0, 0, 0, 0);
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t idesc = idesc_bf16(N);
+
+  if (warp == 0) {
+    // ---- TMA producer
+    if (lane == 0) {
+      const uint32_t bytes = static_cast<uint32_t>((kTcM + N) * kTmKC * 4);
+      for (int st = 0; st < nst; ++st) {
+        const int slot = st % kTmRing;
+        if (st >= kTmRing) mbar_wait(&tempty[slot], ((st / kTmRing) - 1) & 1);
+        mbar_expect_tx(&tfull[slot], bytes);
+        const uint32_t dst = smem_u32(ring + slot * kTmStage);
+        const uint32_t bar = smem_u32(&tfull[slot]);
+        tma_load_2d(dst, &tmA, stage_row(st), i0, bar);
+        tma_load_2d(dst + kTcM * kTmKC * 4, &tmB, stage_row(st), j0, bar);
+      }
+    }
+  } else if (warp == 1 + kTmSplitThreads / 32) {
+    // ---- MMA issuer
+    if (lane == 0) {
+      for (int st = 0; st < nst; ++st) {
+        const int buf = st & 1;
+        mbar_wait(&sfull[buf], (st >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        const uint32_t a0 = smem_u32(split + buf * kTmBuf), b0 = a0 + 3 * kTmPartA;
+        constexpr int pa_of[kTcProducts] = {0, 0, 1, 0, 1, 2, 1, 2};
+        constexpr int pb_of[kTcProducts] = {0, 1, 0, 2, 1, 0, 2, 1};
+        const uint32_t part_b = static_cast<uint32_t>(N * kTmKC * 2);
+#pragma unroll
+        for (int pr = 0; pr < kTcProducts; ++pr)
+#pragma unroll
+          for (int kk = 0; kk < kTmKC / 16; ++kk) {
+            const uint64_t ad = umma_desc(a0 + pa_of[pr] * kTmPartA + kk * 256, 128, 512);
+            const uint64_t bd = umma_desc(b0 + pb_of[pr] * part_b + kk * 256, 128, 512);
+            if (pr == 0)
+              mma_bf16(tmem, ad, bd, idesc, (st | kk) != 0);
+            else
+              mma_bf16(tmem + kAcc1, ad, bd, idesc, (st | (pr - 1) | kk) != 0);
+          }
+        mma_commit(&sempty[buf]);
+      }
+    }
+  } else {
+    // ---- split warps: item = (8-column group g, row half hq); lane (cl, jl)
+    const int sw = warp - 1;  // 0..7
+    const int cl = lane & 7, jl = lane >> 3;
+    const int ncols = kTcM + N;
+    const int nitems = ncols / 8 * 2;
+    constexpr int kSlots = (kTcM + kTmN) / 8 * 2 / (kTmSplitThreads / 32);
+    int roff[kSlots], soff[kSlots], sprt[kSlots];
+    bool live[kSlots];
+#pragma unroll
+    for (int q = 0; q < kSlots; ++q) {
+      const int it = sw + (kTmSplitThreads / 32) * q;
+      const int g = it >> 1, hq = it & 1;
+      const int col = g * 8 + cl, ch = jl + 4 * hq;
+      const bool isa = col < kTcM;
+      const int c = isa ? col : col - kTcM;
+      live[q] = it < nitems && (isa ? i0 + c < ka : (c < N && j0 + c < kb));
+      // the box row of column col is 128 B; its 16-B chunk ch sits at ch ^ (col & 7)
+      roff[q] = col * 128 + ((ch ^ (col & 7)) << 4);
+      soff[q] = (isa ? 0 : 3 * kTmPartA) + (c >> 3) * 512 + (ch >> 1) * 128 + (c & 7) * 16 + (ch & 1) * 8;
+      sprt[q] = isa ? kTmPartA : N * kTmKC * 2;
+    }
+    for (int st = 0; st < nst; ++st) {
+      const int slot = st % kTmRing, buf = st & 1;
+      mbar_wait(&tfull[slot], (st / kTmRing) & 1);
+      if (st >= 2) mbar_wait(&sempty[buf], ((st >> 1) - 1) & 1);
+      const unsigned char* rs = ring + slot * kTmStage;
+      unsigned char* bp = split + buf * kTmBuf;
+#pragma unroll
+      for (int q = 0; q < kSlots; ++q) {
+        if (!live[q]) continue;
+        const float4 v = *reinterpret_cast<const float4*>(rs + roff[q]);
+        uint32_t h0, m0, l0, h1, m1, l1, h2, m2, l2, h3, m3, l3;
+        split3(v.x, h0, m0, l0);
+        split3(v.y, h1, m1, l1);
+        split3(v.z, h2, m2, l2);
+        split3(v.w, h3, m3, l3);
+        unsigned char* d = bp + soff[q];
+        *reinterpret_cast<uint2*>(d) = make_uint2(pack_hi(h0, h1), pack_hi(h2, h3));
+        *reinterpret_cast<uint2*>(d + sprt[q]) = make_uint2(pack_hi(m0, m1), pack_hi(m2, m3));
+        *reinterpret_cast<uint2*>(d + 2 * sprt[q]) = make_uint2(pack_hi(l0, l1), pack_hi(l2, l3));
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n");
+      mbar_arrive(&sfull[buf]);
+      mbar_arrive(&tempty[slot]);
+    }
+    if (nst >= 1) mbar_wait(&sempty[(nst - 1) & 1], ((nst - 1) >> 1) & 1);
+    if (nst >= 2) mbar_wait(&sempty[(nst - 2) & 1], ((nst - 2) >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    // epilogue: split warp w: TMEM lane quarter w % 4, column half w / 4
+    float* out = part + static_cast<int64_t>(blockIdx.y) * ka * kb;
+    const int quarter = warp & 3;  // the hardware lane quarter of this warp
+    const int half = sw >> 2;
+    const int i = i0 + 32 * quarter + lane;
+    const int cbeg = half * (N / 2), cend = cbeg + N / 2;
+    for (int c0 = cbeg; c0 < cend; c0 += 8) {
+      uint32_t v[8], w[8];
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + c0;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                     "=r"(v[6]), "=r"(v[7])
+                   : "r"(taddr));
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                   : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
+                     "=r"(w[6]), "=r"(w[7])
+                   : "r"(taddr + kAcc1));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+      if (i < ka) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int j = j0 + c0 + q;
+          if (j < kb && c0 + q < N)
+            out[i + static_cast<int64_t>(j) * ka] = __uint_as_float(v[q]) + __uint_as_float(w[q]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "r"(2 * kTmN));
+}
+
 // ---- Y = beta Z + alpha A C on tcgen05 ---------------------------------------
 // CTA = 128 rows of Y (MMA M) x one N-wide column tile (N <= 128); K (= k,
 // the columns of A) in stages of 32.  A's tile is M-contiguous in memory, so
@@ -599,6 +805,41 @@ bool gram_tc_eligible(int64_t n, int64_t ka, int64_t kb, int64_t lda, int64_t ld
          ka >= 1 && kb >= 1;
 }
 
+namespace {
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiled encode_tiled() {
+  static EncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiled>(p);
+  }();
+  return fn;
+}
+
+// 2-D map of a column-major rows x cols fp32 block (ld elements between
+// columns), boxes of 32 rows x box_cols columns, 128-B swizzle
+bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld,
+              int box_cols) {
+  EncodeTiled enc = encode_tiled();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kTmKC), static_cast<cuuint32_t>(box_cols)};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+int g_gram_tma = 1;
+
 // Chunk partials of G = A^T B (ka x kb each, column-major, ld ka) into part,
 // nchunk row chunks; returns nchunk (the caller's deterministic combine sums them).
 int64_t gram_tc_f32(int64_t n, int64_t ka, const float* A, int64_t lda, int64_t kb, const float* B,
@@ -621,6 +862,25 @@ int64_t gram_tc_f32(int64_t n, int64_t ka, const float* A, int64_t lda, int64_t 
     MPB_LAUNCH_CHECK();
     return nchunk;
   };
+  if (g_gram_tma && n < (int64_t(1) << 31)) {
+    // TMA-fed stages: B tiles up to 128 wide (240 = 2 x 120)
+    const int64_t tiles_m = ceil_div(ka, kTcM), tiles_n = ceil_div(kb, kTmN);
+    const int64_t ntile = round_up(ceil_div(kb, tiles_n), 16);
+    CUtensorMap ma, mb;
+    if (make_map(&ma, A, n, ka, lda, kTcM) && make_map(&mb, B, n, kb, ldb, static_cast<int>(ntile))) {
+      const int64_t tiles = tiles_m * tiles_n;
+      int64_t nchunk = std::max<int64_t>(1, kNumSMs / tiles);
+      nchunk = std::min(nchunk, std::max<int64_t>(1, max_chunks));
+      nchunk = std::min(nchunk, ceil_div(n, kTmKC));
+      smem_opt_in(reinterpret_cast<const void*>(k_gram_tma), kTmSmem);
+      const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(nchunk));
+      k_gram_tma<<<grid, kTmSplitThreads + 64, kTmSmem, s>>>(ma, mb, n, static_cast<int>(ka),
+                                                           static_cast<int>(kb), static_cast<int>(tiles_n),
+                                                           static_cast<int>(ntile), part);
+      MPB_LAUNCH_CHECK();
+      return nchunk;
+    }
+  }
   if (kb <= 128) return go(std::integral_constant<int, 128>(), std::integral_constant<int, 32>());
   return go(std::integral_constant<int, 256>(), std::integral_constant<int, 16>());
 }
