@@ -356,14 +356,13 @@ def run_ours(args):
         prof = mp.profile.report()
     # ---- the north-star target's per-iteration time at this N (cfg4: 256^3,
     # k = 64, m = 80, row-sharded over the N GPUs; evidence key, all ranks)
-    cfg4 = None
-    # (N > 1: the per-GPU share of 256^3; at N = 1 the whole 16.8M-row problem
-    # needs ~150 GB of the 180 GB and is measured by scripts/cfg_run.py instead)
+    at_scale = {}
     if (world > 1 or args.cfg4) and not args.no_at_scale and args.workload == "cfg1" and not args.replicas:
-        try:
-            cfg4 = cfg4_per_iteration(mp, ctx, rank, world, dist, shard)
-        except Exception as exc:  # evidence only: never fail the bench line
-            cfg4 = {"error": f"{type(exc).__name__}: {exc}"}
+        for which in ("cfg4", "cfg5"):
+            try:
+                at_scale[which] = cfg4_per_iteration(mp, ctx, rank, world, dist, shard, which=which)
+            except Exception as exc:  # evidence only: never fail the bench line
+                at_scale[which] = {"error": f"{type(exc).__name__}: {exc}"}
     if rank != 0:
         if dist:
             dist.destroy_process_group()

@@ -76,6 +76,7 @@ def main():
         for name, p, lo, wk, conv, st in ex.map(one, jobs):
             res[name][p] = (lo, wk, conv, st)
             print(f"{name} p={p}: {lo}+{wk} conv={conv} status={st}", flush=True)
+    env = json.load(open(OUT)) if os.path.exists(OUT) else {}  # merge with concurrent runs
     for c in cases:
         r = res[c]
         env[c] = {"ref": list(r[0][:2]), "npert": a.npert,
