@@ -793,6 +793,227 @@ k_gemm_tc(int64_t n, int k, int c, int ntile, int tiles_n, int64_t ntiles, float
                  "r"(2 * kGmN));
 }
 
+
+// ---- the binary32 block update with TMA-fed stages ----------------------------
+// k_gemm_tc's scheme (persistent CTAs over 128-row tiles, K in stages of 32,
+// two TMEM accumulators) with the fp32 tiles brought in by TMA: A's box is
+// 128 rows x 32 columns (row-contiguous, unswizzled), C's 32 k-rows x N
+// columns (128-B swizzled).  A's bf16 parts use the MN-major core-matrix
+// layout with a 528-B group stride (16 B of padding per 8-row group), so the
+// split's stores are conflict-free.
+constexpr int kGtN = 128, kGtKC = 32, kGtRing = 4;
+constexpr int kGtStageA = kGtKC * kTcM * 4;   // [k][128 rows] fp32
+constexpr int kGtStage = kGtStageA + kGtN * kGtKC * 4;
+constexpr int kGtSbo = 528;
+constexpr int kGtPartA = (kTcM / 8) * kGtSbo, kGtPartC = kGtN * kGtKC * 2;
+constexpr int kGtBuf = 3 * (kGtPartA + kGtPartC);
+constexpr int kGtSmem = kGtRing * kGtStage + 2 * kGtBuf + 1024 + 128;
+static_assert(kGtSmem <= 232448, "k_gemm_tma shared memory");
+
+__global__ void __launch_bounds__(kTmSplitThreads + 64, 1)
+k_gemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
+           int64_t n, int k, int c, int ntile, int tiles_n, int64_t ntiles, float alpha, float beta,
+           const float* Z, int64_t ldz, float* Y, int64_t ldy) {
+  extern __shared__ unsigned char gsm_raw[];
+  unsigned char* gsm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  unsigned char* ring = gsm;
+  unsigned char* split = gsm + kGtRing * kGtStage;
+  uint64_t* tfull = reinterpret_cast<uint64_t*>(split + 2 * kGtBuf);
+  uint64_t* tempty = tfull + kGtRing;
+  uint64_t* sfull = tempty + kGtRing;
+  uint64_t* sempty = sfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 2);
+  constexpr uint32_t kAcc1 = kGtN;
+  const int N = ntile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(2 * kGtN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kGtRing; ++q) {
+      mbar_init(&tfull[q], 1);
+      mbar_init(&tempty[q], kTmSplitThreads);
+    }
+    mbar_init(&sfull[0], kTmSplitThreads);
+    mbar_init(&sfull[1], kTmSplitThreads);
+    mbar_init(&sempty[0], 1);
+    mbar_init(&sempty[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)));
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmC)));
+  }
+  for (int e = threadIdx.x; e < 2 * kGtBuf / 16; e += blockDim.x)
+    reinterpret_cast<uint4*>(split)[e] = make_uint4(0, 0, 0, 0);
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = *tmem_slot;
+  const int nst = (k + kGtKC - 1) / kGtKC;
+  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t total = my_tiles * nst;
+  auto tile_of = [&](int64_t g) { return blockIdx.x + (g / nst) * gridDim.x; };
+  // bf16 x bf16 -> f32, A MN-major (bit 15), B K-major
+  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
+                         (static_cast<uint32_t>(N >> 3) << 17) |
+                         (static_cast<uint32_t>(kTcM >> 4) << 24);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t bytes = static_cast<uint32_t>(kGtStageA + N * kGtKC * 4);
+      for (int64_t g = 0; g < total; ++g) {
+        const int slot = static_cast<int>(g % kGtRing);
+        if (g >= kGtRing) mbar_wait(&tempty[slot], static_cast<uint32_t>(((g / kGtRing) - 1) & 1));
+        const int64_t t = tile_of(g);
+        const int row0 = static_cast<int>((t / tiles_n) * kTcM);
+        const int j0 = static_cast<int>(t % tiles_n) * N;
+        const int k0 = static_cast<int>(g % nst) * kGtKC;
+        mbar_expect_tx(&tfull[slot], bytes);
+        const uint32_t dst = smem_u32(ring + slot * kGtStage);
+        const uint32_t bar = smem_u32(&tfull[slot]);
+        tma_load_2d(dst, &tmA, row0, k0, bar);
+        tma_load_2d(dst + kGtStageA, &tmC, k0, j0, bar);
+      }
+    }
+  } else if (warp == 1 + kTmSplitThreads / 32) {
+    if (lane == 0) {
+      for (int64_t g = 0; g < total; ++g) {
+        const int buf = static_cast<int>(g & 1);
+        const int st = static_cast<int>(g % nst);
+        mbar_wait(&sfull[buf], static_cast<uint32_t>((g >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        const uint32_t a0 = smem_u32(split + buf * kGtBuf), c0 = a0 + 3 * kGtPartA;
+        constexpr int pa_of[kTcProducts] = {0, 0, 1, 0, 1, 2, 1, 2};
+        constexpr int pb_of[kTcProducts] = {0, 1, 0, 2, 1, 0, 2, 1};
+#pragma unroll
+        for (int pr = 0; pr < kTcProducts; ++pr)
+#pragma unroll
+          for (int kk = 0; kk < kGtKC / 16; ++kk) {
+            const uint64_t ad = umma_desc(a0 + pa_of[pr] * kGtPartA + kk * 256, 128, kGtSbo);
+            const uint64_t bd = umma_desc(c0 + pb_of[pr] * kGtPartC + kk * 256, 128, 512);
+            if (pr == 0)
+              mma_bf16(tmem, ad, bd, idesc, (st | kk) != 0);
+            else
+              mma_bf16(tmem + kAcc1, ad, bd, idesc, (st | (pr - 1) | kk) != 0);
+          }
+        mma_commit(&sempty[buf]);
+      }
+    }
+  } else {
+    const int sw = warp - 1;
+    const int cl = lane & 7, jl = lane >> 3;
+    // C items (K-major, the Gram's B mapping): column 8 g + cl, float4 ch
+    constexpr int kCSlots = kGtN / 8 * 2 / (kTmSplitThreads / 32);
+    int croff[kCSlots], csoff[kCSlots];
+    bool clive[kCSlots];
+#pragma unroll
+    for (int q = 0; q < kCSlots; ++q) {
+      const int it = sw + (kTmSplitThreads / 32) * q;
+      const int g = it >> 1, hq = it & 1;
+      const int col = 8 * g + cl, ch = jl + 4 * hq;
+      clive[q] = col < N;
+      croff[q] = kGtStageA + col * 128 + ((ch ^ (col & 7)) << 4);
+      csoff[q] = 3 * kGtPartA + (col >> 3) * 512 + (ch >> 1) * 128 + (col & 7) * 16 + (ch & 1) * 8;
+    }
+    constexpr int kAItems = kGtKC * (kTcM / 8) / kTmSplitThreads;  // (k, 8-row group) items
+    auto epilogue = [&](int64_t t) {
+      const int64_t i0 = (t / tiles_n) * kTcM;
+      const int j0 = static_cast<int>(t % tiles_n) * N;
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      const int quarter = warp & 3, half = sw >> 2;
+      const int64_t i = i0 + 32 * quarter + lane;
+      const int cbeg = half * (N / 2), cend = cbeg + N / 2;
+      for (int cc = cbeg; cc < cend; cc += 8) {
+        uint32_t v[8], w[8];
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + cc;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                       "=r"(v[6]), "=r"(v[7])
+                     : "r"(taddr));
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
+                       "=r"(w[6]), "=r"(w[7])
+                     : "r"(taddr + kAcc1));
+        float z[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int j = j0 + cc + q;
+          z[q] = (beta != 0.f && i < n && j < c && cc + q < cend) ? Z[i + static_cast<int64_t>(j) * ldz] : 0.f;
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+        if (i < n) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int j = j0 + cc + q;
+            if (j < c && cc + q < cend) {
+              float y = alpha * (__uint_as_float(v[q]) + __uint_as_float(w[q]));
+              if (beta != 0.f) y = fmaf(beta, z[q], y);
+              Y[i + static_cast<int64_t>(j) * ldy] = y;
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n");
+    };
+    for (int64_t g = 0; g < total; ++g) {
+      const int slot = static_cast<int>(g % kGtRing), buf = static_cast<int>(g & 1);
+      mbar_wait(&tfull[slot], static_cast<uint32_t>((g / kGtRing) & 1));
+      if (g >= 2) mbar_wait(&sempty[buf], static_cast<uint32_t>(((g >> 1) - 1) & 1));
+      const unsigned char* rs = ring + slot * kGtStage;
+      unsigned char* bp = split + buf * kGtBuf;
+      // A -> MN-major: item (row group gm fastest, column kc): 8 rows of column kc
+#pragma unroll
+      for (int q = 0; q < kAItems; ++q) {
+        const int e = (threadIdx.x - 32) + kTmSplitThreads * q;
+        const int gm = e % (kTcM / 8), kc = e / (kTcM / 8);
+        const float4 v0 = *reinterpret_cast<const float4*>(rs + kc * (kTcM * 4) + gm * 32);
+        const float4 v1 = *reinterpret_cast<const float4*>(rs + kc * (kTcM * 4) + gm * 32 + 16);
+        const float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        uint32_t h[8], m[8], l[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) split3(f[t], h[t], m[t], l[t]);
+        const int off = gm * kGtSbo + (kc >> 3) * 128 + (kc & 7) * 16;
+        *reinterpret_cast<uint4*>(bp + off) =
+            make_uint4(pack_hi(h[0], h[1]), pack_hi(h[2], h[3]), pack_hi(h[4], h[5]), pack_hi(h[6], h[7]));
+        *reinterpret_cast<uint4*>(bp + kGtPartA + off) =
+            make_uint4(pack_hi(m[0], m[1]), pack_hi(m[2], m[3]), pack_hi(m[4], m[5]), pack_hi(m[6], m[7]));
+        *reinterpret_cast<uint4*>(bp + 2 * kGtPartA + off) =
+            make_uint4(pack_hi(l[0], l[1]), pack_hi(l[2], l[3]), pack_hi(l[4], l[5]), pack_hi(l[6], l[7]));
+      }
+#pragma unroll
+      for (int q = 0; q < kCSlots; ++q) {
+        if (!clive[q]) continue;
+        const float4 v = *reinterpret_cast<const float4*>(rs + croff[q]);
+        uint32_t h0, m0, l0, h1, m1, l1, h2, m2, l2, h3, m3, l3;
+        split3(v.x, h0, m0, l0);
+        split3(v.y, h1, m1, l1);
+        split3(v.z, h2, m2, l2);
+        split3(v.w, h3, m3, l3);
+        unsigned char* d = bp + csoff[q];
+        *reinterpret_cast<uint2*>(d) = make_uint2(pack_hi(h0, h1), pack_hi(h2, h3));
+        *reinterpret_cast<uint2*>(d + kGtPartC) = make_uint2(pack_hi(m0, m1), pack_hi(m2, m3));
+        *reinterpret_cast<uint2*>(d + 2 * kGtPartC) = make_uint2(pack_hi(l0, l1), pack_hi(l2, l3));
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n");
+      mbar_arrive(&sfull[buf]);
+      mbar_arrive(&tempty[slot]);
+      if (g % nst == nst - 1) {
+        mbar_wait(&sempty[buf], static_cast<uint32_t>((g >> 1) & 1));
+        epilogue(tile_of(g));
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "r"(2 * kGtN));
+}
+
 }  // namespace
 
 int g_gram_tc = 1, g_gemm_tc = 1;
@@ -824,6 +1045,21 @@ EncodeTiled encode_tiled() {
 
 // 2-D map of a column-major rows x cols fp32 block (ld elements between
 // columns), boxes of 32 rows x box_cols columns, 128-B swizzle
+// general: boxes of box_rows x box_cols, 128-B swizzle or none
+bool make_map_rows(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld,
+                   int box_rows, int box_cols, bool swizzle) {
+  EncodeTiled enc = encode_tiled();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(box_cols)};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld,
               int box_cols) {
   EncodeTiled enc = encode_tiled();
@@ -894,6 +1130,28 @@ bool gemm_tc_eligible(int64_t n, int64_t k, int64_t c, int64_t lda, int64_t ldc,
 void gemm_tc_f32(int64_t n, int64_t k, int64_t c, float alpha, const float* A, int64_t lda,
                  const float* C, int64_t ldc, float beta, const float* Z, int64_t ldz, float* Y,
                  int64_t ldy, const float* A2, float* Y2, cudaStream_t s) {
+  if (g_gram_tma && n < (int64_t(1) << 31) && k < (int64_t(1) << 31)) {
+    // TMA-fed stages; the paired product (A2 C -> Y2) as a second launch
+    const int64_t tiles_n = ceil_div(c, kGtN);
+    const int64_t ntile = round_up(ceil_div(c, tiles_n), 16);
+    const int64_t tiles = ceil_div(n, kTcM) * tiles_n;
+    CUtensorMap mc;
+    bool ok = make_map_rows(&mc, C, k, c, ldc, kGtKC, static_cast<int>(ntile), true);
+    for (int z = 0; ok && z < (A2 ? 2 : 1); ++z) {
+      CUtensorMap ma;
+      if (!make_map_rows(&ma, z ? A2 : A, n, k, lda, kTcM, kGtKC, false)) {
+        ok = false;
+        break;
+      }
+      smem_opt_in(reinterpret_cast<const void*>(k_gemm_tma), kGtSmem);
+      const int64_t ctas = std::min<int64_t>(tiles, kNumSMs);
+      k_gemm_tma<<<static_cast<unsigned>(ctas), kTmSplitThreads + 64, kGtSmem, s>>>(
+          ma, mc, n, static_cast<int>(k), static_cast<int>(c), static_cast<int>(ntile),
+          static_cast<int>(tiles_n), tiles, alpha, beta, Z, ldz, z ? Y2 : Y, ldy);
+      MPB_LAUNCH_CHECK();
+    }
+    if (ok) return;
+  }
   const int64_t tiles_n = ceil_div(c, kGmN);
   const int64_t ntile = round_up(ceil_div(c, tiles_n), 16);
   const int64_t tiles = ceil_div(n, kTcM) * tiles_n;
