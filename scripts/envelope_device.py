@@ -19,7 +19,8 @@ cases = sys.argv[1:] or ["lap3d8-dlobpcg-dchol", "lap3d8-dlobpcg-schol", "lap3d8
                          "lap3d16-dlobpcg-dchol", "lap3d16-dlobpcg-schol", "lap3d16-mplobpcg-schol",
                          "lap2d50-mplobpcg-schol", "dense256-dlobpcg-dchol", "dense256-mplobpcg-schol",
                          "lap2d5x500-mplobpcg-schol", "cfg1-mplobpcg-schol", "cfg1-dlobpcg-dchol",
-                         "cfg1-dlobpcg-schol"]
+                         "cfg1-dlobpcg-schol", "lap2d64k32-dlobpcg-dchol", "lap2d64k32-mplobpcg-schol",
+                         "lap2d128k32-dlobpcg-dchol", "ks32-dlobpcg-dchol", "ks32-mplobpcg-schol"]
 out = {}
 for c in cases:
     env = envelope(c)
