@@ -924,6 +924,24 @@ void orthonormal_q(Work<T>& w, int64_t m, T* W, int64_t ldw, bool use_mixed) {
               st == MPEIG_E_RANK_DEFICIENT || st == MPEIG_E_SINGULAR_TRI ? idx : m - 1);
 }
 
+// Q in place by two Cholesky-QR passes, the first guarded on the equilibrated
+// pivots (cholqr_tau2); true on success, W untouched otherwise (the caller then
+// runs the reference's QR chain).  Q of a full-rank W is unique to rounding, so
+// this is the reference's mixed_qr / householder_qr Q without the TSQR's
+// column-serial chain.
+template <typename T>
+static bool guarded_cholqr2(Work<T>& w, int64_t m, T* W, int64_t ldw) {
+  cudaStream_t s = w.s;
+  status_clear(w.ctx);
+  gram_chol<T>(w, m, w.ctx->d_status, W, ldw, cholqr_tau2<T>(w.ctx));
+  gemm_tn<T>(w.n, m, m, T(1), W, ldw, w.Uinv(), m, T(0), nullptr, 0, w.V.p, w.ld, s);
+  gram_chol<T>(w, m, w.ctx->d_status);
+  status_fetch(w.ctx);
+  if (w.ctx->h_status[0] != 0) return false;
+  gemm_tn<T>(w.n, m, m, T(1), w.V.p, w.ld, w.Uinv(), m, T(0), nullptr, 0, W, ldw, s);
+  return true;
+}
+
 // orthonormalize_dropping (ortho.hpp:205-250): two-pass Gram-Schmidt that
 // drops columns whose projected norm falls below drop_tol * original norm.
 template <typename T>
@@ -977,16 +995,7 @@ int64_t orthonormal_q_dropping(Work<T>& w, int64_t m, T* W, int64_t ldw, bool us
     // the guarded Cholesky-QR of qr_spec first (so the eager, careful and
     // speculative paths take identical steps); W is overwritten only when
     // both passes succeed, else the reference's QR chain below runs on it
-    cudaStream_t s = w.s;
-    status_clear(w.ctx);
-    gram_chol<T>(w, m, w.ctx->d_status, W, ldw, cholqr_tau2<T>(w.ctx));
-    gemm_tn<T>(w.n, m, m, T(1), W, ldw, w.Uinv(), m, T(0), nullptr, 0, w.V.p, w.ld, s);
-    gram_chol<T>(w, m, w.ctx->d_status);
-    status_fetch(w.ctx);
-    if (w.ctx->h_status[0] == 0) {
-      gemm_tn<T>(w.n, m, m, T(1), w.V.p, w.ld, w.Uinv(), m, T(0), nullptr, 0, W, ldw, s);
-      return m;
-    }
+    if (guarded_cholqr2<T>(w, m, W, ldw)) return m;
   }
   try {
     orthonormal_q<T>(w, m, W, ldw, use_mixed);
@@ -1579,7 +1588,11 @@ StageResult pinvit(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const double* X
     timer.start();
     copy_block<T>(n, m, Xt, w.ld, w.S.p, w.ld, s);
     try {
-      orthonormal_q<T>(w, m, w.S.p, w.ld, true);
+      // X = orthonormal_q(Xt, true) (eigensolvers.hpp:342-347): the guarded
+      // Cholesky-QR first (the iterate is X minus a small correction, well
+      // conditioned), the reference's mixed_qr chain when the guard fails
+      if (!(ctx->spec_qr && guarded_cholqr2<T>(w, m, w.S.p, w.ld)))
+        orthonormal_q<T>(w, m, w.S.p, w.ld, true);
     } catch (const Error& e) {
       if (e.code == MPEIG_E_RANK_DEFICIENT)
         throw Error(MPEIG_E_RANK_COLLAPSE, "pinvit: iterate block lost rank");
