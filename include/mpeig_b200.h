@@ -377,7 +377,10 @@ int mpeig_gemm_f64(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, double alpha
  *   "gram_tc" / "gemm_tc" / "tc" (both): the binary32 Gram / block update
  *              on the tcgen05 tensor cores (exact 3-way bf16 split, fp32
  *              accumulation): 1 = for products with n * k * c >= 2^28
- *              (default), 0 = never (SIMT FFMA kernels), 2 = always. */
+ *              (default), 0 = never (SIMT FFMA kernels), 2 = always.
+ *   "gram_tma":  TMA-fed tensor-core Gram (1, default) or the cp.async one (0).
+ *   "gemm_tma2": tensor-core block update with C split once per call (1,
+ *              default) or the per-tile split (0; in place only c <= 128). */
 int mpeig_set_process_option(const char* key, int value);
 /* the same two products in binary32 (the lower-precision stage's kernels) */
 int mpeig_gram_f32(mpeig_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda,
@@ -388,7 +391,8 @@ int mpeig_gemm_f32(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, float alpha,
 /* block_project_out (ortho.hpp:190-200): W -= B (B^T W), `passes` times */
 int mpeig_project_out_f64(mpeig_ctx* ctx, int64_t n, int64_t b, const double* B,
                           int64_t ldb, int64_t w, double* W, int64_t ldw, int32_t passes);
-/* small_herm_eig (small_eig.hpp:92-218) on device (cuSOLVER syevd):
+/* small_herm_eig (small_eig.hpp:92-218) on device: the reference's Householder
+ * tridiagonalisation + implicit QL (k_small_ql3) for s <= 96, cuSOLVER syevd above:
  * M device s x s, values (device, ascending), vectors (device s x s) */
 int mpeig_small_eig_f64(mpeig_ctx* ctx, int64_t s, const double* M, double* values,
                         double* vectors);

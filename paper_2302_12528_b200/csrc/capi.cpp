@@ -815,6 +815,10 @@ int mpeig_gemm_f64(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, double alpha
 int mpeig_set_process_option(const char* key, int value) {
   const std::string k = key ? key : "";
   if (k == "gram_tma") { g_gram_tma = value; return MPEIG_OK; }
+  if (k == "gemm_tma2") { g_gemm_tma2 = value; return MPEIG_OK; }
+  if (k == "tc_twoacc") { g_tc_twoacc = value; return MPEIG_OK; }
+  if (k == "tc_ablate") { g_tc_ablate = value; return MPEIG_OK; }
+  if (k == "g2_depth") { g_g2_depth = value; return MPEIG_OK; }
   if (k == "tc_nprod") { g_tc_nprod = value; return MPEIG_OK; }
   if (k == "tc_store") { g_tc_store = value; return MPEIG_OK; }
   if (k == "gram_tc" || k == "gemm_tc" || k == "tc") {

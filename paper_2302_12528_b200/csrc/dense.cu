@@ -787,18 +787,26 @@ bool gram_cholesky(int64_t n, int64_t m, const T* V, int64_t ldv, T* G, T* work,
   return true;
 }
 
+bool gemm_inplace_ok(bool f64, int64_t n, int64_t k, int64_t c) {
+  if (c <= kGemmInplaceCols) return true;
+  if (f64) return c <= 96;
+  return gemm_tc_wanted(n, k, c) && gemm_tc_inplace_ok(c);
+}
+
 template <typename T>
 static void gemm_impl(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, const T* C,
                       int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y, int64_t ldy, const T* A2,
                       T* Y2, cudaStream_t s) {
   const unsigned nz = A2 ? 2u : 1u;
   if (n <= 0 || c <= 0) return;
+  bool inplace = false;
   if (c > kGemmInplaceCols && k > 0) {
     // Y aliasing A: only legal within one output column tile (kernels.cuh)
     const auto lo = [](const T* p) { return reinterpret_cast<uintptr_t>(p); };
     const uintptr_t a0 = lo(A), a1 = lo(A + (k - 1) * lda + n), y0 = lo(Y), y1 = lo(Y + (c - 1) * ldy + n);
-    if (a0 < y1 && y0 < a1)
-      throw Error(MPEIG_E_DIMENSION, "gemm_tn: output overlaps A with more than 64 output columns");
+    inplace = a0 < y1 && y0 < a1;
+    if (inplace && (A2 || !gemm_inplace_ok(sizeof(T) == 8, n, k, c)))
+      throw Error(MPEIG_E_DIMENSION, "gemm_tn: output overlaps A beyond the in-place column limit");
   }
   if (k <= 0) {
     // Y = beta Z
@@ -831,7 +839,7 @@ static void gemm_impl(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int6
       // deep K (the dense operator A X, K = n): one column tile up to 96 wide,
       // so the n x n operand streams from HBM once instead of once per tile
       const bool deep = k > 4 * kDBK;
-      if (deep && c > 16 * nt && c <= 96) nt = static_cast<int>(ceil_div(c, 16));
+      if ((deep || inplace) && c > 16 * nt && c <= 96) nt = static_cast<int>(ceil_div(c, 16));
       const dim3 g2(static_cast<unsigned>(ceil_div(n, kTile)),
                     static_cast<unsigned>(ceil_div(c, 16 * nt)), nz);
       const int ki = static_cast<int>(k), ci = static_cast<int>(c);
@@ -863,6 +871,7 @@ static void gemm_impl(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int6
       MPB_LAUNCH_CHECK();
       return;
     }
+    if (inplace) throw Error(MPEIG_E_DIMENSION, "gemm_tn: in-place product needs 16-B aligned operands");
   }
   if constexpr (sizeof(T) == 4) {
     // binary32 on the tcgen05 tensor cores (tc.cu: exact 3-way bf16 split);
@@ -870,10 +879,9 @@ static void gemm_impl(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int6
     // all of its rows of A, so the Y = A in-place contract (c <= 64) holds
     if (gemm_tc_wanted(n, k, c) && gemm_tc_eligible(n, k, c, lda, ldc, A, C) &&
         (!A2 || gemm_tc_eligible(n, k, c, lda, ldc, A2, C)) &&
-        (c <= 128 || (Y != A && (!A2 || Y2 != A2)))) {
-      gemm_tc_f32(n, k, c, alpha, A, lda, C, ldc, beta, Z, ldz, Y, ldy, A2, Y2, s);
+        gemm_tc_f32(n, k, c, alpha, A, lda, C, ldc, beta, Z, ldz, Y, ldy, A2, Y2, inplace, s))
       return;
-    }
+    if (inplace) throw Error(MPEIG_E_DIMENSION, "gemm_tn: in-place product needs the tensor-core path");
   }
   if (c <= 64 && k <= 1024) {
     const int ct = c <= 16 ? 16 : c <= 32 ? 32 : c <= 48 ? 48 : 64;

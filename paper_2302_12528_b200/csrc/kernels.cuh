@@ -30,6 +30,10 @@ void gram(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb, const T* B
 // reads all of them before it writes; wider outputs span several CTAs per row
 // block and an in-place call would race.
 constexpr int64_t kGemmInplaceCols = 64;
+// Y = A C in place for wider c: binary64 c <= 96 (one DMMA column tile),
+// binary32 c <= 256 on the tensor-core path when it applies (gemm_tn checks)
+bool gemm_inplace_ok(bool f64, int64_t n, int64_t k, int64_t c);
+bool gemm_tc_inplace_ok(int64_t c);
 template <typename T>
 void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, const T* C,
              int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y, int64_t ldy, cudaStream_t s);
@@ -42,13 +46,16 @@ int64_t gram_tc_f32(int64_t n, int64_t ka, const float* A, int64_t lda, int64_t 
 // binary32 Y = beta Z + alpha A C (+ the paired A2 C) on tcgen05 (tc.cu)
 bool gemm_tc_eligible(int64_t n, int64_t k, int64_t c, int64_t lda, int64_t ldc, const float* A,
                       const float* C);
-void gemm_tc_f32(int64_t n, int64_t k, int64_t c, float alpha, const float* A, int64_t lda,
+// returns false (nothing launched) when `inplace` (Y aliases A) and no
+// single-column-tile kernel is available for c
+bool gemm_tc_f32(int64_t n, int64_t k, int64_t c, float alpha, const float* A, int64_t lda,
                  const float* C, int64_t ldc, float beta, const float* Z, int64_t ldz, float* Y,
-                 int64_t ldy, const float* A2, float* Y2, cudaStream_t s);
+                 int64_t ldy, const float* A2, float* Y2, bool inplace, cudaStream_t s);
 // policy: the tensor-core path for Grams big enough to be bandwidth/compute
 // bound (the m = 16 cfg1 shapes stay on the latency-lean SIMT kernel);
 // g_gram_tc: 1 = by size (default), 0 = never, 2 = always (tests)
 extern int g_gram_tc, g_gemm_tc;
+extern int g_gemm_tma2, g_tc_twoacc, g_tc_ablate, g_g2_depth;
 extern int g_tc_nprod, g_tc_store;
 extern int g_gram_tma;  // TMA-fed tensor-core Gram (1, default) or the cp.async one (0)
 // (crossovers measured at n = 2M, scripts/dense_shapes.py: the tensor-core

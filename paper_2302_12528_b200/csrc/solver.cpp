@@ -866,7 +866,7 @@ constexpr T kCholQrSingleTau2 = T(0.25);
 // the product goes through the QR scratch w.V and is copied back.
 template <typename T>
 static void gemm_right_inplace(Work<T>& w, int64_t m, T* W, int64_t ldw, const T* C) {
-  if (m <= kGemmInplaceCols) {
+  if (gemm_inplace_ok(sizeof(T) == 8, w.n, m, m)) {
     gemm_tn<T>(w.n, m, m, T(1), W, ldw, C, m, T(0), nullptr, 0, W, ldw, w.s);
     return;
   }

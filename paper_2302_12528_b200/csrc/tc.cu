@@ -26,6 +26,9 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -1014,6 +1017,303 @@ k_gemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
                  "r"(2 * kGtN));
 }
 
+
+// ---- the binary32 block update, C split once ----------------------------------
+// Y = beta Z + alpha A C with C (k x c, the small coefficient block) split into
+// its bf16 parts ONCE per call by k_csplit, straight into the shared-memory
+// image the MMA reads (per 32-row K stage: 3 parts x N columns, K-major core
+// matrices), so the persistent CTAs only split their A tiles; one column tile
+// up to 256 wide (A is read and split once per row tile).  Roles:
+//   warp 0       TMA producer of A (128 rows x 32 columns, 4-deep ring);
+//   warps 1..8   split A into the MN-major bf16 parts (double-buffered);
+//   warp 9       MMA issuer (8 part products x 2 K-steps per stage);
+//   warps 10..17 epilogue: TMEM -> registers -> Y (two accumulator sets when
+//                4 N <= 512 TMEM columns, so a tile drains while the next one
+//                accumulates);
+//   warp 18      bulk-copies the stage's C image (L2-resident) into a 2-deep
+//                buffer behind the MMAs.
+// Each CTA reads every K column of its rows before the epilogue writes them
+// and one column tile covers all of c, so Y may alias A (in-place V U^-1).
+constexpr int kG2KC = 32, kG2NMax = 256;
+constexpr int kG2StageA = kG2KC * kTcM * 4;
+constexpr int kG2Sbo = 528;
+constexpr int kG2PartA = (kTcM / 8) * kG2Sbo, kG2BufA = 3 * kG2PartA;
+constexpr int kG2Warps = 19, kG2Threads = 32 * kG2Warps;
+constexpr int kG2SplitThreads = 256, kG2EpiThreads = 256;
+__host__ __device__ constexpr int g2_cimg(int N) { return 3 * N * kG2KC * 2; }  // bytes per stage
+// Ring depths (each 2..4) as shared memory allows: R fp32 A stages
+// (TMA, HBM latency), S split A buffers (the split of stage g + S overlaps the
+// MMAs of g + 1 .. g + S - 1), D C images (L2 latency of the bulk copies).
+constexpr int kG2SmemMax = 232448 - 1024;  // less the static shared memory
+struct G2Depth {
+  int R, S, D;
+};
+__host__ __device__ constexpr int g2_smem(int N, G2Depth d) {
+  return d.R * kG2StageA + d.S * kG2BufA + d.D * g2_cimg(N) + 1024 + 256;
+}
+inline G2Depth g2_depth(int N) {
+  // (measured: deeper S and D past 2 change nothing at n = 2M, N = 80 .. 160)
+  constexpr G2Depth pref[] = {{4, 2, 4}, {4, 2, 3}, {4, 2, 2}, {3, 2, 2}, {2, 2, 2}};
+  for (const G2Depth& d : pref)
+    if (g2_smem(N, d) <= kG2SmemMax) return d;
+  return {2, 2, 2};
+}
+static_assert(g2_smem(kG2NMax, G2Depth{3, 3, 2}) <= kG2SmemMax, "k_gemm_tma2 shared memory");
+
+// C image: [tn][st] stage images of 3 parts x N columns x 32 k (bf16), zero
+// beyond k and c; thread = (column, 8-k chunk) of one stage
+__global__ void k_csplit(int k, int c, int N, int nst, int tiles_n, const float* __restrict__ C,
+                         int64_t ldc, unsigned char* __restrict__ img) {
+  const int64_t total = static_cast<int64_t>(tiles_n) * nst * N * (kG2KC / 8);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int kc = static_cast<int>(e % (kG2KC / 8));
+    const int col = static_cast<int>((e / (kG2KC / 8)) % N);
+    const int64_t ts = e / (kG2KC / 8) / N;  // tn * nst + st
+    const int st = static_cast<int>(ts % nst), tn = static_cast<int>(ts / nst);
+    const int j = tn * N + col;
+    uint32_t h[8], m[8], l[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int kk = st * kG2KC + kc * 8 + q;
+      const float x = (kk < k && j < c && col < N) ? C[kk + static_cast<int64_t>(j) * ldc] : 0.f;
+      split3(x, h[q], m[q], l[q]);
+    }
+    unsigned char* d = img + ts * g2_cimg(N) + (col >> 3) * 512 + kc * 128 + (col & 7) * 16;
+    const int part = N * kG2KC * 2;
+    *reinterpret_cast<uint4*>(d) =
+        make_uint4(pack_hi(h[0], h[1]), pack_hi(h[2], h[3]), pack_hi(h[4], h[5]), pack_hi(h[6], h[7]));
+    *reinterpret_cast<uint4*>(d + part) =
+        make_uint4(pack_hi(m[0], m[1]), pack_hi(m[2], m[3]), pack_hi(m[4], m[5]), pack_hi(m[6], m[7]));
+    *reinterpret_cast<uint4*>(d + 2 * part) =
+        make_uint4(pack_hi(l[0], l[1]), pack_hi(l[2], l[3]), pack_hi(l[4], l[5]), pack_hi(l[6], l[7]));
+  }
+}
+
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kG2Threads, 1)
+k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const unsigned char* __restrict__ cimg, int64_t n,
+            int k, int c, int N, int tiles_n, int64_t rtiles, G2Depth dep, int two_acc, int nprod,
+            int ablate, float alpha, float beta, const float* Z, int64_t ldz, float* Y, int64_t ldy) {
+  extern __shared__ unsigned char g2_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(g2_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int cbytes = g2_cimg(N);
+  unsigned char* ring = sm;
+  const int R = dep.R, S = dep.S, D = dep.D;
+  unsigned char* abuf = ring + R * kG2StageA;
+  unsigned char* cbuf = abuf + S * kG2BufA;
+  uint64_t* afull = reinterpret_cast<uint64_t*>(cbuf + D * cbytes);  // [4]: A stage landed
+  uint64_t* aempty = afull + 4;       // [4]: A stage split
+  uint64_t* sfull = aempty + 4;       // [4]: split buffer stored
+  uint64_t* cfull = sfull + 4;        // [4]: C image landed
+  uint64_t* cdone = cfull + 4;        // [4]: MMAs of the image's stage done
+  uint64_t* mdone = cdone + 4;        // [4]: MMAs of the split buffer's stage done
+  uint64_t* accfull = mdone + 4;
+  uint64_t* accempty = accfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // accumulator set = 1 or 2 TMEM accumulators of N columns (the second
+  // collects the 7 smaller part products); two sets when they fit in 512
+  const int set_cols = two_acc ? 2 * N : N;
+  const int nacc = 2 * set_cols <= 512 ? 2 : 1;
+  const uint32_t acc1_off = two_acc ? static_cast<uint32_t>(N) : 0u;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 4; ++q) {
+      mbar_init(&afull[q], 1);
+      mbar_init(&aempty[q], kG2SplitThreads);
+      mbar_init(&cfull[q], 1);
+      mbar_init(&cdone[q], 1);
+      mbar_init(&sfull[q], kG2SplitThreads);
+      mbar_init(&mdone[q], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&accfull[q], 1);
+      mbar_init(&accempty[q], kG2EpiThreads);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)));
+  }
+  for (int e = threadIdx.x; e < S * kG2BufA / 16; e += blockDim.x)
+    reinterpret_cast<uint4*>(abuf)[e] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;\n");
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = *tmem_slot;
+  const int nst = (k + kG2KC - 1) / kG2KC;
+  // local tile tl: row tile blockIdx.x + (tl / tiles_n) * gridDim.x, column
+  // tile tl % tiles_n (a row tile's column tiles back to back: A from L2)
+  const int64_t my_rows = blockIdx.x < rtiles ? (rtiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t my_tiles = my_rows * tiles_n;
+  const int64_t total = my_tiles * nst;
+  auto row_of = [&](int64_t tl) { return blockIdx.x + (tl / tiles_n) * gridDim.x; };
+  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
+                         (static_cast<uint32_t>(N >> 3) << 17) |
+                         (static_cast<uint32_t>(kTcM >> 4) << 24);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int64_t g = 0; g < total; ++g) {
+        const int slot = static_cast<int>(g % R);
+        if (g >= R) mbar_wait(&aempty[slot], static_cast<uint32_t>(((g / R) - 1) & 1));
+        const int row0 = static_cast<int>(row_of(g / nst) * kTcM);
+        const int k0 = static_cast<int>(g % nst) * kG2KC;
+        mbar_expect_tx(&afull[slot], kG2StageA);
+        tma_load_2d(smem_u32(ring + slot * kG2StageA), &tmA, row0, k0, smem_u32(&afull[slot]));
+      }
+    }
+  } else if (warp == kG2Warps - 1) {
+    if (lane == 0) {
+      for (int64_t g = 0; g < total; ++g) {
+        const int cb = static_cast<int>(g % D);
+        if (g >= D) mbar_wait(&cdone[cb], static_cast<uint32_t>(((g / D) - 1) & 1));
+        const int64_t ts = ((g / nst) % tiles_n) * nst + g % nst;
+        if ((ablate & 1) && g >= D) {  // diagnostics: no C reloads
+          mbar_arrive(&cfull[cb]);
+          continue;
+        }
+        mbar_expect_tx(&cfull[cb], static_cast<uint32_t>(cbytes));
+        bulk_load(smem_u32(cbuf + cb * cbytes), cimg + ts * cbytes, static_cast<uint32_t>(cbytes),
+                  smem_u32(&cfull[cb]));
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      const uint32_t part_c = static_cast<uint32_t>(N * kG2KC * 2);
+      for (int64_t g = 0; g < total; ++g) {
+        const int buf = static_cast<int>(g % S);
+        const int st = static_cast<int>(g % nst);
+        const int64_t tl = g / nst;
+        const int a = static_cast<int>(tl % nacc);
+        if (st == 0 && tl >= nacc)
+          mbar_wait(&accempty[a], static_cast<uint32_t>(((tl / nacc) - 1) & 1));
+        const int cb = static_cast<int>(g % D);
+        mbar_wait(&sfull[buf], static_cast<uint32_t>((g / S) & 1));
+        mbar_wait(&cfull[cb], static_cast<uint32_t>((g / D) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        const uint32_t a0 = smem_u32(abuf + buf * kG2BufA), c0 = smem_u32(cbuf + cb * cbytes);
+        const uint32_t acc = tmem + static_cast<uint32_t>(a * set_cols);
+        constexpr int pa_of[kTcProducts] = {0, 0, 1, 0, 1, 2, 1, 2};
+        constexpr int pb_of[kTcProducts] = {0, 1, 0, 2, 1, 0, 2, 1};
+#pragma unroll
+        for (int pr = 0; pr < kTcProducts; ++pr)
+#pragma unroll
+          for (int kk = 0; kk < kG2KC / 16; ++kk) {
+            if (pr >= nprod) continue;
+            const uint64_t ad = umma_desc(a0 + pa_of[pr] * kG2PartA + kk * 256, 128, kG2Sbo);
+            const uint64_t bd = umma_desc(c0 + pb_of[pr] * part_c + kk * 256, 128, 512);
+            if (pr == 0)
+              mma_bf16(acc, ad, bd, idesc, (st | kk) != 0);
+            else
+              mma_bf16(acc + acc1_off, ad, bd, idesc, two_acc ? ((st | (pr - 1) | kk) != 0) : 1u);
+          }
+        mma_commit(&mdone[buf]);
+        mma_commit(&cdone[cb]);
+        if (st == nst - 1) mma_commit(&accfull[a]);
+      }
+    }
+  } else if (warp <= 8) {
+    // ---- split A: item (8-row group gm fastest, column kc)
+    constexpr int kAItems = kG2KC * (kTcM / 8) / kG2SplitThreads;
+    const int tid = threadIdx.x - 32;
+    for (int64_t g = 0; g < total; ++g) {
+      const int slot = static_cast<int>(g % R), buf = static_cast<int>(g % S);
+      mbar_wait(&afull[slot], static_cast<uint32_t>((g / R) & 1));
+      if (g >= S) mbar_wait(&mdone[buf], static_cast<uint32_t>(((g / S) - 1) & 1));
+      const unsigned char* rs = ring + slot * kG2StageA;
+      unsigned char* bp = abuf + buf * kG2BufA;
+#pragma unroll
+      for (int q = 0; q < kAItems; ++q) {
+        if (ablate & 2) break;  // diagnostics: no split
+        const int e = tid + kG2SplitThreads * q;
+        const int gm = e % (kTcM / 8), kc = e / (kTcM / 8);
+        const float4 v0 = *reinterpret_cast<const float4*>(rs + kc * (kTcM * 4) + gm * 32);
+        const float4 v1 = *reinterpret_cast<const float4*>(rs + kc * (kTcM * 4) + gm * 32 + 16);
+        const float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        uint32_t h[8], m[8], l[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) split3(f[t], h[t], m[t], l[t]);
+        const int off = gm * kG2Sbo + (kc >> 3) * 128 + (kc & 7) * 16;
+        *reinterpret_cast<uint4*>(bp + off) =
+            make_uint4(pack_hi(h[0], h[1]), pack_hi(h[2], h[3]), pack_hi(h[4], h[5]), pack_hi(h[6], h[7]));
+        *reinterpret_cast<uint4*>(bp + kG2PartA + off) =
+            make_uint4(pack_hi(m[0], m[1]), pack_hi(m[2], m[3]), pack_hi(m[4], m[5]), pack_hi(m[6], m[7]));
+        *reinterpret_cast<uint4*>(bp + 2 * kG2PartA + off) =
+            make_uint4(pack_hi(l[0], l[1]), pack_hi(l[2], l[3]), pack_hi(l[4], l[5]), pack_hi(l[6], l[7]));
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n");
+      mbar_arrive(&sfull[buf]);
+      mbar_arrive(&aempty[slot]);
+    }
+  } else {
+    // ---- epilogue: warp w reads TMEM lane quarter w % 4, column half
+    const int quarter = warp & 3, half = (warp - 10) >> 2;
+    const int cbeg = half * (N / 2), cend = cbeg + N / 2;
+    for (int64_t tl = 0; tl < my_tiles; ++tl) {
+      const int a = static_cast<int>(tl % nacc);
+      mbar_wait(&accfull[a], static_cast<uint32_t>((tl / nacc) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      const int64_t i = row_of(tl) * kTcM + 32 * quarter + lane;
+      const int j0 = static_cast<int>(tl % tiles_n) * N;
+      const uint32_t acc = tmem + static_cast<uint32_t>(a * set_cols) + (static_cast<uint32_t>(32 * quarter) << 16);
+      for (int cc = cbeg; cc < cend; cc += 8) {
+        uint32_t v[8], w[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                       "=r"(v[6]), "=r"(v[7])
+                     : "r"(acc + cc));
+        if (two_acc) {
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                       : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
+                         "=r"(w[6]), "=r"(w[7])
+                       : "r"(acc + N + cc));
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) w[q] = 0u;
+        }
+        float z[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int j = j0 + cc + q;
+          z[q] = (beta != 0.f && i < n && j < c) ? Z[i + static_cast<int64_t>(j) * ldz] : 0.f;
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+        if (i < n && !(ablate & 4)) {  // ablate 4 (diagnostics): no stores
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int j = j0 + cc + q;
+            if (j < c) {
+              float y = alpha * (__uint_as_float(v[q]) + __uint_as_float(w[q]));
+              if (beta != 0.f) y = fmaf(beta, z[q], y);
+              Y[i + static_cast<int64_t>(j) * ldy] = y;
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n");
+      mbar_arrive(&accempty[a]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+}
+
 }  // namespace
 
 int g_gram_tc = 1, g_gemm_tc = 1;
@@ -1127,9 +1427,77 @@ bool gemm_tc_eligible(int64_t n, int64_t k, int64_t c, int64_t lda, int64_t ldc,
          (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
 }
 
-void gemm_tc_f32(int64_t n, int64_t k, int64_t c, float alpha, const float* A, int64_t lda,
+namespace {
+// Per (device, stream) scratch for the split C images; grown outside stream
+// capture only (a captured call that needs more falls back to k_gemm_tma).
+// Old buffers are kept (never freed while a graph may reference them).
+unsigned char* tc_scratch(size_t bytes, cudaStream_t s) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> bufs;
+  int dev = 0;
+  MPB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  auto& b = bufs[{dev, s}];
+  if (b.second >= bytes) return static_cast<unsigned char*>(b.first);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  MPB_CUDA(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return nullptr;
+  const size_t want = std::max<size_t>({bytes, 2 * b.second, size_t(4) << 20});
+  void* p = nullptr;
+  if (cudaMalloc(&p, want) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  b = {p, want};
+  return static_cast<unsigned char*>(p);
+}
+}  // namespace
+
+int g_gemm_tma2 = 1, g_tc_twoacc = 1, g_tc_ablate = 0, g_g2_depth = 0;
+
+bool gemm_tc_inplace_ok(int64_t c) { return g_gemm_tma2 && c <= kG2NMax; }
+
+bool gemm_tc_f32(int64_t n, int64_t k, int64_t c, float alpha, const float* A, int64_t lda,
                  const float* C, int64_t ldc, float beta, const float* Z, int64_t ldz, float* Y,
-                 int64_t ldy, const float* A2, float* Y2, cudaStream_t s) {
+                 int64_t ldy, const float* A2, float* Y2, bool inplace, cudaStream_t s) {
+  if (g_gemm_tma2 && n < (int64_t(1) << 31) && k < (int64_t(1) << 31)) {
+    // C split once into its shared-memory stage images; A streamed by TMA
+    // c > 128: one column tile (one accumulator set) or two column tiles of
+    // <= 128 (double-buffered accumulators, A re-read from L2); in place: one
+    const int64_t tiles_n = ceil_div(c, (g_gemm_tma2 == 2 && !inplace) ? kGtN : kG2NMax);
+    const int N = static_cast<int>(round_up(ceil_div(c, tiles_n), 16));
+    const int nst = static_cast<int>(ceil_div(k, kG2KC));
+    const size_t img = static_cast<size_t>(tiles_n) * nst * g2_cimg(N);
+    unsigned char* cimg = tc_scratch(img, s);
+    if (cimg) {
+      const int64_t items = tiles_n * nst * N * (kG2KC / 8);
+      k_csplit<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(items, 256), 4 * kNumSMs)), 256, 0, s>>>(
+          static_cast<int>(k), static_cast<int>(c), N, nst, static_cast<int>(tiles_n), C, ldc, cimg);
+      MPB_LAUNCH_CHECK();
+      const int64_t rtiles = ceil_div(n, kTcM);
+      G2Depth dep = g2_depth(N);
+      if (g_g2_depth) {  // diagnostics: forced ring depths RSD (e.g. 423)
+        const G2Depth f{g_g2_depth / 100, g_g2_depth / 10 % 10, g_g2_depth % 10};
+        if (f.R >= 2 && f.R <= 4 && f.S >= 2 && f.S <= 4 && f.D >= 2 && f.D <= 4 &&
+            g2_smem(N, f) <= kG2SmemMax)
+          dep = f;
+      }
+      CUtensorMap ma[2];
+      bool ok = make_map_rows(&ma[0], A, n, k, lda, kTcM, kG2KC, false) &&
+                (!A2 || make_map_rows(&ma[1], A2, n, k, lda, kTcM, kG2KC, false));
+      for (int z = 0; ok && z < (A2 ? 2 : 1); ++z) {
+        smem_opt_in(reinterpret_cast<const void*>(k_gemm_tma2), kG2SmemMax);
+        const int64_t ctas = std::min<int64_t>(rtiles, kNumSMs);
+        k_gemm_tma2<<<static_cast<unsigned>(ctas), kG2Threads, g2_smem(N, dep), s>>>(
+            ma[z], cimg, n, static_cast<int>(k), static_cast<int>(c), N, static_cast<int>(tiles_n),
+            rtiles, dep, g_tc_twoacc, g_tc_nprod, g_tc_ablate, alpha, beta, Z, ldz, z ? Y2 : Y, ldy);
+        MPB_LAUNCH_CHECK();
+      }
+      if (ok) return true;
+    }
+  }
+  // the kernels below cover c in column tiles of <= 128: in place only up to 128
+  if (inplace && c > kGtN) return false;
   if (g_gram_tma && n < (int64_t(1) << 31) && k < (int64_t(1) << 31)) {
     // TMA-fed stages; the paired product (A2 C -> Y2) as a second launch
     const int64_t tiles_n = ceil_div(c, kGtN);
@@ -1150,8 +1518,9 @@ void gemm_tc_f32(int64_t n, int64_t k, int64_t c, float alpha, const float* A, i
           static_cast<int>(tiles_n), tiles, alpha, beta, Z, ldz, z ? Y2 : Y, ldy);
       MPB_LAUNCH_CHECK();
     }
-    if (ok) return;
+    if (ok) return true;
   }
+  if (inplace && c > kGmN) return false;
   const int64_t tiles_n = ceil_div(c, kGmN);
   const int64_t ntile = round_up(ceil_div(c, tiles_n), 16);
   const int64_t tiles = ceil_div(n, kTcM) * tiles_n;
@@ -1164,6 +1533,7 @@ void gemm_tc_f32(int64_t n, int64_t k, int64_t c, float alpha, const float* A, i
                                                    tiles, alpha, A, lda, C, ldc, beta, Z, ldz, Y, ldy,
                                                    A2, Y2);
   MPB_LAUNCH_CHECK();
+  return true;
 }
 
 }  // namespace mpb

@@ -8,6 +8,7 @@ iteration issues at m = 16 / 48 / 80 (project-out Grams [X P]^T W, CholQR
 Grams W^T W, S^T AS, the S C / AS C update, W - B G, V U^-1)."""
 import ctypes as C
 import json
+import os
 import sys
 
 import torch
@@ -16,8 +17,14 @@ sys.path.insert(0, __file__.rsplit("/scripts/", 1)[0])
 import paper_2302_12528_b200 as mp  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 2 * 1024 * 1024
+ms_list = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [16, 48, 80]
+dtypes = sys.argv[3].split(",") if len(sys.argv) > 3 else ["f64", "f32"]
 reps = 5
 ctx = mp.default_context()
+# MPEIG_OPTS="gemm_tma2=2,gram_tma=0": process options (kernel-selection experiments)
+for kv in filter(None, os.environ.get("MPEIG_OPTS", "").split(",")):
+    key, val = kv.split("=")
+    assert ctx.lib.mpeig_set_process_option(key.encode(), int(val)) == 0, kv
 out = {"n": n, "rows": []}
 
 
@@ -32,10 +39,10 @@ def prof(fn):
     return rep
 
 
-for dt in (torch.float64, torch.float32):
-    sfx = "f64" if dt == torch.float64 else "f32"
+for sfx in dtypes:
+    dt = torch.float64 if sfx == "f64" else torch.float32
     ld = n
-    for m in (16, 48, 80):
+    for m in ms_list:
         s = 3 * m
         S = torch.randn(s, ld, dtype=dt, device="cuda")  # column-major n x s (ld = n)
         G = torch.zeros(s, s, dtype=dt, device="cuda")

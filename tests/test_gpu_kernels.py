@@ -251,7 +251,8 @@ def test_gemm(gpu, n, k, c, dtype):
 
 @pytest.mark.parametrize("n,k,c", [(40000, 240, 160), (30001, 160, 80), (20000, 80, 80),
                                    (10007, 144, 96), (5000, 48, 48), (4099, 37, 13),
-                                   (1000, 16, 200)])
+                                   (1000, 16, 200), (3001, 576, 384), (2000, 100, 256),
+                                   (2500, 33, 257)])
 @pytest.mark.parametrize("beta", [0.0, 1.0])
 def test_gemm_f32_tensor_cores(gpu, n, k, c, beta):
     """The binary32 block update on tcgen05 (tc.cu, forced for every shape):
@@ -285,17 +286,61 @@ def test_gemm_f32_tensor_cores(gpu, n, k, c, beta):
 
 
 def test_gemm_inplace_wide_is_refused(gpu):
-    """Y aliasing A with more than 64 output columns would race across column
-    tiles: the library refuses instead of returning wrong columns."""
+    """Y aliasing A: allowed only where one output column tile covers all of c
+    (binary64 c <= 96; binary32 c <= 256 on the tensor-core path); wider, the
+    column tiles would race, so the library refuses instead of
+    returning wrong columns."""
     mp = gpu
     import torch
-    n, k = 10000, 80
-    W = torch.randn(k, n, dtype=torch.float64, device="cuda")
-    U = torch.eye(k, dtype=torch.float64, device="cuda")
+    n = 10000
     ctx = mp.default_context()
-    rc = ctx.lib.mpeig_gemm_f64(ctx.h, n, k, k, 1.0, C.c_void_p(W.data_ptr()), n,
-                                C.c_void_p(U.data_ptr()), k, 0.0, None, 0, C.c_void_p(W.data_ptr()), n)
-    assert rc == 1  # DimensionMismatch
+    for k in (97, 112):
+        W = torch.randn(k, n, dtype=torch.float64, device="cuda")
+        U = torch.eye(k, dtype=torch.float64, device="cuda")
+        rc = ctx.lib.mpeig_gemm_f64(ctx.h, n, k, k, 1.0, C.c_void_p(W.data_ptr()), n,
+                                    C.c_void_p(U.data_ptr()), k, 0.0, None, 0,
+                                    C.c_void_p(W.data_ptr()), n)
+        assert rc == 1  # DimensionMismatch
+    # binary32 without the tensor-core path: the SIMT kernels tile c by 64
+    W = torch.randn(80, n, dtype=torch.float32, device="cuda")
+    U = torch.eye(80, dtype=torch.float32, device="cuda")
+    assert ctx.lib.mpeig_set_process_option(b"gemm_tc", 0) == 0
+    try:
+        rc = ctx.lib.mpeig_gemm_f32(ctx.h, n, 80, 80, 1.0, C.c_void_p(W.data_ptr()), n,
+                                    C.c_void_p(U.data_ptr()), 80, 0.0, None, 0,
+                                    C.c_void_p(W.data_ptr()), n)
+    finally:
+        ctx.lib.mpeig_set_process_option(b"gemm_tc", 1)
+    assert rc == 1
+
+
+@pytest.mark.parametrize("dtype,k", [("f64", 80), ("f64", 96), ("f32", 80), ("f32", 192),
+                                     ("f32", 256)])
+def test_gemm_inplace_matches_out_of_place(gpu, dtype, k):
+    """W <- W U in place (the CholQR V U^-1 step at m = 80 .. 256) is bitwise the
+    out-of-place product: each CTA reads all k columns of its rows before its
+    single column tile is written."""
+    mp = gpu
+    import torch
+    n = 100004  # ld a multiple of 4: the aligned (in-place capable) kernels
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    g = torch.Generator(device="cuda").manual_seed(k)
+    W = torch.randn(k, n, dtype=tdt, device="cuda", generator=g)
+    U = torch.randn(k, k, dtype=tdt, device="cuda", generator=g) / k ** 0.5
+    ctx = mp.default_context()
+    fn = ctx.lib.mpeig_gemm_f64 if dtype == "f64" else ctx.lib.mpeig_gemm_f32
+    if dtype == "f32":
+        assert ctx.lib.mpeig_set_process_option(b"gemm_tc", 2) == 0
+    try:
+        Y = torch.empty_like(W)
+        ctx.check(fn(ctx.h, n, k, k, 1.0, C.c_void_p(W.data_ptr()), n, C.c_void_p(U.data_ptr()), k,
+                     0.0, None, 0, C.c_void_p(Y.data_ptr()), n))
+        ctx.check(fn(ctx.h, n, k, k, 1.0, C.c_void_p(W.data_ptr()), n, C.c_void_p(U.data_ptr()), k,
+                     0.0, None, 0, C.c_void_p(W.data_ptr()), n))
+    finally:
+        ctx.lib.mpeig_set_process_option(b"gemm_tc", 1)
+    torch.cuda.synchronize()
+    assert torch.equal(W, Y)
 
 
 def graded(n, m, kappa, seed):
@@ -385,12 +430,25 @@ def test_project_out(gpu):
     assert np.abs(B.T @ Y).max() <= 1e-13
 
 
-def test_small_eig(gpu):
+@pytest.mark.parametrize("s", [12, 48, 96])
+@pytest.mark.parametrize("spectrum", ["random", "pairs"])
+def test_small_eig(gpu, s, spectrum):
+    """small_herm_eig (small_eig.hpp:92-218) against the reference's own values AND
+    vectors (up to column sign): the Rayleigh-Ritz basis is what the block update
+    consumes.  "pairs": eigenvalues in close pairs (relative split 1e-6), the
+    near-degenerate clusters of the Laplacian's Ritz matrices."""
     mp = gpu
     import torch
-    s = 48
-    M = rand(s, s, 25)
-    M = np.asfortranarray(M + M.T)
+    if spectrum == "random":
+        M = rand(s, s, 25)
+        M = M + M.T
+    else:
+        Q, _ = np.linalg.qr(rand(s, s, 26))
+        lam = np.repeat(np.arange(1, s // 2 + 1, dtype=np.float64), 2)
+        lam[1::2] *= 1 + 1e-6
+        M = (Q * lam) @ Q.T
+        M = 0.5 * (M + M.T)
+    M = np.asfortranarray(M)
     Md = mp.to_device(M)
     vals = torch.zeros(s, dtype=torch.float64, device="cuda")
     vecs = torch.zeros((s, s), dtype=torch.float64, device="cuda")
@@ -399,9 +457,14 @@ def test_small_eig(gpu):
                                           C.c_void_p(vals.data_ptr()), C.c_void_p(vecs.data_ptr())))
     st, vr, Vr = ref_or_port().small_herm_eig(M)
     v = vals.cpu().numpy()
-    assert np.abs(v - vr).max() <= 1e-13 * np.abs(vr).max()
+    scale = np.abs(vr).max()
+    assert np.abs(v - vr).max() <= 1e-13 * scale
     V = mp.to_host(vecs)
-    assert np.linalg.norm(M @ V - V * v) <= 1e-12 * np.abs(vr).max()
+    assert np.linalg.norm(M @ V - V * v) <= 1e-12 * scale
+    gap = np.min(np.diff(vr)) / scale
+    sign = np.sign(np.sum(V * Vr, axis=0))
+    err = np.abs(V * sign - Vr).max()
+    assert err <= 1e-13 / gap, (err, gap)
 
 
 def test_hl_coeffs_match_reference(gpu):
