@@ -819,6 +819,7 @@ int mpeig_set_process_option(const char* key, int value) {
   if (k == "tc_twoacc") { g_tc_twoacc = value; return MPEIG_OK; }
   if (k == "tc_ablate") { g_tc_ablate = value; return MPEIG_OK; }
   if (k == "g2_depth") { g_g2_depth = value; return MPEIG_OK; }
+  if (k == "tc_stage") { g_tc_stage = value; return MPEIG_OK; }
   if (k == "tc_nprod") { g_tc_nprod = value; return MPEIG_OK; }
   if (k == "tc_store") { g_tc_store = value; return MPEIG_OK; }
   if (k == "gram_tc" || k == "gemm_tc" || k == "tc") {

@@ -55,7 +55,7 @@ bool gemm_tc_f32(int64_t n, int64_t k, int64_t c, float alpha, const float* A, i
 // bound (the m = 16 cfg1 shapes stay on the latency-lean SIMT kernel);
 // g_gram_tc: 1 = by size (default), 0 = never, 2 = always (tests)
 extern int g_gram_tc, g_gemm_tc;
-extern int g_gemm_tma2, g_tc_twoacc, g_tc_ablate, g_g2_depth;
+extern int g_gemm_tma2, g_tc_twoacc, g_tc_ablate, g_g2_depth, g_tc_stage;
 extern int g_tc_nprod, g_tc_store;
 extern int g_gram_tma;  // TMA-fed tensor-core Gram (1, default) or the cp.async one (0)
 // (crossovers measured at n = 2M, scripts/dense_shapes.py: the tensor-core

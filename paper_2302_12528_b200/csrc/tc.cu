@@ -95,6 +95,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity));
 }
 
+// position in a ring of n slots: slot, phase parity, and whether the slot was
+// used before (lap: wait for its release, parity phase ^ 1)
+struct RingPos {
+  int slot = 0;
+  uint32_t phase = 0;
+  bool lap = false;
+  __device__ __forceinline__ void next(int n) {
+    if (++slot == n) {
+      slot = 0;
+      phase ^= 1u;
+      lap = true;
+    }
+  }
+};
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)));
 }
@@ -394,10 +409,10 @@ k_gram_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
   if (threadIdx.x == 0) {
     for (int q = 0; q < kTmRing; ++q) {
       mbar_init(&tfull[q], 1);
-      mbar_init(&tempty[q], kTmSplitThreads);
+      mbar_init(&tempty[q], kTmSplitThreads / 32);
     }
-    mbar_init(&sfull[0], kTmSplitThreads);
-    mbar_init(&sfull[1], kTmSplitThreads);
+    mbar_init(&sfull[0], kTmSplitThreads / 32);
+    mbar_init(&sfull[1], kTmSplitThreads / 32);
     mbar_init(&sempty[0], 1);
     mbar_init(&sempty[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n");
@@ -494,8 +509,11 @@ k_gram_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         *reinterpret_cast<uint2*>(d + 2 * sprt[q]) = make_uint2(pack_hi(l0, l1), pack_hi(l2, l3));
       }
       asm volatile("fence.proxy.async.shared::cta;\n");
-      mbar_arrive(&sfull[buf]);
-      mbar_arrive(&tempty[slot]);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&sfull[buf]);
+        mbar_arrive(&tempty[slot]);
+      }
     }
     if (nst >= 1) mbar_wait(&sempty[(nst - 1) & 1], ((nst - 1) >> 1) & 1);
     if (nst >= 2) mbar_wait(&sempty[(nst - 2) & 1], ((nst - 2) >> 1) & 1);
@@ -1098,9 +1116,10 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
 }
 
 __global__ void __launch_bounds__(kG2Threads, 1)
-k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const unsigned char* __restrict__ cimg, int64_t n,
-            int k, int c, int N, int tiles_n, int64_t rtiles, G2Depth dep, int two_acc, int nprod,
-            int ablate, float alpha, float beta, const float* Z, int64_t ldz, float* Y, int64_t ldy) {
+k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmY,
+            const unsigned char* __restrict__ cimg, int64_t n, int k, int c, int N, int tiles_n,
+            int64_t rtiles, G2Depth dep, int stage_out, int two_acc, int nprod, int ablate,
+            float alpha, float beta, const float* Z, int64_t ldz, float* Y, int64_t ldy) {
   extern __shared__ unsigned char g2_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(g2_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -1109,7 +1128,11 @@ k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const unsigned char* __rest
   const int R = dep.R, S = dep.S, D = dep.D;
   unsigned char* abuf = ring + R * kG2StageA;
   unsigned char* cbuf = abuf + S * kG2BufA;
-  uint64_t* afull = reinterpret_cast<uint64_t*>(cbuf + D * cbytes);  // [4]: A stage landed
+  // stage_out: the output tile (128 x N fp32, column-major) is staged in shared
+  // memory and written by one TMA store, so the accumulators are released
+  // as soon as they are read (one accumulator set: N > 128)
+  float* stg = reinterpret_cast<float*>(cbuf + D * cbytes);
+  uint64_t* afull = reinterpret_cast<uint64_t*>(cbuf + D * cbytes + (stage_out ? kTcM * N * 4 : 0));
   uint64_t* aempty = afull + 4;       // [4]: A stage split
   uint64_t* sfull = aempty + 4;       // [4]: split buffer stored
   uint64_t* cfull = sfull + 4;        // [4]: C image landed
@@ -1119,6 +1142,7 @@ k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const unsigned char* __rest
   uint64_t* accempty = accfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto wait_ = [](uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); };
   // accumulator set = 1 or 2 TMEM accumulators of N columns (the second
   // collects the 7 smaller part products); two sets when they fit in 512
   const int set_cols = two_acc ? 2 * N : N;
@@ -1134,15 +1158,15 @@ k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const unsigned char* __rest
   if (threadIdx.x == 0) {
     for (int q = 0; q < 4; ++q) {
       mbar_init(&afull[q], 1);
-      mbar_init(&aempty[q], kG2SplitThreads);
+      mbar_init(&aempty[q], kG2SplitThreads / 32);
       mbar_init(&cfull[q], 1);
       mbar_init(&cdone[q], 1);
-      mbar_init(&sfull[q], kG2SplitThreads);
+      mbar_init(&sfull[q], kG2SplitThreads / 32);
       mbar_init(&mdone[q], 1);
     }
     for (int q = 0; q < 2; ++q) {
       mbar_init(&accfull[q], 1);
-      mbar_init(&accempty[q], kG2EpiThreads);
+      mbar_init(&accempty[q], kG2EpiThreads / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)));
@@ -1160,53 +1184,70 @@ k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const unsigned char* __rest
   const int64_t my_rows = blockIdx.x < rtiles ? (rtiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   const int64_t my_tiles = my_rows * tiles_n;
   const int64_t total = my_tiles * nst;
-  auto row_of = [&](int64_t tl) { return blockIdx.x + (tl / tiles_n) * gridDim.x; };
   const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
                          (static_cast<uint32_t>(N >> 3) << 17) |
                          (static_cast<uint32_t>(kTcM >> 4) << 24);
 
+  // loop state advanced incrementally: no 64-bit divisions on the hand-off path
+  // (a runtime int64 div / mod is a ~100-instruction call; several per stage
+  // per role cost ~1 us per stage)
   if (warp == 0) {
     if (lane == 0) {
+      RingPos rp;
+      int st = 0, ct = 0;
+      int64_t rt = blockIdx.x;
       for (int64_t g = 0; g < total; ++g) {
-        const int slot = static_cast<int>(g % R);
-        if (g >= R) mbar_wait(&aempty[slot], static_cast<uint32_t>(((g / R) - 1) & 1));
-        const int row0 = static_cast<int>(row_of(g / nst) * kTcM);
-        const int k0 = static_cast<int>(g % nst) * kG2KC;
-        mbar_expect_tx(&afull[slot], kG2StageA);
-        tma_load_2d(smem_u32(ring + slot * kG2StageA), &tmA, row0, k0, smem_u32(&afull[slot]));
+        if (rp.lap) wait_(&aempty[rp.slot], rp.phase ^ 1u);
+        if (ablate & 8) {  // diagnostics: no A loads
+          mbar_arrive(&afull[rp.slot]);
+        } else {
+          mbar_expect_tx(&afull[rp.slot], kG2StageA);
+          tma_load_2d(smem_u32(ring + rp.slot * kG2StageA), &tmA, static_cast<int>(rt * kTcM),
+                      st * kG2KC, smem_u32(&afull[rp.slot]));
+        }
+        rp.next(R);
+        if (++st == nst) {
+          st = 0;
+          if (++ct == tiles_n) {
+            ct = 0;
+            rt += gridDim.x;
+          }
+        }
       }
     }
   } else if (warp == kG2Warps - 1) {
     if (lane == 0) {
+      RingPos cp;
+      int st = 0, ct = 0;
       for (int64_t g = 0; g < total; ++g) {
-        const int cb = static_cast<int>(g % D);
-        if (g >= D) mbar_wait(&cdone[cb], static_cast<uint32_t>(((g / D) - 1) & 1));
-        const int64_t ts = ((g / nst) % tiles_n) * nst + g % nst;
+        if (cp.lap) wait_(&cdone[cp.slot], cp.phase ^ 1u);
         if ((ablate & 1) && g >= D) {  // diagnostics: no C reloads
-          mbar_arrive(&cfull[cb]);
-          continue;
+          mbar_arrive(&cfull[cp.slot]);
+        } else {
+          mbar_expect_tx(&cfull[cp.slot], static_cast<uint32_t>(cbytes));
+          bulk_load(smem_u32(cbuf + cp.slot * cbytes),
+                    cimg + static_cast<int64_t>(ct * nst + st) * cbytes, static_cast<uint32_t>(cbytes),
+                    smem_u32(&cfull[cp.slot]));
         }
-        mbar_expect_tx(&cfull[cb], static_cast<uint32_t>(cbytes));
-        bulk_load(smem_u32(cbuf + cb * cbytes), cimg + ts * cbytes, static_cast<uint32_t>(cbytes),
-                  smem_u32(&cfull[cb]));
+        cp.next(D);
+        if (++st == nst) {
+          st = 0;
+          if (++ct == tiles_n) ct = 0;
+        }
       }
     }
   } else if (warp == 9) {
     if (lane == 0) {
       const uint32_t part_c = static_cast<uint32_t>(N * kG2KC * 2);
+      RingPos sp, cp, ap;
+      int st = 0;
       for (int64_t g = 0; g < total; ++g) {
-        const int buf = static_cast<int>(g % S);
-        const int st = static_cast<int>(g % nst);
-        const int64_t tl = g / nst;
-        const int a = static_cast<int>(tl % nacc);
-        if (st == 0 && tl >= nacc)
-          mbar_wait(&accempty[a], static_cast<uint32_t>(((tl / nacc) - 1) & 1));
-        const int cb = static_cast<int>(g % D);
-        mbar_wait(&sfull[buf], static_cast<uint32_t>((g / S) & 1));
-        mbar_wait(&cfull[cb], static_cast<uint32_t>((g / D) & 1));
+        if (st == 0 && ap.lap) wait_(&accempty[ap.slot], ap.phase ^ 1u);
+        wait_(&sfull[sp.slot], sp.phase);
+        wait_(&cfull[cp.slot], cp.phase);
         asm volatile("tcgen05.fence::after_thread_sync;\n");
-        const uint32_t a0 = smem_u32(abuf + buf * kG2BufA), c0 = smem_u32(cbuf + cb * cbytes);
-        const uint32_t acc = tmem + static_cast<uint32_t>(a * set_cols);
+        const uint32_t a0 = smem_u32(abuf + sp.slot * kG2BufA), c0 = smem_u32(cbuf + cp.slot * cbytes);
+        const uint32_t acc = tmem + static_cast<uint32_t>(ap.slot * set_cols);
         constexpr int pa_of[kTcProducts] = {0, 0, 1, 0, 1, 2, 1, 2};
         constexpr int pb_of[kTcProducts] = {0, 1, 0, 2, 1, 0, 2, 1};
 #pragma unroll
@@ -1221,19 +1262,28 @@ k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const unsigned char* __rest
             else
               mma_bf16(acc + acc1_off, ad, bd, idesc, two_acc ? ((st | (pr - 1) | kk) != 0) : 1u);
           }
-        mma_commit(&mdone[buf]);
-        mma_commit(&cdone[cb]);
-        if (st == nst - 1) mma_commit(&accfull[a]);
+        mma_commit(&mdone[sp.slot]);
+        mma_commit(&cdone[cp.slot]);
+        sp.next(S);
+        cp.next(D);
+        if (++st == nst) {
+          mma_commit(&accfull[ap.slot]);
+          ap.next(nacc);
+          st = 0;
+        }
       }
     }
   } else if (warp <= 8) {
     // ---- split A: item (8-row group gm fastest, column kc)
     constexpr int kAItems = kG2KC * (kTcM / 8) / kG2SplitThreads;
     const int tid = threadIdx.x - 32;
+    RingPos rp, sp;
     for (int64_t g = 0; g < total; ++g) {
-      const int slot = static_cast<int>(g % R), buf = static_cast<int>(g % S);
-      mbar_wait(&afull[slot], static_cast<uint32_t>((g / R) & 1));
-      if (g >= S) mbar_wait(&mdone[buf], static_cast<uint32_t>(((g / S) - 1) & 1));
+      const int slot = rp.slot, buf = sp.slot;
+      wait_(&afull[slot], rp.phase);
+      if (sp.lap) wait_(&mdone[buf], sp.phase ^ 1u);
+      rp.next(R);
+      sp.next(S);
       const unsigned char* rs = ring + slot * kG2StageA;
       unsigned char* bp = abuf + buf * kG2BufA;
 #pragma unroll
@@ -1255,22 +1305,41 @@ k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const unsigned char* __rest
         *reinterpret_cast<uint4*>(bp + 2 * kG2PartA + off) =
             make_uint4(pack_hi(l[0], l[1]), pack_hi(l[2], l[3]), pack_hi(l[4], l[5]), pack_hi(l[6], l[7]));
       }
-      asm volatile("fence.proxy.async.shared::cta;\n");
-      mbar_arrive(&sfull[buf]);
-      mbar_arrive(&aempty[slot]);
+      if (!(ablate & 32)) {  // 32: no proxy fence (diagnostics); 64: one per warp
+        if (!(ablate & 64)) {
+          asm volatile("fence.proxy.async.shared::cta;\n");
+        } else {
+          __syncwarp();
+          if (lane == 0) asm volatile("fence.proxy.async.shared::cta;\n");
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&sfull[buf]);
+        mbar_arrive(&aempty[slot]);
+      }
     }
   } else {
     // ---- epilogue: warp w reads TMEM lane quarter w % 4, column half
     const int quarter = warp & 3, half = (warp - 10) >> 2;
     const int cbeg = half * (N / 2), cend = cbeg + N / 2;
+    RingPos ap;
+    int ct = 0;
+    int64_t rt = blockIdx.x;
     for (int64_t tl = 0; tl < my_tiles; ++tl) {
-      const int a = static_cast<int>(tl % nacc);
-      mbar_wait(&accfull[a], static_cast<uint32_t>((tl / nacc) & 1));
+      const int a = ap.slot;
+      wait_(&accfull[a], ap.phase);
+      ap.next(nacc);
       asm volatile("tcgen05.fence::after_thread_sync;\n");
-      const int64_t i = row_of(tl) * kTcM + 32 * quarter + lane;
-      const int j0 = static_cast<int>(tl % tiles_n) * N;
+      const int64_t row0 = rt * kTcM, i = row0 + 32 * quarter + lane;
+      const int j0 = ct * N;
+      if (++ct == tiles_n) {
+        ct = 0;
+        rt += gridDim.x;
+      }
       const uint32_t acc = tmem + static_cast<uint32_t>(a * set_cols) + (static_cast<uint32_t>(32 * quarter) << 16);
       for (int cc = cbeg; cc < cend; cc += 8) {
+        if (ablate & 16) break;  // diagnostics: no TMEM drain
         uint32_t v[8], w[8];
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
                      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
@@ -1292,7 +1361,15 @@ k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const unsigned char* __rest
           z[q] = (beta != 0.f && i < n && j < c) ? Z[i + static_cast<int64_t>(j) * ldz] : 0.f;
         }
         asm volatile("tcgen05.wait::ld.sync.aligned;\n");
-        if (i < n && !(ablate & 4)) {  // ablate 4 (diagnostics): no stores
+        if (stage_out) {
+          float* col = stg + static_cast<int64_t>(cc) * kTcM + 32 * quarter + lane;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float y = alpha * (__uint_as_float(v[q]) + __uint_as_float(w[q]));
+            if (beta != 0.f) y = fmaf(beta, z[q], y);
+            col[q * kTcM] = y;
+          }
+        } else if (i < n && !(ablate & 4)) {  // ablate 4 (diagnostics): no stores
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const int j = j0 + cc + q;
@@ -1305,8 +1382,32 @@ k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const unsigned char* __rest
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n");
-      mbar_arrive(&accempty[a]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&accempty[a]);
+      if (stage_out) {
+        // all epilogue threads' staging stores -> the async proxy; one TMA
+        // store of the tile (rows >= n and columns >= c are clipped by the
+        // map); the staging buffer is reused once the store has read it
+        asm volatile("fence.proxy.async.shared::cta;\n");
+        __syncwarp();
+        asm volatile("bar.sync 1, %0;\n" ::"r"(kG2EpiThreads));
+        if (ablate & 128) {  // diagnostics: staged tile written by the epilogue threads
+          for (int cc = cbeg; cc < cend; ++cc)
+            if (i < n && j0 + cc < c) Y[i + static_cast<int64_t>(j0 + cc) * ldy] = stg[cc * kTcM + 32 * quarter + lane];
+        } else if (warp == 10 && lane == 0) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                  reinterpret_cast<uint64_t>(&tmY)),
+              "r"(static_cast<int>(row0)), "r"(j0), "r"(smem_u32(stg))
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;\n");
+          asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        }
+        __syncwarp();  // bar.sync counts whole warps: reconverge lane 0 first
+        asm volatile("bar.sync 1, %0;\n" ::"r"(kG2EpiThreads));
+      }
     }
+    if (stage_out && warp == 10 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
@@ -1453,7 +1554,7 @@ unsigned char* tc_scratch(size_t bytes, cudaStream_t s) {
 }
 }  // namespace
 
-int g_gemm_tma2 = 1, g_tc_twoacc = 1, g_tc_ablate = 0, g_g2_depth = 0;
+int g_gemm_tma2 = 1, g_tc_twoacc = 1, g_tc_ablate = 0, g_g2_depth = 0, g_tc_stage = 1;
 
 bool gemm_tc_inplace_ok(int64_t c) { return g_gemm_tma2 && c <= kG2NMax; }
 
@@ -1476,21 +1577,37 @@ bool gemm_tc_f32(int64_t n, int64_t k, int64_t c, float alpha, const float* A, i
       MPB_LAUNCH_CHECK();
       const int64_t rtiles = ceil_div(n, kTcM);
       G2Depth dep = g2_depth(N);
+      // one accumulator set (two accumulators of N > 128 columns): stage the
+      // output for a TMA store when the smem allows (ring depths 2)
+      const bool one_set = 2 * (g_tc_twoacc ? 2 * N : N) > 512;
+      const auto aligned16 = [](const float* p, int64_t ld) {
+        return p && reinterpret_cast<uintptr_t>(p) % 16 == 0 && ld % 4 == 0;
+      };
+      int stage_out = one_set && g_tc_stage && aligned16(Y, ldy) && (!A2 || aligned16(Y2, ldy)) &&
+                      g2_smem(N, G2Depth{2, 2, 2}) + kTcM * N * 4 <= kG2SmemMax;
+      if (stage_out) dep = G2Depth{2, 2, 2};
       if (g_g2_depth) {  // diagnostics: forced ring depths RSD (e.g. 423)
         const G2Depth f{g_g2_depth / 100, g_g2_depth / 10 % 10, g_g2_depth % 10};
         if (f.R >= 2 && f.R <= 4 && f.S >= 2 && f.S <= 4 && f.D >= 2 && f.D <= 4 &&
-            g2_smem(N, f) <= kG2SmemMax)
+            g2_smem(N, f) + (stage_out ? kTcM * N * 4 : 0) <= kG2SmemMax)
           dep = f;
       }
-      CUtensorMap ma[2];
+      CUtensorMap ma[2], my[2];
       bool ok = make_map_rows(&ma[0], A, n, k, lda, kTcM, kG2KC, false) &&
                 (!A2 || make_map_rows(&ma[1], A2, n, k, lda, kTcM, kG2KC, false));
+      if (ok && stage_out)
+        stage_out = make_map_rows(&my[0], Y, n, c, ldy, kTcM, N, false) &&
+                    (!A2 || make_map_rows(&my[1], Y2, n, c, ldy, kTcM, N, false));
+      if (!stage_out) my[0] = my[1] = ma[0];  // unused
+      const int smem = g2_smem(N, dep) + (stage_out ? kTcM * N * 4 : 0);
       for (int z = 0; ok && z < (A2 ? 2 : 1); ++z) {
         smem_opt_in(reinterpret_cast<const void*>(k_gemm_tma2), kG2SmemMax);
-        const int64_t ctas = std::min<int64_t>(rtiles, kNumSMs);
-        k_gemm_tma2<<<static_cast<unsigned>(ctas), kG2Threads, g2_smem(N, dep), s>>>(
-            ma[z], cimg, n, static_cast<int>(k), static_cast<int>(c), N, static_cast<int>(tiles_n),
-            rtiles, dep, g_tc_twoacc, g_tc_nprod, g_tc_ablate, alpha, beta, Z, ldz, z ? Y2 : Y, ldy);
+        int64_t ctas = std::min<int64_t>(rtiles, kNumSMs);
+        if (g_tc_ablate >> 16) ctas = std::min<int64_t>(ctas, g_tc_ablate >> 16);  // diagnostics
+        k_gemm_tma2<<<static_cast<unsigned>(ctas), kG2Threads, smem, s>>>(
+            ma[z], my[z], cimg, n, static_cast<int>(k), static_cast<int>(c), N,
+            static_cast<int>(tiles_n), rtiles, dep, stage_out, g_tc_twoacc, g_tc_nprod, g_tc_ablate,
+            alpha, beta, Z, ldz, z ? Y2 : Y, ldy);
         MPB_LAUNCH_CHECK();
       }
       if (ok) return true;
