@@ -377,7 +377,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 
 __global__ void __launch_bounds__(kTmSplitThreads + 64, 1)
 k_gram_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           int64_t n, int ka, int kb, int tiles_n, int ntile, float* __restrict__ part) {
+           int64_t n, int ka, int kb, int tiles_n, int ntile, float* __restrict__ part, int ablate) {
   extern __shared__ unsigned char tsm_raw[];
   // 1024-B alignment for the 128-B swizzled TMA boxes
   unsigned char* tsm = reinterpret_cast<unsigned char*>(
@@ -434,6 +434,10 @@ k_gram_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       for (int st = 0; st < nst; ++st) {
         const int slot = st % kTmRing;
         if (st >= kTmRing) mbar_wait(&tempty[slot], ((st / kTmRing) - 1) & 1);
+        if (ablate & 1) {  // diagnostics: no loads
+          mbar_arrive(&tfull[slot]);
+          continue;
+        }
         mbar_expect_tx(&tfull[slot], bytes);
         const uint32_t dst = smem_u32(ring + slot * kTmStage);
         const uint32_t bar = smem_u32(&tfull[slot]);
@@ -456,6 +460,7 @@ k_gram_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         for (int pr = 0; pr < kTcProducts; ++pr)
 #pragma unroll
           for (int kk = 0; kk < kTmKC / 16; ++kk) {
+            if ((ablate & 4) && pr > 0) continue;  // diagnostics: one product
             const uint64_t ad = umma_desc(a0 + pa_of[pr] * kTmPartA + kk * 256, 128, 512);
             const uint64_t bd = umma_desc(b0 + pb_of[pr] * part_b + kk * 256, 128, 512);
             if (pr == 0)
@@ -496,6 +501,7 @@ k_gram_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       unsigned char* bp = split + buf * kTmBuf;
 #pragma unroll
       for (int q = 0; q < kSlots; ++q) {
+        if (ablate & 2) break;  // diagnostics: no split
         if (!live[q]) continue;
         const float4 v = *reinterpret_cast<const float4*>(rs + roff[q]);
         uint32_t h0, m0, l0, h1, m1, l1, h2, m2, l2, h3, m3, l3;
@@ -1513,7 +1519,7 @@ int64_t gram_tc_f32(int64_t n, int64_t ka, const float* A, int64_t lda, int64_t 
       const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(nchunk));
       k_gram_tma<<<grid, kTmSplitThreads + 64, kTmSmem, s>>>(ma, mb, n, static_cast<int>(ka),
                                                            static_cast<int>(kb), static_cast<int>(tiles_n),
-                                                           static_cast<int>(ntile), part);
+                                                           static_cast<int>(ntile), part, g_tc_ablate);
       MPB_LAUNCH_CHECK();
       return nchunk;
     }
