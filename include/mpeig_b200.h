@@ -224,6 +224,19 @@ int mpeig_op_lap2d(mpeig_ctx* ctx, int64_t nx, int64_t ny, mpeig_op** out);
  * columns, host arrays (copied to the device) */
 int mpeig_op_csr(mpeig_ctx* ctx, int64_t n, const int64_t* row_ptr_host,
                  const int64_t* col_idx_host, const double* vals_host, mpeig_op** out);
+/* this rank's row block [row0, row0 + n_local) of an n_global x n_global CSR
+ * matrix (row-sharded): row_ptr over the local rows, GLOBAL
+ * column indices, sorted per row.  Rank r must hold the r-th contiguous
+ * block (collective over the context's communicator: the ranks agree on the
+ * partition and on the ghost-row lists, the other ranks' rows this block's
+ * entries touch).  Each apply packs the rows the peers need, exchanges them
+ * (NCCL send / recv, or host-staged) on a side stream while the rows without
+ * ghost entries are computed, then the boundary rows: every row's sum keeps
+ * the global column order, bitwise the unsharded apply.  A sharded solve
+ * needs every block at least as tall as the search basis is wide (3m). */
+int mpeig_op_csr_rows(mpeig_ctx* ctx, int64_t n_global, int64_t row0, int64_t n_local,
+                      const int64_t* row_ptr_host, const int64_t* col_idx_host,
+                      const double* vals_host, mpeig_op** out);
 /* dense symmetric n x n, herm_product (dense_kernels.hpp:66-72); host array */
 int mpeig_op_dense(mpeig_ctx* ctx, int64_t n, const double* A_host, int64_t lda,
                    mpeig_op** out);

@@ -11,7 +11,7 @@ from .api import (  # noqa: F401
     slab_partition,
     EigResult, IterationRecord, MpeigError, NoConvergence, NotPositiveDefinite, Operator,
     OverflowError_, RankCollapse, RankDeficient, SingularTriangular, SolverConfig,
-    StageOptions, StageOutcome, StageTimings, build_precision_for, converged_count, csr_matrix,
+    StageOptions, StageOutcome, StageTimings, build_precision_for, converged_count, csr_matrix, csr_rows,
     default_context, dense_cholesky, dense_matrix, rcm_ordering, solve_csr, sparse_cholesky,
     ks_hamiltonian, ks_hamiltonian_slab, read_matrix_market, ParseError, NotSymmetricHeader, NotSquare, gaussian_matrix, host_operator, jacobi, laplace2d, laplace3d,
     lobpcg_stage, mixed_lobpcg, pinvit, profile, run_variant, solve, solve_prepared,

@@ -67,7 +67,7 @@ HOST_APPLY = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, 
 # exported symbols declared by include/mpeig_b200.h (checked by tests)
 SYMBOLS = [
     "mpeig_ctx_create", "mpeig_ctx_destroy", "mpeig_last_error", "mpeig_launch_count",
-    "mpeig_ctx_stream", "mpeig_ctx_set_option", "mpeig_spec_rollbacks", "mpeig_op_lap3d", "mpeig_op_lap3d_diag", "mpeig_op_lap3d_slab_diag", "mpeig_op_lap2d", "mpeig_op_csr", "mpeig_op_dense",
+    "mpeig_ctx_stream", "mpeig_ctx_set_option", "mpeig_spec_rollbacks", "mpeig_op_lap3d", "mpeig_op_lap3d_diag", "mpeig_op_lap3d_slab_diag", "mpeig_op_lap2d", "mpeig_op_csr", "mpeig_op_csr_rows", "mpeig_op_dense",
     "mpeig_op_device_callback", "mpeig_op_host_callback", "mpeig_precond_jacobi", "mpeig_precond_dense_chol", "mpeig_precond_shift",
     "mpeig_precond_sparse_chol", "mpeig_precond_factor_nnz", "mpeig_rcm_ordering",
     "mpeig_op_destroy", "mpeig_op_n", "mpeig_op_apply", "mpeig_spectral_norm_estimate",
@@ -110,6 +110,7 @@ def load() -> C.CDLL:
         "mpeig_op_lap3d": (C.c_int, [vp, i64, i64, i64, pvp]),
         "mpeig_op_lap2d": (C.c_int, [vp, i64, i64, pvp]),
         "mpeig_op_csr": (C.c_int, [vp, i64, vp, vp, vp, pvp]),
+        "mpeig_op_csr_rows": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, pvp]),
         "mpeig_op_dense": (C.c_int, [vp, i64, vp, i64, pvp]),
         "mpeig_op_device_callback": (C.c_int, [vp, i64, DEV_APPLY, DEV_APPLY, vp, pvp]),
         "mpeig_op_host_callback": (C.c_int, [vp, i64, HOST_APPLY, HOST_APPLY, vp, pvp]),

@@ -413,6 +413,20 @@ def csr_matrix(row_ptr, col_idx, vals, ctx: Context = None) -> Operator:
     return Operator(ctx, h, n, "csr")
 
 
+def csr_rows(n_global: int, row0: int, row_ptr, col_idx, vals, ctx: Context = None) -> Operator:
+    """This rank's row block [row0, row0 + n_local) of a row-sharded CSR matrix
+    (global column indices; collective over the context's communicator --
+    ghost rows exchanged per apply)."""
+    ctx = ctx or default_context()
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col_idx, np.int64)
+    v = np.ascontiguousarray(vals, np.float64)
+    n = len(rp) - 1
+    h = _mk(ctx, ctx.lib.mpeig_op_csr_rows, n_global, row0, n, rp.ctypes.data, ci.ctypes.data,
+            v.ctypes.data)
+    return Operator(ctx, h, n, "csr_rows")
+
+
 def dense_matrix(A, ctx: Context = None) -> Operator:
     """Dense symmetric operator (herm_product, dense_kernels.hpp:66-72)."""
     ctx = ctx or default_context()

@@ -6,6 +6,7 @@
 #include <cublas_v2.h>
 #include <cusolverDn.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -352,6 +353,145 @@ int mpeig_op_csr(mpeig_ctx* ctx, int64_t n, const int64_t* row_ptr_host,
   });
 }
 
+namespace {
+// small host vectors through the communicator's device-side collectives
+std::vector<int64_t> allgather_host(Comm* c, const std::vector<int64_t>& mine, cudaStream_t s) {
+  const size_t cnt = mine.size();
+  DevBuf<int64_t> d(cnt, s), all(cnt * c->nranks, s);
+  MPB_CUDA(cudaMemcpyAsync(d.p, mine.data(), sizeof(int64_t) * cnt, cudaMemcpyHostToDevice, s));
+  c->allgather(d.p, all.p, static_cast<int64_t>(sizeof(int64_t) * cnt), s);
+  std::vector<int64_t> out(cnt * c->nranks);
+  MPB_CUDA(cudaMemcpyAsync(out.data(), all.p, sizeof(int64_t) * out.size(), cudaMemcpyDeviceToHost, s));
+  MPB_CUDA(cudaStreamSynchronize(s));
+  return out;
+}
+}  // namespace
+
+int mpeig_op_csr_rows(mpeig_ctx* ctx, int64_t n_global, int64_t row0, int64_t n_local,
+                      const int64_t* row_ptr_host, const int64_t* col_idx_host,
+                      const double* vals_host, mpeig_op** out) {
+  return guard(ctx, [&] {
+    set_device(ctx);
+    Comm* c = dist(ctx);
+    const int nr = c ? c->nranks : 1, me = c ? c->rank : 0;
+    if (n_local < 1 || row0 < 0 || row0 + n_local > n_global)
+      throw Error(MPEIG_E_DIMENSION, "csr_rows: bad row range");
+    if (!c && (row0 != 0 || n_local != n_global))
+      throw Error(MPEIG_E_CONFIG, "csr_rows: a partial row block needs a communicator");
+    const int64_t nnz = row_ptr_host[n_local];
+    for (int64_t i = 0; i < n_local; ++i) {
+      if (row_ptr_host[i + 1] < row_ptr_host[i]) throw Error(MPEIG_E_DIMENSION, "csr: row_ptr not monotone");
+      for (int64_t q = row_ptr_host[i]; q < row_ptr_host[i + 1]; ++q) {
+        if (col_idx_host[q] < 0 || col_idx_host[q] >= n_global)
+          throw Error(MPEIG_E_DIMENSION, "from_triplets: index out of range");
+        if (q > row_ptr_host[i] && col_idx_host[q] <= col_idx_host[q - 1])
+          throw Error(MPEIG_E_DIMENSION, "csr: columns must be sorted and unique per row");
+      }
+    }
+    if (n_global >= INT32_MAX || nnz >= INT32_MAX)
+      throw Error(MPEIG_E_CONFIG, "csr: n and nnz must stay below 2^31 (int32 device indices)");
+    cudaStream_t s = ctx->stream;
+    // the rank partition: contiguous row blocks in rank order covering n_global
+    std::vector<int64_t> start(static_cast<size_t>(nr) + 1, 0);
+    if (c) {
+      const std::vector<int64_t> rr = allgather_host(c, {row0, n_local}, s);
+      for (int q = 0; q < nr; ++q) {
+        if (rr[2 * q] != start[q])
+          throw Error(MPEIG_E_CONFIG, "csr_rows: rank row blocks must be contiguous in rank order");
+        start[q + 1] = rr[2 * q] + rr[2 * q + 1];
+      }
+    } else {
+      start[1] = n_global;
+    }
+    if (start[nr] != n_global) throw Error(MPEIG_E_CONFIG, "csr_rows: row blocks do not cover n_global");
+    // ghost columns (sorted, hence grouped by owner) and local column indices
+    std::vector<int64_t> ghosts;
+    for (int64_t q = 0; q < nnz; ++q) {
+      const int64_t g = col_idx_host[q];
+      if (g < row0 || g >= row0 + n_local) ghosts.push_back(g);
+    }
+    std::sort(ghosts.begin(), ghosts.end());
+    ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+    const int64_t ng = static_cast<int64_t>(ghosts.size());
+    std::vector<int> ci32(static_cast<size_t>(nnz)), rp32(row_ptr_host, row_ptr_host + n_local + 1);
+    std::vector<int> inner, bnd;
+    for (int64_t i = 0; i < n_local; ++i) {
+      bool has_ghost = false;
+      for (int64_t q = row_ptr_host[i]; q < row_ptr_host[i + 1]; ++q) {
+        const int64_t g = col_idx_host[q];
+        if (g >= row0 && g < row0 + n_local) {
+          ci32[q] = static_cast<int>(g - row0);
+        } else {
+          ci32[q] = static_cast<int>(n_local + (std::lower_bound(ghosts.begin(), ghosts.end(), g) -
+                                                ghosts.begin()));
+          has_ghost = true;
+        }
+      }
+      (has_ghost ? bnd : inner).push_back(static_cast<int>(i));
+    }
+    mpeig_op* op = new_op(ctx, kOpCsr, n_local);
+    op->n_global = n_global;
+    op->row0 = row0;
+    op->nnz = nnz;
+    op->n_ghost = ng;
+    // per peer: the rows this rank receives (its ghosts owned by q) ...
+    op->gx_recv_rows.assign(nr, 0);
+    op->gx_recv_off.assign(nr, 0);
+    for (int64_t g : ghosts) {
+      const int q = static_cast<int>(std::upper_bound(start.begin(), start.end(), g) - start.begin()) - 1;
+      ++op->gx_recv_rows[q];
+    }
+    for (int q = 1; q < nr; ++q) op->gx_recv_off[q] = op->gx_recv_off[q - 1] + op->gx_recv_rows[q - 1];
+    // ... and the rows it sends: the count matrix, then the index lists
+    op->gx_send_rows.assign(nr, 0);
+    op->gx_send_off.assign(nr, 0);
+    std::vector<int64_t> send_idx;
+    if (c) {
+      const std::vector<int64_t> cm = allgather_host(c, op->gx_recv_rows, s);  // cm[r * nr + q]
+      for (int q = 0; q < nr; ++q) op->gx_send_rows[q] = cm[static_cast<size_t>(q) * nr + me];
+      for (int q = 1; q < nr; ++q) op->gx_send_off[q] = op->gx_send_off[q - 1] + op->gx_send_rows[q - 1];
+      op->n_send = op->gx_send_off[nr - 1] + op->gx_send_rows[nr - 1];
+      // rank r asks owner q for its ghost list's q-part (global row indices)
+      std::vector<int64_t> sb(nr), so(nr), rb(nr), ro(nr);
+      for (int q = 0; q < nr; ++q) {
+        sb[q] = 8 * op->gx_recv_rows[q];
+        so[q] = 8 * op->gx_recv_off[q];
+        rb[q] = 8 * op->gx_send_rows[q];
+        ro[q] = 8 * op->gx_send_off[q];
+      }
+      DevBuf<int64_t> dreq(static_cast<size_t>(std::max<int64_t>(ng, 1)), s);
+      DevBuf<int64_t> dgot(static_cast<size_t>(std::max<int64_t>(op->n_send, 1)), s);
+      if (ng) MPB_CUDA(cudaMemcpyAsync(dreq.p, ghosts.data(), 8 * ng, cudaMemcpyHostToDevice, s));
+      c->alltoallv(dreq.p, sb.data(), so.data(), dgot.p, rb.data(), ro.data(), s);
+      send_idx.resize(static_cast<size_t>(op->n_send));
+      if (op->n_send)
+        MPB_CUDA(cudaMemcpyAsync(send_idx.data(), dgot.p, 8 * op->n_send, cudaMemcpyDeviceToHost, s));
+      MPB_CUDA(cudaStreamSynchronize(s));
+      for (int64_t& g : send_idx) {
+        if (g < row0 || g >= row0 + n_local) throw Error(MPEIG_E_COMM, "csr_rows: ghost request for a foreign row");
+        g -= row0;
+      }
+    }
+    std::vector<int> send32(send_idx.begin(), send_idx.end());
+    op->rp = upload(row_ptr_host, static_cast<size_t>(n_local + 1), s);
+    op->ci = upload(col_idx_host, static_cast<size_t>(nnz), s);  // global (Jacobi's diagonal)
+    op->rp32 = upload(rp32.data(), rp32.size(), s);
+    op->ci32 = upload(ci32.data(), ci32.size(), s);
+    op->gx_send_idx = upload(send32.data(), send32.size(), s);
+    op->rows_inner = upload(inner.data(), inner.size(), s);
+    op->rows_bnd = upload(bnd.data(), bnd.size(), s);
+    op->n_inner = static_cast<int64_t>(inner.size());
+    op->n_bnd = static_cast<int64_t>(bnd.size());
+    op->vals = upload(vals_host, static_cast<size_t>(nnz), s);
+    std::vector<float> vl;
+    op->lower_overflow = !narrow(vals_host, static_cast<size_t>(nnz), vl);
+    op->vals_l = upload(vl.data(), vl.size(), s);
+    MPB_CUDA(cudaStreamSynchronize(s));  // host staging vectors go out of scope
+    op->slab = c != nullptr;
+    *out = op;
+  });
+}
+
 int mpeig_op_dense(mpeig_ctx* ctx, int64_t n, const double* A_host, int64_t lda, mpeig_op** out) {
   return guard(ctx, [&] {
     set_device(ctx);
@@ -417,10 +557,10 @@ int mpeig_precond_jacobi(mpeig_ctx* ctx, const mpeig_op* A, int32_t precision, m
         MPB_CUDA(cudaMemcpyAsync(ci.data(), A->ci, sizeof(int64_t) * rp[n], cudaMemcpyDeviceToHost, s));
         MPB_CUDA(cudaMemcpyAsync(v.data(), A->vals, sizeof(double) * rp[n], cudaMemcpyDeviceToHost, s));
         MPB_CUDA(cudaStreamSynchronize(s));
-        for (int64_t i = 0; i < n; ++i) {
+        for (int64_t i = 0; i < n; ++i) {  // (global column indices: row0 + i on a shard)
           d[i] = 0.0;
           for (int64_t q = rp[i]; q < rp[i + 1]; ++q)
-            if (ci[q] == i) d[i] = v[q];
+            if (ci[q] == A->row0 + i) d[i] = v[q];
         }
         break;
       }
@@ -530,6 +670,9 @@ void mpeig_op_destroy(mpeig_op* op) {
   cudaFree(op->sp_Usp);
   cudaFree(op->sp_Lv);
   cudaFree(op->sp_Uv);
+  cudaFree(op->gx_send_idx);
+  cudaFree(op->rows_inner);
+  cudaFree(op->rows_bnd);
   if (op->halo) cudaFree(op->halo);
   if (op->halo_stream) cudaStreamDestroy(op->halo_stream);
   if (op->ev_packed) cudaEventDestroy(op->ev_packed);

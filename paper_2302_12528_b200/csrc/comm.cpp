@@ -89,6 +89,36 @@ void HostComm::exchange(const void* send_lo, const void* send_hi, void* recv_lo,
   MPB_CUDA(cudaStreamSynchronize(s));
 }
 
+void HostComm::alltoallv(const void* send, const int64_t* send_bytes, const int64_t* send_off,
+                         void* recv, const int64_t* recv_bytes, const int64_t* recv_off,
+                         cudaStream_t s) {
+  // slots[r]: rank r's whole send buffer; slots2[r]: its (offset, bytes) table
+  int64_t extent = 0;
+  for (int q = 0; q < nranks; ++q)
+    if (send_bytes[q] > 0) extent = std::max(extent, send_off[q] + send_bytes[q]);
+  auto& mine = group->slots[rank];
+  auto& table = group->slots2[rank];
+  mine.resize(static_cast<size_t>(extent));
+  table.resize(sizeof(int64_t) * 2 * nranks);
+  int64_t* t = reinterpret_cast<int64_t*>(table.data());
+  for (int q = 0; q < nranks; ++q) {
+    t[q] = send_off[q];
+    t[nranks + q] = send_bytes[q];
+  }
+  if (extent > 0) MPB_CUDA(cudaMemcpyAsync(mine.data(), send, extent, cudaMemcpyDeviceToHost, s));
+  MPB_CUDA(cudaStreamSynchronize(s));
+  group->barrier();
+  for (int q = 0; q < nranks; ++q) {
+    if (recv_bytes[q] <= 0) continue;
+    const int64_t* tq = reinterpret_cast<const int64_t*>(group->slots2[q].data());
+    if (tq[nranks + rank] != recv_bytes[q]) throw Error(MPEIG_E_COMM, "alltoallv: size mismatch");
+    MPB_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + recv_off[q], group->slots[q].data() + tq[rank],
+                             recv_bytes[q], cudaMemcpyHostToDevice, s));
+  }
+  MPB_CUDA(cudaStreamSynchronize(s));
+  group->barrier();  // all reads done before any slot is reused
+}
+
 // ------------------------------------------------------------------ NCCL
 namespace {
 
@@ -171,6 +201,22 @@ struct NcclComm final : Comm {
     if (rank + 1 < nranks) {
       nccl_check(api().send(send_hi, b, ncclUint8, rank + 1, comm, s), "ncclSend");
       nccl_check(api().recv(recv_hi, b, ncclUint8, rank + 1, comm, s), "ncclRecv");
+    }
+    nccl_check(api().group_end(), "ncclGroupEnd");
+  }
+  void alltoallv(const void* send, const int64_t* send_bytes, const int64_t* send_off, void* recv,
+                 const int64_t* recv_bytes, const int64_t* recv_off, cudaStream_t s) override {
+    nccl_check(api().group_start(), "ncclGroupStart");
+    for (int q = 0; q < nranks; ++q) {
+      if (q == rank) continue;
+      if (send_bytes[q] > 0)
+        nccl_check(api().send(static_cast<const char*>(send) + send_off[q],
+                              static_cast<size_t>(send_bytes[q]), ncclUint8, q, comm, s),
+                   "ncclSend");
+      if (recv_bytes[q] > 0)
+        nccl_check(api().recv(static_cast<char*>(recv) + recv_off[q], static_cast<size_t>(recv_bytes[q]),
+                              ncclUint8, q, comm, s),
+                   "ncclRecv");
     }
     nccl_check(api().group_end(), "ncclGroupEnd");
   }

@@ -36,6 +36,12 @@ struct Comm {
   // to rank+1 (its recv_lo); a missing neighbour sends / receives nothing
   virtual void exchange(const void* send_lo, const void* send_hi, void* recv_lo, void* recv_hi,
                         int64_t bytes, cudaStream_t s) = 0;
+  // point-to-point to any peers (the CSR ghost rows): send_bytes[q] bytes at
+  // send + send_off[q] go to rank q, which receives them at recv + recv_off[me];
+  // sizes agreed beforehand (recv_bytes[q] == rank q's send_bytes[me])
+  virtual void alltoallv(const void* send, const int64_t* send_bytes, const int64_t* send_off,
+                         void* recv, const int64_t* recv_bytes, const int64_t* recv_off,
+                         cudaStream_t s) = 0;
 };
 
 // ---- ranks as threads of one process ------------------------------------
@@ -62,6 +68,8 @@ struct HostComm final : Comm {
   void allgather(const void* send, void* recv, int64_t bytes, cudaStream_t s) override;
   void exchange(const void* send_lo, const void* send_hi, void* recv_lo, void* recv_hi,
                 int64_t bytes, cudaStream_t s) override;
+  void alltoallv(const void* send, const int64_t* send_bytes, const int64_t* send_off, void* recv,
+                 const int64_t* recv_bytes, const int64_t* recv_off, cudaStream_t s) override;
 
  private:
   template <typename T, typename Op>

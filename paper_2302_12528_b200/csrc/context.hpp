@@ -63,6 +63,15 @@ struct mpeig_op {
   int64_t nnz = 0;
   double* vals = nullptr;
   float* vals_l = nullptr;
+  // row-sharded CSR (mpeig_op_csr_rows): local column indices, owned rows
+  // first then the ghost rows (other ranks' rows this rank's entries touch),
+  // grouped by owner; per peer the rows sent / received (host, in rows)
+  int64_t n_ghost = 0, n_send = 0;
+  std::vector<int64_t> gx_send_rows, gx_send_off, gx_recv_rows, gx_recv_off;
+  int* gx_send_idx = nullptr;  // local rows packed for the peers, peer order
+  int* rows_inner = nullptr;   // rows without ghost entries (computed during the exchange)
+  int* rows_bnd = nullptr;     // rows with ghost entries (after it)
+  int64_t n_inner = 0, n_bnd = 0;
   // dense (device)
   double* A = nullptr;
   float* Al = nullptr;

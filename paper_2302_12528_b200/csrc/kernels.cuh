@@ -154,6 +154,14 @@ void stencil5(int64_t nx, int64_t ny, int64_t c, const T* X, int64_t ldx, T* Y, 
 template <typename T>
 void csr_spmm(int64_t n, const int* row_ptr, const int* col_idx, const T* vals, int64_t nnz,
               int64_t c, const T* X, int64_t ldx, T* Y, int64_t ldy, cudaStream_t s);
+// the row-sharded CSR apply: rows of a list, ghost columns (>= nown) from G
+template <typename T>
+void csr_spmm_rows(int64_t nrows, const int* rows, const int* row_ptr, const int* col_idx,
+                   const T* vals, int64_t c, const T* X, int64_t ldx, int64_t nown, const T* G,
+                   int64_t ldg, T* Y, int64_t ldy, cudaStream_t s);
+template <typename T>
+void gather_rows(int64_t nrows, const int* idx, int64_t c, const T* X, int64_t ldx, T* Y, int64_t ldy,
+                 cudaStream_t s);
 
 // ---------------------------------------------------------- small dense
 // Small (<= ~600) matrices, single-CTA kernels working in global memory.

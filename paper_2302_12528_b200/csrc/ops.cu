@@ -7,6 +7,8 @@
 // identical to the reference operator, so A.X never contributes to
 // trajectory drift.  Coefficients are exactly representable in fp32 as well
 // (to_lower of -1, 4, 6), so the lower-precision apply follows the same code.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "rn.cuh"
@@ -304,7 +306,90 @@ k_csr_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci, const 
     if (u < nc) Y[i + (c0 + u) * ldy] = acc[u];
 }
 
+// Row-sharded CSR: the rows of a list (rows == nullptr: 0 .. n-1), columns
+// >= nown read from the ghost block G (ld ldg) -- the entries keep their
+// global ascending order, so every row's sum is bitwise the global apply's.
+template <typename T, int CB, bool kGhost>
+__global__ void __launch_bounds__(256)
+k_csr_spmm_rows(int nrows, const int* __restrict__ rows, const int* __restrict__ rp,
+                const int* __restrict__ ci, const T* __restrict__ v, int c, const T* __restrict__ X,
+                int64_t ldx, int nown, const T* __restrict__ G, int64_t ldg, T* __restrict__ Y,
+                int64_t ldy) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nrows) return;
+  const int i = rows ? __ldg(rows + t) : t;
+  const int c0 = blockIdx.y * CB;
+  const int nc = min(CB, c - c0);
+  const T* x = X + c0 * ldx;
+  const T* g = kGhost ? G + c0 * ldg : nullptr;
+  T acc[CB];
+#pragma unroll
+  for (int u = 0; u < CB; ++u) acc[u] = T(0);
+  const int e = __ldg(rp + i + 1);
+  for (int q = __ldg(rp + i); q < e; ++q) {
+    const int col = __ldg(ci + q);
+    const T a = __ldg(v + q);
+    if (!kGhost || col < nown) {
+#pragma unroll
+      for (int u = 0; u < CB; ++u)
+        if (u < nc) acc[u] = add_rn(acc[u], mul_rn(a, __ldg(x + u * ldx + col)));
+    } else {
+#pragma unroll
+      for (int u = 0; u < CB; ++u)
+        if (u < nc) acc[u] = add_rn(acc[u], mul_rn(a, __ldg(g + u * ldg + (col - nown))));
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < CB; ++u)
+    if (u < nc) Y[i + (c0 + u) * ldy] = acc[u];
+}
+
+// Y(k, j) = X(idx[k], j): the rows packed for one peer
+template <typename T>
+__global__ void k_gather_rows(int64_t nrows, const int* __restrict__ idx, int64_t c,
+                              const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy) {
+  const int64_t total = nrows * c;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t k = e % nrows, j = e / nrows;
+    Y[k + j * ldy] = X[__ldg(idx + k) + j * ldx];
+  }
+}
+
 }  // namespace
+
+template <typename T>
+void csr_spmm_rows(int64_t nrows, const int* rows, const int* row_ptr, const int* col_idx,
+                   const T* vals, int64_t c, const T* X, int64_t ldx, int64_t nown, const T* G,
+                   int64_t ldg, T* Y, int64_t ldy, cudaStream_t s) {
+  if (nrows <= 0 || c <= 0) return;
+  auto go = [&](auto cb_tag) {
+    constexpr int CB = decltype(cb_tag)::value;
+    const dim3 grid(static_cast<unsigned>(ceil_div(nrows, 256)), static_cast<unsigned>(ceil_div(c, CB)));
+    if (G)
+      k_csr_spmm_rows<T, CB, true><<<grid, 256, 0, s>>>(static_cast<int>(nrows), rows, row_ptr, col_idx,
+                                                        vals, static_cast<int>(c), X, ldx,
+                                                        static_cast<int>(nown), G, ldg, Y, ldy);
+    else
+      k_csr_spmm_rows<T, CB, false><<<grid, 256, 0, s>>>(static_cast<int>(nrows), rows, row_ptr, col_idx,
+                                                         vals, static_cast<int>(c), X, ldx,
+                                                         static_cast<int>(nown), nullptr, 0, Y, ldy);
+  };
+  if constexpr (sizeof(T) == 8)
+    go(std::integral_constant<int, 16>());
+  else
+    go(std::integral_constant<int, 4>());
+  MPB_LAUNCH_CHECK();
+}
+
+template <typename T>
+void gather_rows(int64_t nrows, const int* idx, int64_t c, const T* X, int64_t ldx, T* Y, int64_t ldy,
+                 cudaStream_t s) {
+  if (nrows <= 0 || c <= 0) return;
+  const int64_t blocks = std::min<int64_t>(ceil_div(nrows * c, 256), 8 * kNumSMs);
+  k_gather_rows<T><<<static_cast<unsigned>(blocks), 256, 0, s>>>(nrows, idx, c, X, ldx, Y, ldy);
+  MPB_LAUNCH_CHECK();
+}
 
 template <typename T>
 void stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t c, const T* X, int64_t ldx, T* Y,
@@ -397,7 +482,12 @@ void csr_spmm(int64_t n, const int* row_ptr, const int* col_idx, const T* vals, 
   template void stencil5<T>(int64_t, int64_t, int64_t, const T*, int64_t, T*, int64_t,       \
                             cudaStream_t);                                                   \
   template void csr_spmm<T>(int64_t, const int*, const int*, const T*, int64_t, int64_t,     \
-                            const T*, int64_t, T*, int64_t, cudaStream_t);
+                            const T*, int64_t, T*, int64_t, cudaStream_t);                   \
+  template void csr_spmm_rows<T>(int64_t, const int*, const int*, const int*, const T*,      \
+                                 int64_t, const T*, int64_t, int64_t, const T*, int64_t, T*, \
+                                 int64_t, cudaStream_t);                                     \
+  template void gather_rows<T>(int64_t, const int*, int64_t, const T*, int64_t, T*, int64_t, \
+                               cudaStream_t);
 MPB_INST(double)
 MPB_INST(float)
 #undef MPB_INST

@@ -522,14 +522,65 @@ void op_apply(mpeig_ctx* ctx, const mpeig_op* op, int64_t ncols, const T* X, int
     case kOpLap2d:
       stencil5<T>(op->nx, op->ny, ncols, X, ldx, Y, ldy, s);
       return;
-    case kOpCsr:
+    case kOpCsr: {
+      const T* vals;
       if constexpr (kW) {
-        csr_spmm<double>(op->n, op->rp32, op->ci32, op->vals, op->nnz, ncols, X, ldx, Y, ldy, s);
+        vals = op->vals;
       } else {
         if (op->lower_overflow) throw Error(MPEIG_E_OVERFLOW, "to_lower: matrix exceeds binary32 range");
-        csr_spmm<float>(op->n, op->rp32, op->ci32, op->vals_l, op->nnz, ncols, X, ldx, Y, ldy, s);
+        vals = op->vals_l;
       }
+      Comm* c = dist(ctx);
+      if (!op->slab || !c) {
+        csr_spmm<T>(op->n, op->rp32, op->ci32, vals, op->nnz, ncols, X, ldx, Y, ldy, s);
+        return;
+      }
+      // row block of a sharded CSR matrix (SURVEY §8e ghost rows): pack the
+      // rows the peers need, exchange them on a side stream while the rows
+      // without ghost entries are computed, then the boundary rows
+      const int nr = c->nranks;
+      const size_t row_bytes = sizeof(T) * static_cast<size_t>(ncols);
+      const size_t need = row_bytes * static_cast<size_t>(op->n_send + 2 * op->n_ghost);
+      if (op->halo_bytes < need) {
+        if (op->halo) MPB_CUDA(cudaFreeAsync(op->halo, s));
+        MPB_CUDA(cudaMallocAsync(&op->halo, std::max<size_t>(need, 16), s));
+        op->halo_bytes = std::max<size_t>(need, 16);
+      }
+      T* sendb = static_cast<T*>(op->halo);
+      T* recvb = sendb + op->n_send * ncols;  // per peer: rows_q x ncols blocks
+      T* G = recvb + op->n_ghost * ncols;     // the ghost rows, ld n_ghost
+      for (int q = 0; q < nr; ++q)
+        gather_rows<T>(op->gx_send_rows[q], op->gx_send_idx + op->gx_send_off[q], ncols, X, ldx,
+                       sendb + op->gx_send_off[q] * ncols, op->gx_send_rows[q], s);
+      if (!op->halo_stream) {
+        MPB_CUDA(cudaStreamCreateWithFlags(&op->halo_stream, cudaStreamNonBlocking));
+        MPB_CUDA(cudaEventCreateWithFlags(&op->ev_packed, cudaEventDisableTiming));
+        MPB_CUDA(cudaEventCreateWithFlags(&op->ev_halo, cudaEventDisableTiming));
+      }
+      MPB_CUDA(cudaEventRecord(op->ev_packed, s));
+      MPB_CUDA(cudaStreamWaitEvent(op->halo_stream, op->ev_packed, 0));
+      std::vector<int64_t> sb(nr), so(nr), rb(nr), ro(nr);
+      for (int q = 0; q < nr; ++q) {
+        sb[q] = static_cast<int64_t>(row_bytes) * op->gx_send_rows[q];
+        so[q] = static_cast<int64_t>(row_bytes) * op->gx_send_off[q];
+        rb[q] = static_cast<int64_t>(row_bytes) * op->gx_recv_rows[q];
+        ro[q] = static_cast<int64_t>(row_bytes) * op->gx_recv_off[q];
+      }
+      c->alltoallv(sendb, sb.data(), so.data(), recvb, rb.data(), ro.data(), op->halo_stream);
+      for (int q = 0; q < nr; ++q)
+        if (op->gx_recv_rows[q] > 0)
+          MPB_CUDA(cudaMemcpy2DAsync(G + op->gx_recv_off[q], sizeof(T) * op->n_ghost,
+                                     recvb + op->gx_recv_off[q] * ncols,
+                                     sizeof(T) * op->gx_recv_rows[q], sizeof(T) * op->gx_recv_rows[q],
+                                     ncols, cudaMemcpyDeviceToDevice, op->halo_stream));
+      MPB_CUDA(cudaEventRecord(op->ev_halo, op->halo_stream));
+      csr_spmm_rows<T>(op->n_inner, op->rows_inner, op->rp32, op->ci32, vals, ncols, X, ldx, op->n,
+                       nullptr, 0, Y, ldy, s);
+      MPB_CUDA(cudaStreamWaitEvent(s, op->ev_halo, 0));
+      csr_spmm_rows<T>(op->n_bnd, op->rows_bnd, op->rp32, op->ci32, vals, ncols, X, ldx, op->n,
+                       op->n_ghost ? G : nullptr, op->n_ghost, Y, ldy, s);
       return;
+    }
     case kOpDense: {
       // herm_product (dense_kernels.hpp:66-72): a plain library GEMM (cuBLAS
       // DGEMM 35 TF/s = 95 % of the DMMA peak at cfg3, scripts/dense_ax_bench.py)

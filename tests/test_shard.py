@@ -201,3 +201,142 @@ def test_one_rank_sharded_path(gpu, transport):
     tot1 = r1.iterations_lower + r1.iterations_working
     tot = res.iterations_lower + res.iterations_working
     assert abs(tot - tot1) <= max(2, int(0.1 * tot1)), (tot, tot1)
+
+
+# ------------------------------------------------------- sharded CSR (ghost rows)
+
+
+def _row_blocks(n, nranks, seed=0):
+    """Uneven contiguous row blocks in rank order (each within +-25 % of n / nranks:
+    the sharded QR needs every block at least as tall as the basis is wide)."""
+    rng = np.random.default_rng(seed)
+    even = n / nranks
+    cuts = [int(round(even * (r + 1) + rng.uniform(-0.25, 0.25) * even)) for r in range(nranks - 1)]
+    b = np.concatenate([[0], cuts, [n]])
+    return [(int(a), int(c - a)) for a, c in zip(b[:-1], b[1:])]
+
+
+def _csr_block(rp, ci, v, r0, nl):
+    lo, hi = rp[r0], rp[r0 + nl]
+    return rp[r0:r0 + nl + 1] - lo, ci[lo:hi], v[lo:hi]
+
+
+def _run_csr_ranks(nranks, n, rp, ci, v, blocks, fn):
+    """fn(rank, ctx, op_rows) on `nranks` thread-ranks sharing one HostGroup."""
+    import torch
+    group = mp.HostGroup(nranks)
+    out, errs = [None] * nranks, []
+
+    def work(r):
+        try:
+            ctx = mp.Context(0, stream=torch.cuda.Stream())
+            ctx.attach_host(group, r)
+            r0, nl = blocks[r]
+            A = mp.csr_rows(n, r0, *_csr_block(rp, ci, v, r0, nl), ctx=ctx)
+            out[r] = fn(r, ctx, A)
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    return out
+
+
+def _long_range_csr(nx, ny, extra, seed):
+    """5-pt Laplacian plus `extra` random symmetric long-range couplings: ghost
+    rows from non-neighbouring ranks as well as the row-block neighbours."""
+    from problems import lap_csr
+    rp, ci, v = lap_csr(nx, ny)
+    n = nx * ny
+    rows = [dict(zip(ci[rp[i]:rp[i + 1]].tolist(), v[rp[i]:rp[i + 1]].tolist())) for i in range(n)]
+    rng = np.random.default_rng(seed)
+    for _ in range(extra):
+        i, j = (int(t) for t in rng.integers(0, n, 2))
+        if i != j:
+            w = -0.25 * rng.random()
+            rows[i][j] = rows[i].get(j, 0.0) + w
+            rows[j][i] = rows[j].get(i, 0.0) + w
+            rows[i][i] += 0.5
+            rows[j][j] += 0.5
+    rp2, ci2, v2 = [0], [], []
+    for d in rows:
+        for c in sorted(d):
+            ci2.append(c)
+            v2.append(d[c])
+        rp2.append(len(ci2))
+    return np.array(rp2, np.int64), np.array(ci2, np.int64), np.array(v2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+@pytest.mark.parametrize("prec", ["working", "lower"])
+def test_sharded_csr_apply_bitwise(gpu, nranks, prec):
+    """Row-block CSR with ghost-row exchange (any peer, uneven blocks, rows with
+    and without ghost entries) == the global spmv_block apply, bit for bit."""
+    import torch
+    nx, ny = 23, 19
+    n = nx * ny
+    rp, ci, v = _long_range_csr(nx, ny, 60, 7)
+    dt, pr = (np.float64, mp.WORKING) if prec == "working" else (np.float32, mp.LOWER)
+    X = np.asfortranarray(np.random.default_rng(5).standard_normal((n, 7)).astype(dt))
+    Ag = gpu.csr_matrix(rp, ci, v)
+    Y = mp.to_host(Ag.apply(mp.to_device(X), precision=pr))
+    blocks = _row_blocks(n, nranks, seed=nranks)
+
+    def fn(r, ctx, A):
+        r0, nl = blocks[r]
+        Xl = mp.to_device(np.asfortranarray(X[r0:r0 + nl]))
+        out = A.apply(Xl, precision=pr)
+        torch.cuda.synchronize()
+        return mp.to_host(out)
+
+    parts = _run_csr_ranks(nranks, n, rp, ci, v, blocks, fn)
+    assert np.array_equal(np.vstack(parts), Y)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["dlobpcg-dchol", "mplobpcg-schol"])
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_sharded_csr_solve_matches_single_gpu(gpu, nranks, variant):
+    """cfg2's family (2-D 5-pt Laplacian, here as CSR) row-sharded over thread
+    ranks with ghost-row exchange: same answer as the single-GPU solve."""
+    from problems import lap_csr
+    nx, ny = 26, 21
+    n = nx * ny
+    rp, ci, v = lap_csr(nx, ny)
+    cfg = mp.SolverConfig(k=5, tol=1e-10, maxit=2000, variant=variant)
+    prec = mp.WORKING if variant == "dlobpcg-dchol" else mp.LOWER
+    A1 = gpu.csr_matrix(rp, ci, v)
+    r1 = gpu.solve(A1, cfg, T=gpu.jacobi(A1, prec))
+    blocks = _row_blocks(n, nranks, seed=11)
+
+    def fn(r, ctx, A):
+        res = mp.solve(A, cfg, T=mp.jacobi(A, prec))
+        return res, mp.to_host(res.X)
+
+    outs = _run_csr_ranks(nranks, n, rp, ci, v, blocks, fn)
+    res = outs[0][0]
+    for rr, _ in outs:
+        assert np.array_equal(rr.theta, res.theta)
+    assert res.converged
+    assert np.abs(res.theta - r1.theta).max() <= 1e-10 * np.abs(r1.theta).max()
+    tot1 = r1.iterations_lower + r1.iterations_working
+    tot = res.iterations_lower + res.iterations_working
+    assert abs(tot - tot1) <= max(2, int(0.1 * tot1)), (tot, tot1)
+    X = np.vstack([x for _, x in outs])
+    assert np.linalg.norm(X.T @ X - np.eye(cfg.k)) < 1e-10
+
+
+@pytest.mark.gpu
+def test_csr_rows_partition_errors(gpu):
+    """Row blocks out of rank order are refused on every rank."""
+    from problems import lap_csr
+    rp, ci, v = lap_csr(8, 8)
+    n = 64
+    with pytest.raises(Exception):
+        _run_csr_ranks(2, n, rp, ci, v, [(32, 32), (0, 32)], lambda r, ctx, A: None)
