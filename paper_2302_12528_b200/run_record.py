@@ -4,8 +4,10 @@ eigenpair, run-level fields repeated) and the per-iteration history as JSON
 (:124-160), numbers in shortest round-trip form exactly as std::to_chars writes
 them (format_shortest, :97-102), so GPU and CPU reports diff cleanly.
 
-Host-side reporting only; the bound-analysis columns (analysis.cpp, --bounds)
-are not produced (records never carry bounds, so the CSV has the base header).
+Host-side reporting.  A record may carry an analysis.BoundReport (the reference
+CLI's --bounds, analysis.cpp / bench_main.cpp:116-171); the CSV then grows the
+bound columns (run_record.cpp:14-16, 50-66), with empty cells for records
+without bounds.
 """
 from __future__ import annotations
 
@@ -15,6 +17,8 @@ from typing import List, Optional
 
 BASE_HEADER = ("matrix,n,nnz,variant,k,m,seed,iters_lower,iters_working,converged,idx,"
                "theta,resid,t_factor,t_total")
+BOUNDS_HEADER = (",kappa,eps_A,eps_r,eps_T,eps_T_vacuous,gamma_precond,norm_te_norm_a,"
+                 "beta_mid,gamma_total_mid,rate_mid,floor")
 
 
 def format_shortest(v: float) -> str:
@@ -83,16 +87,29 @@ class RunRecord:
                    list(r.history))
 
 
+def _bound_cells(b) -> str:
+    """The 11 bound cells of one row (run_record.cpp:50-66); empty without bounds."""
+    if b is None:
+        return "," * 11
+    cells = [format_shortest(v) for v in (b.kappa, b.eps_A, b.eps_r, b.eps_T)]
+    cells.append("1" if b.eps_T_vacuous else "0")
+    cells += [format_shortest(v) for v in (b.gamma_precond_meas, b.norm_te_norm_a, b.beta_mid,
+                                           b.gamma_total_mid, b.rate_mid, b.floor)]
+    return "," + ",".join(cells)
+
+
 def run_record_csv(records: List[RunRecord]) -> str:
-    """run_record_csv (run_record.cpp:104-116)."""
-    out = [BASE_HEADER + "\n"]
+    """run_record_csv (run_record.cpp:104-116); bound columns only when a record has them."""
+    with_bounds = any(r.bounds is not None for r in records)
+    out = [BASE_HEADER + (BOUNDS_HEADER if with_bounds else "") + "\n"]
     for r in records:
         for j in range(len(r.theta)):
             out.append(",".join([
                 r.matrix_name, str(r.n), str(r.nnz), r.variant, str(r.k), str(r.m), str(r.seed),
                 str(r.iters_lower), str(r.iters_working), "1" if r.converged else "0", str(j + 1),
                 format_shortest(r.theta[j]), format_shortest(r.resid[j]),
-                format_shortest(r.t_factor), format_shortest(r.t_total)]) + "\n")
+                format_shortest(r.t_factor), format_shortest(r.t_total)]) +
+                (_bound_cells(r.bounds) if with_bounds else "") + "\n")
     return "".join(out)
 
 

@@ -110,3 +110,25 @@ def test_dense_cholesky_m96(gpu, name):
     cfg = mp.SolverConfig(variant=variant, **kw)
     r = mp.solve(A, cfg, T=T)
     check_parity(g, cfg, r, name, iter_slack=2)
+
+
+@pytest.mark.gpu
+def test_bound_report_measured_through_device_preconditioner(gpu):
+    """--bounds (bench_main.cpp:116-171, test_analysis.cpp:159-176): gamma measured by
+    densifying the DEVICE dense-Cholesky preconditioner; the working build is
+    essentially exact, the binary32 build inside Lemma 2's bound."""
+    import paper_2302_12528_b200.analysis as an
+    from problems import spd_dense
+    n, kappa = 30, 100.0
+    A, lam = spd_dense(n, kappa, 31)
+    bw = an.bounds_for(A, "dlobpcg-dchol")
+    bl = an.bounds_for(A, "mplobpcg-schol")
+    assert abs(bw.kappa - lam[-1] / lam[0]) <= 1e-8 * bw.kappa
+    assert bw.gamma_precond_meas < 1e4 * kappa * 2.0 ** -53
+    assert bw.gamma_precond_meas < bl.gamma_precond_meas <= an.gamma_precond_bound(n, kappa, 2.0 ** -24)
+    assert bl.norm_te_norm_a == pytest.approx(kappa, rel=1e-3)
+    assert 0 < bl.rate_mid < 1 and 0 < bl.floor < 1e-10
+    from paper_2302_12528_b200.run_record import RunRecord, run_record_csv
+    rec = RunRecord("spd30", n, n * n, "mplobpcg-schol", 2, 3, 0, 1, 1, True, [1.0, 2.0], [0, 0],
+                    bounds=bl)
+    assert ",kappa," in run_record_csv([rec])
