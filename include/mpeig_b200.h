@@ -393,7 +393,14 @@ int mpeig_gemm_f64(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, double alpha
  *              (default), 0 = never (SIMT FFMA kernels), 2 = always.
  *   "gram_tma":  TMA-fed tensor-core Gram (1, default) or the cp.async one (0).
  *   "gemm_tma2": tensor-core block update with C split once per call (1,
- *              default) or the per-tile split (0; in place only c <= 128). */
+ *              default) or the per-tile split (0; in place only c <= 128).
+ * Diagnostics of the tensor-core kernels (results change with "tc_nprod",
+ * "tc_twoacc" and "tc_ablate"; never set them for a real solve):
+ *   "tc_nprod" part products (8), "tc_twoacc" second accumulator (1),
+ *   "tc_stage" staged TMA-store epilogue (1), "g2_depth" ring depths as RSD
+ *   digits (0 = by shared memory), "tc_ablate" bit mask that removes data
+ *   paths (1 C copies / loads, 2 split, 4 stores, 8 A loads, 16 TMEM drain;
+ *   bits 16+: CTA cap) to find what bounds a kernel. */
 int mpeig_set_process_option(const char* key, int value);
 /* the same two products in binary32 (the lower-precision stage's kernels) */
 int mpeig_gram_f32(mpeig_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda,

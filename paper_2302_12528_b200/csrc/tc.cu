@@ -1397,10 +1397,7 @@ k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         asm volatile("fence.proxy.async.shared::cta;\n");
         __syncwarp();
         asm volatile("bar.sync 1, %0;\n" ::"r"(kG2EpiThreads));
-        if (ablate & 128) {  // diagnostics: staged tile written by the epilogue threads
-          for (int cc = cbeg; cc < cend; ++cc)
-            if (i < n && j0 + cc < c) Y[i + static_cast<int64_t>(j0 + cc) * ldy] = stg[cc * kTcM + 32 * quarter + lane];
-        } else if (warp == 10 && lane == 0) {
+        if (warp == 10 && lane == 0) {
           asm volatile(
               "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
                   reinterpret_cast<uint64_t>(&tmY)),
