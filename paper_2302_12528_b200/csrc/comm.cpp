@@ -171,6 +171,7 @@ void nccl_check(ncclResult_t rc, const char* what) {
 
 struct NcclComm final : Comm {
   ncclComm_t comm = nullptr;
+  bool capturable() const override { return true; }
   ~NcclComm() override {
     if (comm) api().destroy(comm);
   }

@@ -42,6 +42,9 @@ struct Comm {
   virtual void alltoallv(const void* send, const int64_t* send_bytes, const int64_t* send_off,
                          void* recv, const int64_t* recv_bytes, const int64_t* recv_off,
                          cudaStream_t s) = 0;
+  // every exchange is stream-ordered without host synchronisation (NCCL), so
+  // an iteration body containing them can be captured into a CUDA graph
+  virtual bool capturable() const { return false; }
 };
 
 // ---- ranks as threads of one process ------------------------------------

@@ -1438,8 +1438,10 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
   mpeig_timings local{};
   mpeig_timings& tm = tim ? *tim : local;
   const bool mixed = opt.use_mixed_qr != 0;
-  // (row-sharded runs exchange through the host or NCCL inside the body: no graph)
-  const bool use_graphs = ctx->use_graphs != 0 && !g_prof_on && !dist(ctx);
+  // row-sharded runs: the body's collectives and halo / ghost exchanges are
+  // captured with it over NCCL (stream-ordered); the host-staged transport
+  // synchronises inside the body and runs it eagerly
+  const bool use_graphs = ctx->use_graphs != 0 && !g_prof_on && (!dist(ctx) || dist(ctx)->capturable());
 
   copy_block<T>(n, m, X0, ldx0, w.S.p, w.ld, s);
   op_apply<T>(ctx, A, m, w.S.p, w.ld, w.AS.p, w.ld);
