@@ -441,6 +441,8 @@ def run_ours(args):
 
 
 DMMA_PEAK_TFS = 37.1  # fp64 mma.sync m8n8k4, measured in-repo (profiles/r01_microbench_b200.txt)
+BF16_PEAK_TFS = 2150.0  # tcgen05 kind::f16 M=128 N=160 issue rate, scripts/micro/umma_rate.cu
+TC_FAMILIES = ("gram_f32", "gemm_f32")
 
 
 AT_SCALE = {
@@ -530,7 +532,10 @@ def at_scale_kernels(mp, peak_gbs):
             "GBps": round(gbs, 1) if gbs else None,
             "hbm_frac": round(gbs / peak_gbs, 3) if gbs else None,
             "TFps": round(tfs, 2) if tfs else None,
-            "dmma_frac_if_fp64": round(tfs / DMMA_PEAK_TFS, 3) if tfs else None}
+            # fp64 families against the DMMA peak; the binary32 tensor-core families
+            # (gram_f32 / gemm_f32: 8 bf16 part products each) against bf16 peak / 8
+            "tensor_frac": (round(tfs / DMMA_PEAK_TFS, 3) if tfs and not name.endswith("_f32") else
+                            round(8 * tfs / BF16_PEAK_TFS, 3) if tfs and name in TC_FAMILIES else None)}
     return out
 
 

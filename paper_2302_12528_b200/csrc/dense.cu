@@ -704,7 +704,7 @@ static void gram_impl(int64_t n, int64_t ka, const T* A, int64_t lda, int64_t kb
       MPB_CUDA(cudaMemsetAsync(G + j * ldg, 0, sizeof(T) * ka, s));
     return;
   }
-  ProfScope prof("gram", s, double(sizeof(T)) * n * (A == B ? ka : ka + kb),
+  ProfScope prof(sizeof(T) == 8 ? "gram" : "gram_f32", s, double(sizeof(T)) * n * (A == B ? ka : ka + kb),
                  2.0 * n * ka * kb);
   const GramPlan p = gram_plan(n, ka, kb);
   // workspace: [CholQR ticket (16 B, fixed place for every shape) | partials]
@@ -817,7 +817,7 @@ static void gemm_impl(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int6
     }
     return;
   }
-  ProfScope prof("gemm", s, double(sizeof(T)) * n * (k + (beta != T(0) ? 2 : 1) * c),
+  ProfScope prof(sizeof(T) == 8 ? "gemm" : "gemm_f32", s, double(sizeof(T)) * n * (k + (beta != T(0) ? 2 : 1) * c),
                  2.0 * n * k * c);
   dim3 grid(static_cast<unsigned>(ceil_div(n, kTile)), static_cast<unsigned>(ceil_div(c, kTile)), nz);
   if constexpr (sizeof(T) == 8) {

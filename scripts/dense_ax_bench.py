@@ -58,8 +58,9 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / reps
-            if name.startswith("ours") and "gemm" in rep:
-                ms = rep["gemm"]["ms"] / rep["gemm"]["count"]  # kernel-only (library events)
+            key = "gemm" if "gemm" in rep else "gemm_f32"
+            if name.startswith("ours") and key in rep:
+                ms = rep[key]["ms"] / rep[key]["count"]  # kernel-only (library events)
             out[name] = {"ms": round(ms, 4), "TFps": round(flops / ms / 1e9, 2),
                          "GBps": round(bytes_ / ms / 1e6, 1)}
         out[f"max_rel_diff_{sfx}"] = (Y1.double() - Y2.double()).abs().max().item() / Y2.double().abs().max().item()

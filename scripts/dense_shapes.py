@@ -58,7 +58,7 @@ for sfx in dtypes:
         ]
         for name, ka, kb, fn in cases:
             ctx.check(fn())
-            r = prof(lambda: ctx.check(fn()))["gram"]
+            r = prof(lambda: ctx.check(fn()))["gram" if sfx == "f64" else "gram_f32"]
             ms = r["ms"] / r["count"]
             out["rows"].append({"dtype": sfx, "m": m, "op": name, "shape": [ka, kb],
                                 "ms": round(ms, 4), "TFps": round(2.0 * n * ka * kb / (ms * 1e9), 2),
@@ -71,7 +71,7 @@ for sfx in dtypes:
         ]
         for name, k, c, fn in gcases:
             ctx.check(fn())
-            r = prof(lambda: ctx.check(fn()))["gemm"]
+            r = prof(lambda: ctx.check(fn()))["gemm" if sfx == "f64" else "gemm_f32"]
             ms = r["ms"] / r["count"]
             out["rows"].append({"dtype": sfx, "m": m, "op": name, "shape": [k, c],
                                 "ms": round(ms, 4), "TFps": round(2.0 * n * k * c / (ms * 1e9), 2),

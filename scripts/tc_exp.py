@@ -16,6 +16,6 @@ for ka in (48, 240):
         with mp.profile():
             for _ in range(3): f()
             torch.cuda.synchronize()
-            r = mp.profile.report()["gram"]
+            r = mp.profile.report()["gram_f32"]
         out.append((ka, nprod, st, r["ms"] / r["count"]))
         print(out[-1], flush=True)
