@@ -394,6 +394,9 @@ int mpeig_gemm_f64(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, double alpha
  *   "gram_tma":  TMA-fed tensor-core Gram (1, default) or the cp.async one (0).
  *   "gemm_tma2": tensor-core block update with C split once per call (1,
  *              default) or the per-tile split (0; in place only c <= 128).
+ *   "spchol_threads": host threads of the sparse-Cholesky factorisation (0 =
+ *              the hardware's, capped at 32; the factor is bitwise the same
+ *              for any count).
  * Diagnostics of the tensor-core kernels (results change with "tc_nprod",
  * "tc_twoacc" and "tc_ablate"; never set them for a real solve):
  *   "tc_nprod" part products (8), "tc_twoacc" second accumulator (1),

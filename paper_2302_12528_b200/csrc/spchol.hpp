@@ -14,6 +14,8 @@ struct HostFactor {  // CSR lower factor, diagonal last in each row
   std::vector<F> v;
 };
 
+// host factorisation threads (process option "spchol_threads"; 0 = hardware)
+extern int g_spchol_threads;
 std::vector<int64_t> rcm_ordering(int64_t n, const int64_t* rp, const int64_t* ci);
 template <typename V>
 void csr_permute(int64_t n, const int64_t* rp, const int64_t* ci, const V* v,

@@ -4,9 +4,12 @@
 // sparse_kernels.hpp:92-170); the per-iteration triangular solves run on the
 // device (spchol.cu).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <memory>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "context.hpp"
@@ -81,9 +84,19 @@ template void csr_permute<double>(int64_t, const int64_t*, const int64_t*, const
                                   const std::vector<int64_t>&, std::vector<int64_t>&,
                                   std::vector<int64_t>&, std::vector<double>&);
 
+int g_spchol_threads = 0;  // host factorisation threads (0: the hardware's, capped at 32)
+
 // Up-looking Cholesky of B = L L^T (sparse_cholesky, sparse_kernels.hpp:92-170),
 // arithmetic in F: row i of L solves L(0:i, 0:i) l = b_i over the etree
 // reach of row i, columns ascending; diagonal stored last in each row.
+//
+// Rows run concurrently, round-robin over host threads: row i's solve reads
+// the finished rows j of its reach (each published with a release flag), so
+// a thread waits only where its reach meets a row still in flight -- for the
+// banded RCM orderings that is the tail of the reach.  Every entry is formed
+// by the same operations in the same order as the sequential algorithm, so
+// the factor is bitwise the reference's; the first failing row (lowest index)
+// raises the sequential error.
 template <typename F>
 HostFactor<F> sparse_cholesky_host(int64_t n, const std::vector<int64_t>& rp,
                                    const std::vector<int64_t>& ci, const std::vector<F>& v) {
@@ -97,54 +110,107 @@ HostFactor<F> sparse_cholesky_host(int64_t n, const std::vector<int64_t>& rp,
         if (up == -1) parent[j] = i;
         j = up;
       }
+  int nt = g_spchol_threads > 0 ? g_spchol_threads
+                                 : static_cast<int>(std::min(32u, std::max(1u, std::thread::hardware_concurrency())));
+  if (n < 4096) nt = 1;
+  // per row: the reach columns then the diagonal, values alike
+  std::vector<std::vector<int64_t>> rci(static_cast<size_t>(n));
+  std::vector<std::vector<F>> rv(static_cast<size_t>(n));
+  std::unique_ptr<std::atomic<int>[]> done(new std::atomic<int>[static_cast<size_t>(n)]);
+  for (int64_t i = 0; i < n; ++i) done[i].store(0, std::memory_order_relaxed);
+  std::atomic<int64_t> first_bad{n};
+  std::vector<int> bad_kind(static_cast<size_t>(n), 0);  // 1 overflow, 2 not PD, 3 after a failed row
+  auto worker = [&](int t) {
+    std::vector<F> x(static_cast<size_t>(n), F(0));
+    std::vector<char> mark(static_cast<size_t>(n), 0);
+    std::vector<int64_t> reach;
+    for (int64_t i = t; i < n; i += nt) {
+      // reach of row i in the etree, ascending (ereach, :60-83)
+      reach.clear();
+      mark[i] = 1;
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+        for (int64_t j = ci[p]; j != -1 && j < i && !mark[j]; j = parent[j]) {
+          mark[j] = 1;
+          reach.push_back(j);
+        }
+      std::sort(reach.begin(), reach.end());
+      for (int64_t j : reach) mark[j] = 0;
+      mark[i] = 0;
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+        if (ci[p] <= i) x[ci[p]] = v[p];
+      F sq = F(0);
+      bool upstream_bad = false;
+      for (int64_t j : reach) {
+        int st;
+        while ((st = done[j].load(std::memory_order_acquire)) == 0) std::this_thread::yield();
+        if (st != 1) {
+          upstream_bad = true;
+          break;
+        }
+        const std::vector<int64_t>& cj = rci[j];
+        const std::vector<F>& vj = rv[j];
+        F s = x[j];
+        const size_t nd = cj.size() - 1;  // the diagonal is last
+        for (size_t p = 0; p < nd; ++p) s -= x[cj[p]] * vj[p];
+        const F lij = s / vj[nd];
+        x[j] = lij;
+        sq += lij * lij;
+      }
+      int kind = upstream_bad ? 3 : 0;
+      F d = F(0);
+      if (!upstream_bad) {
+        d = x[i] - sq;
+        if (!std::isfinite(static_cast<double>(d)))
+          kind = 1;
+        else if (!(d > F(0)))
+          kind = 2;
+      }
+      if (kind == 0) {
+        std::vector<int64_t>& c = rci[i];
+        std::vector<F>& w = rv[i];
+        c.reserve(reach.size() + 1);
+        w.reserve(reach.size() + 1);
+        for (int64_t j : reach) {
+          c.push_back(j);
+          w.push_back(x[j]);
+        }
+        c.push_back(i);
+        w.push_back(std::sqrt(d));
+      } else {
+        bad_kind[i] = kind;
+        int64_t cur = first_bad.load();
+        while (i < cur && !first_bad.compare_exchange_weak(cur, i)) {
+        }
+      }
+      for (int64_t j : reach) x[j] = F(0);
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+        if (ci[p] <= i) x[ci[p]] = F(0);
+      done[i].store(kind == 0 ? 1 : 2, std::memory_order_release);
+    }
+  };
+  if (nt == 1) {
+    worker(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t) pool.emplace_back(worker, t);
+    for (auto& th : pool) th.join();
+  }
+  const int64_t bad = first_bad.load();
+  if (bad < n) {  // the lowest failing row is the sequential algorithm's first
+    if (bad_kind[bad] == 1)
+      throw Error(MPEIG_E_OVERFLOW, "sparse_cholesky: row " + std::to_string(bad) + " overflowed", bad);
+    throw Error(MPEIG_E_NOT_PD, "sparse_cholesky: nonpositive pivot at row " + std::to_string(bad), bad);
+  }
   HostFactor<F> L;
-  L.rp.assign(1, 0);
-  std::vector<F> x(static_cast<size_t>(n), F(0));
-  std::vector<char> mark(static_cast<size_t>(n), 0);
-  std::vector<int64_t> reach, row_of(static_cast<size_t>(n)), diag_at(static_cast<size_t>(n));
+  L.rp.assign(static_cast<size_t>(n) + 1, 0);
+  for (int64_t i = 0; i < n; ++i) L.rp[i + 1] = L.rp[i] + static_cast<int64_t>(rci[i].size());
+  L.ci.reserve(static_cast<size_t>(L.rp[n]));
+  L.v.reserve(static_cast<size_t>(L.rp[n]));
   for (int64_t i = 0; i < n; ++i) {
-    // reach of row i in the etree, ascending (ereach, :60-83)
-    reach.clear();
-    mark[i] = 1;
-    for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
-      for (int64_t j = ci[p]; j != -1 && j < i && !mark[j]; j = parent[j]) {
-        mark[j] = 1;
-        reach.push_back(j);
-      }
-    std::sort(reach.begin(), reach.end());
-    for (int64_t j : reach) mark[j] = 0;
-    mark[i] = 0;
-    bool has_diag = false;
-    for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
-      if (ci[p] <= i) {
-        x[ci[p]] = v[p];
-        has_diag |= ci[p] == i;
-      }
-    (void)has_diag;
-    F sq = F(0);
-    for (int64_t j : reach) {
-      F s = x[j];
-      for (int64_t p = row_of[j]; p < diag_at[j]; ++p) s -= x[L.ci[p]] * L.v[p];
-      const F lij = s / L.v[diag_at[j]];
-      x[j] = lij;
-      sq += lij * lij;
-    }
-    const F d = x[i] - sq;
-    if (!std::isfinite(static_cast<double>(d)))
-      throw Error(MPEIG_E_OVERFLOW, "sparse_cholesky: row " + std::to_string(i) + " overflowed", i);
-    if (!(d > F(0)))
-      throw Error(MPEIG_E_NOT_PD, "sparse_cholesky: nonpositive pivot at row " + std::to_string(i), i);
-    row_of[i] = static_cast<int64_t>(L.ci.size());
-    for (int64_t j : reach) {
-      L.ci.push_back(j);
-      L.v.push_back(x[j]);
-      x[j] = F(0);
-    }
-    diag_at[i] = static_cast<int64_t>(L.ci.size());
-    L.ci.push_back(i);
-    L.v.push_back(std::sqrt(d));
-    x[i] = F(0);
-    L.rp.push_back(static_cast<int64_t>(L.ci.size()));
+    L.ci.insert(L.ci.end(), rci[i].begin(), rci[i].end());
+    L.v.insert(L.v.end(), rv[i].begin(), rv[i].end());
+    std::vector<int64_t>().swap(rci[i]);
+    std::vector<F>().swap(rv[i]);
   }
   return L;
 }

@@ -129,3 +129,50 @@ def test_sparse_cholesky_errors(gpu):
     T = mp.sparse_cholesky(mp.csr_matrix(rp, ci, v), mp.WORKING)
     with pytest.raises(mp.ConfigError):
         T.apply(torch.ones((1, 64), dtype=torch.float32, device="cuda"), precision=mp.LOWER)
+
+
+@pytest.mark.parametrize("prec", ["working", "lower"])
+def test_parallel_host_factor_is_bitwise_sequential(gpu, prec):
+    """The up-looking factor with rows in flight on host threads (spchol_host.cpp)
+    forms every entry by the same operations in the same order as one thread:
+    the preconditioner applies bitwise identically for any thread count."""
+    import torch
+    mp = gpu
+    rp, ci, v = lap_csr(20, 22, 18)
+    n = len(rp) - 1
+    A = mp.csr_matrix(rp, ci, v)
+    p = mp.WORKING if prec == "working" else mp.LOWER
+    dt = np.float64 if prec == "working" else np.float32
+    X = mp.to_device(np.asfortranarray(np.random.default_rng(9).standard_normal((n, 5)).astype(dt)))
+    ctx = A.ctx
+    outs = []
+    try:
+        for th in (1, 3, 8):
+            assert ctx.lib.mpeig_set_process_option(b"spchol_threads", th) == 0
+            T = mp.sparse_cholesky(A, p)
+            outs.append((T.factor_nnz, mp.to_host(T.apply(X, precision=p))))
+            torch.cuda.synchronize()
+    finally:
+        ctx.lib.mpeig_set_process_option(b"spchol_threads", 0)
+    for nnz, Y in outs[1:]:
+        assert nnz == outs[0][0]
+        assert np.array_equal(Y, outs[0][1])
+
+
+def test_parallel_host_factor_reports_first_failing_row(gpu):
+    """An indefinite system: every thread count reports the sequential algorithm's
+    first nonpositive pivot (the lowest failing row)."""
+    mp = gpu
+    rp, ci, v = lap_csr(18, 17, 16, shift=0.5)  # lambda_min < 0.5: indefinite
+    A = mp.csr_matrix(rp, ci, v)
+    ctx = A.ctx
+    idx = []
+    try:
+        for th in (1, 6):
+            assert ctx.lib.mpeig_set_process_option(b"spchol_threads", th) == 0
+            with pytest.raises(mp.NotPositiveDefinite) as e:
+                mp.sparse_cholesky(A, mp.WORKING, perm=None)
+            idx.append(e.value.index)
+    finally:
+        ctx.lib.mpeig_set_process_option(b"spchol_threads", 0)
+    assert idx[0] == idx[1] and idx[0] >= 0
