@@ -374,33 +374,47 @@ int mpeig_op_csr_rows(mpeig_ctx* ctx, int64_t n_global, int64_t row0, int64_t n_
     set_device(ctx);
     Comm* c = dist(ctx);
     const int nr = c ? c->nranks : 1, me = c ? c->rank : 0;
-    if (n_local < 1 || row0 < 0 || row0 + n_local > n_global)
-      throw Error(MPEIG_E_DIMENSION, "csr_rows: bad row range");
     if (!c && (row0 != 0 || n_local != n_global))
       throw Error(MPEIG_E_CONFIG, "csr_rows: a partial row block needs a communicator");
-    const int64_t nnz = row_ptr_host[n_local];
-    for (int64_t i = 0; i < n_local; ++i) {
-      if (row_ptr_host[i + 1] < row_ptr_host[i]) throw Error(MPEIG_E_DIMENSION, "csr: row_ptr not monotone");
-      for (int64_t q = row_ptr_host[i]; q < row_ptr_host[i + 1]; ++q) {
+    // validate locally, then agree: a rank with a bad block must not leave the
+    // others waiting in the partition exchange, so every rank throws together
+    int bad_code = MPEIG_OK;
+    std::string bad_msg;
+    const auto fail = [&](int code, const char* msg) {
+      if (bad_code == MPEIG_OK) {
+        bad_code = code;
+        bad_msg = msg;
+      }
+    };
+    if (n_local < 1 || row0 < 0 || row0 + n_local > n_global) fail(MPEIG_E_DIMENSION, "csr_rows: bad row range");
+    const int64_t nnz = bad_code == MPEIG_OK ? row_ptr_host[n_local] : 0;
+    for (int64_t i = 0; bad_code == MPEIG_OK && i < n_local; ++i) {
+      if (row_ptr_host[i + 1] < row_ptr_host[i]) fail(MPEIG_E_DIMENSION, "csr: row_ptr not monotone");
+      for (int64_t q = row_ptr_host[i]; bad_code == MPEIG_OK && q < row_ptr_host[i + 1]; ++q) {
         if (col_idx_host[q] < 0 || col_idx_host[q] >= n_global)
-          throw Error(MPEIG_E_DIMENSION, "from_triplets: index out of range");
-        if (q > row_ptr_host[i] && col_idx_host[q] <= col_idx_host[q - 1])
-          throw Error(MPEIG_E_DIMENSION, "csr: columns must be sorted and unique per row");
+          fail(MPEIG_E_DIMENSION, "from_triplets: index out of range");
+        else if (q > row_ptr_host[i] && col_idx_host[q] <= col_idx_host[q - 1])
+          fail(MPEIG_E_DIMENSION, "csr: columns must be sorted and unique per row");
       }
     }
-    if (n_global >= INT32_MAX || nnz >= INT32_MAX)
-      throw Error(MPEIG_E_CONFIG, "csr: n and nnz must stay below 2^31 (int32 device indices)");
+    if (bad_code == MPEIG_OK && (n_global >= INT32_MAX || nnz >= INT32_MAX))
+      fail(MPEIG_E_CONFIG, "csr: n and nnz must stay below 2^31 (int32 device indices)");
     cudaStream_t s = ctx->stream;
     // the rank partition: contiguous row blocks in rank order covering n_global
     std::vector<int64_t> start(static_cast<size_t>(nr) + 1, 0);
     if (c) {
-      const std::vector<int64_t> rr = allgather_host(c, {row0, n_local}, s);
+      const std::vector<int64_t> rr = allgather_host(c, {row0, n_local, bad_code}, s);
+      if (bad_code != MPEIG_OK) throw Error(bad_code, bad_msg);
+      for (int q = 0; q < nr; ++q)
+        if (rr[3 * q + 2] != MPEIG_OK)
+          throw Error(static_cast<int>(rr[3 * q + 2]), "csr_rows: rank " + std::to_string(q) + "'s row block is invalid");
       for (int q = 0; q < nr; ++q) {
-        if (rr[2 * q] != start[q])
+        if (rr[3 * q] != start[q])
           throw Error(MPEIG_E_CONFIG, "csr_rows: rank row blocks must be contiguous in rank order");
-        start[q + 1] = rr[2 * q] + rr[2 * q + 1];
+        start[q + 1] = rr[3 * q] + rr[3 * q + 1];
       }
     } else {
+      if (bad_code != MPEIG_OK) throw Error(bad_code, bad_msg);
       start[1] = n_global;
     }
     if (start[nr] != n_global) throw Error(MPEIG_E_CONFIG, "csr_rows: row blocks do not cover n_global");

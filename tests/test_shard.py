@@ -340,3 +340,36 @@ def test_csr_rows_partition_errors(gpu):
     n = 64
     with pytest.raises(Exception):
         _run_csr_ranks(2, n, rp, ci, v, [(32, 32), (0, 32)], lambda r, ctx, A: None)
+
+
+@pytest.mark.gpu
+def test_csr_rows_invalid_block_raises_on_every_rank(gpu):
+    """A rank whose block is invalid (column out of range) makes every rank raise
+    after the partition exchange -- nobody is left waiting in a collective."""
+    import torch
+    from problems import lap_csr
+    rp, ci, v = lap_csr(8, 8)
+    n = 64
+    group = mp.HostGroup(2)
+    errs = [None, None]
+
+    def work(r):
+        try:
+            ctx = mp.Context(0, stream=torch.cuda.Stream())
+            ctx.attach_host(group, r)
+            r0, nl = (0, 32) if r == 0 else (32, 32)
+            brp, bci, bv = _csr_block(rp, ci, v, r0, nl)
+            if r == 1:
+                bci = bci.copy()
+                bci[-1] = n + 5
+            mp.csr_rows(n, r0, brp, bci, bv, ctx=ctx)
+        except Exception as e:
+            errs[r] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert all(not t.is_alive() for t in th)
+    assert all(isinstance(e, mp.MpeigError) for e in errs), errs
