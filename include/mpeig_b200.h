@@ -394,6 +394,8 @@ int mpeig_gemm_f64(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, double alpha
  *   "gram_tma":  TMA-fed tensor-core Gram (1, default) or the cp.async one (0).
  *   "gemm_tma2": tensor-core block update with C split once per call (1,
  *              default) or the per-tile split (0; in place only c <= 128).
+ *   "pdl":      programmatic kernel -> kernel edges in the captured iteration
+ *              graphs (1, default; 0 = ordinary edges; bitwise identical).
  *   "spchol_threads": host threads of the sparse-Cholesky factorisation (0 =
  *              the hardware's, capped at 32; the factor is bitwise the same
  *              for any count).

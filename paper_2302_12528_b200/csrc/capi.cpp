@@ -972,6 +972,7 @@ int mpeig_gemm_f64(mpeig_ctx* ctx, int64_t n, int64_t k, int64_t c, double alpha
 int mpeig_set_process_option(const char* key, int value) {
   const std::string k = key ? key : "";
   if (k == "gram_tma") { g_gram_tma = value; return MPEIG_OK; }
+  if (k == "pdl") { g_pdl = value; return MPEIG_OK; }
   if (k == "spchol_threads") { g_spchol_threads = value; return MPEIG_OK; }
   if (k == "gemm_tma2") { g_gemm_tma2 = value; return MPEIG_OK; }
   if (k == "tc_twoacc") { g_tc_twoacc = value; return MPEIG_OK; }

@@ -36,6 +36,12 @@ void smem_opt_in(const void* kernel, size_t bytes);
 // Kernels launched by this library (reported as gpu_launches by bench.py).
 extern std::atomic<int64_t> g_launches;
 
+// Programmatic dependent launch: every kernel waits here for the grids it
+// depends on (complete, memory visible) before touching global memory, so a
+// captured iteration graph may launch it early (programmatic edges, solver.cpp);
+// a no-op for an ordinary launch
+#define MPB_PDL_WAIT() asm volatile("griddepcontrol.wait;\n" ::: "memory")
+
 #define MPB_LAUNCH_CHECK()                      \
   do {                                          \
     ::mpb::g_launches.fetch_add(1, std::memory_order_relaxed); \

@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(256)
 k_gram_combine(int64_t nchunk, int ka, int kb, const T* __restrict__ part, T* __restrict__ G,
                int64_t ldg, int sym, int* __restrict__ ticket, T* __restrict__ L,
                T* __restrict__ Uinv, int* status, T tau2) {
+  MPB_PDL_WAIT();
   combine_body(nchunk, ka, kb, part, G, ldg, sym);
   if (!ticket) return;
   __shared__ int s_last;
@@ -173,6 +174,7 @@ k_gram_partial(int64_t n, int ka, int kb, const T* __restrict__ A, int64_t lda,
                const T* __restrict__ B, int64_t ldb, int64_t rows_per_chunk, int tiles_n,
                int64_t nchunk, T* __restrict__ part, int* __restrict__ ctr, T* G, int64_t ldg,
                int sym) {
+  MPB_PDL_WAIT();
   constexpr int TILE = 16 * TM;
   constexpr int kSm = 2 * kGramBK * (TILE + 1) > TILE * TILE ? 2 * kGramBK * (TILE + 1) : TILE * TILE;
   __shared__ T sm[kSm];
@@ -296,6 +298,7 @@ k_gram_dmma(int64_t n, int ka, int kb, const double* __restrict__ A, int64_t lda
             const double* __restrict__ B, int64_t ldb, int64_t rows_per_chunk, int tiles_n,
             int64_t nchunk, double* __restrict__ part, int* __restrict__ ctr, double* G,
             int64_t ldg, int sym) {
+  MPB_PDL_WAIT();
   constexpr int TILE = 16 * MT;
   extern __shared__ __align__(16) unsigned char gsm[];
   auto As = reinterpret_cast<double(*)[TILE][kDPitch]>(gsm);
@@ -379,6 +382,7 @@ __global__ void __launch_bounds__(128)
 k_gemm_dmma(int64_t n, int k, int c, double alpha, const double* __restrict__ A, int64_t lda,
             const double* __restrict__ Cm, int64_t ldc, double beta, const double* Z, int64_t ldz,
             double* Y, int64_t ldy, const double* __restrict__ A2, double* Y2) {
+  MPB_PDL_WAIT();
   constexpr int TN = 16 * NT;
   if (blockIdx.z) {  // paired product Y2 = alpha A2 C (same C, k, c; beta = 0)
     A = A2;
@@ -472,6 +476,7 @@ __global__ void __launch_bounds__(256)
 k_gemm_tn(int64_t n, int k, int c, T alpha, const T* __restrict__ A, int64_t lda,
           const T* __restrict__ Cm, int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y,
           int64_t ldy, const T* __restrict__ A2, T* Y2) {
+  MPB_PDL_WAIT();
   if (blockIdx.z) {
     A = A2;
     Y = Y2;
@@ -537,6 +542,7 @@ __global__ void __launch_bounds__(128)
 k_gemm_rows(int64_t n, int k, int c, T alpha, const T* __restrict__ A, int64_t lda,
             const T* __restrict__ Cm, int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y,
             int64_t ldy, const T* __restrict__ A2, T* Y2) {
+  MPB_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char rows_sm[];
   T* Cs = reinterpret_cast<T*>(rows_sm);  // k x CT, row l contiguous
   if (blockIdx.z) {
@@ -595,6 +601,7 @@ k_gemm_rows(int64_t n, int k, int c, T alpha, const T* __restrict__ A, int64_t l
 
 __global__ void k_f64_to_f32(int64_t n, int64_t c, const double* __restrict__ src, int64_t lds,
                              float* __restrict__ dst, int64_t ldd, int* overflow) {
+  MPB_PDL_WAIT();
   const int64_t total = n * c;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -608,6 +615,7 @@ __global__ void k_f64_to_f32(int64_t n, int64_t c, const double* __restrict__ sr
 
 __global__ void k_f32_to_f64(int64_t n, int64_t c, const float* __restrict__ src, int64_t lds,
                              double* __restrict__ dst, int64_t ldd) {
+  MPB_PDL_WAIT();
   const int64_t total = n * c;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -619,6 +627,7 @@ __global__ void k_f32_to_f64(int64_t n, int64_t c, const float* __restrict__ src
 template <typename T>
 __global__ void k_copy_block(int64_t n, int64_t c, const T* __restrict__ src, int64_t lds,
                              T* __restrict__ dst, int64_t ldd) {
+  MPB_PDL_WAIT();
   const int64_t total = n * c;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -630,6 +639,7 @@ __global__ void k_copy_block(int64_t n, int64_t c, const T* __restrict__ src, in
 template <typename T>
 __global__ void k_scale(int64_t n, int64_t c, T alpha, const T* __restrict__ X, int64_t ldx,
                         T* __restrict__ Y, int64_t ldy) {
+  MPB_PDL_WAIT();
   const int64_t total = n * c;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -641,6 +651,7 @@ __global__ void k_scale(int64_t n, int64_t c, T alpha, const T* __restrict__ X, 
 template <typename T>
 __global__ void k_frob_partial(int64_t n, int64_t c, const T* __restrict__ X, int64_t ldx,
                                double* __restrict__ part) {
+  MPB_PDL_WAIT();
   __shared__ double red[256];
   double acc = 0;
   const int64_t total = n * c;
@@ -660,6 +671,7 @@ __global__ void k_frob_partial(int64_t n, int64_t c, const T* __restrict__ X, in
 }
 
 __global__ void k_sum_partials(int64_t np, const double* __restrict__ part, double* out) {
+  MPB_PDL_WAIT();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double s = 0;
     for (int64_t i = 0; i < np; ++i) s += part[i];
@@ -935,6 +947,7 @@ void convert_f64_to_f32(int64_t n, int64_t c, const double* src, int64_t lds, fl
 }
 
 __global__ void k_add_diag(int64_t n, double* __restrict__ A, int64_t lda, double shift) {
+  MPB_PDL_WAIT();
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) A[i + i * lda] = __dadd_rn(A[i + i * lda], shift);
 }
@@ -943,6 +956,7 @@ __global__ void k_add_diag(int64_t n, double* __restrict__ A, int64_t lda, doubl
 // the lower-triangle reads and the upper-triangle writes are coalesced
 template <typename T>
 __global__ void k_symmetrize_lower(int64_t n, T* __restrict__ A, int64_t lda) {
+  MPB_PDL_WAIT();
   __shared__ T tile[32][33];
   const int64_t bi = blockIdx.x, bj = blockIdx.y;  // tile row / column
   if (bi < bj) return;
@@ -997,6 +1011,7 @@ void copy_block(int64_t n, int64_t c, const T* src, int64_t lds, T* dst, int64_t
 __global__ void k_scatter_rows(int64_t n, int64_t c, const double* __restrict__ src, int64_t lds,
                                const int64_t* __restrict__ perm, double* __restrict__ dst,
                                int64_t ldd) {
+  MPB_PDL_WAIT();
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (t >= n * c) return;
   const int64_t i = t % n, j = t / n;

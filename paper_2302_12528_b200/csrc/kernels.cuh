@@ -57,7 +57,8 @@ bool gemm_tc_f32(int64_t n, int64_t k, int64_t c, float alpha, const float* A, i
 extern int g_gram_tc, g_gemm_tc;
 extern int g_gemm_tma2, g_tc_twoacc, g_tc_ablate, g_g2_depth, g_tc_stage;
 extern int g_tc_nprod, g_tc_store;
-extern int g_gram_tma;  // TMA-fed tensor-core Gram (1, default) or the cp.async one (0)
+extern int g_gram_tma;
+extern int g_pdl;  // programmatic edges in the captured iteration graphs (solver.cpp)  // TMA-fed tensor-core Gram (1, default) or the cp.async one (0)
 // (crossovers measured at n = 2M, scripts/dense_shapes.py: the tensor-core
 // Gram wins from 32 x 16 up, the tensor-core block update once k * c reaches
 // the m = 48 project-out's 96 x 48; narrower updates stay on the FFMA kernel)

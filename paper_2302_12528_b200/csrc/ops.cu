@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(256)
 k_stencil7(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t ldx,
            T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi,
            const T* __restrict__ dg, int64_t ldl, int64_t ldu) {
+  MPB_PDL_WAIT();
   const int64_t n = nx * ny * nz;
   const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (p >= n) return;
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(256)
 k_stencil7_vec(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t ldx,
                T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi,
            const T* __restrict__ dg, int64_t ldl, int64_t ldu) {
+  MPB_PDL_WAIT();
   using VT = typename VecT<T, V>::type;
   const int64_t nv = nx * ny * nz / V;
   const int64_t pv = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(256)
 k_stencil7_zm(int64_t nx, int64_t ny, int64_t nz, const T* __restrict__ X, int64_t ldx,
               T* __restrict__ Y, int64_t ldy, const T* __restrict__ hlo, const T* __restrict__ hhi,
            const T* __restrict__ dg, int64_t ldl, int64_t ldu) {
+  MPB_PDL_WAIT();
   using VT = typename VecT<T, V>::type;
   const int64_t sz = nx * ny;
   const int64_t npv = sz / V;
@@ -214,6 +217,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_stencil5(int64_t nx, int64_t ny, const T* __restrict__ X, int64_t ldx, T* __restrict__ Y,
            int64_t ldy) {
+  MPB_PDL_WAIT();
   const int64_t n = nx * ny;
   const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (p >= n) return;
@@ -236,6 +240,7 @@ template <typename T, int V, int YC>
 __global__ void __launch_bounds__(256)
 k_stencil5_ym(int64_t nx, int64_t ny, const T* __restrict__ X, int64_t ldx, T* __restrict__ Y,
               int64_t ldy) {
+  MPB_PDL_WAIT();
   using VT = typename VecT<T, V>::type;
   const int64_t xv = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (xv * V >= nx) return;
@@ -285,6 +290,7 @@ template <typename T, int CB>
 __global__ void __launch_bounds__(256)
 k_csr_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ v,
            int c, const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy) {
+  MPB_PDL_WAIT();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int c0 = blockIdx.y * CB;
@@ -315,6 +321,7 @@ k_csr_spmm_rows(int nrows, const int* __restrict__ rows, const int* __restrict__
                 const int* __restrict__ ci, const T* __restrict__ v, int c, const T* __restrict__ X,
                 int64_t ldx, int nown, const T* __restrict__ G, int64_t ldg, T* __restrict__ Y,
                 int64_t ldy) {
+  MPB_PDL_WAIT();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nrows) return;
   const int i = rows ? __ldg(rows + t) : t;
@@ -348,6 +355,7 @@ k_csr_spmm_rows(int nrows, const int* __restrict__ rows, const int* __restrict__
 template <typename T>
 __global__ void k_gather_rows(int64_t nrows, const int* __restrict__ idx, int64_t c,
                               const T* __restrict__ X, int64_t ldx, T* __restrict__ Y, int64_t ldy) {
+  MPB_PDL_WAIT();
   const int64_t total = nrows * c;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {

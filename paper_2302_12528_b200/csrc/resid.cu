@@ -59,6 +59,7 @@ k_residual(int64_t n, int m, const T* __restrict__ X, int64_t ldx, const T* __re
            int64_t ldax, const T* __restrict__ theta, const void* __restrict__ dinv,
            T* __restrict__ W, int64_t ldw, int64_t rows_per_chunk, double* __restrict__ part,
            int* overflow) {
+  MPB_PDL_WAIT();
   // norms accumulate in real_t<T> like DenseMatrix<T>::col_norm
   // (dense_matrix.hpp:74-82): fp32 sums in the fp32 stage, fp64 otherwise
   using Acc = T;
@@ -152,6 +153,7 @@ k_residual(int64_t n, int m, const T* __restrict__ X, int64_t ldx, const T* __re
 template <typename Acc>
 __global__ void k_resid_norms(int64_t nchunk, int m, const double* __restrict__ part,
                               double* __restrict__ rnorm, double* __restrict__ xnorm, int raw) {
+  MPB_PDL_WAIT();
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (t >= 2 * m) return;
   const int j = t >> 1, which = t & 1;
@@ -165,6 +167,7 @@ __global__ void k_resid_norms(int64_t nchunk, int m, const double* __restrict__ 
 // sqrt in real_t<T> after the row-sharded sums were allreduced
 template <typename Acc>
 __global__ void k_norms_sqrt(int64_t count, double* __restrict__ v) {
+  MPB_PDL_WAIT();
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < count) v[i] = static_cast<double>(sqrt(static_cast<Acc>(v[i])));
 }
@@ -173,6 +176,7 @@ template <typename T, int MODE>
 __global__ void k_jacobi(int64_t n, int64_t c, const T* __restrict__ R, int64_t ldr,
                          const void* __restrict__ dinv, T* __restrict__ W, int64_t ldw,
                          int* overflow) {
+  MPB_PDL_WAIT();
   int ovf = 0;
   const int64_t total = n * c;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -187,6 +191,7 @@ template <typename T>
 __global__ void k_subtract(int64_t n, int64_t c, const T* __restrict__ X, int64_t ldx,
                            const T* __restrict__ W, int64_t ldw, T* __restrict__ Y,
                            int64_t ldy) {
+  MPB_PDL_WAIT();
   const int64_t total = n * c;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {

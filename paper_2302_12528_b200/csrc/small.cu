@@ -27,6 +27,7 @@ constexpr int kMaxHlP = 256;  // largest P block (block size m) of the HL update
 
 template <typename T>
 __global__ void k_symmetrize(int64_t s, T* G, int64_t ldg) {
+  MPB_PDL_WAIT();
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < s * s;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t i = idx % s, j = idx / s;
@@ -53,6 +54,7 @@ template <typename T>
 __global__ void __launch_bounds__(kSmallThreads)
 k_cholesky_inv(int m, const T* __restrict__ G, int64_t ldg, T* __restrict__ L,
                T* __restrict__ Uinv, int* status, int use_smem, T tau2) {
+  MPB_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char raw[];
   T* As = use_smem ? reinterpret_cast<T*>(raw) : L;  // working lower triangle -> L
   T* Us = use_smem ? As + m * m : Uinv;
@@ -133,6 +135,7 @@ template <typename T>
 __global__ void __launch_bounds__(kSmallThreads)
 k_upper_inverse(int m, const T* __restrict__ R, int64_t ldr, T* __restrict__ Rinv, int* status,
                 int use_smem) {
+  MPB_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char raw[];
   T* Rs = reinterpret_cast<T*>(raw);
   T* Is = use_smem ? Rs + m * m : Rinv;
@@ -189,6 +192,7 @@ k_upper_inverse(int m, const T* __restrict__ R, int64_t ldr, T* __restrict__ Rin
 template <typename T>
 __global__ void k_small_transpose(int r, int c, const T* __restrict__ A, int64_t lda,
                                   T* __restrict__ B, int64_t ldb) {
+  MPB_PDL_WAIT();
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
        idx < static_cast<int64_t>(r) * c; idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int i = static_cast<int>(idx % r), j = static_cast<int>(idx / r);
@@ -199,6 +203,7 @@ __global__ void k_small_transpose(int r, int c, const T* __restrict__ A, int64_t
 template <typename T>
 __global__ void k_small_matmul(int r, int k, int c, const T* __restrict__ A, int64_t lda,
                                const T* __restrict__ B, int64_t ldb, T* __restrict__ C, int64_t ldc) {
+  MPB_PDL_WAIT();
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
        idx < static_cast<int64_t>(r) * c; idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int i = static_cast<int>(idx % r), j = static_cast<int>(idx / r);
@@ -218,6 +223,7 @@ template <typename T>
 __global__ void __launch_bounds__(kSmallThreads)
 k_hl_coeffs(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __restrict__ coef,
             T* __restrict__ scratch, int* fallback, int use_smem, T* __restrict__ qout) {
+  MPB_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char raw[];
   T* M = use_smem ? reinterpret_cast<T*>(raw) : scratch;
   T* V = M + p * m;
@@ -353,6 +359,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_hl_cpv(int s, int m, int p, const T* __restrict__ C, int64_t ldc, const T* __restrict__ Q,
          T* __restrict__ coef, const int* fallback) {
+  MPB_PDL_WAIT();
   const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<int64_t>(s) * p) return;
   const int i = static_cast<int>(idx % s), j = static_cast<int>(idx / s);
@@ -383,6 +390,7 @@ template <typename T, int MAXM>
 __global__ void __launch_bounds__(32)
 k_cholesky_inv_warp(int m, const T* __restrict__ G, int64_t ldg, T* __restrict__ L,
                     T* __restrict__ Uinv, int* status, T tau2) {
+  MPB_PDL_WAIT();
   warp_cholesky_inv<T, MAXM>(m, G, ldg, L, Uinv, status, tau2);
 }
 
@@ -391,6 +399,7 @@ template <typename T, int MAXM>
 __global__ void __launch_bounds__(32)
 k_upper_inverse_warp(int m, const T* __restrict__ R, int64_t ldr, T* __restrict__ Rinv,
                      int* status) {
+  MPB_PDL_WAIT();
   warp_upper_inverse<T, T, MAXM>(m, R, ldr, nullptr, Rinv, status);
 }
 
@@ -405,6 +414,7 @@ template <typename T, int MAXM>
 __global__ void __launch_bounds__(kSmallThreads)
 k_hl_coeffs_warp(int s, int m, int p, const T* __restrict__ C, int64_t ldc, T* __restrict__ coef,
                  int* fallback) {
+  MPB_PDL_WAIT();
   __shared__ T Vs[MAXM][MAXM + 1];  // Vs[j][a]: reflector j, component a (a >= j)
   __shared__ double Bs[MAXM];       // reflector scalars (fp64)
   __shared__ T Sg[MAXM];            // sign of R(j, j)

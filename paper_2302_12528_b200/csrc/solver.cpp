@@ -1407,6 +1407,38 @@ static void spec_body(Work<T>& w, const mpeig_op* A, const mpeig_op* T_op, int64
   if (ev.on) MPB_CUDA(cudaEventRecord(ev.e[3], s));
 }
 
+// Programmatic dependent launch inside the iteration graph: every kernel ->
+// kernel edge becomes a programmatic edge, so a kernel is launched while its
+// predecessor's CTAs drain and waits in MPB_PDL_WAIT (every kernel's first
+// statement) for the predecessor to complete with its memory visible.
+// Memset / memcpy edges keep full ordering.  Results are bitwise unchanged;
+// cfg1 0.4467 -> 0.4420 s (scripts/pdl_ab.py).  g_pdl = 2 (diagnostic): the
+// launch-completion port, dependents resident from the predecessor's start --
+// 0.484 s, they crowd the SMs the chain still needs.
+int g_pdl = 1;
+
+static void make_kernel_edges_programmatic(cudaGraph_t graph) {
+  size_t ne = 0;
+  MPB_CUDA(cudaGraphGetEdges_v2(graph, nullptr, nullptr, nullptr, &ne));
+  if (ne == 0) return;
+  std::vector<cudaGraphNode_t> from(ne), to(ne);
+  std::vector<cudaGraphEdgeData> data(ne);
+  MPB_CUDA(cudaGraphGetEdges_v2(graph, from.data(), to.data(), data.data(), &ne));
+  for (size_t e = 0; e < ne; ++e) {
+    cudaGraphNodeType tf, tt;
+    MPB_CUDA(cudaGraphNodeGetType(from[e], &tf));
+    MPB_CUDA(cudaGraphNodeGetType(to[e], &tt));
+    if (tf != cudaGraphNodeTypeKernel || tt != cudaGraphNodeTypeKernel) continue;
+    if (data[e].type != cudaGraphDependencyTypeDefault) continue;
+    MPB_CUDA(cudaGraphRemoveDependencies_v2(graph, &from[e], &to[e], &data[e], 1));
+    cudaGraphEdgeData pd{};
+    pd.from_port = g_pdl == 2 ? cudaGraphKernelNodePortLaunchCompletion : cudaGraphKernelNodePortProgrammatic;
+    pd.to_port = 0;
+    pd.type = cudaGraphDependencyTypeProgrammatic;
+    MPB_CUDA(cudaGraphAddDependencies_v2(graph, &from[e], &to[e], &pd, 1));
+  }
+}
+
 static bool graph_capturable(const mpeig_op* op) {
   return op && (op->kind == kOpLap3d || op->kind == kOpLap2d || op->kind == kOpCsr ||
                 op->kind == kOpJacobi);
@@ -1535,6 +1567,7 @@ StageResult lobpcg_stage(mpeig_ctx* ctx, const mpeig_op* A, int64_t n, const T* 
             throw;
           }
           MPB_CUDA(cudaStreamEndCapture(s, &graph));
+          if (g_pdl) make_kernel_edges_programmatic(graph);
           MPB_CUDA(cudaGraphInstantiate(&exec, graph, 0));
           cudaGraphDestroy(graph);
           // capture records launches without running them: count them per replay

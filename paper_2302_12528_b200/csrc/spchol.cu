@@ -78,6 +78,7 @@ k_spchol_solve(int n, const int* __restrict__ Lrp, const int* __restrict__ Lci,
                const int* __restrict__ Urp, const int* __restrict__ Uci, const F* __restrict__ Uv,
                const int* __restrict__ Usp, const int* __restrict__ Usp2, const int* __restrict__ perm, const Tin* __restrict__ B, int64_t ldb,
                Tout* __restrict__ Y, int64_t ldy, int* overflow, F* gy, int use_smem) {
+  MPB_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char raw[];
   __shared__ double tile_raw[32 * 33];
   __shared__ double acc_raw[32], dg_raw[32];

@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
 k_gram_tc(int64_t n, int ka, int kb, const float* __restrict__ A, int64_t lda,
           const float* __restrict__ B, int64_t ldb, int64_t rows_per_chunk, int tiles_n, int ntile,
           float* __restrict__ part, int nprod, int do_store) {
+  MPB_PDL_WAIT();
   using Cf = TcCfg<NMAX, KC>;
   constexpr int kTcSlots = Cf::kSlots, kTcSbo = Cf::kSbo, kTcPartA = Cf::kPartA;
   constexpr int kTcBufBytes = Cf::kBufBytes, kTcPitch = Cf::kPitch, kTcRingBytes = Cf::kRingBytes;
@@ -378,6 +379,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __global__ void __launch_bounds__(kTmSplitThreads + 64, 1)
 k_gram_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            int64_t n, int ka, int kb, int tiles_n, int ntile, float* __restrict__ part, int ablate) {
+  MPB_PDL_WAIT();
   extern __shared__ unsigned char tsm_raw[];
   // 1024-B alignment for the 128-B swizzled TMA boxes
   unsigned char* tsm = reinterpret_cast<unsigned char*>(
@@ -580,6 +582,7 @@ k_gemm_tc(int64_t n, int k, int c, int ntile, int tiles_n, int64_t ntiles, float
           const float* __restrict__ A, int64_t lda, const float* __restrict__ Cm, int64_t ldc,
           float beta, const float* Z, int64_t ldz, float* Y, int64_t ldy,
           const float* __restrict__ A2, float* Y2) {
+  MPB_PDL_WAIT();
   if (blockIdx.z) {
     A = A2;
     Y = Y2;
@@ -841,6 +844,7 @@ __global__ void __launch_bounds__(kTmSplitThreads + 64, 1)
 k_gemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
            int64_t n, int k, int c, int ntile, int tiles_n, int64_t ntiles, float alpha, float beta,
            const float* Z, int64_t ldz, float* Y, int64_t ldy) {
+  MPB_PDL_WAIT();
   extern __shared__ unsigned char gsm_raw[];
   unsigned char* gsm = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -1088,6 +1092,7 @@ static_assert(g2_smem(kG2NMax, G2Depth{3, 3, 2}) <= kG2SmemMax, "k_gemm_tma2 sha
 // beyond k and c; thread = (column, 8-k chunk) of one stage
 __global__ void k_csplit(int k, int c, int N, int nst, int tiles_n, const float* __restrict__ C,
                          int64_t ldc, unsigned char* __restrict__ img) {
+  MPB_PDL_WAIT();
   const int64_t total = static_cast<int64_t>(tiles_n) * nst * N * (kG2KC / 8);
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1126,6 +1131,7 @@ k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             const unsigned char* __restrict__ cimg, int64_t n, int k, int c, int N, int tiles_n,
             int64_t rtiles, G2Depth dep, int stage_out, int two_acc, int nprod, int ablate,
             float alpha, float beta, const float* Z, int64_t ldz, float* Y, int64_t ldy) {
+  MPB_PDL_WAIT();
   extern __shared__ unsigned char g2_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(g2_raw) + 1023) & ~static_cast<uintptr_t>(1023));

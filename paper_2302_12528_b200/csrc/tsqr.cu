@@ -145,6 +145,7 @@ template <typename Tin, typename Tq>
 __global__ void __launch_bounds__(kThreads)
 k_tsqr_leaf(int64_t n, int m, const Tin* __restrict__ W, int64_t ldw, int b, Tq* __restrict__ Rout,
             int* status) {
+  MPB_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tq* t = reinterpret_cast<Tq*>(smem_raw);
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * b;
@@ -167,6 +168,7 @@ k_tsqr_leaf(int64_t n, int m, const Tin* __restrict__ W, int64_t ldw, int b, Tq*
 template <typename Tq>
 __global__ void __launch_bounds__(kThreads)
 k_tsqr_node(int64_t nR, int m, int group, const Tq* __restrict__ Rin, Tq* __restrict__ Rout) {
+  MPB_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tq* t = reinterpret_cast<Tq*>(smem_raw);
   const int b = group * m;
@@ -190,6 +192,7 @@ k_tsqr_node(int64_t nR, int m, int group, const Tq* __restrict__ Rin, Tq* __rest
 template <typename Tq>
 __global__ void k_tsqr_finish(int m, const Tq* __restrict__ Rin, Tq* __restrict__ R, int64_t ldr,
                               int* status, int numeric_rank_check) {
+  MPB_PDL_WAIT();
   for (int64_t idx = threadIdx.x; idx < static_cast<int64_t>(m) * m; idx += blockDim.x) {
     const int i = static_cast<int>(idx % m), j = static_cast<int>(idx / m);
     const Tq d = Rin[i + static_cast<int64_t>(i) * m];
@@ -331,6 +334,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
 k_tsqr_reg(int64_t n, int m, const Tin* __restrict__ W, int64_t ldw, Tq* __restrict__ Rbuf,
            int* __restrict__ counters, int64_t nleaf, int G, Tq* __restrict__ Rfinal, int64_t ldr,
            int* status, int numeric_rank_check, Tin* __restrict__ Rw_out, Tin* __restrict__ Rinv_out) {
+  MPB_PDL_WAIT();
   using Tile = RegTile<Tq, NW, RPL, MPW>;
   constexpr int B = Tile::B;
   __shared__ __align__(16) Tq vbuf[2][B];
@@ -478,6 +482,7 @@ template <typename Tin, typename Tq, int RPL>
 __global__ void __launch_bounds__(128)
 k_tsqr_warpleaf(int64_t rows, int m, const Tin* __restrict__ W, int64_t ldw, int64_t nleaf,
                 Tq* __restrict__ out, int* status) {
+  MPB_PDL_WAIT();
   constexpr int B = 32 * RPL;
   extern __shared__ __align__(16) unsigned char wl_sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
