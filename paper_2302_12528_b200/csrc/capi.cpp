@@ -148,7 +148,10 @@ void mpeig_ctx_destroy(mpeig_ctx* ctx) {
   if (ctx->d_status) cudaFree(ctx->d_status);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
-  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->own_stream && ctx->stream) {
+    tc_scratch_release(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+  }
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
   if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
   delete ctx->comm;

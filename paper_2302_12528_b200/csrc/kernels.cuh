@@ -34,6 +34,8 @@ constexpr int64_t kGemmInplaceCols = 64;
 // binary32 c <= 256 on the tensor-core path when it applies (gemm_tn checks)
 bool gemm_inplace_ok(bool f64, int64_t n, int64_t k, int64_t c);
 bool gemm_tc_inplace_ok(int64_t c);
+// frees the tensor-core scratch of a stream about to be destroyed
+void tc_scratch_release(cudaStream_t s);
 template <typename T>
 void gemm_tn(int64_t n, int64_t k, int64_t c, T alpha, const T* A, int64_t lda, const T* C,
              int64_t ldc, T beta, const T* Z, int64_t ldz, T* Y, int64_t ldy, cudaStream_t s);

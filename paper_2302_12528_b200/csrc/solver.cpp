@@ -190,8 +190,8 @@ static void chol_apply_gemm(mpeig_ctx* ctx, const F* M, int64_t n, int64_t c, co
                              static_cast<int>(ldb), &zero, Y, static_cast<int>(ldy)),
                  "cublasDgemm");
   } else {
-    // fp32: the tcgen05 block update (exact 3-way bf16 split; 53 TF/s at
-    // n = 16384, c = 96, faster than cuBLAS SGEMM's 46)
+    // fp32: the tcgen05 block update (exact 3-way bf16 split; 96 TF/s at
+    // n = 16384, c = 96 against cuBLAS SGEMM's 46, profiles/r02_dense_ax.json)
     (void)one;
     (void)zero;
     (void)ni;

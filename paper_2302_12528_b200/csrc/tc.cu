@@ -29,6 +29,7 @@
 #include <map>
 #include <mutex>
 #include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -1540,28 +1541,57 @@ bool gemm_tc_eligible(int64_t n, int64_t k, int64_t c, int64_t lda, int64_t ldc,
 namespace {
 // Per (device, stream) scratch for the split C images; grown outside stream
 // capture only (a captured call that needs more falls back to k_gemm_tma).
-// Old buffers are kept (never freed while a graph may reference them).
-unsigned char* tc_scratch(size_t bytes, cudaStream_t s) {
+// Outgrown buffers stay allocated (a captured graph may still use them) until
+// the owning context releases its stream (tc_scratch_release).
+struct TcScratch {
+  void* cur = nullptr;
+  size_t cap = 0;
+  std::vector<void*> old;
+};
+std::mutex& tc_scratch_mu() {
   static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> bufs;
+  return mu;
+}
+std::map<std::pair<int, cudaStream_t>, TcScratch>& tc_scratch_map() {
+  static std::map<std::pair<int, cudaStream_t>, TcScratch> m;
+  return m;
+}
+unsigned char* tc_scratch(size_t bytes, cudaStream_t s) {
   int dev = 0;
   MPB_CUDA(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> lock(mu);
-  auto& b = bufs[{dev, s}];
-  if (b.second >= bytes) return static_cast<unsigned char*>(b.first);
+  std::lock_guard<std::mutex> lock(tc_scratch_mu());
+  TcScratch& b = tc_scratch_map()[{dev, s}];
+  if (b.cap >= bytes) return static_cast<unsigned char*>(b.cur);
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   MPB_CUDA(cudaStreamIsCapturing(s, &cs));
   if (cs != cudaStreamCaptureStatusNone) return nullptr;
-  const size_t want = std::max<size_t>({bytes, 2 * b.second, size_t(4) << 20});
+  const size_t want = std::max<size_t>({bytes, 2 * b.cap, size_t(4) << 20});
   void* p = nullptr;
   if (cudaMalloc(&p, want) != cudaSuccess) {
     (void)cudaGetLastError();
     return nullptr;
   }
-  b = {p, want};
+  if (b.cur) b.old.push_back(b.cur);
+  b.cur = p;
+  b.cap = want;
   return static_cast<unsigned char*>(p);
 }
 }  // namespace
+
+// the scratch of a stream the caller is about to destroy (its work finished)
+void tc_scratch_release(cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(tc_scratch_mu());
+  auto& m = tc_scratch_map();
+  for (auto it = m.begin(); it != m.end();) {
+    if (it->first.second == s) {
+      cudaFree(it->second.cur);
+      for (void* p : it->second.old) cudaFree(p);
+      it = m.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
 
 int g_gemm_tma2 = 1, g_tc_twoacc = 1, g_tc_ablate = 0, g_g2_depth = 0, g_tc_stage = 1;
 
