@@ -456,6 +456,7 @@ k_gram_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         mbar_wait(&sfull[buf], (st >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         const uint32_t a0 = smem_u32(split + buf * kTmBuf), b0 = a0 + 3 * kTmPartA;
+        const uint64_t ad0 = umma_desc(a0, 128, 512), bd0 = umma_desc(b0, 128, 512);
         constexpr int pa_of[kTcProducts] = {0, 0, 1, 0, 1, 2, 1, 2};
         constexpr int pb_of[kTcProducts] = {0, 1, 0, 2, 1, 0, 2, 1};
         const uint32_t part_b = static_cast<uint32_t>(N * kTmKC * 2);
@@ -464,8 +465,9 @@ k_gram_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
 #pragma unroll
           for (int kk = 0; kk < kTmKC / 16; ++kk) {
             if ((ablate & 4) && pr > 0) continue;  // diagnostics: one product
-            const uint64_t ad = umma_desc(a0 + pa_of[pr] * kTmPartA + kk * 256, 128, 512);
-            const uint64_t bd = umma_desc(b0 + pb_of[pr] * part_b + kk * 256, 128, 512);
+            // descriptor = base + (byte offset >> 4): smem addresses stay below 2^18
+            const uint64_t ad = ad0 + static_cast<uint64_t>((pa_of[pr] * kTmPartA + kk * 256) >> 4);
+            const uint64_t bd = bd0 + static_cast<uint64_t>((pb_of[pr] * part_b + kk * 256) >> 4);
             if (pr == 0)
               mma_bf16(tmem, ad, bd, idesc, (st | kk) != 0);
             else
@@ -1260,6 +1262,8 @@ k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         wait_(&cfull[cp.slot], cp.phase);
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         const uint32_t a0 = smem_u32(abuf + sp.slot * kG2BufA), c0 = smem_u32(cbuf + cp.slot * cbytes);
+        // descriptor = base + (byte offset >> 4): smem addresses stay below 2^18
+        const uint64_t ad0 = umma_desc(a0, 128, kG2Sbo), bd0 = umma_desc(c0, 128, 512);
         const uint32_t acc = tmem + static_cast<uint32_t>(ap.slot * set_cols);
         constexpr int pa_of[kTcProducts] = {0, 0, 1, 0, 1, 2, 1, 2};
         constexpr int pb_of[kTcProducts] = {0, 1, 0, 2, 1, 0, 2, 1};
@@ -1268,8 +1272,8 @@ k_gemm_tma2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll
           for (int kk = 0; kk < kG2KC / 16; ++kk) {
             if (pr >= nprod) continue;
-            const uint64_t ad = umma_desc(a0 + pa_of[pr] * kG2PartA + kk * 256, 128, kG2Sbo);
-            const uint64_t bd = umma_desc(c0 + pb_of[pr] * part_c + kk * 256, 128, 512);
+            const uint64_t ad = ad0 + static_cast<uint64_t>((pa_of[pr] * kG2PartA + kk * 256) >> 4);
+            const uint64_t bd = bd0 + static_cast<uint64_t>((pb_of[pr] * part_c + kk * 256) >> 4);
             if (pr == 0)
               mma_bf16(acc, ad, bd, idesc, (st | kk) != 0);
             else

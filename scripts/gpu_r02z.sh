@@ -1,5 +1,5 @@
-for o in gram_tma=1 gram_tma=2; do
+timeout 600 python -m pytest tests/test_gpu_kernels.py -q -p no:cacheprovider -x -k "gram or gemm" 2>&1 | tail -2
+for o in "" "tc_ablate=31"; do
 echo "== $o"
-MPEIG_OPTS=$o timeout 300 python scripts/tc_acc.py 2>&1 | grep gram
-MPEIG_OPTS=$o timeout 600 python scripts/dense_shapes.py 2097152 16,48,80,192 f32 2>&1 >/dev/null | grep gram | cut -c1-105
+MPEIG_OPTS=$o timeout 600 python scripts/dense_shapes.py 2097152 48,80 f32 2>&1 >/dev/null | cut -c1-100
 done
