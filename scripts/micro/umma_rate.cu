@@ -29,11 +29,12 @@ __device__ bool wait_bar(uint64_t* bar, uint32_t phase) {
   }
 }
 
-__global__ void __launch_bounds__(128, 1) k_rate(int N, int layout, int iters, long long* cyc) {
+__global__ void __launch_bounds__(128, 1) k_rate(int N, int layout, int iters, long long* cyc, int mode) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t bar2[2];
   for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&slot)), "r"(512));
@@ -42,6 +43,8 @@ __global__ void __launch_bounds__(128, 1) k_rate(int N, int layout, int iters, l
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&bar[0])), "r"(1));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&bar[1])), "r"(1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&bar2[0])), "r"(1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&bar2[1])), "r"(1));
     asm volatile("fence.mbarrier_init.release.cluster;\n");
   }
   asm volatile("fence.proxy.async.shared::cta;\n");
@@ -69,12 +72,20 @@ __global__ void __launch_bounds__(128, 1) k_rate(int N, int layout, int iters, l
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
+      if (mode >= 4 && it >= 1) {  // the MMA warp waits on an already completed barrier + fence
+        wait_bar(&bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
+      }
+      if (mode >= 2) asm volatile("tcgen05.fence::after_thread_sync;\n");
+#pragma unroll
       for (int j = 0; j < 16; ++j) {
+        // mode 0: alternate two accumulators; mode >= 1: 2 MMAs to acc 0 then 14 to acc 1
+        const uint32_t acc = mode == 0 ? (j & 1) * 256 : (j < 2 ? 0 : 256);
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + (j & 1) * 256),
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + acc),
                      "l"(ad[j & 1]), "l"(bd[j & 1]), "r"(idesc), "r"(1));
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&bar[it & 1])));
+      if (mode >= 3) asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&bar2[it & 1])));
       if (it >= 1) {  // keep at most two batches in flight (one barrier each)
         const int p = it - 1;
         if (!wait_bar(&bar[p & 1], (p >> 1) & 1)) { cyc[blockIdx.x] = -1; break; }
@@ -96,30 +107,28 @@ int main() {
   const int smem = 96 * 1024 + 1024;
   cudaFuncSetAttribute(k_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
-  for (int layout = 0; layout < 3; ++layout)
-    for (int N : {64, 128, 160, 256}) {
+  for (int mode = 0; mode < 5; ++mode)
+    for (int N : {80, 160}) {
+      const int layout = 1;
       for (int rep = 0; rep < 2; ++rep) {
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaMemset(d, 0, 148 * sizeof(long long));
         cudaEventRecord(e0);
-        k_rate<<<148, 128, smem>>>(N, layout, iters, d);
+        k_rate<<<148, 128, smem>>>(N, layout, iters, d, mode);
         cudaEventRecord(e1);
         cudaError_t err = cudaDeviceSynchronize();
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
         long long h[148];
         cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+        if (err != cudaSuccess || h[0] < 0) { printf("mode %d N %d: %s / timeout\n", mode, N, cudaGetErrorString(err)); return 1; }
         double avg = 0;
         for (int i = 0; i < 148; ++i) avg += h[i];
         avg /= 148;
-        const double per = avg / (iters * 16.0);
-        const double tflops = 2.0 * 128 * N * 16 * 16.0 * iters * 148 / (ms * 1e-3) / 1e12;
-        if (err != cudaSuccess || h[0] < 0) { printf("layout %d N %d: %s / timeout\n", layout, N, cudaGetErrorString(err)); return 1; }
         if (rep)
-          printf("layout %d N %3d: %7.1f clk/MMA (floor %5.1f)  %7.1f TF/s bf16  %s\n", layout, N, per,
-                 128.0 * N / 256, tflops, cudaGetErrorString(err));
+          printf("mode %d N %3d: %7.1f clk/MMA (floor %5.1f)\n", mode, N, avg / (iters * 16.0), 128.0 * N / 256);
       }
     }
   return 0;

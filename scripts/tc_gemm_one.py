@@ -13,6 +13,10 @@ k = int(sys.argv[2]) if len(sys.argv) > 2 else 240
 c = int(sys.argv[3]) if len(sys.argv) > 3 else 160
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 ctx = mp.default_context()
+import os  # noqa: E402
+for kv in filter(None, os.environ.get("MPEIG_OPTS", "").split(",")):
+    key, val = kv.split("=")
+    assert ctx.lib.mpeig_set_process_option(key.encode(), int(val)) == 0, kv
 A = torch.randn(k, n, device="cuda")
 Cm = torch.randn(c, k, device="cuda")
 Y = torch.empty(c, n, device="cuda")
