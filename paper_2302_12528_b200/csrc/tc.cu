@@ -1,27 +1,28 @@
-// tc.cu -- binary32 Gram products on the 5th-generation tensor cores (tcgen05).
+// tc.cu -- the binary32 stage's Gram products and block updates on the
+// 5th-generation tensor cores (tcgen05 / TMEM / TMA).
 //
-// The lower-precision stage's Gram G = A^T B (adjoint_matmul<float>,
-// dense_kernels.hpp:36-52) on B200's tcgen05 MMA.  tcgen05 has no fp32
-// multiplicand kind, so each binary32 operand is split exactly into three
+// G = A^T B (adjoint_matmul<float>, dense_kernels.hpp:36-52) and Y = beta Z +
+// alpha A C (matmul<float>, :20-34) on B200's tcgen05 MMA.  tcgen05 has no
+// fp32 multiplicand kind, so each binary32 operand is split exactly into three
 // bfloat16 parts, x = hi + mid + lo (8 + 8 + 8 significand bits: every split
-// is exact, bf16 has binary32's exponent range), and the part products are
-// accumulated in fp32 in tensor memory.  Each bf16 x bf16 product is exact
-// in fp32, so the result carries only fp32 accumulation rounding -- the same
-// order of error as the reference's binary32 dot products, at tensor-core
-// throughput instead of the FFMA pipe's.
+// is exact, bf16 has binary32's exponent range), and 8 part products (all but
+// lo x lo, ~2^-32 relative) are accumulated in fp32 in tensor memory: hi x hi
+// in one accumulator, the 7 smaller products in a second, summed once in the
+// epilogue.  Each bf16 x bf16 product is exact in fp32, so the result carries
+// only fp32 accumulation rounding -- the order of error of the reference's
+// binary32 dot products, at tensor-core throughput.
 //
-// CTA (256 threads) = one 128 x N output tile x one row chunk of n:
-//   * all 8 warps stream the fp32 columns of A and B (32 rows per stage,
-//     prefetched two stages ahead into registers; the column-major operands
-//     are K-major here), split them by truncation into the bf16 hi/mid/lo
-//     operand tiles and store those in the canonical K-major no-swizzle
-//     core-matrix layout (8 rows x 16 B);
-//   * thread 0 issues 8 part products (all but lo x lo, ~2^-32 relative) x 2
-//     K-steps of tcgen05.mma (M = 128, N = the B tile width <= 256, K = 16)
-//     into one TMEM accumulator and commits them to an mbarrier, so the split
-//     of the next stage overlaps the MMAs of this one (double-buffered);
-//   * epilogue: tcgen05.ld (32x32b) -- thread = output row -- to the chunk's
-//     partial, reduced GPU-wide by the deterministic combine of dense.cu.
+// Kernels (newest first; the older ones remain as fallbacks):
+//   * k_gemm_tma2: block update, C split once per call into its shared-memory
+//     stage images (k_csplit), A streamed by TMA, warp roles (TMA, split, MMA,
+//     epilogue, C bulk copy), double-buffered accumulator sets or a staged
+//     TMA-store epilogue; in place when one column tile covers c.
+//   * k_gram_tma: Gram chunk partials with TMA-fed 4-deep rings (reduced by
+//     the deterministic combine of dense.cu).
+//   * k_gemm_tma / k_gemm_tc / k_gram_tc: per-tile C split / cp.async loaders
+//     (fallbacks: a call inside stream capture without scratch, no tensor-map
+//     encoder).
+// DESIGN.md §3.3-3.4 has the measurements and what bounds each kernel.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
