@@ -67,6 +67,62 @@ def test_nccl_id_broadcast_world2():
     assert res[0][1] == (0, 16) and res[1][1] == (16, 16)
 
 
+def _gloo_inputs_worker(rank, world, port, out):
+    """Each rank builds its share of a sharded run's inputs the way bench.py does
+    (slab, start block and sketch rows), gathers them over gloo, and rank 0
+    compares with the single-process draw; the timings reduce by max."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    nx, ny, nz, m, seed = 6, 5, 11, 4, 7
+    z0, nzl = mp.slab_partition(nz, world)[rank]
+    n_glob, row0, n = nx * ny * nz, nx * ny * z0, nx * ny * nzl
+    X0 = mp.gaussian_matrix_rows(n_glob, m, seed, row0, n)
+    Om = mp.gaussian_matrix_rows(n_glob, 3, seed ^ 0x9E3779B97F4A7C15, row0, n)
+    sizes = [None] * world
+    dist.all_gather_object(sizes, (row0, n))
+    parts = [None] * world
+    dist.all_gather_object(parts, (X0, Om))
+    t = torch.tensor([0.1 * (rank + 1), 0.2 * (world - rank)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        ok_rows = all(a + b == c for (a, b), (c, _) in zip(sizes, sizes[1:])) and \
+            sizes[-1][0] + sizes[-1][1] == n_glob
+        X = np.vstack([p[0] for p in parts])
+        O = np.vstack([p[1] for p in parts])
+        out.put((ok_rows, np.array_equal(X, mp.gaussian_matrix(n_glob, m, seed)),
+                 np.array_equal(O, mp.gaussian_matrix(n_glob, 3, seed ^ 0x9E3779B97F4A7C15)),
+                 t.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_inputs_gloo(world):
+    """The N > 1 host plumbing on CPU ranks (gloo): the slab partition covers the
+    rows in rank order, every rank's start block / sketch rows are bitwise the
+    global draw's, and the per-rank times reduce by max."""
+    import socket
+
+    import torch.multiprocessing as tmp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_inputs_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    ok_rows, ok_x, ok_o, t = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert ok_rows and ok_x and ok_o
+    assert t == [0.1 * world, 0.2 * world]
+
+
 # ------------------------------------------------------------------ GPU
 
 
